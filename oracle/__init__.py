@@ -1,0 +1,179 @@
+"""TEST INFRASTRUCTURE ONLY -- the independent CPU oracle for the epsilon self-join.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  It shares no code with the CUDA path
+(``paper_1803_04120_b200``) and never imports it; the only thing both sides share is the
+seeded input generators in ``datagen`` (which hold none of the method's arithmetic).
+
+Contents, each citing the passage it follows (PAPER.md line numbers, SPEC.md as S.<line>):
+
+* ``brute_force`` / ``grid_join`` / ``rows`` -- the join itself (§3), in plain C
+  (``sj_oracle.c``, gcc -O2 -ffp-contract=off): brute force is the definition written out;
+  the grid join is a filter with its own robust width and a full 3^d neighbourhood.
+* ``index_ref`` -- the grid index of §4.2-4.4 (geometry, cell coordinates, linearisation, B, G,
+  A, M) and the Alg. 1 / Alg. 2 cell enumerations, in plain numpy / Python, following the
+  paper's notation with the DESIGN.md readings R6-R13.
+* ``expected_pairs_uniform`` -- the exact expectation of |S| for iid uniform points (SURVEY.md
+  §8(c) P4), used as a statistical pin.
+
+Pins (tests/test_oracle_pins.py) tie every function here to something other than itself:
+closed forms on integer lattices, the tie/self-pair worked examples of SPEC S.235-236,
+S.272-273, S.316-317, the Figure 2 facts of PAPER.md:179/201-202, the P4 expectation,
+symmetry, and brute force on tiny inputs.  ``estimate`` / batching has no oracle: "parity
+unpinned" by design (reading R13) -- the result set is invariant to batching.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import index_ref  # noqa: F401  (re-export)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sj_oracle.c")
+_LIB = os.path.join(_HERE, "libsj_oracle.so")
+_lib = None
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fno-unsafe-math-optimizations",
+          "-shared", "-fPIC", "-pthread", "-std=c11"]
+
+
+def build(force: bool = False) -> str:
+    """Compile the C oracle (building the checker is not using it)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        i64, i32, dbl = ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        p = ctypes.c_void_p
+        lib.orc_pair_within.argtypes = [p, p, i32, dbl]
+        lib.orc_pair_within.restype = i32
+        lib.orc_brute_force.argtypes = [p, i64, i32, dbl, i32, p, i64]
+        lib.orc_brute_force.restype = i64
+        lib.orc_rows.argtypes = [p, i64, i32, dbl, i32, p, i64, i32, p, p]
+        lib.orc_rows.restype = i64
+        lib.orc_grid_join.argtypes = [p, i64, i32, dbl, i32, i64, i64, i32, p, p, i64]
+        lib.orc_grid_join.restype = i64
+        _lib = lib
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _pts(points) -> np.ndarray:
+    a = np.ascontiguousarray(points, dtype=np.float64)
+    if a.ndim != 2:
+        raise ValueError("points must be N x d")
+    return a
+
+
+def default_threads() -> int:
+    return os.cpu_count() or 1
+
+
+def pair_within(a: Sequence[float], b: Sequence[float], eps: float) -> bool:
+    """The predicate s(a,b) <= fl(eps*eps) (R1) as the C oracle evaluates it."""
+    A = np.ascontiguousarray(a, dtype=np.float64)
+    B = np.ascontiguousarray(b, dtype=np.float64)
+    return bool(_load().orc_pair_within(_ptr(A), _ptr(B), len(A), float(eps)))
+
+
+def brute_force(points, eps: float, include_self: bool = True) -> np.ndarray:
+    """All ordered pairs (i<<32|k) with s(p_i,p_k) <= fl(eps^2), sorted."""
+    P = _pts(points)
+    n, d = P.shape
+    lib = _load()
+    total = lib.orc_brute_force(_ptr(P), n, d, float(eps), int(include_self), None, 0)
+    if total < 0:
+        raise ValueError("bad arguments")
+    out = np.empty(total, dtype=np.uint64)
+    lib.orc_brute_force(_ptr(P), n, d, float(eps), int(include_self), _ptr(out), total)
+    return out
+
+
+def grid_join(points, eps: float, include_self: bool = True, q0: int = 0, q1: int | None = None,
+              nthreads: int | None = None, count_only: bool = False):
+    """Pairs (or per-query counts) of queries [q0,q1) against all points; full 3^d scan."""
+    P = _pts(points)
+    n, d = P.shape
+    q1 = n if q1 is None else q1
+    nthreads = nthreads or default_threads()
+    lib = _load()
+    counts = np.zeros(max(q1 - q0, 0), dtype=np.int64)
+    if count_only:
+        total = lib.orc_grid_join(_ptr(P), n, d, float(eps), int(include_self), q0, q1, nthreads,
+                                  _ptr(counts), None, 0)
+        if total < 0:
+            raise ValueError("bad arguments")
+        return counts
+    total = lib.orc_grid_join(_ptr(P), n, d, float(eps), int(include_self), q0, q1, nthreads,
+                              _ptr(counts), None, 0)
+    if total < 0:
+        raise ValueError("bad arguments")
+    out = np.empty(total, dtype=np.uint64)
+    got = lib.orc_grid_join(_ptr(P), n, d, float(eps), int(include_self), q0, q1, nthreads,
+                            None, _ptr(out), total)
+    assert got == total
+    return out
+
+
+def rows(points, eps: float, qids: Iterable[int], include_self: bool = True,
+         nthreads: int | None = None):
+    """Brute-force neighbour rows of the given queries: (counts[nq], concatenated pairs)."""
+    P = _pts(points)
+    n, d = P.shape
+    q = np.ascontiguousarray(np.asarray(list(qids) if not isinstance(qids, np.ndarray) else qids,
+                                        dtype=np.int64))
+    nthreads = nthreads or default_threads()
+    lib = _load()
+    counts = np.zeros(len(q), dtype=np.int64)
+    total = lib.orc_rows(_ptr(P), n, d, float(eps), int(include_self), _ptr(q), len(q), nthreads,
+                         _ptr(counts), None)
+    out = np.empty(total, dtype=np.uint64)
+    lib.orc_rows(_ptr(P), n, d, float(eps), int(include_self), _ptr(q), len(q), nthreads,
+                 _ptr(counts), _ptr(out))
+    return counts, out
+
+
+def pair_counts(pairs: np.ndarray, n: int) -> np.ndarray:
+    """cnt[i] = |{k : (i,k) in S}|."""
+    keys = (np.asarray(pairs, dtype=np.uint64) >> np.uint64(32)).astype(np.int64)
+    return np.bincount(keys, minlength=n)
+
+
+def transpose_pairs(pairs: np.ndarray) -> np.ndarray:
+    p = np.asarray(pairs, dtype=np.uint64)
+    lo = p & np.uint64(0xFFFFFFFF)
+    hi = p >> np.uint64(32)
+    return np.sort((lo << np.uint64(32)) | hi)
+
+
+def expected_pairs_uniform(n: int, d: int, eps: float, L: float = 100.0) -> float:
+    """E|S| for n iid uniform points in [0,L]^d, self pairs included.
+
+    E|S| = n + n(n-1) F_d(r), r = eps/L, where F_d(r) = P(|X-Y| <= r) for X,Y iid uniform in the
+    unit cube: F_d(r) = sum_k (-1)^k C(d,k) pi^{(d-k)/2} / Gamma(1+(d+k)/2) r^{d+k}, exact for r<=1
+    (the (d-k)-dim ball volume times the mixed-volume correction of the cube's boundary).
+    """
+    r = eps / L
+    if r > 1.0:
+        raise ValueError("formula exact only for eps <= L")
+    F = 0.0
+    for k in range(d + 1):
+        F += ((-1) ** k) * math.comb(d, k) * math.pi ** ((d - k) / 2) / math.gamma(1 + (d + k) / 2) \
+            * r ** (d + k)
+    return n + n * (n - 1) * F
