@@ -1,0 +1,211 @@
+/*
+ * sj.h -- C ABI of the B200-native epsilon-distance self-join (arXiv 1803.04120, "GPU
+ * Accelerated Self-join for the Distance Similarity Metric", Gowanlock & Karsin).
+ *
+ * Library: paper_1803_04120_b200/libsj.so (hand-written CUDA for sm_100a, no CPU fallback).
+ * Conventions for every entry point:
+ *   - returns sj_status; out-parameters are written only when SJ_OK is returned;
+ *   - no C++ exception crosses the ABI; on failure sj_last_error() returns a thread-local,
+ *     human-readable message (valid until the next failing call on the same thread);
+ *   - argument errors are detected on the host BEFORE any allocation or CUDA call;
+ *   - CUDA failures return SJ_ERR_CUDA with cudaGetErrorString() in sj_last_error().
+ *
+ * The problem (§3 "Problem Statement"): for points D = (p_0..p_{N-1}) in d
+ * dimensions (2 <= d <= 6) and eps > 0, return every ORDERED pair (i,k) with
+ *     s(p_i,p_k) <= fl(eps*eps),  s(a,b) = (((a_0-b_0)^2 + (a_1-b_1)^2) + ...) + (a_{d-1}-b_{d-1})^2,
+ * every -, *, + one IEEE-754 binary64 round-to-nearest operation, left to right, no FMA
+ * (readings R1-R2: the squared form of PAPER.md:130's sqrt(...) <= eps; ties kept).
+ * Both orientations are returned ("add both (p,q) and (q,p)"); (p,p) is
+ * returned unless include_self == 0 (reading R3).  A pair is packed as one uint64
+ * (key << 32) | value with key = query id, value = neighbour id ("key/value
+ * pair"), ids = 0-based input row positions (reading R5), so integer order == (key,value)
+ * order.  The SET of pairs is deterministic; their order inside a batch is not (atomic
+ * emission); compare after a canonical sort.
+ */
+#ifndef SJ_H
+#define SJ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SJ_ABI_VERSION 1
+#define SJ_MAX_DIM 6
+
+typedef enum {
+    SJ_OK = 0,
+    SJ_ERR_ARG = 1,           /* bad pointer/size/eps/option (eps<=0, non-finite, fl(eps^2) not
+                                 normal, N==0, N>=2^32, query range outside [0,N), ...)        */
+    SJ_ERR_NONFINITE = 2,     /* a coordinate is NaN or +-inf                                   */
+    SJ_ERR_DIM = 3,           /* d not in [2, 6] ("we only focus on dimensions 2--6") */
+    SJ_ERR_KEY_OVERFLOW = 4,  /* prod_j |g_j| >= 2^64: linear cell ids would not fit a uint64;
+                                 use a larger eps (SPEC S.132)                                  */
+    SJ_ERR_NOMEM = 5,         /* device or pinned-host allocation failed                        */
+    SJ_ERR_CUDA = 6,          /* any other CUDA runtime error                                    */
+    SJ_ERR_EPS_MISMATCH = 7,  /* reserved (S.233); the index carries eps, so not raised today  */
+    SJ_ERR_STATE = 8          /* NULL handle / handle used on the wrong device / no GPU          */
+} sj_status;
+
+typedef struct sj_index sj_index;    /* opaque; immutable after build; device-resident; may be
+                                        shared read-only by concurrent joins                      */
+typedef struct sj_result sj_result;  /* opaque; owns its batches (device or pinned host memory);
+                                        independent of the index (either may be freed first)      */
+
+/* ---- options ------------------------------------------------------------------------------ */
+typedef struct {
+    int device;            /* CUDA device ordinal                                                */
+    int points_on_device;  /* 1: `points` is a device pointer on `device`; 0: host memory (copied
+                              H2D inside the call; pinned memory gives full PCIe bandwidth)       */
+    void *stream;          /* cudaStream_t to order the build on (NULL = library stream); the call
+                              returns after the build completed                                   */
+    int build_masks;       /* 1 (default): build the per-dimension masks M_j       */
+} sj_build_opts;
+
+typedef struct {
+    int unicomp;                   /* 1 (default): duplicate-search removal, Alg. 2;
+                                      0: full 3^d search, Alg. 1              */
+    int include_self;              /* 1 (default): emit (p,p)                                      */
+    uint64_t batch_capacity_pairs; /* C: pairs per result batch buffer (default 2^28)             */
+    int min_batches;               /* minimum number of batches (default 3)         */
+    int n_streams;                 /* concurrent CUDA streams for the batch pipeline (default 3)  */
+    int result_on_host;            /* 0 (default): batches stay in device memory; 1: each batch is
+                                      drained into pinned host memory while later batches compute */
+    uint64_t query_begin;          /* queries = A-order positions [query_begin, query_end)       */
+    uint64_t query_end;            /*   (0,0 = all N).  A-order is the cell-sorted order of the
+                                      index; ranges of it are the multi-GPU shard unit.  With
+                                      unicomp, a shard emits both orientations of the pairs its
+                                      queries decide, so the union over a partition of [0,N) is
+                                      exactly S with no duplicates.                               */
+    int use_masks;                 /* 1 (default): filter adjacent coordinates by M_j (Alg. 1 l.6) */
+} sj_join_opts;
+
+typedef struct {
+    uint64_t pairs;              /* pairs emitted (sum over batches)                              */
+    uint64_t cells_probed;       /* binary searches of B performed (work counter)                  */
+    uint64_t candidates_tested;  /* distance evaluations (work counter)                            */
+    uint64_t estimated_pairs;    /* the sampled estimate used to plan the batches                  */
+    uint32_t batches;            /* batches delivered                                              */
+    uint32_t retries;            /* batches re-run after a buffer overflow                         */
+    float estimate_ms;           /* device time of the estimator kernel (CUDA events)             */
+    float refine_ms;             /* sum of device times of the refine kernels (CUDA events)       */
+    float refine_max_ms;         /* longest single refine launch                                   */
+    float total_ms;              /* host wall time of sj_self_join                                 */
+    uint32_t refine_launches;    /* refine kernel launches (incl. retries)                         */
+    uint32_t reserved;
+} sj_stats;
+
+typedef struct {
+    int d, device;
+    uint64_t n;                  /* |D|                                                            */
+    uint64_t n_cells;            /* |G| = |B|                                       */
+    double eps, eps2, w;         /* eps, fl(eps*eps), cell width (reading R6)                      */
+    double mins[SJ_MAX_DIM];     /* per-dimension minima (exact)                                   */
+    uint64_t cpd[SJ_MAX_DIM];    /* |g_j| = cells per dimension incl. one pad cell each side (R7) */
+    uint64_t strides[SJ_MAX_DIM];/* linearisation strides, dimension 1 fastest (R8)               */
+    int key_bits;                /* ceil(log2(prod |g_j|)): bits sorted by the radix sort          */
+    uint64_t mask_offsets[SJ_MAX_DIM + 1]; /* byte offsets of M_j inside `masks`; [d] = total      */
+    /* device pointers (owned by the index; valid while it lives):                                 */
+    const uint64_t *B;           /* [n_cells] sorted linear ids of the non-empty cells             */
+    const uint32_t *G;           /* [n_cells+1] cell h holds A-positions [G[h], G[h+1])            */
+    const uint32_t *A;           /* [n] original point id at each A-position                       */
+    const uint32_t *pcell;       /* [n] cell h of each A-position                                  */
+    const double *X;             /* [d][n] SoA coordinates in A-order: X[j*n+k] = D[A[k]][j]      */
+    const uint8_t *masks;        /* concatenated M_j byte maps (1 = coordinate occupied) or NULL   */
+    /* build timings (CUDA events, ms) */
+    float t_h2d_ms, t_geometry_ms, t_keys_ms, t_sort_ms, t_compact_ms, t_total_ms;
+} sj_index_view;
+
+/* Fill *o with the defaults above. */
+void sj_build_opts_default(sj_build_opts *o);
+void sj_join_opts_default(sj_join_opts *o);
+
+/* ---- REQUIRED entry points (north_star) ---------------------------------------------------- */
+
+/* Build the sparse eps-grid index (§4.2-4.4): geometry (per-dimension
+ * min/max, cell width w, |g_j|), per-point linear cell ids, stable radix sort on device,
+ * compaction into the non-empty-cell list B / ranges G / point list A, SoA coordinate gather
+ * and masks M_j.
+ *   points : row-major N x d float64 (AoS), host or device per opts->points_on_device; borrowed
+ *            for the duration of the call only (copied).
+ *   n      : N, 1 <= N < 2^32.     d: 2..6.     eps: finite, > 0, fl(eps*eps) normal.
+ *   opts   : NULL = defaults.      *out: receives the new index (free with sj_free_index).
+ * Errors: SJ_ERR_ARG, SJ_ERR_DIM, SJ_ERR_NONFINITE, SJ_ERR_KEY_OVERFLOW, SJ_ERR_NOMEM,
+ *         SJ_ERR_CUDA, SJ_ERR_STATE (no device). */
+sj_status sj_build_index(const double *points, uint64_t n, int d, double eps,
+                         const sj_build_opts *opts, sj_index **out);
+
+/* Run the self-join over the index (Alg. 1-2, §5.1 batching): estimate the result size
+ * on a deterministic sample (count-only kernel), cut the A-order queries into k >= min_batches
+ * contiguous batches, run the refine kernel per batch on n_streams streams with warp-aggregated
+ * emission into batch buffers, drain to pinned host memory if result_on_host, re-run any batch
+ * whose buffer overflowed.  Returns after all batches completed.
+ *   idx : an index built or imported on the current process.   opts: NULL = defaults.
+ *   *out: receives the result (free with sj_free_result).
+ * Errors: SJ_ERR_ARG (bad options / query range), SJ_ERR_STATE (NULL index), SJ_ERR_NOMEM,
+ *         SJ_ERR_CUDA. */
+sj_status sj_self_join(const sj_index *idx, const sj_join_opts *opts, sj_result **out);
+
+/* Release a result and every batch buffer it owns.  NULL-safe. */
+void sj_free_result(sj_result *r);
+
+/* ---- supporting entry points ---------------------------------------------------------------- */
+
+void sj_free_index(sj_index *idx);   /* NULL-safe */
+
+/* Totals and work counters of a result. Any out pointer may be NULL. */
+sj_status sj_result_info(const sj_result *r, uint64_t *n_pairs, uint32_t *n_batches, sj_stats *stats);
+
+/* Batch b of a result: *pairs points to *n packed uint64 pairs in device memory (*on_device=1,
+ * on the index's device) or pinned host memory (*on_device=0); owned by the result. */
+sj_status sj_result_batch(const sj_result *r, uint32_t b, const uint64_t **pairs, uint64_t *n,
+                          int *on_device);
+
+/* Copy all pairs of a result, batch after batch, into host memory dst (capacity cap pairs).
+ * Errors: SJ_ERR_ARG if cap < total. */
+sj_status sj_result_copy_to_host(const sj_result *r, uint64_t *dst, uint64_t cap);
+
+/* Per-point neighbour counts cnt[i] = |{k : (i,k) in S}| without materialising
+ * pairs.  cnt: device pointer to N uint32 on the index's device (zeroed by the call), or NULL.
+ * *total receives |S| (restricted to the pairs decided by queries of opts' query range). */
+sj_status sj_neighbor_counts(const sj_index *idx, const sj_join_opts *opts, uint32_t *cnt,
+                             uint64_t *total);
+
+/* Geometry, sizes, timings and device pointers of an index (for tests and NCCL broadcast). */
+sj_status sj_index_export(const sj_index *idx, sj_index_view *view);
+
+/* Build an index on `device` from a view whose array pointers are device memory on that device
+ * (e.g. buffers received by an NCCL broadcast); the arrays are copied. */
+sj_status sj_index_import(const sj_index_view *view, int device, sj_index **out);
+
+/* Optional allocator hook for device memory (index arrays, result batches, scratch).
+ * alloc(bytes, device, stream, ctx) returns a device pointer or NULL; release(ptr, ctx).
+ * Pass NULLs to restore the default (cudaMallocAsync from the device's default pool). */
+void sj_set_allocator(void *(*alloc)(size_t, int, void *, void *), void (*release)(void *, void *),
+                      void *ctx);
+
+/* Batch planner (host-only, no GPU needed): given per-sample emission counts of a strided sample
+ * (sample s stands for `step` consecutive queries starting at q_begin + s*step), cut
+ * [q_begin, q_end) into k >= min_batches ranges whose estimated pairs stay below
+ * capacity/(1+margin).  cuts[0..k] receives the boundaries (cuts capacity max_cuts+1).
+ * Returns k in *k.  (§5.1; reading R13.) */
+sj_status sj_plan_batches(const uint32_t *sample_counts, uint64_t n_samples, uint64_t step,
+                          uint64_t q_begin, uint64_t q_end, uint64_t capacity, int min_batches,
+                          double margin, uint64_t *cuts, uint32_t max_cuts, uint32_t *k,
+                          uint64_t *estimated_total);
+
+/* Number of CUDA kernels this library has launched in the process (monotone counter). */
+uint64_t sj_kernel_launches(void);
+
+/* Thread-local message of the last failure ("" if none). */
+const char *sj_last_error(void);
+
+/* SJ_ABI_VERSION. */
+int sj_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SJ_H */

@@ -1,0 +1,12 @@
+"""B200-native (sm_100a) epsilon-distance self-join -- arXiv 1803.04120 (GPU-SJ) hot path.
+
+The work runs in ``libsj.so`` (hand-written CUDA behind the C ABI of ``include/sj.h``); this
+package is its thin ctypes binding plus the multi-GPU glue.  There is no CPU fallback.
+"""
+from .sj import (  # noqa: F401
+    Index, Result, SJError, build_index, self_join, neighbor_counts, import_index, plan_batches,
+    kernel_launches, load_library, LIB_PATH,
+)
+
+__all__ = ["Index", "Result", "SJError", "build_index", "self_join", "neighbor_counts", "import_index",
+           "plan_batches", "kernel_launches", "load_library", "LIB_PATH"]

@@ -1,0 +1,334 @@
+// api.cu -- the C ABI of libsj (include/sj.h): argument marshalling, error translation,
+// device / pinned-host memory management.  No compute happens here.
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
+
+#include "sj_common.cuh"
+
+namespace sj {
+
+std::atomic<uint64_t> g_kernel_launches{0};
+
+namespace {
+thread_local std::string t_last_error;
+
+struct AllocHook {
+    void *(*alloc)(size_t, int, void *, void *) = nullptr;
+    void (*release)(void *, void *) = nullptr;
+    void *ctx = nullptr;
+};
+AllocHook g_hook;
+std::mutex g_hook_mu;
+std::set<int> g_pool_configured;
+std::mutex g_pool_mu;
+
+void configure_pool(int dev)
+{
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (g_pool_configured.count(dev)) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;  // keep freed memory cached in the pool (no OS round trips)
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    g_pool_configured.insert(dev);
+}
+
+// ---- pinned host pool (result batches drained to the host; reused across joins)
+std::mutex g_pin_mu;
+std::multimap<size_t, void *> g_pin_free;     // size -> block
+std::map<void *, size_t> g_pin_size;          // block -> size
+}  // namespace
+
+void fail(sj_status st, const std::string &msg) { throw Error{st, msg}; }
+
+void cuda_check(cudaError_t e, const char *what, const char *file, int line)
+{
+    if (e == cudaSuccess) return;
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "%s: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+    cudaGetLastError();  // clear sticky-free errors
+    if (e == cudaErrorMemoryAllocation) throw Error{SJ_ERR_NOMEM, buf};
+    throw Error{SJ_ERR_CUDA, buf};
+}
+
+void *dev_alloc(size_t bytes, cudaStream_t s)
+{
+    if (bytes == 0) bytes = 1;
+    int dev = 0;
+    SJ_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(g_hook_mu);
+        if (g_hook.alloc) {
+            void *p = g_hook.alloc(bytes, dev, s, g_hook.ctx);
+            if (!p) fail(SJ_ERR_NOMEM, "allocator hook returned NULL");
+            return p;
+        }
+    }
+    configure_pool(dev);
+    void *p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        char buf[160];
+        std::snprintf(buf, sizeof buf, "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+        fail(SJ_ERR_NOMEM, buf);
+    }
+    return p;
+}
+
+void dev_free(void *p, cudaStream_t s)
+{
+    if (!p) return;
+    {
+        std::lock_guard<std::mutex> lk(g_hook_mu);
+        if (g_hook.release) {
+            // hooked memory is released stream-unordered: make prior work complete first
+            if (s) cudaStreamSynchronize(s);
+            g_hook.release(p, g_hook.ctx);
+            return;
+        }
+    }
+    cudaFreeAsync(p, s);
+}
+
+void *host_pinned_alloc(size_t bytes, size_t *granted)
+{
+    if (bytes == 0) bytes = 1;
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        auto it = g_pin_free.lower_bound(bytes);
+        if (it != g_pin_free.end() && it->first <= 2 * bytes + (64u << 20)) {
+            void *p = it->second;
+            if (granted) *granted = it->first;
+            g_pin_free.erase(it);
+            return p;
+        }
+    }
+    const size_t gran = 2u << 20;
+    const size_t sz = (bytes + gran - 1) / gran * gran;
+    void *p = nullptr;
+    cudaError_t e = cudaHostAlloc(&p, sz, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        // trim the pool once and retry
+        {
+            std::lock_guard<std::mutex> lk(g_pin_mu);
+            for (auto &kv : g_pin_free) { cudaFreeHost(kv.second); g_pin_size.erase(kv.second); }
+            g_pin_free.clear();
+        }
+        e = cudaHostAlloc(&p, sz, cudaHostAllocPortable);
+        if (e != cudaSuccess) { cudaGetLastError(); fail(SJ_ERR_NOMEM, "pinned host allocation failed"); }
+    }
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_size[p] = sz;
+    if (granted) *granted = sz;
+    return p;
+}
+
+void host_pinned_free(void *p)
+{
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_size.find(p);
+    if (it == g_pin_size.end()) return;
+    g_pin_free.emplace(it->second, p);
+}
+
+}  // namespace sj
+
+using sj::Error;
+
+#define SJ_API_BEGIN try {
+#define SJ_API_END                                                                    \
+    }                                                                                 \
+    catch (const Error &e) {                                                          \
+        sj::t_last_error = e.msg;                                                     \
+        return e.status;                                                              \
+    }                                                                                 \
+    catch (const std::bad_alloc &) {                                                  \
+        sj::t_last_error = "host allocation failed";                                  \
+        return SJ_ERR_NOMEM;                                                          \
+    }                                                                                 \
+    catch (...) {                                                                     \
+        sj::t_last_error = "unexpected internal error";                               \
+        return SJ_ERR_CUDA;                                                           \
+    }
+
+extern "C" {
+
+int sj_abi_version(void) { return SJ_ABI_VERSION; }
+
+const char *sj_last_error(void) { return sj::t_last_error.c_str(); }
+
+uint64_t sj_kernel_launches(void) { return sj::g_kernel_launches.load(); }
+
+void sj_build_opts_default(sj_build_opts *o)
+{
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->device = 0;
+    o->points_on_device = 0;
+    o->stream = nullptr;
+    o->build_masks = 1;
+}
+
+void sj_join_opts_default(sj_join_opts *o)
+{
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->unicomp = 1;
+    o->include_self = 1;
+    o->batch_capacity_pairs = 1ull << 28;
+    o->min_batches = 3;
+    o->n_streams = 3;
+    o->result_on_host = 0;
+    o->query_begin = 0;
+    o->query_end = 0;
+    o->use_masks = 1;
+}
+
+sj_status sj_build_index(const double *points, uint64_t n, int d, double eps, const sj_build_opts *opts,
+                         sj_index **out)
+{
+    SJ_API_BEGIN
+    if (!out) sj::fail(SJ_ERR_ARG, "out is NULL");
+    sj_build_opts o;
+    if (opts) o = *opts;
+    else sj_build_opts_default(&o);
+    *out = sj::build_index_impl(points, n, d, eps, o);
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_self_join(const sj_index *idx, const sj_join_opts *opts, sj_result **out)
+{
+    SJ_API_BEGIN
+    if (!out) sj::fail(SJ_ERR_ARG, "out is NULL");
+    if (!idx) sj::fail(SJ_ERR_STATE, "index is NULL");
+    sj_join_opts o;
+    if (opts) o = *opts;
+    else sj_join_opts_default(&o);
+    *out = sj::self_join_impl(idx, o);
+    return SJ_OK;
+    SJ_API_END
+}
+
+void sj_free_result(sj_result *r)
+{
+    if (!r) return;
+    cudaSetDevice(r->device);
+    for (auto &b : r->batches) {
+        if (!b.pairs) continue;
+        if (b.on_device) sj::dev_free(b.pairs, nullptr);
+        else sj::host_pinned_free(b.pairs);
+    }
+    delete r;
+}
+
+void sj_free_index(sj_index *idx) { sj::free_index_impl(idx); }
+
+sj_status sj_result_info(const sj_result *r, uint64_t *n_pairs, uint32_t *n_batches, sj_stats *stats)
+{
+    SJ_API_BEGIN
+    if (!r) sj::fail(SJ_ERR_STATE, "result is NULL");
+    if (n_pairs) *n_pairs = r->total;
+    if (n_batches) *n_batches = (uint32_t)r->batches.size();
+    if (stats) *stats = r->stats;
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_result_batch(const sj_result *r, uint32_t b, const uint64_t **pairs, uint64_t *n, int *on_device)
+{
+    SJ_API_BEGIN
+    if (!r) sj::fail(SJ_ERR_STATE, "result is NULL");
+    if (b >= r->batches.size()) sj::fail(SJ_ERR_ARG, "batch index out of range");
+    const sj_batch &bt = r->batches[b];
+    if (pairs) *pairs = bt.pairs;
+    if (n) *n = bt.n;
+    if (on_device) *on_device = bt.on_device;
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_result_copy_to_host(const sj_result *r, uint64_t *dst, uint64_t cap)
+{
+    SJ_API_BEGIN
+    if (!r) sj::fail(SJ_ERR_STATE, "result is NULL");
+    if (!dst && r->total) sj::fail(SJ_ERR_ARG, "dst is NULL");
+    if (cap < r->total) sj::fail(SJ_ERR_ARG, "dst capacity smaller than the result");
+    SJ_CUDA(cudaSetDevice(r->device));
+    uint64_t off = 0;
+    for (const auto &b : r->batches) {
+        if (!b.n) continue;
+        if (b.on_device) SJ_CUDA(cudaMemcpy(dst + off, b.pairs, b.n * 8, cudaMemcpyDeviceToHost));
+        else std::memcpy(dst + off, b.pairs, b.n * 8);
+        off += b.n;
+    }
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_neighbor_counts(const sj_index *idx, const sj_join_opts *opts, uint32_t *cnt, uint64_t *total)
+{
+    SJ_API_BEGIN
+    if (!idx) sj::fail(SJ_ERR_STATE, "index is NULL");
+    sj_join_opts o;
+    if (opts) o = *opts;
+    else sj_join_opts_default(&o);
+    sj::neighbor_counts_impl(idx, o, cnt, total);
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_index_export(const sj_index *idx, sj_index_view *view)
+{
+    SJ_API_BEGIN
+    if (!idx) sj::fail(SJ_ERR_STATE, "index is NULL");
+    if (!view) sj::fail(SJ_ERR_ARG, "view is NULL");
+    *view = idx->view;
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_index_import(const sj_index_view *view, int device, sj_index **out)
+{
+    SJ_API_BEGIN
+    if (!view || !out) sj::fail(SJ_ERR_ARG, "NULL argument");
+    *out = sj::import_index_impl(*view, device);
+    return SJ_OK;
+    SJ_API_END
+}
+
+void sj_set_allocator(void *(*alloc)(size_t, int, void *, void *), void (*release)(void *, void *), void *ctx)
+{
+    std::lock_guard<std::mutex> lk(sj::g_hook_mu);
+    sj::g_hook.alloc = alloc;
+    sj::g_hook.release = release;
+    sj::g_hook.ctx = ctx;
+}
+
+sj_status sj_plan_batches(const uint32_t *sample_counts, uint64_t n_samples, uint64_t step, uint64_t q_begin,
+                          uint64_t q_end, uint64_t capacity, int min_batches, double margin, uint64_t *cuts,
+                          uint32_t max_cuts, uint32_t *k, uint64_t *estimated_total)
+{
+    SJ_API_BEGIN
+    if ((!sample_counts && n_samples) || !cuts || !k) sj::fail(SJ_ERR_ARG, "NULL argument");
+    if (q_end < q_begin || step == 0 || capacity == 0 || min_batches < 1 || margin < 0)
+        sj::fail(SJ_ERR_ARG, "bad planner arguments");
+    std::vector<uint64_t> c, e;
+    uint64_t tot = 0;
+    sj::plan_batches(sample_counts, n_samples, step, q_begin, q_end, capacity, min_batches, margin, c, e, &tot);
+    if (c.size() > (size_t)max_cuts + 1) sj::fail(SJ_ERR_ARG, "cuts buffer too small");
+    std::memcpy(cuts, c.data(), c.size() * sizeof(uint64_t));
+    *k = (uint32_t)(c.size() - 1);
+    if (estimated_total) *estimated_total = tot;
+    return SJ_OK;
+    SJ_API_END
+}
+
+}  // extern "C"

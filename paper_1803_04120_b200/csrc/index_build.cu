@@ -1,0 +1,445 @@
+// index_build.cu -- steps a1-a4 of the hot path: the sparse epsilon-grid index.
+//
+// PAPER.md §4.2 "Index Properties" (lines 155-168), §4.3 "Index Components" (170-173, 181):
+// only non-empty cells are stored: B = sorted linear ids, G = per-cell ranges into A,
+// A = point ids grouped by cell, M_j = occupied coordinates per dimension.  Readings
+// (DESIGN.md): R6 cell width w = eps + 2^-44 (eps + R); R7 c_j = 1 + floor(fl(fl(x_j-min_j)/w)),
+// |g_j| = 3 + floor(fl(fl(max_j-min_j)/w)) (one empty pad cell each side);
+// R8 dimension 1 fastest; R9 M_j as occupied sets; R14 A ordered by (linear id, point id).
+//
+// Kernels (all HBM-bound; algorithmic bytes in DESIGN.md §Roofline):
+//   k_minmax_partial/k_minmax_final : exact per-dimension min/max + non-finite check (a1)
+//   k_keys                          : cell coordinates -> linear id, identity ids, mask bytes (a2)
+//   radix sort                      : stable LSD over key_bits (a3, radix_sort.cu)
+//   k_heads + inclusive scan        : cell index of every A-position (a4)
+//   k_compact_gather                : B, G starts, SoA coordinates X[j][k] = D[A[k]][j] (a4)
+#include <cmath>
+#include <cstring>
+
+#include "sj_common.cuh"
+
+namespace sj {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+k_minmax_partial(const double *__restrict__ pts, uint32_t n, double *__restrict__ part, uint32_t *nonfinite)
+{
+    double mn[D], mx[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) { mn[j] = INFINITY; mx[j] = -INFINITY; }
+    bool bad = false;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const double x = pts[i * D + j];
+            bad |= !isfinite(x);
+            mn[j] = fmin(mn[j], x);
+            mx[j] = fmax(mx[j], x);
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
+    __shared__ double s_mn[kThreads / 32][D], s_mx[kThreads / 32][D];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        double a = mn[j], b = mx[j];
+        for (int o = 16; o; o >>= 1) {
+            a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+        if (lane == 0) { s_mn[warp][j] = a; s_mx[warp][j] = b; }
+    }
+    __syncthreads();
+    if (threadIdx.x < D) {
+        const int j = threadIdx.x;
+        double a = INFINITY, b = -INFINITY;
+        for (int w = 0; w < kThreads / 32; ++w) { a = fmin(a, s_mn[w][j]); b = fmax(b, s_mx[w][j]); }
+        part[(uint64_t)blockIdx.x * 2 * D + j] = a;
+        part[(uint64_t)blockIdx.x * 2 * D + D + j] = b;
+    }
+}
+
+__global__ void k_minmax_final(const double *__restrict__ part, int nparts, int d, double *__restrict__ out)
+{
+    // out[0..d) = mins, out[d..2d) = maxs ; one thread per (j, min|max)
+    const int t = threadIdx.x;
+    if (t >= 2 * d) return;
+    const bool is_max = t >= d;
+    double acc = is_max ? -INFINITY : INFINITY;
+    for (int p = 0; p < nparts; ++p) {
+        const double v = part[(uint64_t)p * 2 * d + t];
+        acc = is_max ? fmax(acc, v) : fmin(acc, v);
+    }
+    out[t] = acc;
+}
+
+// Cell coordinate c_j = 1 + floor(fl(fl(x_j - min_j) / w))  (reading R7), linear id with
+// dimension 1 fastest (R8): key = sum_j c_j * stride_j (exact: < prod |g_j| < 2^64).
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+k_keys(const double *__restrict__ pts, uint32_t n, DevIndex ix, uint64_t *__restrict__ keys,
+       uint32_t *__restrict__ ids, uint8_t *__restrict__ masks)
+{
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t key = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        const double x = pts[i * D + j];
+        const double t = floor(__ddiv_rn(__dsub_rn(x, ix.mins[j]), ix.w));
+        const uint64_t c = 1ull + (uint64_t)t;
+        key += c * ix.strides[j];
+        if (masks) masks[ix.mask_off[j] + c] = 1;   // benign same-value races
+    }
+    keys[i] = key;
+    ids[i] = (uint32_t)i;
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_heads(const uint64_t *__restrict__ keys, uint32_t n, uint32_t *__restrict__ flags)
+{
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    flags[k] = (k == 0 || keys[k] != keys[k - 1]) ? 1u : 0u;
+}
+
+// pcell holds the inclusive scan of head flags on entry (1-based cell number) and the
+// 0-based cell index on exit.
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ A,
+                 const double *__restrict__ pts, uint32_t n, uint32_t *__restrict__ pcell,
+                 uint64_t *__restrict__ B, uint32_t *__restrict__ G, double *__restrict__ X)
+{
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t h = pcell[k] - 1u;
+    pcell[k] = h;
+    const uint64_t key = keys[k];
+    if (k == 0 || keys[k - 1] != key) {
+        B[h] = key;
+        G[h] = (uint32_t)k;
+    }
+    if (k == n - 1) G[h + 1] = n;
+    const uint64_t src = (uint64_t)A[k] * D;
+#pragma unroll
+    for (int j = 0; j < D; ++j) X[(uint64_t)j * n + k] = pts[src + j];
+}
+
+template <int D>
+void launch_dim(int which, dim3 g, dim3 b, cudaStream_t s, const double *pts, uint32_t n, DevIndex &ix,
+                uint64_t *keys, uint32_t *ids, uint8_t *masks, double *part, uint32_t *nonfinite,
+                const uint32_t *A, uint32_t *pcell, uint64_t *B, uint32_t *G, double *X)
+{
+    if (which == 0) k_minmax_partial<D><<<g, b, 0, s>>>(pts, n, part, nonfinite);
+    else if (which == 1) k_keys<D><<<g, b, 0, s>>>(pts, n, ix, keys, ids, masks);
+    else k_compact_gather<D><<<g, b, 0, s>>>(keys, A, pts, n, pcell, B, G, X);
+    SJ_LAUNCHED();
+}
+
+void launch(int d, int which, dim3 g, dim3 b, cudaStream_t s, const double *pts, uint32_t n, DevIndex &ix,
+            uint64_t *keys, uint32_t *ids, uint8_t *masks, double *part, uint32_t *nonfinite,
+            const uint32_t *A, uint32_t *pcell, uint64_t *B, uint32_t *G, double *X)
+{
+    switch (d) {
+    case 2: launch_dim<2>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X); break;
+    case 3: launch_dim<3>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X); break;
+    case 4: launch_dim<4>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X); break;
+    case 5: launch_dim<5>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X); break;
+    case 6: launch_dim<6>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X); break;
+    default: fail(SJ_ERR_DIM, "d must be in [2,6]");
+    }
+}
+
+struct EventTimer {
+    cudaEvent_t e[8];
+    int n = 0;
+    explicit EventTimer(int k) : n(k) { for (int i = 0; i < n; ++i) SJ_CUDA(cudaEventCreate(&e[i])); }
+    ~EventTimer() { for (int i = 0; i < n; ++i) cudaEventDestroy(e[i]); }
+    void rec(int i, cudaStream_t s) { SJ_CUDA(cudaEventRecord(e[i], s)); }
+    float ms(int a, int b) { float t = 0; cudaEventElapsedTime(&t, e[a], e[b]); return t; }
+};
+
+// Host-side geometry (a1 epilogue): R, w, |g_j|, strides, key bits.  Exact same IEEE
+// operations as written in DESIGN.md R6/R7.
+void host_geometry(int d, double eps, const double *mins, const double *maxs, sj_index_view &v)
+{
+    double R = 0.0;
+    double ranges[SJ_MAX_DIM];
+    for (int j = 0; j < d; ++j) {
+        volatile double r = maxs[j] - mins[j];
+        ranges[j] = r;
+        if (r > R) R = r;
+    }
+    volatile double er = eps + R;
+    volatile double w = eps + std::ldexp((double)er, -44);
+    v.w = w;
+    long double prod = 1.0L;
+    unsigned __int128 iprod = 1;
+    for (int j = 0; j < d; ++j) {
+        volatile double q = ranges[j] / (double)w;
+        const double t = std::floor((double)q);
+        if (!(t < 9.0e18)) fail(SJ_ERR_KEY_OVERFLOW, "cells per dimension overflow: use a larger eps");
+        v.cpd[j] = 3ull + (uint64_t)t;
+        prod *= (long double)v.cpd[j];
+        if (prod >= 18446744073709551616.0L)
+            fail(SJ_ERR_KEY_OVERFLOW, "prod |g_j| >= 2^64: linear cell ids overflow uint64; use a larger eps");
+        iprod *= v.cpd[j];
+    }
+    v.strides[0] = 1;
+    for (int j = 1; j < d; ++j) v.strides[j] = v.strides[j - 1] * v.cpd[j - 1];
+    // bits needed for linear ids in [0, prod-1]
+    unsigned __int128 maxkey = iprod - 1;
+    int bits = 0;
+    while (maxkey > 0) { ++bits; maxkey >>= 1; }
+    v.key_bits = bits;
+}
+
+}  // namespace
+
+sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &o)
+{
+    // ---- argument validation before any allocation (sj.h contract)
+    if (d < 2 || d > SJ_MAX_DIM) fail(SJ_ERR_DIM, "d must be in [2,6] (PAPER.md:391)");
+    if (!points) fail(SJ_ERR_ARG, "points is NULL");
+    if (n == 0 || n >= (1ull << 32)) fail(SJ_ERR_ARG, "N must satisfy 1 <= N < 2^32");
+    if (!std::isfinite(eps) || !(eps > 0.0)) fail(SJ_ERR_ARG, "eps must be finite and > 0");
+    {
+        volatile double e2 = eps * eps;
+        if (!std::isnormal((double)e2)) fail(SJ_ERR_ARG, "fl(eps*eps) must be a normal double");
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        fail(SJ_ERR_STATE, "no CUDA device available (the library has no CPU fallback)");
+    }
+    if (o.device < 0 || o.device >= ndev) fail(SJ_ERR_ARG, "bad device ordinal");
+    SJ_CUDA(cudaSetDevice(o.device));
+
+    cudaStream_t s = static_cast<cudaStream_t>(o.stream);
+    bool own_stream = false;
+    if (!s) {
+        SJ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        own_stream = true;
+    }
+    struct StreamGuard {
+        cudaStream_t s; bool own;
+        ~StreamGuard() { if (own) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } }
+    } sg{s, own_stream};
+
+    const uint32_t N = (uint32_t)n;
+    EventTimer ev(7);
+    ev.rec(0, s);
+
+    // ---- inputs on device
+    const double *pts = points;
+    Scratch<double> d_pts;
+    if (!o.points_on_device) {
+        d_pts.p = dalloc<double>((size_t)n * d, s);
+        d_pts.s = s;
+        SJ_CUDA(cudaMemcpyAsync(d_pts.p, points, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
+        pts = d_pts.p;
+    }
+    ev.rec(1, s);
+
+    // ---- a1: exact per-dimension min/max + finiteness
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device);
+    const uint32_t parts = (uint32_t)std::min<uint64_t>((n + kThreads - 1) / kThreads, (uint64_t)nsm * 4);
+    Scratch<double> part((size_t)parts * 2 * d, s);
+    Scratch<double> mm(2 * d, s);
+    Scratch<uint32_t> nonfinite(1, s);
+    SJ_CUDA(cudaMemsetAsync(nonfinite.p, 0, sizeof(uint32_t), s));
+    DevIndex ix{};
+    ix.d = d;
+    ix.n = N;
+    launch(d, 0, dim3(parts), dim3(kThreads), s, pts, N, ix, nullptr, nullptr, nullptr, part.p, nonfinite.p,
+           nullptr, nullptr, nullptr, nullptr, nullptr);
+    k_minmax_final<<<1, 32, 0, s>>>(part.p, (int)parts, d, mm.p);
+    SJ_LAUNCHED();
+    double h_mm[2 * SJ_MAX_DIM];
+    uint32_t h_bad = 0;
+    SJ_CUDA(cudaMemcpyAsync(h_mm, mm.p, sizeof(double) * 2 * d, cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaMemcpyAsync(&h_bad, nonfinite.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaStreamSynchronize(s));
+    ev.rec(2, s);
+    if (h_bad) fail(SJ_ERR_NONFINITE, "a coordinate is NaN or infinite");
+
+    sj_index_view v{};
+    v.d = d;
+    v.device = o.device;
+    v.n = n;
+    v.eps = eps;
+    {
+        volatile double e2 = eps * eps;
+        v.eps2 = e2;
+    }
+    for (int j = 0; j < d; ++j) v.mins[j] = h_mm[j];
+    host_geometry(d, eps, h_mm, h_mm + d, v);
+
+    ix.w = v.w;
+    ix.eps2 = v.eps2;
+    for (int j = 0; j < d; ++j) {
+        ix.mins[j] = v.mins[j];
+        ix.cpd[j] = v.cpd[j];
+        ix.strides[j] = v.strides[j];
+    }
+    // masks: byte maps of |g_j| bytes each, only when small (they never change S)
+    uint64_t mask_total = 0;
+    bool want_masks = o.build_masks != 0;
+    for (int j = 0; j < d; ++j) {
+        v.mask_offsets[j] = mask_total;
+        mask_total += v.cpd[j];
+        if (mask_total > (1ull << 26)) want_masks = false;
+    }
+    v.mask_offsets[d] = mask_total;
+    for (int j = 0; j <= d; ++j) ix.mask_off[j] = v.mask_offsets[j];
+
+    // ---- a2: keys
+    sj_index *idx = new sj_index();
+    idx->device = o.device;
+    auto own = [&](void *p) { idx->bufs[idx->nbufs++] = p; return p; };
+    try {
+        uint8_t *masks = nullptr;
+        if (want_masks) {
+            masks = static_cast<uint8_t *>(own(dev_alloc(mask_total, s)));
+            SJ_CUDA(cudaMemsetAsync(masks, 0, mask_total, s));
+        }
+        Scratch<uint64_t> keys(n, s), keys_tmp(n, s);
+        uint32_t *A = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
+        Scratch<uint32_t> ids_tmp(n, s);
+        const dim3 grid((unsigned)((n + kThreads - 1) / kThreads));
+        launch(d, 1, grid, dim3(kThreads), s, pts, N, ix, keys.p, A, masks, nullptr, nullptr, nullptr, nullptr,
+               nullptr, nullptr, nullptr);
+        ev.rec(3, s);
+
+        // ---- a3: stable radix sort of (key, id)
+        bool in_tmp = false;
+        radix_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, v.key_bits, s, &in_tmp);
+        const uint64_t *skeys = in_tmp ? keys_tmp.p : keys.p;
+        if (in_tmp) SJ_CUDA(cudaMemcpyAsync(A, ids_tmp.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
+        ev.rec(4, s);
+
+        // ---- a4: heads, cell numbering, compaction, SoA gather
+        uint32_t *pcell = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
+        {
+            Scratch<uint32_t> flags(n, s);
+            k_heads<<<grid, kThreads, 0, s>>>(skeys, N, flags.p);
+            SJ_LAUNCHED();
+            inclusive_scan_u32(flags.p, pcell, n, s);
+        }
+        uint32_t nG = 0;
+        SJ_CUDA(cudaMemcpyAsync(&nG, pcell + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        SJ_CUDA(cudaStreamSynchronize(s));
+        uint64_t *B = static_cast<uint64_t *>(own(dev_alloc(sizeof(uint64_t) * nG, s)));
+        uint32_t *G = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * ((size_t)nG + 1), s)));
+        double *X = static_cast<double *>(own(dev_alloc(sizeof(double) * n * d, s)));
+        launch(d, 2, grid, dim3(kThreads), s, pts, N, ix, const_cast<uint64_t *>(skeys), nullptr, nullptr, nullptr,
+               nullptr, A, pcell, B, G, X);
+        ev.rec(5, s);
+        SJ_CUDA(cudaStreamSynchronize(s));
+        ev.rec(6, s);
+
+        v.n_cells = nG;
+        v.B = B;
+        v.G = G;
+        v.A = A;
+        v.pcell = pcell;
+        v.X = X;
+        v.masks = masks;
+        v.t_h2d_ms = ev.ms(0, 1);
+        v.t_geometry_ms = ev.ms(1, 2);
+        v.t_keys_ms = ev.ms(2, 3);
+        v.t_sort_ms = ev.ms(3, 4);
+        v.t_compact_ms = ev.ms(4, 5);
+        v.t_total_ms = ev.ms(0, 5);
+        ix.nG = nG;
+        ix.B = B;
+        ix.G = G;
+        ix.A = A;
+        ix.pcell = pcell;
+        ix.X = X;
+        ix.masks = masks;
+        idx->view = v;
+        idx->dev = ix;
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        free_index_impl(idx);
+        throw;
+    }
+    return idx;
+}
+
+void free_index_impl(sj_index *idx)
+{
+    if (!idx) return;
+    cudaSetDevice(idx->device);
+    for (int i = 0; i < idx->nbufs; ++i) dev_free(idx->bufs[i], nullptr);
+    cudaDeviceSynchronize();
+    delete idx;
+}
+
+sj_index *import_index_impl(const sj_index_view &src, int device)
+{
+    if (src.d < 2 || src.d > SJ_MAX_DIM) fail(SJ_ERR_DIM, "d must be in [2,6]");
+    if (src.n == 0 || src.n >= (1ull << 32) || src.n_cells == 0 || src.n_cells > src.n)
+        fail(SJ_ERR_ARG, "inconsistent index view sizes");
+    if (!src.B || !src.G || !src.A || !src.pcell || !src.X) fail(SJ_ERR_ARG, "index view has NULL arrays");
+    SJ_CUDA(cudaSetDevice(device));
+    cudaStream_t s;
+    SJ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    sj_index *idx = new sj_index();
+    idx->device = device;
+    auto own = [&](size_t bytes) { void *p = dev_alloc(bytes, s); idx->bufs[idx->nbufs++] = p; return p; };
+    try {
+        const uint64_t n = src.n, nG = src.n_cells;
+        const int d = src.d;
+        sj_index_view v = src;
+        v.device = device;
+        uint64_t *B = static_cast<uint64_t *>(own(8 * nG));
+        uint32_t *G = static_cast<uint32_t *>(own(4 * (nG + 1)));
+        uint32_t *A = static_cast<uint32_t *>(own(4 * n));
+        uint32_t *pcell = static_cast<uint32_t *>(own(4 * n));
+        double *X = static_cast<double *>(own(8 * n * d));
+        uint8_t *masks = nullptr;
+        SJ_CUDA(cudaMemcpyAsync(B, src.B, 8 * nG, cudaMemcpyDefault, s));
+        SJ_CUDA(cudaMemcpyAsync(G, src.G, 4 * (nG + 1), cudaMemcpyDefault, s));
+        SJ_CUDA(cudaMemcpyAsync(A, src.A, 4 * n, cudaMemcpyDefault, s));
+        SJ_CUDA(cudaMemcpyAsync(pcell, src.pcell, 4 * n, cudaMemcpyDefault, s));
+        SJ_CUDA(cudaMemcpyAsync(X, src.X, 8 * n * d, cudaMemcpyDefault, s));
+        if (src.masks && src.mask_offsets[d] > 0) {
+            masks = static_cast<uint8_t *>(own(src.mask_offsets[d]));
+            SJ_CUDA(cudaMemcpyAsync(masks, src.masks, src.mask_offsets[d], cudaMemcpyDefault, s));
+        }
+        SJ_CUDA(cudaStreamSynchronize(s));
+        v.B = B; v.G = G; v.A = A; v.pcell = pcell; v.X = X; v.masks = masks;
+        DevIndex ix{};
+        ix.d = d;
+        ix.n = (uint32_t)n;
+        ix.nG = (uint32_t)nG;
+        ix.w = v.w;
+        ix.eps2 = v.eps2;
+        for (int j = 0; j < d; ++j) {
+            ix.mins[j] = v.mins[j];
+            ix.cpd[j] = v.cpd[j];
+            ix.strides[j] = v.strides[j];
+        }
+        for (int j = 0; j <= d; ++j) ix.mask_off[j] = v.mask_offsets[j];
+        ix.B = B; ix.G = G; ix.A = A; ix.pcell = pcell; ix.X = X; ix.masks = masks;
+        idx->view = v;
+        idx->dev = ix;
+    } catch (...) {
+        cudaStreamDestroy(s);
+        free_index_impl(idx);
+        throw;
+    }
+    cudaStreamDestroy(s);
+    return idx;
+}
+
+}  // namespace sj

@@ -1,0 +1,123 @@
+// sj_common.cuh -- internal declarations of libsj (B200 / sm_100a epsilon self-join).
+// Nothing here is shared with oracle/ (task rule ③).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "sj.h"
+
+namespace sj {
+
+// ---------------------------------------------------------------- errors
+struct Error {
+    sj_status status;
+    std::string msg;
+};
+
+[[noreturn]] void fail(sj_status st, const std::string &msg);
+void cuda_check(cudaError_t e, const char *what, const char *file, int line);
+#define SJ_CUDA(x) ::sj::cuda_check((x), #x, __FILE__, __LINE__)
+
+// ---------------------------------------------------------------- launch accounting
+extern std::atomic<uint64_t> g_kernel_launches;
+inline void count_launch(uint64_t k = 1) { g_kernel_launches.fetch_add(k, std::memory_order_relaxed); }
+// Checks the launch configuration error right after a <<<>>> launch.
+#define SJ_LAUNCHED() do { ::sj::count_launch(); SJ_CUDA(cudaGetLastError()); } while (0)
+
+// ---------------------------------------------------------------- device memory
+void *dev_alloc(size_t bytes, cudaStream_t s);
+void dev_free(void *p, cudaStream_t s);
+void *host_pinned_alloc(size_t bytes, size_t *granted);   // pooled pinned memory
+void host_pinned_free(void *p);
+
+template <class T>
+T *dalloc(size_t count, cudaStream_t s) { return static_cast<T *>(dev_alloc(count * sizeof(T), s)); }
+
+// RAII scratch buffer freed stream-ordered.
+template <class T>
+struct Scratch {
+    T *p = nullptr;
+    cudaStream_t s = nullptr;
+    Scratch() = default;
+    Scratch(size_t n, cudaStream_t st) : p(dalloc<T>(n ? n : 1, st)), s(st) {}
+    ~Scratch() { if (p) dev_free(p, s); }
+    Scratch(const Scratch &) = delete;
+    Scratch &operator=(const Scratch &) = delete;
+    T *release() { T *q = p; p = nullptr; return q; }
+};
+
+// ---------------------------------------------------------------- the index as kernels see it
+// Layout in HBM:
+//   B[nG]   uint64  sorted linear ids of non-empty cells
+//   G[nG+1] uint32  CSR starts: cell h = A-positions [G[h],G[h+1])
+//   A[N]    uint32  original point id per A-position            (|A| = |D|)
+//   pcell[N] uint32 cell of each A-position
+//   X[d][N] double  SoA coordinates in A-order
+//   masks   uint8   M_j byte maps, concatenated (mask_off[j] .. mask_off[j+1])
+struct DevIndex {
+    int d;
+    uint32_t n;
+    uint32_t nG;
+    double w;
+    double eps2;                 // fl(eps*eps)
+    double mins[SJ_MAX_DIM];
+    uint64_t cpd[SJ_MAX_DIM];
+    uint64_t strides[SJ_MAX_DIM];
+    const uint64_t *B;
+    const uint32_t *G;
+    const uint32_t *A;
+    const uint32_t *pcell;
+    const double *X;
+    const uint8_t *masks;        // nullptr when masks were not built
+    uint64_t mask_off[SJ_MAX_DIM + 1];
+};
+
+}  // namespace sj
+
+// The opaque handle.
+struct sj_index {
+    int device = 0;
+    sj_index_view view{};        // geometry + device pointers (exported as is)
+    sj::DevIndex dev{};          // same, in kernel form
+    void *bufs[8] = {nullptr};   // owned device allocations
+    int nbufs = 0;
+};
+
+struct sj_batch {
+    uint64_t *pairs = nullptr;   // device or pinned host
+    uint64_t n = 0;
+    uint64_t cap = 0;
+    int on_device = 1;
+};
+
+struct sj_result {
+    int device = 0;
+    std::vector<sj_batch> batches;
+    sj_stats stats{};
+    uint64_t total = 0;
+};
+
+namespace sj {
+// index_build.cu
+sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &o);
+sj_index *import_index_impl(const sj_index_view &v, int device);
+void free_index_impl(sj_index *idx);
+
+// radix_sort.cu
+void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp,
+                      uint32_t n, int key_bits, cudaStream_t s, bool *result_in_tmp);
+void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s);
+void inclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s);
+
+// join.cu
+sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o);
+void neighbor_counts_impl(const sj_index *idx, const sj_join_opts &o, uint32_t *cnt, uint64_t *total);
+void plan_batches(const uint32_t *sample_counts, uint64_t n_samples, uint64_t step, uint64_t q_begin,
+                  uint64_t q_end, uint64_t capacity, int min_batches, double margin,
+                  std::vector<uint64_t> &cuts, std::vector<uint64_t> &est, uint64_t *estimated_total);
+}  // namespace sj

@@ -1,0 +1,370 @@
+"""Thin Python binding of libsj (include/sj.h) -- argument marshalling only.
+
+Every step of the self-join runs in the CUDA library; there is no CPU fallback: if libsj.so is
+missing or no GPU is present the calls raise (``SJError`` / ``RuntimeError``).
+
+    idx = build_index(points, eps)              # points: torch tensor (cuda or cpu) or numpy N x d f64
+    res = self_join(idx)                        # device-resident batches (torch uint64 views)
+    pairs = res.to_numpy(sort=True)             # canonical order
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsj.so")
+
+SJ_MAX_DIM = 6
+STATUS = {0: "SJ_OK", 1: "SJ_ERR_ARG", 2: "SJ_ERR_NONFINITE", 3: "SJ_ERR_DIM", 4: "SJ_ERR_KEY_OVERFLOW",
+          5: "SJ_ERR_NOMEM", 6: "SJ_ERR_CUDA", 7: "SJ_ERR_EPS_MISMATCH", 8: "SJ_ERR_STATE"}
+
+u64, u32, i32, dbl, f32, vp = (ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_double,
+                               ctypes.c_float, ctypes.c_void_p)
+
+
+class BuildOpts(ctypes.Structure):
+    _fields_ = [("device", i32), ("points_on_device", i32), ("stream", vp), ("build_masks", i32)]
+
+
+class JoinOpts(ctypes.Structure):
+    _fields_ = [("unicomp", i32), ("include_self", i32), ("batch_capacity_pairs", u64),
+                ("min_batches", i32), ("n_streams", i32), ("result_on_host", i32),
+                ("query_begin", u64), ("query_end", u64), ("use_masks", i32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("pairs", u64), ("cells_probed", u64), ("candidates_tested", u64),
+                ("estimated_pairs", u64), ("batches", u32), ("retries", u32),
+                ("estimate_ms", f32), ("refine_ms", f32), ("refine_max_ms", f32), ("total_ms", f32),
+                ("refine_launches", u32), ("reserved", u32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+class IndexView(ctypes.Structure):
+    _fields_ = [("d", i32), ("device", i32), ("n", u64), ("n_cells", u64),
+                ("eps", dbl), ("eps2", dbl), ("w", dbl),
+                ("mins", dbl * SJ_MAX_DIM), ("cpd", u64 * SJ_MAX_DIM), ("strides", u64 * SJ_MAX_DIM),
+                ("key_bits", i32), ("mask_offsets", u64 * (SJ_MAX_DIM + 1)),
+                ("B", vp), ("G", vp), ("A", vp), ("pcell", vp), ("X", vp), ("masks", vp),
+                ("t_h2d_ms", f32), ("t_geometry_ms", f32), ("t_keys_ms", f32), ("t_sort_ms", f32),
+                ("t_compact_ms", f32), ("t_total_ms", f32)]
+
+
+class SJError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libsj.so (fails loudly: the product path has no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"libsj.so not built at {path}: run `python -m paper_1803_04120_b200.build` "
+                           "(or __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(path)
+    P = ctypes.POINTER
+    L.sj_build_opts_default.argtypes = [P(BuildOpts)]
+    L.sj_build_opts_default.restype = None
+    L.sj_join_opts_default.argtypes = [P(JoinOpts)]
+    L.sj_join_opts_default.restype = None
+    L.sj_build_index.argtypes = [vp, u64, i32, dbl, P(BuildOpts), P(vp)]
+    L.sj_build_index.restype = i32
+    L.sj_self_join.argtypes = [vp, P(JoinOpts), P(vp)]
+    L.sj_self_join.restype = i32
+    L.sj_free_result.argtypes = [vp]
+    L.sj_free_result.restype = None
+    L.sj_free_index.argtypes = [vp]
+    L.sj_free_index.restype = None
+    L.sj_result_info.argtypes = [vp, P(u64), P(u32), P(Stats)]
+    L.sj_result_info.restype = i32
+    L.sj_result_batch.argtypes = [vp, u32, P(vp), P(u64), P(i32)]
+    L.sj_result_batch.restype = i32
+    L.sj_result_copy_to_host.argtypes = [vp, vp, u64]
+    L.sj_result_copy_to_host.restype = i32
+    L.sj_neighbor_counts.argtypes = [vp, P(JoinOpts), vp, P(u64)]
+    L.sj_neighbor_counts.restype = i32
+    L.sj_index_export.argtypes = [vp, P(IndexView)]
+    L.sj_index_export.restype = i32
+    L.sj_index_import.argtypes = [P(IndexView), i32, P(vp)]
+    L.sj_index_import.restype = i32
+    L.sj_set_allocator.argtypes = [vp, vp, vp]
+    L.sj_set_allocator.restype = None
+    L.sj_plan_batches.argtypes = [vp, u64, u64, u64, u64, u64, i32, dbl, vp, u32, P(u32), P(u64)]
+    L.sj_plan_batches.restype = i32
+    L.sj_kernel_launches.argtypes = []
+    L.sj_kernel_launches.restype = u64
+    L.sj_last_error.argtypes = []
+    L.sj_last_error.restype = ctypes.c_char_p
+    L.sj_abi_version.argtypes = []
+    L.sj_abi_version.restype = i32
+    _lib = L
+    return L
+
+
+def _check(st: int):
+    if st != 0:
+        msg = _lib.sj_last_error().decode(errors="replace")
+        raise SJError(st, msg)
+
+
+def kernel_launches() -> int:
+    return int(load_library().sj_kernel_launches())
+
+
+def join_opts(**kw) -> JoinOpts:
+    L = load_library()
+    o = JoinOpts()
+    L.sj_join_opts_default(ctypes.byref(o))
+    for k, v in kw.items():
+        if v is None:
+            continue
+        if not hasattr(o, k):
+            raise TypeError(f"unknown join option {k}")
+        setattr(o, k, int(v))
+    return o
+
+
+class Index:
+    """An sj_index handle (device-resident, immutable)."""
+
+    def __init__(self, handle: int, keepalive=None):
+        self._h = ctypes.c_void_p(handle)
+        self._keep = keepalive
+        self.view = IndexView()
+        _check(load_library().sj_index_export(self._h, ctypes.byref(self.view)))
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def n(self) -> int:
+        return int(self.view.n)
+
+    @property
+    def d(self) -> int:
+        return int(self.view.d)
+
+    @property
+    def n_cells(self) -> int:
+        return int(self.view.n_cells)
+
+    @property
+    def device(self) -> int:
+        return int(self.view.device)
+
+    def geometry(self) -> dict:
+        v = self.view
+        d = v.d
+        return dict(d=d, n=v.n, n_cells=v.n_cells, eps=v.eps, eps2=v.eps2, w=v.w,
+                    mins=list(v.mins[:d]), cpd=list(v.cpd[:d]), strides=list(v.strides[:d]),
+                    key_bits=v.key_bits, mask_offsets=list(v.mask_offsets[:d + 1]))
+
+    def timings(self) -> dict:
+        v = self.view
+        return dict(h2d_ms=v.t_h2d_ms, geometry_ms=v.t_geometry_ms, keys_ms=v.t_keys_ms,
+                    sort_ms=v.t_sort_ms, compact_ms=v.t_compact_ms, total_ms=v.t_total_ms)
+
+    def arrays(self) -> dict:
+        """Zero-copy torch views of the device arrays (B, G, A, pcell, X, masks)."""
+        import torch
+        v = self.view
+        n, nG, d = int(v.n), int(v.n_cells), int(v.d)
+        out = {
+            "B": _device_tensor(v.B, (nG,), torch.uint64, self.device, self),
+            "G": _device_tensor(v.G, (nG + 1,), torch.uint32, self.device, self),
+            "A": _device_tensor(v.A, (n,), torch.uint32, self.device, self),
+            "pcell": _device_tensor(v.pcell, (n,), torch.uint32, self.device, self),
+            "X": _device_tensor(v.X, (d, n), torch.float64, self.device, self),
+        }
+        if v.masks:
+            out["masks"] = _device_tensor(v.masks, (int(v.mask_offsets[d]),), torch.uint8, self.device, self)
+        return out
+
+    def free(self):
+        if self._h and self._h.value:
+            load_library().sj_free_index(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class _CudaArray:
+    """__cuda_array_interface__ wrapper so torch.as_tensor can view library-owned memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str, owner):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr or 0), False), "version": 3, "strides": None}
+        self._owner = owner
+
+
+_TYPESTR = {"uint64": "<u8", "uint32": "<u4", "float64": "<f8", "uint8": "|u1"}
+
+
+def _device_tensor(ptr, shape, dtype, device, owner):
+    import torch
+    name = str(dtype).replace("torch.", "")
+    if int(np.prod(shape)) == 0:
+        return torch.empty(shape, dtype=dtype, device=f"cuda:{device}")
+    t = torch.as_tensor(_CudaArray(ptr, shape, _TYPESTR[name], owner), device=f"cuda:{device}")
+    return t
+
+
+def build_index(points, eps: float, device: Optional[int] = None, stream=None, build_masks: bool = True) -> Index:
+    """sj_build_index.  points: N x d float64 (torch cuda/cpu tensor or numpy array)."""
+    L = load_library()
+    o = BuildOpts()
+    L.sj_build_opts_default(ctypes.byref(o))
+    o.build_masks = int(build_masks)
+    keep = None
+    try:
+        import torch
+        is_torch = isinstance(points, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        is_torch = False
+    if is_torch:
+        t = points
+        if t.dtype != torch.float64 or t.dim() != 2:
+            raise TypeError("points must be a 2-D float64 tensor")
+        t = t.contiguous()
+        keep = t
+        n, d = t.shape
+        ptr = t.data_ptr()
+        if t.is_cuda:
+            o.points_on_device = 1
+            o.device = t.device.index if device is None else device
+            o.stream = ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream) if stream is None \
+                else ctypes.c_void_p(stream)
+        else:
+            o.points_on_device = 0
+            o.device = 0 if device is None else device
+    else:
+        a = np.ascontiguousarray(points, dtype=np.float64)
+        if a.ndim != 2:
+            raise TypeError("points must be N x d")
+        keep = a
+        n, d = a.shape
+        ptr = a.ctypes.data
+        o.points_on_device = 0
+        o.device = 0 if device is None else device
+    h = ctypes.c_void_p()
+    _check(L.sj_build_index(ctypes.c_void_p(ptr), n, d, float(eps), ctypes.byref(o), ctypes.byref(h)))
+    del keep
+    return Index(h.value)
+
+
+class Result:
+    """An sj_result handle; batches are zero-copy views (torch on device, numpy on host)."""
+
+    def __init__(self, handle: int):
+        self._h = ctypes.c_void_p(handle)
+        L = load_library()
+        n, nb, st = u64(), u32(), Stats()
+        _check(L.sj_result_info(self._h, ctypes.byref(n), ctypes.byref(nb), ctypes.byref(st)))
+        self.n_pairs = int(n.value)
+        self.n_batches = int(nb.value)
+        self.stats = st.as_dict()
+        self.device = None
+
+    def batch(self, b: int):
+        L = load_library()
+        p, n, dev = vp(), u64(), i32()
+        _check(L.sj_result_batch(self._h, b, ctypes.byref(p), ctypes.byref(n), ctypes.byref(dev)))
+        if dev.value:
+            import torch
+            d = torch.cuda.current_device() if self.device is None else self.device
+            return _device_tensor(p.value, (int(n.value),), torch.uint64, d, self)
+        if n.value == 0:
+            return np.empty(0, dtype=np.uint64)
+        buf = (ctypes.c_uint64 * int(n.value)).from_address(p.value)
+        arr = np.ctypeslib.as_array(buf)
+        arr.flags.writeable = False
+        return arr
+
+    def batches(self):
+        return [self.batch(b) for b in range(self.n_batches)]
+
+    def to_numpy(self, sort: bool = True) -> np.ndarray:
+        out = np.empty(self.n_pairs, dtype=np.uint64)
+        _check(load_library().sj_result_copy_to_host(self._h, out.ctypes.data, self.n_pairs))
+        if sort:
+            out.sort()
+        return out
+
+    def free(self):
+        if self._h and self._h.value:
+            load_library().sj_free_result(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def self_join(index: Index, unicomp: bool = True, include_self: bool = True,
+              batch_capacity_pairs: Optional[int] = None, min_batches: Optional[int] = None,
+              n_streams: Optional[int] = None, result_on_host: bool = False,
+              query_begin: int = 0, query_end: int = 0, use_masks: bool = True) -> Result:
+    """sj_self_join over the index; see include/sj.h for the option semantics."""
+    L = load_library()
+    o = join_opts(unicomp=unicomp, include_self=include_self, batch_capacity_pairs=batch_capacity_pairs,
+                  min_batches=min_batches, n_streams=n_streams, result_on_host=result_on_host,
+                  query_begin=query_begin, query_end=query_end, use_masks=use_masks)
+    h = ctypes.c_void_p()
+    _check(L.sj_self_join(index.handle, ctypes.byref(o), ctypes.byref(h)))
+    r = Result(h.value)
+    r.device = index.device
+    return r
+
+
+def neighbor_counts(index: Index, unicomp: bool = True, include_self: bool = True,
+                    query_begin: int = 0, query_end: int = 0, out=None):
+    """sj_neighbor_counts -> (torch uint32 counts by original id on the device, total)."""
+    import torch
+    L = load_library()
+    o = join_opts(unicomp=unicomp, include_self=include_self, query_begin=query_begin, query_end=query_end)
+    if out is None:
+        out = torch.empty(index.n, dtype=torch.uint32, device=f"cuda:{index.device}")
+    tot = u64()
+    _check(L.sj_neighbor_counts(index.handle, ctypes.byref(o), ctypes.c_void_p(out.data_ptr()), ctypes.byref(tot)))
+    return out, int(tot.value)
+
+
+def import_index(view: IndexView, device: int) -> Index:
+    L = load_library()
+    h = ctypes.c_void_p()
+    _check(L.sj_index_import(ctypes.byref(view), device, ctypes.byref(h)))
+    return Index(h.value)
+
+
+def plan_batches(sample_counts, step: int, q_begin: int, q_end: int, capacity: int, min_batches: int = 3,
+                 margin: float = 0.25):
+    """Host-only batch planner (sj_plan_batches): returns (cuts, estimated_total)."""
+    L = load_library()
+    c = np.ascontiguousarray(sample_counts, dtype=np.uint32)
+    max_cuts = max(16, int(len(c)) * 4 + min_batches + 8)
+    cuts = np.zeros(max_cuts + 1, dtype=np.uint64)
+    k, tot = u32(), u64()
+    _check(L.sj_plan_batches(c.ctypes.data if len(c) else None, len(c), step, q_begin, q_end, capacity,
+                             min_batches, margin, cuts.ctypes.data, max_cuts, ctypes.byref(k), ctypes.byref(tot)))
+    return cuts[: k.value + 1].copy(), int(tot.value)

@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Bar (task rule ③): integer pair sets bit-exact after canonical sort; the FP64 predicate is
+evaluated with the same operation order on both sides, so there is no tolerance anywhere.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+from oracle import index_ref as ir
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def sj():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1803_04120_b200 as m
+    m.load_library()
+    return m
+
+
+def gpu_pairs(sj, pts, eps, **kw):
+    on_dev = kw.pop("points_on_device", True)
+    P = torch.from_numpy(pts).cuda() if on_dev else pts
+    idx = sj.build_index(P, eps)
+    res = sj.self_join(idx, **kw)
+    out = res.to_numpy(sort=True)
+    assert len(out) == res.n_pairs
+    return out, res, idx
+
+
+# ------------------------------------------------------------------ small exact parity matrix
+def _eps_for(n, d, mean_nbrs, L=100.0):
+    # eps such that the expected neighbours per point ~ mean_nbrs (ball volume, no boundary)
+    vol = mean_nbrs / n * L ** d
+    return (vol * math.gamma(1 + d / 2) / math.pi ** (d / 2)) ** (1.0 / d)
+
+
+MATRIX = [(d, n, m) for d in (2, 3, 4, 5, 6) for n in (10, 100, 1000, 5000) for m in (1, 10, 100)]
+
+
+@pytest.mark.parametrize("d,n,m", MATRIX)
+def test_uniform_matrix_exact(sj, d, n, m):
+    """SPEC criterion 1 (S.398): n in {10..5000}, d in 2..6, mean neighbours ~{1,10,100}."""
+    pts = datagen.uniform(n, d, seed=1000 * d + n + m)
+    eps = _eps_for(n, d, m)
+    want = oracle.brute_force(pts, eps)
+    got, res, _ = gpu_pairs(sj, pts, eps)
+    assert np.array_equal(got, want)
+    assert res.n_batches >= 3 or n < 3
+
+
+@pytest.mark.parametrize("d", [2, 3, 4, 5, 6])
+@pytest.mark.parametrize("kind", ["clustered", "knife", "dups", "lattice"])
+def test_structured_inputs_exact(sj, d, kind):
+    if kind == "clustered":
+        pts, eps = datagen.clustered_small(3000, d, seed=d), 0.5
+    elif kind == "knife":
+        pts, eps = datagen.knife_edge(3000, d, 0.1, seed=d), 0.1
+    elif kind == "dups":
+        pts = np.concatenate([datagen.duplicates(300, d), datagen.uniform(700, d, seed=d, hi=5.0)])
+        eps = 0.7
+    else:
+        L = {2: 40, 3: 12, 4: 6, 5: 4, 6: 3}[d]
+        pts, eps = datagen.lattice(L, d), 1.0
+    want = oracle.brute_force(pts, eps)
+    for unicomp in (True, False):
+        got, _, _ = gpu_pairs(sj, pts, eps, unicomp=unicomp)
+        assert np.array_equal(got, want), f"unicomp={unicomp}"
+
+
+@pytest.mark.parametrize("d,L", [(2, 30), (3, 10), (4, 6), (6, 3)])
+def test_lattice_closed_form(sj, d, L):
+    """P2 on the GPU: |S| = L^d + 2d(L-1)L^(d-1) (eps = 1, unit lattice)."""
+    got, _, _ = gpu_pairs(sj, datagen.lattice(L, d), 1.0)
+    assert len(got) == L ** d + 2 * d * (L - 1) * L ** (d - 1)
+
+
+def test_sqrt2_lattice(sj):
+    """P3: eps = fl(sqrt 2) accepts the face diagonals (interior count 1 + 2d^2)."""
+    d, L = 3, 6
+    P = datagen.lattice(L, d)
+    got, _, _ = gpu_pairs(sj, P, math.sqrt(2.0))
+    cnt = oracle.pair_counts(got, len(P))
+    interior = np.all((P > 0) & (P < L - 1), axis=1)
+    assert np.all(cnt[interior] == 1 + 2 * d * d)
+
+
+def test_worked_examples(sj):
+    """SPEC S.235-236, S.272-273, S.316."""
+    P = np.array([[0.0, 0.0], [3.0, 4.0]])
+    assert gpu_pairs(sj, P, 5.0)[0].tolist() == [0, 1, (1 << 32), (1 << 32) | 1]
+    assert gpu_pairs(sj, P, 4.9)[0].tolist() == [0, (1 << 32) | 1]
+    assert gpu_pairs(sj, np.array([[1.5, 2.5]]), 1.0)[0].tolist() == [0]
+    assert len(gpu_pairs(sj, np.array([[1.0, 1.0], [1.0, 1.0]]), 1.0)[0]) == 4
+    P = np.array([[0.0, 0.0], [1.0, 0.0], [2.0, 0.0]])
+    assert len(gpu_pairs(sj, P, 1.0)[0]) == 7
+
+
+def test_include_self_false(sj):
+    pts = datagen.uniform(3000, 3, seed=5)
+    want = oracle.brute_force(pts, 6.0, include_self=False)
+    for unicomp in (True, False):
+        got, _, _ = gpu_pairs(sj, pts, 6.0, include_self=False, unicomp=unicomp)
+        assert np.array_equal(got, want)
+
+
+def test_host_points_and_host_results(sj):
+    pts = datagen.uniform(4000, 4, seed=9)
+    want = oracle.brute_force(pts, 12.0)
+    got, res, _ = gpu_pairs(sj, pts, 12.0, points_on_device=False, result_on_host=True)
+    assert np.array_equal(got, want)
+    b0 = res.batch(0)
+    assert isinstance(b0, np.ndarray)
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_batching_invariance_and_overflow(sj, host):
+    """SPEC criterion 4 (S.401): identical output for any capacity / min_batches; tiny
+    capacities force overflow re-runs (device: exact realloc; host: split)."""
+    pts = datagen.uniform(6000, 2, seed=3)
+    eps = 2.0
+    want = oracle.brute_force(pts, eps)
+    for cap, mb in ((1 << 28, 3), (1000, 5), (100, 8), (10_000_000, 1)):
+        got, res, _ = gpu_pairs(sj, pts, eps, batch_capacity_pairs=cap, min_batches=mb, result_on_host=host)
+        assert np.array_equal(got, want)
+        assert res.n_batches >= min(mb, 1)
+        if cap == 100:
+            assert res.stats["retries"] > 0
+
+
+@pytest.mark.parametrize("streams", [1, 2, 5])
+def test_stream_count_invariance(sj, streams):
+    pts = datagen.uniform(5000, 3, seed=4)
+    want = oracle.brute_force(pts, 7.0)
+    for host in (False, True):
+        got, _, _ = gpu_pairs(sj, pts, 7.0, n_streams=streams, result_on_host=host)
+        assert np.array_equal(got, want)
+
+
+def test_query_range_shards_union(sj):
+    """North star sharding: the union over a partition of [0,N) in A-order is S (no dups)."""
+    pts = datagen.uniform(5000, 4, seed=12)
+    eps = 15.0
+    want = oracle.brute_force(pts, eps)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    for parts in (2, 3, 8):
+        cuts = np.linspace(0, 5000, parts + 1).astype(int)
+        allp = np.concatenate([sj.self_join(idx, query_begin=int(a), query_end=int(b)).to_numpy(sort=False)
+                               for a, b in zip(cuts[:-1], cuts[1:])])
+        allp.sort()
+        assert np.array_equal(allp, want)
+
+
+def test_neighbor_counts(sj):
+    """P6: per-point counts equal the oracle's; the total equals |S|."""
+    pts = datagen.clustered_small(4000, 3, seed=8)
+    eps = 0.6
+    want = oracle.brute_force(pts, eps)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    for unicomp in (True, False):
+        cnt, tot = sj.neighbor_counts(idx, unicomp=unicomp)
+        assert tot == len(want)
+        assert np.array_equal(cnt.cpu().numpy().astype(np.int64), oracle.pair_counts(want, len(pts)))
+
+
+# ------------------------------------------------------------------ index parity
+@pytest.mark.parametrize("d", [2, 3, 4, 5, 6])
+def test_index_matches_oracle_index(sj, d):
+    """a1-a4 vs the oracle's statement of §4.2-4.4: geometry, B, G, A, masks bit-exact."""
+    for pts, eps in ((datagen.uniform(3000, d, seed=d), 9.0), (datagen.knife_edge(2000, d, 0.1, seed=d), 0.1),
+                     (datagen.clustered_small(2500, d, seed=d), 0.3)):
+        ref = ir.build_index(pts, eps)
+        idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+        g = idx.geometry()
+        assert g["w"] == ref.geom.w and g["cpd"] == ref.geom.cpd and g["strides"] == ref.geom.strides
+        assert g["mins"] == ref.geom.mins.tolist()
+        arr = idx.arrays()
+        assert arr["B"].cpu().numpy().tolist() == ref.B
+        assert arr["G"].cpu().numpy().astype(np.int64).tolist() == ref.G.tolist()
+        assert np.array_equal(arr["A"].cpu().numpy().astype(np.int64), ref.A)
+        X = arr["X"].cpu().numpy()
+        assert np.array_equal(X, pts[ref.A].T)
+        pc = arr["pcell"].cpu().numpy().astype(np.int64)
+        assert np.array_equal(pc, np.repeat(np.arange(len(ref.B)), np.diff(ref.G)))
+        if "masks" in arr:
+            m = arr["masks"].cpu().numpy()
+            off = g["mask_offsets"]
+            for j in range(d):
+                assert np.nonzero(m[off[j]:off[j + 1]])[0].tolist() == ref.M[j]
+
+
+def test_fig2_fixture_on_gpu(sj):
+    """the GPU index of the Fig. 2 replica."""
+    P = np.loadtxt(os.path.join(GOLDEN, "fig2_points.txt"))
+    idx = sj.build_index(torch.from_numpy(P).cuda(), 1.0)
+    arr = idx.arrays()
+    B = arr["B"].cpu().numpy().tolist()
+    assert len(B) == 11 and B[5] == 22 and B[6] == 30
+    G = arr["G"].cpu().numpy()
+    A = arr["A"].cpu().numpy()
+    assert set(A[G[5]:G[6]].tolist()) == {35, 6}
+    assert np.array_equal(gpu_pairs(sj, P, 1.0)[0], oracle.brute_force(P, 1.0))
+
+
+def test_errors(sj):
+    P = datagen.uniform(100, 3, seed=1)
+    bad = P.copy()
+    bad[17, 2] = np.nan
+    with pytest.raises(sj.SJError) as e:
+        sj.build_index(torch.from_numpy(bad).cuda(), 1.0)
+    assert e.value.name == "SJ_ERR_NONFINITE"
+    with pytest.raises(sj.SJError) as e:
+        sj.build_index(torch.from_numpy(datagen.uniform(100, 6, seed=2, hi=1e6)).cuda(), 1e-3)
+    assert e.value.name == "SJ_ERR_KEY_OVERFLOW"
+    idx = sj.build_index(torch.from_numpy(P).cuda(), 1.0)
+    with pytest.raises(sj.SJError) as e:
+        sj.self_join(idx, query_begin=5, query_end=1000)
+    assert e.value.name == "SJ_ERR_ARG"
+
+
+def test_c1_config_exact(sj):
+    """BASELINE.json configs[0]: Syn-2D 10K, eps=2.5 -- full pair set."""
+    pts = datagen.uniform_config("C1", 2)
+    want = oracle.grid_join(pts, 2.5)
+    for unicomp in (True, False):
+        got, _, _ = gpu_pairs(sj, pts, 2.5, unicomp=unicomp)
+        assert np.array_equal(got, want)
+
+
+# ------------------------------------------------------------------ full-size sampled parity
+def _sampled_rows_check(sj, pts, eps, nsample=64, seed=0, **kw):
+    n = len(pts)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    res = sj.self_join(idx, **kw)
+    rng = np.random.default_rng(seed)
+    q = np.unique(rng.integers(0, n, nsample))
+    cnt, want = oracle.rows(pts, eps, q)
+    qt = torch.from_numpy(q.astype(np.int64)).cuda()
+    got = []
+    for b in res.batches():
+        bt = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.asarray(b)).cuda()
+        keys = (bt.view(torch.int64) >> 32)
+        sel = torch.isin(keys, qt)
+        got.append(bt[sel].cpu().numpy())
+    got = np.sort(np.concatenate(got)) if got else np.empty(0, np.uint64)
+    assert np.array_equal(got, want)
+    return res
+
+
+@pytest.mark.parametrize("d", [2, 3, 4, 5, 6])
+def test_c2_full_size_sampled_rows(sj, d):
+    """BASELINE.json configs[1] (Syn-dD 2M, eps=1) at full size, in the bench's launch
+    configuration: sampled neighbour rows == oracle brute-force rows; |S| vs P4 expectation."""
+    pts = datagen.uniform_config("C2", d)
+    res = _sampled_rows_check(sj, pts, 1.0, nsample=48, seed=d)
+    exp = oracle.expected_pairs_uniform(len(pts), d, 1.0)
+    assert abs(res.n_pairs - exp) / exp < 0.01
+
+
+def test_c2_6d_total_equals_oracle_count(sj):
+    """Total |S| for the bench workload equals the oracle's exact count (grid join)."""
+    pts = datagen.uniform_config("C2", 6)
+    want = int(oracle.grid_join(pts, 1.0, count_only=True).sum())
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), 1.0)
+    assert sj.self_join(idx).n_pairs == want
+    cnt, tot = sj.neighbor_counts(idx)
+    assert tot == want
+
+
+def test_c3_eps8_sampled_rows(sj):
+    """C3 (Syn-6D 2M, eps=8): sampled rows exact."""
+    pts = datagen.uniform_config("C3", 6)
+    _sampled_rows_check(sj, pts, 8.0, nsample=32, seed=8)
