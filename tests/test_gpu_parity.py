@@ -249,9 +249,9 @@ def _sampled_rows_check(sj, pts, eps, nsample=64, seed=0, **kw):
     got = []
     for b in res.batches():
         bt = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.asarray(b)).cuda()
-        keys = (bt.view(torch.int64) >> 32)
-        sel = torch.isin(keys, qt)
-        got.append(bt[sel].cpu().numpy())
+        b64 = bt.view(torch.int64)
+        sel = torch.isin(b64 >> 32, qt)
+        got.append(b64[sel].cpu().numpy().view(np.uint64))
     got = np.sort(np.concatenate(got)) if got else np.empty(0, np.uint64)
     assert np.array_equal(got, want)
     return res
