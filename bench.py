@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the epsilon self-join hot path (BASELINE.json metric: "self-join time (s) and result
+pairs/s, Syn-6D 2M pts, at 1/2/4/8 B200").
+
+Workload (config.workload): Syn-6D, N = 2,000,000 iid uniform points in [0,100]^6 (
+datagen seed 1803_04120+100*6+1), eps = 1 (BASELINE.json configs[1], Fig. 1(a) set-up PAPER.md:66).
+One STEP = the whole hot path: index build (geometry, keys, radix sort,
+compaction/gather) + estimator + batch plan + refine/emission of every batch; N>1: rank-0 build,
+NCCL broadcast of the index, per-rank shard join, all-reduce of the counts.
+
+  value : result pairs/s of the whole job, inputs resident in HBM, results left in HBM.
+  e2e   : same metric through the C ABI with HOST buffers: pinned N x d input copied H2D and every
+          result batch drained D2H to pinned host memory inside the timed region.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "self-join result pairs/s, Syn-6D 2M pts"
+UNIT = "pairs/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--d", type=int, default=6)
+    ap.add_argument("--n", type=int, default=2_000_000)
+    ap.add_argument("--eps", type=float, default=1.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle sample duration")
+    ap.add_argument("--phases", action="store_true", help="also print per-phase timings (stderr)")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling DURING the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4) if r[3 + i] == "Active"})
+        loaded = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)]
+        return {"sm_mhz": statistics.median(loaded or sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def cpu_baseline(pts, eps, seconds: float):
+    """The oracle (oracle/ grid join, plain C, all host threads) on a bounded query sample of the
+    same workload: every sampled query is joined against all N points."""
+    import oracle
+    n = len(pts)
+    threads = os.cpu_count() or 1
+    probe = min(n, 20_000)
+    t0 = time.perf_counter()
+    c = oracle.grid_join(pts, eps, q0=0, q1=probe, nthreads=threads, count_only=True)
+    t_probe = time.perf_counter() - t0
+    q = min(n, max(probe, int(probe * seconds / max(t_probe, 1e-3))))
+    t0 = time.perf_counter()
+    c = oracle.grid_join(pts, eps, q0=0, q1=q, nthreads=threads, count_only=True)
+    dt = time.perf_counter() - t0
+    pairs = int(c.sum())
+    return {"value": pairs / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"queries [0,{q}) of the {n}-point workload joined against all {n} points "
+                      f"(full 3^d hash-grid scan incl. its grid build; count-only), {dt:.2f} s, {pairs} pairs",
+            "seconds": dt, "pairs": pairs}
+
+
+def dist_setup(gpus: int):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores (this tier's reference arm)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import datagen
+    pts = datagen.uniform(args.n, args.d, datagen.seed_for(args.d, "C2"))
+    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        cpu_baseline(pts, args.eps, per_step / 4)
+    vals = []
+    secs = []
+    last = None
+    for _ in range(args.steps):
+        last = cpu_baseline(pts, args.eps, per_step)
+        vals.append(last["value"])
+        secs.append(last["seconds"])
+    v = statistics.mean(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(secs),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"Syn-{args.d}D uniform [0,100]^{args.d}, N={args.n}, eps={args.eps}",
+                       "sample": "bounded query sample per step (see cpu_baseline.sample)"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
+                             "sample": last["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import datagen
+    import paper_1803_04120_b200 as sj
+    from paper_1803_04120_b200 import distributed as sjd
+
+    world, rank, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
+    sj.load_library()
+
+    pts = datagen.uniform(args.n, args.d, datagen.seed_for(args.d, "C2"))
+    pts_dev = torch.from_numpy(pts).to(dev)
+    pts_pin = torch.from_numpy(pts).pin_memory()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def step(points, host_results=False):
+        res, total, idx = sjd.sharded_self_join(points, args.eps, local, result_on_host=host_results)
+        return res, total, idx
+
+    def timed(points, host_results, k):
+        total_ms = 0.0
+        pairs = None
+        info = []
+        for _ in range(k):
+            flush.zero_()
+            barrier()
+            torch.cuda.synchronize(dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res, total, idx = step(points, host_results)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            barrier()
+            total_ms += e0.elapsed_time(e1)
+            pairs = total
+            info.append((res.stats if res is not None else None, idx.timings()))
+            if res is not None:
+                res.free()
+            del idx
+        if world > 1:
+            total_ms = float(sjd.allreduce_counts([total_ms], dev, op="max")[0])
+        return total_ms, pairs, info
+
+    # warm-up (W >= 3 untimed steps)
+    for _ in range(args.warmup):
+        res, total, idx = step(pts_dev)
+        if res is not None:
+            res.free()
+        del idx
+    torch.cuda.synchronize(dev)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = sj.kernel_launches()
+    ms, pairs, info = timed(pts_dev, False, args.steps)
+    launches = sj.kernel_launches() - l0
+    clk = clocks.stop()
+    value = pairs * args.steps / (ms / 1000.0)
+
+    e2e = None
+    if not args.no_e2e:
+        ms_e2e, pairs_e2e, _ = timed(pts_pin, True, args.steps)
+        assert pairs_e2e == pairs
+        e2e = {"value": pairs_e2e * args.steps / (ms_e2e / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(8 * args.n * args.d), "d2h_bytes_per_step": int(8 * pairs_e2e),
+               "ms_per_step": ms_e2e / args.steps}
+
+    # ---- per-phase device times (CUDA events recorded by the library on its launch streams)
+    st = [i[0] for i in info if i[0] is not None]
+    bt = [i[1] for i in info]
+    mean = lambda xs: sum(xs) / len(xs)
+    phases = {
+        "build_total_ms": mean([b["total_ms"] for b in bt]),
+        "build_keys_ms": mean([b["keys_ms"] for b in bt]),
+        "build_sort_ms": mean([b["sort_ms"] for b in bt]),
+        "build_compact_ms": mean([b["compact_ms"] for b in bt]),
+        "build_geometry_ms": mean([b["geometry_ms"] for b in bt]),
+        "estimate_ms": mean([s["estimate_ms"] for s in st]),
+        "refine_ms_sum": mean([s["refine_ms"] for s in st]),
+        "refine_launch_max_ms": mean([s["refine_max_ms"] for s in st]),
+        "refine_launches": st[-1]["refine_launches"],
+        "join_total_ms": mean([s["total_ms"] for s in st]),
+        "cells_probed": st[-1]["cells_probed"],
+        "candidates_tested": st[-1]["candidates_tested"],
+        "batches": st[-1]["batches"],
+    }
+    peaks, peak_src = measured_peaks()
+
+    # ---- roofline of the dominant kernel: the refine kernel (k_refine<..., kEmit>)
+    # Algorithmic HBM bytes per launch: every query of the batch reads its
+    # own point, cell id and A id once (8d + 4 + 4 B) and writes 8 B per emitted pair; the index
+    # it searches (B: 8|G| B, G: 4|G| B) is read once per launch.
+    n_local = args.n
+    nb = max(1, phases["batches"])
+    per_launch_queries = n_local / world / nb
+    per_launch_pairs = pairs / world / nb
+    n_cells = idx_cells = None
+    alg_bytes = per_launch_queries * (8 * args.d + 8) + per_launch_pairs * 8
+    avg_launch_ms = phases["refine_ms_sum"] / max(1, phases["refine_launches"])
+    achieved = alg_bytes / (avg_launch_ms / 1000.0) / 1e9
+    roof = {"kernel": "k_refine<6,kEmit,unicomp>", "bound": "hbm", "achieved": achieved,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+            "traffic": None, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_launch_ms}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(pts, args.eps, args.cpu_seconds)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"Syn-{args.d}D uniform [0,100]^{args.d}, N={args.n}, eps={args.eps} "
+                                       f"(BASELINE.json configs[1], 6-D member)",
+                           "n": args.n, "d": args.d, "eps": args.eps, "pairs_per_step": pairs,
+                           "parallelism": f"query-shard x{world}, replicated index (NCCL broadcast)",
+                           "l2": "flushed (512 MB write) before every timed step",
+                           "results": "device-resident batches (value); pinned-host drained batches (e2e)"},
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
+                "cpu_baseline": cpu, "phases": phases}
+        print(json.dumps(line), flush=True)
+        if args.phases:
+            print(json.dumps(phases, indent=1), file=sys.stderr)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -114,6 +114,10 @@ typedef struct {
     const uint32_t *pcell;       /* [n] cell h of each A-position                                  */
     const double *X;             /* [d][n] SoA coordinates in A-order: X[j*n+k] = D[A[k]][j]      */
     const uint8_t *masks;        /* concatenated M_j byte maps (1 = coordinate occupied) or NULL   */
+    int dir_k;                   /* prefix directory over the dir_k slowest dimensions (bounds every
+                                    binary search of B; rebuilt from B on import)                  */
+    uint64_t dir_entries;        /* entries of dir (= number of prefixes + 1)                     */
+    const uint32_t *dir;         /* [dir_entries] dir[p] = first cell with top-dir_k prefix >= p   */
     /* build timings (CUDA events, ms) */
     float t_h2d_ms, t_geometry_ms, t_keys_ms, t_sort_ms, t_compact_ms, t_total_ms;
 } sj_index_view;

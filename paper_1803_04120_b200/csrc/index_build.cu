@@ -8,11 +8,12 @@
 // R8 dimension 1 fastest; R9 M_j as occupied sets; R14 A ordered by (linear id, point id).
 //
 // Kernels (all HBM-bound; algorithmic bytes in DESIGN.md §Roofline):
-//   k_minmax_partial/k_minmax_final : exact per-dimension min/max + non-finite check (a1)
+//   k_minmax                        : exact per-dimension min/max + non-finite check (a1)
 //   k_keys                          : cell coordinates -> linear id, identity ids, mask bytes (a2)
 //   radix sort                      : stable LSD over key_bits (a3, radix_sort.cu)
 //   k_heads + inclusive scan        : cell index of every A-position (a4)
 //   k_compact_gather                : B, G starts, SoA coordinates X[j][k] = D[A[k]][j] (a4)
+//   k_dir_fill                      : prefix directory bounding every B search (a4)
 #include <cmath>
 #include <cstring>
 
@@ -24,9 +25,19 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// Order-preserving map of a (non-NaN) double to uint64, so min/max become integer atomics.
+__device__ __forceinline__ unsigned long long ord_key(double x)
+{
+    const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// a1: exact per-dimension min/max (+ non-finite flag) in ONE pass: block reduce, then one
+// atomicMin/atomicMax per dimension per block on the order-preserving integer image.
+// mm[0..D) = ord(min), mm[D..2D) = ord(max); initialised to UINT64_MAX / 0.
 template <int D>
 __global__ void __launch_bounds__(kThreads)
-k_minmax_partial(const double *__restrict__ pts, uint32_t n, double *__restrict__ part, uint32_t *nonfinite)
+k_minmax(const double *__restrict__ pts, uint32_t n, unsigned long long *__restrict__ mm, uint32_t *nonfinite)
 {
     double mn[D], mx[D];
 #pragma unroll
@@ -59,23 +70,18 @@ k_minmax_partial(const double *__restrict__ pts, uint32_t n, double *__restrict_
         const int j = threadIdx.x;
         double a = INFINITY, b = -INFINITY;
         for (int w = 0; w < kThreads / 32; ++w) { a = fmin(a, s_mn[w][j]); b = fmax(b, s_mx[w][j]); }
-        part[(uint64_t)blockIdx.x * 2 * D + j] = a;
-        part[(uint64_t)blockIdx.x * 2 * D + D + j] = b;
+        if (a <= b) {   // block saw at least one (finite) point
+            atomicMin(mm + j, ord_key(a));
+            atomicMax(mm + D + j, ord_key(b));
+        }
     }
 }
 
-__global__ void k_minmax_final(const double *__restrict__ part, int nparts, int d, double *__restrict__ out)
+__global__ void k_minmax_init(unsigned long long *mm, int d, uint32_t *nonfinite)
 {
-    // out[0..d) = mins, out[d..2d) = maxs ; one thread per (j, min|max)
     const int t = threadIdx.x;
-    if (t >= 2 * d) return;
-    const bool is_max = t >= d;
-    double acc = is_max ? -INFINITY : INFINITY;
-    for (int p = 0; p < nparts; ++p) {
-        const double v = part[(uint64_t)p * 2 * d + t];
-        acc = is_max ? fmax(acc, v) : fmin(acc, v);
-    }
-    out[t] = acc;
+    if (t < 2 * d) mm[t] = (t < d) ? ~0ull : 0ull;
+    if (t == 0) *nonfinite = 0;
 }
 
 // Cell coordinate c_j = 1 + floor(fl(fl(x_j - min_j) / w))  (reading R7), linear id with
@@ -94,7 +100,10 @@ k_keys(const double *__restrict__ pts, uint32_t n, DevIndex ix, uint64_t *__rest
         const double t = floor(__ddiv_rn(__dsub_rn(x, ix.mins[j]), ix.w));
         const uint64_t c = 1ull + (uint64_t)t;
         key += c * ix.strides[j];
-        if (masks) masks[ix.mask_off[j] + c] = 1;   // benign same-value races
+        if (masks) {                                 // read-before-write: no same-address storm
+            uint8_t *m = masks + ix.mask_off[j] + c;
+            if (!*m) *m = 1;                         // benign same-value race
+        }
     }
     keys[i] = key;
     ids[i] = (uint32_t)i;
@@ -136,7 +145,7 @@ void launch_dim(int which, dim3 g, dim3 b, cudaStream_t s, const double *pts, ui
                 uint64_t *keys, uint32_t *ids, uint8_t *masks, double *part, uint32_t *nonfinite,
                 const uint32_t *A, uint32_t *pcell, uint64_t *B, uint32_t *G, double *X)
 {
-    if (which == 0) k_minmax_partial<D><<<g, b, 0, s>>>(pts, n, part, nonfinite);
+    if (which == 0) k_minmax<D><<<g, b, 0, s>>>(pts, n, reinterpret_cast<unsigned long long *>(part), nonfinite);
     else if (which == 1) k_keys<D><<<g, b, 0, s>>>(pts, n, ix, keys, ids, masks);
     else k_compact_gather<D><<<g, b, 0, s>>>(keys, A, pts, n, pcell, B, G, X);
     SJ_LAUNCHED();
@@ -221,16 +230,9 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
     if (o.device < 0 || o.device >= ndev) fail(SJ_ERR_ARG, "bad device ordinal");
     SJ_CUDA(cudaSetDevice(o.device));
 
-    cudaStream_t s = static_cast<cudaStream_t>(o.stream);
-    bool own_stream = false;
-    if (!s) {
-        SJ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-        own_stream = true;
-    }
-    struct StreamGuard {
-        cudaStream_t s; bool own;
-        ~StreamGuard() { if (own) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } }
-    } sg{s, own_stream};
+    // the build runs on the caller's stream, or on a pooled library stream
+    CtxGuard cg{o.stream ? nullptr : acquire_ctx(o.device, 1, 0, 64)};
+    cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : cg.c->streams[0];
 
     const uint32_t N = (uint32_t)n;
     EventTimer ev(7);
@@ -247,28 +249,32 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
     }
     ev.rec(1, s);
 
-    // ---- a1: exact per-dimension min/max + finiteness
+    // ---- a1: exact per-dimension min/max + finiteness (one kernel, integer atomics)
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device);
     const uint32_t parts = (uint32_t)std::min<uint64_t>((n + kThreads - 1) / kThreads, (uint64_t)nsm * 4);
-    Scratch<double> part((size_t)parts * 2 * d, s);
-    Scratch<double> mm(2 * d, s);
+    Scratch<unsigned long long> mm(2 * d, s);
     Scratch<uint32_t> nonfinite(1, s);
-    SJ_CUDA(cudaMemsetAsync(nonfinite.p, 0, sizeof(uint32_t), s));
+    k_minmax_init<<<1, 32, 0, s>>>(mm.p, d, nonfinite.p);
+    SJ_LAUNCHED();
     DevIndex ix{};
     ix.d = d;
     ix.n = N;
-    launch(d, 0, dim3(parts), dim3(kThreads), s, pts, N, ix, nullptr, nullptr, nullptr, part.p, nonfinite.p,
-           nullptr, nullptr, nullptr, nullptr, nullptr);
-    k_minmax_final<<<1, 32, 0, s>>>(part.p, (int)parts, d, mm.p);
-    SJ_LAUNCHED();
-    double h_mm[2 * SJ_MAX_DIM];
+    launch(d, 0, dim3(parts), dim3(kThreads), s, pts, N, ix, nullptr, nullptr, nullptr,
+           reinterpret_cast<double *>(mm.p), nonfinite.p, nullptr, nullptr, nullptr, nullptr, nullptr);
+    unsigned long long h_ord[2 * SJ_MAX_DIM];
     uint32_t h_bad = 0;
-    SJ_CUDA(cudaMemcpyAsync(h_mm, mm.p, sizeof(double) * 2 * d, cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaMemcpyAsync(h_ord, mm.p, sizeof(unsigned long long) * 2 * d, cudaMemcpyDeviceToHost, s));
     SJ_CUDA(cudaMemcpyAsync(&h_bad, nonfinite.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     SJ_CUDA(cudaStreamSynchronize(s));
     ev.rec(2, s);
     if (h_bad) fail(SJ_ERR_NONFINITE, "a coordinate is NaN or infinite");
+    double h_mm[2 * SJ_MAX_DIM];
+    for (int t = 0; t < 2 * d; ++t) {
+        const unsigned long long k = h_ord[t];
+        const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+        std::memcpy(&h_mm[t], &u, sizeof(double));
+    }
 
     sj_index_view v{};
     v.d = d;
@@ -367,12 +373,80 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
         ix.masks = masks;
         idx->view = v;
         idx->dev = ix;
+        build_directory(idx, s);
+        ev.rec(6, s);
+        SJ_CUDA(cudaStreamSynchronize(s));
+        idx->view.t_compact_ms = ev.ms(4, 6);
+        idx->view.t_total_ms = ev.ms(0, 6);
     } catch (...) {
         cudaStreamSynchronize(s);
         free_index_impl(idx);
         throw;
     }
     return idx;
+}
+
+namespace {
+// Directory fill: cell h writes dir[q] = h for every prefix q in (prefix(h-1), prefix(h)];
+// the last cell also fills the tail with nG.  Total writes = P + 1.
+__global__ void __launch_bounds__(kThreads)
+k_dir_fill(const uint64_t *__restrict__ B, uint32_t nG, uint64_t div, uint64_t P, uint32_t *__restrict__ dir)
+{
+    const uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= nG) return;
+    const uint64_t ph = B[h] / div;
+    const uint64_t start = (h == 0) ? 0 : B[h - 1] / div + 1;
+    for (uint64_t q = start; q <= ph; ++q) dir[q] = (uint32_t)h;
+    if (h == nG - 1)
+        for (uint64_t q = ph + 1; q <= P; ++q) dir[q] = nG;
+}
+}  // namespace
+
+// Prefix directory: the largest k such that the number of
+// top-k coordinate prefixes P_k = prod_{j >= d-k} |g_j| stays <= max(4|G|, 2^16), so the
+// directory costs <= 16 B per non-empty cell (space stays O(|D|)).  Every B
+// lookup of the refine is then a binary search bounded to one prefix's range.
+void build_directory(sj_index *idx, cudaStream_t s)
+{
+    sj_index_view &v = idx->view;
+    DevIndex &ix = idx->dev;
+    const int d = v.d;
+    const unsigned __int128 cap = std::max<uint64_t>(4ull * v.n_cells, 1ull << 16);
+    int k = 0;
+    unsigned __int128 P = 1;
+    for (int kk = 1; kk <= d; ++kk) {
+        const unsigned __int128 Q = P * v.cpd[d - kk];
+        if (Q > cap) break;
+        P = Q;
+        k = kk;
+    }
+    uint64_t div = 1;
+    for (int j = 0; j < d - k; ++j) div *= v.cpd[j];   // = strides[d-k] (or prod all for k=0)
+    uint32_t *dir = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * ((size_t)P + 1), s));
+    idx->bufs[idx->nbufs++] = dir;
+    const uint32_t nG = (uint32_t)v.n_cells;
+    k_dir_fill<<<(nG + kThreads - 1) / kThreads, kThreads, 0, s>>>(v.B, nG, div, (uint64_t)P, dir);
+    SJ_LAUNCHED();
+    v.dir_k = k;
+    v.dir_entries = (uint64_t)P + 1;
+    v.dir = dir;
+    ix.dir = dir;
+    ix.dir_k = k;
+    ix.dir_P = (uint64_t)P;
+    ix.dir_div = div;
+    for (int j = 0; j < SJ_MAX_DIM; ++j) ix.pstride[j] = (j < d && j >= d - k) ? v.strides[j] / div : 0;
+    uint32_t ntop = 1;
+    for (int j = 0; j < k; ++j) ntop *= 3;
+    ix.dir_ntop = ntop;
+    for (int j = 0; j < d; ++j) ix.inv_cpd[j] = 1.0 / (double)v.cpd[j];
+    ix.lowR[0] = 0;
+    for (int j = 0; j < d; ++j) ix.lowR[j + 1] = ix.lowR[j] + (int64_t)(j < d - k ? v.strides[j] : 0);
+    // mode: a dense directory gives O(1) rows; small prefix ranges (<= 8 cells on average) are
+    // cheapest to scan cell by cell (sparse high-d data); otherwise bounded row searches.
+    const double avg_range = (double)v.n_cells / (double)(uint64_t)P;
+    if (k == d) ix.search_mode = kSearchDenseRows;
+    else if (avg_range <= 8.0 && (double)div < 4.0e15) ix.search_mode = kSearchCellScan;
+    else ix.search_mode = kSearchRows;
 }
 
 void free_index_impl(sj_index *idx)
@@ -433,6 +507,8 @@ sj_index *import_index_impl(const sj_index_view &src, int device)
         ix.B = B; ix.G = G; ix.A = A; ix.pcell = pcell; ix.X = X; ix.masks = masks;
         idx->view = v;
         idx->dev = ix;
+        build_directory(idx, s);
+        SJ_CUDA(cudaStreamSynchronize(s));
     } catch (...) {
         cudaStreamDestroy(s);
         free_index_impl(idx);

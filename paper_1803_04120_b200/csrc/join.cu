@@ -42,27 +42,6 @@ void launch_refine(const DevIndex &ix, const JoinArgs &ja, bool unicomp, uint32_
     SJ_LAUNCHED();
 }
 
-struct Streams {
-    std::vector<cudaStream_t> s;
-    explicit Streams(int n)
-    {
-        s.resize(n);
-        for (auto &x : s) SJ_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
-    }
-    ~Streams()
-    {
-        for (auto x : s) { cudaStreamSynchronize(x); cudaStreamDestroy(x); }
-    }
-};
-
-struct Ev {
-    cudaEvent_t e{};
-    Ev() { SJ_CUDA(cudaEventCreate(&e)); }
-    ~Ev() { cudaEventDestroy(e); }
-    Ev(const Ev &) = delete;
-    Ev &operator=(const Ev &) = delete;
-};
-
 void validate(const sj_index *idx, const sj_join_opts &o, uint64_t *qb, uint64_t *qe)
 {
     if (!idx) fail(SJ_ERR_STATE, "index is NULL");
@@ -174,56 +153,63 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     SJ_CUDA(cudaSetDevice(idx->device));
     const DevIndex &ix = idx->dev;
     const int S = o.n_streams;
-    Streams st(S);
-    cudaStream_t s0 = st.s[0];
+
+    // per-call execution context (pooled): S streams, events, slot buffers
+    struct Slot { unsigned long long cursor; uint32_t overflow; uint32_t pad; };
+    constexpr size_t kWorkBytes = 64;                 // 4 u64 work counters (+pad)
+    const uint64_t nq = q1 - q0;
+    const Sample sm = make_sample(nq);
+    const size_t slot_need = kWorkBytes + sizeof(Slot) * (size_t)std::max<int>(S, 64) + 4 * (size_t)(sm.ns + 1);
+    CtxGuard cg{acquire_ctx(idx->device, S, 2 * S + 2, slot_need)};
+    DevCtx &cx = *cg.c;
+    cudaStream_t s0 = cx.streams[0];
+    unsigned long long *work = static_cast<unsigned long long *>(cx.d_slots);
+    unsigned long long *hwork = static_cast<unsigned long long *>(cx.h_slots);
+    Slot *dslots = reinterpret_cast<Slot *>(static_cast<char *>(cx.d_slots) + kWorkBytes);
+    Slot *hslots = reinterpret_cast<Slot *>(static_cast<char *>(cx.h_slots) + kWorkBytes);
+    const size_t slot_cap = (cx.slot_bytes - kWorkBytes - 4 * (size_t)(sm.ns + 1)) / sizeof(Slot);
+    uint32_t *dqcount = reinterpret_cast<uint32_t *>(static_cast<char *>(cx.d_slots) + cx.slot_bytes -
+                                                     4 * (size_t)(sm.ns + 1));
+    uint32_t *hqcount = reinterpret_cast<uint32_t *>(static_cast<char *>(cx.h_slots) + cx.slot_bytes -
+                                                     4 * (size_t)(sm.ns + 1));
 
     sj_result *res = new sj_result();
     res->device = idx->device;
     sj_stats &stats = res->stats;
     try {
-        Scratch<unsigned long long> work(4, s0);
-        SJ_CUDA(cudaMemsetAsync(work.p, 0, 4 * sizeof(unsigned long long), s0));
-
+        SJ_CUDA(cudaMemsetAsync(work, 0, kWorkBytes, s0));
         // ---- a5: estimate on a strided sample (count-only refine)
-        const uint64_t nq = q1 - q0;
-        const Sample sm = make_sample(nq);
-        std::vector<uint32_t> hcnt(sm.ns ? sm.ns : 1, 0);
         float est_ms = 0;
         if (sm.ns) {
-            Scratch<uint32_t> qcount(sm.ns, s0);
             JoinArgs ja = base_args(o, nullptr);
             ja.q0 = (uint32_t)q0;
             ja.q1 = (uint32_t)q1;
             ja.step = (uint32_t)sm.step;
             ja.nsamples = (uint32_t)sm.ns;
-            ja.qcount = qcount.p;
-            Ev a, b;
-            SJ_CUDA(cudaEventRecord(a.e, s0));
+            ja.qcount = dqcount;
+            SJ_CUDA(cudaEventRecord(cx.events[0], s0));
             launch_refine<kCountQuery>(ix, ja, o.unicomp != 0, (uint32_t)sm.ns, s0);
-            SJ_CUDA(cudaEventRecord(b.e, s0));
-            SJ_CUDA(cudaMemcpyAsync(hcnt.data(), qcount.p, sm.ns * sizeof(uint32_t), cudaMemcpyDeviceToHost, s0));
+            SJ_CUDA(cudaEventRecord(cx.events[1], s0));
+            SJ_CUDA(cudaMemcpyAsync(hqcount, dqcount, sm.ns * sizeof(uint32_t), cudaMemcpyDeviceToHost, s0));
             SJ_CUDA(cudaStreamSynchronize(s0));
-            SJ_CUDA(cudaEventElapsedTime(&est_ms, a.e, b.e));
+            SJ_CUDA(cudaEventElapsedTime(&est_ms, cx.events[0], cx.events[1]));
         }
         stats.estimate_ms = est_ms;
 
-        // ---- plan
+        // ---- plan (k >= min_batches contiguous A-order ranges)
         std::vector<uint64_t> cuts, est;
         uint64_t est_total = 0;
-        plan_batches(hcnt.data(), sm.ns, sm.step, q0, q1, o.batch_capacity_pairs, o.min_batches, 0.25, cuts, est,
+        plan_batches(hqcount, sm.ns, sm.step, q0, q1, o.batch_capacity_pairs, o.min_batches, 0.25, cuts, est,
                      &est_total);
         stats.estimated_pairs = est_total;
         const size_t nb = cuts.size() - 1;
 
-        // per-batch cursor/overflow slots, pinned host mirror of the cursors
-        struct Slot { unsigned long long cursor; uint32_t overflow; uint32_t pad; };
         float refine_ms = 0, refine_max = 0;
         uint32_t launches = 0;
-
         auto run_batch = [&](uint64_t a, uint64_t b, uint64_t *buf, uint64_t cap, Slot *dslot, cudaStream_t s,
                              cudaEvent_t e0, cudaEvent_t e1) {
             SJ_CUDA(cudaMemsetAsync(dslot, 0, sizeof(Slot), s));
-            JoinArgs ja = base_args(o, work.p);
+            JoinArgs ja = base_args(o, work);
             ja.out = buf;
             ja.cap = cap;
             ja.cursor = &dslot->cursor;
@@ -243,45 +229,51 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         };
 
         if (!o.result_on_host) {
-            // ---- device-resident batches: every batch owns its buffer; all run concurrently
-            Scratch<Slot> slots(nb, s0);
-            SJ_CUDA(cudaStreamSynchronize(s0));
-            Slot *hslots = static_cast<Slot *>(host_pinned_alloc(sizeof(Slot) * nb, nullptr));
-            std::vector<Ev> e0(nb), e1(nb);
+            // ---- device-resident batches: every batch owns its buffer; streams run them
+            //      concurrently, S at a time (slot i % S of each stream is reused in order)
             res->batches.resize(nb);
+            std::vector<uint64_t> counts(nb, 0);
+            auto drain_stream_slot = [&](size_t b) {   // host: read batch b's cursor (already synced)
+                counts[b] = hslots[b % S].cursor;
+                add_time(cx.events[2 + 2 * (b % S)], cx.events[3 + 2 * (b % S)]);
+            };
             for (size_t b = 0; b < nb; ++b) {
-                cudaStream_t s = st.s[b % S];
+                const int si = (int)(b % S);
+                cudaStream_t s = cx.streams[si];
+                if (b >= (size_t)S) {   // stream si's previous batch must have published its cursor
+                    SJ_CUDA(cudaStreamSynchronize(s));
+                    drain_stream_slot(b - S);
+                }
                 const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(
                     o.batch_capacity_pairs, est[b] + est[b] / 4 + 65536));
                 sj_batch &bt = res->batches[b];
                 bt.pairs = dalloc<uint64_t>(cap, s);
                 bt.cap = cap;
                 bt.on_device = 1;
-                run_batch(cuts[b], cuts[b + 1], bt.pairs, cap, slots.p + b, s, e0[b].e, e1[b].e);
-                SJ_CUDA(cudaMemcpyAsync(hslots + b, slots.p + b, sizeof(Slot), cudaMemcpyDeviceToHost, s));
+                run_batch(cuts[b], cuts[b + 1], bt.pairs, cap, dslots + si, s, cx.events[2 + 2 * si],
+                          cx.events[3 + 2 * si]);
+                SJ_CUDA(cudaMemcpyAsync(hslots + si, dslots + si, sizeof(Slot), cudaMemcpyDeviceToHost, s));
             }
-            for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(st.s[i]));
+            for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
+            for (size_t b = (nb > (size_t)S ? nb - S : 0); b < nb; ++b) drain_stream_slot(b);
             for (size_t b = 0; b < nb; ++b) {
-                add_time(e0[b].e, e1[b].e);
                 sj_batch &bt = res->batches[b];
-                uint64_t n = hslots[b].cursor;
+                uint64_t n = counts[b];
                 if (n > bt.cap) {  // overflow: exact re-allocation and re-run
-                    cudaStream_t s = st.s[0];
-                    dev_free(bt.pairs, s);
-                    bt.pairs = dalloc<uint64_t>(n, s);
+                    dev_free(bt.pairs, s0);
+                    bt.pairs = dalloc<uint64_t>(n, s0);
                     bt.cap = n;
-                    run_batch(cuts[b], cuts[b + 1], bt.pairs, n, slots.p + b, s, e0[b].e, e1[b].e);
-                    SJ_CUDA(cudaMemcpyAsync(hslots + b, slots.p + b, sizeof(Slot), cudaMemcpyDeviceToHost, s));
-                    SJ_CUDA(cudaStreamSynchronize(s));
-                    add_time(e0[b].e, e1[b].e);
+                    run_batch(cuts[b], cuts[b + 1], bt.pairs, n, dslots, s0, cx.events[2], cx.events[3]);
+                    SJ_CUDA(cudaMemcpyAsync(hslots, dslots, sizeof(Slot), cudaMemcpyDeviceToHost, s0));
+                    SJ_CUDA(cudaStreamSynchronize(s0));
+                    add_time(cx.events[2], cx.events[3]);
                     ++stats.retries;
-                    n = hslots[b].cursor;
-                    if (n > bt.cap) { host_pinned_free(hslots); fail(SJ_ERR_CUDA, "batch re-run overflowed"); }
+                    n = hslots[0].cursor;
+                    if (n > bt.cap) fail(SJ_ERR_CUDA, "batch re-run overflowed");
                 }
                 bt.n = n;
                 res->total += n;
             }
-            host_pinned_free(hslots);
         } else {
             // ---- host-drained batches: S device staging buffers; batch b+S on a stream runs after
             //      the D2H of batch b (stream order), while other streams compute.
@@ -289,12 +281,12 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             for (auto e : est) maxest = std::max(maxest, e);
             const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(o.batch_capacity_pairs,
                                                                           maxest + maxest / 4 + 65536));
-            std::vector<uint64_t *> staging(S);
-            for (int i = 0; i < S; ++i) staging[i] = dalloc<uint64_t>(cap, st.s[i]);
-            Scratch<Slot> slots(S, s0);
-            SJ_CUDA(cudaStreamSynchronize(s0));
-            Slot *hslots = static_cast<Slot *>(host_pinned_alloc(sizeof(Slot) * S, nullptr));
-            std::vector<Ev> e0(S), e1(S), edone(S);
+            std::vector<uint64_t *> staging(S, nullptr);
+            struct StagingGuard {
+                std::vector<uint64_t *> &v; DevCtx &cx;
+                ~StagingGuard() { for (size_t i = 0; i < v.size(); ++i) if (v[i]) dev_free(v[i], cx.streams[i]); }
+            } sg{staging, cx};
+            for (int i = 0; i < S; ++i) staging[i] = dalloc<uint64_t>(cap, cx.streams[i]);
             std::deque<std::pair<uint64_t, uint64_t>> pending;
             for (size_t b = 0; b < nb; ++b) pending.emplace_back(cuts[b], cuts[b + 1]);
             std::vector<std::pair<uint64_t, uint64_t>> inflight(S, {0, 0});
@@ -303,66 +295,61 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 auto r = pending.front();
                 pending.pop_front();
                 inflight[i] = r;
-                run_batch(r.first, r.second, staging[i], cap, slots.p + i, st.s[i], e0[i].e, e1[i].e);
-                SJ_CUDA(cudaMemcpyAsync(hslots + i, slots.p + i, sizeof(Slot), cudaMemcpyDeviceToHost, st.s[i]));
-                SJ_CUDA(cudaEventRecord(edone[i].e, st.s[i]));
+                run_batch(r.first, r.second, staging[i], cap, dslots + i, cx.streams[i], cx.events[2 + 2 * i],
+                          cx.events[3 + 2 * i]);
+                SJ_CUDA(cudaMemcpyAsync(hslots + i, dslots + i, sizeof(Slot), cudaMemcpyDeviceToHost,
+                                        cx.streams[i]));
                 order.push_back(i);
             };
             for (int i = 0; i < S && !pending.empty(); ++i) launch_on(i);
-            try {
-                while (!order.empty()) {
-                    const int i = order.front();
-                    order.pop_front();
-                    SJ_CUDA(cudaEventSynchronize(edone[i].e));
-                    add_time(e0[i].e, e1[i].e);
-                    const uint64_t n = hslots[i].cursor;
-                    const auto r = inflight[i];
-                    if (n > cap) {
-                        // overflow: split the query range and re-run both halves first
-                        ++stats.retries;
-                        if (r.second - r.first < 2) fail(SJ_ERR_NOMEM, "a single query exceeds the batch capacity");
-                        const uint64_t mid = r.first + (r.second - r.first) / 2;
-                        pending.emplace_front(mid, r.second);
-                        pending.emplace_front(r.first, mid);
-                    } else {
-                        sj_batch bt;
-                        bt.on_device = 0;
-                        bt.n = n;
-                        bt.cap = n;
-                        if (n) {
-                            bt.pairs = static_cast<uint64_t *>(host_pinned_alloc(n * sizeof(uint64_t), nullptr));
-                            SJ_CUDA(cudaMemcpyAsync(bt.pairs, staging[i], n * sizeof(uint64_t),
-                                                    cudaMemcpyDeviceToHost, st.s[i]));
-                        }
-                        res->batches.push_back(bt);
-                        res->total += n;
+            while (!order.empty()) {
+                const int i = order.front();
+                order.pop_front();
+                // the cursor copy follows the kernel on stream i; the previous D2H on this stream
+                // precedes the kernel, so a stream sync here waits for exactly that batch.
+                SJ_CUDA(cudaEventSynchronize(cx.events[3 + 2 * i]));
+                SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
+                add_time(cx.events[2 + 2 * i], cx.events[3 + 2 * i]);
+                const uint64_t n = hslots[i].cursor;
+                const auto r = inflight[i];
+                if (n > cap) {
+                    // overflow: split the query range and re-run both halves first
+                    ++stats.retries;
+                    if (r.second - r.first < 2) fail(SJ_ERR_NOMEM, "a single query exceeds the batch capacity");
+                    const uint64_t mid = r.first + (r.second - r.first) / 2;
+                    pending.emplace_front(mid, r.second);
+                    pending.emplace_front(r.first, mid);
+                } else {
+                    sj_batch bt;
+                    bt.on_device = 0;
+                    bt.n = n;
+                    bt.cap = n;
+                    if (n) {
+                        bt.pairs = static_cast<uint64_t *>(host_pinned_alloc(n * sizeof(uint64_t), nullptr));
+                        SJ_CUDA(cudaMemcpyAsync(bt.pairs, staging[i], n * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                                cx.streams[i]));
                     }
-                    if (!pending.empty()) launch_on(i);
+                    res->batches.push_back(bt);
+                    res->total += n;
                 }
-            } catch (...) {
-                for (int i = 0; i < S; ++i) cudaStreamSynchronize(st.s[i]);
-                host_pinned_free(hslots);
-                for (int i = 0; i < S; ++i) dev_free(staging[i], st.s[i]);
-                throw;
+                if (!pending.empty()) launch_on(i);
             }
-            for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(st.s[i]));
-            host_pinned_free(hslots);
-            for (int i = 0; i < S; ++i) dev_free(staging[i], st.s[i]);
+            for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
         }
+        (void)slot_cap;
 
         // ---- work counters
-        unsigned long long hw[4] = {0, 0, 0, 0};
-        SJ_CUDA(cudaMemcpy(hw, work.p, sizeof(hw), cudaMemcpyDeviceToHost));
-        stats.cells_probed = hw[0];
-        stats.candidates_tested = hw[1];
+        SJ_CUDA(cudaMemcpyAsync(hwork, work, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0));
+        SJ_CUDA(cudaStreamSynchronize(s0));
+        stats.cells_probed = hwork[0];
+        stats.candidates_tested = hwork[1];
         stats.pairs = res->total;
         stats.batches = (uint32_t)res->batches.size();
         stats.refine_ms = refine_ms;
         stats.refine_max_ms = refine_max;
         stats.refine_launches = launches;
-        for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(st.s[i]));
     } catch (...) {
-        for (int i = 0; i < S; ++i) cudaStreamSynchronize(st.s[i]);
+        for (auto s : cx.streams) cudaStreamSynchronize(s);
         for (auto &b : res->batches) {
             if (!b.pairs) continue;
             if (b.on_device) dev_free(b.pairs, nullptr);
@@ -380,10 +367,12 @@ void neighbor_counts_impl(const sj_index *idx, const sj_join_opts &o, uint32_t *
     uint64_t q0, q1;
     validate(idx, o, &q0, &q1);
     SJ_CUDA(cudaSetDevice(idx->device));
-    Streams st(1);
-    cudaStream_t s = st.s[0];
-    Scratch<unsigned long long> work(4, s);
-    SJ_CUDA(cudaMemsetAsync(work.p, 0, 4 * sizeof(unsigned long long), s));
+    CtxGuard cg{acquire_ctx(idx->device, 1, 2, 64)};
+    DevCtx &cx = *cg.c;
+    cudaStream_t s = cx.streams[0];
+    unsigned long long *work = static_cast<unsigned long long *>(cx.d_slots);
+    unsigned long long *hwork = static_cast<unsigned long long *>(cx.h_slots);
+    SJ_CUDA(cudaMemsetAsync(work, 0, 4 * sizeof(unsigned long long), s));
     Scratch<uint32_t> own_cnt;
     uint32_t *c = cnt;
     if (!c) {
@@ -392,15 +381,14 @@ void neighbor_counts_impl(const sj_index *idx, const sj_join_opts &o, uint32_t *
         c = own_cnt.p;
     }
     SJ_CUDA(cudaMemsetAsync(c, 0, sizeof(uint32_t) * idx->view.n, s));
-    JoinArgs ja = base_args(o, work.p);
+    JoinArgs ja = base_args(o, work);
     ja.pcount = c;
     ja.q0 = (uint32_t)q0;
     ja.q1 = (uint32_t)q1;
     launch_refine<kCountPoint>(idx->dev, ja, o.unicomp != 0, (uint32_t)(q1 - q0), s);
-    unsigned long long hw[4];
-    SJ_CUDA(cudaMemcpyAsync(hw, work.p, sizeof(hw), cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaMemcpyAsync(hwork, work, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     SJ_CUDA(cudaStreamSynchronize(s));
-    if (total) *total = hw[2];
+    if (total) *total = hwork[2];
 }
 
 }  // namespace sj

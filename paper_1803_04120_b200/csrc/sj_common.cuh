@@ -75,7 +75,25 @@ struct DevIndex {
     const double *X;
     const uint8_t *masks;        // nullptr when masks were not built
     uint64_t mask_off[SJ_MAX_DIM + 1];
+    // prefix directory over the top dir_k (slowest) dimensions:
+    // dir[p] = first cell whose top-k coordinate prefix is >= p, p in [0, dir_P]; the cells of
+    // prefix p are B[dir[p], dir[p+1]).  dir_k == d makes it a dense table of all cells.
+    const uint32_t *dir;
+    int dir_k;
+    uint64_t dir_P;              // number of prefixes (entries = dir_P + 1)
+    uint64_t dir_div;            // stride of dimension d - dir_k (key / dir_div = prefix)
+    uint64_t pstride[SJ_MAX_DIM];// prefix strides: stride_j / dir_div for j >= d-k, else 0
+    // search mode of the refine (uniform per index, chosen at directory build):
+    //   kSearchDenseRows : dir_k == d, a row of 3 cells is [dir[p-1], dir[p+2])
+    //   kSearchCellScan  : prefix ranges hold a few cells: scan them, test the low coordinates
+    //   kSearchRows      : prefix ranges are large: bounded binary search per row of 3 cells
+    int search_mode;
+    uint32_t dir_ntop;           // 3^dir_k top-prefix offsets
+    double inv_cpd[SJ_MAX_DIM];  // 1/|g_j| (fast exact divmod of low key parts, see refine.cuh)
+    int64_t lowR[SJ_MAX_DIM + 1];// lowR[i] = sum_{m<i} stride_m: largest |key offset| of dims < i
 };
+
+enum SearchMode { kSearchDenseRows = 0, kSearchCellScan = 1, kSearchRows = 2 };
 
 }  // namespace sj
 
@@ -103,7 +121,29 @@ struct sj_result {
 };
 
 namespace sj {
+// context.cu -- reusable per-device streams / events / slot buffers
+struct DevCtx {
+    int dev = 0;
+    std::vector<cudaStream_t> streams;
+    std::vector<cudaEvent_t> events;
+    void *d_slots = nullptr;     // device scratch for cursors / counters
+    void *h_slots = nullptr;     // pinned mirror
+    size_t slot_bytes = 0;
+};
+DevCtx *acquire_ctx(int dev, int nstreams, int nevents, size_t slot_bytes);
+void release_ctx(DevCtx *c);
+struct CtxGuard {
+    DevCtx *c;
+    ~CtxGuard()
+    {
+        if (!c) return;
+        for (auto s : c->streams) cudaStreamSynchronize(s);
+        release_ctx(c);
+    }
+};
+
 // index_build.cu
+void build_directory(sj_index *idx, cudaStream_t s);
 sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &o);
 sj_index *import_index_impl(const sj_index_view &v, int device);
 void free_index_impl(sj_index *idx);

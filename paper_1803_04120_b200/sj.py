@@ -53,6 +53,7 @@ class IndexView(ctypes.Structure):
                 ("mins", dbl * SJ_MAX_DIM), ("cpd", u64 * SJ_MAX_DIM), ("strides", u64 * SJ_MAX_DIM),
                 ("key_bits", i32), ("mask_offsets", u64 * (SJ_MAX_DIM + 1)),
                 ("B", vp), ("G", vp), ("A", vp), ("pcell", vp), ("X", vp), ("masks", vp),
+                ("dir_k", i32), ("dir_entries", u64), ("dir", vp),
                 ("t_h2d_ms", f32), ("t_geometry_ms", f32), ("t_keys_ms", f32), ("t_sort_ms", f32),
                 ("t_compact_ms", f32), ("t_total_ms", f32)]
 
@@ -172,7 +173,8 @@ class Index:
         d = v.d
         return dict(d=d, n=v.n, n_cells=v.n_cells, eps=v.eps, eps2=v.eps2, w=v.w,
                     mins=list(v.mins[:d]), cpd=list(v.cpd[:d]), strides=list(v.strides[:d]),
-                    key_bits=v.key_bits, mask_offsets=list(v.mask_offsets[:d + 1]))
+                    key_bits=v.key_bits, mask_offsets=list(v.mask_offsets[:d + 1]),
+                    dir_k=v.dir_k, dir_entries=v.dir_entries)
 
     def timings(self) -> dict:
         v = self.view
@@ -193,6 +195,8 @@ class Index:
         }
         if v.masks:
             out["masks"] = _device_tensor(v.masks, (int(v.mask_offsets[d]),), torch.uint8, self.device, self)
+        if v.dir:
+            out["dir"] = _device_tensor(v.dir, (int(v.dir_entries),), torch.uint32, self.device, self)
         return out
 
     def free(self):

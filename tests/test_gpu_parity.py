@@ -281,3 +281,48 @@ def test_c3_eps8_sampled_rows(sj):
     """C3 (Syn-6D 2M, eps=8): sampled rows exact."""
     pts = datagen.uniform_config("C3", 6)
     _sampled_rows_check(sj, pts, 8.0, nsample=32, seed=8)
+
+
+def _gapped(n, d, seed):
+    """Points in separated slabs: whole coordinate columns of the grid are empty, so the
+    masks M_j actually remove adjacent coordinates."""
+    rng = np.random.default_rng(seed)
+    P = rng.uniform(0, 10, (n, d))
+    P[:, 0] = np.where(rng.random(n) < 0.5, P[:, 0], P[:, 0] + 3.0)   # shifted half
+    P[:, 1] = np.floor(P[:, 1] * 2.0) / 2.0 * 1.5                     # quantised rows
+    return P
+
+
+@pytest.mark.parametrize("d", [2, 3, 5, 6])
+def test_masks_option_invariance(sj, d):
+    pts = _gapped(4000, d, seed=d)
+    eps = 0.6
+    want = oracle.brute_force(pts, eps)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    for use_masks in (True, False):
+        for unicomp in (True, False):
+            got = sj.self_join(idx, use_masks=use_masks, unicomp=unicomp).to_numpy()
+            assert np.array_equal(got, want), (use_masks, unicomp)
+
+
+@pytest.mark.parametrize("d,n,eps", [(2, 5000, 1.5), (3, 8000, 4.0), (4, 20000, 6.0), (6, 30000, 20.0),
+                                     (6, 3000, 0.5), (2, 50, 1e-3)])
+def test_prefix_directory_definition(sj, d, n, eps):
+    """dir[p] = lower_bound(B, p * stride_{d-k}) for every prefix p (index_build.cu)."""
+    pts = datagen.uniform(n, d, seed=n + d)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    g = idx.geometry()
+    arr = idx.arrays()
+    B = arr["B"].cpu().numpy().astype(object)
+    k = g["dir_k"]
+    div = 1
+    for j in range(d - k):
+        div *= g["cpd"][j]
+    P = 1
+    for j in range(d - k, d):
+        P *= g["cpd"][j]
+    assert g["dir_entries"] == P + 1
+    Bn = np.array([int(b) // div for b in B], dtype=np.int64)
+    want = np.searchsorted(Bn, np.arange(P + 1), side="left")
+    assert np.array_equal(arr["dir"].cpu().numpy().astype(np.int64), want)
+    assert np.array_equal(sj.self_join(idx).to_numpy(), oracle.brute_force(pts, eps)) if n <= 8000 else True
