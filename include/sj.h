@@ -106,14 +106,15 @@ typedef struct {
     uint64_t cpd[SJ_MAX_DIM];    /* |g_j| = cells per dimension incl. one pad cell each side (R7) */
     uint64_t strides[SJ_MAX_DIM];/* linearisation strides, dimension 1 fastest (R8)               */
     int key_bits;                /* ceil(log2(prod |g_j|)): bits sorted by the radix sort          */
-    uint64_t mask_offsets[SJ_MAX_DIM + 1]; /* byte offsets of M_j inside `masks`; [d] = total      */
+    uint64_t mask_offsets[SJ_MAX_DIM + 1]; /* bit offsets of M_j inside `masks`; [d] = total bits   */
     /* device pointers (owned by the index; valid while it lives):                                 */
     const uint64_t *B;           /* [n_cells] sorted linear ids of the non-empty cells             */
     const uint32_t *G;           /* [n_cells+1] cell h holds A-positions [G[h], G[h+1])            */
     const uint32_t *A;           /* [n] original point id at each A-position                       */
     const uint32_t *pcell;       /* [n] cell h of each A-position                                  */
     const double *X;             /* [d][n] SoA coordinates in A-order: X[j*n+k] = D[A[k]][j]      */
-    const uint8_t *masks;        /* concatenated M_j byte maps (1 = coordinate occupied) or NULL   */
+    const uint32_t *masks;       /* bitmap of the M_j: bit mask_offsets[j]+c set iff coordinate c of
+                                    dimension j is occupied (little-endian words), or NULL          */
     int dir_k;                   /* prefix directory over the dir_k slowest dimensions (bounds every
                                     binary search of B; rebuilt from B on import)                  */
     uint64_t dir_entries;        /* entries of dir (= number of prefixes + 1)                     */

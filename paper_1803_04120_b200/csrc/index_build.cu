@@ -86,27 +86,44 @@ __global__ void k_minmax_init(unsigned long long *mm, int d, uint32_t *nonfinite
 
 // Cell coordinate c_j = 1 + floor(fl(fl(x_j - min_j) / w))  (reading R7), linear id with
 // dimension 1 fastest (R8): key = sum_j c_j * stride_j (exact: < prod |g_j| < 2^64).
+// Masks M_j as one bitmap over all dimensions (bit mask_off[j] + c): when it is
+// small (<= kSmemMaskWords words) each CTA ORs into a shared copy and flushes only the non-zero
+// words, so the few hot words are not hammered by every point; otherwise global atomicOr.
+constexpr int kSmemMaskWords = 2048;   // 64 K bits, 8 KB of shared memory
 template <int D>
 __global__ void __launch_bounds__(kThreads)
 k_keys(const double *__restrict__ pts, uint32_t n, DevIndex ix, uint64_t *__restrict__ keys,
-       uint32_t *__restrict__ ids, uint8_t *__restrict__ masks)
+       uint32_t *__restrict__ ids, uint32_t *__restrict__ masks, uint32_t mask_words)
 {
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    uint64_t key = 0;
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        const double x = pts[i * D + j];
-        const double t = floor(__ddiv_rn(__dsub_rn(x, ix.mins[j]), ix.w));
-        const uint64_t c = 1ull + (uint64_t)t;
-        key += c * ix.strides[j];
-        if (masks) {                                 // read-before-write: no same-address storm
-            uint8_t *m = masks + ix.mask_off[j] + c;
-            if (!*m) *m = 1;                         // benign same-value race
-        }
+    extern __shared__ uint32_t s_mask[];
+    const bool smem_masks = masks && mask_words <= (uint32_t)kSmemMaskWords;
+    if (smem_masks) {
+        for (uint32_t w = threadIdx.x; w < mask_words; w += blockDim.x) s_mask[w] = 0;
+        __syncthreads();
     }
-    keys[i] = key;
-    ids[i] = (uint32_t)i;
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        uint64_t key = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const double x = pts[i * D + j];
+            const double t = floor(__ddiv_rn(__dsub_rn(x, ix.mins[j]), ix.w));
+            const uint64_t c = 1ull + (uint64_t)t;
+            key += c * ix.strides[j];
+            if (masks) {
+                const uint64_t bit = ix.mask_off[j] + c;
+                if (smem_masks) atomicOr(s_mask + (bit >> 5), 1u << (bit & 31));
+                else atomicOr(masks + (bit >> 5), 1u << (bit & 31));
+            }
+        }
+        keys[i] = key;
+        ids[i] = (uint32_t)i;
+    }
+    if (smem_masks) {
+        __syncthreads();
+        for (uint32_t w = threadIdx.x; w < mask_words; w += blockDim.x)
+            if (s_mask[w]) atomicOr(masks + w, s_mask[w]);
+    }
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -142,17 +159,20 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
 
 template <int D>
 void launch_dim(int which, dim3 g, dim3 b, cudaStream_t s, const double *pts, uint32_t n, DevIndex &ix,
-                uint64_t *keys, uint32_t *ids, uint8_t *masks, double *part, uint32_t *nonfinite,
+                uint64_t *keys, uint32_t *ids, uint32_t *masks, double *part, uint32_t *nonfinite,
                 const uint32_t *A, uint32_t *pcell, uint64_t *B, uint32_t *G, double *X)
 {
+    const uint32_t mask_words = (uint32_t)((ix.mask_off[ix.d] + 31) / 32);
     if (which == 0) k_minmax<D><<<g, b, 0, s>>>(pts, n, reinterpret_cast<unsigned long long *>(part), nonfinite);
-    else if (which == 1) k_keys<D><<<g, b, 0, s>>>(pts, n, ix, keys, ids, masks);
+    else if (which == 1)
+        k_keys<D><<<g, b, (masks && mask_words <= (uint32_t)kSmemMaskWords) ? 4 * mask_words : 0, s>>>(
+            pts, n, ix, keys, ids, masks, mask_words);
     else k_compact_gather<D><<<g, b, 0, s>>>(keys, A, pts, n, pcell, B, G, X);
     SJ_LAUNCHED();
 }
 
 void launch(int d, int which, dim3 g, dim3 b, cudaStream_t s, const double *pts, uint32_t n, DevIndex &ix,
-            uint64_t *keys, uint32_t *ids, uint8_t *masks, double *part, uint32_t *nonfinite,
+            uint64_t *keys, uint32_t *ids, uint32_t *masks, double *part, uint32_t *nonfinite,
             const uint32_t *A, uint32_t *pcell, uint64_t *B, uint32_t *G, double *X)
 {
     switch (d) {
@@ -295,13 +315,13 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
         ix.cpd[j] = v.cpd[j];
         ix.strides[j] = v.strides[j];
     }
-    // masks: byte maps of |g_j| bytes each, only when small (they never change S)
+    // masks: one bitmap, |g_j| bits per dimension, only when <= 2^30 bits (they never change S)
     uint64_t mask_total = 0;
     bool want_masks = o.build_masks != 0;
     for (int j = 0; j < d; ++j) {
         v.mask_offsets[j] = mask_total;
         mask_total += v.cpd[j];
-        if (mask_total > (1ull << 26)) want_masks = false;
+        if (mask_total > (1ull << 30)) want_masks = false;
     }
     v.mask_offsets[d] = mask_total;
     for (int j = 0; j <= d; ++j) ix.mask_off[j] = v.mask_offsets[j];
@@ -311,10 +331,11 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
     idx->device = o.device;
     auto own = [&](void *p) { idx->bufs[idx->nbufs++] = p; return p; };
     try {
-        uint8_t *masks = nullptr;
+        uint32_t *masks = nullptr;
+        const size_t mask_bytes = 4 * ((mask_total + 31) / 32);
         if (want_masks) {
-            masks = static_cast<uint8_t *>(own(dev_alloc(mask_total, s)));
-            SJ_CUDA(cudaMemsetAsync(masks, 0, mask_total, s));
+            masks = static_cast<uint32_t *>(own(dev_alloc(mask_bytes, s)));
+            SJ_CUDA(cudaMemsetAsync(masks, 0, mask_bytes, s));
         }
         Scratch<uint64_t> keys(n, s), keys_tmp(n, s);
         uint32_t *A = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
@@ -480,15 +501,16 @@ sj_index *import_index_impl(const sj_index_view &src, int device)
         uint32_t *A = static_cast<uint32_t *>(own(4 * n));
         uint32_t *pcell = static_cast<uint32_t *>(own(4 * n));
         double *X = static_cast<double *>(own(8 * n * d));
-        uint8_t *masks = nullptr;
+        uint32_t *masks = nullptr;
         SJ_CUDA(cudaMemcpyAsync(B, src.B, 8 * nG, cudaMemcpyDefault, s));
         SJ_CUDA(cudaMemcpyAsync(G, src.G, 4 * (nG + 1), cudaMemcpyDefault, s));
         SJ_CUDA(cudaMemcpyAsync(A, src.A, 4 * n, cudaMemcpyDefault, s));
         SJ_CUDA(cudaMemcpyAsync(pcell, src.pcell, 4 * n, cudaMemcpyDefault, s));
         SJ_CUDA(cudaMemcpyAsync(X, src.X, 8 * n * d, cudaMemcpyDefault, s));
         if (src.masks && src.mask_offsets[d] > 0) {
-            masks = static_cast<uint8_t *>(own(src.mask_offsets[d]));
-            SJ_CUDA(cudaMemcpyAsync(masks, src.masks, src.mask_offsets[d], cudaMemcpyDefault, s));
+            const size_t mb = 4 * ((src.mask_offsets[d] + 31) / 32);
+            masks = static_cast<uint32_t *>(own(mb));
+            SJ_CUDA(cudaMemcpyAsync(masks, src.masks, mb, cudaMemcpyDefault, s));
         }
         SJ_CUDA(cudaStreamSynchronize(s));
         v.B = B; v.G = G; v.A = A; v.pcell = pcell; v.X = X; v.masks = masks;

@@ -230,8 +230,10 @@ __device__ __forceinline__ void adjacent_masks(const DevIndex &ix, const JoinArg
     for (int i = 0; i < D; ++i) {
         allow[i] = 7u;
         if (masked) {
-            const uint8_t *m = ix.masks + ix.mask_off[i];
-            allow[i] = 2u | (__ldg(m + q.c[i] - 1ull) ? 1u : 0u) | (__ldg(m + q.c[i] + 1ull) ? 4u : 0u);
+            const uint64_t lo = ix.mask_off[i] + q.c[i] - 1ull, hi = lo + 2ull;
+            const uint32_t blo = (__ldg(ix.masks + (lo >> 5)) >> (lo & 31)) & 1u;
+            const uint32_t bhi = (__ldg(ix.masks + (hi >> 5)) >> (hi & 31)) & 1u;
+            allow[i] = 2u | blo | (bhi << 2);
         }
     }
 }

@@ -58,7 +58,7 @@ struct Scratch {
 //   A[N]    uint32  original point id per A-position            (|A| = |D|)
 //   pcell[N] uint32 cell of each A-position
 //   X[d][N] double  SoA coordinates in A-order
-//   masks   uint8   M_j byte maps, concatenated (mask_off[j] .. mask_off[j+1])
+//   masks   uint32  M_j bitmaps, concatenated (bits mask_off[j] .. mask_off[j+1])
 struct DevIndex {
     int d;
     uint32_t n;
@@ -73,7 +73,7 @@ struct DevIndex {
     const uint32_t *A;
     const uint32_t *pcell;
     const double *X;
-    const uint8_t *masks;        // nullptr when masks were not built
+    const uint32_t *masks;       // bitmap, bit mask_off[j] + c = M_j contains c; nullptr if not built
     uint64_t mask_off[SJ_MAX_DIM + 1];
     // prefix directory over the top dir_k (slowest) dimensions:
     // dir[p] = first cell whose top-k coordinate prefix is >= p, p in [0, dir_P]; the cells of

@@ -19,7 +19,7 @@ from typing import Dict, Optional, Sequence, Tuple
 import numpy as np
 
 SJ_MAX_DIM = 6
-# meta layout (int64 words): n, d, n_cells, key_bits, mask_bytes, device-independent geometry
+# meta layout (int64 words): n, d, n_cells, key_bits, mask_bits, device-independent geometry
 _META_WORDS = 5 + 3 + SJ_MAX_DIM * 3 + (SJ_MAX_DIM + 1)
 
 
@@ -31,11 +31,11 @@ def _i2f(x: int) -> float:
     return struct.unpack("<d", struct.pack("<q", int(x)))[0]
 
 
-def pack_meta(geom: dict, n: int, n_cells: int, mask_bytes: int) -> np.ndarray:
+def pack_meta(geom: dict, n: int, n_cells: int, mask_bits: int) -> np.ndarray:
     """Geometry of an index as int64 words (float64 fields bit-cast, so transfer is exact)."""
     d = int(geom["d"])
     m = np.zeros(_META_WORDS, dtype=np.int64)
-    m[0:5] = [n, d, n_cells, geom["key_bits"], mask_bytes]
+    m[0:5] = [n, d, n_cells, geom["key_bits"], mask_bits]
     m[5:8] = [_f2i(geom["eps"]), _f2i(geom["eps2"]), _f2i(geom["w"])]
     o = 8
     for j in range(d):
@@ -50,7 +50,7 @@ def pack_meta(geom: dict, n: int, n_cells: int, mask_bytes: int) -> np.ndarray:
 
 def unpack_meta(m: np.ndarray) -> Tuple[dict, int, int, int]:
     m = np.asarray(m, dtype=np.int64)
-    n, d, n_cells, key_bits, mask_bytes = (int(v) for v in m[0:5])
+    n, d, n_cells, key_bits, mask_bits = (int(v) for v in m[0:5])
     geom = dict(d=d, key_bits=key_bits, eps=_i2f(m[5]), eps2=_i2f(m[6]), w=_i2f(m[7]))
     o = 8
     geom["mins"] = [_i2f(m[o + j]) for j in range(d)]
@@ -58,16 +58,16 @@ def unpack_meta(m: np.ndarray) -> Tuple[dict, int, int, int]:
     geom["strides"] = [int(np.int64(m[o + 2 * SJ_MAX_DIM + j]).astype(np.uint64)) for j in range(d)]
     o += 3 * SJ_MAX_DIM
     geom["mask_offsets"] = [int(m[o + j]) for j in range(d + 1)]
-    return geom, n, n_cells, mask_bytes
+    return geom, n, n_cells, mask_bits
 
 
 ARRAY_SPECS = ("B", "G", "A", "pcell", "X", "masks")
 
 
-def _shapes(n: int, d: int, n_cells: int, mask_bytes: int) -> Dict[str, Tuple[tuple, str]]:
+def _shapes(n: int, d: int, n_cells: int, mask_bits: int) -> Dict[str, Tuple[tuple, str]]:
     # torch has no unsigned 64/32-bit collectives: int64/int32 carry the same bits
     return {"B": ((n_cells,), "int64"), "G": ((n_cells + 1,), "int32"), "A": ((n,), "int32"),
-            "pcell": ((n,), "int32"), "X": ((d, n), "float64"), "masks": ((mask_bytes,), "uint8")}
+            "pcell": ((n,), "int32"), "X": ((d, n), "float64"), "masks": (((mask_bits + 31) // 32,), "int32")}
 
 
 def broadcast_index_arrays(arrays: Optional[Dict[str, "torch.Tensor"]], meta: Optional[np.ndarray],
@@ -85,10 +85,10 @@ def broadcast_index_arrays(arrays: Optional[Dict[str, "torch.Tensor"]], meta: Op
         mt.copy_(torch.from_numpy(np.asarray(meta, dtype=np.int64)))
     dist.broadcast(mt, src=src, group=group)
     meta = mt.cpu().numpy()
-    geom, n, n_cells, mask_bytes = unpack_meta(meta)
+    geom, n, n_cells, mask_bits = unpack_meta(meta)
     out = {}
-    for name, (shape, dt) in _shapes(n, geom["d"], n_cells, mask_bytes).items():
-        if name == "masks" and mask_bytes == 0:
+    for name, (shape, dt) in _shapes(n, geom["d"], n_cells, mask_bits).items():
+        if name == "masks" and mask_bits == 0:
             continue
         if rank == src:
             t = arrays[name]
@@ -106,9 +106,9 @@ def index_to_arrays(idx) -> Tuple[np.ndarray, Dict[str, "torch.Tensor"]]:
     import torch
     g = idx.geometry()
     arr = idx.arrays()
-    mask_bytes = int(g["mask_offsets"][-1]) if "masks" in arr else 0
-    meta = pack_meta(g, idx.n, idx.n_cells, mask_bytes)
-    conv = {"B": torch.int64, "G": torch.int32, "A": torch.int32, "pcell": torch.int32}
+    mask_bits = int(g["mask_offsets"][-1]) if "masks" in arr else 0
+    meta = pack_meta(g, idx.n, idx.n_cells, mask_bits)
+    conv = {"B": torch.int64, "G": torch.int32, "A": torch.int32, "pcell": torch.int32, "masks": torch.int32}
     out = {k: (v.view(conv[k]) if k in conv else v) for k, v in arr.items()}
     return meta, out
 
@@ -117,7 +117,7 @@ def arrays_to_index(meta: np.ndarray, arrays: Dict[str, "torch.Tensor"], device:
     """sj_index_import of broadcast arrays (copied into a library-owned index)."""
     import ctypes
     from . import sj
-    geom, n, n_cells, mask_bytes = unpack_meta(meta)
+    geom, n, n_cells, mask_bits = unpack_meta(meta)
     v = sj.IndexView()
     d = geom["d"]
     v.d, v.device, v.n, v.n_cells = d, device, n, n_cells
@@ -131,7 +131,7 @@ def arrays_to_index(meta: np.ndarray, arrays: Dict[str, "torch.Tensor"], device:
         v.mask_offsets[j] = geom["mask_offsets"][j]
     for name in ("B", "G", "A", "pcell", "X"):
         setattr(v, name, ctypes.c_void_p(arrays[name].data_ptr()))
-    v.masks = ctypes.c_void_p(arrays["masks"].data_ptr()) if mask_bytes and "masks" in arrays else None
+    v.masks = ctypes.c_void_p(arrays["masks"].data_ptr()) if mask_bits and "masks" in arrays else None
     return sj.import_index(v, device)
 
 

@@ -194,7 +194,8 @@ class Index:
             "X": _device_tensor(v.X, (d, n), torch.float64, self.device, self),
         }
         if v.masks:
-            out["masks"] = _device_tensor(v.masks, (int(v.mask_offsets[d]),), torch.uint8, self.device, self)
+            words = (int(v.mask_offsets[d]) + 31) // 32
+            out["masks"] = _device_tensor(v.masks, (words,), torch.uint32, self.device, self)
         if v.dir:
             out["dir"] = _device_tensor(v.dir, (int(v.dir_entries),), torch.uint32, self.device, self)
         return out

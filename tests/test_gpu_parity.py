@@ -193,10 +193,11 @@ def test_index_matches_oracle_index(sj, d):
         pc = arr["pcell"].cpu().numpy().astype(np.int64)
         assert np.array_equal(pc, np.repeat(np.arange(len(ref.B)), np.diff(ref.G)))
         if "masks" in arr:
-            m = arr["masks"].cpu().numpy()
+            words = arr["masks"].cpu().numpy().astype(np.uint64)
+            bits = ((words[:, None] >> np.arange(32, dtype=np.uint64)) & np.uint64(1)).reshape(-1)
             off = g["mask_offsets"]
             for j in range(d):
-                assert np.nonzero(m[off[j]:off[j + 1]])[0].tolist() == ref.M[j]
+                assert np.nonzero(bits[off[j]:off[j + 1]])[0].tolist() == ref.M[j]
 
 
 def test_fig2_fixture_on_gpu(sj):
