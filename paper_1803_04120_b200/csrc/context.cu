@@ -2,6 +2,9 @@
 // counter / cursor slots in device + pinned memory), so a build or a join does not create and
 // destroy CUDA objects on every call.  A context is owned by one call at a time (pool + mutex);
 // concurrent calls on one device simply get different contexts.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -71,6 +74,26 @@ void release_ctx(DevCtx *c)
     if (!c) return;
     std::lock_guard<std::mutex> lk(g_ctx_mu);
     g_ctx_free.push_back(c);
+}
+
+static double now_us()
+{
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+HostTrace::HostTrace(const char *w) : what(w)
+{
+    static const bool enabled = [] { const char *e = std::getenv("SJ_TRACE"); return e && *e && *e != '0'; }();
+    on = enabled;
+    t0 = last = on ? now_us() : 0.0;
+}
+
+void HostTrace::mark(const char *stage)
+{
+    if (!on) return;
+    const double t = now_us();
+    std::fprintf(stderr, "[sj-trace] %-10s %-28s +%8.1f us  (t=%8.1f us)\n", what, stage, t - last, t - t0);
+    last = t;
 }
 
 }  // namespace sj

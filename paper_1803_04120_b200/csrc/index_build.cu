@@ -13,7 +13,7 @@
 //   radix sort                      : stable LSD over key_bits (a3, radix_sort.cu)
 //   k_heads + inclusive scan        : cell index of every A-position (a4)
 //   k_compact_gather                : B, G starts, SoA coordinates X[j][k] = D[A[k]][j] (a4)
-//   k_dir_fill                      : prefix directory bounding every B search (a4)
+//   k_dir_hist + exclusive scan     : prefix directory bounding every B search (a4)
 #include <cmath>
 #include <cstring>
 
@@ -250,6 +250,7 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
     if (o.device < 0 || o.device >= ndev) fail(SJ_ERR_ARG, "bad device ordinal");
     SJ_CUDA(cudaSetDevice(o.device));
 
+    HostTrace tr("build");
     // the build runs on the caller's stream, or on a pooled library stream
     CtxGuard cg{o.stream ? nullptr : acquire_ctx(o.device, 1, 0, 64)};
     cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : cg.c->streams[0];
@@ -288,6 +289,7 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
     SJ_CUDA(cudaMemcpyAsync(&h_bad, nonfinite.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     SJ_CUDA(cudaStreamSynchronize(s));
     ev.rec(2, s);
+    tr.mark("minmax (synced)");
     if (h_bad) fail(SJ_ERR_NONFINITE, "a coordinate is NaN or infinite");
     double h_mm[2 * SJ_MAX_DIM];
     for (int t = 0; t < 2 * d; ++t) {
@@ -363,6 +365,7 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
         uint32_t nG = 0;
         SJ_CUDA(cudaMemcpyAsync(&nG, pcell + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         SJ_CUDA(cudaStreamSynchronize(s));
+        tr.mark("keys+sort+scan (synced)");
         uint64_t *B = static_cast<uint64_t *>(own(dev_alloc(sizeof(uint64_t) * nG, s)));
         uint32_t *G = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * ((size_t)nG + 1), s)));
         double *X = static_cast<double *>(own(dev_alloc(sizeof(double) * n * d, s)));
@@ -397,6 +400,7 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
         build_directory(idx, s);
         ev.rec(6, s);
         SJ_CUDA(cudaStreamSynchronize(s));
+        tr.mark("compact+dir (synced)");
         idx->view.t_compact_ms = ev.ms(4, 6);
         idx->view.t_total_ms = ev.ms(0, 6);
     } catch (...) {
@@ -408,18 +412,22 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
 }
 
 namespace {
-// Directory fill: cell h writes dir[q] = h for every prefix q in (prefix(h-1), prefix(h)];
-// the last cell also fills the tail with nG.  Total writes = P + 1.
+// floor(x / d) for quotients < 2^50: double estimate (|error| <= 1) + integer correction
+__device__ __forceinline__ uint64_t div_small_quot(uint64_t x, uint64_t d, double inv)
+{
+    uint64_t q = (uint64_t)((double)x * inv);
+    if (q * d > x) --q;
+    else if ((q + 1) * d <= x) ++q;
+    return q;
+}
+
+// dir[q] = #cells with prefix < q = exclusive prefix sum of the per-prefix cell histogram
 __global__ void __launch_bounds__(kThreads)
-k_dir_fill(const uint64_t *__restrict__ B, uint32_t nG, uint64_t div, uint64_t P, uint32_t *__restrict__ dir)
+k_dir_hist(const uint64_t *__restrict__ B, uint32_t nG, uint64_t div, double inv, uint32_t *__restrict__ hist)
 {
     const uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (h >= nG) return;
-    const uint64_t ph = B[h] / div;
-    const uint64_t start = (h == 0) ? 0 : B[h - 1] / div + 1;
-    for (uint64_t q = start; q <= ph; ++q) dir[q] = (uint32_t)h;
-    if (h == nG - 1)
-        for (uint64_t q = ph + 1; q <= P; ++q) dir[q] = nG;
+    atomicAdd(hist + div_small_quot(B[h], div, inv), 1u);
 }
 }  // namespace
 
@@ -446,8 +454,13 @@ void build_directory(sj_index *idx, cudaStream_t s)
     uint32_t *dir = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * ((size_t)P + 1), s));
     idx->bufs[idx->nbufs++] = dir;
     const uint32_t nG = (uint32_t)v.n_cells;
-    k_dir_fill<<<(nG + kThreads - 1) / kThreads, kThreads, 0, s>>>(v.B, nG, div, (uint64_t)P, dir);
-    SJ_LAUNCHED();
+    {
+        Scratch<uint32_t> hist((size_t)P + 1, s);
+        SJ_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(uint32_t) * ((size_t)P + 1), s));
+        k_dir_hist<<<(nG + kThreads - 1) / kThreads, kThreads, 0, s>>>(v.B, nG, div, 1.0 / (double)div, hist.p);
+        SJ_LAUNCHED();
+        exclusive_scan_u32(hist.p, dir, (uint64_t)P + 1, s);
+    }
     v.dir_k = k;
     v.dir_entries = (uint64_t)P + 1;
     v.dir = dir;

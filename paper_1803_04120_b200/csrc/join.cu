@@ -59,26 +59,32 @@ void validate(const sj_index *idx, const sj_join_opts &o, uint64_t *qb, uint64_t
 }  // namespace
 
 // ------------------------------------------------------------------ batch planner (host only)
-void plan_batches(const uint32_t *cnt, uint64_t ns, uint64_t step, uint64_t q0, uint64_t q1, uint64_t capacity,
-                  int min_batches, double margin, std::vector<uint64_t> &cuts, std::vector<uint64_t> &est,
-                  uint64_t *estimated_total)
+// Bucket i stands for queries [q0 + i*width, min(q1, q0 + (i+1)*width)) with estimated output
+// bucket_est[i].  Cut points are placed at bucket boundaries where the running estimate crosses
+// multiples of total/k, k = max(min_batches, ceil(total / (capacity/(1+margin)))); a bucket whose
+// estimate alone exceeds the target is split evenly (it is not sampled any finer).
+void plan_from_buckets(const double *bucket_est, uint64_t nbk, uint64_t width, uint64_t q0, uint64_t q1,
+                       uint64_t capacity, int min_batches, double margin, std::vector<uint64_t> &cuts,
+                       std::vector<uint64_t> &est, uint64_t *estimated_total)
 {
     cuts.clear();
     est.clear();
     const uint64_t nq = q1 - q0;
     struct Unit { uint64_t a, b; double e; };
     std::vector<Unit> units;
+    units.reserve(nbk);
     const double target = std::max(1.0, (double)capacity / (1.0 + margin));
     double total = 0;
-    // sample s stands for queries [q0 + s*step, min(q1, q0 + (s+1)*step)); a unit whose estimate
-    // alone exceeds the target is split evenly (it is not sampled any finer)
-    for (uint64_t s = 0; s < ns; ++s) {
-        const uint64_t a = q0 + s * step, b = std::min(q1, a + step);
+    for (uint64_t s = 0; s < nbk; ++s) {
+        const uint64_t a = q0 + s * width, b = std::min(q1, a + width);
         if (a >= b) break;
-        const double bv = (double)cnt[s] * (double)(b - a);
+        const double bv = bucket_est[s];
         total += bv;
-        uint64_t parts = 1;
-        if (bv > target) parts = std::min<uint64_t>(b - a, (uint64_t)std::ceil(bv / target));
+        if (!(bv > target) || b - a < 2) {
+            units.push_back({a, b, bv});
+            continue;
+        }
+        const uint64_t parts = std::min<uint64_t>(b - a, (uint64_t)std::ceil(bv / target));
         for (uint64_t p = 0; p < parts; ++p) {
             const uint64_t ua = a + (b - a) * p / parts, ub = a + (b - a) * (p + 1) / parts;
             units.push_back({ua, ub, bv * (double)(ub - ua) / (double)(b - a)});
@@ -108,14 +114,41 @@ void plan_batches(const uint32_t *cnt, uint64_t ns, uint64_t step, uint64_t q0, 
         if (bl < 2) break;
         cuts.insert(cuts.begin() + best + 1, cuts[best] + bl / 2);
     }
-    for (size_t i = 0; i + 1 < cuts.size(); ++i) {
-        double e = 0;
-        for (const Unit &u : units) {
-            const uint64_t lo = std::max(u.a, cuts[i]), hi = std::min(u.b, cuts[i + 1]);
-            if (hi > lo) e += u.e * (double)(hi - lo) / (double)(u.b - u.a);
+    // per-range estimates: one merge walk over units and ranges (units only straddle a cut made by
+    // the min-batches split; their estimate is then shared by query count)
+    est.assign(cuts.size() - 1, 0);
+    std::vector<double> e(cuts.size() - 1, 0.0);
+    size_t r = 0;
+    for (const Unit &u : units) {
+        uint64_t a = u.a;
+        while (a < u.b) {
+            while (r + 1 < cuts.size() - 1 && cuts[r + 1] <= a) ++r;
+            const uint64_t b = std::min(u.b, cuts[r + 1]);
+            e[r] += (b - a == u.b - u.a) ? u.e : u.e * (double)(b - a) / (double)(u.b - u.a);
+            a = b;
+            if (r + 1 >= cuts.size() - 1) {     // last range takes the rest
+                if (a < u.b) e[r] += u.e * (double)(u.b - a) / (double)(u.b - u.a);
+                break;
+            }
         }
-        est.push_back((uint64_t)std::ceil(e));
     }
+    for (size_t i = 0; i < e.size(); ++i) est[i] = (uint64_t)std::ceil(e[i]);
+}
+
+// Counts of a strided sample (sample s = query q0 + s*step, standing for `step` queries).
+void plan_batches(const uint32_t *cnt, uint64_t ns, uint64_t step, uint64_t q0, uint64_t q1, uint64_t capacity,
+                  int min_batches, double margin, std::vector<uint64_t> &cuts, std::vector<uint64_t> &est,
+                  uint64_t *estimated_total)
+{
+    // at most ~1024 planning buckets: merge g consecutive samples (cuts need no finer grain)
+    const uint64_t g = std::max<uint64_t>(1, (ns + 1023) / 1024);
+    const uint64_t nbk = (ns + g - 1) / g;
+    std::vector<double> be(nbk, 0.0);
+    for (uint64_t s = 0; s < ns; ++s) {
+        const uint64_t a = q0 + s * step, b = std::min(q1, a + step);
+        if (a < b) be[s / g] += (double)cnt[s] * (double)(b - a);
+    }
+    plan_from_buckets(be.data(), nbk, step * g, q0, q1, capacity, min_batches, margin, cuts, est, estimated_total);
 }
 
 namespace {
@@ -124,13 +157,17 @@ struct Sample {
     uint64_t step = 1, ns = 0;
 };
 
+// Deterministic sample of >= 1% and >= 1000 queries (SPEC S.260), taken as runs of 32
+// consecutive A-order queries every 32*step queries (warp-coherent); each sample stands for
+// `step` queries.  ns counts sample slots (multiple of 32; the ragged last run is masked).
 Sample make_sample(uint64_t nq)
 {
     Sample sm;
     if (nq == 0) return sm;
     const uint64_t target = std::min<uint64_t>(nq, std::max<uint64_t>(1000, (nq + 99) / 100));
     sm.step = std::max<uint64_t>(1, nq / target);
-    sm.ns = (nq + sm.step - 1) / sm.step;
+    const uint64_t runs = (nq + 32 * sm.step - 1) / (32 * sm.step);
+    sm.ns = runs * 32;
     return sm;
 }
 
@@ -150,6 +187,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     uint64_t q0, q1;
     validate(idx, o, &q0, &q1);
     const auto t_begin = std::chrono::steady_clock::now();
+    HostTrace tr("join");
     SJ_CUDA(cudaSetDevice(idx->device));
     const DevIndex &ix = idx->dev;
     const int S = o.n_streams;
@@ -159,50 +197,59 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     constexpr size_t kWorkBytes = 64;                 // 4 u64 work counters (+pad)
     const uint64_t nq = q1 - q0;
     const Sample sm = make_sample(nq);
-    const size_t slot_need = kWorkBytes + sizeof(Slot) * (size_t)std::max<int>(S, 64) + 4 * (size_t)(sm.ns + 1);
+    const uint64_t group = 32 * std::max<uint64_t>(1, (sm.ns / 32 + 1023) / 1024);  // whole runs per bucket
+    const uint64_t nbk = sm.ns ? (sm.ns + group - 1) / group : 0;
+    const size_t kSlotsBytes = sizeof(Slot) * 64;
+    const size_t slot_need = kWorkBytes + kSlotsBytes + 8 * (size_t)(nbk + 1);
     CtxGuard cg{acquire_ctx(idx->device, S, 2 * S + 2, slot_need)};
     DevCtx &cx = *cg.c;
     cudaStream_t s0 = cx.streams[0];
-    unsigned long long *work = static_cast<unsigned long long *>(cx.d_slots);
-    unsigned long long *hwork = static_cast<unsigned long long *>(cx.h_slots);
-    Slot *dslots = reinterpret_cast<Slot *>(static_cast<char *>(cx.d_slots) + kWorkBytes);
-    Slot *hslots = reinterpret_cast<Slot *>(static_cast<char *>(cx.h_slots) + kWorkBytes);
-    const size_t slot_cap = (cx.slot_bytes - kWorkBytes - 4 * (size_t)(sm.ns + 1)) / sizeof(Slot);
-    uint32_t *dqcount = reinterpret_cast<uint32_t *>(static_cast<char *>(cx.d_slots) + cx.slot_bytes -
-                                                     4 * (size_t)(sm.ns + 1));
-    uint32_t *hqcount = reinterpret_cast<uint32_t *>(static_cast<char *>(cx.h_slots) + cx.slot_bytes -
-                                                     4 * (size_t)(sm.ns + 1));
-
+    char *dbase = static_cast<char *>(cx.d_slots), *hbase = static_cast<char *>(cx.h_slots);
+    unsigned long long *work = reinterpret_cast<unsigned long long *>(dbase);
+    unsigned long long *hwork = reinterpret_cast<unsigned long long *>(hbase);
+    Slot *dslots = reinterpret_cast<Slot *>(dbase + kWorkBytes);
+    Slot *hslots = reinterpret_cast<Slot *>(hbase + kWorkBytes);
+    unsigned long long *dbk = reinterpret_cast<unsigned long long *>(dbase + kWorkBytes + kSlotsBytes);
+    unsigned long long *hbk = reinterpret_cast<unsigned long long *>(hbase + kWorkBytes + kSlotsBytes);
+    tr.mark("acquire ctx");
     sj_result *res = new sj_result();
     res->device = idx->device;
     sj_stats &stats = res->stats;
     try {
         SJ_CUDA(cudaMemsetAsync(work, 0, kWorkBytes, s0));
-        // ---- a5: estimate on a strided sample (count-only refine)
+        // ---- a5: estimate on a strided sample (count-only refine), summed per planning bucket
         float est_ms = 0;
         if (sm.ns) {
+            SJ_CUDA(cudaMemsetAsync(dbk, 0, 8 * nbk, s0));
             JoinArgs ja = base_args(o, nullptr);
             ja.q0 = (uint32_t)q0;
             ja.q1 = (uint32_t)q1;
             ja.step = (uint32_t)sm.step;
             ja.nsamples = (uint32_t)sm.ns;
-            ja.qcount = dqcount;
+            ja.qbucket = dbk;
+            ja.group = (uint32_t)group;
             SJ_CUDA(cudaEventRecord(cx.events[0], s0));
             launch_refine<kCountQuery>(ix, ja, o.unicomp != 0, (uint32_t)sm.ns, s0);
             SJ_CUDA(cudaEventRecord(cx.events[1], s0));
-            SJ_CUDA(cudaMemcpyAsync(hqcount, dqcount, sm.ns * sizeof(uint32_t), cudaMemcpyDeviceToHost, s0));
+            SJ_CUDA(cudaMemcpyAsync(hbk, dbk, nbk * 8, cudaMemcpyDeviceToHost, s0));
             SJ_CUDA(cudaStreamSynchronize(s0));
             SJ_CUDA(cudaEventElapsedTime(&est_ms, cx.events[0], cx.events[1]));
         }
         stats.estimate_ms = est_ms;
+        tr.mark("estimate (synced)");
 
         // ---- plan (k >= min_batches contiguous A-order ranges)
         std::vector<uint64_t> cuts, est;
         uint64_t est_total = 0;
-        plan_batches(hqcount, sm.ns, sm.step, q0, q1, o.batch_capacity_pairs, o.min_batches, 0.25, cuts, est,
-                     &est_total);
+        {
+            std::vector<double> be(nbk);
+            for (uint64_t i = 0; i < nbk; ++i) be[i] = (double)hbk[i] * (double)sm.step;
+            plan_from_buckets(be.data(), nbk, sm.step * group, q0, q1, o.batch_capacity_pairs, o.min_batches, 0.25,
+                              cuts, est, &est_total);
+        }
         stats.estimated_pairs = est_total;
         const size_t nb = cuts.size() - 1;
+        tr.mark("plan");
 
         float refine_ms = 0, refine_max = 0;
         uint32_t launches = 0;
@@ -254,7 +301,9 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                           cx.events[3 + 2 * si]);
                 SJ_CUDA(cudaMemcpyAsync(hslots + si, dslots + si, sizeof(Slot), cudaMemcpyDeviceToHost, s));
             }
+            tr.mark("batches launched");
             for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
+            tr.mark("batches done (synced)");
             for (size_t b = (nb > (size_t)S ? nb - S : 0); b < nb; ++b) drain_stream_slot(b);
             for (size_t b = 0; b < nb; ++b) {
                 sj_batch &bt = res->batches[b];
@@ -336,7 +385,6 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             }
             for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
         }
-        (void)slot_cap;
 
         // ---- work counters
         SJ_CUDA(cudaMemcpyAsync(hwork, work, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0));
@@ -348,6 +396,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         stats.refine_ms = refine_ms;
         stats.refine_max_ms = refine_max;
         stats.refine_launches = launches;
+        tr.mark("stats");
     } catch (...) {
         for (auto s : cx.streams) cudaStreamSynchronize(s);
         for (auto &b : res->batches) {

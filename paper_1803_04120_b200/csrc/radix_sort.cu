@@ -5,88 +5,104 @@
 // A.  Stability (ties keep the ascending point-id order of the input) makes A deterministic
 // (reading R14).  Only the key_bits actually used by prod|g_j| are sorted.
 //
-// Per 8-bit digit pass (HBM-bound; 3 kernels):
-//   hist    : each CTA histograms its TILE of digits in shared memory -> counts[digit][cta]
+// ceil(key_bits/11) passes of <= 11-bit digits (41-bit 6-D keys: 4 passes); per pass (HBM-bound):
+//   hist    : each CTA histograms its 4096-item tile in shared memory -> counts[digit][cta]
 //   scan    : exclusive scan over counts in digit-major order -> scatter base per (digit, cta)
-//   scatter : each CTA re-reads its tile in order and places every item at
-//             base[digit][cta] + (rank among equal digits before it in the tile), the rank
-//             computed with __match_any_sync inside a warp plus per-warp digit counts in smem.
+//   scatter : each warp ranks its 512 consecutive items in registers (__match_any_sync + warp
+//             private digit counters, no CTA barrier per round), one CTA prefix over the warps,
+//             then every item goes to base[digit][cta] + its stable rank.
 #include "sj_common.cuh"
 
 namespace sj {
 
 namespace {
 
-constexpr int kRadixBits = 8;
-constexpr int kRadix = 1 << kRadixBits;
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 16;
-constexpr int kTile = kSortThreads * kSortItems;
+constexpr int kSortRounds = 16;                       // items per thread
+constexpr int kWarpTile = 32 * kSortRounds;           // 512 consecutive items per warp
+constexpr int kTile = kSortWarps * kWarpTile;         // 4096 items per CTA
 
+template <int BITS>
 __global__ void __launch_bounds__(kSortThreads)
 k_radix_hist(const uint64_t *__restrict__ keys, uint32_t n, int shift, uint32_t *__restrict__ counts,
-             uint32_t nblocks)
+             uint32_t ntiles)
 {
-    __shared__ uint32_t h[kRadix];
-    for (int i = threadIdx.x; i < kRadix; i += kSortThreads) h[i] = 0;
+    constexpr int R = 1 << BITS;
+    __shared__ uint32_t h[R];
+    for (int i = threadIdx.x; i < R; i += kSortThreads) h[i] = 0;
     __syncthreads();
     const uint64_t base = (uint64_t)blockIdx.x * kTile;
 #pragma unroll 4
-    for (int r = 0; r < kSortItems; ++r) {
-        uint64_t i = base + (uint64_t)r * kSortThreads + threadIdx.x;
-        if (i < n) atomicAdd(&h[(keys[i] >> shift) & (kRadix - 1)], 1u);
+    for (int r = 0; r < kTile / kSortThreads; ++r) {
+        const uint64_t i = base + (uint64_t)r * kSortThreads + threadIdx.x;
+        if (i < n) atomicAdd(&h[(keys[i] >> shift) & (R - 1)], 1u);
     }
     __syncthreads();
-    for (int dg = threadIdx.x; dg < kRadix; dg += kSortThreads)
-        counts[(uint64_t)dg * nblocks + blockIdx.x] = h[dg];
+    for (int dg = threadIdx.x; dg < R; dg += kSortThreads) counts[(uint64_t)dg * ntiles + blockIdx.x] = h[dg];
 }
 
+// Stable scatter of one digit pass.  Each warp ranks its own 512 consecutive items round by
+// round (32 items per round, __match_any_sync for equal digits, a warp-private running count per
+// digit in shared memory) -- no CTA barrier inside the rounds; one CTA-wide exclusive prefix over
+// the warps per digit then turns warp ranks into tile ranks.  Item order == rank order within a
+// digit, so the pass is stable (A ties keep ascending point ids, reading R14).
+template <int BITS>
 __global__ void __launch_bounds__(kSortThreads)
-k_radix_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin,
-                uint64_t *__restrict__ kout, uint32_t *__restrict__ vout, uint32_t n, int shift,
-                const uint32_t *__restrict__ offsets, uint32_t nblocks)
+k_radix_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
+                uint32_t *__restrict__ vout, uint32_t n, int shift, const uint32_t *__restrict__ offsets,
+                uint32_t ntiles)
 {
-    __shared__ uint32_t s_base[kRadix];
-    __shared__ uint32_t s_wcnt[kSortWarps][kRadix];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int dg = tid; dg < kRadix; dg += kSortThreads)
-        s_base[dg] = offsets[(uint64_t)dg * nblocks + blockIdx.x];
-    const unsigned lt_mask = (1u << lane) - 1u;
-    const uint64_t base = (uint64_t)blockIdx.x * kTile;
-    for (int r = 0; r < kSortItems; ++r) {
-        const uint64_t i = base + (uint64_t)r * kSortThreads + tid;
-        const bool valid = i < n;
-        uint64_t k = 0;
-        uint32_t v = 0;
-        int dg = kRadix;  // sentinel for invalid lanes
-        if (valid) {
-            k = kin[i];
-            v = vin[i];
-            dg = (int)((k >> shift) & (kRadix - 1));
-        }
-        const unsigned peers = __match_any_sync(0xffffffffu, dg);
-        const int leader = __ffs(peers) - 1;
-        const uint32_t rank_w = __popc(peers & lt_mask);
-        for (int w = 0; w < kSortWarps; ++w) s_wcnt[w][tid] = 0;  // kSortThreads == kRadix
-        __syncthreads();
-        if (valid && lane == leader) s_wcnt[warp][dg] = __popc(peers);
-        __syncthreads();
-        if (valid) {
-            uint32_t pre = 0;
-            for (int w = 0; w < warp; ++w) pre += s_wcnt[w][dg];
-            const uint32_t pos = s_base[dg] + pre + rank_w;
-            kout[pos] = k;
-            vout[pos] = v;
-        }
-        __syncthreads();
-        {
-            uint32_t tot = 0;
+    constexpr int R = 1 << BITS;
+    extern __shared__ uint32_t s_cnt[];               // [kSortWarps][R]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t *wc = s_cnt + warp * R;
+    for (int i = lane; i < R; i += 32) wc[i] = 0;
+    __syncwarp();
+    const unsigned lt = (1u << lane) - 1u;
+    const uint64_t wbase = (uint64_t)blockIdx.x * kTile + (uint64_t)warp * kWarpTile;
+    uint64_t k[kSortRounds];
+    uint32_t v[kSortRounds], rk[kSortRounds];
 #pragma unroll
-            for (int w = 0; w < kSortWarps; ++w) tot += s_wcnt[w][tid];
-            s_base[tid] += tot;
+    for (int r = 0; r < kSortRounds; ++r) {
+        const uint64_t i = wbase + (uint64_t)r * 32 + lane;
+        const bool valid = i < n;
+        k[r] = valid ? kin[i] : 0;
+        v[r] = valid ? vin[i] : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < kSortRounds; ++r) {
+        const uint64_t i = wbase + (uint64_t)r * 32 + lane;
+        const bool valid = i < n;
+        const uint32_t dg = valid ? (uint32_t)((k[r] >> shift) & (R - 1)) : (uint32_t)R;
+        const unsigned peers = __match_any_sync(0xffffffffu, dg);
+        const uint32_t before = valid ? wc[dg] : 0u;
+        rk[r] = before + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (peers & lt) == 0u) wc[dg] = before + __popc(peers);   // group leader
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: tile offset = global offset of (digit, tile) + counts of the warps before
+    for (int dg = threadIdx.x; dg < R; dg += kSortThreads) {
+        uint32_t run = offsets[(uint64_t)dg * ntiles + blockIdx.x];
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w) {
+            const uint32_t c = s_cnt[w * R + dg];
+            s_cnt[w * R + dg] = run;
+            run += c;
         }
-        __syncthreads();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kSortRounds; ++r) {
+        const uint64_t i = wbase + (uint64_t)r * 32 + lane;
+        if (i < n) {
+            const uint32_t dg = (uint32_t)((k[r] >> shift) & (R - 1));
+            const uint32_t pos = wc[dg] + rk[r];
+            kout[pos] = k[r];
+            vout[pos] = v[r];
+        }
     }
 }
 
@@ -209,22 +225,45 @@ void inclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStrea
     scan_u32(in, out, n, true, s);
 }
 
+namespace {
+template <int BITS>
+void radix_pass(const uint64_t *ka, const uint32_t *va, uint64_t *kb, uint32_t *vb, uint32_t n, int shift,
+                uint32_t *counts, uint32_t *offs, uint32_t nt, cudaStream_t s)
+{
+    constexpr int R = 1 << BITS;
+    k_radix_hist<BITS><<<nt, kSortThreads, 0, s>>>(ka, n, shift, counts, nt);
+    SJ_LAUNCHED();
+    exclusive_scan_u32(counts, offs, (uint64_t)R * nt, s);
+    const size_t smem = sizeof(uint32_t) * kSortWarps * R;
+    SJ_CUDA(cudaFuncSetAttribute(k_radix_scatter<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_radix_scatter<BITS><<<nt, kSortThreads, smem, s>>>(ka, va, kb, vb, n, shift, offs, nt);
+    SJ_LAUNCHED();
+}
+}  // namespace
+
+// Stable LSD radix sort over the low key_bits bits: ceil(key_bits/11) passes of equal width
+// (<= 11 bits: 2048 buckets, 64 KB of warp counters per CTA).
 void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp,
                       uint32_t n, int key_bits, cudaStream_t s, bool *result_in_tmp)
 {
     *result_in_tmp = false;
     if (n <= 1 || key_bits <= 0) return;
-    const uint32_t nb = (n + kTile - 1) / kTile;
-    Scratch<uint32_t> counts((size_t)kRadix * nb, s);
-    Scratch<uint32_t> offs((size_t)kRadix * nb, s);
+    const uint32_t nt = (n + kTile - 1) / kTile;
+    const int passes = (key_bits + 10) / 11;
+    const int bits = (key_bits + passes - 1) / passes;   // 1..11
+    Scratch<uint32_t> counts((size_t)(1u << bits) * nt, s);
+    Scratch<uint32_t> offs((size_t)(1u << bits) * nt, s);
     uint64_t *ka = keys, *kb = keys_tmp;
     uint32_t *va = vals, *vb = vals_tmp;
-    for (int shift = 0; shift < key_bits; shift += kRadixBits) {
-        k_radix_hist<<<nb, kSortThreads, 0, s>>>(ka, n, shift, counts.p, nb);
-        SJ_LAUNCHED();
-        exclusive_scan_u32(counts.p, offs.p, (uint64_t)kRadix * nb, s);
-        k_radix_scatter<<<nb, kSortThreads, 0, s>>>(ka, va, kb, vb, n, shift, offs.p, nb);
-        SJ_LAUNCHED();
+    for (int p = 0; p < passes; ++p) {
+        const int shift = p * bits;
+        switch (bits) {
+#define SJ_PASS(B) case B: radix_pass<B>(ka, va, kb, vb, n, shift, counts.p, offs.p, nt, s); break;
+            SJ_PASS(1) SJ_PASS(2) SJ_PASS(3) SJ_PASS(4) SJ_PASS(5) SJ_PASS(6)
+            SJ_PASS(7) SJ_PASS(8) SJ_PASS(9) SJ_PASS(10) SJ_PASS(11)
+#undef SJ_PASS
+        default: fail(SJ_ERR_ARG, "bad radix width");
+        }
         std::swap(ka, kb);
         std::swap(va, vb);
         *result_in_tmp = !*result_in_tmp;

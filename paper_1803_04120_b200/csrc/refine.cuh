@@ -38,11 +38,12 @@ struct JoinArgs {
     unsigned long long *cursor;    // kEmit: pairs emitted (exact even on overflow)
     uint64_t cap;                  // kEmit: capacity of out
     uint32_t *overflow;            // kEmit: set when a write was dropped
-    uint32_t *qcount;              // kCountQuery: emissions of sample t
+    unsigned long long *qbucket;   // kCountQuery: emissions summed per planning bucket (t / group)
+    uint32_t group;                // kCountQuery: samples per bucket
     uint32_t *pcount;              // kCountPoint: cnt[original id]
     unsigned long long *work;      // [0] B searches, [1] distance tests, [2] emissions
     uint32_t q0, q1;               // A-position range of the queries
-    uint32_t step, nsamples;       // kCountQuery: sample t is query q0 + t*step
+    uint32_t step, nsamples;       // kCountQuery: sample t = query q0 + (t/32)*32*step + t%32
     int include_self;
     int use_masks;
 };
@@ -420,8 +421,10 @@ k_refine(const DevIndex ix, const JoinArgs ja)
     uint32_t k;
     bool active;
     if constexpr (MODE == kCountQuery) {
-        active = t < ja.nsamples;
-        k = ja.q0 + t * ja.step;
+        // sample t: lane t%32 of run t/32; run r = the first 32 queries of block [r*32*step, ...),
+        // so a warp samples 32 consecutive (cell-coherent) queries
+        k = ja.q0 + (t >> 5) * (32u * ja.step) + (t & 31u);
+        active = t < ja.nsamples && k < ja.q1;
     } else {
         k = ja.q0 + t;
         active = k < ja.q1;
@@ -435,7 +438,7 @@ k_refine(const DevIndex ix, const JoinArgs ja)
     q.emitted = q.probes = q.tests = 0;
     if (active) {
         refine_query<D, MODE, UNICOMP>(ix, ja, k, q, tt);
-        if constexpr (MODE == kCountQuery) ja.qcount[t] = q.emitted;
+        if constexpr (MODE == kCountQuery) atomicAdd(ja.qbucket + t / ja.group, (unsigned long long)q.emitted);
     }
     // work counters: warp reduce, one atomic per warp
     unsigned long long p = q.probes, c = q.tests, em = q.emitted;

@@ -29,6 +29,15 @@ inline void count_launch(uint64_t k = 1) { g_kernel_launches.fetch_add(k, std::m
 // Checks the launch configuration error right after a <<<>>> launch.
 #define SJ_LAUNCHED() do { ::sj::count_launch(); SJ_CUDA(cudaGetLastError()); } while (0)
 
+// ---------------------------------------------------------------- host tracing (SJ_TRACE=1)
+struct HostTrace {
+    bool on;
+    const char *what;
+    double t0, last;
+    explicit HostTrace(const char *w);
+    void mark(const char *stage);
+};
+
 // ---------------------------------------------------------------- device memory
 void *dev_alloc(size_t bytes, cudaStream_t s);
 void dev_free(void *p, cudaStream_t s);
@@ -157,6 +166,9 @@ void inclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStrea
 // join.cu
 sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o);
 void neighbor_counts_impl(const sj_index *idx, const sj_join_opts &o, uint32_t *cnt, uint64_t *total);
+void plan_from_buckets(const double *bucket_est, uint64_t nbk, uint64_t width, uint64_t q0, uint64_t q1,
+                       uint64_t capacity, int min_batches, double margin, std::vector<uint64_t> &cuts,
+                       std::vector<uint64_t> &est, uint64_t *estimated_total);
 void plan_batches(const uint32_t *sample_counts, uint64_t n_samples, uint64_t step, uint64_t q_begin,
                   uint64_t q_end, uint64_t capacity, int min_batches, double margin,
                   std::vector<uint64_t> &cuts, std::vector<uint64_t> &est, uint64_t *estimated_total);
