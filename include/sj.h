@@ -80,6 +80,9 @@ typedef struct {
                                       queries decide, so the union over a partition of [0,N) is
                                       exactly S with no duplicates.                               */
     int use_masks;                 /* 1 (default): filter adjacent coordinates by M_j (Alg. 1 l.6) */
+    int lanes_per_query;           /* 0 (default): chosen per index; else 1,2,4,8,16 or 32 GPU lanes
+                                      cooperate on one query (a tuning / testing knob; S is
+                                      independent of it)                                         */
 } sj_join_opts;
 
 typedef struct {

@@ -21,9 +21,12 @@ namespace sj {
 namespace {
 
 template <int MODE>
-void launch_refine(const DevIndex &ix, const JoinArgs &ja, bool unicomp, uint32_t nthreads, cudaStream_t s)
+void launch_refine(const DevIndex &ix, const JoinArgs &ja, bool unicomp, uint32_t nqueries, cudaStream_t s)
 {
-    if (nthreads == 0) return;
+    if (nqueries == 0) return;
+    const uint64_t nthreads64 = (uint64_t)nqueries << ja.lanes_log2;
+    if (nthreads64 >= (1ull << 32)) fail(SJ_ERR_ARG, "too many queries x lanes for one launch");
+    const uint32_t nthreads = (uint32_t)nthreads64;
     const dim3 grid((nthreads + kRefineThreads - 1) / kRefineThreads), block(kRefineThreads);
 #define SJ_REFINE_CASE(DD)                                                                       \
     case DD:                                                                                     \
@@ -44,6 +47,9 @@ void launch_refine(const DevIndex &ix, const JoinArgs &ja, bool unicomp, uint32_
 
 void validate(const sj_index *idx, const sj_join_opts &o, uint64_t *qb, uint64_t *qe)
 {
+    if (o.lanes_per_query != 0 && (o.lanes_per_query < 1 || o.lanes_per_query > 32 ||
+                                   (o.lanes_per_query & (o.lanes_per_query - 1))))
+        fail(SJ_ERR_ARG, "lanes_per_query must be 0 (auto) or a power of two <= 32");
     if (!idx) fail(SJ_ERR_STATE, "index is NULL");
     if (o.min_batches < 1 || o.min_batches > 1 << 20) fail(SJ_ERR_ARG, "min_batches must be >= 1");
     if (o.n_streams < 1 || o.n_streams > 32) fail(SJ_ERR_ARG, "n_streams must be in [1,32]");
@@ -171,12 +177,36 @@ Sample make_sample(uint64_t nq)
     return sm;
 }
 
-JoinArgs base_args(const sj_join_opts &o, unsigned long long *work)
+// Lanes per query (G): the largest power of two with G * 64 <= per-query work units (top-prefix
+// offsets in cell-scan mode, rows otherwise).  Measured on 6-D 2 M: eps=1 (27 offsets) is best at
+// G=1 (0.59 ms vs 0.70 at G=2); eps=8 (243 offsets) at G=2-4 (14.8 ms vs 17.0 at G=1).
+uint32_t lanes_log2_for(const DevIndex &ix, const sj_join_opts &o)
+{
+    uint32_t G = (uint32_t)o.lanes_per_query;
+    if (G == 0) {
+        uint32_t units;
+        if (ix.search_mode == kSearchCellScan) {
+            units = ix.dir_ntop;
+        } else {
+            units = 1;
+            for (int j = 1; j < ix.d; ++j) units *= 3;
+            units -= 1;
+        }
+        G = 1;
+        while (G < 32 && G * 2 * 64 <= units) G *= 2;
+    }
+    uint32_t l = 0;
+    while ((1u << l) < G) ++l;
+    return l;
+}
+
+JoinArgs base_args(const sj_index *idx, const sj_join_opts &o, unsigned long long *work)
 {
     JoinArgs ja{};
     ja.include_self = o.include_self;
     ja.use_masks = o.use_masks;
     ja.work = work;
+    ja.lanes_log2 = lanes_log2_for(idx->dev, o);
     return ja;
 }
 
@@ -221,7 +251,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         float est_ms = 0;
         if (sm.ns) {
             SJ_CUDA(cudaMemsetAsync(dbk, 0, 8 * nbk, s0));
-            JoinArgs ja = base_args(o, nullptr);
+            JoinArgs ja = base_args(idx, o, nullptr);
             ja.q0 = (uint32_t)q0;
             ja.q1 = (uint32_t)q1;
             ja.step = (uint32_t)sm.step;
@@ -256,7 +286,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         auto run_batch = [&](uint64_t a, uint64_t b, uint64_t *buf, uint64_t cap, Slot *dslot, cudaStream_t s,
                              cudaEvent_t e0, cudaEvent_t e1) {
             SJ_CUDA(cudaMemsetAsync(dslot, 0, sizeof(Slot), s));
-            JoinArgs ja = base_args(o, work);
+            JoinArgs ja = base_args(idx, o, work);
             ja.out = buf;
             ja.cap = cap;
             ja.cursor = &dslot->cursor;
@@ -430,7 +460,7 @@ void neighbor_counts_impl(const sj_index *idx, const sj_join_opts &o, uint32_t *
         c = own_cnt.p;
     }
     SJ_CUDA(cudaMemsetAsync(c, 0, sizeof(uint32_t) * idx->view.n, s));
-    JoinArgs ja = base_args(o, work);
+    JoinArgs ja = base_args(idx, o, work);
     ja.pcount = c;
     ja.q0 = (uint32_t)q0;
     ja.q1 = (uint32_t)q1;

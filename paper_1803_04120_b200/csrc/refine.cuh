@@ -1,30 +1,34 @@
-// refine.cuh -- the per-point refine kernel (steps a5-a7 of the hot path).
+// refine.cuh -- the refine kernel (steps a5-a7 of the hot path).
 //
-// PAPER.md §4.5 Alg. 1 (lines 216-251, GPUSelfJoinGlobal): one thread per query point, in
-// A-order (the cell-sorted order, so a warp's queries share cells and index prefixes).  The
-// thread holds its point in registers (Alg. 1 l.4), finds its home cell, enumerates the
-// adjacent cells (l.5-10), looks each up in B (l.11) and tests the points of every non-empty
-// one (l.12-16).  With unicomp (§5.2, Alg. 2, readings R10-R13) only the
-// cells whose highest differing dimension j has c_j odd are searched, and every hit is
-// emitted in both orientations; the home cell emits (p,p) once plus, for
-// every q after p in A-order, both (p,q) and (q,p).
+// PAPER.md §4.5 Alg. 1 (lines 216-251, GPUSelfJoinGlobal): queries in A-order (the cell-sorted
+// order, so neighbouring queries share cells and index prefixes); each query holds its point in
+// registers (Alg. 1 l.4), finds its home cell, enumerates the adjacent cells (l.5-10), looks each
+// up in B (l.11) and tests the points of every non-empty one (l.12-16).  With unicomp (PAPER.md
+// §5.2, Alg. 2, readings R10-R13) a neighbour cell is searched only when the query's
+// coordinate in the highest differing dimension is odd, and every hit is emitted in both
+// orientations; the home cell emits (p,p) once plus, for every q after p in
+// A-order, both (p,q) and (q,p).
 //
-// B200-specific choices:
-//  * bounded binary search: the linear id is dimension-1-fastest, so the three cells
-//    c_1-1..c_1+1 of a "row" (fixed dims >= 2) are consecutive ids, hence consecutive in B and
-//    their points ONE contiguous A-range: one lookup per row of 3 cells, not per cell.  The
-//    cells sharing the top-k coordinates form one contiguous range of B too; a prefix
-//    directory (index_build.cu build_directory, <= 16 B per non-empty cell) maps a row's top-k
-//    prefix to that range in O(1), and the binary search for the row is bounded to it (a few
-//    entries).  When the directory covers every dimension a row costs two loads.  Eight
-//    rows' directory loads are issued together for memory-level parallelism.
-//  * the distance is s = (((x_0-y_0)^2 + (x_1-y_1)^2) + ...) with __dsub_rn/__dmul_rn/__dadd_rn
-//    (no FMA contraction possible) compared with fl(eps^2): bit-identical decisions to the
-//    oracle (readings R1, R2).
+// B200-specific design:
+//  * G lanes per query (G = 1..32, power of two, chosen per index from the expected work): the
+//    lanes of a group split the query's top-prefix offsets (cell-scan mode), rows (row modes) and
+//    home-cell points, so a warp stays converged even when per-query work varies (a 6-D eps=8
+//    join ran with 7 of 32 lanes active at G=1).
+//  * bounded search through the prefix directory: the cells sharing their top-k coordinates form
+//    one contiguous range of B, dir[p] gives it in O(1), and every search is bounded to it.
+//    Three modes (index_build.cu): dense rows (k = d), cell scan (few cells per prefix: test the
+//    low coordinates greedily on the key difference) and rows (bounded binary search per row of
+//    three consecutive ids = one contiguous A-range).
+//  * per-CTA shared-memory table of the top-prefix offsets: unicomp / mask decisions per offset
+//    are two bit tests.
+//  * the distance s = (((x_0-y_0)^2 + (x_1-y_1)^2) + ...) with __dsub_rn/__dmul_rn/__dadd_rn (no FMA
+//    contraction possible) compared with fl(eps^2): bit-identical decisions to the oracle (R1, R2).
 //  * warp-aggregated emission: __ballot_sync of the hits, __popc, ONE atomicAdd per warp on the
-//    batch cursor, __shfl_sync of the base, each hitting lane writes its 1 or 2 packed pairs.
+//    batch cursor, __shfl_sync of the base; each hitting lane writes its 1 or 2 packed pairs.
 //    Writes past the batch capacity are dropped and flag an overflow; the cursor keeps counting
-//    so the host learns the exact size and re-runs the batch (split-retry / exact realloc).
+//    so the host learns the exact size and re-runs the batch.
+//  * every search loop is rolled and the candidate loop is inlined at four call sites only,
+//    keeping the kernel ~3 K SASS (an unrolled version measured 28 K SASS, 47% no_inst stalls).
 #pragma once
 
 #include "sj_common.cuh"
@@ -41,18 +45,19 @@ struct JoinArgs {
     unsigned long long *qbucket;   // kCountQuery: emissions summed per planning bucket (t / group)
     uint32_t group;                // kCountQuery: samples per bucket
     uint32_t *pcount;              // kCountPoint: cnt[original id]
-    unsigned long long *work;      // [0] B searches, [1] distance tests, [2] emissions
+    unsigned long long *work;      // [0] directory/row lookups, [1] distance tests, [2] emissions
     uint32_t q0, q1;               // A-position range of the queries
     uint32_t step, nsamples;       // kCountQuery: sample t = query q0 + (t/32)*32*step + t%32
+    uint32_t lanes_log2;           // G = 1 << lanes_log2 lanes cooperate on one query
     int include_self;
     int use_masks;
 };
 
 constexpr int kRefineThreads = 256;
 #ifndef SJ_REFINE_MIN_BLOCKS
-#define SJ_REFINE_MIN_BLOCKS 2
+#define SJ_REFINE_MIN_BLOCKS 3
 #endif
-constexpr int kRefineMinBlocks = SJ_REFINE_MIN_BLOCKS;  // 2 x 256 threads: <= 128 registers
+constexpr int kRefineMinBlocks = SJ_REFINE_MIN_BLOCKS;  // 3 x 256 threads: <= 85 registers
 
 __device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t *__restrict__ B, uint32_t lo, uint32_t hi,
                                                     uint64_t key)
@@ -72,8 +77,9 @@ struct QueryState {
     uint32_t k;        // A-position of the query
     uint32_t pid;      // original id A[k]
     uint32_t odd;      // bit j = parity of c_j (unicomp decisions without dynamic indexing)
-    uint32_t emitted;  // pairs emitted by this thread
-    uint32_t probes;   // binary searches
+    uint32_t sub, G;   // this lane's rank in the query's group, group size
+    uint32_t emitted;  // pairs emitted by this lane
+    uint32_t probes;   // directory / row lookups
     uint32_t tests;    // distance evaluations
 };
 
@@ -113,82 +119,29 @@ __device__ __forceinline__ void emit(const JoinArgs &ja, bool hit, uint32_t pid,
     }
 }
 
-// Everything the candidate loop needs, passed BY VALUE to the non-inlined scan (no stack copy
-// of the kernel parameter structs).
-template <int D>
-struct ScanArgs {
-    double x[D];                   // the query point
-    const double *X;               // SoA coordinates [D][n]
-    const uint32_t *A;
-    uint64_t *out;
-    unsigned long long *cursor;
-    uint32_t *overflow;
-    uint32_t *pcount;
-    uint64_t cap;
-    double eps2;
-    uint32_t n;
-    uint32_t pid;
-};
-
-// Test the points at A-positions [m0, m1) against the query.  Returns (tests << 32) | emitted.
-// Not inlined on purpose: it is called from every neighbour-cell site; one copy keeps the kernel
-// inside the instruction cache (an inlined version measured 28K SASS instructions, 47% no_inst).
+// Test the points at A-positions m0, m0+stride, ... < m1 against the query.
 template <int D, int MODE, bool BOTH>
-__device__ __noinline__ uint64_t scan_range_impl(const ScanArgs<D> sa, uint32_t m0, uint32_t m1)
+__device__ __forceinline__ void scan_range(const DevIndex &ix, const JoinArgs &ja, QueryState<D> &q, uint32_t m0,
+                                           uint32_t m1, uint32_t stride)
 {
-    JoinArgs ja{};
-    ja.out = sa.out;
-    ja.cursor = sa.cursor;
-    ja.cap = sa.cap;
-    ja.overflow = sa.overflow;
-    ja.pcount = sa.pcount;
-    uint32_t emitted = 0;
-    for (uint32_t m = m0; m < m1; ++m) {
+    const uint32_t n = ix.n;
+    for (uint32_t m = m0; m < m1; m += stride) {
         double s;
         {
-            const double t = __dsub_rn(sa.x[0], __ldg(sa.X + m));
+            const double t = __dsub_rn(q.x[0], __ldg(ix.X + m));
             s = __dmul_rn(t, t);
         }
 #pragma unroll
         for (int j = 1; j < D; ++j) {
-            const double t = __dsub_rn(sa.x[j], __ldg(sa.X + (uint64_t)j * sa.n + m));
+            const double t = __dsub_rn(q.x[j], __ldg(ix.X + (uint64_t)j * n + m));
             s = __dadd_rn(s, __dmul_rn(t, t));
         }
-        const bool hit = s <= sa.eps2;
+        ++q.tests;
+        const bool hit = s <= ix.eps2;
         uint32_t qid = 0;
-        if (MODE != kCountQuery && hit) qid = __ldg(sa.A + m);
-        emit<MODE, BOTH>(ja, hit, sa.pid, qid, emitted);
+        if (MODE != kCountQuery && hit) qid = __ldg(ix.A + m);
+        emit<MODE, BOTH>(ja, hit, q.pid, qid, q.emitted);
     }
-    return ((uint64_t)(m1 - m0) << 32) | emitted;
-}
-
-template <int D>
-__device__ __forceinline__ ScanArgs<D> make_scan_args(const DevIndex &ix, const JoinArgs &ja, const QueryState<D> &q)
-{
-    ScanArgs<D> sa;
-#pragma unroll
-    for (int j = 0; j < D; ++j) sa.x[j] = q.x[j];
-    sa.X = ix.X;
-    sa.A = ix.A;
-    sa.out = ja.out;
-    sa.cursor = ja.cursor;
-    sa.overflow = ja.overflow;
-    sa.pcount = ja.pcount;
-    sa.cap = ja.cap;
-    sa.eps2 = ix.eps2;
-    sa.n = ix.n;
-    sa.pid = q.pid;
-    return sa;
-}
-
-template <int D, int MODE, bool BOTH>
-__device__ __forceinline__ void scan_range(const DevIndex &ix, const JoinArgs &ja, QueryState<D> &q, uint32_t m0,
-                                           uint32_t m1)
-{
-    if (m0 >= m1) return;
-    const uint64_t r = scan_range_impl<D, MODE, BOTH>(make_scan_args<D>(ix, ja, q), m0, m1);
-    q.tests += (uint32_t)(r >> 32);
-    q.emitted += (uint32_t)r;
 }
 
 // Offsets of the top-k (directory) dimensions, precomputed once per CTA in shared memory:
@@ -220,76 +173,64 @@ __device__ __forceinline__ void build_top_table(const DevIndex &ix, TopTable &tt
     }
 }
 
-// Alg. 1 lines 5-6 (getAdjCells, maskCellRange): the adjacent range of every dimension
-// intersected with M_j, as a 3-bit set over the offsets {-1, 0, +1} (bit 1 = home, always in).
-template <int D>
-__device__ __forceinline__ void adjacent_masks(const DevIndex &ix, const JoinArgs &ja, const QueryState<D> &q,
-                                               uint32_t (&allow)[D])
+// Alg. 1 lines 5-6 (getAdjCells, maskCellRange): which moves of each dimension stay inside M_j,
+// as a "bad" bit set: bit i = move -1 in dim i leaves M_i, bit 8+i = move +1 leaves M_i;
+// unicomp adds bit 16+i when the query's c_i is even (cells decided by dim i are not searched).
+template <int D, bool UNICOMP>
+__device__ __forceinline__ uint32_t bad_moves(const DevIndex &ix, const JoinArgs &ja, const QueryState<D> &q)
 {
+    uint32_t bad = 0;
     const bool masked = ja.use_masks && ix.masks;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-        allow[i] = 7u;
         if (masked) {
             const uint64_t lo = ix.mask_off[i] + q.c[i] - 1ull, hi = lo + 2ull;
-            const uint32_t blo = (__ldg(ix.masks + (lo >> 5)) >> (lo & 31)) & 1u;
-            const uint32_t bhi = (__ldg(ix.masks + (hi >> 5)) >> (hi & 31)) & 1u;
-            allow[i] = 2u | blo | (bhi << 2);
+            if (!((__ldg(ix.masks + (lo >> 5)) >> (lo & 31)) & 1u)) bad |= 1u << i;
+            if (!((__ldg(ix.masks + (hi >> 5)) >> (hi & 31)) & 1u)) bad |= 1u << (i + 8);
         }
+        if (UNICOMP && !((q.odd >> i) & 1u)) bad |= 1u << (i + 16);
     }
-}
-
-// select element j (runtime) of a small register array without dynamic indexing
-template <int D, class T>
-__device__ __forceinline__ T sel(const T (&a)[D], int j)
-{
-    T v = a[0];
-#pragma unroll
-    for (int i = 1; i < D; ++i) v = (i == j) ? a[i] : v;
-    return v;
+    return bad;
 }
 
 // ---- search mode kSearchCellScan (sparse high-d data): for each offset of the top-k
 // (directory) dimensions, the cells of that prefix are B[dir[p], dir[p+1]) -- a handful.  Each
-// is tested by its low coordinates (decoded from its linear id): adjacent iff every low
-// coordinate is within +-1; unicomp keeps it iff the query's coordinate in the highest
-// differing dimension is odd (reading R13).  Covers every neighbour cell except the home cell.
+// is tested by its low coordinates: it is adjacent iff its key differs from the home key moved
+// into prefix p by sum_{i<L} delta_i * stride_i with every delta_i in {-1,0,1}.  Mixed-radix
+// digits are unique and stride_i > 2 * sum_{m<i} stride_m (|g_j| >= 3), so the deltas follow
+// greedily from the top low dimension (delta_i = sign(D) if |D| > lowR[i], else 0) -- no division.
+// Lanes of a query's group take offsets t = sub, sub+G, ...  Covers every neighbour cell except
+// the home cell.
 template <int D, int MODE, bool UNICOMP>
 __device__ __forceinline__ void search_cell_scan(const DevIndex &ix, const JoinArgs &ja, QueryState<D> &q,
-                                                 uint32_t h, const uint32_t (&allow)[D], const TopTable &tt)
+                                                 uint32_t h, uint64_t key, uint32_t bad, const TopTable &tt,
+                                                 unsigned wmask)
 {
     const int L = D - ix.dir_k;     // low dimensions 0..L-1 are not in the directory prefix
     uint64_t ph = 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) ph += q.c[j] * ix.pstride[j];
-    // masked-out moves (Alg. 1 line 6) and, for unicomp, the dims whose home coordinate is even
-    uint32_t bad = 0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        if (!(allow[i] & 1u)) bad |= 1u << i;
-        if (!(allow[i] & 4u)) bad |= 1u << (i + 8);
-        if (UNICOMP && !((q.odd >> i) & 1u)) bad |= 1u << (i + 16);
-    }
-    const uint32_t ntop = ix.dir_ntop;
-    const uint64_t key = __ldg(ix.B + h);
+    const int64_t Rl = ix.lowR[L];
+    // Uniform trip count for every lane of the warp and an explicit __syncwarp per offset: without
+    // it the lanes drift apart (independent thread scheduling) and their divergent cell loops
+    // serialise -- measured 2.4 of 32 lanes active on 6-D eps=8.
 #pragma unroll 1
-    for (uint32_t t = 0; t < ntop; ++t) {
+    for (uint32_t t0 = 0; t0 < ix.dir_ntop; t0 += q.G) {
+        __syncwarp(wmask);
+        const uint32_t t = t0 + q.sub;
+        if (t >= ix.dir_ntop) continue;
         const uint32_t bits = tt.bits[t];
         if (bits & bad) continue;      // masked-out coordinate, or decided by an even top dim
         const int jtop = (bits >> 16) ? (__ffs(bits >> 16) - 1) : -1;
         const uint64_t p = ph + (uint64_t)tt.dp[t];
         ++q.probes;
         const uint32_t lo = __ldg(ix.dir + p), hi = __ldg(ix.dir + p + 1);
-        // the home key moved into prefix p: a cell there is adjacent iff its key differs from it by
-        // sum_{i<L} delta_i * stride_i with every delta_i in {-1,0,1}.  Mixed-radix digits are
-        // unique and stride_i > 2 * sum_{m<i} stride_m (|g_j| >= 3), so the deltas follow greedily
-        // from the top low dimension: delta_i = sign(D) if |D| > lowR[i] else 0.
         const uint64_t kal = key + (uint64_t)tt.dk[t];
 #pragma unroll 1
         for (uint32_t hh = lo; hh < hi; ++hh) {
-            if (hh == h) continue;                       // home cell handled by the caller
+            if (hh == h) continue;                       // home cell handled separately
             int64_t dlt = (int64_t)(__ldg(ix.B + hh) - kal);
-            if (dlt > ix.lowR[L] || dlt < -ix.lowR[L]) continue;   // outside the +-1 box
+            if (dlt > Rl || dlt < -Rl) continue;         // outside the +-1 box
             int jlow = -1;
 #pragma unroll
             for (int i = D - 2; i >= 0; --i) {
@@ -301,7 +242,7 @@ __device__ __forceinline__ void search_cell_scan(const DevIndex &ix, const JoinA
             if (dlt != 0) continue;                      // not representable: not adjacent
             const int j = jtop >= 0 ? jtop : jlow;
             if (UNICOMP && !((q.odd >> j) & 1u)) continue;
-            scan_range<D, MODE, UNICOMP>(ix, ja, q, __ldg(ix.G + hh), __ldg(ix.G + hh + 1));
+            scan_range<D, MODE, UNICOMP>(ix, ja, q, __ldg(ix.G + hh), __ldg(ix.G + hh + 1), 1u);
         }
     }
 }
@@ -309,63 +250,72 @@ __device__ __forceinline__ void search_cell_scan(const DevIndex &ix, const JoinA
 // ---- search modes kSearchDenseRows / kSearchRows: rows whose highest differing dimension is
 // j = D-1 .. 1 (a row = the three cells c_0-1..c_0+1 of fixed dims >= 1: consecutive linear ids,
 // one contiguous A-range).  Unicomp: only when c_j is odd (reading R13).  Each row is looked up
-// in the prefix directory, then (kSearchRows) by a search bounded to that prefix's range.
+// in the prefix directory, then (kSearchRows) by a search bounded to that prefix's range.  The
+// rows of all j are numbered 0..3^(D-1)-2 (j = D-1 first) and dealt to the group's lanes.
 template <int D, int MODE, bool UNICOMP>
 __device__ __forceinline__ void search_rows(const DevIndex &ix, const JoinArgs &ja, QueryState<D> &q,
-                                            uint64_t key, const uint32_t (&allow)[D])
+                                            uint64_t key, uint32_t bad, unsigned wmask)
 {
     uint64_t ph = 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) ph += q.c[j] * ix.pstride[j];
     const bool dense = ix.search_mode == kSearchDenseRows;
-    uint64_t st[D], ps[D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) { st[i] = ix.strides[i]; ps[i] = ix.pstride[i]; }
+    constexpr uint32_t kPow3[7] = {1, 3, 9, 27, 81, 243, 729};
+    constexpr uint32_t nrows_all = kPow3[D - 1] - 1;
 #pragma unroll 1
-    for (int j = D - 1; j >= 1; --j) {
-        if (UNICOMP && !((q.odd >> j) & 1u)) continue;
-        uint32_t nrows = 2u;
-        for (int i = 1; i < j; ++i) nrows *= 3u;
-        const uint64_t stj = sel<D>(st, j), psj = sel<D>(ps, j);
-        const uint32_t allowj = sel<D>(allow, j);
-#pragma unroll 1
-        for (uint32_t r = 0; r < nrows; ++r) {
-            // row offsets: dim j = +-1 (bit 0 of r), dims 1..j-1 in {-1,0,1} (base-3 digits)
-            uint64_t b = (r & 1u) ? key + stj : key - stj;
-            uint64_t p = (r & 1u) ? ph + psj : ph - psj;
-            uint32_t ok = (allowj >> ((r & 1u) ? 2u : 0u)) & 1u;
-            uint32_t rest = r >> 1;
+    for (uint32_t R0 = 0; R0 < nrows_all; R0 += q.G) {
+        __syncwarp(wmask);                    // re-converge the warp every row (see cell scan)
+        const uint32_t R = R0 + q.sub;
+        if (R >= nrows_all) continue;
+        // decode (j, r): rows of top dim j are 2*3^(j-1), j = D-1 first
+        int j = D - 1;
+        uint32_t r = R;
 #pragma unroll
-            for (int i = 1; i < D - 1; ++i) {
-                if (i >= j) break;
-                const uint32_t dl = rest % 3u;
-                rest /= 3u;
-                ok &= allow[i] >> dl;
-                if (dl == 0u) { b -= st[i]; p -= ps[i]; }
-                else if (dl == 2u) { b += st[i]; p += ps[i]; }
-            }
-            if (!(ok & 1u)) continue;   // a masked-out coordinate: the row is empty
-            ++q.probes;
-            uint32_t s, e;
-            if (dense) {                // p is the centre cell's key: its row is [p-1, p+1]
-                s = __ldg(ix.dir + p - 1);
-                e = __ldg(ix.dir + p + 2);
-            } else {                    // bounded search inside the prefix's range for [b-1, b+1]
-                s = __ldg(ix.dir + p);
-                e = __ldg(ix.dir + p + 1);
-                if (s >= e) continue;
-                const uint64_t a = b - 1ull;
-                if (e - s <= 8u) {
-                    while (s < e && __ldg(ix.B + s) < a) ++s;
-                } else {
-                    s = lower_bound_u64(ix.B, s, e, a);
-                }
-                uint32_t f = s;
-                while (f < e && __ldg(ix.B + f) <= a + 2ull) ++f;
-                e = f;
-            }
-            if (s < e) scan_range<D, MODE, UNICOMP>(ix, ja, q, __ldg(ix.G + s), __ldg(ix.G + e));
+        for (int jj = D - 1; jj >= 1; --jj) {
+            const uint32_t cnt = 2u * kPow3[jj - 1];
+            if (j == jj && r >= cnt) { r -= cnt; j = jj - 1; }
         }
+        if (UNICOMP && !((q.odd >> j) & 1u)) continue;
+        // row offsets: dim j = +-1 (bit 0 of r), dims 1..j-1 in {-1,0,1} (base-3 digits of r>>1)
+        uint64_t b = key, p = ph;
+        uint32_t moves = (r & 1u) ? (1u << (j + 8)) : (1u << j);
+#pragma unroll
+        for (int i = 1; i < D; ++i) {
+            if (i == j) {
+                if (r & 1u) { b += ix.strides[i]; p += ix.pstride[i]; }
+                else { b -= ix.strides[i]; p -= ix.pstride[i]; }
+            }
+        }
+        uint32_t rest = r >> 1;
+#pragma unroll
+        for (int i = 1; i < D - 1; ++i) {
+            if (i >= j) break;
+            const uint32_t dl = rest % 3u;
+            rest /= 3u;
+            if (dl == 0u) { b -= ix.strides[i]; p -= ix.pstride[i]; moves |= 1u << i; }
+            else if (dl == 2u) { b += ix.strides[i]; p += ix.pstride[i]; moves |= 1u << (i + 8); }
+        }
+        if (moves & bad & 0xFFFFu) continue;   // a masked-out coordinate: the row is empty
+        ++q.probes;
+        uint32_t s, e;
+        if (dense) {                // p is the centre cell's key: its row is [p-1, p+1]
+            s = __ldg(ix.dir + p - 1);
+            e = __ldg(ix.dir + p + 2);
+        } else {                    // bounded search inside the prefix's range for [b-1, b+1]
+            s = __ldg(ix.dir + p);
+            e = __ldg(ix.dir + p + 1);
+            if (s >= e) continue;
+            const uint64_t a = b - 1ull;
+            if (e - s <= 8u) {
+                while (s < e && __ldg(ix.B + s) < a) ++s;
+            } else {
+                s = lower_bound_u64(ix.B, s, e, a);
+            }
+            uint32_t f = s;
+            while (f < e && __ldg(ix.B + f) <= a + 2ull) ++f;
+            e = f;
+        }
+        if (s < e) scan_range<D, MODE, UNICOMP>(ix, ja, q, __ldg(ix.G + s), __ldg(ix.G + e), 1u);
     }
 }
 
@@ -373,9 +323,9 @@ template <int D, int MODE, bool UNICOMP>
 __device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs &ja, uint32_t k,
                                             QueryState<D> &q, const TopTable &tt)
 {
+    const unsigned wmask = __activemask();   // the warp's active queries, converged at entry
     q.k = k;
     q.pid = __ldg(ix.A + k);
-    q.emitted = q.probes = q.tests = 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
         q.x[j] = __ldg(ix.X + (uint64_t)j * ix.n + k);
@@ -390,55 +340,65 @@ __device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs 
     const uint32_t cs = __ldg(ix.G + h), ce = __ldg(ix.G + h + 1);
 
     // ---- home cell: (p,p) once; unicomp: q after p in A-order, both orientations (R10)
-    emit<MODE, false>(ja, ja.include_self != 0, q.pid, q.pid, q.emitted);
+    if (q.sub == 0) emit<MODE, false>(ja, ja.include_self != 0, q.pid, q.pid, q.emitted);
     if constexpr (UNICOMP) {
-        scan_range<D, MODE, true>(ix, ja, q, k + 1, ce);
+        scan_range<D, MODE, true>(ix, ja, q, k + 1 + q.sub, ce, q.G);
     } else {
-        scan_range<D, MODE, false>(ix, ja, q, cs, k);
-        scan_range<D, MODE, false>(ix, ja, q, k + 1, ce);
+#pragma unroll 1
+        for (int part = 0; part < 2; ++part)
+            scan_range<D, MODE, false>(ix, ja, q, (part ? k + 1 : cs) + q.sub, part ? ce : k, q.G);
     }
-    uint32_t allow[D];
-    adjacent_masks<D>(ix, ja, q, allow);
+    const uint32_t bad = bad_moves<D, UNICOMP>(ix, ja, q);
+    __syncwarp(wmask);
     if (ix.search_mode == kSearchCellScan) {
-        search_cell_scan<D, MODE, UNICOMP>(ix, ja, q, h, allow, tt);
+        search_cell_scan<D, MODE, UNICOMP>(ix, ja, q, h, key, bad, tt, wmask);
         return;
     }
     // ---- home row: cells key-1 / key+1 (dims >= 1 equal); unicomp: only when c_0 is odd
     if (!UNICOMP || (q.c[0] & 1ull)) {
-        if (h > 0 && __ldg(ix.B + h - 1) == key - 1ull)
-            scan_range<D, MODE, UNICOMP>(ix, ja, q, __ldg(ix.G + h - 1), cs);
-        if (h + 1 < ix.nG && __ldg(ix.B + h + 1) == key + 1ull)
-            scan_range<D, MODE, UNICOMP>(ix, ja, q, ce, __ldg(ix.G + h + 2));
+#pragma unroll 1
+        for (uint32_t side = q.sub; side < 2u; side += q.G) {
+            uint32_t m0 = 0, m1 = 0;
+            if (side == 0 && h > 0 && __ldg(ix.B + h - 1) == key - 1ull) { m0 = __ldg(ix.G + h - 1); m1 = cs; }
+            if (side == 1 && h + 1 < ix.nG && __ldg(ix.B + h + 1) == key + 1ull) { m0 = ce; m1 = __ldg(ix.G + h + 2); }
+            scan_range<D, MODE, UNICOMP>(ix, ja, q, m0, m1, 1u);
+        }
     }
-    search_rows<D, MODE, UNICOMP>(ix, ja, q, key, allow);
+    __syncwarp(wmask);
+    search_rows<D, MODE, UNICOMP>(ix, ja, q, key, bad, wmask);
 }
 
 template <int D, int MODE, bool UNICOMP>
 __global__ void __launch_bounds__(kRefineThreads, kRefineMinBlocks)
 k_refine(const DevIndex ix, const JoinArgs ja)
 {
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t k;
-    bool active;
-    if constexpr (MODE == kCountQuery) {
-        // sample t: lane t%32 of run t/32; run r = the first 32 queries of block [r*32*step, ...),
-        // so a warp samples 32 consecutive (cell-coherent) queries
-        k = ja.q0 + (t >> 5) * (32u * ja.step) + (t & 31u);
-        active = t < ja.nsamples && k < ja.q1;
-    } else {
-        k = ja.q0 + t;
-        active = k < ja.q1;
-    }
     __shared__ TopTable tt;
     if (ix.search_mode == kSearchCellScan) {
         build_top_table<D>(ix, tt);
         __syncthreads();
     }
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t qi = t >> ja.lanes_log2;            // query slot of this lane's group
     QueryState<D> q;
+    q.G = 1u << ja.lanes_log2;
+    q.sub = t & (q.G - 1u);
     q.emitted = q.probes = q.tests = 0;
-    if (active) {
-        refine_query<D, MODE, UNICOMP>(ix, ja, k, q, tt);
-        if constexpr (MODE == kCountQuery) atomicAdd(ja.qbucket + t / ja.group, (unsigned long long)q.emitted);
+    uint32_t k;
+    bool active;
+    if constexpr (MODE == kCountQuery) {
+        // sample qi: lane qi%32 of run qi/32; run r = the first 32 queries of block [r*32*step, ...)
+        k = ja.q0 + (qi >> 5) * (32u * ja.step) + (qi & 31u);
+        active = qi < ja.nsamples && k < ja.q1;
+    } else {
+        k = ja.q0 + qi;
+        active = k < ja.q1;
+    }
+    if (active) refine_query<D, MODE, UNICOMP>(ix, ja, k, q, tt);
+    if constexpr (MODE == kCountQuery) {
+        // sum the group's partial counts (all lanes of a group share `active`)
+        uint32_t e = q.emitted;
+        for (uint32_t o = 1; o < q.G; o <<= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        if (active && q.sub == 0) atomicAdd(ja.qbucket + qi / ja.group, (unsigned long long)e);
     }
     // work counters: warp reduce, one atomic per warp
     unsigned long long p = q.probes, c = q.tests, em = q.emitted;

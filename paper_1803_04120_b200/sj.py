@@ -17,7 +17,7 @@ from typing import Optional
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsj.so")
+LIB_PATH = os.environ.get("SJ_LIB") or os.path.join(_PKG, "libsj.so")   # SJ_LIB: experiment override
 
 SJ_MAX_DIM = 6
 STATUS = {0: "SJ_OK", 1: "SJ_ERR_ARG", 2: "SJ_ERR_NONFINITE", 3: "SJ_ERR_DIM", 4: "SJ_ERR_KEY_OVERFLOW",
@@ -34,7 +34,7 @@ class BuildOpts(ctypes.Structure):
 class JoinOpts(ctypes.Structure):
     _fields_ = [("unicomp", i32), ("include_self", i32), ("batch_capacity_pairs", u64),
                 ("min_batches", i32), ("n_streams", i32), ("result_on_host", i32),
-                ("query_begin", u64), ("query_end", u64), ("use_masks", i32)]
+                ("query_begin", u64), ("query_end", u64), ("use_masks", i32), ("lanes_per_query", i32)]
 
 
 class Stats(ctypes.Structure):
@@ -329,12 +329,14 @@ class Result:
 def self_join(index: Index, unicomp: bool = True, include_self: bool = True,
               batch_capacity_pairs: Optional[int] = None, min_batches: Optional[int] = None,
               n_streams: Optional[int] = None, result_on_host: bool = False,
-              query_begin: int = 0, query_end: int = 0, use_masks: bool = True) -> Result:
+              query_begin: int = 0, query_end: int = 0, use_masks: bool = True,
+              lanes_per_query: int = 0) -> Result:
     """sj_self_join over the index; see include/sj.h for the option semantics."""
     L = load_library()
     o = join_opts(unicomp=unicomp, include_self=include_self, batch_capacity_pairs=batch_capacity_pairs,
                   min_batches=min_batches, n_streams=n_streams, result_on_host=result_on_host,
-                  query_begin=query_begin, query_end=query_end, use_masks=use_masks)
+                  query_begin=query_begin, query_end=query_end, use_masks=use_masks,
+                  lanes_per_query=lanes_per_query)
     h = ctypes.c_void_p()
     _check(L.sj_self_join(index.handle, ctypes.byref(o), ctypes.byref(h)))
     r = Result(h.value)
@@ -343,11 +345,12 @@ def self_join(index: Index, unicomp: bool = True, include_self: bool = True,
 
 
 def neighbor_counts(index: Index, unicomp: bool = True, include_self: bool = True,
-                    query_begin: int = 0, query_end: int = 0, out=None):
+                    query_begin: int = 0, query_end: int = 0, out=None, lanes_per_query: int = 0):
     """sj_neighbor_counts -> (torch uint32 counts by original id on the device, total)."""
     import torch
     L = load_library()
-    o = join_opts(unicomp=unicomp, include_self=include_self, query_begin=query_begin, query_end=query_end)
+    o = join_opts(unicomp=unicomp, include_self=include_self, query_begin=query_begin, query_end=query_end,
+                  lanes_per_query=lanes_per_query)
     if out is None:
         out = torch.empty(index.n, dtype=torch.uint32, device=f"cuda:{index.device}")
     tot = u64()

@@ -44,7 +44,7 @@ def test_abi_struct_sizes_match_header(sj):
 def test_defaults(sj):
     o = sj.sj.join_opts()
     assert (o.unicomp, o.include_self, o.batch_capacity_pairs, o.min_batches, o.n_streams,
-            o.result_on_host, o.use_masks) == (1, 1, 1 << 28, 3, 3, 0, 1)
+            o.result_on_host, o.use_masks, o.lanes_per_query) == (1, 1, 1 << 28, 3, 3, 0, 1, 0)
 
 
 def test_argument_errors_before_cuda(sj):

@@ -327,3 +327,19 @@ def test_prefix_directory_definition(sj, d, n, eps):
     want = np.searchsorted(Bn, np.arange(P + 1), side="left")
     assert np.array_equal(arr["dir"].cpu().numpy().astype(np.int64), want)
     assert np.array_equal(sj.self_join(idx).to_numpy(), oracle.brute_force(pts, eps)) if n <= 8000 else True
+
+
+@pytest.mark.parametrize("d,n,eps", [(2, 4000, 2.0), (3, 5000, 6.0), (4, 6000, 12.0), (6, 5000, 25.0),
+                                     (6, 4000, 60.0), (5, 3000, 8.0)])
+def test_lanes_per_query_invariance(sj, d, n, eps):
+    """S is independent of how many lanes cooperate on a query (G = 1..32), in every search
+    mode the index picks (dense rows / cell scan / rows), unicomp and full."""
+    pts = datagen.uniform(n, d, seed=5 * n + d)
+    want = oracle.brute_force(pts, eps)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    for G in (1, 2, 4, 8, 16, 32):
+        for unicomp in (True, False):
+            got = sj.self_join(idx, lanes_per_query=G, unicomp=unicomp).to_numpy()
+            assert np.array_equal(got, want), (G, unicomp)
+        cnt, tot = sj.neighbor_counts(idx, lanes_per_query=G)
+        assert tot == len(want)
