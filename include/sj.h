@@ -97,7 +97,8 @@ typedef struct {
     float refine_max_ms;         /* longest single refine launch                                   */
     float total_ms;              /* host wall time of sj_self_join                                 */
     uint32_t refine_launches;    /* refine kernel launches (incl. retries)                         */
-    uint32_t reserved;
+    float refine_span_ms;        /* device time from the first refine launch's start to the last
+                                    one's end (batches on different streams overlap)              */
 } sj_stats;
 
 typedef struct {

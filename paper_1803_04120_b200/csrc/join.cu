@@ -231,7 +231,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     const uint64_t nbk = sm.ns ? (sm.ns + group - 1) / group : 0;
     const size_t kSlotsBytes = sizeof(Slot) * 64;
     const size_t slot_need = kWorkBytes + kSlotsBytes + 8 * (size_t)(nbk + 1);
-    CtxGuard cg{acquire_ctx(idx->device, S, 2 * S + 2, slot_need)};
+    CtxGuard cg{acquire_ctx(idx->device, S, 2 * S + 4, slot_need)};
     DevCtx &cx = *cg.c;
     cudaStream_t s0 = cx.streams[0];
     char *dbase = static_cast<char *>(cx.d_slots), *hbase = static_cast<char *>(cx.h_slots);
@@ -281,8 +281,10 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         const size_t nb = cuts.size() - 1;
         tr.mark("plan");
 
-        float refine_ms = 0, refine_max = 0;
+        float refine_ms = 0, refine_max = 0, refine_span = 0;
         uint32_t launches = 0;
+        cudaEvent_t ev_span0 = cx.events[2 * S + 2];   // first refine launch start (stream 0)
+        bool span_started = false;
         auto run_batch = [&](uint64_t a, uint64_t b, uint64_t *buf, uint64_t cap, Slot *dslot, cudaStream_t s,
                              cudaEvent_t e0, cudaEvent_t e1) {
             SJ_CUDA(cudaMemsetAsync(dslot, 0, sizeof(Slot), s));
@@ -293,16 +295,22 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             ja.overflow = &dslot->overflow;
             ja.q0 = (uint32_t)a;
             ja.q1 = (uint32_t)b;
+            if (!span_started) {
+                SJ_CUDA(cudaEventRecord(ev_span0, s));
+                span_started = true;
+            }
             SJ_CUDA(cudaEventRecord(e0, s));
             launch_refine<kEmit>(ix, ja, o.unicomp != 0, (uint32_t)(b - a), s);
             SJ_CUDA(cudaEventRecord(e1, s));
             ++launches;
         };
         auto add_time = [&](cudaEvent_t e0, cudaEvent_t e1) {
-            float ms = 0;
+            float ms = 0, span = 0;
             SJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            SJ_CUDA(cudaEventElapsedTime(&span, ev_span0, e1));
             refine_ms += ms;
             refine_max = std::max(refine_max, ms);
+            refine_span = std::max(refine_span, span);
         };
 
         if (!o.result_on_host) {
@@ -426,6 +434,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         stats.refine_ms = refine_ms;
         stats.refine_max_ms = refine_max;
         stats.refine_launches = launches;
+        stats.refine_span_ms = refine_span;
         tr.mark("stats");
     } catch (...) {
         for (auto s : cx.streams) cudaStreamSynchronize(s);

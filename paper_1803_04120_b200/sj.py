@@ -41,10 +41,10 @@ class Stats(ctypes.Structure):
     _fields_ = [("pairs", u64), ("cells_probed", u64), ("candidates_tested", u64),
                 ("estimated_pairs", u64), ("batches", u32), ("retries", u32),
                 ("estimate_ms", f32), ("refine_ms", f32), ("refine_max_ms", f32), ("total_ms", f32),
-                ("refine_launches", u32), ("reserved", u32)]
+                ("refine_launches", u32), ("refine_span_ms", f32)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 class IndexView(ctypes.Structure):

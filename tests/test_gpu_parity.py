@@ -343,3 +343,37 @@ def test_lanes_per_query_invariance(sj, d, n, eps):
             assert np.array_equal(got, want), (G, unicomp)
         cnt, tot = sj.neighbor_counts(idx, lanes_per_query=G)
         assert tot == len(want)
+
+
+# ------------------------------------------------------------------ full-size configs C3, C4, C5
+@pytest.mark.parametrize("eps", [16.0, 24.0])
+def test_c3_eps_sweep_sampled_rows(sj, eps):
+    """C3 (Syn-6D 2M): eps=16 (~1 buffer of 2^28 pairs) and eps=24 (~9.5 buffers, 20 GB):
+    sampled rows exact, batching engaged (k > 3 at eps=24), total within 1% of the P4
+    expectation."""
+    pts = datagen.uniform_config("C3", 6)
+    res = _sampled_rows_check(sj, pts, eps, nsample=24, seed=int(eps))
+    exp = oracle.expected_pairs_uniform(len(pts), 6, eps)
+    assert abs(res.n_pairs - exp) / exp < 0.01
+    if eps == 24.0:
+        assert res.n_batches > 3
+
+
+@pytest.mark.parametrize("d,eps", [(2, 0.005), (3, 0.1)])
+def test_c4_skewed_sampled_rows(sj, d, eps):
+    """C4 (skewed 15.2M-point cloud, real-data stand-in): sampled rows exact, including rows of
+    queries from the densest cells (heavy skew tail)."""
+    pts = datagen.skewed(15_228_633, d)
+    _sampled_rows_check(sj, pts, eps, nsample=48, seed=d)
+
+
+@pytest.mark.parametrize("d,eps", [(4, 2.0), (6, 8.0)])
+def test_c5_16m_sampled_rows_and_shards(sj, d, eps):
+    """C5 (16M uniform): sampled rows exact on the full join, and the union of 4 query shards
+    has exactly the full join's size (what each GPU of the scaling run computes)."""
+    pts = datagen.uniform_config("C5", d)
+    res = _sampled_rows_check(sj, pts, eps, nsample=24, seed=d)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    cuts = np.linspace(0, len(pts), 5).astype(np.int64)
+    tot = sum(sj.self_join(idx, query_begin=int(a), query_end=int(b)).n_pairs for a, b in zip(cuts[:-1], cuts[1:]))
+    assert tot == res.n_pairs
