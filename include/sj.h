@@ -83,6 +83,8 @@ typedef struct {
     int lanes_per_query;           /* 0 (default): chosen per index; else 1,2,4,8,16 or 32 GPU lanes
                                       cooperate on one query (a tuning / testing knob; S is
                                       independent of it)                                         */
+    int dense_cells;               /* 1 (default): queries of populous cells (>= 16 points) run one
+                                      warp per 32 queries with warp-buffered emission; 0: off     */
 } sj_join_opts;
 
 typedef struct {

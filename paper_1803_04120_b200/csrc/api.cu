@@ -190,6 +190,7 @@ void sj_join_opts_default(sj_join_opts *o)
     o->query_end = 0;
     o->use_masks = 1;
     o->lanes_per_query = 0;
+    o->dense_cells = 1;
 }
 
 sj_status sj_build_index(const double *points, uint64_t n, int d, double eps, const sj_build_opts *opts,

@@ -398,6 +398,7 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
         idx->view = v;
         idx->dev = ix;
         build_directory(idx, s);
+        build_dense_tasks(idx, s);
         ev.rec(6, s);
         SJ_CUDA(cudaStreamSynchronize(s));
         tr.mark("compact+dir (synced)");
@@ -429,7 +430,54 @@ k_dir_hist(const uint64_t *__restrict__ B, uint32_t nG, uint64_t div, double inv
     if (h >= nG) return;
     atomicAdd(hist + div_small_quot(B[h], div, inv), 1u);
 }
+__global__ void __launch_bounds__(kThreads)
+k_dense_count(const uint32_t *__restrict__ G, uint32_t nG, uint32_t T, uint32_t *__restrict__ cnt)
+{
+    const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= nG) return;
+    const uint32_t n = G[h + 1] - G[h];
+    cnt[h] = n >= T ? (n + 31u) / 32u : 0u;
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_dense_fill(const uint32_t *__restrict__ G, uint32_t nG, uint32_t T, const uint32_t *__restrict__ off,
+             uint32_t *__restrict__ tasks)
+{
+    const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= nG) return;
+    const uint32_t s = G[h], n = G[h + 1] - s;
+    if (n < T) return;
+    const uint32_t o = off[h];
+    for (uint32_t i = 0; i < (n + 31u) / 32u; ++i) tasks[o + i] = s + 32u * i;
+}
 }  // namespace
+
+// Dense-cell task list (a property of the index): every cell with >= T points is cut into tasks
+// of <= 32 consecutive queries, one warp each in k_refine_dense.
+constexpr uint32_t kDenseT = 16;
+void build_dense_tasks(sj_index *idx, cudaStream_t s)
+{
+    DevIndex &ix = idx->dev;
+    const uint32_t nG = ix.nG;
+    Scratch<uint32_t> cnt((size_t)nG + 1, s), off((size_t)nG + 1, s);
+    SJ_CUDA(cudaMemsetAsync(cnt.p + nG, 0, sizeof(uint32_t), s));
+    k_dense_count<<<(nG + kThreads - 1) / kThreads, kThreads, 0, s>>>(ix.G, nG, kDenseT, cnt.p);
+    SJ_LAUNCHED();
+    exclusive_scan_u32(cnt.p, off.p, (uint64_t)nG + 1, s);
+    uint32_t total = 0;
+    SJ_CUDA(cudaMemcpyAsync(&total, off.p + nG, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaStreamSynchronize(s));
+    uint32_t *tasks = nullptr;
+    if (total) {
+        tasks = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * total, s));
+        idx->bufs[idx->nbufs++] = tasks;
+        k_dense_fill<<<(nG + kThreads - 1) / kThreads, kThreads, 0, s>>>(ix.G, nG, kDenseT, off.p, tasks);
+        SJ_LAUNCHED();
+    }
+    ix.dense_tasks = tasks;
+    ix.n_dense_tasks = total;
+    ix.dense_T = kDenseT;
+}
 
 // Prefix directory: the largest k such that the number of
 // top-k coordinate prefixes P_k = prod_{j >= d-k} |g_j| stays <= max(4|G|, 2^16), so the
@@ -543,6 +591,7 @@ sj_index *import_index_impl(const sj_index_view &src, int device)
         idx->view = v;
         idx->dev = ix;
         build_directory(idx, s);
+        build_dense_tasks(idx, s);
         SJ_CUDA(cudaStreamSynchronize(s));
     } catch (...) {
         cudaStreamDestroy(s);

@@ -20,6 +20,35 @@ namespace sj {
 
 namespace {
 
+void launch_dense(const DevIndex &ix, const JoinArgs &ja, bool unicomp, cudaStream_t s)
+{
+    if (!ja.dense_T || ix.n_dense_tasks == 0) return;
+    const dim3 grid((ix.n_dense_tasks + kDenseWarps - 1) / kDenseWarps), block(32 * kDenseWarps);
+    const size_t smem = sizeof(uint64_t) * kDenseWarps * kWarpBufPairs;
+#define SJ_DENSE_CASE(DD)                                                                              \
+    case DD:                                                                                           \
+        if (unicomp) {                                                                                 \
+            SJ_CUDA(cudaFuncSetAttribute(k_refine_dense<DD, true>,                                     \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
+            k_refine_dense<DD, true><<<grid, block, smem, s>>>(ix, ja);                               \
+        } else {                                                                                       \
+            SJ_CUDA(cudaFuncSetAttribute(k_refine_dense<DD, false>,                                    \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
+            k_refine_dense<DD, false><<<grid, block, smem, s>>>(ix, ja);                              \
+        }                                                                                              \
+        break;
+    switch (ix.d) {
+        SJ_DENSE_CASE(2)
+        SJ_DENSE_CASE(3)
+        SJ_DENSE_CASE(4)
+        SJ_DENSE_CASE(5)
+        SJ_DENSE_CASE(6)
+    default: fail(SJ_ERR_DIM, "bad d");
+    }
+#undef SJ_DENSE_CASE
+    SJ_LAUNCHED();
+}
+
 template <int MODE>
 void launch_refine(const DevIndex &ix, const JoinArgs &ja, bool unicomp, uint32_t nqueries, cudaStream_t s)
 {
@@ -299,8 +328,14 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 SJ_CUDA(cudaEventRecord(ev_span0, s));
                 span_started = true;
             }
+            if (o.dense_cells && ix.n_dense_tasks) {
+                ja.dense_T = ix.dense_T;
+                ja.dense_tasks = ix.dense_tasks;
+                ja.n_dense_tasks = ix.n_dense_tasks;
+            }
             SJ_CUDA(cudaEventRecord(e0, s));
             launch_refine<kEmit>(ix, ja, o.unicomp != 0, (uint32_t)(b - a), s);
+            launch_dense(ix, ja, o.unicomp != 0, s);
             SJ_CUDA(cudaEventRecord(e1, s));
             ++launches;
         };
@@ -369,6 +404,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(o.batch_capacity_pairs,
                                                                           maxest + maxest / 4 + 65536));
             std::vector<uint64_t *> staging(S, nullptr);
+            std::vector<uint64_t> scap(S, cap);           // per-stream staging capacity
             struct StagingGuard {
                 std::vector<uint64_t *> &v; DevCtx &cx;
                 ~StagingGuard() { for (size_t i = 0; i < v.size(); ++i) if (v[i]) dev_free(v[i], cx.streams[i]); }
@@ -382,7 +418,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 auto r = pending.front();
                 pending.pop_front();
                 inflight[i] = r;
-                run_batch(r.first, r.second, staging[i], cap, dslots + i, cx.streams[i], cx.events[2 + 2 * i],
+                run_batch(r.first, r.second, staging[i], scap[i], dslots + i, cx.streams[i], cx.events[2 + 2 * i],
                           cx.events[3 + 2 * i]);
                 SJ_CUDA(cudaMemcpyAsync(hslots + i, dslots + i, sizeof(Slot), cudaMemcpyDeviceToHost,
                                         cx.streams[i]));
@@ -394,18 +430,24 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 order.pop_front();
                 // the cursor copy follows the kernel on stream i; the previous D2H on this stream
                 // precedes the kernel, so a stream sync here waits for exactly that batch.
-                SJ_CUDA(cudaEventSynchronize(cx.events[3 + 2 * i]));
                 SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
                 add_time(cx.events[2 + 2 * i], cx.events[3 + 2 * i]);
                 const uint64_t n = hslots[i].cursor;
                 const auto r = inflight[i];
-                if (n > cap) {
-                    // overflow: split the query range and re-run both halves first
+                if (n > scap[i]) {
                     ++stats.retries;
-                    if (r.second - r.first < 2) fail(SJ_ERR_NOMEM, "a single query exceeds the batch capacity");
-                    const uint64_t mid = r.first + (r.second - r.first) / 2;
-                    pending.emplace_front(mid, r.second);
-                    pending.emplace_front(r.first, mid);
+                    if (r.second - r.first < 2) {
+                        // one query emits more than the staging buffer holds: grow it to fit
+                        dev_free(staging[i], cx.streams[i]);
+                        staging[i] = dalloc<uint64_t>(n, cx.streams[i]);
+                        scap[i] = n;
+                        pending.emplace_front(r);
+                    } else {
+                        // overflow: split the query range and re-run both halves first
+                        const uint64_t mid = r.first + (r.second - r.first) / 2;
+                        pending.emplace_front(mid, r.second);
+                        pending.emplace_front(r.first, mid);
+                    }
                 } else {
                     sj_batch bt;
                     bt.on_device = 0;

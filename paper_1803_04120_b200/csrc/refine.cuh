@@ -49,8 +49,20 @@ struct JoinArgs {
     uint32_t q0, q1;               // A-position range of the queries
     uint32_t step, nsamples;       // kCountQuery: sample t = query q0 + (t/32)*32*step + t%32
     uint32_t lanes_log2;           // G = 1 << lanes_log2 lanes cooperate on one query
+    uint32_t dense_T;              // kEmit: queries of cells with >= dense_T points go to the
+                                   // warp-per-task dense kernel (0 = off)
+    const uint32_t *dense_tasks;   // start A-position of each dense task (<= 32 queries of a cell)
+    uint32_t n_dense_tasks;
     int include_self;
     int use_masks;
+};
+
+// Per-warp emission buffer of the dense kernel (shared memory): hits are appended at warp-uniform
+// points; one atomicAdd on the batch cursor per flush of up to kWarpBufPairs pairs.
+constexpr int kWarpBufPairs = 1024;
+struct WarpBuf {
+    uint64_t *buf;     // [kWarpBufPairs] in shared memory
+    uint32_t cnt;      // warp-uniform fill level (kept identical in every lane)
 };
 
 constexpr int kRefineThreads = 256;
@@ -119,12 +131,76 @@ __device__ __forceinline__ void emit(const JoinArgs &ja, bool hit, uint32_t pid,
     }
 }
 
+// Warp-converged emission into the per-warp buffer (dense kernel only: every lane of `mask`
+// executes this at the same candidate).  Flush = one atomicAdd + coalesced copy-out.
+__device__ __forceinline__ void warpbuf_flush(const JoinArgs &ja, WarpBuf &wb, unsigned mask)
+{
+    if (wb.cnt == 0) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(ja.cursor, (unsigned long long)wb.cnt);
+    base = __shfl_sync(mask, base, leader);
+    const uint32_t nl = __popc(mask), rank = __popc(mask & ((1u << lane) - 1u));
+    for (uint32_t i = rank; i < wb.cnt; i += nl) {
+        const unsigned long long pos = base + i;
+        if (pos < ja.cap) ja.out[pos] = wb.buf[i];
+        else atomicOr(ja.overflow, 1u);
+    }
+    __syncwarp(mask);
+    wb.cnt = 0;
+}
+
+template <bool BOTH>
+__device__ __forceinline__ void emit_buffered(const JoinArgs &ja, WarpBuf &wb, unsigned mask, bool hit,
+                                              uint32_t pid, uint32_t qid, uint32_t &emitted)
+{
+    const unsigned hits = __ballot_sync(mask, hit);
+    if (hits == 0u) return;
+    constexpr uint32_t per = BOTH ? 2u : 1u;
+    const uint32_t n = __popc(hits) * per;
+    if (wb.cnt + n > (uint32_t)kWarpBufPairs) warpbuf_flush(ja, wb, mask);
+    if (hit) {
+        const int lane = threadIdx.x & 31;
+        const uint32_t pos = wb.cnt + __popc(hits & ((1u << lane) - 1u)) * per;
+        wb.buf[pos] = ((uint64_t)pid << 32) | qid;
+        if (BOTH) wb.buf[pos + 1] = ((uint64_t)qid << 32) | pid;
+        emitted += per;
+    }
+    __syncwarp(mask);
+    wb.cnt += n;
+}
+
 // Test the points at A-positions m0, m0+stride, ... < m1 against the query.
-template <int D, int MODE, bool BOTH>
+// DENSE (dense kernel): the loop bounds are warp-uniform; HOME selects the home-cell predicate
+// (unicomp: m > k; full: m != k) and hits go to the per-warp buffer.
+template <int D, int MODE, bool BOTH, bool DENSE = false, bool HOME = false>
 __device__ __forceinline__ void scan_range(const DevIndex &ix, const JoinArgs &ja, QueryState<D> &q, uint32_t m0,
-                                           uint32_t m1, uint32_t stride)
+                                           uint32_t m1, uint32_t stride, WarpBuf *wb = nullptr,
+                                           unsigned wmask = 0u)
 {
     const uint32_t n = ix.n;
+    if constexpr (DENSE) {
+        for (uint32_t m = m0; m < m1; ++m) {
+            double s;
+            {
+                const double t = __dsub_rn(q.x[0], __ldg(ix.X + m));
+                s = __dmul_rn(t, t);
+            }
+#pragma unroll
+            for (int j = 1; j < D; ++j) {
+                const double t = __dsub_rn(q.x[j], __ldg(ix.X + (uint64_t)j * n + m));
+                s = __dadd_rn(s, __dmul_rn(t, t));
+            }
+            bool ok = true;
+            if (HOME) ok = BOTH ? (m > q.k) : (m != q.k);
+            q.tests += ok ? 1u : 0u;
+            const bool hit = ok && s <= ix.eps2;
+            const uint32_t qid = __ldg(ix.A + m);      // uniform address: one broadcast load
+            emit_buffered<BOTH>(ja, *wb, wmask, hit, q.pid, qid, q.emitted);
+        }
+        return;
+    }
     for (uint32_t m = m0; m < m1; m += stride) {
         double s;
         {
@@ -201,10 +277,10 @@ __device__ __forceinline__ uint32_t bad_moves(const DevIndex &ix, const JoinArgs
 // greedily from the top low dimension (delta_i = sign(D) if |D| > lowR[i], else 0) -- no division.
 // Lanes of a query's group take offsets t = sub, sub+G, ...  Covers every neighbour cell except
 // the home cell.
-template <int D, int MODE, bool UNICOMP>
+template <int D, int MODE, bool UNICOMP, bool DENSE = false>
 __device__ __forceinline__ void search_cell_scan(const DevIndex &ix, const JoinArgs &ja, QueryState<D> &q,
                                                  uint32_t h, uint64_t key, uint32_t bad, const TopTable &tt,
-                                                 unsigned wmask)
+                                                 unsigned wmask, WarpBuf *wb = nullptr)
 {
     const int L = D - ix.dir_k;     // low dimensions 0..L-1 are not in the directory prefix
     uint64_t ph = 0;
@@ -242,7 +318,7 @@ __device__ __forceinline__ void search_cell_scan(const DevIndex &ix, const JoinA
             if (dlt != 0) continue;                      // not representable: not adjacent
             const int j = jtop >= 0 ? jtop : jlow;
             if (UNICOMP && !((q.odd >> j) & 1u)) continue;
-            scan_range<D, MODE, UNICOMP>(ix, ja, q, __ldg(ix.G + hh), __ldg(ix.G + hh + 1), 1u);
+            scan_range<D, MODE, UNICOMP, DENSE>(ix, ja, q, __ldg(ix.G + hh), __ldg(ix.G + hh + 1), 1u, wb, wmask);
         }
     }
 }
@@ -252,9 +328,9 @@ __device__ __forceinline__ void search_cell_scan(const DevIndex &ix, const JoinA
 // one contiguous A-range).  Unicomp: only when c_j is odd (reading R13).  Each row is looked up
 // in the prefix directory, then (kSearchRows) by a search bounded to that prefix's range.  The
 // rows of all j are numbered 0..3^(D-1)-2 (j = D-1 first) and dealt to the group's lanes.
-template <int D, int MODE, bool UNICOMP>
+template <int D, int MODE, bool UNICOMP, bool DENSE = false>
 __device__ __forceinline__ void search_rows(const DevIndex &ix, const JoinArgs &ja, QueryState<D> &q,
-                                            uint64_t key, uint32_t bad, unsigned wmask)
+                                            uint64_t key, uint32_t bad, unsigned wmask, WarpBuf *wb = nullptr)
 {
     uint64_t ph = 0;
 #pragma unroll
@@ -315,15 +391,23 @@ __device__ __forceinline__ void search_rows(const DevIndex &ix, const JoinArgs &
             while (f < e && __ldg(ix.B + f) <= a + 2ull) ++f;
             e = f;
         }
-        if (s < e) scan_range<D, MODE, UNICOMP>(ix, ja, q, __ldg(ix.G + s), __ldg(ix.G + e), 1u);
+        if (s < e) scan_range<D, MODE, UNICOMP, DENSE>(ix, ja, q, __ldg(ix.G + s), __ldg(ix.G + e), 1u, wb, wmask);
     }
 }
 
-template <int D, int MODE, bool UNICOMP>
+template <int D, int MODE, bool UNICOMP, bool DENSE = false>
 __device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs &ja, uint32_t k,
-                                            QueryState<D> &q, const TopTable &tt)
+                                            QueryState<D> &q, const TopTable &tt, WarpBuf *wb = nullptr)
 {
-    const unsigned wmask = __activemask();   // the warp's active queries, converged at entry
+    const uint32_t h = __ldg(ix.pcell + k);
+    const uint32_t cs = __ldg(ix.G + h), ce = __ldg(ix.G + h + 1);
+    if constexpr (MODE == kEmit && !DENSE) {
+        // queries of populous cells are handled by the warp-per-task dense kernel
+        if (ja.dense_T && ce - cs >= ja.dense_T) return;
+    }
+    // The warp's remaining active queries, taken AFTER the only divergent early exit: every
+    // __syncwarp(wmask) below must be reached by all lanes of wmask.
+    const unsigned wmask = __activemask();
     q.k = k;
     q.pid = __ldg(ix.A + k);
 #pragma unroll
@@ -335,23 +419,26 @@ __device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs 
     q.odd = 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) q.odd |= (uint32_t)(q.c[j] & 1ull) << j;
-    const uint32_t h = __ldg(ix.pcell + k);
     const uint64_t key = __ldg(ix.B + h);
-    const uint32_t cs = __ldg(ix.G + h), ce = __ldg(ix.G + h + 1);
 
     // ---- home cell: (p,p) once; unicomp: q after p in A-order, both orientations (R10)
-    if (q.sub == 0) emit<MODE, false>(ja, ja.include_self != 0, q.pid, q.pid, q.emitted);
-    if constexpr (UNICOMP) {
-        scan_range<D, MODE, true>(ix, ja, q, k + 1 + q.sub, ce, q.G);
+    if constexpr (DENSE) {
+        emit_buffered<false>(ja, *wb, wmask, ja.include_self != 0, q.pid, q.pid, q.emitted);
+        scan_range<D, MODE, UNICOMP, true, true>(ix, ja, q, cs, ce, 1u, wb, wmask);
     } else {
+        if (q.sub == 0) emit<MODE, false>(ja, ja.include_self != 0, q.pid, q.pid, q.emitted);
+        if constexpr (UNICOMP) {
+            scan_range<D, MODE, true>(ix, ja, q, k + 1 + q.sub, ce, q.G);
+        } else {
 #pragma unroll 1
-        for (int part = 0; part < 2; ++part)
-            scan_range<D, MODE, false>(ix, ja, q, (part ? k + 1 : cs) + q.sub, part ? ce : k, q.G);
+            for (int part = 0; part < 2; ++part)
+                scan_range<D, MODE, false>(ix, ja, q, (part ? k + 1 : cs) + q.sub, part ? ce : k, q.G);
+        }
     }
     const uint32_t bad = bad_moves<D, UNICOMP>(ix, ja, q);
     __syncwarp(wmask);
     if (ix.search_mode == kSearchCellScan) {
-        search_cell_scan<D, MODE, UNICOMP>(ix, ja, q, h, key, bad, tt, wmask);
+        search_cell_scan<D, MODE, UNICOMP, DENSE>(ix, ja, q, h, key, bad, tt, wmask, wb);
         return;
     }
     // ---- home row: cells key-1 / key+1 (dims >= 1 equal); unicomp: only when c_0 is odd
@@ -361,11 +448,58 @@ __device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs 
             uint32_t m0 = 0, m1 = 0;
             if (side == 0 && h > 0 && __ldg(ix.B + h - 1) == key - 1ull) { m0 = __ldg(ix.G + h - 1); m1 = cs; }
             if (side == 1 && h + 1 < ix.nG && __ldg(ix.B + h + 1) == key + 1ull) { m0 = ce; m1 = __ldg(ix.G + h + 2); }
-            scan_range<D, MODE, UNICOMP>(ix, ja, q, m0, m1, 1u);
+            scan_range<D, MODE, UNICOMP, DENSE>(ix, ja, q, m0, m1, 1u, wb, wmask);
         }
     }
     __syncwarp(wmask);
-    search_rows<D, MODE, UNICOMP>(ix, ja, q, key, bad, wmask);
+    search_rows<D, MODE, UNICOMP, DENSE>(ix, ja, q, key, bad, wmask, wb);
+}
+
+// Dense kernel (kEmit): one warp per task = up to 32 consecutive queries of one populous cell
+// (>= dense_T points).  All lanes share the home cell, so the whole neighbour enumeration and every
+// candidate loop are warp-uniform: candidates are broadcast loads, hits go through the per-warp
+// shared-memory buffer (one cursor atomic per flush instead of one per candidate step).
+constexpr int kDenseWarps = 8;
+template <int D, bool UNICOMP>
+__global__ void __launch_bounds__(32 * kDenseWarps, 2)
+k_refine_dense(const DevIndex ix, const JoinArgs ja)
+{
+    __shared__ TopTable tt;
+    extern __shared__ __align__(16) uint64_t s_buf[];     // [kDenseWarps][kWarpBufPairs]
+    if (ix.search_mode == kSearchCellScan) {
+        build_top_table<D>(ix, tt);
+        __syncthreads();
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t task = blockIdx.x * kDenseWarps + warp;
+    if (task >= ja.n_dense_tasks) return;
+    const uint32_t start = __ldg(ja.dense_tasks + task);
+    const uint32_t h = __ldg(ix.pcell + start);
+    const uint32_t end = min(start + 32u, __ldg(ix.G + h + 1));
+    const uint32_t a = max(start, ja.q0), b = min(end, ja.q1);
+    if (a >= b) return;                                // task outside this batch
+    WarpBuf wb{s_buf + (size_t)warp * kWarpBufPairs, 0u};
+    QueryState<D> q;
+    q.G = 1u;
+    q.sub = 0u;
+    q.emitted = q.probes = q.tests = 0;
+    const uint32_t k = a + lane;
+    if (k < b) {
+        refine_query<D, kEmit, UNICOMP, true>(ix, ja, k, q, tt, &wb);
+        warpbuf_flush(ja, wb, __activemask());
+    }
+    unsigned long long p = q.probes, c = q.tests, em = q.emitted;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        p += __shfl_xor_sync(0xffffffffu, p, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+        em += __shfl_xor_sync(0xffffffffu, em, o);
+    }
+    if (lane == 0 && ja.work) {
+        atomicAdd(ja.work + 0, p);
+        atomicAdd(ja.work + 1, c);
+        atomicAdd(ja.work + 2, em);
+    }
 }
 
 template <int D, int MODE, bool UNICOMP>

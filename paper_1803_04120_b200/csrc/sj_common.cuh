@@ -100,6 +100,11 @@ struct DevIndex {
     uint32_t dir_ntop;           // 3^dir_k top-prefix offsets
     double inv_cpd[SJ_MAX_DIM];  // 1/|g_j| (fast exact divmod of low key parts, see refine.cuh)
     int64_t lowR[SJ_MAX_DIM + 1];// lowR[i] = sum_{m<i} stride_m: largest |key offset| of dims < i
+    // dense-cell tasks: every cell with >= dense_T points is cut into tasks of <= 32 consecutive
+    // queries (start A-positions), processed one warp per task by k_refine_dense
+    const uint32_t *dense_tasks;
+    uint32_t n_dense_tasks;
+    uint32_t dense_T;
 };
 
 enum SearchMode { kSearchDenseRows = 0, kSearchCellScan = 1, kSearchRows = 2 };
@@ -111,7 +116,7 @@ struct sj_index {
     int device = 0;
     sj_index_view view{};        // geometry + device pointers (exported as is)
     sj::DevIndex dev{};          // same, in kernel form
-    void *bufs[8] = {nullptr};   // owned device allocations
+    void *bufs[12] = {nullptr};  // owned device allocations
     int nbufs = 0;
 };
 
@@ -153,6 +158,7 @@ struct CtxGuard {
 
 // index_build.cu
 void build_directory(sj_index *idx, cudaStream_t s);
+void build_dense_tasks(sj_index *idx, cudaStream_t s);
 sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &o);
 sj_index *import_index_impl(const sj_index_view &v, int device);
 void free_index_impl(sj_index *idx);

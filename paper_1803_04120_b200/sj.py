@@ -34,7 +34,8 @@ class BuildOpts(ctypes.Structure):
 class JoinOpts(ctypes.Structure):
     _fields_ = [("unicomp", i32), ("include_self", i32), ("batch_capacity_pairs", u64),
                 ("min_batches", i32), ("n_streams", i32), ("result_on_host", i32),
-                ("query_begin", u64), ("query_end", u64), ("use_masks", i32), ("lanes_per_query", i32)]
+                ("query_begin", u64), ("query_end", u64), ("use_masks", i32), ("lanes_per_query", i32),
+                ("dense_cells", i32)]
 
 
 class Stats(ctypes.Structure):
@@ -330,13 +331,13 @@ def self_join(index: Index, unicomp: bool = True, include_self: bool = True,
               batch_capacity_pairs: Optional[int] = None, min_batches: Optional[int] = None,
               n_streams: Optional[int] = None, result_on_host: bool = False,
               query_begin: int = 0, query_end: int = 0, use_masks: bool = True,
-              lanes_per_query: int = 0) -> Result:
+              lanes_per_query: int = 0, dense_cells: bool = True) -> Result:
     """sj_self_join over the index; see include/sj.h for the option semantics."""
     L = load_library()
     o = join_opts(unicomp=unicomp, include_self=include_self, batch_capacity_pairs=batch_capacity_pairs,
                   min_batches=min_batches, n_streams=n_streams, result_on_host=result_on_host,
                   query_begin=query_begin, query_end=query_end, use_masks=use_masks,
-                  lanes_per_query=lanes_per_query)
+                  lanes_per_query=lanes_per_query, dense_cells=dense_cells)
     h = ctypes.c_void_p()
     _check(L.sj_self_join(index.handle, ctypes.byref(o), ctypes.byref(h)))
     r = Result(h.value)

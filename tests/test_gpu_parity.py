@@ -377,3 +377,26 @@ def test_c5_16m_sampled_rows_and_shards(sj, d, eps):
     cuts = np.linspace(0, len(pts), 5).astype(np.int64)
     tot = sum(sj.self_join(idx, query_begin=int(a), query_end=int(b)).n_pairs for a, b in zip(cuts[:-1], cuts[1:]))
     assert tot == res.n_pairs
+
+
+@pytest.mark.parametrize("kind,d,eps", [("uniform", 2, 3.0), ("uniform", 3, 9.0), ("clustered", 2, 0.4),
+                                        ("clustered", 3, 0.5), ("clustered", 6, 1.2), ("dups", 4, 0.5)])
+def test_dense_cells_path_invariance(sj, kind, d, eps):
+    """The warp-per-task dense path (cells with >= 16 points, warp-buffered emission) gives the
+    same S as the per-query path, for unicomp and full search, device and host batches, and with
+    capacities small enough to overflow inside the warp buffers' flushes."""
+    if kind == "uniform":
+        pts = datagen.uniform(6000, d, seed=d)
+    elif kind == "clustered":
+        pts = datagen.clustered_small(6000, d, seed=d, sigma=0.3)
+    else:
+        pts = np.concatenate([datagen.duplicates(700, d), datagen.uniform(1500, d, seed=d, hi=4.0)])
+    want = oracle.brute_force(pts, eps)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    for dense in (True, False):
+        for unicomp in (True, False):
+            got = sj.self_join(idx, dense_cells=dense, unicomp=unicomp).to_numpy()
+            assert np.array_equal(got, want), (dense, unicomp)
+    for cap in (5000, 300):
+        got = sj.self_join(idx, batch_capacity_pairs=cap, result_on_host=True).to_numpy()
+        assert np.array_equal(got, want)
