@@ -347,14 +347,35 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
                nullptr, nullptr, nullptr);
         ev.rec(3, s);
 
-        // ---- a3: stable radix sort of (key, id)
+        // ---- a3: sort of (key, id) into (key, id)-ascending order (= stable sort by key, R14).
+        // Sparse keys (<= 2 points per top-k prefix on average, prefixes <= 4N): prefix buckets +
+        // per-bucket sort; otherwise (or when a bucket is large) stable LSD radix sort.
         bool in_tmp = false;
-        radix_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, v.key_bits, s, &in_tmp);
+        bool sorted = false;
+        {
+            const unsigned __int128 cap = std::max<uint64_t>(4ull * n, 1ull << 16);
+            unsigned __int128 P = 1;
+            int k = 0;
+            for (int kk = 1; kk <= d; ++kk) {
+                const unsigned __int128 Q = P * v.cpd[d - kk];
+                if (Q > cap) break;
+                P = Q;
+                k = kk;
+            }
+            // (bucket arrays stay L2-sized: P <= 2^22; measured slower than LSD at P = 11.4 M)
+            if (k >= 1 && (double)n <= 2.0 * (double)(uint64_t)P && P <= ((unsigned __int128)1 << 22)) {
+                uint64_t div = 1;
+                for (int j = 0; j < d - k; ++j) div *= v.cpd[j];
+                sorted = bucket_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, div, (uint64_t)P, s);
+            }
+        }
+        if (!sorted) radix_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, v.key_bits, s, &in_tmp);
         const uint64_t *skeys = in_tmp ? keys_tmp.p : keys.p;
         if (in_tmp) SJ_CUDA(cudaMemcpyAsync(A, ids_tmp.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
         ev.rec(4, s);
 
-        // ---- a4: heads, cell numbering, compaction, SoA gather
+        // ---- a4: heads, cell numbering, compaction, SoA gather.  B and G are sized for the upper
+        // bound N cells so no host round trip is needed here; |G| is read back by build_aux's sync.
         uint32_t *pcell = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
         {
             Scratch<uint32_t> flags(n, s);
@@ -362,33 +383,24 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
             SJ_LAUNCHED();
             inclusive_scan_u32(flags.p, pcell, n, s);
         }
-        uint32_t nG = 0;
-        SJ_CUDA(cudaMemcpyAsync(&nG, pcell + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-        SJ_CUDA(cudaStreamSynchronize(s));
-        tr.mark("keys+sort+scan (synced)");
-        uint64_t *B = static_cast<uint64_t *>(own(dev_alloc(sizeof(uint64_t) * nG, s)));
-        uint32_t *G = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * ((size_t)nG + 1), s)));
+        uint64_t *B = static_cast<uint64_t *>(own(dev_alloc(sizeof(uint64_t) * n, s)));
+        uint32_t *G = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * ((size_t)n + 1), s)));
         double *X = static_cast<double *>(own(dev_alloc(sizeof(double) * n * d, s)));
+        uint32_t *aux = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * 4, s)));  // [0]=|G| [1]=#dense tasks
+        SJ_CUDA(cudaMemsetAsync(aux, 0, sizeof(uint32_t) * 4, s));
+        SJ_CUDA(cudaMemcpyAsync(aux, pcell + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
         launch(d, 2, grid, dim3(kThreads), s, pts, N, ix, const_cast<uint64_t *>(skeys), nullptr, nullptr, nullptr,
                nullptr, A, pcell, B, G, X);
         ev.rec(5, s);
-        SJ_CUDA(cudaStreamSynchronize(s));
-        ev.rec(6, s);
 
-        v.n_cells = nG;
+        v.n_cells = n;            // provisional upper bound until build_aux() reads |G|
         v.B = B;
         v.G = G;
         v.A = A;
         v.pcell = pcell;
         v.X = X;
         v.masks = masks;
-        v.t_h2d_ms = ev.ms(0, 1);
-        v.t_geometry_ms = ev.ms(1, 2);
-        v.t_keys_ms = ev.ms(2, 3);
-        v.t_sort_ms = ev.ms(3, 4);
-        v.t_compact_ms = ev.ms(4, 5);
-        v.t_total_ms = ev.ms(0, 5);
-        ix.nG = nG;
+        ix.nG = N;
         ix.B = B;
         ix.G = G;
         ix.A = A;
@@ -397,11 +409,14 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
         ix.masks = masks;
         idx->view = v;
         idx->dev = ix;
-        build_directory(idx, s);
-        build_dense_tasks(idx, s);
+        build_aux(idx, s, aux);    // directory + dense tasks; the build's only late host sync
         ev.rec(6, s);
         SJ_CUDA(cudaStreamSynchronize(s));
-        tr.mark("compact+dir (synced)");
+        tr.mark("compact+dir+dense (synced)");
+        idx->view.t_h2d_ms = ev.ms(0, 1);
+        idx->view.t_geometry_ms = ev.ms(1, 2);
+        idx->view.t_keys_ms = ev.ms(2, 3);
+        idx->view.t_sort_ms = ev.ms(3, 4);
         idx->view.t_compact_ms = ev.ms(4, 6);
         idx->view.t_total_ms = ev.ms(0, 6);
     } catch (...) {
@@ -424,71 +439,46 @@ __device__ __forceinline__ uint64_t div_small_quot(uint64_t x, uint64_t d, doubl
 
 // dir[q] = #cells with prefix < q = exclusive prefix sum of the per-prefix cell histogram
 __global__ void __launch_bounds__(kThreads)
-k_dir_hist(const uint64_t *__restrict__ B, uint32_t nG, uint64_t div, double inv, uint32_t *__restrict__ hist)
+k_dir_hist(const uint64_t *__restrict__ B, const uint32_t *__restrict__ nG, uint64_t div, double inv,
+           uint32_t *__restrict__ hist)
 {
     const uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (h >= nG) return;
+    if (h >= *nG) return;
     atomicAdd(hist + div_small_quot(B[h], div, inv), 1u);
 }
-__global__ void __launch_bounds__(kThreads)
-k_dense_count(const uint32_t *__restrict__ G, uint32_t nG, uint32_t T, uint32_t *__restrict__ cnt)
-{
-    const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
-    if (h >= nG) return;
-    const uint32_t n = G[h + 1] - G[h];
-    cnt[h] = n >= T ? (n + 31u) / 32u : 0u;
-}
 
+// dense tasks: cells with >= T points cut into <= 32-query tasks; task order is irrelevant, so the
+// tasks are appended with an atomic cursor (aux[1]) into a buffer sized for the N/T upper bound
 __global__ void __launch_bounds__(kThreads)
-k_dense_fill(const uint32_t *__restrict__ G, uint32_t nG, uint32_t T, const uint32_t *__restrict__ off,
-             uint32_t *__restrict__ tasks)
+k_dense_tasks(const uint32_t *__restrict__ G, const uint32_t *__restrict__ nG, uint32_t T,
+              uint32_t *__restrict__ cursor, uint32_t *__restrict__ tasks)
 {
     const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
-    if (h >= nG) return;
+    if (h >= *nG) return;
     const uint32_t s = G[h], n = G[h + 1] - s;
     if (n < T) return;
-    const uint32_t o = off[h];
-    for (uint32_t i = 0; i < (n + 31u) / 32u; ++i) tasks[o + i] = s + 32u * i;
+    const uint32_t m = (n + 31u) / 32u;
+    const uint32_t o = atomicAdd(cursor, m);
+    for (uint32_t i = 0; i < m; ++i) tasks[o + i] = s + 32u * i;
 }
 }  // namespace
 
-// Dense-cell task list (a property of the index): every cell with >= T points is cut into tasks
-// of <= 32 consecutive queries, one warp each in k_refine_dense.
+// Auxiliary structures built on the device from B/G, with the cell count |G| = aux[0] known only on
+// the device; the single host sync at the end reads |G| and the dense-task count.
+//  * prefix directory (DESIGN.md §6 "bounded search"): the largest k such that the number of top-k
+//    coordinate prefixes P_k = prod_{j >= d-k} |g_j| stays <= max(4N, 2^16) (<= 16 B per point, so
+//    the index stays O(|D|)); every B lookup of the refine is a binary search bounded
+//    to one prefix's range.
+//  * dense-cell tasks: every cell with >= kDenseT points is cut into tasks of <= 32 queries, one
+//    warp each in k_refine_dense.
 constexpr uint32_t kDenseT = 16;
-void build_dense_tasks(sj_index *idx, cudaStream_t s)
-{
-    DevIndex &ix = idx->dev;
-    const uint32_t nG = ix.nG;
-    Scratch<uint32_t> cnt((size_t)nG + 1, s), off((size_t)nG + 1, s);
-    SJ_CUDA(cudaMemsetAsync(cnt.p + nG, 0, sizeof(uint32_t), s));
-    k_dense_count<<<(nG + kThreads - 1) / kThreads, kThreads, 0, s>>>(ix.G, nG, kDenseT, cnt.p);
-    SJ_LAUNCHED();
-    exclusive_scan_u32(cnt.p, off.p, (uint64_t)nG + 1, s);
-    uint32_t total = 0;
-    SJ_CUDA(cudaMemcpyAsync(&total, off.p + nG, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    SJ_CUDA(cudaStreamSynchronize(s));
-    uint32_t *tasks = nullptr;
-    if (total) {
-        tasks = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * total, s));
-        idx->bufs[idx->nbufs++] = tasks;
-        k_dense_fill<<<(nG + kThreads - 1) / kThreads, kThreads, 0, s>>>(ix.G, nG, kDenseT, off.p, tasks);
-        SJ_LAUNCHED();
-    }
-    ix.dense_tasks = tasks;
-    ix.n_dense_tasks = total;
-    ix.dense_T = kDenseT;
-}
-
-// Prefix directory: the largest k such that the number of
-// top-k coordinate prefixes P_k = prod_{j >= d-k} |g_j| stays <= max(4|G|, 2^16), so the
-// directory costs <= 16 B per non-empty cell (space stays O(|D|)).  Every B
-// lookup of the refine is then a binary search bounded to one prefix's range.
-void build_directory(sj_index *idx, cudaStream_t s)
+void build_aux(sj_index *idx, cudaStream_t s, uint32_t *aux)
 {
     sj_index_view &v = idx->view;
     DevIndex &ix = idx->dev;
     const int d = v.d;
-    const unsigned __int128 cap = std::max<uint64_t>(4ull * v.n_cells, 1ull << 16);
+    const uint64_t n = v.n;
+    const unsigned __int128 cap = std::max<uint64_t>(4ull * n, 1ull << 16);
     int k = 0;
     unsigned __int128 P = 1;
     for (int kk = 1; kk <= d; ++kk) {
@@ -501,14 +491,25 @@ void build_directory(sj_index *idx, cudaStream_t s)
     for (int j = 0; j < d - k; ++j) div *= v.cpd[j];   // = strides[d-k] (or prod all for k=0)
     uint32_t *dir = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * ((size_t)P + 1), s));
     idx->bufs[idx->nbufs++] = dir;
-    const uint32_t nG = (uint32_t)v.n_cells;
+    const uint32_t gN = (uint32_t)((n + kThreads - 1) / kThreads);
     {
         Scratch<uint32_t> hist((size_t)P + 1, s);
         SJ_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(uint32_t) * ((size_t)P + 1), s));
-        k_dir_hist<<<(nG + kThreads - 1) / kThreads, kThreads, 0, s>>>(v.B, nG, div, 1.0 / (double)div, hist.p);
+        k_dir_hist<<<gN, kThreads, 0, s>>>(v.B, aux, div, 1.0 / (double)div, hist.p);
         SJ_LAUNCHED();
         exclusive_scan_u32(hist.p, dir, (uint64_t)P + 1, s);
     }
+    const uint64_t max_tasks = n / kDenseT + 1;
+    uint32_t *tasks = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * max_tasks, s));
+    idx->bufs[idx->nbufs++] = tasks;
+    k_dense_tasks<<<gN, kThreads, 0, s>>>(v.G, aux, kDenseT, aux + 1, tasks);
+    SJ_LAUNCHED();
+    uint32_t h_aux[2] = {0, 0};
+    SJ_CUDA(cudaMemcpyAsync(h_aux, aux, sizeof(h_aux), cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaStreamSynchronize(s));
+    const uint32_t nG = h_aux[0];
+    v.n_cells = nG;
+    ix.nG = nG;
     v.dir_k = k;
     v.dir_entries = (uint64_t)P + 1;
     v.dir = dir;
@@ -525,10 +526,13 @@ void build_directory(sj_index *idx, cudaStream_t s)
     for (int j = 0; j < d; ++j) ix.lowR[j + 1] = ix.lowR[j] + (int64_t)(j < d - k ? v.strides[j] : 0);
     // mode: a dense directory gives O(1) rows; small prefix ranges (<= 8 cells on average) are
     // cheapest to scan cell by cell (sparse high-d data); otherwise bounded row searches.
-    const double avg_range = (double)v.n_cells / (double)(uint64_t)P;
+    const double avg_range = (double)nG / (double)(uint64_t)P;
     if (k == d) ix.search_mode = kSearchDenseRows;
     else if (avg_range <= 8.0 && (double)div < 4.0e15) ix.search_mode = kSearchCellScan;
     else ix.search_mode = kSearchRows;
+    ix.dense_tasks = tasks;
+    ix.n_dense_tasks = h_aux[1];
+    ix.dense_T = kDenseT;
 }
 
 void free_index_impl(sj_index *idx)
@@ -590,9 +594,10 @@ sj_index *import_index_impl(const sj_index_view &src, int device)
         ix.B = B; ix.G = G; ix.A = A; ix.pcell = pcell; ix.X = X; ix.masks = masks;
         idx->view = v;
         idx->dev = ix;
-        build_directory(idx, s);
-        build_dense_tasks(idx, s);
-        SJ_CUDA(cudaStreamSynchronize(s));
+        uint32_t *aux = static_cast<uint32_t *>(own(4 * 4));
+        const uint32_t hn[4] = {(uint32_t)nG, 0u, 0u, 0u};
+        SJ_CUDA(cudaMemcpyAsync(aux, hn, sizeof(hn), cudaMemcpyHostToDevice, s));
+        build_aux(idx, s, aux);
     } catch (...) {
         cudaStreamDestroy(s);
         free_index_impl(idx);

@@ -270,4 +270,106 @@ void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32
     }
 }
 
+// ---------------------------------------------------------------- prefix-bucket sort (sparse keys)
+// Two stages for keys whose top-k-dimension prefix splits the points into small buckets:
+//   1. histogram of prefixes, exclusive scan -> bucket starts, scatter (atomic cursor per bucket,
+//      order inside a bucket arbitrary);
+//   2. one thread per bucket sorts its <= kBucketMax items by (key, id) (insertion sort).
+// The result is the (key, id)-ascending order -- exactly what the stable LSD sort produces, so A is
+// unchanged (reading R14).  Returns false (nothing written) when some bucket exceeds kBucketMax;
+// the caller then runs the LSD sort.
+namespace {
+constexpr uint32_t kBucketMax = 64;
+
+__device__ __forceinline__ uint64_t bucket_of(uint64_t key, uint64_t div, double inv)
+{
+    uint64_t q = (uint64_t)((double)key * inv);
+    if (q * div > key) --q;
+    else if ((q + 1) * div <= key) ++q;
+    return q;
+}
+
+__global__ void __launch_bounds__(256)
+k_bucket_hist(const uint64_t *__restrict__ keys, uint32_t n, uint64_t div, double inv, uint32_t *__restrict__ hist)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) atomicAdd(hist + bucket_of(keys[i], div, inv), 1u);
+}
+
+__global__ void __launch_bounds__(256)
+k_bucket_max(const uint32_t *__restrict__ hist, uint64_t P, uint32_t *__restrict__ mx)
+{
+    uint32_t m = 0;
+    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < P; b += (uint64_t)gridDim.x * blockDim.x)
+        m = max(m, hist[b]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+}
+
+__global__ void __launch_bounds__(256)
+k_bucket_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t n, uint64_t div,
+                 double inv, uint32_t *__restrict__ cursor, uint64_t *__restrict__ kout, uint32_t *__restrict__ vout)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t k = kin[i];
+    const uint32_t pos = atomicAdd(cursor + bucket_of(k, div, inv), 1u);
+    kout[pos] = k;
+    vout[pos] = vin[i];
+}
+
+__global__ void __launch_bounds__(256)
+k_bucket_sort(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, const uint32_t *__restrict__ start,
+              uint64_t P, uint64_t *__restrict__ kout, uint32_t *__restrict__ vout)
+{
+    const uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= P) return;
+    const uint32_t s = start[b], e = start[b + 1];
+    if (e == s) return;
+    // insertion sort by (key, id) directly in the output range (a few L1-resident entries)
+    for (uint32_t i = s; i < e; ++i) {
+        const uint64_t ki = kin[i];
+        const uint32_t vi = vin[i];
+        uint32_t j = i;
+        while (j > s) {
+            const uint64_t kj = kout[j - 1];
+            const uint32_t vj = vout[j - 1];
+            if (kj < ki || (kj == ki && vj < vi)) break;
+            kout[j] = kj;
+            vout[j] = vj;
+            --j;
+        }
+        kout[j] = ki;
+        vout[j] = vi;
+    }
+}
+}  // namespace
+
+bool bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp, uint32_t n,
+                       uint64_t div, uint64_t P, cudaStream_t s)
+{
+    if (n == 0) return true;
+    const double inv = 1.0 / (double)div;
+    Scratch<uint32_t> hist((size_t)P + 1, s), start((size_t)P + 1, s), mx(1, s);
+    SJ_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(uint32_t) * ((size_t)P + 1), s));
+    SJ_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(uint32_t), s));
+    const uint32_t g = (n + 255) / 256;
+    k_bucket_hist<<<g, 256, 0, s>>>(keys, n, div, inv, hist.p);
+    SJ_LAUNCHED();
+    k_bucket_max<<<(uint32_t)std::min<uint64_t>((P + 255) / 256, 148 * 8), 256, 0, s>>>(hist.p, P, mx.p);
+    SJ_LAUNCHED();
+    uint32_t hmax = 0;
+    SJ_CUDA(cudaMemcpyAsync(&hmax, mx.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaStreamSynchronize(s));
+    if (hmax > kBucketMax) return false;
+    exclusive_scan_u32(hist.p, start.p, (uint64_t)P + 1, s);
+    SJ_CUDA(cudaMemcpyAsync(hist.p, start.p, sizeof(uint32_t) * ((size_t)P + 1), cudaMemcpyDeviceToDevice, s));
+    k_bucket_scatter<<<g, 256, 0, s>>>(keys, vals, n, div, inv, hist.p, keys_tmp, vals_tmp);
+    SJ_LAUNCHED();
+    k_bucket_sort<<<(uint32_t)((P + 255) / 256), 256, 0, s>>>(keys_tmp, vals_tmp, start.p, P, keys, vals);
+    SJ_LAUNCHED();
+    return true;
+}
+
 }  // namespace sj

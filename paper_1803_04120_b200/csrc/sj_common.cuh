@@ -157,8 +157,7 @@ struct CtxGuard {
 };
 
 // index_build.cu
-void build_directory(sj_index *idx, cudaStream_t s);
-void build_dense_tasks(sj_index *idx, cudaStream_t s);
+void build_aux(sj_index *idx, cudaStream_t s, uint32_t *aux);
 sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &o);
 sj_index *import_index_impl(const sj_index_view &v, int device);
 void free_index_impl(sj_index *idx);
@@ -166,6 +165,8 @@ void free_index_impl(sj_index *idx);
 // radix_sort.cu
 void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp,
                       uint32_t n, int key_bits, cudaStream_t s, bool *result_in_tmp);
+bool bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp, uint32_t n,
+                       uint64_t div, uint64_t P, cudaStream_t s);
 void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s);
 void inclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s);
 
