@@ -447,6 +447,17 @@ k_dir_hist(const uint64_t *__restrict__ B, const uint32_t *__restrict__ nG, uint
     atomicAdd(hist + div_small_quot(B[h], div, inv), 1u);
 }
 
+// occupancy bits of the top-(k+1) prefixes: bit q = key / occ_div
+__global__ void __launch_bounds__(kThreads)
+k_occ_bits(const uint64_t *__restrict__ B, const uint32_t *__restrict__ nG, uint64_t div, double inv,
+           uint32_t *__restrict__ occ)
+{
+    const uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= *nG) return;
+    const uint64_t q = div_small_quot(B[h], div, inv);
+    atomicOr(occ + (q >> 5), 1u << (q & 31));
+}
+
 // dense tasks: cells with >= T points cut into <= 32-query tasks; task order is irrelevant, so the
 // tasks are appended with an atomic cursor (aux[1]) into a buffer sized for the N/T upper bound
 __global__ void __launch_bounds__(kThreads)
@@ -499,6 +510,25 @@ void build_aux(sj_index *idx, cudaStream_t s, uint32_t *aux)
         SJ_LAUNCHED();
         exclusive_scan_u32(hist.p, dir, (uint64_t)P + 1, s);
     }
+    // occupancy bitmap over the top-(k+1) prefixes when it costs <= 8 bytes per point
+    uint32_t *occ = nullptr;
+    uint64_t occ_div = 0, occ_cpd = 0;
+    if (k >= 1 && k < d) {
+        const unsigned __int128 P1 = P * v.cpd[d - k - 1];
+        // ... and when it filters: the +-1 window of 3 sub-prefixes is expected to be occupied
+        // with probability ~3N/P1 (< 0.25 here; 6-D eps=1: 0.06, eps=8: 0.53 -> not built)
+        if (P1 <= (unsigned __int128)64 * std::max<uint64_t>(n, 1ull << 16) &&
+            3.0 * (double)n < 0.25 * (double)(uint64_t)P1) {
+            occ_cpd = v.cpd[d - k - 1];
+            occ_div = div / occ_cpd;                      // = stride of dim d-k-1
+            const size_t words = (size_t)((P1 + 31) / 32);
+            occ = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * words, s));
+            idx->bufs[idx->nbufs++] = occ;
+            SJ_CUDA(cudaMemsetAsync(occ, 0, sizeof(uint32_t) * words, s));
+            k_occ_bits<<<gN, kThreads, 0, s>>>(v.B, aux, occ_div, 1.0 / (double)occ_div, occ);
+            SJ_LAUNCHED();
+        }
+    }
     const uint64_t max_tasks = n / kDenseT + 1;
     uint32_t *tasks = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * max_tasks, s));
     idx->bufs[idx->nbufs++] = tasks;
@@ -530,6 +560,9 @@ void build_aux(sj_index *idx, cudaStream_t s, uint32_t *aux)
     if (k == d) ix.search_mode = kSearchDenseRows;
     else if (avg_range <= 8.0 && (double)div < 4.0e15) ix.search_mode = kSearchCellScan;
     else ix.search_mode = kSearchRows;
+    ix.occ = occ;
+    ix.occ_div = occ_div;
+    ix.occ_cpd = occ_cpd;
     ix.dense_tasks = tasks;
     ix.n_dense_tasks = h_aux[1];
     ix.dense_T = kDenseT;

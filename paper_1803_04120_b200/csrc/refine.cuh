@@ -287,38 +287,77 @@ __device__ __forceinline__ void search_cell_scan(const DevIndex &ix, const JoinA
 #pragma unroll
     for (int j = 0; j < D; ++j) ph += q.c[j] * ix.pstride[j];
     const int64_t Rl = ix.lowR[L];
-    // Uniform trip count for every lane of the warp and an explicit __syncwarp per offset: without
+    // Uniform trip count for every lane of the warp and an explicit __syncwarp per chunk: without
     // it the lanes drift apart (independent thread scheduling) and their divergent cell loops
     // serialise -- measured 2.4 of 32 lanes active on 6-D eps=8.
-#pragma unroll 1
-    for (uint32_t t0 = 0; t0 < ix.dir_ntop; t0 += q.G) {
-        __syncwarp(wmask);
-        const uint32_t t = t0 + q.sub;
-        if (t >= ix.dir_ntop) continue;
-        const uint32_t bits = tt.bits[t];
-        if (bits & bad) continue;      // masked-out coordinate, or decided by an even top dim
-        const int jtop = (bits >> 16) ? (__ffs(bits >> 16) - 1) : -1;
-        const uint64_t p = ph + (uint64_t)tt.dp[t];
-        ++q.probes;
-        const uint32_t lo = __ldg(ix.dir + p), hi = __ldg(ix.dir + p + 1);
-        const uint64_t kal = key + (uint64_t)tt.dk[t];
-#pragma unroll 1
-        for (uint32_t hh = lo; hh < hi; ++hh) {
-            if (hh == h) continue;                       // home cell handled separately
-            int64_t dlt = (int64_t)(__ldg(ix.B + hh) - kal);
-            if (dlt > Rl || dlt < -Rl) continue;         // outside the +-1 box
-            int jlow = -1;
+    // Offsets are taken in chunks of kChunk: phase 1 (unrolled) issues the occupancy-bitmap loads
+    // of the whole chunk together (memory-level parallelism), phase 2 scans the survivors.
+    uint64_t cl = q.c[0];
 #pragma unroll
-            for (int i = D - 2; i >= 0; --i) {
-                if (i >= L) continue;
-                const int64_t R = ix.lowR[i], st = (int64_t)ix.strides[i];
-                if (dlt > R) { dlt -= st; if (jlow < 0) jlow = i; }
-                else if (dlt < -R) { dlt += st; if (jlow < 0) jlow = i; }
+    for (int i = 1; i < D; ++i) if (i == L - 1) cl = q.c[i];
+    constexpr int kChunk = 9;
+    const uint32_t ntop = ix.dir_ntop;
+    const uint32_t step = q.G * kChunk;
+#pragma unroll 1
+    for (uint32_t t0 = 0; t0 < ntop; t0 += step) {
+        __syncwarp(wmask);
+        uint32_t live = 0;                       // bit u: offset t0 + sub + u*G survives the filters
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+            const uint32_t t = t0 + q.sub + (uint32_t)u * q.G;
+            if (t >= ntop) continue;
+            const uint32_t bits = tt.bits[t];
+            if (bits & bad) continue;            // masked-out coordinate, or decided by an even top dim
+            if (ix.occ) {
+                // joint-occupancy filter: is any (k+1)-prefix p*|g_{L-1}| + c_{L-1} + {-1,0,1}
+                // occupied?  (the top low dimension's window; PAPER.md:173 masks, generalised)
+                const uint64_t p = ph + (uint64_t)tt.dp[t];
+                const uint64_t qb = p * ix.occ_cpd + cl - 1ull;
+                uint32_t win = __ldg(ix.occ + (qb >> 5)) >> (qb & 31);
+                if ((qb & 31) > 29) win |= __ldg(ix.occ + (qb >> 5) + 1) << (32 - (qb & 31));
+                if (!(win & 7u)) continue;
             }
-            if (dlt != 0) continue;                      // not representable: not adjacent
-            const int j = jtop >= 0 ? jtop : jlow;
-            if (UNICOMP && !((q.odd >> j) & 1u)) continue;
-            scan_range<D, MODE, UNICOMP, DENSE>(ix, ja, q, __ldg(ix.G + hh), __ldg(ix.G + hh + 1), 1u, wb, wmask);
+            live |= 1u << u;
+        }
+        // phase 2.  With the occupancy bitmap (sparse regime) survivors are rare and each lane walks
+        // its own (measured 0.54 vs 0.71 ms on 6-D eps=1).  Without it (denser regime) survivors are
+        // common and the warp visits the offsets live in ANY lane together, re-converging at each
+        // (lanes' cell loops differ; drifting apart serialises the warp: 14 vs 26 ms on eps=8).
+        const bool sparse = ix.occ != nullptr;
+        uint32_t any = sparse ? live : __reduce_or_sync(wmask, live);
+#pragma unroll 1
+        while (any) {
+            const int u = __ffs(any) - 1;
+            any &= any - 1u;
+            if (!sparse) {
+                __syncwarp(wmask);
+                if (!((live >> u) & 1u)) continue;
+            }
+            const uint32_t t = t0 + q.sub + (uint32_t)u * q.G;
+            const uint32_t bits = tt.bits[t];
+            const int jtop = (bits >> 16) ? (__ffs(bits >> 16) - 1) : -1;
+            const uint64_t p = ph + (uint64_t)tt.dp[t];
+            ++q.probes;
+            const uint32_t lo = __ldg(ix.dir + p), hi = __ldg(ix.dir + p + 1);
+            const uint64_t kal = key + (uint64_t)tt.dk[t];
+#pragma unroll 1
+            for (uint32_t hh = lo; hh < hi; ++hh) {
+                if (hh == h) continue;                       // home cell handled separately
+                int64_t dlt = (int64_t)(__ldg(ix.B + hh) - kal);
+                if (dlt > Rl || dlt < -Rl) continue;         // outside the +-1 box
+                int jlow = -1;
+#pragma unroll
+                for (int i = D - 2; i >= 0; --i) {
+                    if (i >= L) continue;
+                    const int64_t R = ix.lowR[i], st = (int64_t)ix.strides[i];
+                    if (dlt > R) { dlt -= st; if (jlow < 0) jlow = i; }
+                    else if (dlt < -R) { dlt += st; if (jlow < 0) jlow = i; }
+                }
+                if (dlt != 0) continue;                      // not representable: not adjacent
+                const int j = jtop >= 0 ? jtop : jlow;
+                if (UNICOMP && !((q.odd >> j) & 1u)) continue;
+                scan_range<D, MODE, UNICOMP, DENSE>(ix, ja, q, __ldg(ix.G + hh), __ldg(ix.G + hh + 1), 1u, wb, wmask);
+            }
         }
     }
 }

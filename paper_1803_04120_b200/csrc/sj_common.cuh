@@ -100,6 +100,11 @@ struct DevIndex {
     uint32_t dir_ntop;           // 3^dir_k top-prefix offsets
     double inv_cpd[SJ_MAX_DIM];  // 1/|g_j| (fast exact divmod of low key parts, see refine.cuh)
     int64_t lowR[SJ_MAX_DIM + 1];// lowR[i] = sum_{m<i} stride_m: largest |key offset| of dims < i
+    // occupancy bitmap over the top-(k+1) coordinate prefixes (cell-scan mode): bit q set iff some
+    // cell has prefix q = key / occ_div; lets a prefix range be skipped by one bit test
+    const uint32_t *occ;
+    uint64_t occ_div;            // stride of dimension d-k-1
+    uint64_t occ_cpd;            // |g_{d-k-1}|
     // dense-cell tasks: every cell with >= dense_T points is cut into tasks of <= 32 consecutive
     // queries (start A-positions), processed one warp per task by k_refine_dense
     const uint32_t *dense_tasks;
