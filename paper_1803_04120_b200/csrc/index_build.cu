@@ -458,19 +458,27 @@ k_occ_bits(const uint64_t *__restrict__ B, const uint32_t *__restrict__ nG, uint
     atomicOr(occ + (q >> 5), 1u << (q & 31));
 }
 
-// dense tasks: cells with >= T points cut into <= 32-query tasks; task order is irrelevant, so the
-// tasks are appended with an atomic cursor (aux[1]) into a buffer sized for the N/T upper bound
+// dense tasks, in A-order: cells with >= T points are cut into <= 32-query tasks; count, exclusive
+// scan (over the N upper bound, zero past |G|), fill
 __global__ void __launch_bounds__(kThreads)
-k_dense_tasks(const uint32_t *__restrict__ G, const uint32_t *__restrict__ nG, uint32_t T,
-              uint32_t *__restrict__ cursor, uint32_t *__restrict__ tasks)
+k_dense_count(const uint32_t *__restrict__ G, const uint32_t *__restrict__ nG, uint32_t T, uint32_t *__restrict__ cnt)
+{
+    const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= *nG) return;
+    const uint32_t n = G[h + 1] - G[h];
+    cnt[h] = n >= T ? (n + 31u) / 32u : 0u;
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_dense_fill(const uint32_t *__restrict__ G, const uint32_t *__restrict__ nG, uint32_t T,
+             const uint32_t *__restrict__ off, uint32_t *__restrict__ tasks)
 {
     const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
     if (h >= *nG) return;
     const uint32_t s = G[h], n = G[h + 1] - s;
     if (n < T) return;
-    const uint32_t m = (n + 31u) / 32u;
-    const uint32_t o = atomicAdd(cursor, m);
-    for (uint32_t i = 0; i < m; ++i) tasks[o + i] = s + 32u * i;
+    const uint32_t o = off[h];
+    for (uint32_t i = 0; i < (n + 31u) / 32u; ++i) tasks[o + i] = s + 32u * i;
 }
 }  // namespace
 
@@ -532,8 +540,16 @@ void build_aux(sj_index *idx, cudaStream_t s, uint32_t *aux)
     const uint64_t max_tasks = n / kDenseT + 1;
     uint32_t *tasks = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * max_tasks, s));
     idx->bufs[idx->nbufs++] = tasks;
-    k_dense_tasks<<<gN, kThreads, 0, s>>>(v.G, aux, kDenseT, aux + 1, tasks);
-    SJ_LAUNCHED();
+    {
+        Scratch<uint32_t> cnt((size_t)n + 1, s), off((size_t)n + 1, s);
+        SJ_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(uint32_t) * ((size_t)n + 1), s));
+        k_dense_count<<<gN, kThreads, 0, s>>>(v.G, aux, kDenseT, cnt.p);
+        SJ_LAUNCHED();
+        exclusive_scan_u32(cnt.p, off.p, (uint64_t)n + 1, s);
+        SJ_CUDA(cudaMemcpyAsync(aux + 1, off.p + n, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        k_dense_fill<<<gN, kThreads, 0, s>>>(v.G, aux, kDenseT, off.p, tasks);
+        SJ_LAUNCHED();
+    }
     uint32_t h_aux[2] = {0, 0};
     SJ_CUDA(cudaMemcpyAsync(h_aux, aux, sizeof(h_aux), cudaMemcpyDeviceToHost, s));
     SJ_CUDA(cudaStreamSynchronize(s));

@@ -23,7 +23,10 @@ namespace {
 void launch_dense(const DevIndex &ix, const JoinArgs &ja, bool unicomp, cudaStream_t s)
 {
     if (!ja.dense_T || ix.n_dense_tasks == 0) return;
-    const dim3 grid((ix.n_dense_tasks + kDenseWarps - 1) / kDenseWarps), block(32 * kDenseWarps);
+    // tasks intersecting [q0, q1): at most (q1 - q0) / dense_T + 2 (each task holds >= dense_T queries
+    // of its cell, except cell tails), starting at t_lo found on the device
+    const uint64_t max_tasks = std::min<uint64_t>(ix.n_dense_tasks, (uint64_t)(ja.q1 - ja.q0) / ix.dense_T + 2);
+    const dim3 grid((uint32_t)((max_tasks + kDenseWarps - 1) / kDenseWarps)), block(32 * kDenseWarps);
     const size_t smem = sizeof(uint64_t) * kDenseWarps * kWarpBufPairs;
 #define SJ_DENSE_CASE(DD)                                                                              \
     case DD:                                                                                           \

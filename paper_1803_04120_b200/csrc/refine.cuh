@@ -509,8 +509,21 @@ k_refine_dense(const DevIndex ix, const JoinArgs ja)
         build_top_table<D>(ix, tt);
         __syncthreads();
     }
+    // the batch's tasks are the contiguous range [t_lo, t_hi) of the A-ordered task list: tasks
+    // with start + 32 > q0 and start < q1 (one binary search per CTA)
+    __shared__ uint32_t s_tlo;
+    if (threadIdx.x == 0) {
+        uint32_t lo = 0, hi = ja.n_dense_tasks;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(ja.dense_tasks + mid) + 32u <= ja.q0) lo = mid + 1;
+            else hi = mid;
+        }
+        s_tlo = lo;
+    }
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t task = blockIdx.x * kDenseWarps + warp;
+    const uint32_t task = s_tlo + blockIdx.x * kDenseWarps + warp;
     if (task >= ja.n_dense_tasks) return;
     const uint32_t start = __ldg(ja.dense_tasks + task);
     const uint32_t h = __ldg(ix.pcell + start);
