@@ -93,7 +93,7 @@ constexpr int kSmemMaskWords = 2048;   // 64 K bits, 8 KB of shared memory
 template <int D>
 __global__ void __launch_bounds__(kThreads)
 k_keys(const double *__restrict__ pts, uint32_t n, DevIndex ix, uint64_t *__restrict__ keys,
-       uint32_t *__restrict__ ids, uint32_t *__restrict__ masks, uint32_t mask_words)
+       uint32_t *__restrict__ ids, uint32_t *__restrict__ masks, uint32_t mask_words, uint64_t *__restrict__ pc)
 {
     extern __shared__ uint32_t s_mask[];
     const bool smem_masks = masks && mask_words <= (uint32_t)kSmemMaskWords;
@@ -103,13 +103,14 @@ k_keys(const double *__restrict__ pts, uint32_t n, DevIndex ix, uint64_t *__rest
     }
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
-        uint64_t key = 0;
+        uint64_t key = 0, packed = 0;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             const double x = pts[i * D + j];
             const double t = floor(__ddiv_rn(__dsub_rn(x, ix.mins[j]), ix.w));
             const uint64_t c = 1ull + (uint64_t)t;
             key += c * ix.strides[j];
+            packed |= c << ix.cshift[j];
             if (masks) {
                 const uint64_t bit = ix.mask_off[j] + c;
                 if (smem_masks) atomicOr(s_mask + (bit >> 5), 1u << (bit & 31));
@@ -118,6 +119,7 @@ k_keys(const double *__restrict__ pts, uint32_t n, DevIndex ix, uint64_t *__rest
         }
         keys[i] = key;
         ids[i] = (uint32_t)i;
+        if (pc) pc[i] = packed;
     }
     if (smem_masks) {
         __syncthreads();
@@ -136,11 +138,15 @@ k_heads(const uint64_t *__restrict__ keys, uint32_t n, uint32_t *__restrict__ fl
 
 // pcell holds the inclusive scan of head flags on entry (1-based cell number) and the
 // 0-based cell index on exit.
+// Also, at the head of each cell: its packed coordinates (from the per-point pc written by k_keys)
+// and its Alg. 1 line-6 mask word (bit j: c_j - 1 not in M_j; bit 8+j: c_j + 1 not in M_j).
 template <int D>
 __global__ void __launch_bounds__(kThreads)
 k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ A,
                  const double *__restrict__ pts, uint32_t n, uint32_t *__restrict__ pcell,
-                 uint64_t *__restrict__ B, uint32_t *__restrict__ G, double *__restrict__ X)
+                 uint64_t *__restrict__ B, uint32_t *__restrict__ G, double *__restrict__ X,
+                 const uint64_t *__restrict__ pc, uint64_t *__restrict__ ccoord, uint32_t *__restrict__ cmask,
+                 DevIndex ix)
 {
     const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
@@ -150,6 +156,21 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
     if (k == 0 || keys[k - 1] != key) {
         B[h] = key;
         G[h] = (uint32_t)k;
+        if (pc) {
+            const uint64_t packed = pc[A[k]];
+            ccoord[h] = packed;
+            uint32_t mb = 0;
+            if (ix.masks) {
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    const uint64_t c = (packed >> ix.cshift[j]) & ((1ull << ix.cbits[j]) - 1ull);
+                    const uint64_t lo = ix.mask_off[j] + c - 1ull, hi = lo + 2ull;
+                    if (!((ix.masks[lo >> 5] >> (lo & 31)) & 1u)) mb |= 1u << j;
+                    if (!((ix.masks[hi >> 5] >> (hi & 31)) & 1u)) mb |= 1u << (j + 8);
+                }
+            }
+            cmask[h] = mb;
+        }
     }
     if (k == n - 1) G[h + 1] = n;
     const uint64_t src = (uint64_t)A[k] * D;
@@ -160,27 +181,29 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
 template <int D>
 void launch_dim(int which, dim3 g, dim3 b, cudaStream_t s, const double *pts, uint32_t n, DevIndex &ix,
                 uint64_t *keys, uint32_t *ids, uint32_t *masks, double *part, uint32_t *nonfinite,
-                const uint32_t *A, uint32_t *pcell, uint64_t *B, uint32_t *G, double *X)
+                const uint32_t *A, uint32_t *pcell, uint64_t *B, uint32_t *G, double *X,
+                uint64_t *pc = nullptr, uint64_t *ccoord = nullptr, uint32_t *cmask = nullptr)
 {
     const uint32_t mask_words = (uint32_t)((ix.mask_off[ix.d] + 31) / 32);
     if (which == 0) k_minmax<D><<<g, b, 0, s>>>(pts, n, reinterpret_cast<unsigned long long *>(part), nonfinite);
     else if (which == 1)
         k_keys<D><<<g, b, (masks && mask_words <= (uint32_t)kSmemMaskWords) ? 4 * mask_words : 0, s>>>(
-            pts, n, ix, keys, ids, masks, mask_words);
-    else k_compact_gather<D><<<g, b, 0, s>>>(keys, A, pts, n, pcell, B, G, X);
+            pts, n, ix, keys, ids, masks, mask_words, pc);
+    else k_compact_gather<D><<<g, b, 0, s>>>(keys, A, pts, n, pcell, B, G, X, pc, ccoord, cmask, ix);
     SJ_LAUNCHED();
 }
 
 void launch(int d, int which, dim3 g, dim3 b, cudaStream_t s, const double *pts, uint32_t n, DevIndex &ix,
             uint64_t *keys, uint32_t *ids, uint32_t *masks, double *part, uint32_t *nonfinite,
-            const uint32_t *A, uint32_t *pcell, uint64_t *B, uint32_t *G, double *X)
+            const uint32_t *A, uint32_t *pcell, uint64_t *B, uint32_t *G, double *X,
+            uint64_t *pc = nullptr, uint64_t *cc = nullptr, uint32_t *cm = nullptr)
 {
     switch (d) {
-    case 2: launch_dim<2>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X); break;
-    case 3: launch_dim<3>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X); break;
-    case 4: launch_dim<4>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X); break;
-    case 5: launch_dim<5>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X); break;
-    case 6: launch_dim<6>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X); break;
+    case 2: launch_dim<2>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm); break;
+    case 3: launch_dim<3>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm); break;
+    case 4: launch_dim<4>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm); break;
+    case 5: launch_dim<5>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm); break;
+    case 6: launch_dim<6>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm); break;
     default: fail(SJ_ERR_DIM, "d must be in [2,6]");
     }
 }
@@ -327,6 +350,19 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
     }
     v.mask_offsets[d] = mask_total;
     for (int j = 0; j <= d; ++j) ix.mask_off[j] = v.mask_offsets[j];
+    // packed per-cell coordinates (c_j at bit cshift[j]) when the widths fit 64 bits
+    bool pack_fits = true;
+    {
+        uint32_t sh = 0;
+        for (int j = 0; j < d; ++j) {
+            uint32_t b = 0;
+            while (b < 64 && ((v.cpd[j] - 1) >> b)) ++b;
+            ix.cbits[j] = b;
+            ix.cshift[j] = sh;
+            sh += b;
+        }
+        pack_fits = sh <= 64;
+    }
 
     // ---- a2: keys
     sj_index *idx = new sj_index();
@@ -343,8 +379,17 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
         uint32_t *A = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
         Scratch<uint32_t> ids_tmp(n, s);
         const dim3 grid((unsigned)((n + kThreads - 1) / kThreads));
+        Scratch<uint64_t> pcs;
+        uint64_t *ccoord = nullptr;
+        uint32_t *cmask = nullptr;
+        if (pack_fits) {
+            pcs.p = dalloc<uint64_t>(n, s);
+            pcs.s = s;
+            ccoord = static_cast<uint64_t *>(own(dev_alloc(sizeof(uint64_t) * n, s)));
+            cmask = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
+        }
         launch(d, 1, grid, dim3(kThreads), s, pts, N, ix, keys.p, A, masks, nullptr, nullptr, nullptr, nullptr,
-               nullptr, nullptr, nullptr);
+               nullptr, nullptr, nullptr, pcs.p, nullptr, nullptr);
         ev.rec(3, s);
 
         // ---- a3: sort of (key, id) into (key, id)-ascending order (= stable sort by key, R14).
@@ -389,8 +434,11 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
         uint32_t *aux = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * 4, s)));  // [0]=|G| [1]=#dense tasks
         SJ_CUDA(cudaMemsetAsync(aux, 0, sizeof(uint32_t) * 4, s));
         SJ_CUDA(cudaMemcpyAsync(aux, pcell + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        ix.masks = masks;
         launch(d, 2, grid, dim3(kThreads), s, pts, N, ix, const_cast<uint64_t *>(skeys), nullptr, nullptr, nullptr,
-               nullptr, A, pcell, B, G, X);
+               nullptr, A, pcell, B, G, X, pcs.p, ccoord, cmask);
+        ix.ccoord = ccoord;
+        ix.cmask = cmask;
         ev.rec(5, s);
 
         v.n_cells = n;            // provisional upper bound until build_aux() reads |G|

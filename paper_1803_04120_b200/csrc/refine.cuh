@@ -67,9 +67,9 @@ struct WarpBuf {
 
 constexpr int kRefineThreads = 256;
 #ifndef SJ_REFINE_MIN_BLOCKS
-#define SJ_REFINE_MIN_BLOCKS 3
+#define SJ_REFINE_MIN_BLOCKS 4
 #endif
-constexpr int kRefineMinBlocks = SJ_REFINE_MIN_BLOCKS;  // 3 x 256 threads: <= 85 registers
+constexpr int kRefineMinBlocks = SJ_REFINE_MIN_BLOCKS;  // 4 x 256 threads: <= 64 registers (measured best, no spills)
 
 __device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t *__restrict__ B, uint32_t lo, uint32_t hi,
                                                     uint64_t key)
@@ -227,6 +227,7 @@ constexpr int kMaxTop = 243;
 struct TopTable {
     int64_t dp[kMaxTop];     // sum delta_i * pstride_i
     int64_t dk[kMaxTop];     // dp * dir_div (key delta)
+    int64_t dq[kMaxTop];     // dp * occ_cpd (occupancy-bitmap index delta)
     uint32_t bits[kMaxTop];  // [0:6) dims at -1, [8:14) dims at +1, [16:22) one-hot highest moved dim
 };
 
@@ -245,6 +246,7 @@ __device__ __forceinline__ void build_top_table(const DevIndex &ix, TopTable &tt
         }
         tt.dp[t] = dp;
         tt.dk[t] = dp * (int64_t)ix.dir_div;
+        tt.dq[t] = dp * (int64_t)ix.occ_cpd;
         tt.bits[t] = neg | (pos << 8) | (top << 16);
     }
 }
@@ -253,19 +255,23 @@ __device__ __forceinline__ void build_top_table(const DevIndex &ix, TopTable &tt
 // as a "bad" bit set: bit i = move -1 in dim i leaves M_i, bit 8+i = move +1 leaves M_i;
 // unicomp adds bit 16+i when the query's c_i is even (cells decided by dim i are not searched).
 template <int D, bool UNICOMP>
-__device__ __forceinline__ uint32_t bad_moves(const DevIndex &ix, const JoinArgs &ja, const QueryState<D> &q)
+__device__ __forceinline__ uint32_t bad_moves(const DevIndex &ix, const JoinArgs &ja, const QueryState<D> &q,
+                                              uint32_t h)
 {
     uint32_t bad = 0;
-    const bool masked = ja.use_masks && ix.masks;
+    if (ja.use_masks && ix.masks) {
+        if (ix.cmask) {
+            bad = __ldg(ix.cmask + h);                          // precomputed per cell at build time
+        } else {
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-        if (masked) {
-            const uint64_t lo = ix.mask_off[i] + q.c[i] - 1ull, hi = lo + 2ull;
-            if (!((__ldg(ix.masks + (lo >> 5)) >> (lo & 31)) & 1u)) bad |= 1u << i;
-            if (!((__ldg(ix.masks + (hi >> 5)) >> (hi & 31)) & 1u)) bad |= 1u << (i + 8);
+            for (int i = 0; i < D; ++i) {
+                const uint64_t lo = ix.mask_off[i] + q.c[i] - 1ull, hi = lo + 2ull;
+                if (!((__ldg(ix.masks + (lo >> 5)) >> (lo & 31)) & 1u)) bad |= 1u << i;
+                if (!((__ldg(ix.masks + (hi >> 5)) >> (hi & 31)) & 1u)) bad |= 1u << (i + 8);
+            }
         }
-        if (UNICOMP && !((q.odd >> i) & 1u)) bad |= 1u << (i + 16);
     }
+    if (UNICOMP) bad |= ((~q.odd) & ((1u << D) - 1u)) << 16;
     return bad;
 }
 
@@ -295,7 +301,11 @@ __device__ __forceinline__ void search_cell_scan(const DevIndex &ix, const JoinA
     uint64_t cl = q.c[0];
 #pragma unroll
     for (int i = 1; i < D; ++i) if (i == L - 1) cl = q.c[i];
-    constexpr int kChunk = 9;
+    const uint64_t qh = ph * ix.occ_cpd + cl - 1ull;   // bitmap index of the home window's start
+#ifndef SJ_CHUNK
+#define SJ_CHUNK 27
+#endif
+    constexpr int kChunk = SJ_CHUNK;
     const uint32_t ntop = ix.dir_ntop;
     const uint32_t step = q.G * kChunk;
 #pragma unroll 1
@@ -311,8 +321,7 @@ __device__ __forceinline__ void search_cell_scan(const DevIndex &ix, const JoinA
             if (ix.occ) {
                 // joint-occupancy filter: is any (k+1)-prefix p*|g_{L-1}| + c_{L-1} + {-1,0,1}
                 // occupied?  (the top low dimension's window; PAPER.md:173 masks, generalised)
-                const uint64_t p = ph + (uint64_t)tt.dp[t];
-                const uint64_t qb = p * ix.occ_cpd + cl - 1ull;
+                const uint64_t qb = qh + (uint64_t)tt.dq[t];
                 uint32_t win = __ldg(ix.occ + (qb >> 5)) >> (qb & 31);
                 if ((qb & 31) > 29) win |= __ldg(ix.occ + (qb >> 5) + 1) << (32 - (qb & 31));
                 if (!(win & 7u)) continue;
@@ -450,10 +459,15 @@ __device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs 
     q.k = k;
     q.pid = __ldg(ix.A + k);
 #pragma unroll
-    for (int j = 0; j < D; ++j) {
-        q.x[j] = __ldg(ix.X + (uint64_t)j * ix.n + k);
-        // same IEEE operations as the build (reading R7): identical coordinates
-        q.c[j] = 1ull + (uint64_t)floor(__ddiv_rn(__dsub_rn(q.x[j], ix.mins[j]), ix.w));
+    for (int j = 0; j < D; ++j) q.x[j] = __ldg(ix.X + (uint64_t)j * ix.n + k);
+    if (ix.ccoord) {                  // the home cell's coordinates, packed at build time
+        const uint64_t cc = __ldg(ix.ccoord + h);
+#pragma unroll
+        for (int j = 0; j < D; ++j) q.c[j] = (cc >> ix.cshift[j]) & ((1ull << ix.cbits[j]) - 1ull);
+    } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j)   // same IEEE operations as the build (reading R7)
+            q.c[j] = 1ull + (uint64_t)floor(__ddiv_rn(__dsub_rn(q.x[j], ix.mins[j]), ix.w));
     }
     q.odd = 0;
 #pragma unroll
@@ -474,7 +488,7 @@ __device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs 
                 scan_range<D, MODE, false>(ix, ja, q, (part ? k + 1 : cs) + q.sub, part ? ce : k, q.G);
         }
     }
-    const uint32_t bad = bad_moves<D, UNICOMP>(ix, ja, q);
+    const uint32_t bad = bad_moves<D, UNICOMP>(ix, ja, q, h);
     __syncwarp(wmask);
     if (ix.search_mode == kSearchCellScan) {
         search_cell_scan<D, MODE, UNICOMP, DENSE>(ix, ja, q, h, key, bad, tt, wmask, wb);

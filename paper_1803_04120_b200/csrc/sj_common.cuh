@@ -105,6 +105,13 @@ struct DevIndex {
     const uint32_t *occ;
     uint64_t occ_div;            // stride of dimension d-k-1
     uint64_t occ_cpd;            // |g_{d-k-1}|
+    // per non-empty cell, precomputed at build time: packed coordinates (c_j at bit cshift[j],
+    // width cbits[j]; nullptr when sum of widths > 64) and the Alg. 1 line-6 mask word (bit i: move
+    // -1 in dim i leaves M_i; bit 8+i: move +1 leaves M_i)
+    const uint64_t *ccoord;
+    const uint32_t *cmask;
+    uint32_t cshift[SJ_MAX_DIM];
+    uint32_t cbits[SJ_MAX_DIM];
     // dense-cell tasks: every cell with >= dense_T points is cut into tasks of <= 32 consecutive
     // queries (start A-positions), processed one warp per task by k_refine_dense
     const uint32_t *dense_tasks;
@@ -121,7 +128,7 @@ struct sj_index {
     int device = 0;
     sj_index_view view{};        // geometry + device pointers (exported as is)
     sj::DevIndex dev{};          // same, in kernel form
-    void *bufs[12] = {nullptr};  // owned device allocations
+    void *bufs[16] = {nullptr};  // owned device allocations
     int nbufs = 0;
 };
 
