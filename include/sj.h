@@ -85,6 +85,8 @@ typedef struct {
                                       independent of it)                                         */
     int dense_cells;               /* 1 (default): queries of populous cells (>= 16 points) run one
                                       warp per 32 queries with warp-buffered emission; 0: off     */
+    int sort_pairs;                /* 0 (default); 1: each batch is sorted by (key, value) on the
+                                      device before it is returned / drained       */
 } sj_join_opts;
 
 typedef struct {
@@ -183,6 +185,13 @@ sj_status sj_result_copy_to_host(const sj_result *r, uint64_t *dst, uint64_t cap
  * *total receives |S| (restricted to the pairs decided by queries of opts' query range). */
 sj_status sj_neighbor_counts(const sj_index *idx, const sj_join_opts *opts, uint32_t *cnt,
                              uint64_t *total);
+
+/* GPU brute-force nested-loop join: every query compared with
+ * every point with the same predicate; one batch.  points/n/d/eps/bopts as sj_build_index; from
+ * jopts only include_self, sort_pairs and result_on_host are used.  O(N^2): for cross-checks and
+ * the paper's brute-force comparison, not for large N. */
+sj_status sj_brute_force_join(const double *points, uint64_t n, int d, double eps, const sj_build_opts *bopts,
+                              const sj_join_opts *jopts, sj_result **out);
 
 /* Geometry, sizes, timings and device pointers of an index (for tests and NCCL broadcast). */
 sj_status sj_index_export(const sj_index *idx, sj_index_view *view);

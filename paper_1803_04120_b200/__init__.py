@@ -4,9 +4,9 @@ The work runs in ``libsj.so`` (hand-written CUDA behind the C ABI of ``include/s
 package is its thin ctypes binding plus the multi-GPU glue.  There is no CPU fallback.
 """
 from .sj import (  # noqa: F401
-    Index, Result, SJError, build_index, self_join, neighbor_counts, import_index, plan_batches,
+    Index, Result, SJError, build_index, self_join, neighbor_counts, import_index, plan_batches, brute_force_join,
     kernel_launches, load_library, LIB_PATH,
 )
 
 __all__ = ["Index", "Result", "SJError", "build_index", "self_join", "neighbor_counts", "import_index",
-           "plan_batches", "kernel_launches", "load_library", "LIB_PATH"]
+           "plan_batches", "brute_force_join", "kernel_launches", "load_library", "LIB_PATH"]

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libsj.so")
-SOURCES = ["api.cu", "context.cu", "index_build.cu", "radix_sort.cu", "join.cu"]
+SOURCES = ["api.cu", "context.cu", "index_build.cu", "radix_sort.cu", "join.cu", "extras.cu"]
 HEADERS = ["sj_common.cuh", "refine.cuh"]
 
 NVCC_FLAGS = [

@@ -191,6 +191,7 @@ void sj_join_opts_default(sj_join_opts *o)
     o->use_masks = 1;
     o->lanes_per_query = 0;
     o->dense_cells = 1;
+    o->sort_pairs = 0;
 }
 
 sj_status sj_build_index(const double *points, uint64_t n, int d, double eps, const sj_build_opts *opts,
@@ -283,6 +284,22 @@ sj_status sj_neighbor_counts(const sj_index *idx, const sj_join_opts *opts, uint
     if (opts) o = *opts;
     else sj_join_opts_default(&o);
     sj::neighbor_counts_impl(idx, o, cnt, total);
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_brute_force_join(const double *points, uint64_t n, int d, double eps, const sj_build_opts *bopts,
+                              const sj_join_opts *jopts, sj_result **out)
+{
+    SJ_API_BEGIN
+    if (!out) sj::fail(SJ_ERR_ARG, "out is NULL");
+    sj_build_opts bo;
+    if (bopts) bo = *bopts;
+    else sj_build_opts_default(&bo);
+    sj_join_opts jo;
+    if (jopts) jo = *jopts;
+    else sj_join_opts_default(&jo);
+    *out = sj::brute_force_impl(points, n, d, eps, bo, jo);
     return SJ_OK;
     SJ_API_END
 }

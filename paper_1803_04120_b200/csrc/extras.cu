@@ -1,0 +1,178 @@
+// extras.cu -- the SURVEY §8(f) "NEXT" rows built on the same primitives:
+//   f2: on-device sort of a result batch by (key, value) ("After the kernel's
+//       execution, we sort the key/value pairs, and transfer the result to the host").
+//   f3: the GPU brute-force nested-loop join: every query compared with every
+//       point, the paper's epsilon-independent control and a cross-check of the grid join.
+#include <algorithm>
+
+#include "sj_common.cuh"
+
+namespace sj {
+
+// ------------------------------------------------------------------ f2: batch sort
+// Packed pairs (key << 32 | value) sort as plain uint64 (integer order == (key, value) order);
+// only the bits below 32 + ceil(log2 N) are used.
+void sort_pairs_device(uint64_t *pairs, uint64_t n, uint64_t n_points, cudaStream_t s)
+{
+    if (n <= 1) return;
+    if (n >= (1ull << 32)) fail(SJ_ERR_ARG, "sort_pairs: a batch of >= 2^32 pairs cannot be sorted in one pass");
+    int id_bits = 1;
+    while (id_bits < 32 && (1ull << id_bits) < n_points) ++id_bits;
+    Scratch<uint64_t> tmp(n, s);
+    bool in_tmp = false;
+    radix_sort_pairs(pairs, nullptr, tmp.p, nullptr, (uint32_t)n, 32 + id_bits, s, &in_tmp);
+    if (in_tmp) SJ_CUDA(cudaMemcpyAsync(pairs, tmp.p, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+}
+
+// ------------------------------------------------------------------ f3: brute force
+namespace {
+constexpr int kBfThreads = 256;
+constexpr int kBfTile = 256;           // candidates staged per round (SoA in shared memory)
+constexpr int kBfBuf = 512;            // per-warp output buffer (pairs)
+
+template <int D>
+__global__ void __launch_bounds__(kBfThreads)
+k_brute_force(const double *__restrict__ pts, uint32_t n, double eps2, int include_self, uint64_t *out,
+              unsigned long long *cursor, uint64_t cap, uint32_t *overflow)
+{
+    __shared__ double s_x[D][kBfTile];
+    __shared__ uint64_t s_buf[kBfThreads / 32][kBfBuf];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t i = blockIdx.x * kBfThreads + threadIdx.x;
+    const bool active = i < n;
+    double x[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) x[j] = active ? pts[(uint64_t)i * D + j] : 0.0;
+    uint32_t cnt = 0;                  // warp-uniform fill of s_buf[warp]
+    auto flush = [&]() {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(cursor, (unsigned long long)cnt);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (uint32_t e = lane; e < cnt; e += 32) {
+            if (base + e < cap) out[base + e] = s_buf[warp][e];
+            else atomicOr(overflow, 1u);
+        }
+        __syncwarp();
+        cnt = 0;
+    };
+    for (uint32_t t0 = 0; t0 < n; t0 += kBfTile) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kBfTile; e += kBfThreads) {
+            const uint32_t m = t0 + e;
+#pragma unroll
+            for (int j = 0; j < D; ++j) s_x[j][e] = m < n ? pts[(uint64_t)m * D + j] : 0.0;
+        }
+        __syncthreads();
+        const uint32_t lim = min((uint32_t)kBfTile, n - t0);
+        for (uint32_t e = 0; e < lim; ++e) {
+            const uint32_t m = t0 + e;
+            double s;
+            {
+                const double t = __dsub_rn(x[0], s_x[0][e]);
+                s = __dmul_rn(t, t);
+            }
+#pragma unroll
+            for (int j = 1; j < D; ++j) {
+                const double t = __dsub_rn(x[j], s_x[j][e]);
+                s = __dadd_rn(s, __dmul_rn(t, t));
+            }
+            const bool hit = active && s <= eps2 && (include_self || m != i);
+            const unsigned hits = __ballot_sync(0xffffffffu, hit);
+            if (!hits) continue;
+            if (cnt + 32u > (uint32_t)kBfBuf) flush();
+            if (hit) s_buf[warp][cnt + __popc(hits & ((1u << lane) - 1u))] = ((uint64_t)i << 32) | m;
+            __syncwarp();
+            cnt += __popc(hits);
+        }
+    }
+    flush();
+}
+
+template <int D>
+void launch_bf(uint32_t n, cudaStream_t s, const double *pts, double eps2, int inc, uint64_t *out,
+               unsigned long long *cur, uint64_t cap, uint32_t *ovf)
+{
+    k_brute_force<D><<<(n + kBfThreads - 1) / kBfThreads, kBfThreads, 0, s>>>(pts, n, eps2, inc, out, cur, cap, ovf);
+    SJ_LAUNCHED();
+}
+}  // namespace
+
+sj_result *brute_force_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &bo,
+                            const sj_join_opts &jo)
+{
+    if (d < 2 || d > SJ_MAX_DIM) fail(SJ_ERR_DIM, "d must be in [2,6]");
+    if (!points) fail(SJ_ERR_ARG, "points is NULL");
+    if (n == 0 || n >= (1ull << 32)) fail(SJ_ERR_ARG, "N must satisfy 1 <= N < 2^32");
+    if (!(eps > 0.0) || eps != eps || eps > 1e308) fail(SJ_ERR_ARG, "eps must be finite and > 0");
+    SJ_CUDA(cudaSetDevice(bo.device));
+    CtxGuard cg{acquire_ctx(bo.device, 1, 0, 64)};
+    cudaStream_t s = cg.c->streams[0];
+    const double *pts = points;
+    Scratch<double> dp;
+    if (!bo.points_on_device) {
+        dp.p = dalloc<double>(n * d, s);
+        dp.s = s;
+        SJ_CUDA(cudaMemcpyAsync(dp.p, points, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
+        pts = dp.p;
+    }
+    volatile double e2v = eps * eps;
+    const double eps2 = e2v;
+    struct Slot { unsigned long long cursor; uint32_t overflow; uint32_t pad; };
+    Slot *dslot = static_cast<Slot *>(cg.c->d_slots), *hslot = static_cast<Slot *>(cg.c->h_slots);
+    sj_result *res = new sj_result();
+    res->device = bo.device;
+    try {
+        uint64_t cap = std::max<uint64_t>(n * 8, 1024);
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            sj_batch bt;
+            bt.pairs = dalloc<uint64_t>(cap, s);
+            bt.cap = cap;
+            bt.on_device = 1;
+            SJ_CUDA(cudaMemsetAsync(dslot, 0, sizeof(Slot), s));
+            switch (d) {
+            case 2: launch_bf<2>((uint32_t)n, s, pts, eps2, jo.include_self, bt.pairs, &dslot->cursor, cap, &dslot->overflow); break;
+            case 3: launch_bf<3>((uint32_t)n, s, pts, eps2, jo.include_self, bt.pairs, &dslot->cursor, cap, &dslot->overflow); break;
+            case 4: launch_bf<4>((uint32_t)n, s, pts, eps2, jo.include_self, bt.pairs, &dslot->cursor, cap, &dslot->overflow); break;
+            case 5: launch_bf<5>((uint32_t)n, s, pts, eps2, jo.include_self, bt.pairs, &dslot->cursor, cap, &dslot->overflow); break;
+            default: launch_bf<6>((uint32_t)n, s, pts, eps2, jo.include_self, bt.pairs, &dslot->cursor, cap, &dslot->overflow); break;
+            }
+            SJ_CUDA(cudaMemcpyAsync(hslot, dslot, sizeof(Slot), cudaMemcpyDeviceToHost, s));
+            SJ_CUDA(cudaStreamSynchronize(s));
+            const uint64_t got = hslot->cursor;
+            if (got > cap) {                   // exact re-allocation and re-run
+                dev_free(bt.pairs, s);
+                cap = got;
+                continue;
+            }
+            bt.n = got;
+            if (jo.sort_pairs) sort_pairs_device(bt.pairs, bt.n, n, s);
+            if (jo.result_on_host) {
+                uint64_t *h = static_cast<uint64_t *>(host_pinned_alloc(std::max<uint64_t>(1, got) * 8, nullptr));
+                if (got) SJ_CUDA(cudaMemcpyAsync(h, bt.pairs, got * 8, cudaMemcpyDeviceToHost, s));
+                SJ_CUDA(cudaStreamSynchronize(s));
+                dev_free(bt.pairs, s);
+                bt.pairs = h;
+                bt.on_device = 0;
+                bt.cap = got;
+            }
+            res->batches.push_back(bt);
+            res->total = got;
+            break;
+        }
+        SJ_CUDA(cudaStreamSynchronize(s));
+        res->stats.pairs = res->total;
+        res->stats.batches = (uint32_t)res->batches.size();
+        res->stats.candidates_tested = n * n;
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        for (auto &b : res->batches) {
+            if (b.on_device) dev_free(b.pairs, nullptr);
+            else host_pinned_free(b.pairs);
+        }
+        delete res;
+        throw;
+    }
+    return res;
+}
+
+}  // namespace sj

@@ -380,6 +380,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             tr.mark("batches launched");
             for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
             tr.mark("batches done (synced)");
+            cudaStream_t st_sort = s0;
             for (size_t b = (nb > (size_t)S ? nb - S : 0); b < nb; ++b) drain_stream_slot(b);
             for (size_t b = 0; b < nb; ++b) {
                 sj_batch &bt = res->batches[b];
@@ -398,6 +399,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 }
                 bt.n = n;
                 res->total += n;
+                if (o.sort_pairs) sort_pairs_device(bt.pairs, n, ix.n, st_sort);
             }
         } else {
             // ---- host-drained batches: S device staging buffers; batch b+S on a stream runs after
@@ -457,6 +459,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                     bt.n = n;
                     bt.cap = n;
                     if (n) {
+                        if (o.sort_pairs) sort_pairs_device(staging[i], n, ix.n, cx.streams[i]);
                         bt.pairs = static_cast<uint64_t *>(host_pinned_alloc(n * sizeof(uint64_t), nullptr));
                         SJ_CUDA(cudaMemcpyAsync(bt.pairs, staging[i], n * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                                 cx.streams[i]));

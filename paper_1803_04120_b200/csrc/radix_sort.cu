@@ -68,7 +68,7 @@ k_radix_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ v
         const uint64_t i = wbase + (uint64_t)r * 32 + lane;
         const bool valid = i < n;
         k[r] = valid ? kin[i] : 0;
-        v[r] = valid ? vin[i] : 0;
+        v[r] = (valid && vin) ? vin[i] : 0;
     }
 #pragma unroll
     for (int r = 0; r < kSortRounds; ++r) {
@@ -101,7 +101,7 @@ k_radix_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ v
             const uint32_t dg = (uint32_t)((k[r] >> shift) & (R - 1));
             const uint32_t pos = wc[dg] + rk[r];
             kout[pos] = k[r];
-            vout[pos] = v[r];
+            if (vout) vout[pos] = v[r];
         }
     }
 }

@@ -182,6 +182,11 @@ bool bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint3
 void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s);
 void inclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s);
 
+// extras.cu
+void sort_pairs_device(uint64_t *pairs, uint64_t n, uint64_t n_points, cudaStream_t s);
+sj_result *brute_force_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &bo,
+                            const sj_join_opts &jo);
+
 // join.cu
 sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o);
 void neighbor_counts_impl(const sj_index *idx, const sj_join_opts &o, uint32_t *cnt, uint64_t *total);

@@ -35,7 +35,7 @@ class JoinOpts(ctypes.Structure):
     _fields_ = [("unicomp", i32), ("include_self", i32), ("batch_capacity_pairs", u64),
                 ("min_batches", i32), ("n_streams", i32), ("result_on_host", i32),
                 ("query_begin", u64), ("query_end", u64), ("use_masks", i32), ("lanes_per_query", i32),
-                ("dense_cells", i32)]
+                ("dense_cells", i32), ("sort_pairs", i32)]
 
 
 class Stats(ctypes.Structure):
@@ -99,6 +99,8 @@ def load_library(path: str = LIB_PATH):
     L.sj_result_copy_to_host.restype = i32
     L.sj_neighbor_counts.argtypes = [vp, P(JoinOpts), vp, P(u64)]
     L.sj_neighbor_counts.restype = i32
+    L.sj_brute_force_join.argtypes = [vp, u64, i32, dbl, P(BuildOpts), P(JoinOpts), P(vp)]
+    L.sj_brute_force_join.restype = i32
     L.sj_index_export.argtypes = [vp, P(IndexView)]
     L.sj_index_export.restype = i32
     L.sj_index_import.argtypes = [P(IndexView), i32, P(vp)]
@@ -331,13 +333,13 @@ def self_join(index: Index, unicomp: bool = True, include_self: bool = True,
               batch_capacity_pairs: Optional[int] = None, min_batches: Optional[int] = None,
               n_streams: Optional[int] = None, result_on_host: bool = False,
               query_begin: int = 0, query_end: int = 0, use_masks: bool = True,
-              lanes_per_query: int = 0, dense_cells: bool = True) -> Result:
+              lanes_per_query: int = 0, dense_cells: bool = True, sort_pairs: bool = False) -> Result:
     """sj_self_join over the index; see include/sj.h for the option semantics."""
     L = load_library()
     o = join_opts(unicomp=unicomp, include_self=include_self, batch_capacity_pairs=batch_capacity_pairs,
                   min_batches=min_batches, n_streams=n_streams, result_on_host=result_on_host,
                   query_begin=query_begin, query_end=query_end, use_masks=use_masks,
-                  lanes_per_query=lanes_per_query, dense_cells=dense_cells)
+                  lanes_per_query=lanes_per_query, dense_cells=dense_cells, sort_pairs=sort_pairs)
     h = ctypes.c_void_p()
     _check(L.sj_self_join(index.handle, ctypes.byref(o), ctypes.byref(h)))
     r = Result(h.value)
@@ -357,6 +359,37 @@ def neighbor_counts(index: Index, unicomp: bool = True, include_self: bool = Tru
     tot = u64()
     _check(L.sj_neighbor_counts(index.handle, ctypes.byref(o), ctypes.c_void_p(out.data_ptr()), ctypes.byref(tot)))
     return out, int(tot.value)
+
+
+def brute_force_join(points, eps: float, include_self: bool = True, result_on_host: bool = False,
+                     sort_pairs: bool = False, device: Optional[int] = None) -> Result:
+    """sj_brute_force_join: all-pairs GPU join, O(N^2)."""
+    import torch
+    L = load_library()
+    bo = BuildOpts()
+    L.sj_build_opts_default(ctypes.byref(bo))
+    if isinstance(points, torch.Tensor):
+        t = points.contiguous()
+        if t.dtype != torch.float64 or t.dim() != 2:
+            raise TypeError("points must be a 2-D float64 tensor")
+        keep, ptr = t, t.data_ptr()
+        bo.points_on_device = int(t.is_cuda)
+        bo.device = (t.device.index if t.is_cuda else 0) if device is None else device
+        n, d = t.shape
+    else:
+        a = np.ascontiguousarray(points, dtype=np.float64)
+        keep, ptr = a, a.ctypes.data
+        bo.points_on_device = 0
+        bo.device = 0 if device is None else device
+        n, d = a.shape
+    o = join_opts(include_self=include_self, result_on_host=result_on_host, sort_pairs=sort_pairs)
+    h = ctypes.c_void_p()
+    _check(L.sj_brute_force_join(ctypes.c_void_p(ptr), n, d, float(eps), ctypes.byref(bo), ctypes.byref(o),
+                                 ctypes.byref(h)))
+    del keep
+    r = Result(h.value)
+    r.device = bo.device
+    return r
 
 
 def import_index(view: IndexView, device: int) -> Index:

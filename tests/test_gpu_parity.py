@@ -400,3 +400,38 @@ def test_dense_cells_path_invariance(sj, kind, d, eps):
     for cap in (5000, 300):
         got = sj.self_join(idx, batch_capacity_pairs=cap, result_on_host=True).to_numpy()
         assert np.array_equal(got, want)
+
+
+# ------------------------------------------------------------------ NEXT rows f2, f3
+@pytest.mark.parametrize("host", [False, True])
+def test_sort_pairs_per_batch(sj, host):
+    """f2: with sort_pairs every batch comes back sorted by (key, value), and the
+    batches still partition S."""
+    pts = datagen.clustered_small(5000, 3, seed=21)
+    eps = 0.5
+    want = oracle.brute_force(pts, eps)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    res = sj.self_join(idx, sort_pairs=True, result_on_host=host, batch_capacity_pairs=20000)
+    parts = []
+    for b in res.batches():
+        a = b.cpu().numpy().view(np.uint64) if isinstance(b, torch.Tensor) else np.asarray(b)
+        assert np.all(a[1:] >= a[:-1])
+        parts.append(a)
+    assert res.n_batches >= 3
+    assert np.array_equal(np.sort(np.concatenate(parts)), want)
+
+
+@pytest.mark.parametrize("d,n,eps", [(2, 3000, 3.0), (4, 2500, 15.0), (6, 2000, 35.0)])
+def test_brute_force_join(sj, d, n, eps):
+    """f3: the GPU all-pairs join equals the oracle's brute force and the grid
+    join, with and without self pairs; sort_pairs returns it in canonical order."""
+    pts = datagen.uniform(n, d, seed=n + 3 * d)
+    for inc in (True, False):
+        want = oracle.brute_force(pts, eps, include_self=inc)
+        got = sj.brute_force_join(torch.from_numpy(pts).cuda(), eps, include_self=inc).to_numpy()
+        assert np.array_equal(got, want)
+    r = sj.brute_force_join(pts, eps, sort_pairs=True, result_on_host=True)
+    b = np.asarray(r.batch(0))
+    assert np.array_equal(b, oracle.brute_force(pts, eps))
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    assert np.array_equal(sj.self_join(idx).to_numpy(), b)
