@@ -435,3 +435,18 @@ def test_brute_force_join(sj, d, n, eps):
     assert np.array_equal(b, oracle.brute_force(pts, eps))
     idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
     assert np.array_equal(sj.self_join(idx).to_numpy(), b)
+
+
+@pytest.mark.parametrize("d,eps", [(2, 2.0), (3, 4.0), (4, 8.0), (5, 12.0), (6, 18.0)])
+def test_unicomp_halves_the_work(sj, d, eps):
+    """f1 / SPEC criterion 3 (S.400, PAPER.md:346 'reduces ... distance calculations roughly by a
+    factor of two'): uniform 10^5 points, >= 10 neighbours: unicomp's candidate tests are within
+    [0.4, 0.6] of the full 3^d search, with identical pair sets."""
+    pts = datagen.uniform(100_000, d, seed=300 + d)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    ru = sj.self_join(idx, unicomp=True)
+    rf = sj.self_join(idx, unicomp=False)
+    assert ru.n_pairs == rf.n_pairs and ru.n_pairs / len(pts) >= 10
+    ratio = ru.stats["candidates_tested"] / rf.stats["candidates_tested"]
+    assert 0.4 <= ratio <= 0.6, ratio
+    assert np.array_equal(ru.to_numpy(), rf.to_numpy())
