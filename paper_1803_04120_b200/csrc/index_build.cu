@@ -146,7 +146,7 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
                  const double *__restrict__ pts, uint32_t n, uint32_t *__restrict__ pcell,
                  uint64_t *__restrict__ B, uint32_t *__restrict__ G, double *__restrict__ X,
                  const uint64_t *__restrict__ pc, uint64_t *__restrict__ ccoord, uint32_t *__restrict__ cmask,
-                 DevIndex ix)
+                 DevIndex ix, uint32_t dense_T, uint32_t *__restrict__ n_dense_cells)
 {
     const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
@@ -156,6 +156,8 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
     if (k == 0 || keys[k - 1] != key) {
         B[h] = key;
         G[h] = (uint32_t)k;
+        // populous cell (>= dense_T points)?  one extra load: its (dense_T-1)-th successor
+        if (n_dense_cells && k + dense_T - 1 < n && keys[k + dense_T - 1] == key) atomicAdd(n_dense_cells, 1u);
         if (pc) {
             const uint64_t packed = pc[A[k]];
             ccoord[h] = packed;
@@ -182,28 +184,29 @@ template <int D>
 void launch_dim(int which, dim3 g, dim3 b, cudaStream_t s, const double *pts, uint32_t n, DevIndex &ix,
                 uint64_t *keys, uint32_t *ids, uint32_t *masks, double *part, uint32_t *nonfinite,
                 const uint32_t *A, uint32_t *pcell, uint64_t *B, uint32_t *G, double *X,
-                uint64_t *pc = nullptr, uint64_t *ccoord = nullptr, uint32_t *cmask = nullptr)
+                uint64_t *pc = nullptr, uint64_t *ccoord = nullptr, uint32_t *cmask = nullptr,
+                uint32_t *aux = nullptr)
 {
     const uint32_t mask_words = (uint32_t)((ix.mask_off[ix.d] + 31) / 32);
     if (which == 0) k_minmax<D><<<g, b, 0, s>>>(pts, n, reinterpret_cast<unsigned long long *>(part), nonfinite);
     else if (which == 1)
         k_keys<D><<<g, b, (masks && mask_words <= (uint32_t)kSmemMaskWords) ? 4 * mask_words : 0, s>>>(
             pts, n, ix, keys, ids, masks, mask_words, pc);
-    else k_compact_gather<D><<<g, b, 0, s>>>(keys, A, pts, n, pcell, B, G, X, pc, ccoord, cmask, ix);
+    else k_compact_gather<D><<<g, b, 0, s>>>(keys, A, pts, n, pcell, B, G, X, pc, ccoord, cmask, ix, 16u, aux);
     SJ_LAUNCHED();
 }
 
 void launch(int d, int which, dim3 g, dim3 b, cudaStream_t s, const double *pts, uint32_t n, DevIndex &ix,
             uint64_t *keys, uint32_t *ids, uint32_t *masks, double *part, uint32_t *nonfinite,
             const uint32_t *A, uint32_t *pcell, uint64_t *B, uint32_t *G, double *X,
-            uint64_t *pc = nullptr, uint64_t *cc = nullptr, uint32_t *cm = nullptr)
+            uint64_t *pc = nullptr, uint64_t *cc = nullptr, uint32_t *cm = nullptr, uint32_t *aux = nullptr)
 {
     switch (d) {
-    case 2: launch_dim<2>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm); break;
-    case 3: launch_dim<3>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm); break;
-    case 4: launch_dim<4>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm); break;
-    case 5: launch_dim<5>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm); break;
-    case 6: launch_dim<6>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm); break;
+    case 2: launch_dim<2>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm, aux); break;
+    case 3: launch_dim<3>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm, aux); break;
+    case 4: launch_dim<4>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm, aux); break;
+    case 5: launch_dim<5>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm, aux); break;
+    case 6: launch_dim<6>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm, aux); break;
     default: fail(SJ_ERR_DIM, "d must be in [2,6]");
     }
 }
@@ -436,7 +439,7 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
         SJ_CUDA(cudaMemcpyAsync(aux, pcell + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
         ix.masks = masks;
         launch(d, 2, grid, dim3(kThreads), s, pts, N, ix, const_cast<uint64_t *>(skeys), nullptr, nullptr, nullptr,
-               nullptr, A, pcell, B, G, X, pcs.p, ccoord, cmask);
+               nullptr, A, pcell, B, G, X, pcs.p, ccoord, cmask, aux + 2);
         ix.ccoord = ccoord;
         ix.cmask = cmask;
         ev.rec(5, s);
@@ -457,7 +460,7 @@ sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, 
         ix.masks = masks;
         idx->view = v;
         idx->dev = ix;
-        build_aux(idx, s, aux);    // directory + dense tasks; the build's only late host sync
+        build_aux(idx, s, aux, false);  // directory, bitmap, dense tasks; the build's late host sync
         ev.rec(6, s);
         SJ_CUDA(cudaStreamSynchronize(s));
         tr.mark("compact+dir+dense (synced)");
@@ -539,7 +542,7 @@ k_dense_fill(const uint32_t *__restrict__ G, const uint32_t *__restrict__ nG, ui
 //  * dense-cell tasks: every cell with >= kDenseT points is cut into tasks of <= 32 queries, one
 //    warp each in k_refine_dense.
 constexpr uint32_t kDenseT = 16;
-void build_aux(sj_index *idx, cudaStream_t s, uint32_t *aux)
+void build_aux(sj_index *idx, cudaStream_t s, uint32_t *aux, bool aux_force_dense)
 {
     sj_index_view &v = idx->view;
     DevIndex &ix = idx->dev;
@@ -585,22 +588,32 @@ void build_aux(sj_index *idx, cudaStream_t s, uint32_t *aux)
             SJ_LAUNCHED();
         }
     }
-    const uint64_t max_tasks = n / kDenseT + 1;
-    uint32_t *tasks = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * max_tasks, s));
-    idx->bufs[idx->nbufs++] = tasks;
-    {
-        Scratch<uint32_t> cnt((size_t)n + 1, s), off((size_t)n + 1, s);
-        SJ_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(uint32_t) * ((size_t)n + 1), s));
-        k_dense_count<<<gN, kThreads, 0, s>>>(v.G, aux, kDenseT, cnt.p);
-        SJ_LAUNCHED();
-        exclusive_scan_u32(cnt.p, off.p, (uint64_t)n + 1, s);
-        SJ_CUDA(cudaMemcpyAsync(aux + 1, off.p + n, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-        k_dense_fill<<<gN, kThreads, 0, s>>>(v.G, aux, kDenseT, off.p, tasks);
-        SJ_LAUNCHED();
-    }
-    uint32_t h_aux[2] = {0, 0};
+    uint32_t h_aux[3] = {0, 0, 0};
     SJ_CUDA(cudaMemcpyAsync(h_aux, aux, sizeof(h_aux), cudaMemcpyDeviceToHost, s));
     SJ_CUDA(cudaStreamSynchronize(s));
+    // dense-cell tasks in A-order, only when the compaction saw populous cells (aux[2]; the import
+    // path, which has no such count, always builds them): count, scan, fill + one more sync
+    uint32_t *tasks = nullptr;
+    if (h_aux[2] > 0 || aux_force_dense) {
+        const uint64_t nGh = h_aux[0];
+        const uint32_t gG = (uint32_t)((nGh + kThreads - 1) / kThreads);
+        Scratch<uint32_t> cnt((size_t)nGh + 1, s), off((size_t)nGh + 1, s);
+        SJ_CUDA(cudaMemsetAsync(cnt.p + nGh, 0, sizeof(uint32_t), s));
+        k_dense_count<<<gG, kThreads, 0, s>>>(v.G, aux, kDenseT, cnt.p);
+        SJ_LAUNCHED();
+        exclusive_scan_u32(cnt.p, off.p, nGh + 1, s);
+        SJ_CUDA(cudaMemcpyAsync(h_aux + 1, off.p + nGh, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        SJ_CUDA(cudaStreamSynchronize(s));
+        if (h_aux[1]) {
+            tasks = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * h_aux[1], s));
+            idx->bufs[idx->nbufs++] = tasks;
+            k_dense_fill<<<gG, kThreads, 0, s>>>(v.G, aux, kDenseT, off.p, tasks);
+            SJ_LAUNCHED();
+            SJ_CUDA(cudaStreamSynchronize(s));
+        }
+    } else {
+        h_aux[1] = 0;
+    }
     const uint32_t nG = h_aux[0];
     v.n_cells = nG;
     ix.nG = nG;
@@ -694,7 +707,7 @@ sj_index *import_index_impl(const sj_index_view &src, int device)
         uint32_t *aux = static_cast<uint32_t *>(own(4 * 4));
         const uint32_t hn[4] = {(uint32_t)nG, 0u, 0u, 0u};
         SJ_CUDA(cudaMemcpyAsync(aux, hn, sizeof(hn), cudaMemcpyHostToDevice, s));
-        build_aux(idx, s, aux);
+        build_aux(idx, s, aux, true);
     } catch (...) {
         cudaStreamDestroy(s);
         free_index_impl(idx);

@@ -313,6 +313,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         const size_t nb = cuts.size() - 1;
         tr.mark("plan");
 
+        bool work_read = false;
         float refine_ms = 0, refine_max = 0, refine_span = 0;
         uint32_t launches = 0;
         cudaEvent_t ev_span0 = cx.events[2 * S + 2];   // first refine launch start (stream 0)
@@ -378,8 +379,16 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 SJ_CUDA(cudaMemcpyAsync(hslots + si, dslots + si, sizeof(Slot), cudaMemcpyDeviceToHost, s));
             }
             tr.mark("batches launched");
+            // the work counters are read back on stream 0 after every stream's last batch, so the
+            // one round of stream syncs below also covers them
+            for (int i = 1; i < S; ++i) {
+                SJ_CUDA(cudaEventRecord(cx.events[2 * S + 3], cx.streams[i]));
+                SJ_CUDA(cudaStreamWaitEvent(s0, cx.events[2 * S + 3], 0));
+            }
+            SJ_CUDA(cudaMemcpyAsync(hwork, work, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0));
             for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
             tr.mark("batches done (synced)");
+            work_read = true;
             cudaStream_t st_sort = s0;
             for (size_t b = (nb > (size_t)S ? nb - S : 0); b < nb; ++b) drain_stream_slot(b);
             for (size_t b = 0; b < nb; ++b) {
@@ -472,9 +481,11 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
         }
 
-        // ---- work counters
-        SJ_CUDA(cudaMemcpyAsync(hwork, work, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0));
-        SJ_CUDA(cudaStreamSynchronize(s0));
+        // ---- work counters (already read back unless a retry / host mode ran more kernels)
+        if (!work_read || stats.retries || o.sort_pairs) {
+            SJ_CUDA(cudaMemcpyAsync(hwork, work, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0));
+            SJ_CUDA(cudaStreamSynchronize(s0));
+        }
         stats.cells_probed = hwork[0];
         stats.candidates_tested = hwork[1];
         stats.pairs = res->total;

@@ -169,7 +169,7 @@ struct CtxGuard {
 };
 
 // index_build.cu
-void build_aux(sj_index *idx, cudaStream_t s, uint32_t *aux);
+void build_aux(sj_index *idx, cudaStream_t s, uint32_t *aux, bool force_dense_tasks);
 sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &o);
 sj_index *import_index_impl(const sj_index_view &v, int device);
 void free_index_impl(sj_index *idx);
