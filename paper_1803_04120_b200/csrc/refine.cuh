@@ -90,6 +90,7 @@ struct QueryState {
     uint32_t pid;      // original id A[k]
     uint32_t odd;      // bit j = parity of c_j (unicomp decisions without dynamic indexing)
     uint32_t sub, G;   // this lane's rank in the query's group, group size
+    bool valid;        // dense kernel: false for helper lanes past the task's end (never emit)
     uint32_t emitted;  // pairs emitted by this lane
     uint32_t probes;   // directory / row lookups
     uint32_t tests;    // distance evaluations
@@ -181,23 +182,40 @@ __device__ __forceinline__ void scan_range(const DevIndex &ix, const JoinArgs &j
 {
     const uint32_t n = ix.n;
     if constexpr (DENSE) {
-        for (uint32_t m = m0; m < m1; ++m) {
-            double s;
-            {
-                const double t = __dsub_rn(q.x[0], __ldg(ix.X + m));
-                s = __dmul_rn(t, t);
-            }
+        // all 32 lanes are active here (helper lanes included): candidates are loaded 32 at a time,
+        // one per lane (coalesced), and broadcast with shuffles
+        for (uint32_t g = m0; g < m1; g += 32u) {
+            const uint32_t mine = g + (threadIdx.x & 31u);
+            double cx[D];
+            uint32_t cid = 0;
+            if (mine < m1) {
 #pragma unroll
-            for (int j = 1; j < D; ++j) {
-                const double t = __dsub_rn(q.x[j], __ldg(ix.X + (uint64_t)j * n + m));
-                s = __dadd_rn(s, __dmul_rn(t, t));
+                for (int j = 0; j < D; ++j) cx[j] = __ldg(ix.X + (uint64_t)j * n + mine);
+                cid = __ldg(ix.A + mine);
+            } else {
+#pragma unroll
+                for (int j = 0; j < D; ++j) cx[j] = 0.0;
             }
-            bool ok = true;
-            if (HOME) ok = BOTH ? (m > q.k) : (m != q.k);
-            q.tests += ok ? 1u : 0u;
-            const bool hit = ok && s <= ix.eps2;
-            const uint32_t qid = __ldg(ix.A + m);      // uniform address: one broadcast load
-            emit_buffered<BOTH>(ja, *wb, wmask, hit, q.pid, qid, q.emitted);
+            const uint32_t lim = min(32u, m1 - g);
+            for (uint32_t e = 0; e < lim; ++e) {
+                double s;
+                {
+                    const double t = __dsub_rn(q.x[0], __shfl_sync(0xffffffffu, cx[0], e));
+                    s = __dmul_rn(t, t);
+                }
+#pragma unroll
+                for (int j = 1; j < D; ++j) {
+                    const double t = __dsub_rn(q.x[j], __shfl_sync(0xffffffffu, cx[j], e));
+                    s = __dadd_rn(s, __dmul_rn(t, t));
+                }
+                const uint32_t qid = __shfl_sync(0xffffffffu, cid, e);
+                const uint32_t m = g + e;
+                bool ok = q.valid;
+                if (HOME) ok = ok && (BOTH ? (m > q.k) : (m != q.k));
+                q.tests += ok ? 1u : 0u;
+                const bool hit = ok && s <= ix.eps2;
+                emit_buffered<BOTH>(ja, *wb, wmask, hit, q.pid, qid, q.emitted);
+            }
         }
         return;
     }
@@ -476,7 +494,7 @@ __device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs 
 
     // ---- home cell: (p,p) once; unicomp: q after p in A-order, both orientations (R10)
     if constexpr (DENSE) {
-        emit_buffered<false>(ja, *wb, wmask, ja.include_self != 0, q.pid, q.pid, q.emitted);
+        emit_buffered<false>(ja, *wb, wmask, q.valid && ja.include_self != 0, q.pid, q.pid, q.emitted);
         scan_range<D, MODE, UNICOMP, true, true>(ix, ja, q, cs, ce, 1u, wb, wmask);
     } else {
         if (q.sub == 0) emit<MODE, false>(ja, ja.include_self != 0, q.pid, q.pid, q.emitted);
@@ -549,11 +567,12 @@ k_refine_dense(const DevIndex ix, const JoinArgs ja)
     q.G = 1u;
     q.sub = 0u;
     q.emitted = q.probes = q.tests = 0;
+    // every lane runs the (cell-uniform) enumeration; lanes past the task's end are helpers that
+    // load and broadcast candidates but never emit (they take the first query's point)
     const uint32_t k = a + lane;
-    if (k < b) {
-        refine_query<D, kEmit, UNICOMP, true>(ix, ja, k, q, tt, &wb);
-        warpbuf_flush(ja, wb, __activemask());
-    }
+    q.valid = k < b;
+    refine_query<D, kEmit, UNICOMP, true>(ix, ja, q.valid ? k : a, q, tt, &wb);
+    warpbuf_flush(ja, wb, 0xffffffffu);
     unsigned long long p = q.probes, c = q.tests, em = q.emitted;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -580,6 +599,7 @@ k_refine(const DevIndex ix, const JoinArgs ja)
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t qi = t >> ja.lanes_log2;            // query slot of this lane's group
     QueryState<D> q;
+    q.valid = true;
     q.G = 1u << ja.lanes_log2;
     q.sub = t & (q.G - 1u);
     q.emitted = q.probes = q.tests = 0;
