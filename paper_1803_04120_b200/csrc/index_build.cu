@@ -89,11 +89,13 @@ __global__ void k_minmax_init(unsigned long long *mm, int d, uint32_t *nonfinite
 // Masks M_j as one bitmap over all dimensions (bit mask_off[j] + c): when it is
 // small (<= kSmemMaskWords words) each CTA ORs into a shared copy and flushes only the non-zero
 // words, so the few hot words are not hammered by every point; otherwise global atomicOr.
+// bhist (prefix-bucket sort only): points per top-k prefix sum_j c_j * pstride_j, fused here so
+// the sort needs no histogram pass of its own.
 constexpr int kSmemMaskWords = 2048;   // 64 K bits, 8 KB of shared memory
 template <int D>
 __global__ void __launch_bounds__(kThreads)
 k_keys(const double *__restrict__ pts, uint32_t n, DevIndex ix, uint64_t *__restrict__ keys,
-       uint32_t *__restrict__ ids, uint32_t *__restrict__ masks, uint32_t mask_words, uint64_t *__restrict__ pc)
+       uint32_t *__restrict__ ids, uint32_t *__restrict__ masks, uint32_t mask_words, uint32_t *__restrict__ bhist)
 {
     extern __shared__ uint32_t s_mask[];
     const bool smem_masks = masks && mask_words <= (uint32_t)kSmemMaskWords;
@@ -103,14 +105,14 @@ k_keys(const double *__restrict__ pts, uint32_t n, DevIndex ix, uint64_t *__rest
     }
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
-        uint64_t key = 0, packed = 0;
+        uint64_t key = 0, prefix = 0;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             const double x = pts[i * D + j];
             const double t = floor(__ddiv_rn(__dsub_rn(x, ix.mins[j]), ix.w));
             const uint64_t c = 1ull + (uint64_t)t;
             key += c * ix.strides[j];
-            packed |= c << ix.cshift[j];
+            prefix += c * ix.pstride[j];
             if (masks) {
                 const uint64_t bit = ix.mask_off[j] + c;
                 if (smem_masks) atomicOr(s_mask + (bit >> 5), 1u << (bit & 31));
@@ -119,7 +121,7 @@ k_keys(const double *__restrict__ pts, uint32_t n, DevIndex ix, uint64_t *__rest
         }
         keys[i] = key;
         ids[i] = (uint32_t)i;
-        if (pc) pc[i] = packed;
+        if (bhist) atomicAdd(bhist + prefix, 1u);
     }
     if (smem_masks) {
         __syncthreads();
@@ -136,20 +138,48 @@ k_heads(const uint64_t *__restrict__ keys, uint32_t n, uint32_t *__restrict__ fl
     flags[k] = (k == 0 || keys[k] != keys[k - 1]) ? 1u : 0u;
 }
 
+// Cell coordinates from a linear id: c_j = (key / stride_j) mod |g_j|, taken from the slowest
+// dimension down (each quotient < |g_j|).  Fast path: the quotient from a double reciprocal,
+// corrected by +-1 in exact integer arithmetic (valid while quotients < 2^50 and keys < 2^63, which
+// the host checks -> ix.key_fastdiv); otherwise exact 64-bit division.
+template <int D>
+__device__ __forceinline__ void key_to_coords(const DevIndex &ix, uint64_t key, uint64_t (&c)[D])
+{
+    uint64_t rem = key;
+#pragma unroll
+    for (int j = D - 1; j >= 1; --j) {
+        const uint64_t st = ix.strides[j];
+        uint64_t q;
+        if (ix.key_fastdiv) {
+            q = (uint64_t)((double)rem * ix.inv_stride[j]);
+            if (q * st > rem) --q;
+            else if ((q + 1) * st <= rem) ++q;
+        } else {
+            q = rem / st;
+        }
+        c[j] = q;
+        rem -= q * st;
+    }
+    c[0] = rem;
+}
+
 // pcell holds the inclusive scan of head flags on entry (1-based cell number) and the
-// 0-based cell index on exit.
-// Also, at the head of each cell: its packed coordinates (from the per-point pc written by k_keys)
-// and its Alg. 1 line-6 mask word (bit j: c_j - 1 not in M_j; bit 8+j: c_j + 1 not in M_j).
+// 0-based cell index on exit.  At the head of each cell h (one thread per cell):
+//   B[h], G[h]; populous-cell count (dense tasks); its packed coordinates (decoded from the key)
+//   and Alg. 1 line-6 mask word (bit j: c_j - 1 not in M_j; bit 8+j: c_j + 1 not in M_j); the
+//   prefix-directory histogram (cells per top-k prefix) and the occupancy bit of its top-(k+1)
+//   prefix.  Every thread: the SoA gather X[j][k] = D[A[k]][j].
 template <int D>
 __global__ void __launch_bounds__(kThreads)
 k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ A,
                  const double *__restrict__ pts, uint32_t n, uint32_t *__restrict__ pcell,
                  uint64_t *__restrict__ B, uint32_t *__restrict__ G, double *__restrict__ X,
-                 const uint64_t *__restrict__ pc, uint64_t *__restrict__ ccoord, uint32_t *__restrict__ cmask,
-                 DevIndex ix, uint32_t dense_T, uint32_t *__restrict__ n_dense_cells)
+                 uint64_t *__restrict__ ccoord, uint32_t *__restrict__ cmask, DevIndex ix, uint32_t dense_T,
+                 uint32_t *__restrict__ n_dense_cells, uint32_t *__restrict__ dirhist, uint32_t *__restrict__ occ)
 {
     const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
+    const uint32_t a = A[k];
     const uint32_t h = pcell[k] - 1u;
     pcell[k] = h;
     const uint64_t key = keys[k];
@@ -158,55 +188,98 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
         G[h] = (uint32_t)k;
         // populous cell (>= dense_T points)?  one extra load: its (dense_T-1)-th successor
         if (n_dense_cells && k + dense_T - 1 < n && keys[k + dense_T - 1] == key) atomicAdd(n_dense_cells, 1u);
-        if (pc) {
-            const uint64_t packed = pc[A[k]];
-            ccoord[h] = packed;
+        uint64_t c[D];
+        key_to_coords<D>(ix, key, c);
+        if (ccoord) {
+            uint64_t packed = 0;
             uint32_t mb = 0;
-            if (ix.masks) {
 #pragma unroll
-                for (int j = 0; j < D; ++j) {
-                    const uint64_t c = (packed >> ix.cshift[j]) & ((1ull << ix.cbits[j]) - 1ull);
-                    const uint64_t lo = ix.mask_off[j] + c - 1ull, hi = lo + 2ull;
+            for (int j = 0; j < D; ++j) {
+                packed |= c[j] << ix.cshift[j];
+                if (ix.masks) {
+                    const uint64_t lo = ix.mask_off[j] + c[j] - 1ull, hi = lo + 2ull;
                     if (!((ix.masks[lo >> 5] >> (lo & 31)) & 1u)) mb |= 1u << j;
                     if (!((ix.masks[hi >> 5] >> (hi & 31)) & 1u)) mb |= 1u << (j + 8);
                 }
             }
+            ccoord[h] = packed;
             cmask[h] = mb;
+        }
+        uint64_t prefix = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) prefix += c[j] * ix.pstride[j];
+        if (dirhist) atomicAdd(dirhist + prefix, 1u);
+        if (occ) {
+            const int jo = D - ix.dir_k - 1;             // dimension d-k-1 (0-based), >= 0 when occ exists
+            uint64_t cl = c[0];
+#pragma unroll
+            for (int j = 1; j < D; ++j) if (j == jo) cl = c[j];
+            const uint64_t q = prefix * ix.occ_cpd + cl;
+            atomicOr(occ + (q >> 5), 1u << (q & 31));
         }
     }
     if (k == n - 1) G[h + 1] = n;
-    const uint64_t src = (uint64_t)A[k] * D;
+    const double *src = pts + (uint64_t)a * D;
+    if (D % 2 == 0 && (reinterpret_cast<uintptr_t>(pts) & 15u) == 0) {   // 16-B aligned rows: vector loads
 #pragma unroll
-    for (int j = 0; j < D; ++j) X[(uint64_t)j * n + k] = pts[src + j];
+        for (int j = 0; j < D; j += 2) {
+            const double2 v = *reinterpret_cast<const double2 *>(src + j);
+            X[(uint64_t)j * n + k] = v.x;
+            X[(uint64_t)(j + 1) * n + k] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) X[(uint64_t)j * n + k] = src[j];
+    }
 }
 
+
+struct BuildArgs {
+    const double *pts = nullptr;
+    uint32_t n = 0;
+    unsigned long long *mm = nullptr;
+    uint32_t *nonfinite = nullptr;
+    uint64_t *keys = nullptr;
+    uint32_t *ids = nullptr;
+    uint32_t *masks = nullptr;
+    uint32_t mask_words = 0;
+    uint32_t *bhist = nullptr;
+    const uint32_t *A = nullptr;
+    uint32_t *pcell = nullptr;
+    uint64_t *B = nullptr;
+    uint32_t *G = nullptr;
+    double *X = nullptr;
+    uint64_t *ccoord = nullptr;
+    uint32_t *cmask = nullptr;
+    uint32_t *ndense = nullptr;
+    uint32_t *dirhist = nullptr;
+    uint32_t *occ = nullptr;
+};
+
 template <int D>
-void launch_dim(int which, dim3 g, dim3 b, cudaStream_t s, const double *pts, uint32_t n, DevIndex &ix,
-                uint64_t *keys, uint32_t *ids, uint32_t *masks, double *part, uint32_t *nonfinite,
-                const uint32_t *A, uint32_t *pcell, uint64_t *B, uint32_t *G, double *X,
-                uint64_t *pc = nullptr, uint64_t *ccoord = nullptr, uint32_t *cmask = nullptr,
-                uint32_t *aux = nullptr)
+void launch_dim(int which, dim3 g, cudaStream_t s, const DevIndex &ix, const BuildArgs &a)
 {
-    const uint32_t mask_words = (uint32_t)((ix.mask_off[ix.d] + 31) / 32);
-    if (which == 0) k_minmax<D><<<g, b, 0, s>>>(pts, n, reinterpret_cast<unsigned long long *>(part), nonfinite);
-    else if (which == 1)
-        k_keys<D><<<g, b, (masks && mask_words <= (uint32_t)kSmemMaskWords) ? 4 * mask_words : 0, s>>>(
-            pts, n, ix, keys, ids, masks, mask_words, pc);
-    else k_compact_gather<D><<<g, b, 0, s>>>(keys, A, pts, n, pcell, B, G, X, pc, ccoord, cmask, ix, 16u, aux);
+    if (which == 0) {
+        k_minmax<D><<<g, kThreads, 0, s>>>(a.pts, a.n, a.mm, a.nonfinite);
+    } else if (which == 1) {
+        const bool sm = a.masks && a.mask_words <= (uint32_t)kSmemMaskWords;
+        k_keys<D><<<g, kThreads, sm ? 4 * a.mask_words : 0, s>>>(a.pts, a.n, ix, a.keys, a.ids, a.masks, a.mask_words,
+                                                                 a.bhist);
+    } else {
+        k_compact_gather<D><<<g, kThreads, 0, s>>>(a.keys, a.A, a.pts, a.n, a.pcell, a.B, a.G, a.X, a.ccoord, a.cmask,
+                                                   ix, 16u, a.ndense, a.dirhist, a.occ);
+    }
     SJ_LAUNCHED();
 }
 
-void launch(int d, int which, dim3 g, dim3 b, cudaStream_t s, const double *pts, uint32_t n, DevIndex &ix,
-            uint64_t *keys, uint32_t *ids, uint32_t *masks, double *part, uint32_t *nonfinite,
-            const uint32_t *A, uint32_t *pcell, uint64_t *B, uint32_t *G, double *X,
-            uint64_t *pc = nullptr, uint64_t *cc = nullptr, uint32_t *cm = nullptr, uint32_t *aux = nullptr)
+void launch(int d, int which, dim3 g, cudaStream_t s, const DevIndex &ix, const BuildArgs &a)
 {
     switch (d) {
-    case 2: launch_dim<2>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm, aux); break;
-    case 3: launch_dim<3>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm, aux); break;
-    case 4: launch_dim<4>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm, aux); break;
-    case 5: launch_dim<5>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm, aux); break;
-    case 6: launch_dim<6>(which, g, b, s, pts, n, ix, keys, ids, masks, part, nonfinite, A, pcell, B, G, X, pc, cc, cm, aux); break;
+    case 2: launch_dim<2>(which, g, s, ix, a); break;
+    case 3: launch_dim<3>(which, g, s, ix, a); break;
+    case 4: launch_dim<4>(which, g, s, ix, a); break;
+    case 5: launch_dim<5>(which, g, s, ix, a); break;
+    case 6: launch_dim<6>(which, g, s, ix, a); break;
     default: fail(SJ_ERR_DIM, "d must be in [2,6]");
     }
 }
@@ -257,225 +330,87 @@ void host_geometry(int d, double eps, const double *mins, const double *maxs, sj
 
 }  // namespace
 
-sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &o)
+// ---- prefix directory plan (host): DESIGN.md §6 "bounded search".  The largest k such that the
+// number of top-k coordinate prefixes P_k = prod_{j >= d-k} |g_j| stays <= max(4N, 2^16) (<= 16 B
+// per point, so the index stays O(|D|)); every B lookup of the refine is bounded to
+// one prefix's range.  The same k/P drive the prefix-bucket sort.  The occupancy bitmap over the
+// top-(k+1) prefixes is planned when it costs <= 8 B per point and filters (the +-1 window of 3
+// sub-prefixes is expected occupied with probability ~3N/P_{k+1} < 0.25: 6-D eps=1: 0.06; eps=8:
+// 0.53 -> not built).
+struct DirPlan {
+    int k = 0;
+    uint64_t P = 1;
+    uint64_t div = 1;            // stride of dimension d-k: key / div = prefix
+    bool occ = false;
+    uint64_t occ_cpd = 0, occ_div = 0;
+    size_t occ_words = 0;
+};
+
+DirPlan plan_dir(const sj_index_view &v)
 {
-    // ---- argument validation before any allocation (sj.h contract)
-    if (d < 2 || d > SJ_MAX_DIM) fail(SJ_ERR_DIM, "d must be in [2,6] (PAPER.md:391)");
-    if (!points) fail(SJ_ERR_ARG, "points is NULL");
-    if (n == 0 || n >= (1ull << 32)) fail(SJ_ERR_ARG, "N must satisfy 1 <= N < 2^32");
-    if (!std::isfinite(eps) || !(eps > 0.0)) fail(SJ_ERR_ARG, "eps must be finite and > 0");
-    {
-        volatile double e2 = eps * eps;
-        if (!std::isnormal((double)e2)) fail(SJ_ERR_ARG, "fl(eps*eps) must be a normal double");
+    DirPlan dp;
+    const int d = v.d;
+    const uint64_t n = v.n;
+    const unsigned __int128 cap = std::max<uint64_t>(4ull * n, 1ull << 16);
+    unsigned __int128 P = 1;
+    for (int kk = 1; kk <= d; ++kk) {
+        const unsigned __int128 Q = P * v.cpd[d - kk];
+        if (Q > cap) break;
+        P = Q;
+        dp.k = kk;
     }
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
-        cudaGetLastError();
-        fail(SJ_ERR_STATE, "no CUDA device available (the library has no CPU fallback)");
-    }
-    if (o.device < 0 || o.device >= ndev) fail(SJ_ERR_ARG, "bad device ordinal");
-    SJ_CUDA(cudaSetDevice(o.device));
-
-    HostTrace tr("build");
-    // the build runs on the caller's stream, or on a pooled library stream
-    CtxGuard cg{o.stream ? nullptr : acquire_ctx(o.device, 1, 0, 64)};
-    cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : cg.c->streams[0];
-
-    const uint32_t N = (uint32_t)n;
-    EventTimer ev(7);
-    ev.rec(0, s);
-
-    // ---- inputs on device
-    const double *pts = points;
-    Scratch<double> d_pts;
-    if (!o.points_on_device) {
-        d_pts.p = dalloc<double>((size_t)n * d, s);
-        d_pts.s = s;
-        SJ_CUDA(cudaMemcpyAsync(d_pts.p, points, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
-        pts = d_pts.p;
-    }
-    ev.rec(1, s);
-
-    // ---- a1: exact per-dimension min/max + finiteness (one kernel, integer atomics)
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device);
-    const uint32_t parts = (uint32_t)std::min<uint64_t>((n + kThreads - 1) / kThreads, (uint64_t)nsm * 4);
-    Scratch<unsigned long long> mm(2 * d, s);
-    Scratch<uint32_t> nonfinite(1, s);
-    k_minmax_init<<<1, 32, 0, s>>>(mm.p, d, nonfinite.p);
-    SJ_LAUNCHED();
-    DevIndex ix{};
-    ix.d = d;
-    ix.n = N;
-    launch(d, 0, dim3(parts), dim3(kThreads), s, pts, N, ix, nullptr, nullptr, nullptr,
-           reinterpret_cast<double *>(mm.p), nonfinite.p, nullptr, nullptr, nullptr, nullptr, nullptr);
-    unsigned long long h_ord[2 * SJ_MAX_DIM];
-    uint32_t h_bad = 0;
-    SJ_CUDA(cudaMemcpyAsync(h_ord, mm.p, sizeof(unsigned long long) * 2 * d, cudaMemcpyDeviceToHost, s));
-    SJ_CUDA(cudaMemcpyAsync(&h_bad, nonfinite.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    SJ_CUDA(cudaStreamSynchronize(s));
-    ev.rec(2, s);
-    tr.mark("minmax (synced)");
-    if (h_bad) fail(SJ_ERR_NONFINITE, "a coordinate is NaN or infinite");
-    double h_mm[2 * SJ_MAX_DIM];
-    for (int t = 0; t < 2 * d; ++t) {
-        const unsigned long long k = h_ord[t];
-        const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
-        std::memcpy(&h_mm[t], &u, sizeof(double));
-    }
-
-    sj_index_view v{};
-    v.d = d;
-    v.device = o.device;
-    v.n = n;
-    v.eps = eps;
-    {
-        volatile double e2 = eps * eps;
-        v.eps2 = e2;
-    }
-    for (int j = 0; j < d; ++j) v.mins[j] = h_mm[j];
-    host_geometry(d, eps, h_mm, h_mm + d, v);
-
-    ix.w = v.w;
-    ix.eps2 = v.eps2;
-    for (int j = 0; j < d; ++j) {
-        ix.mins[j] = v.mins[j];
-        ix.cpd[j] = v.cpd[j];
-        ix.strides[j] = v.strides[j];
-    }
-    // masks: one bitmap, |g_j| bits per dimension, only when <= 2^30 bits (they never change S)
-    uint64_t mask_total = 0;
-    bool want_masks = o.build_masks != 0;
-    for (int j = 0; j < d; ++j) {
-        v.mask_offsets[j] = mask_total;
-        mask_total += v.cpd[j];
-        if (mask_total > (1ull << 30)) want_masks = false;
-    }
-    v.mask_offsets[d] = mask_total;
-    for (int j = 0; j <= d; ++j) ix.mask_off[j] = v.mask_offsets[j];
-    // packed per-cell coordinates (c_j at bit cshift[j]) when the widths fit 64 bits
-    bool pack_fits = true;
-    {
-        uint32_t sh = 0;
-        for (int j = 0; j < d; ++j) {
-            uint32_t b = 0;
-            while (b < 64 && ((v.cpd[j] - 1) >> b)) ++b;
-            ix.cbits[j] = b;
-            ix.cshift[j] = sh;
-            sh += b;
+    dp.P = (uint64_t)P;
+    for (int j = 0; j < d - dp.k; ++j) dp.div *= v.cpd[j];
+    if (dp.k >= 1 && dp.k < d) {
+        const unsigned __int128 P1 = P * v.cpd[d - dp.k - 1];
+        if (P1 <= (unsigned __int128)64 * std::max<uint64_t>(n, 1ull << 16) &&
+            3.0 * (double)n < 0.25 * (double)(uint64_t)P1) {
+            dp.occ = true;
+            dp.occ_cpd = v.cpd[d - dp.k - 1];
+            dp.occ_div = dp.div / dp.occ_cpd;
+            dp.occ_words = (size_t)((P1 + 31) / 32);
         }
-        pack_fits = sh <= 64;
     }
+    return dp;
+}
 
-    // ---- a2: keys
-    sj_index *idx = new sj_index();
-    idx->device = o.device;
-    auto own = [&](void *p) { idx->bufs[idx->nbufs++] = p; return p; };
-    try {
-        uint32_t *masks = nullptr;
-        const size_t mask_bytes = 4 * ((mask_total + 31) / 32);
-        if (want_masks) {
-            masks = static_cast<uint32_t *>(own(dev_alloc(mask_bytes, s)));
-            SJ_CUDA(cudaMemsetAsync(masks, 0, mask_bytes, s));
-        }
-        Scratch<uint64_t> keys(n, s), keys_tmp(n, s);
-        uint32_t *A = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
-        Scratch<uint32_t> ids_tmp(n, s);
-        const dim3 grid((unsigned)((n + kThreads - 1) / kThreads));
-        Scratch<uint64_t> pcs;
-        uint64_t *ccoord = nullptr;
-        uint32_t *cmask = nullptr;
-        if (pack_fits) {
-            pcs.p = dalloc<uint64_t>(n, s);
-            pcs.s = s;
-            ccoord = static_cast<uint64_t *>(own(dev_alloc(sizeof(uint64_t) * n, s)));
-            cmask = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
-        }
-        launch(d, 1, grid, dim3(kThreads), s, pts, N, ix, keys.p, A, masks, nullptr, nullptr, nullptr, nullptr,
-               nullptr, nullptr, nullptr, pcs.p, nullptr, nullptr);
-        ev.rec(3, s);
+// Geometry-derived constants of the directory in kernel form.
+void apply_dir_geometry(DevIndex &ix, const sj_index_view &v, const DirPlan &dp)
+{
+    const int d = v.d;
+    ix.dir_k = dp.k;
+    ix.dir_P = dp.P;
+    ix.dir_div = dp.div;
+    for (int j = 0; j < SJ_MAX_DIM; ++j) ix.pstride[j] = (j < d && j >= d - dp.k) ? v.strides[j] / dp.div : 0;
+    uint32_t ntop = 1;
+    for (int j = 0; j < dp.k; ++j) ntop *= 3;
+    ix.dir_ntop = ntop;
+    for (int j = 0; j < d; ++j) ix.inv_cpd[j] = 1.0 / (double)v.cpd[j];
+    ix.lowR[0] = 0;
+    for (int j = 0; j < d; ++j) ix.lowR[j + 1] = ix.lowR[j] + (int64_t)(j < d - dp.k ? v.strides[j] : 0);
+    ix.occ_div = dp.occ ? dp.occ_div : 0;
+    ix.occ_cpd = dp.occ ? dp.occ_cpd : 0;
+    // key -> coordinates by double reciprocals when every quotient < 2^50 and keys < 2^63
+    bool fast = v.key_bits <= 63;
+    for (int j = 1; j < d; ++j) fast = fast && v.cpd[j] < (1ull << 50);
+    ix.key_fastdiv = fast ? 1 : 0;
+    for (int j = 0; j < d; ++j) ix.inv_stride[j] = 1.0 / (double)v.strides[j];
+}
 
-        // ---- a3: sort of (key, id) into (key, id)-ascending order (= stable sort by key, R14).
-        // Sparse keys (<= 2 points per top-k prefix on average, prefixes <= 4N): prefix buckets +
-        // per-bucket sort; otherwise (or when a bucket is large) stable LSD radix sort.
-        bool in_tmp = false;
-        bool sorted = false;
-        {
-            const unsigned __int128 cap = std::max<uint64_t>(4ull * n, 1ull << 16);
-            unsigned __int128 P = 1;
-            int k = 0;
-            for (int kk = 1; kk <= d; ++kk) {
-                const unsigned __int128 Q = P * v.cpd[d - kk];
-                if (Q > cap) break;
-                P = Q;
-                k = kk;
-            }
-            // (bucket arrays stay L2-sized: P <= 2^22; measured slower than LSD at P = 11.4 M)
-            if (k >= 1 && (double)n <= 2.0 * (double)(uint64_t)P && P <= ((unsigned __int128)1 << 22)) {
-                uint64_t div = 1;
-                for (int j = 0; j < d - k; ++j) div *= v.cpd[j];
-                sorted = bucket_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, div, (uint64_t)P, s);
-            }
-        }
-        if (!sorted) radix_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, v.key_bits, s, &in_tmp);
-        const uint64_t *skeys = in_tmp ? keys_tmp.p : keys.p;
-        if (in_tmp) SJ_CUDA(cudaMemcpyAsync(A, ids_tmp.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
-        ev.rec(4, s);
-
-        // ---- a4: heads, cell numbering, compaction, SoA gather.  B and G are sized for the upper
-        // bound N cells so no host round trip is needed here; |G| is read back by build_aux's sync.
-        uint32_t *pcell = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
-        {
-            Scratch<uint32_t> flags(n, s);
-            k_heads<<<grid, kThreads, 0, s>>>(skeys, N, flags.p);
-            SJ_LAUNCHED();
-            inclusive_scan_u32(flags.p, pcell, n, s);
-        }
-        uint64_t *B = static_cast<uint64_t *>(own(dev_alloc(sizeof(uint64_t) * n, s)));
-        uint32_t *G = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * ((size_t)n + 1), s)));
-        double *X = static_cast<double *>(own(dev_alloc(sizeof(double) * n * d, s)));
-        uint32_t *aux = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * 4, s)));  // [0]=|G| [1]=#dense tasks
-        SJ_CUDA(cudaMemsetAsync(aux, 0, sizeof(uint32_t) * 4, s));
-        SJ_CUDA(cudaMemcpyAsync(aux, pcell + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-        ix.masks = masks;
-        launch(d, 2, grid, dim3(kThreads), s, pts, N, ix, const_cast<uint64_t *>(skeys), nullptr, nullptr, nullptr,
-               nullptr, A, pcell, B, G, X, pcs.p, ccoord, cmask, aux + 2);
-        ix.ccoord = ccoord;
-        ix.cmask = cmask;
-        ev.rec(5, s);
-
-        v.n_cells = n;            // provisional upper bound until build_aux() reads |G|
-        v.B = B;
-        v.G = G;
-        v.A = A;
-        v.pcell = pcell;
-        v.X = X;
-        v.masks = masks;
-        ix.nG = N;
-        ix.B = B;
-        ix.G = G;
-        ix.A = A;
-        ix.pcell = pcell;
-        ix.X = X;
-        ix.masks = masks;
-        idx->view = v;
-        idx->dev = ix;
-        build_aux(idx, s, aux, false);  // directory, bitmap, dense tasks; the build's late host sync
-        ev.rec(6, s);
-        SJ_CUDA(cudaStreamSynchronize(s));
-        tr.mark("compact+dir+dense (synced)");
-        idx->view.t_h2d_ms = ev.ms(0, 1);
-        idx->view.t_geometry_ms = ev.ms(1, 2);
-        idx->view.t_keys_ms = ev.ms(2, 3);
-        idx->view.t_sort_ms = ev.ms(3, 4);
-        idx->view.t_compact_ms = ev.ms(4, 6);
-        idx->view.t_total_ms = ev.ms(0, 6);
-    } catch (...) {
-        cudaStreamSynchronize(s);
-        free_index_impl(idx);
-        throw;
+// dir (P+1 entries) and the occupancy bitmap (zeroed), owned by the index.
+void alloc_dir(sj_index *idx, const DirPlan &dp, cudaStream_t s)
+{
+    uint32_t *dir = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * ((size_t)dp.P + 1), s));
+    idx->bufs[idx->nbufs++] = dir;
+    idx->view.dir = dir;
+    idx->dev.dir = dir;
+    idx->dev.occ = nullptr;
+    if (dp.occ) {
+        uint32_t *occ = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * dp.occ_words, s));
+        idx->bufs[idx->nbufs++] = occ;
+        SJ_CUDA(cudaMemsetAsync(occ, 0, sizeof(uint32_t) * dp.occ_words, s));
+        idx->dev.occ = occ;
     }
-    return idx;
 }
 
 namespace {
@@ -533,68 +468,24 @@ k_dense_fill(const uint32_t *__restrict__ G, const uint32_t *__restrict__ nG, ui
 }
 }  // namespace
 
-// Auxiliary structures built on the device from B/G, with the cell count |G| = aux[0] known only on
-// the device; the single host sync at the end reads |G| and the dense-task count.
-//  * prefix directory (DESIGN.md §6 "bounded search"): the largest k such that the number of top-k
-//    coordinate prefixes P_k = prod_{j >= d-k} |g_j| stays <= max(4N, 2^16) (<= 16 B per point, so
-//    the index stays O(|D|)); every B lookup of the refine is a binary search bounded
-//    to one prefix's range.
-//  * dense-cell tasks: every cell with >= kDenseT points is cut into tasks of <= 32 queries, one
-//    warp each in k_refine_dense.
+
+// Device-built directory -> dir (exclusive scan of the per-prefix cell histogram); then the single
+// host sync reads |G| (aux[0]), the populous-cell count (aux[2]) and the bucket-sort overflow flag
+// (aux[3]) into h_aux.  Dense-cell tasks (cells with >= kDenseT points cut into <= 32-query tasks,
+// one warp each in k_refine_dense) are built in A-order when the compaction saw populous cells (the
+// import path, which has no such count, always builds them).
 constexpr uint32_t kDenseT = 16;
-void build_aux(sj_index *idx, cudaStream_t s, uint32_t *aux, bool aux_force_dense)
+void finish_aux(sj_index *idx, cudaStream_t s, uint32_t *aux, const DirPlan &dp, const uint32_t *dirhist,
+                bool force_dense, uint32_t *h_aux)
 {
     sj_index_view &v = idx->view;
     DevIndex &ix = idx->dev;
-    const int d = v.d;
-    const uint64_t n = v.n;
-    const unsigned __int128 cap = std::max<uint64_t>(4ull * n, 1ull << 16);
-    int k = 0;
-    unsigned __int128 P = 1;
-    for (int kk = 1; kk <= d; ++kk) {
-        const unsigned __int128 Q = P * v.cpd[d - kk];
-        if (Q > cap) break;
-        P = Q;
-        k = kk;
-    }
-    uint64_t div = 1;
-    for (int j = 0; j < d - k; ++j) div *= v.cpd[j];   // = strides[d-k] (or prod all for k=0)
-    uint32_t *dir = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * ((size_t)P + 1), s));
-    idx->bufs[idx->nbufs++] = dir;
-    const uint32_t gN = (uint32_t)((n + kThreads - 1) / kThreads);
-    {
-        Scratch<uint32_t> hist((size_t)P + 1, s);
-        SJ_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(uint32_t) * ((size_t)P + 1), s));
-        k_dir_hist<<<gN, kThreads, 0, s>>>(v.B, aux, div, 1.0 / (double)div, hist.p);
-        SJ_LAUNCHED();
-        exclusive_scan_u32(hist.p, dir, (uint64_t)P + 1, s);
-    }
-    // occupancy bitmap over the top-(k+1) prefixes when it costs <= 8 bytes per point
-    uint32_t *occ = nullptr;
-    uint64_t occ_div = 0, occ_cpd = 0;
-    if (k >= 1 && k < d) {
-        const unsigned __int128 P1 = P * v.cpd[d - k - 1];
-        // ... and when it filters: the +-1 window of 3 sub-prefixes is expected to be occupied
-        // with probability ~3N/P1 (< 0.25 here; 6-D eps=1: 0.06, eps=8: 0.53 -> not built)
-        if (P1 <= (unsigned __int128)64 * std::max<uint64_t>(n, 1ull << 16) &&
-            3.0 * (double)n < 0.25 * (double)(uint64_t)P1) {
-            occ_cpd = v.cpd[d - k - 1];
-            occ_div = div / occ_cpd;                      // = stride of dim d-k-1
-            const size_t words = (size_t)((P1 + 31) / 32);
-            occ = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * words, s));
-            idx->bufs[idx->nbufs++] = occ;
-            SJ_CUDA(cudaMemsetAsync(occ, 0, sizeof(uint32_t) * words, s));
-            k_occ_bits<<<gN, kThreads, 0, s>>>(v.B, aux, occ_div, 1.0 / (double)occ_div, occ);
-            SJ_LAUNCHED();
-        }
-    }
-    uint32_t h_aux[3] = {0, 0, 0};
-    SJ_CUDA(cudaMemcpyAsync(h_aux, aux, sizeof(h_aux), cudaMemcpyDeviceToHost, s));
+    exclusive_scan_u32(dirhist, const_cast<uint32_t *>(ix.dir), (uint64_t)dp.P + 1, s);
+    SJ_CUDA(cudaMemcpyAsync(h_aux, aux, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     SJ_CUDA(cudaStreamSynchronize(s));
-    // dense-cell tasks in A-order, only when the compaction saw populous cells (aux[2]; the import
-    // path, which has no such count, always builds them): count, scan, fill + one more sync
     uint32_t *tasks = nullptr;
-    if (h_aux[2] > 0 || aux_force_dense) {
+    uint32_t ntasks = 0;
+    if (!h_aux[3] && (h_aux[2] > 0 || force_dense)) {
         const uint64_t nGh = h_aux[0];
         const uint32_t gG = (uint32_t)((nGh + kThreads - 1) / kThreads);
         Scratch<uint32_t> cnt((size_t)nGh + 1, s), off((size_t)nGh + 1, s);
@@ -602,47 +493,285 @@ void build_aux(sj_index *idx, cudaStream_t s, uint32_t *aux, bool aux_force_dens
         k_dense_count<<<gG, kThreads, 0, s>>>(v.G, aux, kDenseT, cnt.p);
         SJ_LAUNCHED();
         exclusive_scan_u32(cnt.p, off.p, nGh + 1, s);
-        SJ_CUDA(cudaMemcpyAsync(h_aux + 1, off.p + nGh, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        SJ_CUDA(cudaMemcpyAsync(&ntasks, off.p + nGh, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         SJ_CUDA(cudaStreamSynchronize(s));
-        if (h_aux[1]) {
-            tasks = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * h_aux[1], s));
+        if (ntasks) {
+            tasks = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * ntasks, s));
             idx->bufs[idx->nbufs++] = tasks;
             k_dense_fill<<<gG, kThreads, 0, s>>>(v.G, aux, kDenseT, off.p, tasks);
             SJ_LAUNCHED();
             SJ_CUDA(cudaStreamSynchronize(s));
         }
-    } else {
-        h_aux[1] = 0;
     }
+    h_aux[1] = ntasks;
     const uint32_t nG = h_aux[0];
     v.n_cells = nG;
     ix.nG = nG;
-    v.dir_k = k;
-    v.dir_entries = (uint64_t)P + 1;
-    v.dir = dir;
-    ix.dir = dir;
-    ix.dir_k = k;
-    ix.dir_P = (uint64_t)P;
-    ix.dir_div = div;
-    for (int j = 0; j < SJ_MAX_DIM; ++j) ix.pstride[j] = (j < d && j >= d - k) ? v.strides[j] / div : 0;
-    uint32_t ntop = 1;
-    for (int j = 0; j < k; ++j) ntop *= 3;
-    ix.dir_ntop = ntop;
-    for (int j = 0; j < d; ++j) ix.inv_cpd[j] = 1.0 / (double)v.cpd[j];
-    ix.lowR[0] = 0;
-    for (int j = 0; j < d; ++j) ix.lowR[j + 1] = ix.lowR[j] + (int64_t)(j < d - k ? v.strides[j] : 0);
+    v.dir_k = dp.k;
+    v.dir_entries = dp.P + 1;
+    v.dir = ix.dir;
     // mode: a dense directory gives O(1) rows; small prefix ranges (<= 8 cells on average) are
     // cheapest to scan cell by cell (sparse high-d data); otherwise bounded row searches.
-    const double avg_range = (double)nG / (double)(uint64_t)P;
-    if (k == d) ix.search_mode = kSearchDenseRows;
-    else if (avg_range <= 8.0 && (double)div < 4.0e15) ix.search_mode = kSearchCellScan;
+    const double avg_range = (double)nG / (double)dp.P;
+    if (dp.k == v.d) ix.search_mode = kSearchDenseRows;
+    else if (avg_range <= 8.0 && (double)dp.div < 4.0e15) ix.search_mode = kSearchCellScan;
     else ix.search_mode = kSearchRows;
-    ix.occ = occ;
-    ix.occ_div = occ_div;
-    ix.occ_cpd = occ_cpd;
     ix.dense_tasks = tasks;
-    ix.n_dense_tasks = h_aux[1];
+    ix.n_dense_tasks = ntasks;
     ix.dense_T = kDenseT;
+}
+
+
+
+sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps, const sj_build_opts &o,
+                            bool allow_bucket);
+
+sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &o)
+{
+    return build_index_impl2(points, n, d, eps, o, true);
+}
+
+sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps, const sj_build_opts &o,
+                            bool allow_bucket)
+{
+    // ---- argument validation before any allocation (sj.h contract)
+    if (d < 2 || d > SJ_MAX_DIM) fail(SJ_ERR_DIM, "d must be in [2,6] (PAPER.md:391)");
+    if (!points) fail(SJ_ERR_ARG, "points is NULL");
+    if (n == 0 || n >= (1ull << 32)) fail(SJ_ERR_ARG, "N must satisfy 1 <= N < 2^32");
+    if (!std::isfinite(eps) || !(eps > 0.0)) fail(SJ_ERR_ARG, "eps must be finite and > 0");
+    {
+        volatile double e2 = eps * eps;
+        if (!std::isnormal((double)e2)) fail(SJ_ERR_ARG, "fl(eps*eps) must be a normal double");
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        fail(SJ_ERR_STATE, "no CUDA device available (the library has no CPU fallback)");
+    }
+    if (o.device < 0 || o.device >= ndev) fail(SJ_ERR_ARG, "bad device ordinal");
+    SJ_CUDA(cudaSetDevice(o.device));
+
+    HostTrace tr("build");
+    // the build runs on the caller's stream, or on a pooled library stream
+    CtxGuard cg{o.stream ? nullptr : acquire_ctx(o.device, 1, 0, 64)};
+    cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : cg.c->streams[0];
+
+    const uint32_t N = (uint32_t)n;
+    EventTimer ev(7);
+    ev.rec(0, s);
+
+    // ---- inputs on device
+    const double *pts = points;
+    Scratch<double> d_pts;
+    if (!o.points_on_device) {
+        d_pts.p = dalloc<double>((size_t)n * d, s);
+        d_pts.s = s;
+        SJ_CUDA(cudaMemcpyAsync(d_pts.p, points, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
+        pts = d_pts.p;
+    }
+    ev.rec(1, s);
+
+    // ---- a1: exact per-dimension min/max + finiteness (one kernel, integer atomics); one D2H copy
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device);
+    const uint32_t parts = (uint32_t)std::min<uint64_t>((n + kThreads - 1) / kThreads, (uint64_t)nsm * 4);
+    Scratch<unsigned long long> mm(2 * d + 1, s);       // [2d] = non-finite flag
+    k_minmax_init<<<1, 32, 0, s>>>(mm.p, d, reinterpret_cast<uint32_t *>(mm.p + 2 * d));
+    SJ_LAUNCHED();
+    DevIndex ix{};
+    ix.d = d;
+    ix.n = N;
+    BuildArgs ba;
+    ba.pts = pts;
+    ba.n = N;
+    ba.mm = mm.p;
+    ba.nonfinite = reinterpret_cast<uint32_t *>(mm.p + 2 * d);
+    launch(d, 0, dim3(parts), s, ix, ba);
+    unsigned long long h_ord[2 * SJ_MAX_DIM + 1];
+    SJ_CUDA(cudaMemcpyAsync(h_ord, mm.p, sizeof(unsigned long long) * (2 * d + 1), cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaStreamSynchronize(s));
+    ev.rec(2, s);
+    tr.mark("minmax (synced)");
+    if ((uint32_t)h_ord[2 * d]) fail(SJ_ERR_NONFINITE, "a coordinate is NaN or infinite");
+    double h_mm[2 * SJ_MAX_DIM];
+    for (int t = 0; t < 2 * d; ++t) {
+        const unsigned long long k = h_ord[t];
+        const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+        std::memcpy(&h_mm[t], &u, sizeof(double));
+    }
+
+    sj_index_view v{};
+    v.d = d;
+    v.device = o.device;
+    v.n = n;
+    v.eps = eps;
+    {
+        volatile double e2 = eps * eps;
+        v.eps2 = e2;
+    }
+    for (int j = 0; j < d; ++j) v.mins[j] = h_mm[j];
+    host_geometry(d, eps, h_mm, h_mm + d, v);
+
+    ix.w = v.w;
+    ix.eps2 = v.eps2;
+    for (int j = 0; j < d; ++j) {
+        ix.mins[j] = v.mins[j];
+        ix.cpd[j] = v.cpd[j];
+        ix.strides[j] = v.strides[j];
+    }
+    // masks: one bitmap, |g_j| bits per dimension, only when <= 2^30 bits (they never change S)
+    uint64_t mask_total = 0;
+    bool want_masks = o.build_masks != 0;
+    for (int j = 0; j < d; ++j) {
+        v.mask_offsets[j] = mask_total;
+        mask_total += v.cpd[j];
+        if (mask_total > (1ull << 30)) want_masks = false;
+    }
+    v.mask_offsets[d] = mask_total;
+    for (int j = 0; j <= d; ++j) ix.mask_off[j] = v.mask_offsets[j];
+    // packed per-cell coordinates (c_j at bit cshift[j]) when the widths fit 64 bits
+    bool pack_fits = true;
+    {
+        uint32_t sh = 0;
+        for (int j = 0; j < d; ++j) {
+            uint32_t b = 0;
+            while (b < 64 && ((v.cpd[j] - 1) >> b)) ++b;
+            ix.cbits[j] = b;
+            ix.cshift[j] = sh;
+            sh += b;
+        }
+        pack_fits = sh <= 64;
+    }
+    const DirPlan dp = plan_dir(v);
+    apply_dir_geometry(ix, v, dp);
+    // a3 strategy: sparse keys (<= 2 points per top-k prefix on average, P <= 2^22 so the bucket
+    // arrays stay L2-sized; measured slower than LSD at P = 11.4 M) -> prefix buckets + per-bucket
+    // sort; otherwise stable LSD radix sort
+    const bool use_bucket = allow_bucket && dp.k >= 1 && (double)n <= 2.0 * (double)dp.P && dp.P <= (1ull << 22);
+
+    sj_index *idx = new sj_index();
+    idx->device = o.device;
+    auto own = [&](void *p) { idx->bufs[idx->nbufs++] = p; return p; };
+    uint32_t h_aux[4] = {0, 0, 0, 0};
+    try {
+        // aux: [0] = |G|, [1] = #dense tasks, [2] = #populous cells, [3] = bucket-sort overflow
+        uint32_t *aux = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * 4, s)));
+        SJ_CUDA(cudaMemsetAsync(aux, 0, sizeof(uint32_t) * 4, s));
+        uint32_t *masks = nullptr;
+        const size_t mask_bytes = 4 * ((mask_total + 31) / 32);
+        if (want_masks) {
+            masks = static_cast<uint32_t *>(own(dev_alloc(mask_bytes, s)));
+            SJ_CUDA(cudaMemsetAsync(masks, 0, mask_bytes, s));
+        }
+        Scratch<uint64_t> keys(n, s), keys_tmp(n, s);
+        uint32_t *A = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
+        Scratch<uint32_t> ids_tmp(n, s);
+        Scratch<uint32_t> bhist;
+        if (use_bucket) {
+            bhist.p = dalloc<uint32_t>((size_t)dp.P + 1, s);
+            bhist.s = s;
+            SJ_CUDA(cudaMemsetAsync(bhist.p, 0, sizeof(uint32_t) * ((size_t)dp.P + 1), s));
+        }
+        const dim3 grid((unsigned)((n + kThreads - 1) / kThreads));
+
+        // ---- a2: keys (+ masks, + prefix histogram of the bucket sort)
+        ba.keys = keys.p;
+        ba.ids = A;
+        ba.masks = masks;
+        ba.mask_words = (uint32_t)((mask_total + 31) / 32);
+        ba.bhist = bhist.p;
+        launch(d, 1, grid, s, ix, ba);
+        ev.rec(3, s);
+
+        // ---- a3: sort of (key, id) into (key, id)-ascending order (= stable sort by key, R14)
+        bool in_tmp = false;
+        if (use_bucket) bucket_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, dp.div, dp.P, bhist.p, aux + 3, s);
+        else radix_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, v.key_bits, s, &in_tmp);
+        const uint64_t *skeys = in_tmp ? keys_tmp.p : keys.p;
+        if (in_tmp) SJ_CUDA(cudaMemcpyAsync(A, ids_tmp.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
+        ev.rec(4, s);
+
+        // ---- a4: heads, cell numbering, compaction, SoA gather, directory histogram, occupancy
+        // bits.  B and G are sized for the upper bound N cells so no host round trip is needed
+        // here; |G| is read back by the single sync of finish_aux.
+        uint32_t *pcell = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
+        {
+            Scratch<uint32_t> flags(n, s);
+            k_heads<<<grid, kThreads, 0, s>>>(skeys, N, flags.p);
+            SJ_LAUNCHED();
+            inclusive_scan_u32(flags.p, pcell, n, s);
+        }
+        uint64_t *B = static_cast<uint64_t *>(own(dev_alloc(sizeof(uint64_t) * n, s)));
+        uint32_t *G = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * ((size_t)n + 1), s)));
+        double *X = static_cast<double *>(own(dev_alloc(sizeof(double) * n * d, s)));
+        uint64_t *ccoord = nullptr;
+        uint32_t *cmask = nullptr;
+        if (pack_fits) {
+            ccoord = static_cast<uint64_t *>(own(dev_alloc(sizeof(uint64_t) * n, s)));
+            cmask = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
+        }
+        idx->view = v;
+        alloc_dir(idx, dp, s);
+        Scratch<uint32_t> dirhist((size_t)dp.P + 1, s);
+        SJ_CUDA(cudaMemsetAsync(dirhist.p, 0, sizeof(uint32_t) * ((size_t)dp.P + 1), s));
+        SJ_CUDA(cudaMemcpyAsync(aux, pcell + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        ix.masks = masks;
+        ix.occ = idx->dev.occ;
+        ix.dir = idx->dev.dir;
+        ba.keys = const_cast<uint64_t *>(skeys);
+        ba.A = A;
+        ba.pcell = pcell;
+        ba.B = B;
+        ba.G = G;
+        ba.X = X;
+        ba.ccoord = ccoord;
+        ba.cmask = cmask;
+        ba.ndense = aux + 2;
+        ba.dirhist = dirhist.p;
+        ba.occ = const_cast<uint32_t *>(ix.occ);
+        launch(d, 2, grid, s, ix, ba);
+        ix.ccoord = ccoord;
+        ix.cmask = cmask;
+        ev.rec(5, s);
+
+        v.n_cells = n;            // provisional upper bound until finish_aux() reads |G|
+        v.B = B;
+        v.G = G;
+        v.A = A;
+        v.pcell = pcell;
+        v.X = X;
+        v.masks = masks;
+        v.dir = ix.dir;
+        ix.nG = N;
+        ix.B = B;
+        ix.G = G;
+        ix.A = A;
+        ix.pcell = pcell;
+        ix.X = X;
+        idx->view = v;
+        idx->dev = ix;
+        finish_aux(idx, s, aux, dp, dirhist.p, false, h_aux);   // the build's late host sync
+        ev.rec(6, s);
+        SJ_CUDA(cudaStreamSynchronize(s));
+        tr.mark("compact+dir+dense (synced)");
+        idx->view.t_h2d_ms = ev.ms(0, 1);
+        idx->view.t_geometry_ms = ev.ms(1, 2);
+        idx->view.t_keys_ms = ev.ms(2, 3);
+        idx->view.t_sort_ms = ev.ms(3, 4);
+        idx->view.t_compact_ms = ev.ms(4, 6);
+        idx->view.t_total_ms = ev.ms(0, 6);
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        free_index_impl(idx);
+        throw;
+    }
+    if (h_aux[3]) {
+        // a prefix bucket held more than the shared-memory sorter takes: rebuild with the LSD sort
+        tr.mark("bucket overflow -> LSD rebuild");
+        free_index_impl(idx);
+        return build_index_impl2(points, n, d, eps, o, false);
+    }
+    return idx;
 }
 
 void free_index_impl(sj_index *idx)
@@ -653,6 +782,7 @@ void free_index_impl(sj_index *idx)
     cudaDeviceSynchronize();
     delete idx;
 }
+
 
 sj_index *import_index_impl(const sj_index_view &src, int device)
 {
@@ -687,7 +817,6 @@ sj_index *import_index_impl(const sj_index_view &src, int device)
             masks = static_cast<uint32_t *>(own(mb));
             SJ_CUDA(cudaMemcpyAsync(masks, src.masks, mb, cudaMemcpyDefault, s));
         }
-        SJ_CUDA(cudaStreamSynchronize(s));
         v.B = B; v.G = G; v.A = A; v.pcell = pcell; v.X = X; v.masks = masks;
         DevIndex ix{};
         ix.d = d;
@@ -702,12 +831,27 @@ sj_index *import_index_impl(const sj_index_view &src, int device)
         }
         for (int j = 0; j <= d; ++j) ix.mask_off[j] = v.mask_offsets[j];
         ix.B = B; ix.G = G; ix.A = A; ix.pcell = pcell; ix.X = X; ix.masks = masks;
+        const DirPlan dp = plan_dir(v);
+        apply_dir_geometry(ix, v, dp);
         idx->view = v;
         idx->dev = ix;
+        alloc_dir(idx, dp, s);
         uint32_t *aux = static_cast<uint32_t *>(own(4 * 4));
         const uint32_t hn[4] = {(uint32_t)nG, 0u, 0u, 0u};
         SJ_CUDA(cudaMemcpyAsync(aux, hn, sizeof(hn), cudaMemcpyHostToDevice, s));
-        build_aux(idx, s, aux, true);
+        // directory histogram and occupancy bits from B (the build fuses these into its compaction)
+        Scratch<uint32_t> hist((size_t)dp.P + 1, s);
+        SJ_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(uint32_t) * ((size_t)dp.P + 1), s));
+        const uint32_t gN = (uint32_t)((nG + kThreads - 1) / kThreads);
+        k_dir_hist<<<gN, kThreads, 0, s>>>(B, aux, dp.div, 1.0 / (double)dp.div, hist.p);
+        SJ_LAUNCHED();
+        if (idx->dev.occ) {
+            k_occ_bits<<<gN, kThreads, 0, s>>>(B, aux, dp.occ_div, 1.0 / (double)dp.occ_div,
+                                               const_cast<uint32_t *>(idx->dev.occ));
+            SJ_LAUNCHED();
+        }
+        uint32_t h_aux[4];
+        finish_aux(idx, s, aux, dp, hist.p, true, h_aux);
     } catch (...) {
         cudaStreamDestroy(s);
         free_index_impl(idx);

@@ -174,7 +174,7 @@ k_scan_sums(uint32_t *__restrict__ sums, uint64_t m)
 template <bool INCLUSIVE>
 __global__ void __launch_bounds__(kScanThreads)
 k_scan_apply(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, uint64_t n,
-             const uint32_t *__restrict__ block_off)
+             const uint32_t *__restrict__ block_off, uint32_t *__restrict__ out2)
 {
     __shared__ uint32_t s_warp[32];
     // each thread owns kScanItems consecutive items
@@ -192,12 +192,16 @@ k_scan_apply(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, uint64
     for (int r = 0; r < kScanItems; ++r) {
         uint64_t i = base + r;
         if (INCLUSIVE) run += v[r];
-        if (i < n) out[i] = run;
+        if (i < n) {
+            out[i] = run;
+            if (out2) out2[i] = run;
+        }
         if (!INCLUSIVE) run += v[r];
     }
 }
 
-void scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, bool inclusive, cudaStream_t s)
+void scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, bool inclusive, cudaStream_t s,
+              uint32_t *out2 = nullptr)
 {
     if (n == 0) return;
     const uint64_t nb = (n + kScanTile - 1) / kScanTile;
@@ -207,9 +211,9 @@ void scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, bool inclusive, cud
     k_scan_sums<<<1, kScanThreads, 0, s>>>(sums.p, nb);
     SJ_LAUNCHED();
     if (inclusive)
-        k_scan_apply<true><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, sums.p);
+        k_scan_apply<true><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, sums.p, out2);
     else
-        k_scan_apply<false><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, sums.p);
+        k_scan_apply<false><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, sums.p, out2);
     SJ_LAUNCHED();
 }
 
@@ -218,6 +222,11 @@ void scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, bool inclusive, cud
 void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s)
 {
     scan_u32(in, out, n, false, s);
+}
+
+void exclusive_scan_u32_dup(const uint32_t *in, uint32_t *out, uint32_t *out2, uint64_t n, cudaStream_t s)
+{
+    scan_u32(in, out, n, false, s, out2);
 }
 
 void inclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s)
@@ -271,41 +280,19 @@ void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32
 }
 
 // ---------------------------------------------------------------- prefix-bucket sort (sparse keys)
-// Two stages for keys whose top-k-dimension prefix splits the points into small buckets:
-//   1. histogram of prefixes, exclusive scan -> bucket starts, scatter (atomic cursor per bucket,
-//      order inside a bucket arbitrary);
-//   2. one thread per bucket sorts its <= kBucketMax items by (key, id) (insertion sort).
+// For keys whose top-k-dimension prefix splits the points into small buckets (the caller has
+// already histogrammed the prefixes, fused into k_keys):
+//   1. exclusive scan -> bucket starts (and a copy used as per-bucket cursors); scatter with an
+//      atomic cursor per bucket (order inside a bucket arbitrary);
+//   2. one thread per bucket of <= kBucketMax items sorts it by (key, id) (insertion sort); larger
+//      buckets are queued and sorted by one CTA each in shared memory (bitonic, <= kBigMax items).
 // The result is the (key, id)-ascending order -- exactly what the stable LSD sort produces, so A is
-// unchanged (reading R14).  Returns false (nothing written) when some bucket exceeds kBucketMax;
-// the caller then runs the LSD sort.
+// unchanged (reading R14).  No host round trip: a bucket larger than kBigMax sets *overflow and
+// is left unsorted; the caller checks the flag at its next sync and rebuilds with the LSD sort.
 namespace {
 constexpr uint32_t kBucketMax = 64;
-
-__device__ __forceinline__ uint64_t bucket_of(uint64_t key, uint64_t div, double inv)
-{
-    uint64_t q = (uint64_t)((double)key * inv);
-    if (q * div > key) --q;
-    else if ((q + 1) * div <= key) ++q;
-    return q;
-}
-
-__global__ void __launch_bounds__(256)
-k_bucket_hist(const uint64_t *__restrict__ keys, uint32_t n, uint64_t div, double inv, uint32_t *__restrict__ hist)
-{
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) atomicAdd(hist + bucket_of(keys[i], div, inv), 1u);
-}
-
-__global__ void __launch_bounds__(256)
-k_bucket_max(const uint32_t *__restrict__ hist, uint64_t P, uint32_t *__restrict__ mx)
-{
-    uint32_t m = 0;
-    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < P; b += (uint64_t)gridDim.x * blockDim.x)
-        m = max(m, hist[b]);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
-}
+constexpr uint32_t kBigMax = 4096;          // 4096 x (8 + 4) B = 48 KB of shared memory
+constexpr int kBigThreads = 512;
 
 __global__ void __launch_bounds__(256)
 k_bucket_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t n, uint64_t div,
@@ -314,19 +301,29 @@ k_bucket_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ 
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t k = kin[i];
-    const uint32_t pos = atomicAdd(cursor + bucket_of(k, div, inv), 1u);
+    uint64_t q = (uint64_t)((double)k * inv);          // prefix = k / div (double estimate, corrected)
+    if (q * div > k) --q;
+    else if ((q + 1) * div <= k) ++q;
+    const uint32_t pos = atomicAdd(cursor + q, 1u);
     kout[pos] = k;
     vout[pos] = vin[i];
 }
 
+// big[0] = number of queued big buckets, big[1..] = their ids
 __global__ void __launch_bounds__(256)
 k_bucket_sort(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, const uint32_t *__restrict__ start,
-              uint64_t P, uint64_t *__restrict__ kout, uint32_t *__restrict__ vout)
+              uint64_t P, uint64_t *__restrict__ kout, uint32_t *__restrict__ vout, uint32_t *__restrict__ big,
+              uint32_t big_cap)
 {
     const uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= P) return;
     const uint32_t s = start[b], e = start[b + 1];
     if (e == s) return;
+    if (e - s > kBucketMax) {
+        const uint32_t slot = atomicAdd(big, 1u);
+        if (slot < big_cap) big[1 + slot] = (uint32_t)b;
+        return;
+    }
     // insertion sort by (key, id) directly in the output range (a few L1-resident entries)
     for (uint32_t i = s; i < e; ++i) {
         const uint64_t ki = kin[i];
@@ -344,32 +341,76 @@ k_bucket_sort(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin
         vout[j] = vi;
     }
 }
+
+// One CTA per queued big bucket (grid-stride over the queue): bitonic sort of (key, id) in shared
+// memory, padded to a power of two with (UINT64_MAX, UINT32_MAX).
+__global__ void __launch_bounds__(kBigThreads)
+k_bucket_sort_big(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin,
+                  const uint32_t *__restrict__ start, const uint32_t *__restrict__ big, uint32_t big_cap,
+                  uint64_t *__restrict__ kout, uint32_t *__restrict__ vout, uint32_t *__restrict__ overflow)
+{
+    __shared__ uint64_t sk[kBigMax];
+    __shared__ uint32_t sv[kBigMax];
+    const uint32_t nbig = min(big[0], big_cap);
+    if (big[0] > big_cap && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(overflow, 1u);
+    for (uint32_t qi = blockIdx.x; qi < nbig; qi += gridDim.x) {
+        const uint32_t b = big[1 + qi];
+        const uint32_t s = start[b], m = start[b + 1] - s;
+        if (m > kBigMax) {
+            if (threadIdx.x == 0) atomicOr(overflow, 1u);
+            continue;
+        }
+        uint32_t m2 = 1;
+        while (m2 < m) m2 <<= 1;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < m2; i += blockDim.x) {
+            sk[i] = i < m ? kin[s + i] : ~0ull;
+            sv[i] = i < m ? vin[s + i] : ~0u;
+        }
+        __syncthreads();
+        for (uint32_t size = 2; size <= m2; size <<= 1) {
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t i = threadIdx.x; i < m2 / 2; i += blockDim.x) {
+                    const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                    const bool up = (lo & size) == 0;
+                    const uint64_t ka = sk[lo], kb = sk[hi];
+                    const uint32_t va = sv[lo], vb = sv[hi];
+                    const bool gt = ka > kb || (ka == kb && va > vb);
+                    if (gt == up) {
+                        sk[lo] = kb; sk[hi] = ka;
+                        sv[lo] = vb; sv[hi] = va;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+            kout[s + i] = sk[i];
+            vout[s + i] = sv[i];
+        }
+    }
+}
 }  // namespace
 
-bool bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp, uint32_t n,
-                       uint64_t div, uint64_t P, cudaStream_t s)
+// hist: per-prefix point counts (P + 1 entries, the last one 0), consumed (it becomes the cursor).
+void bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp, uint32_t n,
+                       uint64_t div, uint64_t P, uint32_t *hist, uint32_t *overflow, cudaStream_t s)
 {
-    if (n == 0) return true;
+    if (n == 0) return;
     const double inv = 1.0 / (double)div;
-    Scratch<uint32_t> hist((size_t)P + 1, s), start((size_t)P + 1, s), mx(1, s);
-    SJ_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(uint32_t) * ((size_t)P + 1), s));
-    SJ_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(uint32_t), s));
+    // at most n / (kBucketMax + 1) buckets are big
+    const uint32_t big_cap = n / (kBucketMax + 1) + 1;
+    Scratch<uint32_t> start((size_t)P + 1, s), big((size_t)big_cap + 1, s);
+    SJ_CUDA(cudaMemsetAsync(big.p, 0, sizeof(uint32_t), s));
+    exclusive_scan_u32_dup(hist, start.p, hist, (uint64_t)P + 1, s);
     const uint32_t g = (n + 255) / 256;
-    k_bucket_hist<<<g, 256, 0, s>>>(keys, n, div, inv, hist.p);
+    k_bucket_scatter<<<g, 256, 0, s>>>(keys, vals, n, div, inv, hist, keys_tmp, vals_tmp);
     SJ_LAUNCHED();
-    k_bucket_max<<<(uint32_t)std::min<uint64_t>((P + 255) / 256, 148 * 8), 256, 0, s>>>(hist.p, P, mx.p);
+    k_bucket_sort<<<(uint32_t)((P + 255) / 256), 256, 0, s>>>(keys_tmp, vals_tmp, start.p, P, keys, vals, big.p,
+                                                               big_cap);
     SJ_LAUNCHED();
-    uint32_t hmax = 0;
-    SJ_CUDA(cudaMemcpyAsync(&hmax, mx.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    SJ_CUDA(cudaStreamSynchronize(s));
-    if (hmax > kBucketMax) return false;
-    exclusive_scan_u32(hist.p, start.p, (uint64_t)P + 1, s);
-    SJ_CUDA(cudaMemcpyAsync(hist.p, start.p, sizeof(uint32_t) * ((size_t)P + 1), cudaMemcpyDeviceToDevice, s));
-    k_bucket_scatter<<<g, 256, 0, s>>>(keys, vals, n, div, inv, hist.p, keys_tmp, vals_tmp);
+    k_bucket_sort_big<<<296, kBigThreads, 0, s>>>(keys_tmp, vals_tmp, start.p, big.p, big_cap, keys, vals, overflow);
     SJ_LAUNCHED();
-    k_bucket_sort<<<(uint32_t)((P + 255) / 256), 256, 0, s>>>(keys_tmp, vals_tmp, start.p, P, keys, vals);
-    SJ_LAUNCHED();
-    return true;
 }
 
 }  // namespace sj

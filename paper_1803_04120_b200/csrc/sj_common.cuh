@@ -110,6 +110,8 @@ struct DevIndex {
     // -1 in dim i leaves M_i; bit 8+i: move +1 leaves M_i)
     const uint64_t *ccoord;
     const uint32_t *cmask;
+    int key_fastdiv;             // key -> coordinates by double reciprocals (see index_build.cu)
+    double inv_stride[SJ_MAX_DIM];
     uint32_t cshift[SJ_MAX_DIM];
     uint32_t cbits[SJ_MAX_DIM];
     // dense-cell tasks: every cell with >= dense_T points is cut into tasks of <= 32 consecutive
@@ -169,7 +171,6 @@ struct CtxGuard {
 };
 
 // index_build.cu
-void build_aux(sj_index *idx, cudaStream_t s, uint32_t *aux, bool force_dense_tasks);
 sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &o);
 sj_index *import_index_impl(const sj_index_view &v, int device);
 void free_index_impl(sj_index *idx);
@@ -177,9 +178,10 @@ void free_index_impl(sj_index *idx);
 // radix_sort.cu
 void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp,
                       uint32_t n, int key_bits, cudaStream_t s, bool *result_in_tmp);
-bool bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp, uint32_t n,
-                       uint64_t div, uint64_t P, cudaStream_t s);
+void bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp, uint32_t n,
+                       uint64_t div, uint64_t P, uint32_t *hist, uint32_t *overflow, cudaStream_t s);
 void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s);
+void exclusive_scan_u32_dup(const uint32_t *in, uint32_t *out, uint32_t *out2, uint64_t n, cudaStream_t s);
 void inclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s);
 
 // extras.cu

@@ -450,3 +450,25 @@ def test_unicomp_halves_the_work(sj, d, eps):
     ratio = ru.stats["candidates_tested"] / rf.stats["candidates_tested"]
     assert 0.4 <= ratio <= 0.6, ratio
     assert np.array_equal(ru.to_numpy(), rf.to_numpy())
+
+
+@pytest.mark.parametrize("m", [3000, 7000])
+def test_prefix_bucket_sort_big_buckets(sj, m):
+    """a3 prefix-bucket sort (sparse 6-D keys, N <= 2P): one top-k prefix holds m points -- a
+    bucket sorted in shared memory by one CTA (m <= 4096) or, beyond that, flagged on the device
+    and rebuilt with the LSD radix sort.  Either way A must equal the stable order (R14)."""
+    rng = np.random.default_rng(m)
+    n = 20000
+    pts = rng.uniform(0, 100, (n, 6))
+    pts[:m, 4:] = 50.25 + rng.uniform(0, 0.5, (m, 2))      # same (c_4, c_5) cell prefix
+    pts[:m, :4] = rng.uniform(40, 60, (m, 4))               # neighbours inside the cluster
+    rng.shuffle(pts)
+    eps = 1.0
+    ref = ir.build_index(pts, eps)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    arr = idx.arrays()
+    assert arr["B"].cpu().numpy().tolist() == ref.B
+    assert np.array_equal(arr["A"].cpu().numpy().astype(np.int64), ref.A)
+    assert np.array_equal(arr["X"].cpu().numpy(), pts[ref.A].T)
+    got = sj.self_join(idx).to_numpy(sort=True)
+    assert np.array_equal(got, oracle.brute_force(pts, eps))
