@@ -168,7 +168,8 @@ void sj_free_result(sj_result *r);
 
 void sj_free_index(sj_index *idx);   /* NULL-safe */
 
-/* Totals and work counters of a result. Any out pointer may be NULL. */
+/* Totals and work counters of a result. Any out pointer may be NULL.  The device timings in
+ * *stats are computed from the join's CUDA events on the first call that asks for stats. */
 sj_status sj_result_info(const sj_result *r, uint64_t *n_pairs, uint32_t *n_batches, sj_stats *stats);
 
 /* Batch b of a result: *pairs points to *n packed uint64 pairs in device memory (*on_device=1,
@@ -195,6 +196,12 @@ sj_status sj_brute_force_join(const double *points, uint64_t n, int d, double ep
 
 /* Geometry, sizes, timings and device pointers of an index (for tests and NCCL broadcast). */
 sj_status sj_index_export(const sj_index *idx, sj_index_view *view);
+
+/* Same as sj_index_export, with the build-phase timings t_*_ms filled in (device time from CUDA
+ * events recorded during sj_build_index; computed on this first request so the build itself never
+ * waits on event queries -- sj_index_export leaves them 0 until then).  Blocks until the build's
+ * events completed. */
+sj_status sj_index_timings(const sj_index *idx, sj_index_view *view);
 
 /* Build an index on `device` from a view whose array pointers are device memory on that device
  * (e.g. buffers received by an NCCL broadcast); the arrays are copied. */

@@ -224,6 +224,7 @@ void sj_free_result(sj_result *r)
 {
     if (!r) return;
     cudaSetDevice(r->device);
+    sj::result_release_events(r);
     for (auto &b : r->batches) {
         if (!b.pairs) continue;
         if (b.on_device) sj::dev_free(b.pairs, nullptr);
@@ -240,7 +241,10 @@ sj_status sj_result_info(const sj_result *r, uint64_t *n_pairs, uint32_t *n_batc
     if (!r) sj::fail(SJ_ERR_STATE, "result is NULL");
     if (n_pairs) *n_pairs = r->total;
     if (n_batches) *n_batches = (uint32_t)r->batches.size();
-    if (stats) *stats = r->stats;
+    if (stats) {
+        sj::result_finalize_timing(const_cast<sj_result *>(r));   // lazy: event queries on request
+        *stats = r->stats;
+    }
     return SJ_OK;
     SJ_API_END
 }
@@ -300,6 +304,17 @@ sj_status sj_brute_force_join(const double *points, uint64_t n, int d, double ep
     if (jopts) jo = *jopts;
     else sj_join_opts_default(&jo);
     *out = sj::brute_force_impl(points, n, d, eps, bo, jo);
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_index_timings(const sj_index *idx, sj_index_view *view)
+{
+    SJ_API_BEGIN
+    if (!idx) sj::fail(SJ_ERR_STATE, "index is NULL");
+    if (!view) sj::fail(SJ_ERR_ARG, "view is NULL");
+    sj::index_finalize_timing(const_cast<sj_index *>(idx));
+    *view = idx->view;
     return SJ_OK;
     SJ_API_END
 }

@@ -2,6 +2,7 @@
 // counter / cursor slots in device + pinned memory), so a build or a join does not create and
 // destroy CUDA objects on every call.  A context is owned by one call at a time (pool + mutex);
 // concurrent calls on one device simply get different contexts.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -74,6 +75,97 @@ void release_ctx(DevCtx *c)
     if (!c) return;
     std::lock_guard<std::mutex> lk(g_ctx_mu);
     g_ctx_free.push_back(c);
+}
+
+namespace {
+std::mutex g_ev_mu;
+std::vector<std::pair<int, cudaEvent_t>> g_ev_free;
+}  // namespace
+
+cudaEvent_t event_get(int dev)
+{
+    {
+        std::lock_guard<std::mutex> lk(g_ev_mu);
+        for (size_t i = g_ev_free.size(); i-- > 0;) {
+            if (g_ev_free[i].first == dev) {
+                cudaEvent_t e = g_ev_free[i].second;
+                g_ev_free.erase(g_ev_free.begin() + (long)i);
+                return e;
+            }
+        }
+    }
+    cudaEvent_t e;
+    SJ_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+void event_put(int dev, cudaEvent_t e)
+{
+    if (!e) return;
+    std::lock_guard<std::mutex> lk(g_ev_mu);
+    g_ev_free.emplace_back(dev, e);
+}
+
+static float elapsed(cudaEvent_t a, cudaEvent_t b)
+{
+    float t = 0;
+    if (a && b && cudaEventElapsedTime(&t, a, b) != cudaSuccess) {
+        cudaGetLastError();
+        t = 0;
+    }
+    return t;
+}
+
+void result_finalize_timing(sj_result *r)
+{
+    if (r->timed) return;
+    cudaSetDevice(r->device);
+    r->stats.estimate_ms = elapsed(r->est_ev[0], r->est_ev[1]);
+    float sum = 0, mx = 0, span = 0;
+    for (auto &pr : r->runs) {
+        cudaEventSynchronize(pr.second);
+        const float ms = elapsed(pr.first, pr.second);
+        sum += ms;
+        mx = std::max(mx, ms);
+        span = std::max(span, elapsed(r->span0, pr.second));
+    }
+    r->stats.refine_ms = sum;
+    r->stats.refine_max_ms = mx;
+    r->stats.refine_span_ms = span;
+    r->timed = true;
+    result_release_events(r);
+}
+
+void result_release_events(sj_result *r)
+{
+    for (auto &pr : r->runs) {
+        event_put(r->device, pr.first);
+        event_put(r->device, pr.second);
+    }
+    r->runs.clear();
+    event_put(r->device, r->est_ev[0]);
+    event_put(r->device, r->est_ev[1]);
+    event_put(r->device, r->span0);
+    r->est_ev[0] = r->est_ev[1] = r->span0 = nullptr;
+}
+
+void index_finalize_timing(sj_index *idx)
+{
+    if (idx->timed || !idx->tev[0]) return;
+    cudaSetDevice(idx->device);
+    cudaEventSynchronize(idx->tev[6]);
+    sj_index_view &v = idx->view;
+    v.t_h2d_ms = elapsed(idx->tev[0], idx->tev[1]);
+    v.t_geometry_ms = elapsed(idx->tev[1], idx->tev[2]);
+    v.t_keys_ms = elapsed(idx->tev[2], idx->tev[3]);
+    v.t_sort_ms = elapsed(idx->tev[3], idx->tev[4]);
+    v.t_compact_ms = elapsed(idx->tev[4], idx->tev[6]);
+    v.t_total_ms = elapsed(idx->tev[0], idx->tev[6]);
+    idx->timed = true;
+    for (auto &e : idx->tev) {
+        event_put(idx->device, e);
+        e = nullptr;
+    }
 }
 
 static double now_us()

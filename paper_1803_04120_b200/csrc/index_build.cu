@@ -284,14 +284,6 @@ void launch(int d, int which, dim3 g, cudaStream_t s, const DevIndex &ix, const 
     }
 }
 
-struct EventTimer {
-    cudaEvent_t e[8];
-    int n = 0;
-    explicit EventTimer(int k) : n(k) { for (int i = 0; i < n; ++i) SJ_CUDA(cudaEventCreate(&e[i])); }
-    ~EventTimer() { for (int i = 0; i < n; ++i) cudaEventDestroy(e[i]); }
-    void rec(int i, cudaStream_t s) { SJ_CUDA(cudaEventRecord(e[i], s)); }
-    float ms(int a, int b) { float t = 0; cudaEventElapsedTime(&t, e[a], e[b]); return t; }
-};
 
 // Host-side geometry (a1 epilogue): R, w, |g_j|, strides, key bits.  Exact same IEEE
 // operations as written in DESIGN.md R6/R7.
@@ -557,7 +549,14 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
     cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : cg.c->streams[0];
 
     const uint32_t N = (uint32_t)n;
-    EventTimer ev(7);
+    // phase events (pooled); handed to the index, which turns them into timings on request
+    struct Events {
+        int dev;
+        cudaEvent_t e[7];
+        explicit Events(int d) : dev(d) { for (auto &x : e) x = nullptr; for (auto &x : e) x = event_get(dev); }
+        ~Events() { for (auto &x : e) event_put(dev, x); }
+        void rec(int i, cudaStream_t st) { SJ_CUDA(cudaEventRecord(e[i], st)); }
+    } ev(o.device);
     ev.rec(0, s);
 
     // ---- inputs on device
@@ -752,14 +751,11 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         idx->dev = ix;
         finish_aux(idx, s, aux, dp, dirhist.p, false, h_aux);   // the build's late host sync
         ev.rec(6, s);
-        SJ_CUDA(cudaStreamSynchronize(s));
         tr.mark("compact+dir+dense (synced)");
-        idx->view.t_h2d_ms = ev.ms(0, 1);
-        idx->view.t_geometry_ms = ev.ms(1, 2);
-        idx->view.t_keys_ms = ev.ms(2, 3);
-        idx->view.t_sort_ms = ev.ms(3, 4);
-        idx->view.t_compact_ms = ev.ms(4, 6);
-        idx->view.t_total_ms = ev.ms(0, 6);
+        for (int i = 0; i < 7; ++i) {
+            idx->tev[i] = ev.e[i];
+            ev.e[i] = nullptr;
+        }
     } catch (...) {
         cudaStreamSynchronize(s);
         free_index_impl(idx);
@@ -780,6 +776,7 @@ void free_index_impl(sj_index *idx)
     cudaSetDevice(idx->device);
     for (int i = 0; i < idx->nbufs; ++i) dev_free(idx->bufs[i], nullptr);
     cudaDeviceSynchronize();
+    for (auto &e : idx->tev) event_put(idx->device, e);
     delete idx;
 }
 

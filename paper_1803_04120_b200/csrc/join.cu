@@ -263,7 +263,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     const uint64_t nbk = sm.ns ? (sm.ns + group - 1) / group : 0;
     const size_t kSlotsBytes = sizeof(Slot) * 64;
     const size_t slot_need = kWorkBytes + kSlotsBytes + 8 * (size_t)(nbk + 1);
-    CtxGuard cg{acquire_ctx(idx->device, S, 2 * S + 4, slot_need)};
+    CtxGuard cg{acquire_ctx(idx->device, S, S + 2, slot_need)};
     DevCtx &cx = *cg.c;
     cudaStream_t s0 = cx.streams[0];
     char *dbase = static_cast<char *>(cx.d_slots), *hbase = static_cast<char *>(cx.h_slots);
@@ -280,8 +280,9 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     try {
         SJ_CUDA(cudaMemsetAsync(work, 0, kWorkBytes, s0));
         // ---- a5: estimate on a strided sample (count-only refine), summed per planning bucket
-        float est_ms = 0;
         if (sm.ns) {
+            res->est_ev[0] = event_get(idx->device);
+            res->est_ev[1] = event_get(idx->device);
             SJ_CUDA(cudaMemsetAsync(dbk, 0, 8 * nbk, s0));
             JoinArgs ja = base_args(idx, o, nullptr);
             ja.q0 = (uint32_t)q0;
@@ -290,14 +291,12 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             ja.nsamples = (uint32_t)sm.ns;
             ja.qbucket = dbk;
             ja.group = (uint32_t)group;
-            SJ_CUDA(cudaEventRecord(cx.events[0], s0));
+            SJ_CUDA(cudaEventRecord(res->est_ev[0], s0));
             launch_refine<kCountQuery>(ix, ja, o.unicomp != 0, (uint32_t)sm.ns, s0);
-            SJ_CUDA(cudaEventRecord(cx.events[1], s0));
+            SJ_CUDA(cudaEventRecord(res->est_ev[1], s0));
             SJ_CUDA(cudaMemcpyAsync(hbk, dbk, nbk * 8, cudaMemcpyDeviceToHost, s0));
             SJ_CUDA(cudaStreamSynchronize(s0));
-            SJ_CUDA(cudaEventElapsedTime(&est_ms, cx.events[0], cx.events[1]));
         }
-        stats.estimate_ms = est_ms;
         tr.mark("estimate (synced)");
 
         // ---- plan (k >= min_batches contiguous A-order ranges)
@@ -314,12 +313,11 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         tr.mark("plan");
 
         bool work_read = false;
-        float refine_ms = 0, refine_max = 0, refine_span = 0;
         uint32_t launches = 0;
-        cudaEvent_t ev_span0 = cx.events[2 * S + 2];   // first refine launch start (stream 0)
-        bool span_started = false;
-        auto run_batch = [&](uint64_t a, uint64_t b, uint64_t *buf, uint64_t cap, Slot *dslot, cudaStream_t s,
-                             cudaEvent_t e0, cudaEvent_t e1) {
+        // every batch run records a (start, end) event pair; timings are computed on request
+        auto run_batch = [&](uint64_t a, uint64_t b, uint64_t *buf, uint64_t cap, Slot *dslot, cudaStream_t s) {
+            cudaEvent_t e0 = event_get(idx->device), e1 = event_get(idx->device);
+            res->runs.emplace_back(e0, e1);
             SJ_CUDA(cudaMemsetAsync(dslot, 0, sizeof(Slot), s));
             JoinArgs ja = base_args(idx, o, work);
             ja.out = buf;
@@ -328,9 +326,9 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             ja.overflow = &dslot->overflow;
             ja.q0 = (uint32_t)a;
             ja.q1 = (uint32_t)b;
-            if (!span_started) {
-                SJ_CUDA(cudaEventRecord(ev_span0, s));
-                span_started = true;
+            if (!res->span0) {
+                res->span0 = event_get(idx->device);
+                SJ_CUDA(cudaEventRecord(res->span0, s));
             }
             if (o.dense_cells && ix.n_dense_tasks) {
                 ja.dense_T = ix.dense_T;
@@ -343,14 +341,6 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             SJ_CUDA(cudaEventRecord(e1, s));
             ++launches;
         };
-        auto add_time = [&](cudaEvent_t e0, cudaEvent_t e1) {
-            float ms = 0, span = 0;
-            SJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-            SJ_CUDA(cudaEventElapsedTime(&span, ev_span0, e1));
-            refine_ms += ms;
-            refine_max = std::max(refine_max, ms);
-            refine_span = std::max(refine_span, span);
-        };
 
         if (!o.result_on_host) {
             // ---- device-resident batches: every batch owns its buffer; streams run them
@@ -359,7 +349,6 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             std::vector<uint64_t> counts(nb, 0);
             auto drain_stream_slot = [&](size_t b) {   // host: read batch b's cursor (already synced)
                 counts[b] = hslots[b % S].cursor;
-                add_time(cx.events[2 + 2 * (b % S)], cx.events[3 + 2 * (b % S)]);
             };
             for (size_t b = 0; b < nb; ++b) {
                 const int si = (int)(b % S);
@@ -374,16 +363,15 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 bt.pairs = dalloc<uint64_t>(cap, s);
                 bt.cap = cap;
                 bt.on_device = 1;
-                run_batch(cuts[b], cuts[b + 1], bt.pairs, cap, dslots + si, s, cx.events[2 + 2 * si],
-                          cx.events[3 + 2 * si]);
+                run_batch(cuts[b], cuts[b + 1], bt.pairs, cap, dslots + si, s);
                 SJ_CUDA(cudaMemcpyAsync(hslots + si, dslots + si, sizeof(Slot), cudaMemcpyDeviceToHost, s));
             }
             tr.mark("batches launched");
             // the work counters are read back on stream 0 after every stream's last batch, so the
             // one round of stream syncs below also covers them
             for (int i = 1; i < S; ++i) {
-                SJ_CUDA(cudaEventRecord(cx.events[2 * S + 3], cx.streams[i]));
-                SJ_CUDA(cudaStreamWaitEvent(s0, cx.events[2 * S + 3], 0));
+                SJ_CUDA(cudaEventRecord(cx.events[2 + i], cx.streams[i]));
+                SJ_CUDA(cudaStreamWaitEvent(s0, cx.events[2 + i], 0));
             }
             SJ_CUDA(cudaMemcpyAsync(hwork, work, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0));
             for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
@@ -391,6 +379,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             work_read = true;
             cudaStream_t st_sort = s0;
             for (size_t b = (nb > (size_t)S ? nb - S : 0); b < nb; ++b) drain_stream_slot(b);
+            tr.mark("drain slots");
             for (size_t b = 0; b < nb; ++b) {
                 sj_batch &bt = res->batches[b];
                 uint64_t n = counts[b];
@@ -398,10 +387,9 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                     dev_free(bt.pairs, s0);
                     bt.pairs = dalloc<uint64_t>(n, s0);
                     bt.cap = n;
-                    run_batch(cuts[b], cuts[b + 1], bt.pairs, n, dslots, s0, cx.events[2], cx.events[3]);
+                    run_batch(cuts[b], cuts[b + 1], bt.pairs, n, dslots, s0);
                     SJ_CUDA(cudaMemcpyAsync(hslots, dslots, sizeof(Slot), cudaMemcpyDeviceToHost, s0));
                     SJ_CUDA(cudaStreamSynchronize(s0));
-                    add_time(cx.events[2], cx.events[3]);
                     ++stats.retries;
                     n = hslots[0].cursor;
                     if (n > bt.cap) fail(SJ_ERR_CUDA, "batch re-run overflowed");
@@ -410,6 +398,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 res->total += n;
                 if (o.sort_pairs) sort_pairs_device(bt.pairs, n, ix.n, st_sort);
             }
+            tr.mark("batch loop");
         } else {
             // ---- host-drained batches: S device staging buffers; batch b+S on a stream runs after
             //      the D2H of batch b (stream order), while other streams compute.
@@ -432,8 +421,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 auto r = pending.front();
                 pending.pop_front();
                 inflight[i] = r;
-                run_batch(r.first, r.second, staging[i], scap[i], dslots + i, cx.streams[i], cx.events[2 + 2 * i],
-                          cx.events[3 + 2 * i]);
+                run_batch(r.first, r.second, staging[i], scap[i], dslots + i, cx.streams[i]);
                 SJ_CUDA(cudaMemcpyAsync(hslots + i, dslots + i, sizeof(Slot), cudaMemcpyDeviceToHost,
                                         cx.streams[i]));
                 order.push_back(i);
@@ -445,7 +433,6 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 // the cursor copy follows the kernel on stream i; the previous D2H on this stream
                 // precedes the kernel, so a stream sync here waits for exactly that batch.
                 SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
-                add_time(cx.events[2 + 2 * i], cx.events[3 + 2 * i]);
                 const uint64_t n = hslots[i].cursor;
                 const auto r = inflight[i];
                 if (n > scap[i]) {
@@ -490,13 +477,11 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         stats.candidates_tested = hwork[1];
         stats.pairs = res->total;
         stats.batches = (uint32_t)res->batches.size();
-        stats.refine_ms = refine_ms;
-        stats.refine_max_ms = refine_max;
         stats.refine_launches = launches;
-        stats.refine_span_ms = refine_span;
         tr.mark("stats");
     } catch (...) {
         for (auto s : cx.streams) cudaStreamSynchronize(s);
+        result_release_events(res);
         for (auto &b : res->batches) {
             if (!b.pairs) continue;
             if (b.on_device) dev_free(b.pairs, nullptr);

@@ -461,19 +461,13 @@ __device__ __forceinline__ void search_rows(const DevIndex &ix, const JoinArgs &
     }
 }
 
+// wmask: the lanes of the warp that run refine_query together (a full-warp ballot taken by the
+// caller before any divergence); every __syncwarp below is over exactly these lanes.
 template <int D, int MODE, bool UNICOMP, bool DENSE = false>
-__device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs &ja, uint32_t k,
-                                            QueryState<D> &q, const TopTable &tt, WarpBuf *wb = nullptr)
+__device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs &ja, uint32_t k, uint32_t h,
+                                            uint32_t cs, uint32_t ce, unsigned wmask, QueryState<D> &q,
+                                            const TopTable &tt, WarpBuf *wb = nullptr)
 {
-    const uint32_t h = __ldg(ix.pcell + k);
-    const uint32_t cs = __ldg(ix.G + h), ce = __ldg(ix.G + h + 1);
-    if constexpr (MODE == kEmit && !DENSE) {
-        // queries of populous cells are handled by the warp-per-task dense kernel
-        if (ja.dense_T && ce - cs >= ja.dense_T) return;
-    }
-    // The warp's remaining active queries, taken AFTER the only divergent early exit: every
-    // __syncwarp(wmask) below must be reached by all lanes of wmask.
-    const unsigned wmask = __activemask();
     q.k = k;
     q.pid = __ldg(ix.A + k);
 #pragma unroll
@@ -571,7 +565,8 @@ k_refine_dense(const DevIndex ix, const JoinArgs ja)
     // load and broadcast candidates but never emit (they take the first query's point)
     const uint32_t k = a + lane;
     q.valid = k < b;
-    refine_query<D, kEmit, UNICOMP, true>(ix, ja, q.valid ? k : a, q, tt, &wb);
+    refine_query<D, kEmit, UNICOMP, true>(ix, ja, q.valid ? k : a, h, __ldg(ix.G + h), __ldg(ix.G + h + 1),
+                                          0xffffffffu, q, tt, &wb);
     warpbuf_flush(ja, wb, 0xffffffffu);
     unsigned long long p = q.probes, c = q.tests, em = q.emitted;
 #pragma unroll
@@ -613,7 +608,16 @@ k_refine(const DevIndex ix, const JoinArgs ja)
         k = ja.q0 + qi;
         active = k < ja.q1;
     }
-    if (active) refine_query<D, MODE, UNICOMP>(ix, ja, k, q, tt);
+    uint32_t h = 0, cs = 0, ce = 0;
+    if (active) {
+        h = __ldg(ix.pcell + k);
+        cs = __ldg(ix.G + h);
+        ce = __ldg(ix.G + h + 1);
+        // queries of populous cells are handled by the warp-per-task dense kernel
+        if (MODE == kEmit && ja.dense_T && ce - cs >= ja.dense_T) active = false;
+    }
+    const unsigned wmask = __ballot_sync(0xffffffffu, active);   // before any divergence
+    if (active) refine_query<D, MODE, UNICOMP>(ix, ja, k, h, cs, ce, wmask, q, tt);
     if constexpr (MODE == kCountQuery) {
         // sum the group's partial counts (all lanes of a group share `active`)
         uint32_t e = q.emitted;

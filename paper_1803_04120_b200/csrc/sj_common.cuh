@@ -128,6 +128,10 @@ enum SearchMode { kSearchDenseRows = 0, kSearchCellScan = 1, kSearchRows = 2 };
 // The opaque handle.
 struct sj_index {
     int device = 0;
+    // build phase events (pooled); the t_*_ms timings are computed from them on first request
+    // (sj_index_timings), so the build itself never waits on event queries
+    cudaEvent_t tev[7] = {nullptr};
+    bool timed = false;
     sj_index_view view{};        // geometry + device pointers (exported as is)
     sj::DevIndex dev{};          // same, in kernel form
     void *bufs[16] = {nullptr};  // owned device allocations
@@ -143,6 +147,12 @@ struct sj_batch {
 
 struct sj_result {
     int device = 0;
+    // pooled events: estimate start/end, first refine launch start, one (start, end) per batch run;
+    // refine/estimate timings are computed on first request (sj_result_info with stats)
+    cudaEvent_t est_ev[2] = {nullptr, nullptr};
+    cudaEvent_t span0 = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> runs;
+    bool timed = false;
     std::vector<sj_batch> batches;
     sj_stats stats{};
     uint64_t total = 0;
@@ -159,6 +169,12 @@ struct DevCtx {
     size_t slot_bytes = 0;
 };
 DevCtx *acquire_ctx(int dev, int nstreams, int nevents, size_t slot_bytes);
+// pooled timing events (cudaEventCreate / elapsed-time queries stay off the critical path)
+cudaEvent_t event_get(int dev);
+void event_put(int dev, cudaEvent_t e);
+void result_finalize_timing(sj_result *r);
+void result_release_events(sj_result *r);
+void index_finalize_timing(sj_index *idx);
 void release_ctx(DevCtx *c);
 struct CtxGuard {
     DevCtx *c;

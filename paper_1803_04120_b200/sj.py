@@ -103,6 +103,8 @@ def load_library(path: str = LIB_PATH):
     L.sj_brute_force_join.restype = i32
     L.sj_index_export.argtypes = [vp, P(IndexView)]
     L.sj_index_export.restype = i32
+    L.sj_index_timings.argtypes = [vp, P(IndexView)]
+    L.sj_index_timings.restype = i32
     L.sj_index_import.argtypes = [P(IndexView), i32, P(vp)]
     L.sj_index_import.restype = i32
     L.sj_set_allocator.argtypes = [vp, vp, vp]
@@ -180,7 +182,8 @@ class Index:
                     dir_k=v.dir_k, dir_entries=v.dir_entries)
 
     def timings(self) -> dict:
-        v = self.view
+        v = IndexView()
+        _check(load_library().sj_index_timings(self._h, ctypes.byref(v)))
         return dict(h2d_ms=v.t_h2d_ms, geometry_ms=v.t_geometry_ms, keys_ms=v.t_keys_ms,
                     sort_ms=v.t_sort_ms, compact_ms=v.t_compact_ms, total_ms=v.t_total_ms)
 
@@ -285,12 +288,22 @@ class Result:
     def __init__(self, handle: int):
         self._h = ctypes.c_void_p(handle)
         L = load_library()
-        n, nb, st = u64(), u32(), Stats()
-        _check(L.sj_result_info(self._h, ctypes.byref(n), ctypes.byref(nb), ctypes.byref(st)))
+        n, nb = u64(), u32()
+        _check(L.sj_result_info(self._h, ctypes.byref(n), ctypes.byref(nb), None))
         self.n_pairs = int(n.value)
         self.n_batches = int(nb.value)
-        self.stats = st.as_dict()
+        self._stats = None
         self.device = None
+
+    @property
+    def stats(self) -> dict:
+        """Work counters and device timings (the timings are computed from the join's CUDA
+        events on this first access, off the join's critical path)."""
+        if self._stats is None:
+            st = Stats()
+            _check(load_library().sj_result_info(self._h, None, None, ctypes.byref(st)))
+            self._stats = st.as_dict()
+        return self._stats
 
     def batch(self, b: int):
         L = load_library()
