@@ -138,6 +138,18 @@ k_heads(const uint64_t *__restrict__ keys, uint32_t n, uint32_t *__restrict__ fl
     flags[k] = (k == 0 || keys[k] != keys[k - 1]) ? 1u : 0u;
 }
 
+// Occupancy bitmap over the top-(k+1) prefixes, stored DILATED along dimension d-k-1: a cell with
+// top-(k+1) prefix q sets bits q-1, q, q+1, so the refine asks "is any of the three windows
+// c_{d-k-1} + {-1,0,1} occupied?" with one bit test.  (q-1 and q+1 stay inside q's top-k prefix:
+// c is in [1, |g|-2] and the pad cells are empty.)
+__device__ __forceinline__ void occ_set_window(uint32_t *occ, uint64_t q)
+{
+    const uint64_t a = q - 1ull;
+    const uint32_t sh = (uint32_t)(a & 31u);
+    atomicOr(occ + (a >> 5), 7u << sh);
+    if (sh > 29) atomicOr(occ + (a >> 5) + 1, 7u >> (32 - sh));
+}
+
 // Cell coordinates from a linear id: c_j = (key / stride_j) mod |g_j|, taken from the slowest
 // dimension down (each quotient < |g_j|).  Fast path: the quotient from a double reciprocal,
 // corrected by +-1 in exact integer arithmetic (valid while quotients < 2^50 and keys < 2^63, which
@@ -214,8 +226,13 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
             uint64_t cl = c[0];
 #pragma unroll
             for (int j = 1; j < D; ++j) if (j == jo) cl = c[j];
-            const uint64_t q = prefix * ix.occ_cpd + cl;
-            atomicOr(occ + (q >> 5), 1u << (q & 31));
+            occ_set_window(occ, prefix * ix.occ_cpd + cl);
+            if (ix.occ2) {
+                uint64_t c2 = c[0];
+#pragma unroll
+                for (int j = 1; j < D; ++j) if (j == jo - 1) c2 = c[j];
+                occ_set_window(const_cast<uint32_t *>(ix.occ2), prefix * ix.occ2_cpd + c2);
+            }
         }
     }
     if (k == n - 1) G[h + 1] = n;
@@ -336,6 +353,9 @@ struct DirPlan {
     bool occ = false;
     uint64_t occ_cpd = 0, occ_div = 0;
     size_t occ_words = 0;
+    bool occ2 = false;           // (top-k prefix, c_{d-k-2}) bitmap, only with occ and >= 2 low dims
+    uint64_t occ2_cpd = 0;
+    size_t occ2_words = 0;
 };
 
 DirPlan plan_dir(const sj_index_view &v)
@@ -361,6 +381,14 @@ DirPlan plan_dir(const sj_index_view &v)
             dp.occ_cpd = v.cpd[d - dp.k - 1];
             dp.occ_div = dp.div / dp.occ_cpd;
             dp.occ_words = (size_t)((P1 + 31) / 32);
+            if (d - dp.k >= 2) {
+                const unsigned __int128 P2 = P * v.cpd[d - dp.k - 2];
+                if (P2 <= (unsigned __int128)64 * std::max<uint64_t>(n, 1ull << 16)) {
+                    dp.occ2 = true;
+                    dp.occ2_cpd = v.cpd[d - dp.k - 2];
+                    dp.occ2_words = (size_t)((P2 + 31) / 32);
+                }
+            }
         }
     }
     return dp;
@@ -382,6 +410,7 @@ void apply_dir_geometry(DevIndex &ix, const sj_index_view &v, const DirPlan &dp)
     for (int j = 0; j < d; ++j) ix.lowR[j + 1] = ix.lowR[j] + (int64_t)(j < d - dp.k ? v.strides[j] : 0);
     ix.occ_div = dp.occ ? dp.occ_div : 0;
     ix.occ_cpd = dp.occ ? dp.occ_cpd : 0;
+    ix.occ2_cpd = dp.occ2 ? dp.occ2_cpd : 0;
     // key -> coordinates by double reciprocals when every quotient < 2^50 and keys < 2^63
     bool fast = v.key_bits <= 63;
     for (int j = 1; j < d; ++j) fast = fast && v.cpd[j] < (1ull << 50);
@@ -402,6 +431,13 @@ void alloc_dir(sj_index *idx, const DirPlan &dp, cudaStream_t s)
         idx->bufs[idx->nbufs++] = occ;
         SJ_CUDA(cudaMemsetAsync(occ, 0, sizeof(uint32_t) * dp.occ_words, s));
         idx->dev.occ = occ;
+    }
+    idx->dev.occ2 = nullptr;
+    if (dp.occ2) {
+        uint32_t *occ2 = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * dp.occ2_words, s));
+        idx->bufs[idx->nbufs++] = occ2;
+        SJ_CUDA(cudaMemsetAsync(occ2, 0, sizeof(uint32_t) * dp.occ2_words, s));
+        idx->dev.occ2 = occ2;
     }
 }
 
@@ -432,8 +468,20 @@ k_occ_bits(const uint64_t *__restrict__ B, const uint32_t *__restrict__ nG, uint
 {
     const uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (h >= *nG) return;
-    const uint64_t q = div_small_quot(B[h], div, inv);
-    atomicOr(occ + (q >> 5), 1u << (q & 31));
+    occ_set_window(occ, div_small_quot(B[h], div, inv));
+}
+
+// second bitmap: bit prefix * |g_{d-k-2}| + c_{d-k-2}, c = (key / stride_{d-k-2}) mod |g_{d-k-2}|
+__global__ void __launch_bounds__(kThreads)
+k_occ2_bits(const uint64_t *__restrict__ B, const uint32_t *__restrict__ nG, uint64_t div, double inv,
+            uint64_t st2, double inv2, uint64_t cpd2, uint32_t *__restrict__ occ2)
+{
+    const uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= *nG) return;
+    const uint64_t key = B[h];
+    const uint64_t prefix = div_small_quot(key, div, inv);
+    const uint64_t c2 = div_small_quot(key - prefix * div, st2, inv2);
+    occ_set_window(occ2, prefix * cpd2 + c2);
 }
 
 // dense tasks, in A-order: cells with >= T points are cut into <= 32-query tasks; count, exclusive
@@ -716,6 +764,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         SJ_CUDA(cudaMemcpyAsync(aux, pcell + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
         ix.masks = masks;
         ix.occ = idx->dev.occ;
+        ix.occ2 = idx->dev.occ2;
         ix.dir = idx->dev.dir;
         ba.keys = const_cast<uint64_t *>(skeys);
         ba.A = A;
@@ -845,6 +894,12 @@ sj_index *import_index_impl(const sj_index_view &src, int device)
         if (idx->dev.occ) {
             k_occ_bits<<<gN, kThreads, 0, s>>>(B, aux, dp.occ_div, 1.0 / (double)dp.occ_div,
                                                const_cast<uint32_t *>(idx->dev.occ));
+            SJ_LAUNCHED();
+        }
+        if (idx->dev.occ2) {
+            const uint64_t st2 = v.strides[d - dp.k - 2];
+            k_occ2_bits<<<gN, kThreads, 0, s>>>(B, aux, dp.div, 1.0 / (double)dp.div, st2, 1.0 / (double)st2,
+                                                dp.occ2_cpd, const_cast<uint32_t *>(idx->dev.occ2));
             SJ_LAUNCHED();
         }
         uint32_t h_aux[4];

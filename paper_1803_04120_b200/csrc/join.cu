@@ -256,7 +256,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
 
     // per-call execution context (pooled): S streams, events, slot buffers
     struct Slot { unsigned long long cursor; uint32_t overflow; uint32_t pad; };
-    constexpr size_t kWorkBytes = 64;                 // 4 u64 work counters (+pad)
+    constexpr size_t kWorkBytes = sizeof(unsigned long long) * 4 * kWorkSlots;   // work counter slots
     const uint64_t nq = q1 - q0;
     const Sample sm = make_sample(nq);
     const uint64_t group = 32 * std::max<uint64_t>(1, (sm.ns / 32 + 1023) / 1024);  // whole runs per bucket
@@ -277,13 +277,15 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     sj_result *res = new sj_result();
     res->device = idx->device;
     sj_stats &stats = res->stats;
+    // self pairs of a batch [a, b): written at fixed slots, counted on the host (see JoinArgs::nself)
+    auto nself_of = [&](uint64_t a, uint64_t b) -> uint64_t { return o.include_self ? b - a : 0; };
     try {
-        SJ_CUDA(cudaMemsetAsync(work, 0, kWorkBytes, s0));
+        // work counters, the 64 batch slots and the planning buckets are contiguous: one memset
+        SJ_CUDA(cudaMemsetAsync(work, 0, kWorkBytes + kSlotsBytes + 8 * nbk, s0));
         // ---- a5: estimate on a strided sample (count-only refine), summed per planning bucket
         if (sm.ns) {
             res->est_ev[0] = event_get(idx->device);
             res->est_ev[1] = event_get(idx->device);
-            SJ_CUDA(cudaMemsetAsync(dbk, 0, 8 * nbk, s0));
             JoinArgs ja = base_args(idx, o, nullptr);
             ja.q0 = (uint32_t)q0;
             ja.q1 = (uint32_t)q1;
@@ -315,10 +317,11 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         bool work_read = false;
         uint32_t launches = 0;
         // every batch run records a (start, end) event pair; timings are computed on request
-        auto run_batch = [&](uint64_t a, uint64_t b, uint64_t *buf, uint64_t cap, Slot *dslot, cudaStream_t s) {
+        auto run_batch = [&](uint64_t a, uint64_t b, uint64_t *buf, uint64_t cap, Slot *dslot, cudaStream_t s,
+                             bool clear_slot) {
             cudaEvent_t e0 = event_get(idx->device), e1 = event_get(idx->device);
             res->runs.emplace_back(e0, e1);
-            SJ_CUDA(cudaMemsetAsync(dslot, 0, sizeof(Slot), s));
+            if (clear_slot) SJ_CUDA(cudaMemsetAsync(dslot, 0, sizeof(Slot), s));
             JoinArgs ja = base_args(idx, o, work);
             ja.out = buf;
             ja.cap = cap;
@@ -326,6 +329,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             ja.overflow = &dslot->overflow;
             ja.q0 = (uint32_t)a;
             ja.q1 = (uint32_t)b;
+            ja.nself = o.include_self ? (uint32_t)(b - a) : 0u;
             if (!res->span0) {
                 res->span0 = event_get(idx->device);
                 SJ_CUDA(cudaEventRecord(res->span0, s));
@@ -344,18 +348,19 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
 
         if (!o.result_on_host) {
             // ---- device-resident batches: every batch owns its buffer; streams run them
-            //      concurrently, S at a time (slot i % S of each stream is reused in order)
+            //      concurrently.  Up to 64 batches own a cursor slot each (cleared by the initial
+            //      memset; all read back by ONE copy at the end, with the work counters); beyond
+            //      that slot i % S of each stream is reused in order, read back per batch.
             res->batches.resize(nb);
             std::vector<uint64_t> counts(nb, 0);
-            auto drain_stream_slot = [&](size_t b) {   // host: read batch b's cursor (already synced)
-                counts[b] = hslots[b % S].cursor;
-            };
+            const bool own_slots = nb <= 64;
             for (size_t b = 0; b < nb; ++b) {
                 const int si = (int)(b % S);
                 cudaStream_t s = cx.streams[si];
-                if (b >= (size_t)S) {   // stream si's previous batch must have published its cursor
+                const size_t slot = own_slots ? b : (size_t)si;
+                if (!own_slots && b >= (size_t)S) {   // stream si's previous batch must have published its cursor
                     SJ_CUDA(cudaStreamSynchronize(s));
-                    drain_stream_slot(b - S);
+                    counts[b - S] = hslots[si].cursor;      // (+ the batch's self pairs below)
                 }
                 const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(
                     o.batch_capacity_pairs, est[b] + est[b] / 4 + 65536));
@@ -363,23 +368,29 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 bt.pairs = dalloc<uint64_t>(cap, s);
                 bt.cap = cap;
                 bt.on_device = 1;
-                run_batch(cuts[b], cuts[b + 1], bt.pairs, cap, dslots + si, s);
-                SJ_CUDA(cudaMemcpyAsync(hslots + si, dslots + si, sizeof(Slot), cudaMemcpyDeviceToHost, s));
+                run_batch(cuts[b], cuts[b + 1], bt.pairs, cap, dslots + slot, s, !own_slots);
+                if (!own_slots)
+                    SJ_CUDA(cudaMemcpyAsync(hslots + si, dslots + si, sizeof(Slot), cudaMemcpyDeviceToHost, s));
             }
             tr.mark("batches launched");
-            // the work counters are read back on stream 0 after every stream's last batch, so the
-            // one round of stream syncs below also covers them
+            // the work counters (and the own slots) are read back on stream 0 after every stream's
+            // last batch, so the one round of stream syncs below also covers them
             for (int i = 1; i < S; ++i) {
                 SJ_CUDA(cudaEventRecord(cx.events[2 + i], cx.streams[i]));
                 SJ_CUDA(cudaStreamWaitEvent(s0, cx.events[2 + i], 0));
             }
-            SJ_CUDA(cudaMemcpyAsync(hwork, work, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0));
+            SJ_CUDA(cudaMemcpyAsync(hwork, work, kWorkBytes + (own_slots ? sizeof(Slot) * nb : 0),
+                                    cudaMemcpyDeviceToHost, s0));
             for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
             tr.mark("batches done (synced)");
             work_read = true;
             cudaStream_t st_sort = s0;
-            for (size_t b = (nb > (size_t)S ? nb - S : 0); b < nb; ++b) drain_stream_slot(b);
-            tr.mark("drain slots");
+            if (own_slots) {
+                for (size_t b = 0; b < nb; ++b) counts[b] = hslots[b].cursor;
+            } else {
+                for (size_t b = (nb > (size_t)S ? nb - S : 0); b < nb; ++b) counts[b] = hslots[b % S].cursor;
+            }
+            for (size_t b = 0; b < nb; ++b) counts[b] += nself_of(cuts[b], cuts[b + 1]);
             for (size_t b = 0; b < nb; ++b) {
                 sj_batch &bt = res->batches[b];
                 uint64_t n = counts[b];
@@ -387,11 +398,11 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                     dev_free(bt.pairs, s0);
                     bt.pairs = dalloc<uint64_t>(n, s0);
                     bt.cap = n;
-                    run_batch(cuts[b], cuts[b + 1], bt.pairs, n, dslots, s0);
+                    run_batch(cuts[b], cuts[b + 1], bt.pairs, n, dslots, s0, true);
                     SJ_CUDA(cudaMemcpyAsync(hslots, dslots, sizeof(Slot), cudaMemcpyDeviceToHost, s0));
                     SJ_CUDA(cudaStreamSynchronize(s0));
                     ++stats.retries;
-                    n = hslots[0].cursor;
+                    n = hslots[0].cursor + nself_of(cuts[b], cuts[b + 1]);
                     if (n > bt.cap) fail(SJ_ERR_CUDA, "batch re-run overflowed");
                 }
                 bt.n = n;
@@ -421,7 +432,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 auto r = pending.front();
                 pending.pop_front();
                 inflight[i] = r;
-                run_batch(r.first, r.second, staging[i], scap[i], dslots + i, cx.streams[i]);
+                run_batch(r.first, r.second, staging[i], scap[i], dslots + i, cx.streams[i], true);
                 SJ_CUDA(cudaMemcpyAsync(hslots + i, dslots + i, sizeof(Slot), cudaMemcpyDeviceToHost,
                                         cx.streams[i]));
                 order.push_back(i);
@@ -433,8 +444,8 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 // the cursor copy follows the kernel on stream i; the previous D2H on this stream
                 // precedes the kernel, so a stream sync here waits for exactly that batch.
                 SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
-                const uint64_t n = hslots[i].cursor;
                 const auto r = inflight[i];
+                const uint64_t n = hslots[i].cursor + nself_of(r.first, r.second);
                 if (n > scap[i]) {
                     ++stats.retries;
                     if (r.second - r.first < 2) {
@@ -470,11 +481,14 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
 
         // ---- work counters (already read back unless a retry / host mode ran more kernels)
         if (!work_read || stats.retries || o.sort_pairs) {
-            SJ_CUDA(cudaMemcpyAsync(hwork, work, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0));
+            SJ_CUDA(cudaMemcpyAsync(hwork, work, kWorkBytes, cudaMemcpyDeviceToHost, s0));
             SJ_CUDA(cudaStreamSynchronize(s0));
         }
-        stats.cells_probed = hwork[0];
-        stats.candidates_tested = hwork[1];
+        unsigned long long wsum[3] = {0, 0, 0};
+        for (int sl = 0; sl < kWorkSlots; ++sl)
+            for (int i = 0; i < 3; ++i) wsum[i] += hwork[4 * sl + i];
+        stats.cells_probed = wsum[0];
+        stats.candidates_tested = wsum[1];
         stats.pairs = res->total;
         stats.batches = (uint32_t)res->batches.size();
         stats.refine_launches = launches;
@@ -499,12 +513,13 @@ void neighbor_counts_impl(const sj_index *idx, const sj_join_opts &o, uint32_t *
     uint64_t q0, q1;
     validate(idx, o, &q0, &q1);
     SJ_CUDA(cudaSetDevice(idx->device));
-    CtxGuard cg{acquire_ctx(idx->device, 1, 2, 64)};
+    constexpr size_t kWorkBytes = sizeof(unsigned long long) * 4 * kWorkSlots;
+    CtxGuard cg{acquire_ctx(idx->device, 1, 2, kWorkBytes)};
     DevCtx &cx = *cg.c;
     cudaStream_t s = cx.streams[0];
     unsigned long long *work = static_cast<unsigned long long *>(cx.d_slots);
     unsigned long long *hwork = static_cast<unsigned long long *>(cx.h_slots);
-    SJ_CUDA(cudaMemsetAsync(work, 0, 4 * sizeof(unsigned long long), s));
+    SJ_CUDA(cudaMemsetAsync(work, 0, kWorkBytes, s));
     Scratch<uint32_t> own_cnt;
     uint32_t *c = cnt;
     if (!c) {
@@ -518,9 +533,11 @@ void neighbor_counts_impl(const sj_index *idx, const sj_join_opts &o, uint32_t *
     ja.q0 = (uint32_t)q0;
     ja.q1 = (uint32_t)q1;
     launch_refine<kCountPoint>(idx->dev, ja, o.unicomp != 0, (uint32_t)(q1 - q0), s);
-    SJ_CUDA(cudaMemcpyAsync(hwork, work, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaMemcpyAsync(hwork, work, kWorkBytes, cudaMemcpyDeviceToHost, s));
     SJ_CUDA(cudaStreamSynchronize(s));
-    if (total) *total = hwork[2];
+    unsigned long long em = 0;
+    for (int sl = 0; sl < kWorkSlots; ++sl) em += hwork[4 * sl + 2];
+    if (total) *total = em;
 }
 
 }  // namespace sj

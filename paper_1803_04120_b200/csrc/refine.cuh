@@ -55,6 +55,8 @@ struct JoinArgs {
     uint32_t n_dense_tasks;
     int include_self;
     int use_masks;
+    uint32_t nself;                // kEmit: self pairs of the batch (q1 - q0 if include_self, else 0):
+                                   // query k's (p,p) sits at out[k - q0], every other pair after them
 };
 
 // Per-warp emission buffer of the dense kernel (shared memory): hits are appended at warp-uniform
@@ -121,7 +123,7 @@ __device__ __forceinline__ void emit(const JoinArgs &ja, bool hit, uint32_t pid,
         base = __shfl_sync(mask, base, leader);
         if (hit) {
             emitted += per;
-            const unsigned long long pos = base + (unsigned long long)(__popc(hits & ((1u << lane) - 1u)) * per);
+            const unsigned long long pos = ja.nself + base + (unsigned long long)(__popc(hits & ((1u << lane) - 1u)) * per);
             if (pos + per <= ja.cap) {
                 ja.out[pos] = ((uint64_t)pid << 32) | qid;
                 if (BOTH) ja.out[pos + 1] = ((uint64_t)qid << 32) | pid;
@@ -129,6 +131,21 @@ __device__ __forceinline__ void emit(const JoinArgs &ja, bool hit, uint32_t pid,
                 atomicOr(ja.overflow, 1u);
             }
         }
+    }
+}
+
+// The self pair (p,p) of query k (reading R3): in kEmit mode its slot is fixed, out[k - q0], so it
+// needs no cursor atomic (one same-address atomic per warp serialised in L2 on sparse data).
+template <int MODE>
+__device__ __forceinline__ void emit_self(const JoinArgs &ja, uint32_t k, uint32_t pid, uint32_t &emitted)
+{
+    if constexpr (MODE == kEmit) {
+        const uint64_t pos = (uint64_t)(k - ja.q0);
+        if (pos < ja.cap) ja.out[pos] = ((uint64_t)pid << 32) | pid;
+        else atomicOr(ja.overflow, 1u);
+        ++emitted;
+    } else {
+        emit<MODE, false>(ja, true, pid, pid, emitted);
     }
 }
 
@@ -144,7 +161,7 @@ __device__ __forceinline__ void warpbuf_flush(const JoinArgs &ja, WarpBuf &wb, u
     base = __shfl_sync(mask, base, leader);
     const uint32_t nl = __popc(mask), rank = __popc(mask & ((1u << lane) - 1u));
     for (uint32_t i = rank; i < wb.cnt; i += nl) {
-        const unsigned long long pos = base + i;
+        const unsigned long long pos = ja.nself + base + i;
         if (pos < ja.cap) ja.out[pos] = wb.buf[i];
         else atomicOr(ja.overflow, 1u);
     }
@@ -246,6 +263,7 @@ struct TopTable {
     int64_t dp[kMaxTop];     // sum delta_i * pstride_i
     int64_t dk[kMaxTop];     // dp * dir_div (key delta)
     int64_t dq[kMaxTop];     // dp * occ_cpd (occupancy-bitmap index delta)
+    int64_t dq2[kMaxTop];    // dp * occ2_cpd (second bitmap)
     uint32_t bits[kMaxTop];  // [0:6) dims at -1, [8:14) dims at +1, [16:22) one-hot highest moved dim
 };
 
@@ -265,6 +283,7 @@ __device__ __forceinline__ void build_top_table(const DevIndex &ix, TopTable &tt
         tt.dp[t] = dp;
         tt.dk[t] = dp * (int64_t)ix.dir_div;
         tt.dq[t] = dp * (int64_t)ix.occ_cpd;
+        tt.dq2[t] = dp * (int64_t)ix.occ2_cpd;
         tt.bits[t] = neg | (pos << 8) | (top << 16);
     }
 }
@@ -293,6 +312,115 @@ __device__ __forceinline__ uint32_t bad_moves(const DevIndex &ix, const JoinArgs
     return bad;
 }
 
+// A cell hh of the prefix range whose key differs from the (offset-moved) home key by dlt, with
+// |dlt| <= lowR[L]: adjacent iff dlt = sum_{i<L} delta_i * stride_i with every delta_i in {-1,0,1}
+// (greedy from the top low dimension; mixed-radix digits are unique and stride_i > 2 sum_{m<i}
+// stride_m).  The deciding dimension of unicomp is the highest moved one: jtop (a top dim) if
+// the offset moved one, else the highest moved low dim.
+template <int D, int MODE, bool UNICOMP, bool DENSE>
+__device__ __forceinline__ void test_low_cell(const DevIndex &ix, const JoinArgs &ja, QueryState<D> &q,
+                                              uint32_t hh, int64_t dlt, int jtop, int L, unsigned wmask,
+                                              WarpBuf *wb)
+{
+    int jlow = -1;
+#pragma unroll
+    for (int i = D - 2; i >= 0; --i) {
+        if (i >= L) continue;
+        const int64_t R = ix.lowR[i], st = (int64_t)ix.strides[i];
+        if (dlt > R) { dlt -= st; if (jlow < 0) jlow = i; }
+        else if (dlt < -R) { dlt += st; if (jlow < 0) jlow = i; }
+    }
+    if (dlt != 0) return;                            // not representable: not adjacent
+    const int j = jtop >= 0 ? jtop : jlow;
+    if (UNICOMP && !((q.odd >> j) & 1u)) return;
+    scan_range<D, MODE, UNICOMP, DENSE>(ix, ja, q, __ldg(ix.G + hh), __ldg(ix.G + hh + 1), 1u, wb, wmask);
+}
+
+// Sparse regime with k <= 3 top dimensions (the occupancy bitmap is built): the top offsets are
+// visited in blocks by their highest moved top dimension, so a block that unicomp rejects (that
+// dimension's coordinate even -- warp-uniform for the slow dimensions of A-ordered queries) is
+// skipped with one branch; the bitmap loads of a block are issued together; the home top offset
+// needs no directory lookup: its adjacent cells are the run of B within +-lowR[L] of the home
+// key around h (B is sorted and |key difference| <= lowR[L] < stride_L keeps the run inside
+// the prefix).
+template <int D, int MODE, bool UNICOMP>
+__device__ __forceinline__ void search_cell_scan_sparse(const DevIndex &ix, const JoinArgs &ja, QueryState<D> &q,
+                                                        uint32_t h, uint64_t key, uint32_t bad, const TopTable &tt,
+                                                        unsigned wmask)
+{
+    const int k = ix.dir_k;
+    const int L = D - k;
+    uint64_t ph = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) ph += q.c[j] * ix.pstride[j];
+    uint64_t cl = q.c[0];
+#pragma unroll
+    for (int i = 1; i < D; ++i) if (i == L - 1) cl = q.c[i];
+    const uint64_t qc = ph * ix.occ_cpd + cl;
+    uint64_t cl2 = q.c[0];
+#pragma unroll
+    for (int i = 1; i < D; ++i) if (i == L - 2) cl2 = q.c[i];
+    const uint64_t qc2 = ph * ix.occ2_cpd + cl2;
+    const int64_t Rl = ix.lowR[L];
+    constexpr uint32_t kPow3[4] = {1, 3, 9, 27};
+#pragma unroll 1
+    for (int jt = k - 1; jt >= 0; --jt) {
+        __syncwarp(wmask);
+        if (UNICOMP && !((q.odd >> (L + jt)) & 1u)) continue;
+        const uint32_t nb = 2u * kPow3[jt];
+        const uint32_t tbase = (kPow3[k] - kPow3[jt + 1]) / 2u;   // digits above jt = "0 move"
+        uint32_t live = 0;
+#pragma unroll
+        for (uint32_t i = 0; i < 18u; ++i) {
+            if (i < nb) {
+                const uint32_t t = tbase + (i >> 1) + ((i & 1u) ? 2u * kPow3[jt] : 0u);
+                if (!(tt.bits[t] & bad)) {
+                    // both bitmaps' loads are issued together (no dependent second round)
+                    const uint64_t qb = qc + (uint64_t)tt.dq[t];
+                    uint32_t ok = __ldg(ix.occ + (qb >> 5)) >> (qb & 31);
+                    if (ix.occ2) {
+                        const uint64_t qb2 = qc2 + (uint64_t)tt.dq2[t];
+                        ok &= __ldg(ix.occ2 + (qb2 >> 5)) >> (qb2 & 31);
+                    }
+                    if (ok & 1u) live |= 1u << i;
+                }
+            }
+        }
+        const int dim = L + jt;
+#pragma unroll 1
+        while (live) {
+            const uint32_t i = __ffs(live) - 1;
+            live &= live - 1u;
+            const uint32_t t = tbase + (i >> 1) + ((i & 1u) ? 2u * kPow3[jt] : 0u);
+            const uint64_t p = ph + (uint64_t)tt.dp[t];
+            ++q.probes;
+            const uint32_t lo = __ldg(ix.dir + p), hi = __ldg(ix.dir + p + 1);
+            const uint64_t kal = key + (uint64_t)tt.dk[t];
+#pragma unroll 1
+            for (uint32_t hh = lo; hh < hi; ++hh) {
+                const int64_t dlt = (int64_t)(__ldg(ix.B + hh) - kal);
+                if (dlt > Rl || dlt < -Rl) continue;
+                test_low_cell<D, MODE, UNICOMP, false>(ix, ja, q, hh, dlt, dim, L, wmask, nullptr);
+            }
+        }
+    }
+    // home top offset: outward from h while |B[hh] - key| <= lowR[L]
+    __syncwarp(wmask);
+    ++q.probes;
+#pragma unroll 1
+    for (uint32_t hh = h; hh-- > 0;) {
+        const int64_t dlt = (int64_t)(__ldg(ix.B + hh) - key);
+        if (dlt < -Rl) break;
+        test_low_cell<D, MODE, UNICOMP, false>(ix, ja, q, hh, dlt, -1, L, wmask, nullptr);
+    }
+#pragma unroll 1
+    for (uint32_t hh = h + 1; hh < ix.nG; ++hh) {
+        const int64_t dlt = (int64_t)(__ldg(ix.B + hh) - key);
+        if (dlt > Rl) break;
+        test_low_cell<D, MODE, UNICOMP, false>(ix, ja, q, hh, dlt, -1, L, wmask, nullptr);
+    }
+}
+
 // ---- search mode kSearchCellScan (sparse high-d data): for each offset of the top-k
 // (directory) dimensions, the cells of that prefix are B[dir[p], dir[p+1]) -- a handful.  Each
 // is tested by its low coordinates: it is adjacent iff its key differs from the home key moved
@@ -319,7 +447,11 @@ __device__ __forceinline__ void search_cell_scan(const DevIndex &ix, const JoinA
     uint64_t cl = q.c[0];
 #pragma unroll
     for (int i = 1; i < D; ++i) if (i == L - 1) cl = q.c[i];
-    const uint64_t qh = ph * ix.occ_cpd + cl - 1ull;   // bitmap index of the home window's start
+    const uint64_t qh = ph * ix.occ_cpd + cl;   // bitmap index of the home top-(k+1) prefix
+    uint64_t cl2 = q.c[0];
+#pragma unroll
+    for (int i = 1; i < D; ++i) if (i == L - 2) cl2 = q.c[i];
+    const uint64_t qh2 = ph * ix.occ2_cpd + cl2;
 #ifndef SJ_CHUNK
 #define SJ_CHUNK 27
 #endif
@@ -338,11 +470,14 @@ __device__ __forceinline__ void search_cell_scan(const DevIndex &ix, const JoinA
             if (bits & bad) continue;            // masked-out coordinate, or decided by an even top dim
             if (ix.occ) {
                 // joint-occupancy filter: is any (k+1)-prefix p*|g_{L-1}| + c_{L-1} + {-1,0,1}
-                // occupied?  (the top low dimension's window; PAPER.md:173 masks, generalised)
+                // occupied?  (the top low dimension's window, one bit of the dilated bitmap;
+                // PAPER.md:173 masks, generalised)
                 const uint64_t qb = qh + (uint64_t)tt.dq[t];
-                uint32_t win = __ldg(ix.occ + (qb >> 5)) >> (qb & 31);
-                if ((qb & 31) > 29) win |= __ldg(ix.occ + (qb >> 5) + 1) << (32 - (qb & 31));
-                if (!(win & 7u)) continue;
+                if (!((__ldg(ix.occ + (qb >> 5)) >> (qb & 31)) & 1u)) continue;
+                if (ix.occ2) {
+                    const uint64_t qb2 = qh2 + (uint64_t)tt.dq2[t];
+                    if (!((__ldg(ix.occ2 + (qb2 >> 5)) >> (qb2 & 31)) & 1u)) continue;
+                }
             }
             live |= 1u << u;
         }
@@ -370,20 +505,9 @@ __device__ __forceinline__ void search_cell_scan(const DevIndex &ix, const JoinA
 #pragma unroll 1
             for (uint32_t hh = lo; hh < hi; ++hh) {
                 if (hh == h) continue;                       // home cell handled separately
-                int64_t dlt = (int64_t)(__ldg(ix.B + hh) - kal);
+                const int64_t dlt = (int64_t)(__ldg(ix.B + hh) - kal);
                 if (dlt > Rl || dlt < -Rl) continue;         // outside the +-1 box
-                int jlow = -1;
-#pragma unroll
-                for (int i = D - 2; i >= 0; --i) {
-                    if (i >= L) continue;
-                    const int64_t R = ix.lowR[i], st = (int64_t)ix.strides[i];
-                    if (dlt > R) { dlt -= st; if (jlow < 0) jlow = i; }
-                    else if (dlt < -R) { dlt += st; if (jlow < 0) jlow = i; }
-                }
-                if (dlt != 0) continue;                      // not representable: not adjacent
-                const int j = jtop >= 0 ? jtop : jlow;
-                if (UNICOMP && !((q.odd >> j) & 1u)) continue;
-                scan_range<D, MODE, UNICOMP, DENSE>(ix, ja, q, __ldg(ix.G + hh), __ldg(ix.G + hh + 1), 1u, wb, wmask);
+                test_low_cell<D, MODE, UNICOMP, DENSE>(ix, ja, q, hh, dlt, jtop, L, wmask, wb);
             }
         }
     }
@@ -488,10 +612,10 @@ __device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs 
 
     // ---- home cell: (p,p) once; unicomp: q after p in A-order, both orientations (R10)
     if constexpr (DENSE) {
-        emit_buffered<false>(ja, *wb, wmask, q.valid && ja.include_self != 0, q.pid, q.pid, q.emitted);
+        if (q.valid && ja.include_self) emit_self<MODE>(ja, q.k, q.pid, q.emitted);
         scan_range<D, MODE, UNICOMP, true, true>(ix, ja, q, cs, ce, 1u, wb, wmask);
     } else {
-        if (q.sub == 0) emit<MODE, false>(ja, ja.include_self != 0, q.pid, q.pid, q.emitted);
+        if (q.sub == 0 && ja.include_self) emit_self<MODE>(ja, q.k, q.pid, q.emitted);
         if constexpr (UNICOMP) {
             scan_range<D, MODE, true>(ix, ja, q, k + 1 + q.sub, ce, q.G);
         } else {
@@ -503,6 +627,12 @@ __device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs 
     const uint32_t bad = bad_moves<D, UNICOMP>(ix, ja, q, h);
     __syncwarp(wmask);
     if (ix.search_mode == kSearchCellScan) {
+        if constexpr (!DENSE) {
+            if (ix.occ && ix.dir_k <= 3 && q.G == 1u) {
+                search_cell_scan_sparse<D, MODE, UNICOMP>(ix, ja, q, h, key, bad, tt, wmask);
+                return;
+            }
+        }
         search_cell_scan<D, MODE, UNICOMP, DENSE>(ix, ja, q, h, key, bad, tt, wmask, wb);
         return;
     }
@@ -520,6 +650,30 @@ __device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs 
     search_rows<D, MODE, UNICOMP, DENSE>(ix, ja, q, key, bad, wmask, wb);
 }
 
+// Work counters (directory/row lookups, distance tests, emissions): warp shuffle-reduce, then one
+// set of fire-and-forget atomics per warp into one of kWorkSlots slots (warp id modulo; the host
+// sums the slots).  Per-warp atomics on three shared addresses serialised in L2 and cost as much
+// as the whole sparse 6-D refine; a CTA-wide reduction instead made every warp wait at a barrier
+// for the CTA's slowest warp (19% of the stall samples).
+constexpr int kWorkSlots = 256;
+__device__ __forceinline__ void flush_work(const JoinArgs &ja, unsigned long long p, unsigned long long c,
+                                           unsigned long long em)
+{
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        p += __shfl_xor_sync(0xffffffffu, p, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+        em += __shfl_xor_sync(0xffffffffu, em, o);
+    }
+    if ((threadIdx.x & 31) == 0 && ja.work) {
+        const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        unsigned long long *w = ja.work + 4 * (gw % kWorkSlots);
+        atomicAdd(w + 0, p);
+        atomicAdd(w + 1, c);
+        atomicAdd(w + 2, em);
+    }
+}
+
 // Dense kernel (kEmit): one warp per task = up to 32 consecutive queries of one populous cell
 // (>= dense_T points).  All lanes share the home cell, so the whole neighbour enumeration and every
 // candidate loop are warp-uniform: candidates are broadcast loads, hits go through the per-warp
@@ -531,10 +685,7 @@ k_refine_dense(const DevIndex ix, const JoinArgs ja)
 {
     __shared__ TopTable tt;
     extern __shared__ __align__(16) uint64_t s_buf[];     // [kDenseWarps][kWarpBufPairs]
-    if (ix.search_mode == kSearchCellScan) {
-        build_top_table<D>(ix, tt);
-        __syncthreads();
-    }
+    if (ix.search_mode == kSearchCellScan) build_top_table<D>(ix, tt);
     // the batch's tasks are the contiguous range [t_lo, t_hi) of the A-ordered task list: tasks
     // with start + 32 > q0 and start < q1 (one binary search per CTA)
     __shared__ uint32_t s_tlo;
@@ -550,36 +701,27 @@ k_refine_dense(const DevIndex ix, const JoinArgs ja)
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t task = s_tlo + blockIdx.x * kDenseWarps + warp;
-    if (task >= ja.n_dense_tasks) return;
-    const uint32_t start = __ldg(ja.dense_tasks + task);
-    const uint32_t h = __ldg(ix.pcell + start);
-    const uint32_t end = min(start + 32u, __ldg(ix.G + h + 1));
-    const uint32_t a = max(start, ja.q0), b = min(end, ja.q1);
-    if (a >= b) return;                                // task outside this batch
-    WarpBuf wb{s_buf + (size_t)warp * kWarpBufPairs, 0u};
     QueryState<D> q;
     q.G = 1u;
     q.sub = 0u;
     q.emitted = q.probes = q.tests = 0;
-    // every lane runs the (cell-uniform) enumeration; lanes past the task's end are helpers that
-    // load and broadcast candidates but never emit (they take the first query's point)
-    const uint32_t k = a + lane;
-    q.valid = k < b;
-    refine_query<D, kEmit, UNICOMP, true>(ix, ja, q.valid ? k : a, h, __ldg(ix.G + h), __ldg(ix.G + h + 1),
-                                          0xffffffffu, q, tt, &wb);
-    warpbuf_flush(ja, wb, 0xffffffffu);
-    unsigned long long p = q.probes, c = q.tests, em = q.emitted;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        p += __shfl_xor_sync(0xffffffffu, p, o);
-        c += __shfl_xor_sync(0xffffffffu, c, o);
-        em += __shfl_xor_sync(0xffffffffu, em, o);
+    if (task < ja.n_dense_tasks) {                     // warp-uniform
+        const uint32_t start = __ldg(ja.dense_tasks + task);
+        const uint32_t h = __ldg(ix.pcell + start);
+        const uint32_t end = min(start + 32u, __ldg(ix.G + h + 1));
+        const uint32_t a = max(start, ja.q0), b = min(end, ja.q1);
+        if (a < b) {                                   // task inside this batch
+            WarpBuf wb{s_buf + (size_t)warp * kWarpBufPairs, 0u};
+            // every lane runs the (cell-uniform) enumeration; lanes past the task's end are helpers
+            // that load and broadcast candidates but never emit (they take the first query's point)
+            const uint32_t k = a + lane;
+            q.valid = k < b;
+            refine_query<D, kEmit, UNICOMP, true>(ix, ja, q.valid ? k : a, h, __ldg(ix.G + h), __ldg(ix.G + h + 1),
+                                                  0xffffffffu, q, tt, &wb);
+            warpbuf_flush(ja, wb, 0xffffffffu);
+        }
     }
-    if (lane == 0 && ja.work) {
-        atomicAdd(ja.work + 0, p);
-        atomicAdd(ja.work + 1, c);
-        atomicAdd(ja.work + 2, em);
-    }
+    flush_work(ja, q.probes, q.tests, q.emitted);
 }
 
 template <int D, int MODE, bool UNICOMP>
@@ -624,19 +766,7 @@ k_refine(const DevIndex ix, const JoinArgs ja)
         for (uint32_t o = 1; o < q.G; o <<= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
         if (active && q.sub == 0) atomicAdd(ja.qbucket + qi / ja.group, (unsigned long long)e);
     }
-    // work counters: warp reduce, one atomic per warp
-    unsigned long long p = q.probes, c = q.tests, em = q.emitted;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        p += __shfl_xor_sync(0xffffffffu, p, o);
-        c += __shfl_xor_sync(0xffffffffu, c, o);
-        em += __shfl_xor_sync(0xffffffffu, em, o);
-    }
-    if ((threadIdx.x & 31) == 0 && ja.work) {
-        atomicAdd(ja.work + 0, p);
-        atomicAdd(ja.work + 1, c);
-        atomicAdd(ja.work + 2, em);
-    }
+    flush_work(ja, q.probes, q.tests, q.emitted);
 }
 
 }  // namespace sj

@@ -105,6 +105,10 @@ struct DevIndex {
     const uint32_t *occ;
     uint64_t occ_div;            // stride of dimension d-k-1
     uint64_t occ_cpd;            // |g_{d-k-1}|
+    // second occupancy bitmap over (top-k prefix, c_{d-k-2}) -- the next low dimension -- for the
+    // survivors of the first (both stored dilated by +-1 along their low dimension)
+    const uint32_t *occ2;
+    uint64_t occ2_cpd;           // |g_{d-k-2}|
     // per non-empty cell, precomputed at build time: packed coordinates (c_j at bit cshift[j],
     // width cbits[j]; nullptr when sum of widths > 64) and the Alg. 1 line-6 mask word (bit i: move
     // -1 in dim i leaves M_i; bit 8+i: move +1 leaves M_i)

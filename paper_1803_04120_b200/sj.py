@@ -74,6 +74,7 @@ def load_library(path: str = LIB_PATH):
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("SJ_LIBRARY", path)      # experiment builds (tools/variants.sh); same ABI
     if not os.path.exists(path):
         raise RuntimeError(f"libsj.so not built at {path}: run `python -m paper_1803_04120_b200.build` "
                            "(or __graft_entry__.build()); there is no CPU fallback")

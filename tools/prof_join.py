@@ -29,7 +29,7 @@ for _ in range(a.reps):
     if a.quiet:
         st = res.stats
         print(f"d={a.d} eps={a.eps} G={a.lanes} pairs={res.n_pairs} join_ms={st['total_ms']:.3f} "
-              f"refine_ms={st['refine_ms']:.3f} est_ms={st['estimate_ms']:.3f} build_ms={idx.timings()['total_ms']:.3f}",
+              f"refine_ms={st['refine_ms']:.3f} span={st['refine_span_ms']:.3f} probes={st['cells_probed']} cand={st['candidates_tested']} est_ms={st['estimate_ms']:.3f} build_ms={idx.timings()['total_ms']:.3f}",
               flush=True)
     else:
         print(res.n_pairs, res.stats, idx.timings(), idx.geometry()["dir_k"], flush=True)
