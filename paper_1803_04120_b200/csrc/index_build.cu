@@ -187,14 +187,23 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
                  const double *__restrict__ pts, uint32_t n, uint32_t *__restrict__ pcell,
                  uint64_t *__restrict__ B, uint32_t *__restrict__ G, double *__restrict__ X,
                  uint64_t *__restrict__ ccoord, uint32_t *__restrict__ cmask, DevIndex ix, uint32_t dense_T,
-                 uint32_t *__restrict__ n_dense_cells, uint32_t *__restrict__ dirhist, uint32_t *__restrict__ occ)
+                 uint32_t *__restrict__ n_dense_cells, uint32_t *__restrict__ dirhist, uint32_t *__restrict__ occ,
+                 bool bucket_cells, double dir_inv)
 {
     const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const uint32_t a = A[k];
-    const uint32_t h = pcell[k] - 1u;
-    pcell[k] = h;
     const uint64_t key = keys[k];
+    uint32_t h;
+    if (bucket_cells) {             // cell = directory start of the key's top-k prefix + index within it
+        uint64_t b = (uint64_t)((double)key * dir_inv);
+        if (b * ix.dir_div > key) --b;
+        else if ((b + 1) * ix.dir_div <= key) ++b;
+        h = __ldg(ix.dir + b) + pcell[k];
+    } else {                        // inclusive scan of head flags (1-based)
+        h = pcell[k] - 1u;
+    }
+    pcell[k] = h;
     if (k == 0 || keys[k - 1] != key) {
         B[h] = key;
         G[h] = (uint32_t)k;
@@ -270,6 +279,8 @@ struct BuildArgs {
     uint32_t *cmask = nullptr;
     uint32_t *ndense = nullptr;
     uint32_t *dirhist = nullptr;
+    bool bucket_cells = false;   // pcell holds the cell index within the top-k prefix; dir is final
+    double dir_inv = 0.0;
     uint32_t *occ = nullptr;
 };
 
@@ -284,7 +295,7 @@ void launch_dim(int which, dim3 g, cudaStream_t s, const DevIndex &ix, const Bui
                                                                  a.bhist);
     } else {
         k_compact_gather<D><<<g, kThreads, 0, s>>>(a.keys, a.A, a.pts, a.n, a.pcell, a.B, a.G, a.X, a.ccoord, a.cmask,
-                                                   ix, 16u, a.ndense, a.dirhist, a.occ);
+                                                   ix, 16u, a.ndense, a.dirhist, a.occ, a.bucket_cells, a.dir_inv);
     }
     SJ_LAUNCHED();
 }
@@ -520,7 +531,7 @@ void finish_aux(sj_index *idx, cudaStream_t s, uint32_t *aux, const DirPlan &dp,
 {
     sj_index_view &v = idx->view;
     DevIndex &ix = idx->dev;
-    exclusive_scan_u32(dirhist, const_cast<uint32_t *>(ix.dir), (uint64_t)dp.P + 1, s);
+    if (dirhist) exclusive_scan_u32(dirhist, const_cast<uint32_t *>(ix.dir), (uint64_t)dp.P + 1, s);
     SJ_CUDA(cudaMemcpyAsync(h_aux, aux, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     SJ_CUDA(cudaStreamSynchronize(s));
     uint32_t *tasks = nullptr;
@@ -694,7 +705,8 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
     // a3 strategy: sparse keys (<= 2 points per top-k prefix on average, P <= 2^22 so the bucket
     // arrays stay L2-sized; measured slower than LSD at P = 11.4 M) -> prefix buckets + per-bucket
     // sort; otherwise stable LSD radix sort
-    const bool use_bucket = allow_bucket && dp.k >= 1 && (double)n <= 2.0 * (double)dp.P && dp.P <= (1ull << 22);
+    const bool use_bucket = allow_bucket && dp.k >= 1 && (double)n <= 2.0 * (double)dp.P && dp.P <= (1ull << 22) &&
+                            v.key_bits <= 62;
 
     sj_index *idx = new sj_index();
     idx->device = o.device;
@@ -731,22 +743,37 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ev.rec(3, s);
 
         // ---- a3: sort of (key, id) into (key, id)-ascending order (= stable sort by key, R14)
+        uint32_t *pcell = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
+        idx->view = v;
+        alloc_dir(idx, dp, s);
+        uint32_t *dir = const_cast<uint32_t *>(idx->dev.dir);
         bool in_tmp = false;
-        if (use_bucket) bucket_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, dp.div, dp.P, bhist.p, aux + 3, s);
-        else radix_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, v.key_bits, s, &in_tmp);
+        Scratch<uint32_t> dirhist;
+        if (use_bucket) {
+            // the bucket sort also numbers each bucket's cells: pcell = cell index within the
+            // bucket, bhist = cells per bucket, whose exclusive scan IS the prefix directory
+            bucket_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, dp.div, dp.P, bhist.p, aux + 3, pcell, bhist.p, s);
+            exclusive_scan_u32(bhist.p, dir, (uint64_t)dp.P + 1, s);
+            SJ_CUDA(cudaMemcpyAsync(aux, dir + dp.P, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        } else {
+            radix_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, v.key_bits, s, &in_tmp);
+        }
         const uint64_t *skeys = in_tmp ? keys_tmp.p : keys.p;
         if (in_tmp) SJ_CUDA(cudaMemcpyAsync(A, ids_tmp.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
         ev.rec(4, s);
 
-        // ---- a4: heads, cell numbering, compaction, SoA gather, directory histogram, occupancy
-        // bits.  B and G are sized for the upper bound N cells so no host round trip is needed
-        // here; |G| is read back by the single sync of finish_aux.
-        uint32_t *pcell = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
-        {
+        // ---- a4: cell numbering (LSD path: heads + scan), compaction, SoA gather, directory
+        // histogram (LSD path), occupancy bits.  B and G are sized for the upper bound N cells so no
+        // host round trip is needed here; |G| is read back by the single sync of finish_aux.
+        if (!use_bucket) {
             Scratch<uint32_t> flags(n, s);
             k_heads<<<grid, kThreads, 0, s>>>(skeys, N, flags.p);
             SJ_LAUNCHED();
             inclusive_scan_u32(flags.p, pcell, n, s);
+            SJ_CUDA(cudaMemcpyAsync(aux, pcell + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+            dirhist.p = dalloc<uint32_t>((size_t)dp.P + 1, s);
+            dirhist.s = s;
+            SJ_CUDA(cudaMemsetAsync(dirhist.p, 0, sizeof(uint32_t) * ((size_t)dp.P + 1), s));
         }
         uint64_t *B = static_cast<uint64_t *>(own(dev_alloc(sizeof(uint64_t) * n, s)));
         uint32_t *G = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * ((size_t)n + 1), s)));
@@ -757,11 +784,6 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
             ccoord = static_cast<uint64_t *>(own(dev_alloc(sizeof(uint64_t) * n, s)));
             cmask = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
         }
-        idx->view = v;
-        alloc_dir(idx, dp, s);
-        Scratch<uint32_t> dirhist((size_t)dp.P + 1, s);
-        SJ_CUDA(cudaMemsetAsync(dirhist.p, 0, sizeof(uint32_t) * ((size_t)dp.P + 1), s));
-        SJ_CUDA(cudaMemcpyAsync(aux, pcell + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
         ix.masks = masks;
         ix.occ = idx->dev.occ;
         ix.occ2 = idx->dev.occ2;
@@ -776,6 +798,8 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ba.cmask = cmask;
         ba.ndense = aux + 2;
         ba.dirhist = dirhist.p;
+        ba.bucket_cells = use_bucket;
+        ba.dir_inv = 1.0 / (double)dp.div;
         ba.occ = const_cast<uint32_t *>(ix.occ);
         launch(d, 2, grid, s, ix, ba);
         ix.ccoord = ccoord;
@@ -799,6 +823,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         idx->view = v;
         idx->dev = ix;
         finish_aux(idx, s, aux, dp, dirhist.p, false, h_aux);   // the build's late host sync
+        v.n_cells = idx->view.n_cells;
         ev.rec(6, s);
         tr.mark("compact+dir+dense (synced)");
         for (int i = 0; i < 7; ++i) {

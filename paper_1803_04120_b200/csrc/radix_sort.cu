@@ -309,20 +309,22 @@ k_bucket_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ 
     vout[pos] = vin[i];
 }
 
-// big[0] = number of queued big buckets, big[1..] = their ids
+// big[0] = number of queued big buckets, big[1..] = their ids.
+// Besides sorting, each bucket reports its cells (distinct keys): local[i] = index of item i's cell
+// among the bucket's cells, cellcnt[b] = the bucket's cell count -- the exclusive scan of cellcnt
+// is the prefix directory and gives every item its global cell number (no head-flag pass/scan).
 __global__ void __launch_bounds__(256)
 k_bucket_sort(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, const uint32_t *__restrict__ start,
               uint64_t P, uint64_t *__restrict__ kout, uint32_t *__restrict__ vout, uint32_t *__restrict__ big,
-              uint32_t big_cap)
+              uint32_t big_cap, uint32_t *__restrict__ local, uint32_t *__restrict__ cellcnt)
 {
     const uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= P) return;
     const uint32_t s = start[b], e = start[b + 1];
-    if (e == s) return;
     if (e - s > kBucketMax) {
         const uint32_t slot = atomicAdd(big, 1u);
         if (slot < big_cap) big[1 + slot] = (uint32_t)b;
-        return;
+        return;                                        // cellcnt[b] written by the big-bucket kernel
     }
     // insertion sort by (key, id) directly in the output range (a few L1-resident entries)
     for (uint32_t i = s; i < e; ++i) {
@@ -340,19 +342,33 @@ k_bucket_sort(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin
         kout[j] = ki;
         vout[j] = vi;
     }
+    uint32_t c = 0;
+    uint64_t prev = 0;
+    for (uint32_t i = s; i < e; ++i) {
+        const uint64_t k = kout[i];
+        if (i > s && k != prev) ++c;
+        local[i] = c;
+        prev = k;
+    }
+    cellcnt[b] = (e > s) ? c + 1 : 0;
 }
 
 // One CTA per queued big bucket (grid-stride over the queue): bitonic sort of (key, id) in shared
-// memory, padded to a power of two with (UINT64_MAX, UINT32_MAX).
+// memory, padded to a power of two with (UINT64_MAX, UINT32_MAX); then the cells of the bucket
+// (head flags, CTA-wide scan) -> local[], cellcnt[b].
 __global__ void __launch_bounds__(kBigThreads)
 k_bucket_sort_big(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin,
                   const uint32_t *__restrict__ start, const uint32_t *__restrict__ big, uint32_t big_cap,
-                  uint64_t *__restrict__ kout, uint32_t *__restrict__ vout, uint32_t *__restrict__ overflow)
+                  uint64_t *__restrict__ kout, uint32_t *__restrict__ vout, uint32_t *__restrict__ overflow,
+                  uint32_t *__restrict__ local, uint32_t *__restrict__ cellcnt)
 {
-    __shared__ uint64_t sk[kBigMax];
-    __shared__ uint32_t sv[kBigMax];
+    extern __shared__ __align__(16) uint64_t s_big[];   // [kBigMax] keys, [kBigMax] ids, warp sums
+    uint64_t *sk = s_big;
+    uint32_t *sv = reinterpret_cast<uint32_t *>(s_big + kBigMax);
+    uint32_t *s_warp = sv + kBigMax;
     const uint32_t nbig = min(big[0], big_cap);
     if (big[0] > big_cap && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(overflow, 1u);
+    constexpr uint32_t kPer = kBigMax / kBigThreads;   // 8 consecutive items per thread in the scan
     for (uint32_t qi = blockIdx.x; qi < nbig; qi += gridDim.x) {
         const uint32_t b = big[1 + qi];
         const uint32_t s = start[b], m = start[b + 1] - s;
@@ -388,13 +404,44 @@ k_bucket_sort_big(const uint64_t *__restrict__ kin, const uint32_t *__restrict__
             kout[s + i] = sk[i];
             vout[s + i] = sv[i];
         }
+        // cells: thread t owns items [t*kPer, t*kPer + kPer); head = first item or key change
+        uint32_t flags = 0, cnt = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < kPer; ++r) {
+            const uint32_t i = threadIdx.x * kPer + r;
+            const bool head = i < m && i > 0 && sk[i] != sk[i - 1];
+            flags |= (head ? 1u : 0u) << r;
+            cnt += head ? 1u : 0u;
+        }
+        uint32_t incl = cnt;                             // block inclusive scan of cnt
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((threadIdx.x & 31) >= (uint32_t)o) incl += y;
+        }
+        if ((threadIdx.x & 31) == 31) s_warp[threadIdx.x >> 5] = incl;
+        __syncthreads();
+        uint32_t woff = 0;
+        for (uint32_t w = 0; w < (threadIdx.x >> 5); ++w) woff += s_warp[w];
+        uint32_t run = woff + incl - cnt;
+#pragma unroll
+        for (uint32_t r = 0; r < kPer; ++r) {
+            const uint32_t i = threadIdx.x * kPer + r;
+            run += (flags >> r) & 1u;
+            if (i < m) local[s + i] = run;
+        }
+        if (threadIdx.x == blockDim.x - 1) cellcnt[b] = woff + incl + 1;   // heads after item 0, + 1
+        __syncthreads();
     }
 }
 }  // namespace
 
 // hist: per-prefix point counts (P + 1 entries, the last one 0), consumed (it becomes the cursor).
+// local[n]: cell index of each sorted item within its bucket; cellcnt[P+1]: cells per bucket (the
+// caller scans it into the prefix directory).
 void bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp, uint32_t n,
-                       uint64_t div, uint64_t P, uint32_t *hist, uint32_t *overflow, cudaStream_t s)
+                       uint64_t div, uint64_t P, uint32_t *hist, uint32_t *overflow, uint32_t *local,
+                       uint32_t *cellcnt, cudaStream_t s)
 {
     if (n == 0) return;
     const double inv = 1.0 / (double)div;
@@ -402,14 +449,18 @@ void bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint3
     const uint32_t big_cap = n / (kBucketMax + 1) + 1;
     Scratch<uint32_t> start((size_t)P + 1, s), big((size_t)big_cap + 1, s);
     SJ_CUDA(cudaMemsetAsync(big.p, 0, sizeof(uint32_t), s));
+    SJ_CUDA(cudaMemsetAsync(cellcnt + P, 0, sizeof(uint32_t), s));
     exclusive_scan_u32_dup(hist, start.p, hist, (uint64_t)P + 1, s);
     const uint32_t g = (n + 255) / 256;
     k_bucket_scatter<<<g, 256, 0, s>>>(keys, vals, n, div, inv, hist, keys_tmp, vals_tmp);
     SJ_LAUNCHED();
     k_bucket_sort<<<(uint32_t)((P + 255) / 256), 256, 0, s>>>(keys_tmp, vals_tmp, start.p, P, keys, vals, big.p,
-                                                               big_cap);
+                                                               big_cap, local, cellcnt);
     SJ_LAUNCHED();
-    k_bucket_sort_big<<<296, kBigThreads, 0, s>>>(keys_tmp, vals_tmp, start.p, big.p, big_cap, keys, vals, overflow);
+    constexpr size_t kBigSmem = kBigMax * (sizeof(uint64_t) + sizeof(uint32_t)) + sizeof(uint32_t) * (kBigThreads / 32);
+    SJ_CUDA(cudaFuncSetAttribute(k_bucket_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem));
+    k_bucket_sort_big<<<296, kBigThreads, kBigSmem, s>>>(keys_tmp, vals_tmp, start.p, big.p, big_cap, keys, vals,
+                                                         overflow, local, cellcnt);
     SJ_LAUNCHED();
 }
 

@@ -199,7 +199,8 @@ void free_index_impl(sj_index *idx);
 void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp,
                       uint32_t n, int key_bits, cudaStream_t s, bool *result_in_tmp);
 void bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp, uint32_t n,
-                       uint64_t div, uint64_t P, uint32_t *hist, uint32_t *overflow, cudaStream_t s);
+                       uint64_t div, uint64_t P, uint32_t *hist, uint32_t *overflow, uint32_t *local,
+                       uint32_t *cellcnt, cudaStream_t s);
 void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s);
 void exclusive_scan_u32_dup(const uint32_t *in, uint32_t *out, uint32_t *out2, uint64_t n, cudaStream_t s);
 void inclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s);
