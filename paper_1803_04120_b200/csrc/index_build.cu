@@ -618,171 +618,178 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
     } ev(o.device);
     ev.rec(0, s);
 
-    // ---- inputs on device
-    const double *pts = points;
-    Scratch<double> d_pts;
-    if (!o.points_on_device) {
-        d_pts.p = dalloc<double>((size_t)n * d, s);
-        d_pts.s = s;
-        SJ_CUDA(cudaMemcpyAsync(d_pts.p, points, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
-        pts = d_pts.p;
-    }
-    ev.rec(1, s);
-
-    // ---- a1: exact per-dimension min/max + finiteness (one kernel, integer atomics); one D2H copy
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device);
-    const uint32_t parts = (uint32_t)std::min<uint64_t>((n + kThreads - 1) / kThreads, (uint64_t)nsm * 4);
-    Scratch<unsigned long long> mm(2 * d + 1, s);       // [2d] = non-finite flag
-    k_minmax_init<<<1, 32, 0, s>>>(mm.p, d, reinterpret_cast<uint32_t *>(mm.p + 2 * d));
-    SJ_LAUNCHED();
-    DevIndex ix{};
-    ix.d = d;
-    ix.n = N;
-    BuildArgs ba;
-    ba.pts = pts;
-    ba.n = N;
-    ba.mm = mm.p;
-    ba.nonfinite = reinterpret_cast<uint32_t *>(mm.p + 2 * d);
-    launch(d, 0, dim3(parts), s, ix, ba);
-    unsigned long long h_ord[2 * SJ_MAX_DIM + 1];
-    SJ_CUDA(cudaMemcpyAsync(h_ord, mm.p, sizeof(unsigned long long) * (2 * d + 1), cudaMemcpyDeviceToHost, s));
-    SJ_CUDA(cudaStreamSynchronize(s));
-    ev.rec(2, s);
-    tr.mark("minmax (synced)");
-    if ((uint32_t)h_ord[2 * d]) fail(SJ_ERR_NONFINITE, "a coordinate is NaN or infinite");
-    double h_mm[2 * SJ_MAX_DIM];
-    for (int t = 0; t < 2 * d; ++t) {
-        const unsigned long long k = h_ord[t];
-        const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
-        std::memcpy(&h_mm[t], &u, sizeof(double));
-    }
-
-    sj_index_view v{};
-    v.d = d;
-    v.device = o.device;
-    v.n = n;
-    v.eps = eps;
-    {
-        volatile double e2 = eps * eps;
-        v.eps2 = e2;
-    }
-    for (int j = 0; j < d; ++j) v.mins[j] = h_mm[j];
-    host_geometry(d, eps, h_mm, h_mm + d, v);
-
-    ix.w = v.w;
-    ix.eps2 = v.eps2;
-    for (int j = 0; j < d; ++j) {
-        ix.mins[j] = v.mins[j];
-        ix.cpd[j] = v.cpd[j];
-        ix.strides[j] = v.strides[j];
-    }
-    // masks: one bitmap, |g_j| bits per dimension, only when <= 2^30 bits (they never change S)
-    uint64_t mask_total = 0;
-    bool want_masks = o.build_masks != 0;
-    for (int j = 0; j < d; ++j) {
-        v.mask_offsets[j] = mask_total;
-        mask_total += v.cpd[j];
-        if (mask_total > (1ull << 30)) want_masks = false;
-    }
-    v.mask_offsets[d] = mask_total;
-    for (int j = 0; j <= d; ++j) ix.mask_off[j] = v.mask_offsets[j];
-    // packed per-cell coordinates (c_j at bit cshift[j]) when the widths fit 64 bits
-    bool pack_fits = true;
-    {
-        uint32_t sh = 0;
-        for (int j = 0; j < d; ++j) {
-            uint32_t b = 0;
-            while (b < 64 && ((v.cpd[j] - 1) >> b)) ++b;
-            ix.cbits[j] = b;
-            ix.cshift[j] = sh;
-            sh += b;
-        }
-        pack_fits = sh <= 64;
-    }
-    const DirPlan dp = plan_dir(v);
-    apply_dir_geometry(ix, v, dp);
-    // a3 strategy: sparse keys (<= 2 points per top-k prefix on average, P <= 2^22 so the bucket
-    // arrays stay L2-sized; measured slower than LSD at P = 11.4 M) -> prefix buckets + per-bucket
-    // sort; otherwise stable LSD radix sort
-    const bool use_bucket = allow_bucket && dp.k >= 1 && (double)n <= 2.0 * (double)dp.P && dp.P <= (1ull << 22) &&
-                            v.key_bits <= 62;
-
     sj_index *idx = new sj_index();
     idx->device = o.device;
     auto own = [&](void *p) { idx->bufs[idx->nbufs++] = p; return p; };
     uint32_t h_aux[4] = {0, 0, 0, 0};
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device);
     try {
+        // ---- inputs on device
+        const double *pts = points;
+        Scratch<double> d_pts;
+        if (!o.points_on_device) {
+            d_pts.p = dalloc<double>((size_t)n * d, s);
+            d_pts.s = s;
+            SJ_CUDA(cudaMemcpyAsync(d_pts.p, points, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
+            pts = d_pts.p;
+        }
+        ev.rec(1, s);
+
+        // ---- a1: exact per-dimension min/max + finiteness (one kernel, integer atomics); one D2H copy
+        const uint32_t parts = (uint32_t)std::min<uint64_t>((n + kThreads - 1) / kThreads, (uint64_t)nsm * 4);
+        Scratch<unsigned long long> mm(2 * d + 1, s);       // [2d] = non-finite flag
+        k_minmax_init<<<1, 32, 0, s>>>(mm.p, d, reinterpret_cast<uint32_t *>(mm.p + 2 * d));
+        SJ_LAUNCHED();
+        DevIndex ix{};
+        ix.d = d;
+        ix.n = N;
+        BuildArgs ba;
+        ba.pts = pts;
+        ba.n = N;
+        ba.mm = mm.p;
+        ba.nonfinite = reinterpret_cast<uint32_t *>(mm.p + 2 * d);
+        launch(d, 0, dim3(parts), s, ix, ba);
+        unsigned long long h_ord[2 * SJ_MAX_DIM + 1];
+        SJ_CUDA(cudaMemcpyAsync(h_ord, mm.p, sizeof(unsigned long long) * (2 * d + 1), cudaMemcpyDeviceToHost, s));
+
+        // ---- while the min/max pass runs: every N-sized array in two arenas (one owned by the
+        // index: A, pcell, B, G, X, cell coordinates/masks, aux; one scratch: keys, sort buffers)
+        auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+        const size_t b_A = al(4 * n), b_pc = al(4 * n), b_B = al(8 * n), b_G = al(4 * (n + 1)), b_X = al(8 * n * d),
+                     b_cc = al(8 * n), b_cm = al(4 * n), b_aux = al(16);
+        char *arena = static_cast<char *>(own(dev_alloc(b_A + b_pc + b_B + b_G + b_X + b_cc + b_cm + b_aux, s)));
+        uint32_t *A = reinterpret_cast<uint32_t *>(arena);
+        uint32_t *pcell = reinterpret_cast<uint32_t *>(arena + b_A);
+        uint64_t *B = reinterpret_cast<uint64_t *>(arena + b_A + b_pc);
+        uint32_t *G = reinterpret_cast<uint32_t *>(arena + b_A + b_pc + b_B);
+        double *X = reinterpret_cast<double *>(arena + b_A + b_pc + b_B + b_G);
+        uint64_t *ccoord = reinterpret_cast<uint64_t *>(arena + b_A + b_pc + b_B + b_G + b_X);
+        uint32_t *cmask = reinterpret_cast<uint32_t *>(arena + b_A + b_pc + b_B + b_G + b_X + b_cc);
         // aux: [0] = |G|, [1] = #dense tasks, [2] = #populous cells, [3] = bucket-sort overflow
-        uint32_t *aux = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * 4, s)));
+        uint32_t *aux = reinterpret_cast<uint32_t *>(arena + b_A + b_pc + b_B + b_G + b_X + b_cc + b_cm);
+        const size_t s_k = al(8 * n), s_i = al(4 * n);
+        Scratch<char> scratch(2 * s_k + 2 * s_i, s);
+        uint64_t *keys = reinterpret_cast<uint64_t *>(scratch.p);
+        uint64_t *keys_tmp = reinterpret_cast<uint64_t *>(scratch.p + s_k);
+        uint32_t *ids_tmp = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k);
+        uint32_t *flags = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k + s_i);
         SJ_CUDA(cudaMemsetAsync(aux, 0, sizeof(uint32_t) * 4, s));
+
+        SJ_CUDA(cudaStreamSynchronize(s));
+        ev.rec(2, s);
+        tr.mark("minmax (synced)");
+        if ((uint32_t)h_ord[2 * d]) fail(SJ_ERR_NONFINITE, "a coordinate is NaN or infinite");
+        double h_mm[2 * SJ_MAX_DIM];
+        for (int t = 0; t < 2 * d; ++t) {
+            const unsigned long long k = h_ord[t];
+            const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+            std::memcpy(&h_mm[t], &u, sizeof(double));
+        }
+
+        sj_index_view v{};
+        v.d = d;
+        v.device = o.device;
+        v.n = n;
+        v.eps = eps;
+        {
+            volatile double e2 = eps * eps;
+            v.eps2 = e2;
+        }
+        for (int j = 0; j < d; ++j) v.mins[j] = h_mm[j];
+        host_geometry(d, eps, h_mm, h_mm + d, v);
+
+        ix.w = v.w;
+        ix.eps2 = v.eps2;
+        for (int j = 0; j < d; ++j) {
+            ix.mins[j] = v.mins[j];
+            ix.cpd[j] = v.cpd[j];
+            ix.strides[j] = v.strides[j];
+        }
+        // masks: one bitmap, |g_j| bits per dimension, only when <= 2^30 bits (they never change S)
+        uint64_t mask_total = 0;
+        bool want_masks = o.build_masks != 0;
+        for (int j = 0; j < d; ++j) {
+            v.mask_offsets[j] = mask_total;
+            mask_total += v.cpd[j];
+            if (mask_total > (1ull << 30)) want_masks = false;
+        }
+        v.mask_offsets[d] = mask_total;
+        for (int j = 0; j <= d; ++j) ix.mask_off[j] = v.mask_offsets[j];
+        // packed per-cell coordinates (c_j at bit cshift[j]) when the widths fit 64 bits
+        bool pack_fits = true;
+        {
+            uint32_t sh = 0;
+            for (int j = 0; j < d; ++j) {
+                uint32_t b = 0;
+                while (b < 64 && ((v.cpd[j] - 1) >> b)) ++b;
+                ix.cbits[j] = b;
+                ix.cshift[j] = sh;
+                sh += b;
+            }
+            pack_fits = sh <= 64;
+        }
+        if (!pack_fits) ccoord = nullptr, cmask = nullptr;
+        const DirPlan dp = plan_dir(v);
+        apply_dir_geometry(ix, v, dp);
+        // a3 strategy: sparse keys (<= 2 points per top-k prefix on average, P <= 2^22 so the
+        // bucket arrays stay L2-sized; measured slower than LSD at P = 11.4 M) -> prefix buckets +
+        // per-bucket sort; otherwise stable LSD radix sort
+        const bool use_bucket = allow_bucket && dp.k >= 1 && (double)n <= 2.0 * (double)dp.P &&
+                                dp.P <= (1ull << 22) && v.key_bits <= 62;
+
+        // ---- geometry-sized arrays: masks, bucket histogram (bucket path), directory, bitmaps
         uint32_t *masks = nullptr;
         const size_t mask_bytes = 4 * ((mask_total + 31) / 32);
-        if (want_masks) {
-            masks = static_cast<uint32_t *>(own(dev_alloc(mask_bytes, s)));
-            SJ_CUDA(cudaMemsetAsync(masks, 0, mask_bytes, s));
-        }
-        Scratch<uint64_t> keys(n, s), keys_tmp(n, s);
-        uint32_t *A = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
-        Scratch<uint32_t> ids_tmp(n, s);
+        if (want_masks) masks = static_cast<uint32_t *>(own(dev_alloc(mask_bytes, s)));
         Scratch<uint32_t> bhist;
         if (use_bucket) {
             bhist.p = dalloc<uint32_t>((size_t)dp.P + 1, s);
             bhist.s = s;
-            SJ_CUDA(cudaMemsetAsync(bhist.p, 0, sizeof(uint32_t) * ((size_t)dp.P + 1), s));
         }
+        if (masks) SJ_CUDA(cudaMemsetAsync(masks, 0, mask_bytes, s));
+        if (use_bucket) SJ_CUDA(cudaMemsetAsync(bhist.p, 0, sizeof(uint32_t) * ((size_t)dp.P + 1), s));
         const dim3 grid((unsigned)((n + kThreads - 1) / kThreads));
 
         // ---- a2: keys (+ masks, + prefix histogram of the bucket sort)
-        ba.keys = keys.p;
+        ba.keys = keys;
         ba.ids = A;
         ba.masks = masks;
         ba.mask_words = (uint32_t)((mask_total + 31) / 32);
         ba.bhist = bhist.p;
         launch(d, 1, grid, s, ix, ba);
         ev.rec(3, s);
-
-        // ---- a3: sort of (key, id) into (key, id)-ascending order (= stable sort by key, R14)
-        uint32_t *pcell = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
         idx->view = v;
         alloc_dir(idx, dp, s);
         uint32_t *dir = const_cast<uint32_t *>(idx->dev.dir);
+
+        // ---- a3: sort of (key, id) into (key, id)-ascending order (= stable sort by key, R14)
         bool in_tmp = false;
         Scratch<uint32_t> dirhist;
         if (use_bucket) {
             // the bucket sort also numbers each bucket's cells: pcell = cell index within the
             // bucket, bhist = cells per bucket, whose exclusive scan IS the prefix directory
-            bucket_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, dp.div, dp.P, bhist.p, aux + 3, pcell, bhist.p, s);
+            bucket_sort_pairs(keys, A, keys_tmp, ids_tmp, N, dp.div, dp.P, bhist.p, aux + 3, pcell, bhist.p, s);
             exclusive_scan_u32(bhist.p, dir, (uint64_t)dp.P + 1, s);
             SJ_CUDA(cudaMemcpyAsync(aux, dir + dp.P, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
         } else {
-            radix_sort_pairs(keys.p, A, keys_tmp.p, ids_tmp.p, N, v.key_bits, s, &in_tmp);
+            radix_sort_pairs(keys, A, keys_tmp, ids_tmp, N, v.key_bits, s, &in_tmp);
         }
-        const uint64_t *skeys = in_tmp ? keys_tmp.p : keys.p;
-        if (in_tmp) SJ_CUDA(cudaMemcpyAsync(A, ids_tmp.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
+        const uint64_t *skeys = in_tmp ? keys_tmp : keys;
+        if (in_tmp) SJ_CUDA(cudaMemcpyAsync(A, ids_tmp, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
         ev.rec(4, s);
 
         // ---- a4: cell numbering (LSD path: heads + scan), compaction, SoA gather, directory
         // histogram (LSD path), occupancy bits.  B and G are sized for the upper bound N cells so no
         // host round trip is needed here; |G| is read back by the single sync of finish_aux.
         if (!use_bucket) {
-            Scratch<uint32_t> flags(n, s);
-            k_heads<<<grid, kThreads, 0, s>>>(skeys, N, flags.p);
+            k_heads<<<grid, kThreads, 0, s>>>(skeys, N, flags);
             SJ_LAUNCHED();
-            inclusive_scan_u32(flags.p, pcell, n, s);
+            inclusive_scan_u32(flags, pcell, n, s);
             SJ_CUDA(cudaMemcpyAsync(aux, pcell + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
             dirhist.p = dalloc<uint32_t>((size_t)dp.P + 1, s);
             dirhist.s = s;
             SJ_CUDA(cudaMemsetAsync(dirhist.p, 0, sizeof(uint32_t) * ((size_t)dp.P + 1), s));
-        }
-        uint64_t *B = static_cast<uint64_t *>(own(dev_alloc(sizeof(uint64_t) * n, s)));
-        uint32_t *G = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * ((size_t)n + 1), s)));
-        double *X = static_cast<double *>(own(dev_alloc(sizeof(double) * n * d, s)));
-        uint64_t *ccoord = nullptr;
-        uint32_t *cmask = nullptr;
-        if (pack_fits) {
-            ccoord = static_cast<uint64_t *>(own(dev_alloc(sizeof(uint64_t) * n, s)));
-            cmask = static_cast<uint32_t *>(own(dev_alloc(sizeof(uint32_t) * n, s)));
         }
         ix.masks = masks;
         ix.occ = idx->dev.occ;
@@ -823,7 +830,6 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         idx->view = v;
         idx->dev = ix;
         finish_aux(idx, s, aux, dp, dirhist.p, false, h_aux);   // the build's late host sync
-        v.n_cells = idx->view.n_cells;
         ev.rec(6, s);
         tr.mark("compact+dir+dense (synced)");
         for (int i = 0; i < 7; ++i) {

@@ -293,6 +293,17 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             ja.nsamples = (uint32_t)sm.ns;
             ja.qbucket = dbk;
             ja.group = (uint32_t)group;
+            // a small sample is one partial wave of long per-query chains: spread each query over
+            // more lanes (the counts do not depend on the lane split) until the GPU is covered
+#ifndef SJ_EST_LANES_MAX
+#define SJ_EST_LANES_MAX 3
+#endif
+            if (o.lanes_per_query == 0) {
+                int nsm = 148;
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, idx->device);
+                while (ja.lanes_log2 < SJ_EST_LANES_MAX && (sm.ns << (ja.lanes_log2 + 1)) <= (uint64_t)nsm * 1024)
+                    ++ja.lanes_log2;
+            }
             SJ_CUDA(cudaEventRecord(res->est_ev[0], s0));
             launch_refine<kCountQuery>(ix, ja, o.unicomp != 0, (uint32_t)sm.ns, s0);
             SJ_CUDA(cudaEventRecord(res->est_ev[1], s0));
