@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -106,6 +107,19 @@ void event_put(int dev, cudaEvent_t e)
     g_ev_free.emplace_back(dev, e);
 }
 
+void set_max_dyn_smem(const void *func, int bytes)
+{
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, int> done;   // (kernel, device) -> bytes set
+    int dev = 0;
+    SJ_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto &b = done[{func, dev}];
+    if (b >= bytes) return;
+    SJ_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    b = bytes;
+}
+
 static float elapsed(cudaEvent_t a, cudaEvent_t b)
 {
     float t = 0;
@@ -173,11 +187,37 @@ static double now_us()
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+static int trace_level()
+{
+    static const int lvl = [] { const char *e = std::getenv("SJ_TRACE"); return (e && *e) ? std::atoi(e) : 0; }();
+    return lvl;
+}
+
 HostTrace::HostTrace(const char *w) : what(w)
 {
-    static const bool enabled = [] { const char *e = std::getenv("SJ_TRACE"); return e && *e && *e != '0'; }();
-    on = enabled;
+    on = trace_level() > 0;
     t0 = last = on ? now_us() : 0.0;
+}
+
+void HostTrace::dev(const char *stage, cudaStream_t s)
+{
+    if (trace_level() < 2) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    dev_ev.emplace_back(stage, e);
+}
+
+HostTrace::~HostTrace()
+{
+    if (dev_ev.empty()) return;
+    cudaEventSynchronize(dev_ev.back().second);
+    for (size_t i = 1; i < dev_ev.size(); ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, dev_ev[i - 1].second, dev_ev[i].second);
+        std::fprintf(stderr, "[sj-dev]   %-10s %-28s +%8.1f us (GPU)\n", what, dev_ev[i].first, 1000.0 * ms);
+    }
+    for (auto &pr : dev_ev) cudaEventDestroy(pr.second);
 }
 
 void HostTrace::mark(const char *stage)

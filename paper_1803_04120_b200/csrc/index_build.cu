@@ -355,8 +355,11 @@ void host_geometry(int d, double eps, const double *mins, const double *maxs, sj
 // per point, so the index stays O(|D|)); every B lookup of the refine is bounded to
 // one prefix's range.  The same k/P drive the prefix-bucket sort.  The occupancy bitmap over the
 // top-(k+1) prefixes is planned when it costs <= 8 B per point and filters (the +-1 window of 3
-// sub-prefixes is expected occupied with probability ~3N/P_{k+1} < 0.25: 6-D eps=1: 0.06; eps=8:
+// sub-prefixes is expected occupied with probability ~3N/P_{k+1} < SJ_OCC_MAXFILL: 6-D eps=1: 0.06; eps=8:
 // 0.53 -> not built).
+#ifndef SJ_OCC_MAXFILL
+#define SJ_OCC_MAXFILL 0.5     // 6-D eps=4: 0.35 -> built (join 2.59 -> 1.72 ms); eps=8: 0.53 -> not (built: slower)
+#endif
 struct DirPlan {
     int k = 0;
     uint64_t P = 1;
@@ -387,7 +390,7 @@ DirPlan plan_dir(const sj_index_view &v)
     if (dp.k >= 1 && dp.k < d) {
         const unsigned __int128 P1 = P * v.cpd[d - dp.k - 1];
         if (P1 <= (unsigned __int128)64 * std::max<uint64_t>(n, 1ull << 16) &&
-            3.0 * (double)n < 0.25 * (double)(uint64_t)P1) {
+            3.0 * (double)n < SJ_OCC_MAXFILL * (double)(uint64_t)P1) {
             dp.occ = true;
             dp.occ_cpd = v.cpd[d - dp.k - 1];
             dp.occ_div = dp.div / dp.occ_cpd;
@@ -617,6 +620,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         void rec(int i, cudaStream_t st) { SJ_CUDA(cudaEventRecord(e[i], st)); }
     } ev(o.device);
     ev.rec(0, s);
+    tr.dev("start", s);
 
     sj_index *idx = new sj_index();
     idx->device = o.device;
@@ -650,6 +654,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ba.mm = mm.p;
         ba.nonfinite = reinterpret_cast<uint32_t *>(mm.p + 2 * d);
         launch(d, 0, dim3(parts), s, ix, ba);
+        tr.dev("minmax", s);
         unsigned long long h_ord[2 * SJ_MAX_DIM + 1];
         SJ_CUDA(cudaMemcpyAsync(h_ord, mm.p, sizeof(unsigned long long) * (2 * d + 1), cudaMemcpyDeviceToHost, s));
 
@@ -675,7 +680,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         uint32_t *ids_tmp = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k);
         uint32_t *flags = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k + s_i);
         SJ_CUDA(cudaMemsetAsync(aux, 0, sizeof(uint32_t) * 4, s));
-
+        tr.mark("minmax + arenas enqueued");
         SJ_CUDA(cudaStreamSynchronize(s));
         ev.rec(2, s);
         tr.mark("minmax (synced)");
@@ -750,6 +755,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         if (masks) SJ_CUDA(cudaMemsetAsync(masks, 0, mask_bytes, s));
         if (use_bucket) SJ_CUDA(cudaMemsetAsync(bhist.p, 0, sizeof(uint32_t) * ((size_t)dp.P + 1), s));
         const dim3 grid((unsigned)((n + kThreads - 1) / kThreads));
+        tr.mark("geometry + allocs");
 
         // ---- a2: keys (+ masks, + prefix histogram of the bucket sort)
         ba.keys = keys;
@@ -757,8 +763,11 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ba.masks = masks;
         ba.mask_words = (uint32_t)((mask_total + 31) / 32);
         ba.bhist = bhist.p;
+        tr.dev("geometry gap + memsets", s);
         launch(d, 1, grid, s, ix, ba);
+        tr.dev("keys", s);
         ev.rec(3, s);
+        tr.mark("keys launched");
         idx->view = v;
         alloc_dir(idx, dp, s);
         uint32_t *dir = const_cast<uint32_t *>(idx->dev.dir);
@@ -771,6 +780,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
             // bucket, bhist = cells per bucket, whose exclusive scan IS the prefix directory
             bucket_sort_pairs(keys, A, keys_tmp, ids_tmp, N, dp.div, dp.P, bhist.p, aux + 3, pcell, bhist.p, s);
             exclusive_scan_u32(bhist.p, dir, (uint64_t)dp.P + 1, s);
+            tr.dev("dir scan", s);
             SJ_CUDA(cudaMemcpyAsync(aux, dir + dp.P, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
         } else {
             radix_sort_pairs(keys, A, keys_tmp, ids_tmp, N, v.key_bits, s, &in_tmp);
@@ -778,6 +788,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         const uint64_t *skeys = in_tmp ? keys_tmp : keys;
         if (in_tmp) SJ_CUDA(cudaMemcpyAsync(A, ids_tmp, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
         ev.rec(4, s);
+        tr.mark("sort enqueued");
 
         // ---- a4: cell numbering (LSD path: heads + scan), compaction, SoA gather, directory
         // histogram (LSD path), occupancy bits.  B and G are sized for the upper bound N cells so no
@@ -808,10 +819,13 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ba.bucket_cells = use_bucket;
         ba.dir_inv = 1.0 / (double)dp.div;
         ba.occ = const_cast<uint32_t *>(ix.occ);
+        tr.dev("pre-compact", s);
         launch(d, 2, grid, s, ix, ba);
+        tr.dev("compact", s);
         ix.ccoord = ccoord;
         ix.cmask = cmask;
         ev.rec(5, s);
+        tr.mark("compact enqueued");
 
         v.n_cells = n;            // provisional upper bound until finish_aux() reads |G|
         v.B = B;
@@ -831,6 +845,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         idx->dev = ix;
         finish_aux(idx, s, aux, dp, dirhist.p, false, h_aux);   // the build's late host sync
         ev.rec(6, s);
+        tr.dev("finish", s);
         tr.mark("compact+dir+dense (synced)");
         for (int i = 0; i < 7; ++i) {
             idx->tev[i] = ev.e[i];

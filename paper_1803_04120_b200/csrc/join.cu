@@ -31,12 +31,10 @@ void launch_dense(const DevIndex &ix, const JoinArgs &ja, bool unicomp, cudaStre
 #define SJ_DENSE_CASE(DD)                                                                              \
     case DD:                                                                                           \
         if (unicomp) {                                                                                 \
-            SJ_CUDA(cudaFuncSetAttribute(k_refine_dense<DD, true>,                                     \
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
+            set_max_dyn_smem(reinterpret_cast<const void *>(k_refine_dense<DD, true>), (int)smem);     \
             k_refine_dense<DD, true><<<grid, block, smem, s>>>(ix, ja);                               \
         } else {                                                                                       \
-            SJ_CUDA(cudaFuncSetAttribute(k_refine_dense<DD, false>,                                    \
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
+            set_max_dyn_smem(reinterpret_cast<const void *>(k_refine_dense<DD, false>), (int)smem);     \
             k_refine_dense<DD, false><<<grid, block, smem, s>>>(ix, ja);                              \
         }                                                                                              \
         break;
@@ -304,8 +302,10 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 while (ja.lanes_log2 < SJ_EST_LANES_MAX && (sm.ns << (ja.lanes_log2 + 1)) <= (uint64_t)nsm * 1024)
                     ++ja.lanes_log2;
             }
+            tr.dev("start", s0);
             SJ_CUDA(cudaEventRecord(res->est_ev[0], s0));
             launch_refine<kCountQuery>(ix, ja, o.unicomp != 0, (uint32_t)sm.ns, s0);
+            tr.dev("estimate", s0);
             SJ_CUDA(cudaEventRecord(res->est_ev[1], s0));
             SJ_CUDA(cudaMemcpyAsync(hbk, dbk, nbk * 8, cudaMemcpyDeviceToHost, s0));
             SJ_CUDA(cudaStreamSynchronize(s0));
@@ -390,8 +390,10 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 SJ_CUDA(cudaEventRecord(cx.events[2 + i], cx.streams[i]));
                 SJ_CUDA(cudaStreamWaitEvent(s0, cx.events[2 + i], 0));
             }
+            tr.dev("gap + batches (stream 0 joined)", s0);
             SJ_CUDA(cudaMemcpyAsync(hwork, work, kWorkBytes + (own_slots ? sizeof(Slot) * nb : 0),
                                     cudaMemcpyDeviceToHost, s0));
+            tr.dev("counter copy", s0);
             for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
             tr.mark("batches done (synced)");
             work_read = true;

@@ -244,7 +244,7 @@ void radix_pass(const uint64_t *ka, const uint32_t *va, uint64_t *kb, uint32_t *
     SJ_LAUNCHED();
     exclusive_scan_u32(counts, offs, (uint64_t)R * nt, s);
     const size_t smem = sizeof(uint32_t) * kSortWarps * R;
-    SJ_CUDA(cudaFuncSetAttribute(k_radix_scatter<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_max_dyn_smem(reinterpret_cast<const void *>(k_radix_scatter<BITS>), (int)smem);
     k_radix_scatter<BITS><<<nt, kSortThreads, smem, s>>>(ka, va, kb, vb, n, shift, offs, nt);
     SJ_LAUNCHED();
 }
@@ -444,24 +444,30 @@ void bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint3
                        uint32_t *cellcnt, cudaStream_t s)
 {
     if (n == 0) return;
+    HostTrace tr("bsort");
     const double inv = 1.0 / (double)div;
     // at most n / (kBucketMax + 1) buckets are big
     const uint32_t big_cap = n / (kBucketMax + 1) + 1;
     Scratch<uint32_t> start((size_t)P + 1, s), big((size_t)big_cap + 1, s);
     SJ_CUDA(cudaMemsetAsync(big.p, 0, sizeof(uint32_t), s));
     SJ_CUDA(cudaMemsetAsync(cellcnt + P, 0, sizeof(uint32_t), s));
+    tr.dev("start", s);
     exclusive_scan_u32_dup(hist, start.p, hist, (uint64_t)P + 1, s);
+    tr.dev("bucket scan", s);
     const uint32_t g = (n + 255) / 256;
     k_bucket_scatter<<<g, 256, 0, s>>>(keys, vals, n, div, inv, hist, keys_tmp, vals_tmp);
     SJ_LAUNCHED();
+    tr.dev("scatter", s);
     k_bucket_sort<<<(uint32_t)((P + 255) / 256), 256, 0, s>>>(keys_tmp, vals_tmp, start.p, P, keys, vals, big.p,
                                                                big_cap, local, cellcnt);
     SJ_LAUNCHED();
+    tr.dev("bucket sort", s);
     constexpr size_t kBigSmem = kBigMax * (sizeof(uint64_t) + sizeof(uint32_t)) + sizeof(uint32_t) * (kBigThreads / 32);
-    SJ_CUDA(cudaFuncSetAttribute(k_bucket_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem));
+    set_max_dyn_smem(reinterpret_cast<const void *>(k_bucket_sort_big), (int)kBigSmem);
     k_bucket_sort_big<<<296, kBigThreads, kBigSmem, s>>>(keys_tmp, vals_tmp, start.p, big.p, big_cap, keys, vals,
                                                          overflow, local, cellcnt);
     SJ_LAUNCHED();
+    tr.dev("big buckets", s);
 }
 
 }  // namespace sj

@@ -34,8 +34,12 @@ struct HostTrace {
     bool on;
     const char *what;
     double t0, last;
+    // device timeline (SJ_TRACE=2): an event per dev() call; printed as GPU-side deltas at exit
+    std::vector<std::pair<const char *, cudaEvent_t>> dev_ev;
     explicit HostTrace(const char *w);
+    ~HostTrace();
     void mark(const char *stage);
+    void dev(const char *stage, cudaStream_t s);
 };
 
 // ---------------------------------------------------------------- device memory
@@ -173,6 +177,9 @@ struct DevCtx {
     size_t slot_bytes = 0;
 };
 DevCtx *acquire_ctx(int dev, int nstreams, int nevents, size_t slot_bytes);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the call costs
+// tens of microseconds of host time, on the build's / join's critical path if repeated.
+void set_max_dyn_smem(const void *func, int bytes);
 // pooled timing events (cudaEventCreate / elapsed-time queries stay off the critical path)
 cudaEvent_t event_get(int dev);
 void event_put(int dev, cudaEvent_t e);

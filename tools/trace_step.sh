@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
-SJ_TRACE=1 python - <<'PY' 2>&1 | tail -30
+SJ_TRACE=${SJ_TRACE:-1} python - <<'PY' 2>&1 | tail -30
 import os, sys, time
 sys.path.insert(0, '.')
 import torch, datagen, paper_1803_04120_b200 as sj
