@@ -15,6 +15,7 @@
 //   k_compact_gather                : B, G starts, SoA coordinates X[j][k] = D[A[k]][j] (a4)
 //   k_dir_hist + exclusive scan     : prefix directory bounding every B search (a4)
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 
 #include "sj_common.cuh"
@@ -84,24 +85,119 @@ __global__ void k_minmax_init(unsigned long long *mm, int d, uint32_t *nonfinite
     if (t == 0) *nonfinite = 0;
 }
 
+// Geometry computed ON THE DEVICE from the min/max (same IEEE operations as host_geometry, so the
+// host's copy -- read while k_keys already runs -- must agree bit for bit): cell width, |g_j|,
+// strides, key bits, the prefix-directory plan (k, P, pstride) and the sort strategy.  This takes
+// the host round trip between the min/max pass and the key pass off the GPU's critical path.
+struct DevGeom {
+    double w;
+    double mins[SJ_MAX_DIM], maxs[SJ_MAX_DIM];
+    uint64_t cpd[SJ_MAX_DIM], strides[SJ_MAX_DIM], pstride[SJ_MAX_DIM];
+    uint64_t mask_off[SJ_MAX_DIM + 1];
+    uint64_t P, div;
+    int key_bits, k, use_bucket, masks_on;
+    int status;                  // 0 ok, 1 non-finite coordinate, 2 key overflow
+};
+
+__device__ __forceinline__ double ord_to_double(unsigned long long k)
+{
+    const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double((long long)u);
+}
+
+constexpr int kSmemMaskWords = 2048;   // 64 K bits, 8 KB of shared memory
+
+__global__ void k_geometry(const unsigned long long *__restrict__ mm, int d, double eps, uint32_t n, int allow_bucket,
+                           int want_masks, DevGeom *__restrict__ g)
+{
+    if (threadIdx.x != 0) return;
+    DevGeom G{};
+    if ((uint32_t)mm[2 * d]) { G.status = 1; *g = G; return; }
+    double R = 0.0, ranges[SJ_MAX_DIM];
+    for (int j = 0; j < d; ++j) {
+        const double mn = ord_to_double(mm[j]), mx = ord_to_double(mm[d + j]);
+        G.mins[j] = mn;
+        G.maxs[j] = mx;
+        ranges[j] = __dsub_rn(mx, mn);
+        if (ranges[j] > R) R = ranges[j];
+    }
+    const double er = __dadd_rn(eps, R);
+    G.w = __dadd_rn(eps, __dmul_rn(er, 0x1p-44));       // = eps + ldexp(er, -44) (exact scaling)
+    unsigned __int128 prod = 1;
+    for (int j = 0; j < d; ++j) {
+        const double t = floor(__ddiv_rn(ranges[j], G.w));
+        if (!(t < 9.0e18)) { G.status = 2; *g = G; return; }
+        G.cpd[j] = 3ull + (uint64_t)t;
+        prod *= G.cpd[j];
+        if (prod >> 64) { G.status = 2; *g = G; return; }
+    }
+    G.strides[0] = 1;
+    for (int j = 1; j < d; ++j) G.strides[j] = G.strides[j - 1] * G.cpd[j - 1];
+    unsigned __int128 maxkey = prod - 1;
+    int bits = 0;
+    while (maxkey > 0) { ++bits; maxkey >>= 1; }
+    G.key_bits = bits;
+    // directory plan (plan_dir): largest k with prod_{top k} |g_j| <= max(4N, 2^16)
+    const uint64_t cap = max((uint64_t)4 * n, (uint64_t)1 << 16);
+    unsigned __int128 P = 1;
+    for (int kk = 1; kk <= d; ++kk) {
+        const unsigned __int128 Q = P * G.cpd[d - kk];
+        if (Q > cap) break;
+        P = Q;
+        G.k = kk;
+    }
+    G.P = (uint64_t)P;
+    G.div = 1;
+    for (int j = 0; j < d - G.k; ++j) G.div *= G.cpd[j];
+    for (int j = 0; j < d; ++j) G.pstride[j] = (j >= d - G.k) ? G.strides[j] / G.div : 0;
+    G.use_bucket = allow_bucket && G.k >= 1 && (double)n <= 2.0 * (double)G.P && G.P <= (1ull << 22) &&
+                   G.key_bits <= 62;
+    uint64_t mt = 0;
+    for (int j = 0; j < d; ++j) { G.mask_off[j] = mt; mt += G.cpd[j]; }
+    G.mask_off[d] = mt;
+    G.masks_on = want_masks && mt <= 32ull * kSmemMaskWords;
+    *g = G;
+}
+
+// zero bhist[0, P] (P known on the device only)
+__global__ void __launch_bounds__(kThreads)
+k_zero_prefix_hist(uint32_t *__restrict__ h, const DevGeom *__restrict__ g)
+{
+    if (!g->use_bucket) return;
+    const uint64_t P = g->P;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= P; i += (uint64_t)gridDim.x * blockDim.x)
+        h[i] = 0;
+}
+
 // Cell coordinate c_j = 1 + floor(fl(fl(x_j - min_j) / w))  (reading R7), linear id with
 // dimension 1 fastest (R8): key = sum_j c_j * stride_j (exact: < prod |g_j| < 2^64).
-// Masks M_j as one bitmap over all dimensions (bit mask_off[j] + c): when it is
-// small (<= kSmemMaskWords words) each CTA ORs into a shared copy and flushes only the non-zero
-// words, so the few hot words are not hammered by every point; otherwise global atomicOr.
+// Masks M_j as one bitmap over all dimensions (bit mask_off[j] + c): each CTA ORs
+// into a shared copy and flushes only the non-zero words, so the few hot words are not hammered by
+// every point (masks larger than kSmemMaskWords words: k_masks_global after the geometry sync).
 // bhist (prefix-bucket sort only): points per top-k prefix sum_j c_j * pstride_j, fused here so
-// the sort needs no histogram pass of its own.
-constexpr int kSmemMaskWords = 2048;   // 64 K bits, 8 KB of shared memory
+// the sort needs no histogram pass of its own.  Geometry from the device (k_geometry).
 template <int D>
 __global__ void __launch_bounds__(kThreads)
-k_keys(const double *__restrict__ pts, uint32_t n, DevIndex ix, uint64_t *__restrict__ keys,
-       uint32_t *__restrict__ ids, uint32_t *__restrict__ masks, uint32_t mask_words, uint32_t *__restrict__ bhist)
+k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g, uint64_t *__restrict__ keys,
+       uint32_t *__restrict__ ids, uint32_t *__restrict__ masks, uint32_t *__restrict__ bhist)
 {
-    extern __shared__ uint32_t s_mask[];
-    const bool smem_masks = masks && mask_words <= (uint32_t)kSmemMaskWords;
-    if (smem_masks) {
+    __shared__ uint32_t s_mask[kSmemMaskWords];
+    if (g->status) return;
+    const bool use_masks = g->masks_on != 0;
+    const bool use_hist = g->use_bucket != 0;
+    const uint32_t mask_words = (uint32_t)((g->mask_off[D] + 31) / 32);
+    if (use_masks) {
         for (uint32_t w = threadIdx.x; w < mask_words; w += blockDim.x) s_mask[w] = 0;
         __syncthreads();
+    }
+    double mins[D], w = g->w;
+    uint64_t strides[D], pstride[D], moff[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        mins[j] = g->mins[j];
+        strides[j] = g->strides[j];
+        pstride[j] = g->pstride[j];
+        moff[j] = g->mask_off[j];
     }
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
@@ -109,24 +205,38 @@ k_keys(const double *__restrict__ pts, uint32_t n, DevIndex ix, uint64_t *__rest
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             const double x = pts[i * D + j];
-            const double t = floor(__ddiv_rn(__dsub_rn(x, ix.mins[j]), ix.w));
+            const double t = floor(__ddiv_rn(__dsub_rn(x, mins[j]), w));
             const uint64_t c = 1ull + (uint64_t)t;
-            key += c * ix.strides[j];
-            prefix += c * ix.pstride[j];
-            if (masks) {
-                const uint64_t bit = ix.mask_off[j] + c;
-                if (smem_masks) atomicOr(s_mask + (bit >> 5), 1u << (bit & 31));
-                else atomicOr(masks + (bit >> 5), 1u << (bit & 31));
+            key += c * strides[j];
+            prefix += c * pstride[j];
+            if (use_masks) {
+                const uint64_t bit = moff[j] + c;
+                atomicOr(s_mask + (bit >> 5), 1u << (bit & 31));
             }
         }
         keys[i] = key;
         ids[i] = (uint32_t)i;
-        if (bhist) atomicAdd(bhist + prefix, 1u);
+        if (use_hist) atomicAdd(bhist + prefix, 1u);
     }
-    if (smem_masks) {
+    if (use_masks) {
         __syncthreads();
-        for (uint32_t w = threadIdx.x; w < mask_words; w += blockDim.x)
-            if (s_mask[w]) atomicOr(masks + w, s_mask[w]);
+        for (uint32_t w2 = threadIdx.x; w2 < mask_words; w2 += blockDim.x)
+            if (s_mask[w2]) atomicOr(masks + w2, s_mask[w2]);
+    }
+}
+
+// masks too large for shared memory (host-launched after the geometry sync): global atomics
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+k_masks_global(const double *__restrict__ pts, uint32_t n, DevIndex ix, uint32_t *__restrict__ masks)
+{
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        const double t = floor(__ddiv_rn(__dsub_rn(pts[i * D + j], ix.mins[j]), ix.w));
+        const uint64_t bit = ix.mask_off[j] + 1ull + (uint64_t)t;
+        atomicOr(masks + (bit >> 5), 1u << (bit & 31));
     }
 }
 
@@ -200,6 +310,7 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
         if (b * ix.dir_div > key) --b;
         else if ((b + 1) * ix.dir_div <= key) ++b;
         h = __ldg(ix.dir + b) + pcell[k];
+        if (h >= n) return;         // only after a flagged bucket overflow (the build is redone)
     } else {                        // inclusive scan of head flags (1-based)
         h = pcell[k] - 1u;
     }
@@ -268,7 +379,7 @@ struct BuildArgs {
     uint64_t *keys = nullptr;
     uint32_t *ids = nullptr;
     uint32_t *masks = nullptr;
-    uint32_t mask_words = 0;
+    const DevGeom *geom = nullptr;
     uint32_t *bhist = nullptr;
     const uint32_t *A = nullptr;
     uint32_t *pcell = nullptr;
@@ -290,9 +401,9 @@ void launch_dim(int which, dim3 g, cudaStream_t s, const DevIndex &ix, const Bui
     if (which == 0) {
         k_minmax<D><<<g, kThreads, 0, s>>>(a.pts, a.n, a.mm, a.nonfinite);
     } else if (which == 1) {
-        const bool sm = a.masks && a.mask_words <= (uint32_t)kSmemMaskWords;
-        k_keys<D><<<g, kThreads, sm ? 4 * a.mask_words : 0, s>>>(a.pts, a.n, ix, a.keys, a.ids, a.masks, a.mask_words,
-                                                                 a.bhist);
+        k_keys<D><<<g, kThreads, 0, s>>>(a.pts, a.n, a.geom, a.keys, a.ids, a.masks, a.bhist);
+    } else if (which == 3) {
+        k_masks_global<D><<<g, kThreads, 0, s>>>(a.pts, a.n, ix, a.masks);
     } else {
         k_compact_gather<D><<<g, kThreads, 0, s>>>(a.keys, a.A, a.pts, a.n, a.pcell, a.B, a.G, a.X, a.ccoord, a.cmask,
                                                    ix, 16u, a.ndense, a.dirhist, a.occ, a.bucket_cells, a.dir_inv);
@@ -606,8 +717,9 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
     SJ_CUDA(cudaSetDevice(o.device));
 
     HostTrace tr("build");
-    // the build runs on the caller's stream, or on a pooled library stream
-    CtxGuard cg{o.stream ? nullptr : acquire_ctx(o.device, 1, 0, 64)};
+    // the build runs on the caller's stream, or on a pooled library stream; the pooled context also
+    // lends its pinned slot memory and an event (device geometry read-back)
+    CtxGuard cg{acquire_ctx(o.device, 1, 1, sizeof(DevGeom) + 64)};
     cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : cg.c->streams[0];
 
     const uint32_t N = (uint32_t)n;
@@ -640,9 +752,12 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         }
         ev.rec(1, s);
 
-        // ---- a1: exact per-dimension min/max + finiteness (one kernel, integer atomics); one D2H copy
+        // ---- a1: exact per-dimension min/max + finiteness (one kernel, integer atomics), then the
+        // geometry on the device (k_geometry) and the key pass right behind it; the host reads the
+        // geometry (one small D2H copy, waited on by an event) while the key pass runs.
         const uint32_t parts = (uint32_t)std::min<uint64_t>((n + kThreads - 1) / kThreads, (uint64_t)nsm * 4);
         Scratch<unsigned long long> mm(2 * d + 1, s);       // [2d] = non-finite flag
+        Scratch<DevGeom> dgeom(1, s);
         k_minmax_init<<<1, 32, 0, s>>>(mm.p, d, reinterpret_cast<uint32_t *>(mm.p + 2 * d));
         SJ_LAUNCHED();
         DevIndex ix{};
@@ -655,15 +770,21 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ba.nonfinite = reinterpret_cast<uint32_t *>(mm.p + 2 * d);
         launch(d, 0, dim3(parts), s, ix, ba);
         tr.dev("minmax", s);
-        unsigned long long h_ord[2 * SJ_MAX_DIM + 1];
-        SJ_CUDA(cudaMemcpyAsync(h_ord, mm.p, sizeof(unsigned long long) * (2 * d + 1), cudaMemcpyDeviceToHost, s));
+        k_geometry<<<1, 32, 0, s>>>(mm.p, d, eps, N, allow_bucket ? 1 : 0, o.build_masks ? 1 : 0, dgeom.p);
+        SJ_LAUNCHED();
+        DevGeom *hgeom = static_cast<DevGeom *>(cg.c->h_slots);
+        SJ_CUDA(cudaMemcpyAsync(hgeom, dgeom.p, sizeof(DevGeom), cudaMemcpyDeviceToHost, s));
+        SJ_CUDA(cudaEventRecord(cg.c->events[0], s));
+        ev.rec(2, s);
 
-        // ---- while the min/max pass runs: every N-sized array in two arenas (one owned by the
-        // index: A, pcell, B, G, X, cell coordinates/masks, aux; one scratch: keys, sort buffers)
+        // every N-sized array in two arenas (one owned by the index: A, pcell, B, G, X, cell
+        // coordinates/masks, the small mask bitmap, aux; one scratch: keys, sort buffers, bucket
+        // histogram sized for the largest possible prefix count)
         auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
         const size_t b_A = al(4 * n), b_pc = al(4 * n), b_B = al(8 * n), b_G = al(4 * (n + 1)), b_X = al(8 * n * d),
-                     b_cc = al(8 * n), b_cm = al(4 * n), b_aux = al(16);
-        char *arena = static_cast<char *>(own(dev_alloc(b_A + b_pc + b_B + b_G + b_X + b_cc + b_cm + b_aux, s)));
+                     b_cc = al(8 * n), b_cm = al(4 * n), b_mk = al(4 * kSmemMaskWords), b_aux = al(16);
+        char *arena =
+            static_cast<char *>(own(dev_alloc(b_A + b_pc + b_B + b_G + b_X + b_cc + b_cm + b_mk + b_aux, s)));
         uint32_t *A = reinterpret_cast<uint32_t *>(arena);
         uint32_t *pcell = reinterpret_cast<uint32_t *>(arena + b_A);
         uint64_t *B = reinterpret_cast<uint64_t *>(arena + b_A + b_pc);
@@ -671,26 +792,37 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         double *X = reinterpret_cast<double *>(arena + b_A + b_pc + b_B + b_G);
         uint64_t *ccoord = reinterpret_cast<uint64_t *>(arena + b_A + b_pc + b_B + b_G + b_X);
         uint32_t *cmask = reinterpret_cast<uint32_t *>(arena + b_A + b_pc + b_B + b_G + b_X + b_cc);
+        uint32_t *small_masks = reinterpret_cast<uint32_t *>(arena + b_A + b_pc + b_B + b_G + b_X + b_cc + b_cm);
         // aux: [0] = |G|, [1] = #dense tasks, [2] = #populous cells, [3] = bucket-sort overflow
-        uint32_t *aux = reinterpret_cast<uint32_t *>(arena + b_A + b_pc + b_B + b_G + b_X + b_cc + b_cm);
-        const size_t s_k = al(8 * n), s_i = al(4 * n);
-        Scratch<char> scratch(2 * s_k + 2 * s_i, s);
+        uint32_t *aux = reinterpret_cast<uint32_t *>(arena + b_A + b_pc + b_B + b_G + b_X + b_cc + b_cm + b_mk);
+        const uint64_t hcap = std::max<uint64_t>(4ull * n, 1ull << 16);
+        const size_t s_k = al(8 * n), s_i = al(4 * n), s_h = al(4 * (hcap + 1));
+        Scratch<char> scratch(2 * s_k + 2 * s_i + s_h, s);
         uint64_t *keys = reinterpret_cast<uint64_t *>(scratch.p);
         uint64_t *keys_tmp = reinterpret_cast<uint64_t *>(scratch.p + s_k);
         uint32_t *ids_tmp = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k);
         uint32_t *flags = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k + s_i);
-        SJ_CUDA(cudaMemsetAsync(aux, 0, sizeof(uint32_t) * 4, s));
-        tr.mark("minmax + arenas enqueued");
-        SJ_CUDA(cudaStreamSynchronize(s));
-        ev.rec(2, s);
-        tr.mark("minmax (synced)");
-        if ((uint32_t)h_ord[2 * d]) fail(SJ_ERR_NONFINITE, "a coordinate is NaN or infinite");
-        double h_mm[2 * SJ_MAX_DIM];
-        for (int t = 0; t < 2 * d; ++t) {
-            const unsigned long long k = h_ord[t];
-            const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
-            std::memcpy(&h_mm[t], &u, sizeof(double));
-        }
+        uint32_t *bhist = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k + 2 * s_i);
+        SJ_CUDA(cudaMemsetAsync(small_masks, 0, b_mk + 4 * sizeof(uint32_t), s));   // small masks + aux
+        k_zero_prefix_hist<<<(unsigned)std::min<uint64_t>((hcap + kThreads) / kThreads, (uint64_t)nsm * 8), kThreads, 0,
+                             s>>>(bhist, dgeom.p);
+        SJ_LAUNCHED();
+        const dim3 grid((unsigned)((n + kThreads - 1) / kThreads));
+
+        // ---- a2: keys (+ small masks, + prefix histogram of the bucket sort)
+        ba.keys = keys;
+        ba.ids = A;
+        ba.masks = small_masks;
+        ba.geom = dgeom.p;
+        ba.bhist = bhist;
+        launch(d, 1, grid, s, ix, ba);
+        ev.rec(3, s);
+        tr.dev("geometry + keys", s);
+        tr.mark("minmax/geometry/keys enqueued");
+        SJ_CUDA(cudaEventSynchronize(cg.c->events[0]));
+        tr.mark("geometry read");
+        const DevGeom hg = *hgeom;
+        if (hg.status == 1) fail(SJ_ERR_NONFINITE, "a coordinate is NaN or infinite");
 
         sj_index_view v{};
         v.d = d;
@@ -701,8 +833,18 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
             volatile double e2 = eps * eps;
             v.eps2 = e2;
         }
-        for (int j = 0; j < d; ++j) v.mins[j] = h_mm[j];
-        host_geometry(d, eps, h_mm, h_mm + d, v);
+        {
+            double h_mm[2 * SJ_MAX_DIM];
+            for (int j = 0; j < d; ++j) {
+                h_mm[j] = hg.mins[j];
+                v.mins[j] = hg.mins[j];
+            }
+            for (int j = 0; j < d; ++j) h_mm[d + j] = hg.maxs[j];
+            host_geometry(d, eps, h_mm, h_mm + d, v);   // throws SJ_ERR_KEY_OVERFLOW like the device
+        }
+        bool same = hg.status == 0 && hg.w == v.w && hg.key_bits == v.key_bits;
+        for (int j = 0; j < d; ++j) same = same && hg.cpd[j] == v.cpd[j] && hg.strides[j] == v.strides[j];
+        if (!same) fail(SJ_ERR_CUDA, "device and host geometry disagree (internal error)");
 
         ix.w = v.w;
         ix.eps2 = v.eps2;
@@ -711,7 +853,8 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
             ix.cpd[j] = v.cpd[j];
             ix.strides[j] = v.strides[j];
         }
-        // masks: one bitmap, |g_j| bits per dimension, only when <= 2^30 bits (they never change S)
+        // masks: one bitmap, |g_j| bits per dimension, only when <= 2^30 bits (they never change S);
+        // small ones were built by the key pass, larger ones by one more pass over the points
         uint64_t mask_total = 0;
         bool want_masks = o.build_masks != 0;
         for (int j = 0; j < d; ++j) {
@@ -739,35 +882,25 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         apply_dir_geometry(ix, v, dp);
         // a3 strategy: sparse keys (<= 2 points per top-k prefix on average, P <= 2^22 so the
         // bucket arrays stay L2-sized; measured slower than LSD at P = 11.4 M) -> prefix buckets +
-        // per-bucket sort; otherwise stable LSD radix sort
+        // per-bucket sort; otherwise stable LSD radix sort.  (Same rule as k_geometry's.)
         const bool use_bucket = allow_bucket && dp.k >= 1 && (double)n <= 2.0 * (double)dp.P &&
                                 dp.P <= (1ull << 22) && v.key_bits <= 62;
-
-        // ---- geometry-sized arrays: masks, bucket histogram (bucket path), directory, bitmaps
+        if (use_bucket != (hg.use_bucket != 0) || dp.P != hg.P || dp.k != hg.k)
+            fail(SJ_ERR_CUDA, "device and host directory plans disagree (internal error)");
         uint32_t *masks = nullptr;
-        const size_t mask_bytes = 4 * ((mask_total + 31) / 32);
-        if (want_masks) masks = static_cast<uint32_t *>(own(dev_alloc(mask_bytes, s)));
-        Scratch<uint32_t> bhist;
-        if (use_bucket) {
-            bhist.p = dalloc<uint32_t>((size_t)dp.P + 1, s);
-            bhist.s = s;
+        if (want_masks) {
+            if (hg.masks_on) {
+                masks = small_masks;
+            } else {
+                const size_t mask_bytes = 4 * ((mask_total + 31) / 32);
+                masks = static_cast<uint32_t *>(own(dev_alloc(mask_bytes, s)));
+                SJ_CUDA(cudaMemsetAsync(masks, 0, mask_bytes, s));
+                ix.mask_off[0] = v.mask_offsets[0];
+                ba.masks = masks;
+                launch(d, 3, grid, s, ix, ba);
+            }
         }
-        if (masks) SJ_CUDA(cudaMemsetAsync(masks, 0, mask_bytes, s));
-        if (use_bucket) SJ_CUDA(cudaMemsetAsync(bhist.p, 0, sizeof(uint32_t) * ((size_t)dp.P + 1), s));
-        const dim3 grid((unsigned)((n + kThreads - 1) / kThreads));
         tr.mark("geometry + allocs");
-
-        // ---- a2: keys (+ masks, + prefix histogram of the bucket sort)
-        ba.keys = keys;
-        ba.ids = A;
-        ba.masks = masks;
-        ba.mask_words = (uint32_t)((mask_total + 31) / 32);
-        ba.bhist = bhist.p;
-        tr.dev("geometry gap + memsets", s);
-        launch(d, 1, grid, s, ix, ba);
-        tr.dev("keys", s);
-        ev.rec(3, s);
-        tr.mark("keys launched");
         idx->view = v;
         alloc_dir(idx, dp, s);
         uint32_t *dir = const_cast<uint32_t *>(idx->dev.dir);
@@ -778,8 +911,8 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         if (use_bucket) {
             // the bucket sort also numbers each bucket's cells: pcell = cell index within the
             // bucket, bhist = cells per bucket, whose exclusive scan IS the prefix directory
-            bucket_sort_pairs(keys, A, keys_tmp, ids_tmp, N, dp.div, dp.P, bhist.p, aux + 3, pcell, bhist.p, s);
-            exclusive_scan_u32(bhist.p, dir, (uint64_t)dp.P + 1, s);
+            bucket_sort_pairs(keys, A, keys_tmp, ids_tmp, N, dp.div, dp.P, bhist, aux + 3, pcell, bhist, s);
+            exclusive_scan_u32(bhist, dir, (uint64_t)dp.P + 1, s);
             tr.dev("dir scan", s);
             SJ_CUDA(cudaMemcpyAsync(aux, dir + dp.P, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
         } else {
@@ -847,6 +980,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ev.rec(6, s);
         tr.dev("finish", s);
         tr.mark("compact+dir+dense (synced)");
+        if (tr.on) std::fprintf(stderr, "[sj-trace] aux = %u %u %u %u  bucket=%d P=%llu\n", h_aux[0], h_aux[1], h_aux[2], h_aux[3], (int)use_bucket, (unsigned long long)dp.P);
         for (int i = 0; i < 7; ++i) {
             idx->tev[i] = ev.e[i];
             ev.e[i] = nullptr;

@@ -373,7 +373,13 @@ k_bucket_sort_big(const uint64_t *__restrict__ kin, const uint32_t *__restrict__
         const uint32_t b = big[1 + qi];
         const uint32_t s = start[b], m = start[b + 1] - s;
         if (m > kBigMax) {
-            if (threadIdx.x == 0) atomicOr(overflow, 1u);
+            // flagged: the build is redone with the LSD sort.  Keep the cell numbering in range
+            // meanwhile (one cell for the whole bucket) so the compaction stays in bounds.
+            if (threadIdx.x == 0) {
+                atomicOr(overflow, 1u);
+                cellcnt[b] = 1;
+            }
+            for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) local[s + i] = 0;
             continue;
         }
         uint32_t m2 = 1;
