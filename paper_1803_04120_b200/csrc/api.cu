@@ -33,6 +33,12 @@ void configure_pool(int dev)
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         uint64_t thr = UINT64_MAX;  // keep freed memory cached in the pool (no OS round trips)
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        // let blocks freed on one stream (e.g. result batches freed on the legacy stream) serve
+        // allocations on another once the free completed, instead of mapping fresh memory
+        int on = 1;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &on);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &on);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolReuseFollowEventDependencies, &on);
     }
     g_pool_configured.insert(dev);
 }

@@ -107,6 +107,44 @@ void event_put(int dev, cudaEvent_t e)
     g_ev_free.emplace_back(dev, e);
 }
 
+// One grow-only scratch buffer per device for the index build's N-sized temporaries (keys, sort
+// buffers, prefix histogram): the stream-ordered pool re-maps memory when a previous join freed
+// gigabytes of result batches on another stream (measured 0.36 ms per build on 2-D eps=1).  A build
+// holds it from allocation to its final stream sync; a concurrent build falls back to the pool.
+namespace {
+struct ScratchSlot { void *p = nullptr; size_t bytes = 0; bool busy = false; };
+std::mutex g_scr_mu;
+std::map<int, ScratchSlot> g_scr;
+}  // namespace
+
+void *scratch_acquire(int dev, size_t bytes)
+{
+    std::lock_guard<std::mutex> lk(g_scr_mu);
+    ScratchSlot &sl = g_scr[dev];
+    if (sl.busy) return nullptr;
+    if (sl.bytes < bytes) {
+        if (sl.p) cudaFree(sl.p);
+        sl.p = nullptr;
+        sl.bytes = 0;
+        const size_t b = bytes + bytes / 4;
+        if (cudaMalloc(&sl.p, b) != cudaSuccess) {
+            cudaGetLastError();
+            sl.p = nullptr;
+            return nullptr;
+        }
+        sl.bytes = b;
+    }
+    sl.busy = true;
+    return sl.p;
+}
+
+void scratch_release(int dev, void *p)
+{
+    std::lock_guard<std::mutex> lk(g_scr_mu);
+    ScratchSlot &sl = g_scr[dev];
+    if (sl.p == p) sl.busy = false;
+}
+
 void set_max_dyn_smem(const void *func, int bytes)
 {
     static std::mutex mu;

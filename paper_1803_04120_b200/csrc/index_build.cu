@@ -777,6 +777,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         SJ_CUDA(cudaEventRecord(cg.c->events[0], s));
         ev.rec(2, s);
 
+        tr.mark("minmax + geometry enqueued");
         // every N-sized array in two arenas (one owned by the index: A, pcell, B, G, X, cell
         // coordinates/masks, the small mask bitmap, aux; one scratch: keys, sort buffers, bucket
         // histogram sized for the largest possible prefix count)
@@ -797,7 +798,29 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         uint32_t *aux = reinterpret_cast<uint32_t *>(arena + b_A + b_pc + b_B + b_G + b_X + b_cc + b_cm + b_mk);
         const uint64_t hcap = std::max<uint64_t>(4ull * n, 1ull << 16);
         const size_t s_k = al(8 * n), s_i = al(4 * n), s_h = al(4 * (hcap + 1));
-        Scratch<char> scratch(2 * s_k + 2 * s_i + s_h, s);
+        // the build's temporaries: the per-device cached scratch buffer (released after the final
+        // stream sync below), else pool memory
+        struct BuildScratch {
+            int dev;
+            char *p = nullptr;
+            bool cached = false;
+            cudaStream_t s;
+            BuildScratch(int d, size_t bytes, cudaStream_t st) : dev(d), s(st)
+            {
+                p = static_cast<char *>(scratch_acquire(dev, bytes));
+                cached = p != nullptr;
+                if (!cached) p = static_cast<char *>(dev_alloc(bytes, s));
+            }
+            ~BuildScratch()
+            {
+                if (cached) {
+                    cudaStreamSynchronize(s);      // (normally already idle: the build ends synced)
+                    scratch_release(dev, p);
+                } else {
+                    dev_free(p, s);
+                }
+            }
+        } scratch(o.device, 2 * s_k + 2 * s_i + s_h, s);
         uint64_t *keys = reinterpret_cast<uint64_t *>(scratch.p);
         uint64_t *keys_tmp = reinterpret_cast<uint64_t *>(scratch.p + s_k);
         uint32_t *ids_tmp = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k);

@@ -180,6 +180,8 @@ DevCtx *acquire_ctx(int dev, int nstreams, int nevents, size_t slot_bytes);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the call costs
 // tens of microseconds of host time, on the build's / join's critical path if repeated.
 void set_max_dyn_smem(const void *func, int bytes);
+void *scratch_acquire(int dev, size_t bytes);   // nullptr if busy (use the pool instead)
+void scratch_release(int dev, void *p);
 // pooled timing events (cudaEventCreate / elapsed-time queries stay off the critical path)
 cudaEvent_t event_get(int dev);
 void event_put(int dev, cudaEvent_t e);
