@@ -117,6 +117,35 @@ std::mutex g_scr_mu;
 std::map<int, ScratchSlot> g_scr;
 }  // namespace
 
+int device_count()
+{
+    static const int n = [] {
+        int c = 0;
+        if (cudaGetDeviceCount(&c) != cudaSuccess) {
+            cudaGetLastError();
+            c = 0;
+        }
+        return c;
+    }();
+    return n;
+}
+
+int device_sm_count(int dev)
+{
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int nsm = 148;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+        cudaGetLastError();
+        nsm = 148;
+    }
+    cache[dev] = nsm;
+    return nsm;
+}
+
 void *scratch_acquire(int dev, size_t bytes)
 {
     std::lock_guard<std::mutex> lk(g_scr_mu);

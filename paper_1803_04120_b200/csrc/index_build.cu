@@ -33,28 +33,41 @@ __device__ __forceinline__ unsigned long long ord_key(double x)
     return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
-// a1: exact per-dimension min/max (+ non-finite flag) in ONE pass: block reduce, then one
-// atomicMin/atomicMax per dimension per block on the order-preserving integer image.
-// mm[0..D) = ord(min), mm[D..2D) = ord(max); initialised to UINT64_MAX / 0.
+// a1: exact per-dimension min/max (+ non-finite flag) in ONE pass: each block reduces its points
+// and writes its partial (order-preserving integer images, no atomics, no initialisation):
+// part[b][0..D) = ord(min), part[b][D..2D) = ord(max), part[b][2D] = non-finite flag.  k_geometry
+// reduces the partials.  Even D: rows are read with 16-byte vector loads when aligned.
 template <int D>
 __global__ void __launch_bounds__(kThreads)
-k_minmax(const double *__restrict__ pts, uint32_t n, unsigned long long *__restrict__ mm, uint32_t *nonfinite)
+k_minmax(const double *__restrict__ pts, uint32_t n, unsigned long long *__restrict__ part)
 {
     double mn[D], mx[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) { mn[j] = INFINITY; mx[j] = -INFINITY; }
     bool bad = false;
+    const bool vec = D % 2 == 0 && (reinterpret_cast<uintptr_t>(pts) & 15u) == 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
+        double x[D];
+        if (vec) {
+#pragma unroll
+            for (int j = 0; j < D; j += 2) {
+                const double2 v = *reinterpret_cast<const double2 *>(pts + i * D + j);
+                x[j] = v.x;
+                if (j + 1 < D) x[j + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < D; ++j) x[j] = pts[i * D + j];
+        }
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            const double x = pts[i * D + j];
-            bad |= !isfinite(x);
-            mn[j] = fmin(mn[j], x);
-            mx[j] = fmax(mx[j], x);
+            bad |= !isfinite(x[j]);
+            mn[j] = fmin(mn[j], x[j]);
+            mx[j] = fmax(mx[j], x[j]);
         }
     }
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
+    const bool any_bad = __syncthreads_or(bad);
     __shared__ double s_mn[kThreads / 32][D], s_mx[kThreads / 32][D];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -67,22 +80,15 @@ k_minmax(const double *__restrict__ pts, uint32_t n, unsigned long long *__restr
         if (lane == 0) { s_mn[warp][j] = a; s_mx[warp][j] = b; }
     }
     __syncthreads();
+    unsigned long long *out = part + (uint64_t)blockIdx.x * (2 * D + 1);
     if (threadIdx.x < D) {
         const int j = threadIdx.x;
         double a = INFINITY, b = -INFINITY;
         for (int w = 0; w < kThreads / 32; ++w) { a = fmin(a, s_mn[w][j]); b = fmax(b, s_mx[w][j]); }
-        if (a <= b) {   // block saw at least one (finite) point
-            atomicMin(mm + j, ord_key(a));
-            atomicMax(mm + D + j, ord_key(b));
-        }
+        out[j] = ord_key(a);            // +inf / -inf when the block saw no point
+        out[D + j] = ord_key(b);
     }
-}
-
-__global__ void k_minmax_init(unsigned long long *mm, int d, uint32_t *nonfinite)
-{
-    const int t = threadIdx.x;
-    if (t < 2 * d) mm[t] = (t < d) ? ~0ull : 0ull;
-    if (t == 0) *nonfinite = 0;
+    if (threadIdx.x == 0) out[2 * D] = any_bad ? 1ull : 0ull;
 }
 
 // Geometry computed ON THE DEVICE from the min/max (same IEEE operations as host_geometry, so the
@@ -106,13 +112,37 @@ __device__ __forceinline__ double ord_to_double(unsigned long long k)
 }
 
 constexpr int kSmemMaskWords = 2048;   // 64 K bits, 8 KB of shared memory
+// context slot layout of the build: min/max partials (<= 4 * SMs blocks), then the DevGeom
+constexpr size_t kGeomOffset = 4 * 256 * (2 * SJ_MAX_DIM + 1) * sizeof(unsigned long long);
 
-__global__ void k_geometry(const unsigned long long *__restrict__ mm, int d, double eps, uint32_t n, int allow_bucket,
-                           int want_masks, DevGeom *__restrict__ g)
+__global__ void __launch_bounds__(256)
+k_geometry(const unsigned long long *__restrict__ part, uint32_t parts, int d, double eps, uint32_t n,
+           int allow_bucket, int want_masks, DevGeom *__restrict__ g)
 {
+    // reduce the per-block partials of k_minmax: min over [0, d), max over [d, 2d), or of [2d]
+    __shared__ unsigned long long s_red[2 * SJ_MAX_DIM + 1][8];
+    __shared__ unsigned long long mm[2 * SJ_MAX_DIM + 1];
+    for (int v = 0; v <= 2 * d; ++v) {
+        unsigned long long acc = v < d ? ~0ull : 0ull;
+        for (uint32_t b = threadIdx.x; b < parts; b += blockDim.x) {
+            const unsigned long long x = part[(uint64_t)b * (2 * d + 1) + v];
+            acc = v < d ? min(acc, x) : max(acc, x);
+        }
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, acc, o);
+            acc = v < d ? min(acc, y) : max(acc, y);
+        }
+        if ((threadIdx.x & 31) == 0) s_red[v][threadIdx.x >> 5] = acc;
+    }
+    __syncthreads();
     if (threadIdx.x != 0) return;
+    for (int v = 0; v <= 2 * d; ++v) {
+        unsigned long long acc = s_red[v][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) acc = v < d ? min(acc, s_red[v][w]) : max(acc, s_red[v][w]);
+        mm[v] = acc;
+    }
     DevGeom G{};
-    if ((uint32_t)mm[2 * d]) { G.status = 1; *g = G; return; }
+    if (mm[2 * d]) { G.status = 1; *g = G; return; }
     double R = 0.0, ranges[SJ_MAX_DIM];
     for (int j = 0; j < d; ++j) {
         const double mn = ord_to_double(mm[j]), mx = ord_to_double(mm[d + j]);
@@ -399,7 +429,7 @@ template <int D>
 void launch_dim(int which, dim3 g, cudaStream_t s, const DevIndex &ix, const BuildArgs &a)
 {
     if (which == 0) {
-        k_minmax<D><<<g, kThreads, 0, s>>>(a.pts, a.n, a.mm, a.nonfinite);
+        k_minmax<D><<<g, kThreads, 0, s>>>(a.pts, a.n, a.mm);
     } else if (which == 1) {
         k_keys<D><<<g, kThreads, 0, s>>>(a.pts, a.n, a.geom, a.keys, a.ids, a.masks, a.bhist);
     } else if (which == 3) {
@@ -708,18 +738,15 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         volatile double e2 = eps * eps;
         if (!std::isnormal((double)e2)) fail(SJ_ERR_ARG, "fl(eps*eps) must be a normal double");
     }
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
-        cudaGetLastError();
-        fail(SJ_ERR_STATE, "no CUDA device available (the library has no CPU fallback)");
-    }
+    const int ndev = device_count();
+    if (ndev == 0) fail(SJ_ERR_STATE, "no CUDA device available (the library has no CPU fallback)");
     if (o.device < 0 || o.device >= ndev) fail(SJ_ERR_ARG, "bad device ordinal");
     SJ_CUDA(cudaSetDevice(o.device));
 
     HostTrace tr("build");
     // the build runs on the caller's stream, or on a pooled library stream; the pooled context also
     // lends its pinned slot memory and an event (device geometry read-back)
-    CtxGuard cg{acquire_ctx(o.device, 1, 1, sizeof(DevGeom) + 64)};
+    CtxGuard cg{acquire_ctx(o.device, 1, 1, kGeomOffset + sizeof(DevGeom))};
     cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : cg.c->streams[0];
 
     const uint32_t N = (uint32_t)n;
@@ -738,8 +765,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
     idx->device = o.device;
     auto own = [&](void *p) { idx->bufs[idx->nbufs++] = p; return p; };
     uint32_t h_aux[4] = {0, 0, 0, 0};
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device);
+    const int nsm = device_sm_count(o.device);
     try {
         // ---- inputs on device
         const double *pts = points;
@@ -755,25 +781,24 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         // ---- a1: exact per-dimension min/max + finiteness (one kernel, integer atomics), then the
         // geometry on the device (k_geometry) and the key pass right behind it; the host reads the
         // geometry (one small D2H copy, waited on by an event) while the key pass runs.
-        const uint32_t parts = (uint32_t)std::min<uint64_t>((n + kThreads - 1) / kThreads, (uint64_t)nsm * 4);
-        Scratch<unsigned long long> mm(2 * d + 1, s);       // [2d] = non-finite flag
-        Scratch<DevGeom> dgeom(1, s);
-        k_minmax_init<<<1, 32, 0, s>>>(mm.p, d, reinterpret_cast<uint32_t *>(mm.p + 2 * d));
-        SJ_LAUNCHED();
+        const uint32_t parts =
+            (uint32_t)std::min<uint64_t>(std::min<uint64_t>((n + kThreads - 1) / kThreads, (uint64_t)nsm * 4), 1024);
+        // min/max partials and the device geometry live in the context's slot memory
+        unsigned long long *part = static_cast<unsigned long long *>(cg.c->d_slots);
+        DevGeom *dgeom = reinterpret_cast<DevGeom *>(static_cast<char *>(cg.c->d_slots) + kGeomOffset);
         DevIndex ix{};
         ix.d = d;
         ix.n = N;
         BuildArgs ba;
         ba.pts = pts;
         ba.n = N;
-        ba.mm = mm.p;
-        ba.nonfinite = reinterpret_cast<uint32_t *>(mm.p + 2 * d);
+        ba.mm = part;
         launch(d, 0, dim3(parts), s, ix, ba);
         tr.dev("minmax", s);
-        k_geometry<<<1, 32, 0, s>>>(mm.p, d, eps, N, allow_bucket ? 1 : 0, o.build_masks ? 1 : 0, dgeom.p);
+        k_geometry<<<1, 256, 0, s>>>(part, parts, d, eps, N, allow_bucket ? 1 : 0, o.build_masks ? 1 : 0, dgeom);
         SJ_LAUNCHED();
         DevGeom *hgeom = static_cast<DevGeom *>(cg.c->h_slots);
-        SJ_CUDA(cudaMemcpyAsync(hgeom, dgeom.p, sizeof(DevGeom), cudaMemcpyDeviceToHost, s));
+        SJ_CUDA(cudaMemcpyAsync(hgeom, dgeom, sizeof(DevGeom), cudaMemcpyDeviceToHost, s));
         SJ_CUDA(cudaEventRecord(cg.c->events[0], s));
         ev.rec(2, s);
 
@@ -828,7 +853,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         uint32_t *bhist = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k + 2 * s_i);
         SJ_CUDA(cudaMemsetAsync(small_masks, 0, b_mk + 4 * sizeof(uint32_t), s));   // small masks + aux
         k_zero_prefix_hist<<<(unsigned)std::min<uint64_t>((hcap + kThreads) / kThreads, (uint64_t)nsm * 8), kThreads, 0,
-                             s>>>(bhist, dgeom.p);
+                             s>>>(bhist, dgeom);
         SJ_LAUNCHED();
         const dim3 grid((unsigned)((n + kThreads - 1) / kThreads));
 
@@ -836,7 +861,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ba.keys = keys;
         ba.ids = A;
         ba.masks = small_masks;
-        ba.geom = dgeom.p;
+        ba.geom = dgeom;
         ba.bhist = bhist;
         launch(d, 1, grid, s, ix, ba);
         ev.rec(3, s);

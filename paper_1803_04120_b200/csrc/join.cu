@@ -297,8 +297,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
 #define SJ_EST_LANES_MAX 3
 #endif
             if (o.lanes_per_query == 0) {
-                int nsm = 148;
-                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, idx->device);
+                const int nsm = device_sm_count(idx->device);
                 while (ja.lanes_log2 < SJ_EST_LANES_MAX && (sm.ns << (ja.lanes_log2 + 1)) <= (uint64_t)nsm * 1024)
                     ++ja.lanes_log2;
             }

@@ -180,6 +180,8 @@ DevCtx *acquire_ctx(int dev, int nstreams, int nevents, size_t slot_bytes);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the call costs
 // tens of microseconds of host time, on the build's / join's critical path if repeated.
 void set_max_dyn_smem(const void *func, int bytes);
+int device_count();                            // cached cudaGetDeviceCount (0 on error)
+int device_sm_count(int dev);                  // cached multiprocessor count
 void *scratch_acquire(int dev, size_t bytes);   // nullptr if busy (use the pool instead)
 void scratch_release(int dev, void *p);
 // pooled timing events (cudaEventCreate / elapsed-time queries stay off the critical path)
