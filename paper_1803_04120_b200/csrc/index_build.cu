@@ -36,7 +36,7 @@ __device__ __forceinline__ unsigned long long ord_key(double x)
 // a1: exact per-dimension min/max (+ non-finite flag) in ONE pass: each block reduces its points
 // and writes its partial (order-preserving integer images, no atomics, no initialisation):
 // part[b][0..D) = ord(min), part[b][D..2D) = ord(max), part[b][2D] = non-finite flag.  k_geometry
-// reduces the partials.  Even D: rows are read with 16-byte vector loads when aligned.
+// reduces the partials.
 template <int D>
 __global__ void __launch_bounds__(kThreads)
 k_minmax(const double *__restrict__ pts, uint32_t n, unsigned long long *__restrict__ part)
@@ -45,26 +45,14 @@ k_minmax(const double *__restrict__ pts, uint32_t n, unsigned long long *__restr
 #pragma unroll
     for (int j = 0; j < D; ++j) { mn[j] = INFINITY; mx[j] = -INFINITY; }
     bool bad = false;
-    const bool vec = D % 2 == 0 && (reinterpret_cast<uintptr_t>(pts) & 15u) == 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        double x[D];
-        if (vec) {
-#pragma unroll
-            for (int j = 0; j < D; j += 2) {
-                const double2 v = *reinterpret_cast<const double2 *>(pts + i * D + j);
-                x[j] = v.x;
-                if (j + 1 < D) x[j + 1] = v.y;
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < D; ++j) x[j] = pts[i * D + j];
-        }
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            bad |= !isfinite(x[j]);
-            mn[j] = fmin(mn[j], x[j]);
-            mx[j] = fmax(mx[j], x[j]);
+            const double x = pts[i * D + j];
+            bad |= !isfinite(x);
+            mn[j] = fmin(mn[j], x);
+            mx[j] = fmax(mx[j], x);
         }
     }
     const bool any_bad = __syncthreads_or(bad);
@@ -104,6 +92,7 @@ struct DevGeom {
     int key_bits, k, use_bucket, masks_on;
     int status;                  // 0 ok, 1 non-finite coordinate, 2 key overflow
 };
+static_assert(sizeof(DevGeom) % 8 == 0, "DevGeom is copied as 64-bit words");
 
 __device__ __forceinline__ double ord_to_double(unsigned long long k)
 {
@@ -115,78 +104,125 @@ constexpr int kSmemMaskWords = 2048;   // 64 K bits, 8 KB of shared memory
 // context slot layout of the build: min/max partials (<= 4 * SMs blocks), then the DevGeom
 constexpr size_t kGeomOffset = 4 * 256 * (2 * SJ_MAX_DIM + 1) * sizeof(unsigned long long);
 
+__device__ __noinline__ void geometry_products(const uint64_t *cpd, int d, uint32_t n, int allow_bucket,
+                                               int want_masks, DevGeom &G);
+
 __global__ void __launch_bounds__(256)
 k_geometry(const unsigned long long *__restrict__ part, uint32_t parts, int d, double eps, uint32_t n,
            int allow_bucket, int want_masks, DevGeom *__restrict__ g)
 {
-    // reduce the per-block partials of k_minmax: min over [0, d), max over [d, 2d), or of [2d]
+    // reduce the per-block partials of k_minmax: min over [0, d), max over [d, 2d), or of [2d];
+    // each thread folds whole rows (independent loads in flight), then warp and CTA reductions
     __shared__ unsigned long long s_red[2 * SJ_MAX_DIM + 1][8];
     __shared__ unsigned long long mm[2 * SJ_MAX_DIM + 1];
-    for (int v = 0; v <= 2 * d; ++v) {
-        unsigned long long acc = v < d ? ~0ull : 0ull;
-        for (uint32_t b = threadIdx.x; b < parts; b += blockDim.x) {
-            const unsigned long long x = part[(uint64_t)b * (2 * d + 1) + v];
-            acc = v < d ? min(acc, x) : max(acc, x);
+    unsigned long long acc[2 * SJ_MAX_DIM + 1];
+#pragma unroll
+    for (int v = 0; v <= 2 * SJ_MAX_DIM; ++v) acc[v] = v < d ? ~0ull : 0ull;
+    for (uint32_t b = threadIdx.x; b < parts; b += blockDim.x) {
+        const unsigned long long *row = part + (uint64_t)b * (2 * d + 1);
+#pragma unroll
+        for (int v = 0; v <= 2 * SJ_MAX_DIM; ++v) {
+            if (v > 2 * d) break;
+            const unsigned long long x = row[v];
+            acc[v] = v < d ? min(acc[v], x) : max(acc[v], x);
         }
+    }
+#pragma unroll
+    for (int v = 0; v <= 2 * SJ_MAX_DIM; ++v) {
+        if (v > 2 * d) break;
         for (int o = 16; o; o >>= 1) {
-            const unsigned long long y = __shfl_xor_sync(0xffffffffu, acc, o);
-            acc = v < d ? min(acc, y) : max(acc, y);
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, acc[v], o);
+            acc[v] = v < d ? min(acc[v], y) : max(acc[v], y);
         }
-        if ((threadIdx.x & 31) == 0) s_red[v][threadIdx.x >> 5] = acc;
+        if ((threadIdx.x & 31) == 0) s_red[v][threadIdx.x >> 5] = acc[v];
     }
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    for (int v = 0; v <= 2 * d; ++v) {
-        unsigned long long acc = s_red[v][0];
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) acc = v < d ? min(acc, s_red[v][w]) : max(acc, s_red[v][w]);
-        mm[v] = acc;
+    if (threadIdx.x >= 32) return;
+    // warp 0: lanes finish the reduction per value, then lane j < d handles dimension j (its
+    // division in parallel with the others); lane 0 does the products
+    const int lane = threadIdx.x;
+    if (lane <= 2 * d) {
+        unsigned long long a = s_red[lane][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) a = lane < d ? min(a, s_red[lane][w]) : max(a, s_red[lane][w]);
+        mm[lane] = a;
     }
-    DevGeom G{};
-    if (mm[2 * d]) { G.status = 1; *g = G; return; }
-    double R = 0.0, ranges[SJ_MAX_DIM];
-    for (int j = 0; j < d; ++j) {
-        const double mn = ord_to_double(mm[j]), mx = ord_to_double(mm[d + j]);
-        G.mins[j] = mn;
-        G.maxs[j] = mx;
-        ranges[j] = __dsub_rn(mx, mn);
-        if (ranges[j] > R) R = ranges[j];
+    __syncwarp();
+    __shared__ DevGeom G;
+    if (lane == 0) {
+        uint64_t *z = reinterpret_cast<uint64_t *>(&G);
+        for (size_t i2 = 0; i2 < sizeof(DevGeom) / 8; ++i2) z[i2] = 0;
     }
+    __syncwarp();
+    const bool bad = mm[2 * d] != 0;
+    double range = 0.0;
+    if (lane < d) {
+        const double mn = ord_to_double(mm[lane]), mx = ord_to_double(mm[d + lane]);
+        G.mins[lane] = mn;
+        G.maxs[lane] = mx;
+        range = __dsub_rn(mx, mn);
+    }
+    double R = range;
+    for (int o = 16; o; o >>= 1) R = fmax(R, __shfl_xor_sync(0xffffffffu, R, o));
     const double er = __dadd_rn(eps, R);
-    G.w = __dadd_rn(eps, __dmul_rn(er, 0x1p-44));       // = eps + ldexp(er, -44) (exact scaling)
+    const double w = __dadd_rn(eps, __dmul_rn(er, 0x1p-44));       // = eps + ldexp(er, -44) (exact scaling)
+    double t = 0.0;
+    if (lane < d) t = floor(__ddiv_rn(range, w));
+    const bool tbad = lane < d && !(t < 9.0e18);
+    const bool any_tbad = __any_sync(0xffffffffu, tbad);
+    const uint64_t mycpd = (lane < d && !tbad) ? 3ull + (uint64_t)t : 0ull;
+    uint64_t cpd[SJ_MAX_DIM];
+#pragma unroll
+    for (int j = 0; j < SJ_MAX_DIM; ++j) cpd[j] = __shfl_sync(0xffffffffu, mycpd, j);
+    if (lane == 0) {
+        G.w = w;
+        if (bad) G.status = 1;
+        else if (any_tbad) G.status = 2;
+        else geometry_products(cpd, d, n, allow_bucket, want_masks, G);
+    }
+    __syncwarp();
+    const uint64_t *src = reinterpret_cast<const uint64_t *>(&G);
+    uint64_t *dst = reinterpret_cast<uint64_t *>(g);
+    for (size_t i2 = lane; i2 < sizeof(DevGeom) / 8; i2 += 32) dst[i2] = src[i2];
+}
+
+// lane 0 of k_geometry: everything that needs only products and sums of the |g_j|
+__device__ __noinline__ void geometry_products(const uint64_t *cpd, int d, uint32_t n, int allow_bucket,
+                                               int want_masks, DevGeom &G)
+{
     unsigned __int128 prod = 1;
     for (int j = 0; j < d; ++j) {
-        const double t = floor(__ddiv_rn(ranges[j], G.w));
-        if (!(t < 9.0e18)) { G.status = 2; *g = G; return; }
-        G.cpd[j] = 3ull + (uint64_t)t;
-        prod *= G.cpd[j];
-        if (prod >> 64) { G.status = 2; *g = G; return; }
+        G.cpd[j] = cpd[j];
+        prod *= cpd[j];
+        if (prod >> 64) { G.status = 2; return; }
     }
     G.strides[0] = 1;
-    for (int j = 1; j < d; ++j) G.strides[j] = G.strides[j - 1] * G.cpd[j - 1];
-    unsigned __int128 maxkey = prod - 1;
-    int bits = 0;
-    while (maxkey > 0) { ++bits; maxkey >>= 1; }
-    G.key_bits = bits;
+    for (int j = 1; j < d; ++j) G.strides[j] = G.strides[j - 1] * cpd[j - 1];
+    const unsigned __int128 maxkey = prod - 1;
+    const uint64_t hi = (uint64_t)(maxkey >> 64), lo = (uint64_t)maxkey;
+    G.key_bits = hi ? 128 - __clzll((long long)hi) : (lo ? 64 - __clzll((long long)lo) : 0);
     // directory plan (plan_dir): largest k with prod_{top k} |g_j| <= max(4N, 2^16)
     const uint64_t cap = max((uint64_t)4 * n, (uint64_t)1 << 16);
     unsigned __int128 P = 1;
     for (int kk = 1; kk <= d; ++kk) {
-        const unsigned __int128 Q = P * G.cpd[d - kk];
+        const unsigned __int128 Q = P * cpd[d - kk];
         if (Q > cap) break;
         P = Q;
         G.k = kk;
     }
     G.P = (uint64_t)P;
     G.div = 1;
-    for (int j = 0; j < d - G.k; ++j) G.div *= G.cpd[j];
-    for (int j = 0; j < d; ++j) G.pstride[j] = (j >= d - G.k) ? G.strides[j] / G.div : 0;
+    for (int j = 0; j < d - G.k; ++j) G.div *= cpd[j];
+    uint64_t ps = 1;                                   // pstride_j = prod_{d-k <= m < j} |g_m|
+    for (int j = 0; j < d; ++j) {
+        G.pstride[j] = (j >= d - G.k) ? ps : 0;
+        if (j >= d - G.k) ps *= cpd[j];
+    }
     G.use_bucket = allow_bucket && G.k >= 1 && (double)n <= 2.0 * (double)G.P && G.P <= (1ull << 22) &&
                    G.key_bits <= 62;
     uint64_t mt = 0;
-    for (int j = 0; j < d; ++j) { G.mask_off[j] = mt; mt += G.cpd[j]; }
+    for (int j = 0; j < d; ++j) { G.mask_off[j] = mt; mt += cpd[j]; }
     G.mask_off[d] = mt;
     G.masks_on = want_masks && mt <= 32ull * kSmemMaskWords;
-    *g = G;
 }
 
 // zero bhist[0, P] (P known on the device only)
@@ -212,35 +248,34 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
        uint32_t *__restrict__ ids, uint32_t *__restrict__ masks, uint32_t *__restrict__ bhist)
 {
     __shared__ uint32_t s_mask[kSmemMaskWords];
+    __shared__ double s_min[D];
+    __shared__ uint64_t s_str[D], s_pstr[D], s_moff[D];
     if (g->status) return;
     const bool use_masks = g->masks_on != 0;
     const bool use_hist = g->use_bucket != 0;
+    const double w = g->w;
     const uint32_t mask_words = (uint32_t)((g->mask_off[D] + 31) / 32);
-    if (use_masks) {
-        for (uint32_t w = threadIdx.x; w < mask_words; w += blockDim.x) s_mask[w] = 0;
-        __syncthreads();
+    if (threadIdx.x < D) {
+        s_min[threadIdx.x] = g->mins[threadIdx.x];
+        s_str[threadIdx.x] = g->strides[threadIdx.x];
+        s_pstr[threadIdx.x] = g->pstride[threadIdx.x];
+        s_moff[threadIdx.x] = g->mask_off[threadIdx.x];
     }
-    double mins[D], w = g->w;
-    uint64_t strides[D], pstride[D], moff[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        mins[j] = g->mins[j];
-        strides[j] = g->strides[j];
-        pstride[j] = g->pstride[j];
-        moff[j] = g->mask_off[j];
-    }
+    if (use_masks)
+        for (uint32_t w2 = threadIdx.x; w2 < mask_words; w2 += blockDim.x) s_mask[w2] = 0;
+    __syncthreads();
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
         uint64_t key = 0, prefix = 0;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             const double x = pts[i * D + j];
-            const double t = floor(__ddiv_rn(__dsub_rn(x, mins[j]), w));
+            const double t = floor(__ddiv_rn(__dsub_rn(x, s_min[j]), w));
             const uint64_t c = 1ull + (uint64_t)t;
-            key += c * strides[j];
-            prefix += c * pstride[j];
+            key += c * s_str[j];
+            prefix += c * s_pstr[j];
             if (use_masks) {
-                const uint64_t bit = moff[j] + c;
+                const uint64_t bit = s_moff[j] + c;
                 atomicOr(s_mask + (bit >> 5), 1u << (bit & 31));
             }
         }
