@@ -325,31 +325,6 @@ __device__ __forceinline__ void occ_set_window(uint32_t *occ, uint64_t q)
     if (sh > 29) atomicOr(occ + (a >> 5) + 1, 7u >> (32 - sh));
 }
 
-// Cell coordinates from a linear id: c_j = (key / stride_j) mod |g_j|, taken from the slowest
-// dimension down (each quotient < |g_j|).  Fast path: the quotient from a double reciprocal,
-// corrected by +-1 in exact integer arithmetic (valid while quotients < 2^50 and keys < 2^63, which
-// the host checks -> ix.key_fastdiv); otherwise exact 64-bit division.
-template <int D>
-__device__ __forceinline__ void key_to_coords(const DevIndex &ix, uint64_t key, uint64_t (&c)[D])
-{
-    uint64_t rem = key;
-#pragma unroll
-    for (int j = D - 1; j >= 1; --j) {
-        const uint64_t st = ix.strides[j];
-        uint64_t q;
-        if (ix.key_fastdiv) {
-            q = (uint64_t)((double)rem * ix.inv_stride[j]);
-            if (q * st > rem) --q;
-            else if ((q + 1) * st <= rem) ++q;
-        } else {
-            q = rem / st;
-        }
-        c[j] = q;
-        rem -= q * st;
-    }
-    c[0] = rem;
-}
-
 // pcell holds the inclusive scan of head flags on entry (1-based cell number) and the
 // 0-based cell index on exit.  At the head of each cell h (one thread per cell):
 //   B[h], G[h]; populous-cell count (dense tasks); its packed coordinates (decoded from the key)
@@ -843,7 +818,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         // histogram sized for the largest possible prefix count)
         auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
         const size_t b_A = al(4 * n), b_pc = al(4 * n), b_B = al(8 * n), b_G = al(4 * (n + 1)), b_X = al(8 * n * d),
-                     b_cc = al(8 * n), b_cm = al(4 * n), b_mk = al(4 * kSmemMaskWords), b_aux = al(16);
+                     b_cc = 0, b_cm = 0, b_mk = al(4 * kSmemMaskWords), b_aux = al(16);   // (no per-cell coords/masks)
         char *arena =
             static_cast<char *>(own(dev_alloc(b_A + b_pc + b_B + b_G + b_X + b_cc + b_cm + b_mk + b_aux, s)));
         uint32_t *A = reinterpret_cast<uint32_t *>(arena);
@@ -960,7 +935,11 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
             }
             pack_fits = sh <= 64;
         }
-        if (!pack_fits) ccoord = nullptr, cmask = nullptr;
+        // (the refine decodes a cell's coordinates from its key and tests the small masks directly:
+        // no per-cell coordinate / mask arrays -- 24 B per cell less to write and read)
+        (void)pack_fits;
+        ccoord = nullptr;
+        cmask = nullptr;
         const DirPlan dp = plan_dir(v);
         apply_dir_geometry(ix, v, dp);
         // a3 strategy: sparse keys (<= 2 points per top-k prefix on average, P <= 2^22 so the

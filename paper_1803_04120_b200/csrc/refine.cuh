@@ -596,19 +596,12 @@ __device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs 
     q.pid = __ldg(ix.A + k);
 #pragma unroll
     for (int j = 0; j < D; ++j) q.x[j] = __ldg(ix.X + (uint64_t)j * ix.n + k);
-    if (ix.ccoord) {                  // the home cell's coordinates, packed at build time
-        const uint64_t cc = __ldg(ix.ccoord + h);
-#pragma unroll
-        for (int j = 0; j < D; ++j) q.c[j] = (cc >> ix.cshift[j]) & ((1ull << ix.cbits[j]) - 1ull);
-    } else {
-#pragma unroll
-        for (int j = 0; j < D; ++j)   // same IEEE operations as the build (reading R7)
-            q.c[j] = 1ull + (uint64_t)floor(__ddiv_rn(__dsub_rn(q.x[j], ix.mins[j]), ix.w));
-    }
+    // the home cell's coordinates, decoded from its linear id (double-reciprocal quotients)
+    const uint64_t key = __ldg(ix.B + h);
+    key_to_coords<D>(ix, key, q.c);
     q.odd = 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) q.odd |= (uint32_t)(q.c[j] & 1ull) << j;
-    const uint64_t key = __ldg(ix.B + h);
 
     // ---- home cell: (p,p) once; unicomp: q after p in A-order, both orientations (R10)
     if constexpr (DENSE) {

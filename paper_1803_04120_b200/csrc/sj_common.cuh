@@ -131,6 +131,32 @@ struct DevIndex {
 
 enum SearchMode { kSearchDenseRows = 0, kSearchCellScan = 1, kSearchRows = 2 };
 
+// Cell coordinates from a linear id: c_j = (key / stride_j) mod |g_j|, taken from the slowest
+// dimension down (each quotient < |g_j|).  Fast path: the quotient from a double reciprocal,
+// corrected by +-1 in exact integer arithmetic (valid while quotients < 2^50 and keys < 2^63, which
+// the host checks -> ix.key_fastdiv); otherwise exact 64-bit division.
+template <int D>
+__device__ __forceinline__ void key_to_coords(const DevIndex &ix, uint64_t key, uint64_t (&c)[D])
+{
+    uint64_t rem = key;
+#pragma unroll
+    for (int j = D - 1; j >= 1; --j) {
+        const uint64_t st = ix.strides[j];
+        uint64_t q;
+        if (ix.key_fastdiv) {
+            q = (uint64_t)((double)rem * ix.inv_stride[j]);
+            if (q * st > rem) --q;
+            else if ((q + 1) * st <= rem) ++q;
+        } else {
+            q = rem / st;
+        }
+        c[j] = q;
+        rem -= q * st;
+    }
+    c[0] = rem;
+}
+
+
 }  // namespace sj
 
 // The opaque handle.
