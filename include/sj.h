@@ -181,6 +181,14 @@ sj_status sj_result_batch(const sj_result *r, uint32_t b, const uint64_t **pairs
  * Errors: SJ_ERR_ARG if cap < total. */
 sj_status sj_result_copy_to_host(const sj_result *r, uint64_t *dst, uint64_t cap);
 
+/* The whole result as CSR neighbour lists (the sorted key/value pairs of
+ * PAPER.md:209): row_offsets[i] .. row_offsets[i+1] (n_points + 1 uint64, DEVICE memory on the
+ * result's device) index the neighbours of point i (original ids) in `neighbors` (n_pairs uint32,
+ * DEVICE memory), ascending within a row.  4 bytes per pair instead of 8.  Both arrays are owned by
+ * the caller.  Blocks until written.  Errors: SJ_ERR_ARG (n_points out of range, NULL arrays,
+ * >= 2^32 pairs), SJ_ERR_NOMEM (scratch of 16 B per pair), SJ_ERR_CUDA. */
+sj_status sj_result_to_csr(const sj_result *r, uint64_t n_points, uint64_t *row_offsets, uint32_t *neighbors);
+
 /* Per-point neighbour counts cnt[i] = |{k : (i,k) in S}| without materialising
  * pairs.  cnt: device pointer to N uint32 on the index's device (zeroed by the call), or NULL.
  * *total receives |S| (restricted to the pairs decided by queries of opts' query range). */

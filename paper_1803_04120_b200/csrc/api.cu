@@ -286,6 +286,14 @@ sj_status sj_result_copy_to_host(const sj_result *r, uint64_t *dst, uint64_t cap
     SJ_API_END
 }
 
+sj_status sj_result_to_csr(const sj_result *r, uint64_t n_points, uint64_t *row_offsets, uint32_t *neighbors)
+{
+    SJ_API_BEGIN
+    sj::result_to_csr_impl(r, n_points, row_offsets, neighbors);
+    return SJ_OK;
+    SJ_API_END
+}
+
 sj_status sj_neighbor_counts(const sj_index *idx, const sj_join_opts *opts, uint32_t *cnt, uint64_t *total)
 {
     SJ_API_BEGIN

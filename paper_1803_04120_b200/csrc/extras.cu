@@ -24,6 +24,70 @@ void sort_pairs_device(uint64_t *pairs, uint64_t n, uint64_t n_points, cudaStrea
     if (in_tmp) SJ_CUDA(cudaMemcpyAsync(pairs, tmp.p, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
 }
 
+// ------------------------------------------------------------------ f2: CSR neighbour lists
+// The whole result as compressed rows: row_offsets[i] .. row_offsets[i+1] index the neighbours of
+// point i (original ids) in `neighbors`, ascending -- 4 B per pair instead of 8 (SURVEY §8(f) rank
+// 2).  All batches are gathered, sorted as packed uint64 (the radix sort above: integer order ==
+// (key, value) order, so rows come out sorted), rows counted, scanned, values extracted.
+namespace {
+__global__ void k_csr_hist(const uint64_t *__restrict__ pairs, uint64_t n, uint32_t *__restrict__ counts)
+{
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(counts + (pairs[i] >> 32), 1u);
+}
+
+__global__ void k_csr_values(const uint64_t *__restrict__ pairs, uint64_t n, uint32_t *__restrict__ nbrs)
+{
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        nbrs[i] = (uint32_t)pairs[i];
+}
+
+__global__ void k_widen_u32(const uint32_t *__restrict__ in, uint64_t n, uint64_t *__restrict__ out)
+{
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+}  // namespace
+
+void result_to_csr_impl(const sj_result *r, uint64_t n_points, uint64_t *row_offsets, uint32_t *neighbors)
+{
+    if (!r) fail(SJ_ERR_STATE, "result is NULL");
+    if (n_points == 0 || n_points >= (1ull << 32)) fail(SJ_ERR_ARG, "n_points must satisfy 1 <= n < 2^32");
+    if (!row_offsets || (!neighbors && r->total)) fail(SJ_ERR_ARG, "NULL output array");
+    if (r->total >= (1ull << 32)) fail(SJ_ERR_ARG, "CSR of >= 2^32 pairs is not supported");
+    SJ_CUDA(cudaSetDevice(r->device));
+    CtxGuard cg{acquire_ctx(r->device, 1, 0, 64)};
+    cudaStream_t s = cg.c->streams[0];
+    const uint64_t n = r->total;
+    const int nsm = device_sm_count(r->device);
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)nsm * 8));
+    Scratch<uint64_t> all(n ? n : 1, s);
+    uint64_t off = 0;
+    for (const auto &b : r->batches) {
+        if (!b.n) continue;
+        SJ_CUDA(cudaMemcpyAsync(all.p + off, b.pairs, b.n * sizeof(uint64_t),
+                                b.on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+        off += b.n;
+    }
+    sort_pairs_device(all.p, n, n_points, s);
+    Scratch<uint32_t> counts(n_points + 1, s), offs(n_points + 1, s);
+    SJ_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(uint32_t) * (n_points + 1), s));
+    if (n) {
+        k_csr_hist<<<grid, 256, 0, s>>>(all.p, n, counts.p);
+        SJ_LAUNCHED();
+    }
+    exclusive_scan_u32(counts.p, offs.p, n_points + 1, s);
+    const unsigned gridN =
+        (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_points + 256) / 256, (uint64_t)nsm * 8));
+    k_widen_u32<<<gridN, 256, 0, s>>>(offs.p, n_points + 1, row_offsets);
+    SJ_LAUNCHED();
+    if (n) {
+        k_csr_values<<<grid, 256, 0, s>>>(all.p, n, neighbors);
+        SJ_LAUNCHED();
+    }
+    SJ_CUDA(cudaStreamSynchronize(s));
+}
+
 // ------------------------------------------------------------------ f3: brute force
 namespace {
 constexpr int kBfThreads = 256;

@@ -403,23 +403,37 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 for (size_t b = (nb > (size_t)S ? nb - S : 0); b < nb; ++b) counts[b] = hslots[b % S].cursor;
             }
             for (size_t b = 0; b < nb; ++b) counts[b] += nself_of(cuts[b], cuts[b + 1]);
+            // overflowed batches (estimate too low): exact re-allocation, all re-runs launched
+            // together across the streams (slots 0..S-1 are free again), one sync for the round
+            std::vector<size_t> redo;
+            for (size_t b = 0; b < nb; ++b)
+                if (counts[b] > res->batches[b].cap) redo.push_back(b);
+            for (size_t r0 = 0; r0 < redo.size(); r0 += (size_t)S) {
+                const size_t r1 = std::min(redo.size(), r0 + (size_t)S);
+                for (size_t r = r0; r < r1; ++r) {
+                    const size_t b = redo[r];
+                    const int si = (int)(r - r0);
+                    cudaStream_t st = cx.streams[si];
+                    sj_batch &bt = res->batches[b];
+                    dev_free(bt.pairs, st);
+                    bt.pairs = dalloc<uint64_t>(counts[b], st);
+                    bt.cap = counts[b];
+                    run_batch(cuts[b], cuts[b + 1], bt.pairs, bt.cap, dslots + si, st, true);
+                    SJ_CUDA(cudaMemcpyAsync(hslots + si, dslots + si, sizeof(Slot), cudaMemcpyDeviceToHost, st));
+                    ++stats.retries;
+                }
+                for (size_t r = r0; r < r1; ++r) SJ_CUDA(cudaStreamSynchronize(cx.streams[r - r0]));
+                for (size_t r = r0; r < r1; ++r) {
+                    const size_t b = redo[r];
+                    const uint64_t n = hslots[r - r0].cursor + nself_of(cuts[b], cuts[b + 1]);
+                    if (n != counts[b]) fail(SJ_ERR_CUDA, "batch re-run produced a different count");
+                }
+            }
             for (size_t b = 0; b < nb; ++b) {
                 sj_batch &bt = res->batches[b];
-                uint64_t n = counts[b];
-                if (n > bt.cap) {  // overflow: exact re-allocation and re-run
-                    dev_free(bt.pairs, s0);
-                    bt.pairs = dalloc<uint64_t>(n, s0);
-                    bt.cap = n;
-                    run_batch(cuts[b], cuts[b + 1], bt.pairs, n, dslots, s0, true);
-                    SJ_CUDA(cudaMemcpyAsync(hslots, dslots, sizeof(Slot), cudaMemcpyDeviceToHost, s0));
-                    SJ_CUDA(cudaStreamSynchronize(s0));
-                    ++stats.retries;
-                    n = hslots[0].cursor + nself_of(cuts[b], cuts[b + 1]);
-                    if (n > bt.cap) fail(SJ_ERR_CUDA, "batch re-run overflowed");
-                }
-                bt.n = n;
-                res->total += n;
-                if (o.sort_pairs) sort_pairs_device(bt.pairs, n, ix.n, st_sort);
+                bt.n = counts[b];
+                res->total += bt.n;
+                if (o.sort_pairs) sort_pairs_device(bt.pairs, bt.n, ix.n, st_sort);
             }
             tr.mark("batch loop");
         } else {

@@ -244,6 +244,7 @@ void inclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStrea
 
 // extras.cu
 void sort_pairs_device(uint64_t *pairs, uint64_t n, uint64_t n_points, cudaStream_t s);
+void result_to_csr_impl(const sj_result *r, uint64_t n_points, uint64_t *row_offsets, uint32_t *neighbors);
 sj_result *brute_force_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &bo,
                             const sj_join_opts &jo);
 

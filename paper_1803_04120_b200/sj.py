@@ -98,6 +98,8 @@ def load_library(path: str = LIB_PATH):
     L.sj_result_batch.restype = i32
     L.sj_result_copy_to_host.argtypes = [vp, vp, u64]
     L.sj_result_copy_to_host.restype = i32
+    L.sj_result_to_csr.argtypes = [vp, u64, vp, vp]
+    L.sj_result_to_csr.restype = i32
     L.sj_neighbor_counts.argtypes = [vp, P(JoinOpts), vp, P(u64)]
     L.sj_neighbor_counts.restype = i32
     L.sj_brute_force_join.argtypes = [vp, u64, i32, dbl, P(BuildOpts), P(JoinOpts), P(vp)]
@@ -330,6 +332,17 @@ class Result:
         if sort:
             out.sort()
         return out
+
+    def to_csr(self, n_points: int):
+        """sj_result_to_csr -> (row_offsets int64[n_points+1], neighbors int32[n_pairs]) on the device;
+        neighbours of point i (original ids) are neighbors[row_offsets[i]:row_offsets[i+1]], ascending."""
+        import torch
+        dev = f"cuda:{self.device if self.device is not None else 0}"
+        offsets = torch.empty(n_points + 1, dtype=torch.int64, device=dev)
+        nbrs = torch.empty(max(self.n_pairs, 1), dtype=torch.int32, device=dev)
+        _check(load_library().sj_result_to_csr(self._h, n_points, ctypes.c_void_p(offsets.data_ptr()),
+                                               ctypes.c_void_p(nbrs.data_ptr())))
+        return offsets, nbrs[:self.n_pairs]
 
     def free(self):
         if self._h and self._h.value:

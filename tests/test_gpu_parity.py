@@ -472,3 +472,20 @@ def test_prefix_bucket_sort_big_buckets(sj, m):
     assert np.array_equal(arr["X"].cpu().numpy(), pts[ref.A].T)
     got = sj.self_join(idx).to_numpy(sort=True)
     assert np.array_equal(got, oracle.brute_force(pts, eps))
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_csr_output(sj, host):
+    """f2 CSR neighbour lists (4 B/pair + offsets) equal the oracle's pairs grouped by key, rows
+    ascending -- across several batches, device- and host-resident."""
+    n, d, eps = 4000, 3, 6.0
+    pts = datagen.uniform(n, d, seed=31)
+    want = oracle.brute_force(pts, eps)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    res = sj.self_join(idx, result_on_host=host, min_batches=5)
+    assert res.n_batches >= 5
+    offsets, nbrs = res.to_csr(n)
+    keys = (want >> np.uint64(32)).astype(np.int64)
+    want_off = np.concatenate([[0], np.cumsum(np.bincount(keys, minlength=n))])
+    assert np.array_equal(offsets.cpu().numpy(), want_off)
+    assert np.array_equal(nbrs.cpu().numpy().astype(np.uint32), (want & np.uint64(0xFFFFFFFF)).astype(np.uint32))
