@@ -276,7 +276,8 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
             prefix += c * s_pstr[j];
             if (use_masks) {
                 const uint64_t bit = s_moff[j] + c;
-                atomicOr(s_mask + (bit >> 5), 1u << (bit & 31));
+                const uint32_t m = 1u << (bit & 31);
+                if (!(s_mask[bit >> 5] & m)) atomicOr(s_mask + (bit >> 5), m);   // (set already: skip the atomic)
             }
         }
         keys[i] = key;
@@ -286,7 +287,7 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
     if (use_masks) {
         __syncthreads();
         for (uint32_t w2 = threadIdx.x; w2 < mask_words; w2 += blockDim.x)
-            if (s_mask[w2]) atomicOr(masks + w2, s_mask[w2]);
+            if (s_mask[w2] && (__ldcg(masks + w2) & s_mask[w2]) != s_mask[w2]) atomicOr(masks + w2, s_mask[w2]);
     }
 }
 
