@@ -577,6 +577,11 @@ void apply_dir_geometry(DevIndex &ix, const sj_index_view &v, const DirPlan &dp)
     ix.occ_div = dp.occ ? dp.occ_div : 0;
     ix.occ_cpd = dp.occ ? dp.occ_cpd : 0;
     ix.occ2_cpd = dp.occ2 ? dp.occ2_cpd : 0;
+    for (int j = 0; j < SJ_MAX_DIM; ++j) {
+        const bool top = j < d && j >= d - dp.k;
+        ix.occ_mul[j] = top ? ix.pstride[j] * ix.occ_cpd : (dp.occ && j == d - dp.k - 1 ? 1 : 0);
+        ix.occ2_mul[j] = top ? ix.pstride[j] * ix.occ2_cpd : (dp.occ2 && j == d - dp.k - 2 ? 1 : 0);
+    }
     // key -> coordinates by double reciprocals when every quotient < 2^50 and keys < 2^63
     bool fast = v.key_bits <= 63;
     for (int j = 1; j < d; ++j) fast = fast && v.cpd[j] < (1ull << 50);

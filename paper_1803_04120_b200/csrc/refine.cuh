@@ -353,27 +353,28 @@ __device__ __forceinline__ void search_cell_scan_sparse(const DevIndex &ix, cons
     uint64_t ph = 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) ph += q.c[j] * ix.pstride[j];
-    uint64_t cl = q.c[0];
+    // bitmap indices as sums with static per-dimension multipliers (a runtime-selected q.c[L-1]
+    // made the compiler keep q in local memory)
+    uint64_t qc = 0, qc2 = 0;
 #pragma unroll
-    for (int i = 1; i < D; ++i) if (i == L - 1) cl = q.c[i];
-    const uint64_t qc = ph * ix.occ_cpd + cl;
-    uint64_t cl2 = q.c[0];
-#pragma unroll
-    for (int i = 1; i < D; ++i) if (i == L - 2) cl2 = q.c[i];
-    const uint64_t qc2 = ph * ix.occ2_cpd + cl2;
+    for (int j = 0; j < D; ++j) {
+        qc += q.c[j] * ix.occ_mul[j];
+        qc2 += q.c[j] * ix.occ2_mul[j];
+    }
     const int64_t Rl = ix.lowR[L];
-    constexpr uint32_t kPow3[4] = {1, 3, 9, 27};
+    const uint32_t pow3k = k == 3 ? 27u : (k == 2 ? 9u : 3u);
 #pragma unroll 1
     for (int jt = k - 1; jt >= 0; --jt) {
         __syncwarp(wmask);
         if (UNICOMP && !((q.odd >> (L + jt)) & 1u)) continue;
-        const uint32_t nb = 2u * kPow3[jt];
-        const uint32_t tbase = (kPow3[k] - kPow3[jt + 1]) / 2u;   // digits above jt = "0 move"
+        const uint32_t p3 = jt == 2 ? 9u : (jt == 1 ? 3u : 1u);     // 3^jt
+        const uint32_t nb = 2u * p3;
+        const uint32_t tbase = (pow3k - 3u * p3) / 2u;               // digits above jt = "0 move"
         uint32_t live = 0;
 #pragma unroll
         for (uint32_t i = 0; i < 18u; ++i) {
             if (i < nb) {
-                const uint32_t t = tbase + (i >> 1) + ((i & 1u) ? 2u * kPow3[jt] : 0u);
+                const uint32_t t = tbase + (i >> 1) + ((i & 1u) ? 2u * p3 : 0u);
                 if (!(tt.bits[t] & bad)) {
                     // both bitmaps' loads are issued together (no dependent second round)
                     const uint64_t qb = qc + (uint64_t)tt.dq[t];
@@ -391,7 +392,7 @@ __device__ __forceinline__ void search_cell_scan_sparse(const DevIndex &ix, cons
         while (live) {
             const uint32_t i = __ffs(live) - 1;
             live &= live - 1u;
-            const uint32_t t = tbase + (i >> 1) + ((i & 1u) ? 2u * kPow3[jt] : 0u);
+            const uint32_t t = tbase + (i >> 1) + ((i & 1u) ? 2u * p3 : 0u);
             const uint64_t p = ph + (uint64_t)tt.dp[t];
             ++q.probes;
             const uint32_t lo = __ldg(ix.dir + p), hi = __ldg(ix.dir + p + 1);
@@ -444,14 +445,12 @@ __device__ __forceinline__ void search_cell_scan(const DevIndex &ix, const JoinA
     // serialise -- measured 2.4 of 32 lanes active on 6-D eps=8.
     // Offsets are taken in chunks of kChunk: phase 1 (unrolled) issues the occupancy-bitmap loads
     // of the whole chunk together (memory-level parallelism), phase 2 scans the survivors.
-    uint64_t cl = q.c[0];
+    uint64_t qh = 0, qh2 = 0;                    // bitmap indices of the home top-(k+1) prefixes
 #pragma unroll
-    for (int i = 1; i < D; ++i) if (i == L - 1) cl = q.c[i];
-    const uint64_t qh = ph * ix.occ_cpd + cl;   // bitmap index of the home top-(k+1) prefix
-    uint64_t cl2 = q.c[0];
-#pragma unroll
-    for (int i = 1; i < D; ++i) if (i == L - 2) cl2 = q.c[i];
-    const uint64_t qh2 = ph * ix.occ2_cpd + cl2;
+    for (int j = 0; j < D; ++j) {
+        qh += q.c[j] * ix.occ_mul[j];
+        qh2 += q.c[j] * ix.occ2_mul[j];
+    }
 #ifndef SJ_CHUNK
 #define SJ_CHUNK 27
 #endif

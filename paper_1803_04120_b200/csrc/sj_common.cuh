@@ -113,6 +113,8 @@ struct DevIndex {
     // survivors of the first (both stored dilated by +-1 along their low dimension)
     const uint32_t *occ2;
     uint64_t occ2_cpd;           // |g_{d-k-2}|
+    uint64_t occ_mul[SJ_MAX_DIM];   // bitmap index = sum_j c_j * occ_mul[j]: pstride_j * |g_{d-k-1}| for top
+    uint64_t occ2_mul[SJ_MAX_DIM];  // dims, 1 for dim d-k-1 (occ) / d-k-2 (occ2), else 0
     // per non-empty cell, precomputed at build time: packed coordinates (c_j at bit cshift[j],
     // width cbits[j]; nullptr when sum of widths > 64) and the Alg. 1 line-6 mask word (bit i: move
     // -1 in dim i leaves M_i; bit 8+i: move +1 leaves M_i)
