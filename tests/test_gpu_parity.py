@@ -489,3 +489,17 @@ def test_csr_output(sj, host):
     want_off = np.concatenate([[0], np.cumsum(np.bincount(keys, minlength=n))])
     assert np.array_equal(offsets.cpu().numpy(), want_off)
     assert np.array_equal(nbrs.cpu().numpy().astype(np.uint32), (want & np.uint64(0xFFFFFFFF)).astype(np.uint32))
+
+
+def test_lazy_timings_and_stats(sj):
+    """Build/join device timings are computed on request from pooled CUDA events
+    (sj_index_timings, sj_result_info with stats): positive and consistent with the work done."""
+    pts = datagen.uniform(200000, 4, seed=5)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), 2.0)
+    res = sj.self_join(idx)
+    t = idx.timings()
+    assert t["total_ms"] > 0 and t["total_ms"] >= t["sort_ms"] >= 0
+    st = res.stats
+    assert st["refine_ms"] > 0 and st["refine_span_ms"] > 0 and st["refine_max_ms"] <= st["refine_ms"] + 1e-6
+    assert st["estimate_ms"] > 0 and st["batches"] == res.n_batches >= 3
+    assert st["pairs"] == res.n_pairs and st["candidates_tested"] >= res.n_pairs // 2
