@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SJ_ABI_VERSION 1
+#define SJ_ABI_VERSION 2
 #define SJ_MAX_DIM 6
 
 typedef enum {
@@ -62,6 +62,10 @@ typedef struct {
     void *stream;          /* cudaStream_t to order the build on (NULL = library stream); the call
                               returns after the build completed                                   */
     int build_masks;       /* 1 (default): build the per-dimension masks M_j       */
+    int speculative_estimate; /* 1 (default): run the a5 result-size estimate of the DEFAULT join
+                              (full range, unicomp, self pairs, masks) on the device before the
+                              build's final sync; sj_self_join with those options then skips its
+                              own estimate launch and host round trip (same sample, same counts) */
 } sj_build_opts;
 
 typedef struct {

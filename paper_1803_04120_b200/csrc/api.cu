@@ -180,6 +180,7 @@ void sj_build_opts_default(sj_build_opts *o)
     o->points_on_device = 0;
     o->stream = nullptr;
     o->build_masks = 1;
+    o->speculative_estimate = 1;
 }
 
 void sj_join_opts_default(sj_join_opts *o)

@@ -103,6 +103,8 @@ __device__ __forceinline__ double ord_to_double(unsigned long long k)
 constexpr int kSmemMaskWords = 2048;   // 64 K bits, 8 KB of shared memory
 // context slot layout of the build: min/max partials (<= 4 * SMs blocks), then the DevGeom
 constexpr size_t kGeomOffset = 4 * 256 * (2 * SJ_MAX_DIM + 1) * sizeof(unsigned long long);
+constexpr size_t kEstOffset = kGeomOffset + 4096;          // speculative estimate buckets (<= 1100)
+constexpr size_t kBuildSlotBytes = kEstOffset + 8 * 1100;
 
 __device__ __noinline__ void geometry_products(const uint64_t *cpd, int d, uint32_t n, int allow_bucket,
                                                int want_masks, DevGeom &G);
@@ -396,7 +398,10 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
             }
         }
     }
-    if (k == n - 1) G[h + 1] = n;
+    if (k == n - 1) {
+        G[h + 1] = n;
+        if (h + 1 < n) B[h + 1] = 1ull << 63;   // sentinel (keys < 2^62 when the build estimates)
+    }
     const double *src = pts + (uint64_t)a * D;
     if (D % 2 == 0 && (reinterpret_cast<uintptr_t>(pts) & 15u) == 0) {   // 16-B aligned rows: vector loads
 #pragma unroll
@@ -762,7 +767,8 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
     HostTrace tr("build");
     // the build runs on the caller's stream, or on a pooled library stream; the pooled context also
     // lends its pinned slot memory and an event (device geometry read-back)
-    CtxGuard cg{acquire_ctx(o.device, 1, 1, kGeomOffset + sizeof(DevGeom))};
+    static_assert(sizeof(DevGeom) <= 4096, "DevGeom fits its slot");
+    CtxGuard cg{acquire_ctx(o.device, 1, 1, kBuildSlotBytes)};
     cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : cg.c->streams[0];
 
     const uint32_t N = (uint32_t)n;
@@ -1044,7 +1050,41 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ix.X = X;
         idx->view = v;
         idx->dev = ix;
-        finish_aux(idx, s, aux, dp, dirhist.p, false, h_aux);   // the build's late host sync
+        // LSD path: the directory from its histogram (the bucket path scanned it before compaction)
+        if (dirhist.p) exclusive_scan_u32(dirhist.p, dir, (uint64_t)dp.P + 1, s);
+        // a5 for the default join, speculatively, before the final sync: the provisional index
+        // bounds cell ranges by N (B carries a sentinel after the last cell) and chooses the search
+        // mode from N; the result is kept only if the mode from |G| is the same
+        const double pavg = (double)n / (double)dp.P;
+        const int prov_mode = dp.k == d ? kSearchDenseRows
+                              : (pavg <= 8.0 && (double)dp.div < 4.0e15 ? kSearchCellScan : kSearchRows);
+        const bool spec = v.key_bits <= 62 && o.speculative_estimate;
+        EstimateShape es_spec;
+        unsigned long long *hbk =
+            reinterpret_cast<unsigned long long *>(static_cast<char *>(cg.c->h_slots) + kEstOffset);
+        if (spec) {
+            DevIndex px = ix;
+            px.search_mode = prov_mode;
+            px.dense_T = 0;
+            px.dense_tasks = nullptr;
+            px.n_dense_tasks = 0;
+            es_spec = estimate_shape(n);
+            if (es_spec.nbk > 1100) fail(SJ_ERR_CUDA, "estimate bucket count out of range (internal error)");
+            unsigned long long *dbk =
+                reinterpret_cast<unsigned long long *>(static_cast<char *>(cg.c->d_slots) + kEstOffset);
+            SJ_CUDA(cudaMemsetAsync(dbk, 0, 8 * es_spec.nbk, s));
+            sj_join_opts jo;
+            sj_join_opts_default(&jo);
+            launch_estimate(px, o.device, jo, 0, n, es_spec, dbk, s);
+            SJ_CUDA(cudaMemcpyAsync(hbk, dbk, 8 * es_spec.nbk, cudaMemcpyDeviceToHost, s));
+            tr.dev("speculative estimate", s);
+        }
+        finish_aux(idx, s, aux, dp, nullptr, false, h_aux);   // the build's late host sync
+        if (spec && !h_aux[3] && idx->dev.search_mode == prov_mode) {
+            idx->spec_est_valid = true;
+            idx->spec_shape = es_spec;
+            idx->spec_buckets.assign(hbk, hbk + es_spec.nbk);
+        }
         ev.rec(6, s);
         tr.dev("finish", s);
         tr.mark("compact+dir+dense (synced)");

@@ -242,6 +242,53 @@ JoinArgs base_args(const sj_index *idx, const sj_join_opts &o, unsigned long lon
 
 }  // namespace
 
+EstimateShape estimate_shape(uint64_t nq)
+{
+    const Sample sm = make_sample(nq);
+    EstimateShape es;
+    es.step = sm.step;
+    es.ns = sm.ns;
+    es.group = 32 * std::max<uint64_t>(1, (sm.ns / 32 + 1023) / 1024);   // whole runs per bucket
+    es.nbk = sm.ns ? (sm.ns + es.group - 1) / es.group : 0;
+    return es;
+}
+
+// a5: count-only refine over the strided sample of [q0, q1), summed per planning bucket into dbk
+// (zeroed by the caller).  A small sample is one partial wave of long per-query chains: each query
+// is spread over more lanes (the counts do not depend on the lane split) until the GPU is covered.
+void launch_estimate(const DevIndex &ix, int device, const sj_join_opts &o, uint64_t q0, uint64_t q1,
+                     const EstimateShape &es, unsigned long long *dbk, cudaStream_t s)
+{
+    if (!es.ns) return;
+    JoinArgs ja{};
+    ja.include_self = o.include_self;
+    ja.use_masks = o.use_masks;
+    ja.lanes_log2 = lanes_log2_for(ix, o);
+    ja.q0 = (uint32_t)q0;
+    ja.q1 = (uint32_t)q1;
+    ja.step = (uint32_t)es.step;
+    ja.nsamples = (uint32_t)es.ns;
+    ja.qbucket = dbk;
+    ja.group = (uint32_t)es.group;
+#ifndef SJ_EST_LANES_MAX
+#define SJ_EST_LANES_MAX 3
+#endif
+    if (o.lanes_per_query == 0) {
+        const int nsm = device_sm_count(device);
+        while (ja.lanes_log2 < SJ_EST_LANES_MAX && (es.ns << (ja.lanes_log2 + 1)) <= (uint64_t)nsm * 1024)
+            ++ja.lanes_log2;
+    }
+    launch_refine<kCountQuery>(ix, ja, o.unicomp != 0, (uint32_t)es.ns, s);
+}
+
+// The build's speculative estimate is valid for a join with the default predicate options over
+// the full query range (sj_join_opts_default: unicomp, self pairs, masks, automatic lanes).
+static bool spec_estimate_applies(const sj_index *idx, const sj_join_opts &o, uint64_t q0, uint64_t q1)
+{
+    return idx->spec_est_valid && o.unicomp == 1 && o.include_self == 1 && o.use_masks == 1 &&
+           o.lanes_per_query == 0 && q0 == 0 && q1 == idx->view.n;
+}
+
 sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
 {
     uint64_t q0, q1;
@@ -256,9 +303,9 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     struct Slot { unsigned long long cursor; uint32_t overflow; uint32_t pad; };
     constexpr size_t kWorkBytes = sizeof(unsigned long long) * 4 * kWorkSlots;   // work counter slots
     const uint64_t nq = q1 - q0;
-    const Sample sm = make_sample(nq);
-    const uint64_t group = 32 * std::max<uint64_t>(1, (sm.ns / 32 + 1023) / 1024);  // whole runs per bucket
-    const uint64_t nbk = sm.ns ? (sm.ns + group - 1) / group : 0;
+    const bool spec = spec_estimate_applies(idx, o, q0, q1);   // estimate already done by the build
+    const EstimateShape es = spec ? idx->spec_shape : estimate_shape(nq);
+    const uint64_t nbk = es.nbk;
     const size_t kSlotsBytes = sizeof(Slot) * 64;
     const size_t slot_need = kWorkBytes + kSlotsBytes + 8 * (size_t)(nbk + 1);
     CtxGuard cg{acquire_ctx(idx->device, S, S + 2, slot_need)};
@@ -281,29 +328,15 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         // work counters, the 64 batch slots and the planning buckets are contiguous: one memset
         SJ_CUDA(cudaMemsetAsync(work, 0, kWorkBytes + kSlotsBytes + 8 * nbk, s0));
         // ---- a5: estimate on a strided sample (count-only refine), summed per planning bucket
-        if (sm.ns) {
+        // (an index built for the default join already carries it: no launch, no round trip)
+        if (spec) {
+            std::copy(idx->spec_buckets.begin(), idx->spec_buckets.end(), hbk);
+        } else if (es.ns) {
             res->est_ev[0] = event_get(idx->device);
             res->est_ev[1] = event_get(idx->device);
-            JoinArgs ja = base_args(idx, o, nullptr);
-            ja.q0 = (uint32_t)q0;
-            ja.q1 = (uint32_t)q1;
-            ja.step = (uint32_t)sm.step;
-            ja.nsamples = (uint32_t)sm.ns;
-            ja.qbucket = dbk;
-            ja.group = (uint32_t)group;
-            // a small sample is one partial wave of long per-query chains: spread each query over
-            // more lanes (the counts do not depend on the lane split) until the GPU is covered
-#ifndef SJ_EST_LANES_MAX
-#define SJ_EST_LANES_MAX 3
-#endif
-            if (o.lanes_per_query == 0) {
-                const int nsm = device_sm_count(idx->device);
-                while (ja.lanes_log2 < SJ_EST_LANES_MAX && (sm.ns << (ja.lanes_log2 + 1)) <= (uint64_t)nsm * 1024)
-                    ++ja.lanes_log2;
-            }
             tr.dev("start", s0);
             SJ_CUDA(cudaEventRecord(res->est_ev[0], s0));
-            launch_refine<kCountQuery>(ix, ja, o.unicomp != 0, (uint32_t)sm.ns, s0);
+            launch_estimate(ix, idx->device, o, q0, q1, es, dbk, s0);
             tr.dev("estimate", s0);
             SJ_CUDA(cudaEventRecord(res->est_ev[1], s0));
             SJ_CUDA(cudaMemcpyAsync(hbk, dbk, nbk * 8, cudaMemcpyDeviceToHost, s0));
@@ -316,8 +349,8 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         uint64_t est_total = 0;
         {
             std::vector<double> be(nbk);
-            for (uint64_t i = 0; i < nbk; ++i) be[i] = (double)hbk[i] * (double)sm.step;
-            plan_from_buckets(be.data(), nbk, sm.step * group, q0, q1, o.batch_capacity_pairs, o.min_batches, 0.25,
+            for (uint64_t i = 0; i < nbk; ++i) be[i] = (double)hbk[i] * (double)es.step;
+            plan_from_buckets(be.data(), nbk, es.step * es.group, q0, q1, o.batch_capacity_pairs, o.min_batches, 0.25,
                               cuts, est, &est_total);
         }
         stats.estimated_pairs = est_total;

@@ -133,6 +133,11 @@ struct DevIndex {
 
 enum SearchMode { kSearchDenseRows = 0, kSearchCellScan = 1, kSearchRows = 2 };
 
+// shape of the a5 sample: sample slots (runs of 32 queries every 32*step), buckets of `group` slots
+struct EstimateShape {
+    uint64_t step = 1, ns = 0, group = 32, nbk = 0;
+};
+
 // Cell coordinates from a linear id: c_j = (key / stride_j) mod |g_j|, taken from the slowest
 // dimension down (each quotient < |g_j|).  Fast path: the quotient from a double reciprocal,
 // corrected by +-1 in exact integer arithmetic (valid while quotients < 2^50 and keys < 2^63, which
@@ -168,6 +173,11 @@ struct sj_index {
     // (sj_index_timings), so the build itself never waits on event queries
     cudaEvent_t tev[7] = {nullptr};
     bool timed = false;
+    // the a5 estimate for the default join (full range, unicomp, self pairs, masks), run by the
+    // build on the device before its final sync (join.cu spec_estimate_applies)
+    bool spec_est_valid = false;
+    sj::EstimateShape spec_shape{};
+    std::vector<unsigned long long> spec_buckets;
     sj_index_view view{};        // geometry + device pointers (exported as is)
     sj::DevIndex dev{};          // same, in kernel form
     void *bufs[16] = {nullptr};  // owned device allocations
@@ -253,6 +263,9 @@ sj_result *brute_force_impl(const double *points, uint64_t n, int d, double eps,
 // join.cu
 sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o);
 void neighbor_counts_impl(const sj_index *idx, const sj_join_opts &o, uint32_t *cnt, uint64_t *total);
+EstimateShape estimate_shape(uint64_t nq);
+void launch_estimate(const DevIndex &ix, int device, const sj_join_opts &o, uint64_t q0, uint64_t q1,
+                     const EstimateShape &es, unsigned long long *dbk, cudaStream_t s);
 void plan_from_buckets(const double *bucket_est, uint64_t nbk, uint64_t width, uint64_t q0, uint64_t q1,
                        uint64_t capacity, int min_batches, double margin, std::vector<uint64_t> &cuts,
                        std::vector<uint64_t> &est, uint64_t *estimated_total);

@@ -28,7 +28,8 @@ u64, u32, i32, dbl, f32, vp = (ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, c
 
 
 class BuildOpts(ctypes.Structure):
-    _fields_ = [("device", i32), ("points_on_device", i32), ("stream", vp), ("build_masks", i32)]
+    _fields_ = [("device", i32), ("points_on_device", i32), ("stream", vp), ("build_masks", i32),
+                ("speculative_estimate", i32)]
 
 
 class JoinOpts(ctypes.Structure):
@@ -242,12 +243,14 @@ def _device_tensor(ptr, shape, dtype, device, owner):
     return t
 
 
-def build_index(points, eps: float, device: Optional[int] = None, stream=None, build_masks: bool = True) -> Index:
+def build_index(points, eps: float, device: Optional[int] = None, stream=None, build_masks: bool = True,
+                speculative_estimate: bool = True) -> Index:
     """sj_build_index.  points: N x d float64 (torch cuda/cpu tensor or numpy array)."""
     L = load_library()
     o = BuildOpts()
     L.sj_build_opts_default(ctypes.byref(o))
     o.build_masks = int(build_masks)
+    o.speculative_estimate = int(speculative_estimate)
     keep = None
     try:
         import torch

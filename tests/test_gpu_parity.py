@@ -495,7 +495,7 @@ def test_lazy_timings_and_stats(sj):
     """Build/join device timings are computed on request from pooled CUDA events
     (sj_index_timings, sj_result_info with stats): positive and consistent with the work done."""
     pts = datagen.uniform(200000, 4, seed=5)
-    idx = sj.build_index(torch.from_numpy(pts).cuda(), 2.0)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), 2.0, speculative_estimate=False)
     res = sj.self_join(idx)
     t = idx.timings()
     assert t["total_ms"] > 0 and t["total_ms"] >= t["sort_ms"] >= 0
@@ -504,3 +504,17 @@ def test_lazy_timings_and_stats(sj):
     assert st["estimate_ms"] > 0 and st["batches"] == res.n_batches >= 3
     # unicomp: every accepted test emits both orientations, self pairs need no test
     assert st["pairs"] == res.n_pairs and 2 * st["candidates_tested"] + len(pts) >= res.n_pairs
+
+
+@pytest.mark.parametrize("d,n,eps", [(6, 300000, 1.0), (5, 200000, 1.5), (4, 200000, 3.0), (3, 200000, 2.0),
+                                     (2, 100000, 0.3)])
+def test_build_time_estimate_is_the_join_estimate(sj, d, n, eps):
+    """The default join's a5 estimate run by the build (before its final sync) equals the join's own
+    estimate (same deterministic sample): same estimated_pairs, same batch plan, same pairs.  Covers
+    both sort paths (prefix buckets, LSD) and all three search modes."""
+    pts = torch.from_numpy(datagen.uniform(n, d, seed=9 + d)).cuda()
+    a = sj.self_join(sj.build_index(pts, eps, speculative_estimate=True))
+    b = sj.self_join(sj.build_index(pts, eps, speculative_estimate=False))
+    assert a.stats["estimated_pairs"] == b.stats["estimated_pairs"] and a.n_batches == b.n_batches
+    assert a.n_pairs == b.n_pairs
+    assert b.stats["estimate_ms"] > 0
