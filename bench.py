@@ -296,7 +296,7 @@ def run_ours(args):
     alg_bytes = n_local * (8 * args.d + 16) + cands * (8 * args.d + 4) + (pairs / world) * 8
     achieved = alg_bytes / (span_ms / 1000.0) / 1e9
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01_refine_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r01d_refine_traffic.json")
     if args.d == 6 and args.eps == 1.0 and args.n == 2_000_000 and os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f)["dram_bytes_per_step"]      # ncu --set full, same workload
