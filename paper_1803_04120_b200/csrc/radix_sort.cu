@@ -155,22 +155,6 @@ k_scan_reduce(const uint32_t *__restrict__ in, uint64_t n, uint32_t *__restrict_
     if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
 }
 
-// single CTA: exclusive scan of block sums in place
-__global__ void __launch_bounds__(kScanThreads)
-k_scan_sums(uint32_t *__restrict__ sums, uint64_t m)
-{
-    __shared__ uint32_t s_warp[32];
-    uint32_t carry = 0;
-    for (uint64_t base = 0; base < m; base += kScanThreads) {
-        uint64_t i = base + threadIdx.x;
-        uint32_t v = (i < m) ? sums[i] : 0;
-        uint32_t tot;
-        uint32_t ex = block_exclusive_scan(v, s_warp, &tot);
-        if (i < m) sums[i] = carry + ex;
-        carry += tot;
-    }
-}
-
 template <bool INCLUSIVE>
 __global__ void __launch_bounds__(kScanThreads)
 k_scan_apply(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, uint64_t n,
@@ -187,7 +171,18 @@ k_scan_apply(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, uint64
         v[r] = (i < n) ? in[i] : 0;
         acc += v[r];
     }
-    uint32_t run = block_off[blockIdx.x] + block_exclusive_scan(acc, s_warp, nullptr);
+    // this block's offset = sum of the preceding blocks' totals (<= a few thousand: every block
+    // reduces them itself, so no separate kernel scans the block sums)
+    uint32_t pre = 0;
+    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) pre += block_off[b];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    __shared__ uint32_t s_pre[kScanThreads / 32];
+    if ((threadIdx.x & 31) == 0) s_pre[threadIdx.x >> 5] = pre;
+    __syncthreads();
+    uint32_t off = 0;
+    for (int w = 0; w < kScanThreads / 32; ++w) off += s_pre[w];
+    uint32_t run = off + block_exclusive_scan(acc, s_warp, nullptr);
 #pragma unroll
     for (int r = 0; r < kScanItems; ++r) {
         uint64_t i = base + r;
@@ -207,8 +202,6 @@ void scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, bool inclusive, cud
     const uint64_t nb = (n + kScanTile - 1) / kScanTile;
     Scratch<uint32_t> sums(nb, s);
     k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, sums.p);
-    SJ_LAUNCHED();
-    k_scan_sums<<<1, kScanThreads, 0, s>>>(sums.p, nb);
     SJ_LAUNCHED();
     if (inclusive)
         k_scan_apply<true><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, sums.p, out2);
