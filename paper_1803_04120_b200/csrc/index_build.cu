@@ -800,31 +800,6 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         }
         ev.rec(1, s);
 
-        // ---- a1: exact per-dimension min/max + finiteness (one kernel, integer atomics), then the
-        // geometry on the device (k_geometry) and the key pass right behind it; the host reads the
-        // geometry (one small D2H copy, waited on by an event) while the key pass runs.
-        const uint32_t parts =
-            (uint32_t)std::min<uint64_t>(std::min<uint64_t>((n + kThreads - 1) / kThreads, (uint64_t)nsm * 4), 1024);
-        // min/max partials and the device geometry live in the context's slot memory
-        unsigned long long *part = static_cast<unsigned long long *>(cg.c->d_slots);
-        DevGeom *dgeom = reinterpret_cast<DevGeom *>(static_cast<char *>(cg.c->d_slots) + kGeomOffset);
-        DevIndex ix{};
-        ix.d = d;
-        ix.n = N;
-        BuildArgs ba;
-        ba.pts = pts;
-        ba.n = N;
-        ba.mm = part;
-        launch(d, 0, dim3(parts), s, ix, ba);
-        tr.dev("minmax", s);
-        k_geometry<<<1, 256, 0, s>>>(part, parts, d, eps, N, allow_bucket ? 1 : 0, o.build_masks ? 1 : 0, dgeom);
-        SJ_LAUNCHED();
-        DevGeom *hgeom = static_cast<DevGeom *>(cg.c->h_slots);
-        SJ_CUDA(cudaMemcpyAsync(hgeom, dgeom, sizeof(DevGeom), cudaMemcpyDeviceToHost, s));
-        SJ_CUDA(cudaEventRecord(cg.c->events[0], s));
-        ev.rec(2, s);
-
-        tr.mark("minmax + geometry enqueued");
         // every N-sized array in two arenas (one owned by the index: A, pcell, B, G, X, cell
         // coordinates/masks, the small mask bitmap, aux; one scratch: keys, sort buffers, bucket
         // histogram sized for the largest possible prefix count)
@@ -873,6 +848,31 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         uint32_t *ids_tmp = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k);
         uint32_t *flags = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k + s_i);
         uint32_t *bhist = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k + 2 * s_i);
+        // ---- a1: exact per-dimension min/max + finiteness (one kernel, integer atomics), then the
+        // geometry on the device (k_geometry) and the key pass right behind it; the host reads the
+        // geometry (one small D2H copy, waited on by an event) while the key pass runs.
+        const uint32_t parts =
+            (uint32_t)std::min<uint64_t>(std::min<uint64_t>((n + kThreads - 1) / kThreads, (uint64_t)nsm * 4), 1024);
+        // min/max partials and the device geometry live in the context's slot memory
+        unsigned long long *part = static_cast<unsigned long long *>(cg.c->d_slots);
+        DevGeom *dgeom = reinterpret_cast<DevGeom *>(static_cast<char *>(cg.c->d_slots) + kGeomOffset);
+        DevIndex ix{};
+        ix.d = d;
+        ix.n = N;
+        BuildArgs ba;
+        ba.pts = pts;
+        ba.n = N;
+        ba.mm = part;
+        launch(d, 0, dim3(parts), s, ix, ba);
+        tr.dev("minmax", s);
+        k_geometry<<<1, 256, 0, s>>>(part, parts, d, eps, N, allow_bucket ? 1 : 0, o.build_masks ? 1 : 0, dgeom);
+        SJ_LAUNCHED();
+        DevGeom *hgeom = static_cast<DevGeom *>(cg.c->h_slots);
+        SJ_CUDA(cudaMemcpyAsync(hgeom, dgeom, sizeof(DevGeom), cudaMemcpyDeviceToHost, s));
+        SJ_CUDA(cudaEventRecord(cg.c->events[0], s));
+        ev.rec(2, s);
+
+        tr.mark("minmax + geometry enqueued");
         SJ_CUDA(cudaMemsetAsync(small_masks, 0, b_mk + 4 * sizeof(uint32_t), s));   // small masks + aux
         k_zero_prefix_hist<<<(unsigned)std::min<uint64_t>((hcap + kThreads) / kThreads, (uint64_t)nsm * 8), kThreads, 0,
                              s>>>(bhist, dgeom);
