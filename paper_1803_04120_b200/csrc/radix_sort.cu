@@ -287,9 +287,13 @@ constexpr uint32_t kBucketMax = 64;
 constexpr uint32_t kBigMax = 4096;          // 4096 x (8 + 4) B = 48 KB of shared memory
 constexpr int kBigThreads = 512;
 
+// Packed mode (idb > 0): the item travels as ONE 64-bit word (key - prefix*div) << idb | id -- within
+// a bucket the prefix is common, so u64 order == (key, id) order -- instead of a key and an id
+// written to two random places.
 __global__ void __launch_bounds__(256)
 k_bucket_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t n, uint64_t div,
-                 double inv, uint32_t *__restrict__ cursor, uint64_t *__restrict__ kout, uint32_t *__restrict__ vout)
+                 double inv, uint32_t *__restrict__ cursor, uint64_t *__restrict__ kout, uint32_t *__restrict__ vout,
+                 int idb)
 {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -298,8 +302,12 @@ k_bucket_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ 
     if (q * div > k) --q;
     else if ((q + 1) * div <= k) ++q;
     const uint32_t pos = atomicAdd(cursor + q, 1u);
-    kout[pos] = k;
-    vout[pos] = vin[i];
+    if (idb) {
+        kout[pos] = ((k - q * div) << idb) | vin[i];
+    } else {
+        kout[pos] = k;
+        vout[pos] = vin[i];
+    }
 }
 
 // big[0] = number of queued big buckets, big[1..] = their ids.
@@ -309,7 +317,7 @@ k_bucket_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ 
 __global__ void __launch_bounds__(256)
 k_bucket_sort(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, const uint32_t *__restrict__ start,
               uint64_t P, uint64_t *__restrict__ kout, uint32_t *__restrict__ vout, uint32_t *__restrict__ big,
-              uint32_t big_cap, uint32_t *__restrict__ local, uint32_t *__restrict__ cellcnt)
+              uint32_t big_cap, uint32_t *__restrict__ local, uint32_t *__restrict__ cellcnt, int idb, uint64_t div)
 {
     const uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= P) return;
@@ -319,6 +327,25 @@ k_bucket_sort(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin
         if (slot < big_cap) big[1 + slot] = (uint32_t)b;
         return;                                        // cellcnt[b] written by the big-bucket kernel
     }
+    if (idb) {
+        // packed items: insertion sort in place (u64 order), then unpack into the output range
+        uint64_t *w = const_cast<uint64_t *>(kin);
+        for (uint32_t i = s + 1; i < e; ++i) {
+            const uint64_t x = w[i];
+            uint32_t j = i;
+            while (j > s && w[j - 1] > x) {
+                w[j] = w[j - 1];
+                --j;
+            }
+            w[j] = x;
+        }
+        const uint64_t base = b * div, mask = (1ull << idb) - 1ull;
+        for (uint32_t i = s; i < e; ++i) {
+            const uint64_t x = w[i];
+            kout[i] = base + (x >> idb);
+            vout[i] = (uint32_t)(x & mask);
+        }
+    } else {
     // insertion sort by (key, id) directly in the output range (a few L1-resident entries)
     for (uint32_t i = s; i < e; ++i) {
         const uint64_t ki = kin[i];
@@ -334,6 +361,7 @@ k_bucket_sort(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin
         }
         kout[j] = ki;
         vout[j] = vi;
+    }
     }
     uint32_t c = 0;
     uint64_t prev = 0;
@@ -353,7 +381,7 @@ __global__ void __launch_bounds__(kBigThreads)
 k_bucket_sort_big(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin,
                   const uint32_t *__restrict__ start, const uint32_t *__restrict__ big, uint32_t big_cap,
                   uint64_t *__restrict__ kout, uint32_t *__restrict__ vout, uint32_t *__restrict__ overflow,
-                  uint32_t *__restrict__ local, uint32_t *__restrict__ cellcnt)
+                  uint32_t *__restrict__ local, uint32_t *__restrict__ cellcnt, int idb, uint64_t div)
 {
     extern __shared__ __align__(16) uint64_t s_big[];   // [kBigMax] keys, [kBigMax] ids, warp sums
     uint64_t *sk = s_big;
@@ -380,7 +408,7 @@ k_bucket_sort_big(const uint64_t *__restrict__ kin, const uint32_t *__restrict__
         __syncthreads();
         for (uint32_t i = threadIdx.x; i < m2; i += blockDim.x) {
             sk[i] = i < m ? kin[s + i] : ~0ull;
-            sv[i] = i < m ? vin[s + i] : ~0u;
+            sv[i] = (i < m && !idb) ? vin[s + i] : ~0u;          // packed: ids inside sk, sv constant
         }
         __syncthreads();
         for (uint32_t size = 2; size <= m2; size <<= 1) {
@@ -399,16 +427,24 @@ k_bucket_sort_big(const uint64_t *__restrict__ kin, const uint32_t *__restrict__
                 __syncthreads();
             }
         }
-        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-            kout[s + i] = sk[i];
-            vout[s + i] = sv[i];
+        if (idb) {
+            const uint64_t base = (uint64_t)b * div, mask = (1ull << idb) - 1ull;
+            for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+                kout[s + i] = base + (sk[i] >> idb);
+                vout[s + i] = (uint32_t)(sk[i] & mask);
+            }
+        } else {
+            for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+                kout[s + i] = sk[i];
+                vout[s + i] = sv[i];
+            }
         }
         // cells: thread t owns items [t*kPer, t*kPer + kPer); head = first item or key change
         uint32_t flags = 0, cnt = 0;
 #pragma unroll
         for (uint32_t r = 0; r < kPer; ++r) {
             const uint32_t i = threadIdx.x * kPer + r;
-            const bool head = i < m && i > 0 && sk[i] != sk[i - 1];
+            const bool head = i < m && i > 0 && (sk[i] >> idb) != (sk[i - 1] >> idb);   // keys only (idb = 0: plain)
             flags |= (head ? 1u : 0u) << r;
             cnt += head ? 1u : 0u;
         }
@@ -454,17 +490,23 @@ void bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint3
     exclusive_scan_u32_dup(hist, start.p, hist, (uint64_t)P + 1, s);
     tr.dev("bucket scan", s);
     const uint32_t g = (n + 255) / 256;
-    k_bucket_scatter<<<g, 256, 0, s>>>(keys, vals, n, div, inv, hist, keys_tmp, vals_tmp);
+    // packed items when (bits of key - prefix*div) + (bits of an id) <= 64
+    int lowb = 0, idb = 0;
+    while (lowb < 64 && ((div - 1) >> lowb)) ++lowb;
+    while (idb < 32 && ((uint64_t)(n - 1) >> idb)) ++idb;
+    if (idb == 0) idb = 1;
+    if (lowb + idb > 64) idb = 0;
+    k_bucket_scatter<<<g, 256, 0, s>>>(keys, vals, n, div, inv, hist, keys_tmp, vals_tmp, idb);
     SJ_LAUNCHED();
     tr.dev("scatter", s);
     k_bucket_sort<<<(uint32_t)((P + 255) / 256), 256, 0, s>>>(keys_tmp, vals_tmp, start.p, P, keys, vals, big.p,
-                                                               big_cap, local, cellcnt);
+                                                               big_cap, local, cellcnt, idb, div);
     SJ_LAUNCHED();
     tr.dev("bucket sort", s);
     constexpr size_t kBigSmem = kBigMax * (sizeof(uint64_t) + sizeof(uint32_t)) + sizeof(uint32_t) * (kBigThreads / 32);
     set_max_dyn_smem(reinterpret_cast<const void *>(k_bucket_sort_big), (int)kBigSmem);
     k_bucket_sort_big<<<296, kBigThreads, kBigSmem, s>>>(keys_tmp, vals_tmp, start.p, big.p, big_cap, keys, vals,
-                                                         overflow, local, cellcnt);
+                                                         overflow, local, cellcnt, idb, div);
     SJ_LAUNCHED();
     tr.dev("big buckets", s);
 }
