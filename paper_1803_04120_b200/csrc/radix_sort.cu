@@ -327,6 +327,36 @@ k_bucket_sort(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin
         if (slot < big_cap) big[1 + slot] = (uint32_t)b;
         return;                                        // cellcnt[b] written by the big-bucket kernel
     }
+    if (idb && e - s <= 8u) {
+        // packed items of a small bucket (the common case: ~2 per prefix on sparse data): sorted in
+        // registers by an unrolled odd-even transposition network, unpacked, cells numbered
+        const uint32_t m = e - s;
+        uint64_t r[8];
+#pragma unroll
+        for (uint32_t i = 0; i < 8; ++i) r[i] = i < m ? kin[s + i] : ~0ull;
+#pragma unroll
+        for (int round = 0; round < 8; ++round) {
+#pragma unroll
+            for (int i = round & 1; i + 1 < 8; i += 2) {
+                const uint64_t a = r[i], c = r[i + 1];
+                r[i] = a < c ? a : c;
+                r[i + 1] = a < c ? c : a;
+            }
+        }
+        const uint64_t base = b * div, mask = (1ull << idb) - 1ull;
+        uint32_t c = 0;
+#pragma unroll
+        for (uint32_t i = 0; i < 8; ++i) {
+            if (i < m) {
+                if (i > 0 && (r[i] >> idb) != (r[i - 1] >> idb)) ++c;
+                kout[s + i] = base + (r[i] >> idb);
+                vout[s + i] = (uint32_t)(r[i] & mask);
+                local[s + i] = c;
+            }
+        }
+        cellcnt[b] = m ? c + 1 : 0;
+        return;
+    }
     if (idb) {
         // packed items: insertion sort in place (u64 order), then unpack into the output range
         uint64_t *w = const_cast<uint64_t *>(kin);
