@@ -518,3 +518,18 @@ def test_build_time_estimate_is_the_join_estimate(sj, d, n, eps):
     assert a.stats["estimated_pairs"] == b.stats["estimated_pairs"] and a.n_batches == b.n_batches
     assert a.n_pairs == b.n_pairs
     assert b.stats["estimate_ms"] > 0
+
+
+@pytest.mark.parametrize("d", [2, 3, 4, 5, 6])
+def test_tiny_inputs(sj, d):
+    """Degenerate sizes: one point, two identical points, two points just outside eps -- device and
+    host results, CSR output."""
+    for pts, eps in ((np.zeros((1, d)), 1.0), (np.ones((2, d)), 0.5),
+                     (np.stack([np.zeros(d), np.full(d, 1.0)]), 0.999)):
+        want = oracle.brute_force(pts, eps)
+        for host in (False, True):
+            got, res, _ = gpu_pairs(sj, pts, eps, result_on_host=host)
+            assert np.array_equal(got, want)
+            off, nb = res.to_csr(len(pts))
+            keys = (want >> np.uint64(32)).astype(np.int64)
+            assert np.array_equal(off.cpu().numpy(), np.concatenate([[0], np.cumsum(np.bincount(keys, minlength=len(pts)))]))
