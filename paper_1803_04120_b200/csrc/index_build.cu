@@ -768,7 +768,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
     // the build runs on the caller's stream, or on a pooled library stream; the pooled context also
     // lends its pinned slot memory and an event (device geometry read-back)
     static_assert(sizeof(DevGeom) <= 4096, "DevGeom fits its slot");
-    CtxGuard cg{acquire_ctx(o.device, 1, 1, kBuildSlotBytes)};
+    CtxGuard cg{acquire_ctx(o.device, 2, 2, kBuildSlotBytes)};   // stream 1: the geometry read-back
     cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : cg.c->streams[0];
 
     const uint32_t N = (uint32_t)n;
@@ -867,9 +867,14 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         tr.dev("minmax", s);
         k_geometry<<<1, 256, 0, s>>>(part, parts, d, eps, N, allow_bucket ? 1 : 0, o.build_masks ? 1 : 0, dgeom);
         SJ_LAUNCHED();
+        // the host's copy of the geometry travels on a side stream, so the key pass does not queue
+        // behind the small D2H copy's latency
         DevGeom *hgeom = static_cast<DevGeom *>(cg.c->h_slots);
-        SJ_CUDA(cudaMemcpyAsync(hgeom, dgeom, sizeof(DevGeom), cudaMemcpyDeviceToHost, s));
-        SJ_CUDA(cudaEventRecord(cg.c->events[0], s));
+        cudaStream_t s_side = cg.c->streams[1];
+        SJ_CUDA(cudaEventRecord(cg.c->events[1], s));
+        SJ_CUDA(cudaStreamWaitEvent(s_side, cg.c->events[1], 0));
+        SJ_CUDA(cudaMemcpyAsync(hgeom, dgeom, sizeof(DevGeom), cudaMemcpyDeviceToHost, s_side));
+        SJ_CUDA(cudaEventRecord(cg.c->events[0], s_side));
         ev.rec(2, s);
 
         tr.mark("minmax + geometry enqueued");
