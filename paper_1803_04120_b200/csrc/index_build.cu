@@ -103,8 +103,10 @@ __device__ __forceinline__ double ord_to_double(unsigned long long k)
 constexpr int kSmemMaskWords = 2048;   // 64 K bits, 8 KB of shared memory
 // context slot layout of the build: min/max partials (<= 4 * SMs blocks), then the DevGeom
 constexpr size_t kGeomOffset = 4 * 256 * (2 * SJ_MAX_DIM + 1) * sizeof(unsigned long long);
-constexpr size_t kEstOffset = kGeomOffset + 4096;          // speculative estimate buckets (<= 1100)
-constexpr size_t kBuildSlotBytes = kEstOffset + 8 * 1100;
+constexpr size_t kEstOffset = kGeomOffset + 4096;          // pinned staging of aux + estimate buckets
+constexpr size_t kMaxEstBuckets = 1100;
+constexpr size_t kAuxEstOffset = 64;                       // estimate buckets, bytes after aux
+constexpr size_t kBuildSlotBytes = kEstOffset + kAuxEstOffset + 8 * kMaxEstBuckets;
 
 __device__ __noinline__ void geometry_products(const uint64_t *cpd, int d, uint32_t n, int allow_bucket,
                                                int want_masks, DevGeom &G);
@@ -692,13 +694,21 @@ k_dense_fill(const uint32_t *__restrict__ G, const uint32_t *__restrict__ nG, ui
 // import path, which has no such count, always builds them).
 constexpr uint32_t kDenseT = 16;
 void finish_aux(sj_index *idx, cudaStream_t s, uint32_t *aux, const DirPlan &dp, const uint32_t *dirhist,
-                bool force_dense, uint32_t *h_aux)
+                bool force_dense, uint32_t *h_aux, void *h_stage = nullptr, size_t stage_bytes = 0)
 {
     sj_index_view &v = idx->view;
     DevIndex &ix = idx->dev;
     if (dirhist) exclusive_scan_u32(dirhist, const_cast<uint32_t *>(ix.dir), (uint64_t)dp.P + 1, s);
-    SJ_CUDA(cudaMemcpyAsync(h_aux, aux, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    SJ_CUDA(cudaStreamSynchronize(s));
+    if (h_stage) {
+        // one copy into pinned memory: aux and whatever the caller placed after it (the build's
+        // estimate buckets)
+        SJ_CUDA(cudaMemcpyAsync(h_stage, aux, stage_bytes, cudaMemcpyDeviceToHost, s));
+        SJ_CUDA(cudaStreamSynchronize(s));
+        std::memcpy(h_aux, h_stage, 4 * sizeof(uint32_t));
+    } else {
+        SJ_CUDA(cudaMemcpyAsync(h_aux, aux, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        SJ_CUDA(cudaStreamSynchronize(s));
+    }
     uint32_t *tasks = nullptr;
     uint32_t ntasks = 0;
     if (!h_aux[3] && (h_aux[2] > 0 || force_dense)) {
@@ -805,7 +815,8 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         // histogram sized for the largest possible prefix count)
         auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
         const size_t b_A = al(4 * n), b_pc = al(4 * n), b_B = al(8 * n), b_G = al(4 * (n + 1)), b_X = al(8 * n * d),
-                     b_cc = 0, b_cm = 0, b_mk = al(4 * kSmemMaskWords), b_aux = al(16);   // (no per-cell coords/masks)
+                     b_cc = 0, b_cm = 0, b_mk = al(4 * kSmemMaskWords),
+                     b_aux = al(kAuxEstOffset + 8 * kMaxEstBuckets);   // aux + the build's estimate buckets
         char *arena =
             static_cast<char *>(own(dev_alloc(b_A + b_pc + b_B + b_G + b_X + b_cc + b_cm + b_mk + b_aux, s)));
         uint32_t *A = reinterpret_cast<uint32_t *>(arena);
@@ -1065,8 +1076,8 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
                               : (pavg <= 8.0 && (double)dp.div < 4.0e15 ? kSearchCellScan : kSearchRows);
         const bool spec = v.key_bits <= 62 && o.speculative_estimate;
         EstimateShape es_spec;
-        unsigned long long *hbk =
-            reinterpret_cast<unsigned long long *>(static_cast<char *>(cg.c->h_slots) + kEstOffset);
+        char *h_stage = static_cast<char *>(cg.c->h_slots) + kEstOffset;
+        const unsigned long long *hbk = reinterpret_cast<const unsigned long long *>(h_stage + kAuxEstOffset);
         if (spec) {
             DevIndex px = ix;
             px.search_mode = prov_mode;
@@ -1074,17 +1085,16 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
             px.dense_tasks = nullptr;
             px.n_dense_tasks = 0;
             es_spec = estimate_shape(n);
-            if (es_spec.nbk > 1100) fail(SJ_ERR_CUDA, "estimate bucket count out of range (internal error)");
-            unsigned long long *dbk =
-                reinterpret_cast<unsigned long long *>(static_cast<char *>(cg.c->d_slots) + kEstOffset);
+            if (es_spec.nbk > kMaxEstBuckets) fail(SJ_ERR_CUDA, "estimate bucket count out of range (internal error)");
+            unsigned long long *dbk = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(aux) + kAuxEstOffset);
             SJ_CUDA(cudaMemsetAsync(dbk, 0, 8 * es_spec.nbk, s));
             sj_join_opts jo;
             sj_join_opts_default(&jo);
             launch_estimate(px, o.device, jo, 0, n, es_spec, dbk, s);
-            SJ_CUDA(cudaMemcpyAsync(hbk, dbk, 8 * es_spec.nbk, cudaMemcpyDeviceToHost, s));
             tr.dev("speculative estimate", s);
         }
-        finish_aux(idx, s, aux, dp, nullptr, false, h_aux);   // the build's late host sync
+        finish_aux(idx, s, aux, dp, nullptr, false, h_aux, h_stage,
+                   kAuxEstOffset + (spec ? 8 * es_spec.nbk : 0));     // the build's late host sync
         if (spec && !h_aux[3] && idx->dev.search_mode == prov_mode) {
             idx->spec_est_valid = true;
             idx->spec_shape = es_spec;
