@@ -61,6 +61,12 @@ void cuda_check(cudaError_t e, const char *what, const char *file, int line)
     throw Error{SJ_ERR_CUDA, buf};
 }
 
+bool alloc_hook_set()
+{
+    std::lock_guard<std::mutex> lk(g_hook_mu);
+    return g_hook.alloc != nullptr;
+}
+
 void *dev_alloc(size_t bytes, cudaStream_t s)
 {
     if (bytes == 0) bytes = 1;
@@ -234,7 +240,7 @@ void sj_free_result(sj_result *r)
     sj::result_release_events(r);
     for (auto &b : r->batches) {
         if (!b.pairs) continue;
-        if (b.on_device) sj::dev_free(b.pairs, nullptr);
+        if (b.on_device) sj::result_buffer_put(r->device, b.pairs, nullptr);
         else sj::host_pinned_free(b.pairs);
     }
     delete r;

@@ -117,6 +117,59 @@ std::mutex g_scr_mu;
 std::map<int, ScratchSlot> g_scr;
 }  // namespace
 
+// Device-resident result batches: a bounded per-device cache of freed batch buffers.  Joins with
+// results of tens of GB otherwise had the stream-ordered pool map fresh memory again (C4 2-D
+// eps=0.02: joins of 0.08 vs 0.8 s).  A freed result is complete (its join synchronised), so any
+// later join may reuse its buffers.  Holds at most kResultCacheBytes; the allocator hook bypasses it.
+namespace {
+constexpr size_t kResultCacheBytes = 48ull << 30;
+std::mutex g_rc_mu;
+std::map<int, std::multimap<size_t, void *>> g_rc;       // device -> (bytes -> buffer)
+std::map<void *, size_t> g_rc_size;                      // buffer -> bytes (cached or handed out)
+std::map<int, size_t> g_rc_held;
+}  // namespace
+
+void *result_buffer_get(int dev, size_t bytes, cudaStream_t s)
+{
+    if (alloc_hook_set()) return dev_alloc(bytes, s);
+    {
+        std::lock_guard<std::mutex> lk(g_rc_mu);
+        auto &m = g_rc[dev];
+        auto it = m.lower_bound(bytes);
+        if (it != m.end() && it->first <= 2 * bytes + (64u << 20)) {
+            void *p = it->second;
+            g_rc_held[dev] -= it->first;
+            m.erase(it);
+            return p;
+        }
+    }
+    void *p = dev_alloc(bytes, s);
+    std::lock_guard<std::mutex> lk(g_rc_mu);
+    g_rc_size[p] = bytes;
+    return p;
+}
+
+void result_buffer_put(int dev, void *p, cudaStream_t s)
+{
+    if (!p) return;
+    size_t bytes = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_rc_mu);
+        auto it = g_rc_size.find(p);
+        if (it != g_rc_size.end() && g_rc_held[dev] + it->second <= kResultCacheBytes) {
+            g_rc[dev].emplace(it->second, p);
+            g_rc_held[dev] += it->second;
+            return;
+        }
+        if (it != g_rc_size.end()) {
+            bytes = it->second;
+            g_rc_size.erase(it);
+        }
+    }
+    (void)bytes;
+    dev_free(p, s);
+}
+
 int device_count()
 {
     static const int n = [] {

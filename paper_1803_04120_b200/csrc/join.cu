@@ -408,7 +408,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(
                     o.batch_capacity_pairs, est[b] + est[b] / 4 + 65536));
                 sj_batch &bt = res->batches[b];
-                bt.pairs = dalloc<uint64_t>(cap, s);
+                bt.pairs = static_cast<uint64_t *>(result_buffer_get(idx->device, cap * sizeof(uint64_t), s));
                 bt.cap = cap;
                 bt.on_device = 1;
                 run_batch(cuts[b], cuts[b + 1], bt.pairs, cap, dslots + slot, s, !own_slots);
@@ -448,8 +448,8 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                     const int si = (int)(r - r0);
                     cudaStream_t st = cx.streams[si];
                     sj_batch &bt = res->batches[b];
-                    dev_free(bt.pairs, st);
-                    bt.pairs = dalloc<uint64_t>(counts[b], st);
+                    result_buffer_put(idx->device, bt.pairs, st);
+                    bt.pairs = static_cast<uint64_t *>(result_buffer_get(idx->device, counts[b] * sizeof(uint64_t), st));
                     bt.cap = counts[b];
                     run_batch(cuts[b], cuts[b + 1], bt.pairs, bt.cap, dslots + si, st, true);
                     SJ_CUDA(cudaMemcpyAsync(hslots + si, dslots + si, sizeof(Slot), cudaMemcpyDeviceToHost, st));
@@ -557,7 +557,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         result_release_events(res);
         for (auto &b : res->batches) {
             if (!b.pairs) continue;
-            if (b.on_device) dev_free(b.pairs, nullptr);
+            if (b.on_device) result_buffer_put(res->device, b.pairs, nullptr);
             else host_pinned_free(b.pairs);
         }
         delete res;

@@ -219,6 +219,9 @@ DevCtx *acquire_ctx(int dev, int nstreams, int nevents, size_t slot_bytes);
 // tens of microseconds of host time, on the build's / join's critical path if repeated.
 void set_max_dyn_smem(const void *func, int bytes);
 int device_count();                            // cached cudaGetDeviceCount (0 on error)
+bool alloc_hook_set();                         // api.cu: a user allocator hook is installed
+void *result_buffer_get(int dev, size_t bytes, cudaStream_t s);   // device batch buffers (cached)
+void result_buffer_put(int dev, void *p, cudaStream_t s);
 int device_sm_count(int dev);                  // cached multiprocessor count
 void *scratch_acquire(int dev, size_t bytes);   // nullptr if busy (use the pool instead)
 void scratch_release(int dev, void *p);
