@@ -270,12 +270,14 @@ void launch_estimate(const DevIndex &ix, int device, const sj_join_opts &o, uint
     ja.nsamples = (uint32_t)es.ns;
     ja.qbucket = dbk;
     ja.group = (uint32_t)es.group;
-#ifndef SJ_EST_LANES_MAX
-#define SJ_EST_LANES_MAX 3
-#endif
+    // (many top offsets per query, e.g. 6-D eps=8's 243: up to 16 lanes and 4 K threads per SM --
+    //  its estimate 0.45 -> 0.23 ms; few offsets: up to 8 lanes within one wave of 1 K per SM)
+    const bool heavy = ix.search_mode == kSearchCellScan && ix.dir_ntop >= 81;
+    const uint32_t lanes_max = heavy ? 4u : 3u;
+    const uint64_t threads_per_sm = heavy ? 4096 : 1024;
     if (o.lanes_per_query == 0) {
         const int nsm = device_sm_count(device);
-        while (ja.lanes_log2 < SJ_EST_LANES_MAX && (es.ns << (ja.lanes_log2 + 1)) <= (uint64_t)nsm * 1024)
+        while (ja.lanes_log2 < lanes_max && (es.ns << (ja.lanes_log2 + 1)) <= (uint64_t)nsm * threads_per_sm)
             ++ja.lanes_log2;
     }
     launch_refine<kCountQuery>(ix, ja, o.unicomp != 0, (uint32_t)es.ns, s);
