@@ -58,10 +58,16 @@ void launch_refine(const DevIndex &ix, const JoinArgs &ja, bool unicomp, uint32_
     if (nthreads64 >= (1ull << 32)) fail(SJ_ERR_ARG, "too many queries x lanes for one launch");
     const uint32_t nthreads = (uint32_t)nthreads64;
     const dim3 grid((nthreads + kRefineThreads - 1) / kRefineThreads), block(kRefineThreads);
+    const bool occ6 = MODE == kEmit && ix.search_mode == kSearchCellScan && !ix.occ && ix.dir_ntop >= 81;
 #define SJ_REFINE_CASE(DD)                                                                       \
     case DD:                                                                                     \
-        if (unicomp) k_refine<DD, MODE, true><<<grid, block, 0, s>>>(ix, ja);                   \
-        else k_refine<DD, MODE, false><<<grid, block, 0, s>>>(ix, ja);                          \
+        if (occ6) {                                                                              \
+            if (unicomp) k_refine<DD, MODE, true, 6><<<grid, block, 0, s>>>(ix, ja);            \
+            else k_refine<DD, MODE, false, 6><<<grid, block, 0, s>>>(ix, ja);                   \
+        } else {                                                                                 \
+            if (unicomp) k_refine<DD, MODE, true><<<grid, block, 0, s>>>(ix, ja);               \
+            else k_refine<DD, MODE, false><<<grid, block, 0, s>>>(ix, ja);                      \
+        }                                                                                        \
         break;
     switch (ix.d) {
         SJ_REFINE_CASE(2)

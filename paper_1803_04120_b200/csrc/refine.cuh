@@ -716,8 +716,11 @@ k_refine_dense(const DevIndex ix, const JoinArgs ja)
     flush_work(ja, q.probes, q.tests, q.emitted);
 }
 
-template <int D, int MODE, bool UNICOMP>
-__global__ void __launch_bounds__(kRefineThreads, kRefineMinBlocks)
+// MINB: CTAs per SM the register budget is sized for -- kRefineMinBlocks (5) in general; 6 for the
+// many-offset cell scan without bitmaps (6-D eps=8: 9.4 -> 9.1 ms), where more warps hide more of
+// the directory/B lookup latency
+template <int D, int MODE, bool UNICOMP, int MINB = kRefineMinBlocks>
+__global__ void __launch_bounds__(kRefineThreads, MINB)
 k_refine(const DevIndex ix, const JoinArgs ja)
 {
     __shared__ TopTable tt;
