@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SJ_ABI_VERSION 2
+#define SJ_ABI_VERSION 3
 #define SJ_MAX_DIM 6
 
 typedef enum {
@@ -165,8 +165,14 @@ sj_status sj_build_index(const double *points, uint64_t n, int d, double eps,
  *         SJ_ERR_CUDA. */
 sj_status sj_self_join(const sj_index *idx, const sj_join_opts *opts, sj_result **out);
 
-/* Release a result and every batch buffer it owns.  NULL-safe. */
+/* Release a result and every batch buffer it owns.  NULL-safe.  Device batch buffers go to a
+ * per-device cache reused by later joins; they are reused only after the work queued before this
+ * call on the legacy default stream (and every blocking stream) completed. */
 void sj_free_result(sj_result *r);
+
+/* Same, ordered after the work queued on `stream` (cudaStream_t; NULL = legacy default stream):
+ * use it when the caller read zero-copy batch views on a non-blocking stream. */
+void sj_free_result_async(sj_result *r, void *stream);
 
 /* ---- supporting entry points ---------------------------------------------------------------- */
 
@@ -193,6 +199,17 @@ sj_status sj_result_copy_to_host(const sj_result *r, uint64_t *dst, uint64_t cap
  * >= 2^32 pairs), SJ_ERR_NOMEM (scratch of 16 B per pair), SJ_ERR_CUDA. */
 sj_status sj_result_to_csr(const sj_result *r, uint64_t n_points, uint64_t *row_offsets, uint32_t *neighbors);
 
+/* Order-independent fingerprints of the result's pair multiset (full-size parity of results too
+ * large to hold twice): fp[0] = sum over pairs x of mix_a(x),
+ * fp[1] = sum of mix_b(x), both mod 2^64, with mix_a = SplitMix64's output function of
+ * x + 0x9E3779B97F4A7C15 and mix_b = MurmurHash3's fmix64 of x ^ 0xC2B2AE3D27D4EB4F.  The
+ * fingerprints add over disjoint results (e.g. query shards).  counts: NULL, or DEVICE memory for
+ * n_points uint32 (the N of the joined point set) receiving cnt[i] = pairs with key i in this
+ * result (zeroed by the call).  Reads device batches in place and pinned host batches through
+ * their UVA mapping.  Blocks until done.  Errors: SJ_ERR_STATE (NULL result, or a key >= N),
+ * SJ_ERR_ARG (fp NULL), SJ_ERR_CUDA. */
+sj_status sj_result_fingerprint(const sj_result *r, uint64_t fp[2], uint32_t *counts);
+
 /* Per-point neighbour counts cnt[i] = |{k : (i,k) in S}| without materialising
  * pairs.  cnt: device pointer to N uint32 on the index's device (zeroed by the call), or NULL.
  * *total receives |S| (restricted to the pairs decided by queries of opts' query range). */
@@ -205,6 +222,14 @@ sj_status sj_neighbor_counts(const sj_index *idx, const sj_join_opts *opts, uint
  * the paper's brute-force comparison, not for large N. */
 sj_status sj_brute_force_join(const double *points, uint64_t n, int d, double eps, const sj_build_opts *bopts,
                               const sj_join_opts *jopts, sj_result **out);
+
+/* Multi-GPU shard plan: cut the A-order queries [0, N) into `world` contiguous
+ * ranges cuts[r] .. cuts[r+1] (cuts: world + 1 host uint64) of about equal estimated work, using
+ * the a5 sampled estimate (the build's own estimate of the default join when it
+ * has one, else a count-only run of the sample now): per query, its estimated emitted pairs plus a
+ * constant search cost.  Joining every range (sj_join_opts.query_begin/end) on its own GPU gives
+ * shards whose union is exactly S.  Errors: SJ_ERR_STATE, SJ_ERR_ARG (world < 1), SJ_ERR_CUDA. */
+sj_status sj_plan_shards(const sj_index *idx, uint32_t world, uint64_t *cuts);
 
 /* Geometry, sizes, timings and device pointers of an index (for tests and NCCL broadcast). */
 sj_status sj_index_export(const sj_index *idx, sj_index_view *view);
@@ -224,6 +249,16 @@ sj_status sj_index_import(const sj_index_view *view, int device, sj_index **out)
  * Pass NULLs to restore the default (cudaMallocAsync from the device's default pool). */
 void sj_set_allocator(void *(*alloc)(size_t, int, void *, void *), void (*release)(void *, void *),
                       void *ctx);
+
+/* Upper bound on the device memory the freed-result-batch cache may hold per device (default
+ * 48 GB, or env SJ_RESULT_CACHE_BYTES); lowering it releases cached buffers above the new bound. */
+void sj_set_result_cache_limit(uint64_t bytes);
+
+/* Release every cache the library keeps on `device` (-1: all devices): freed result batches, the
+ * index-build scratch buffer, pooled pinned host blocks, and memory held by the device's default
+ * stream-ordered pool beyond what live objects use.  Live indexes and results are untouched.
+ * Synchronises the device.  Errors: SJ_ERR_CUDA. */
+sj_status sj_trim(int device);
 
 /* Batch planner (host-only, no GPU needed): given per-sample emission counts of a strided sample
  * (sample s stands for `step` consecutive queries starting at q_begin + s*step), cut

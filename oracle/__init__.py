@@ -66,6 +66,10 @@ def _load():
         lib.orc_rows.restype = i64
         lib.orc_grid_join.argtypes = [p, i64, i32, dbl, i32, i64, i64, i32, p, p, i64]
         lib.orc_grid_join.restype = i64
+        lib.orc_grid_digest.argtypes = [p, i64, i32, dbl, i32, i64, i64, i32, p, p]
+        lib.orc_grid_digest.restype = i64
+        lib.orc_mix.argtypes = [i32, ctypes.c_uint64]
+        lib.orc_mix.restype = ctypes.c_uint64
         _lib = lib
     return _lib
 
@@ -129,6 +133,41 @@ def grid_join(points, eps: float, include_self: bool = True, q0: int = 0, q1: in
                             None, _ptr(out), total)
     assert got == total
     return out
+
+
+def grid_digest(points, eps: float, include_self: bool = True, q0: int = 0, q1: int | None = None,
+                nthreads: int | None = None, with_counts: bool = False):
+    """Order-independent fingerprints of S restricted to queries [q0,q1) (sj_oracle.c
+    orc_grid_digest): returns dict(pairs=|S|, fa=F_a, fb=F_b, fc=F_c[, counts=per-query counts]).
+    Fingerprints are sums mod 2^64, so they add over disjoint query ranges."""
+    P = _pts(points)
+    n, d = P.shape
+    q1 = n if q1 is None else q1
+    nthreads = nthreads or default_threads()
+    counts = np.zeros(max(q1 - q0, 0), dtype=np.int64) if with_counts else None
+    fp = np.zeros(3, dtype=np.uint64)
+    total = _load().orc_grid_digest(_ptr(P), n, d, float(eps), int(include_self), q0, q1, nthreads,
+                                    _ptr(counts) if counts is not None else None, _ptr(fp))
+    if total < 0:
+        raise ValueError("bad arguments")
+    out = dict(pairs=int(total), fa=int(fp[0]), fb=int(fp[1]), fc=int(fp[2]))
+    if with_counts:
+        out["counts"] = counts
+    return out
+
+
+def mix(which: int, x: int) -> int:
+    """The fingerprint mixers of sj_oracle.c (0: SplitMix64 output, 1: MurmurHash3 fmix64)."""
+    return int(_load().orc_mix(int(which), ctypes.c_uint64(int(x) & (2**64 - 1))))
+
+
+def fingerprint_pairs(pairs: np.ndarray) -> tuple:
+    """(F_a, F_b) of an explicit pair array, via the C mixers (slow path for small arrays: tests)."""
+    fa = fb = 0
+    for x in np.asarray(pairs, dtype=np.uint64).tolist():
+        fa = (fa + mix(0, x)) & (2**64 - 1)
+        fb = (fb + mix(1, x)) & (2**64 - 1)
+    return fa, fb
 
 
 def rows(points, eps: float, qids: Iterable[int], include_self: bool = True,

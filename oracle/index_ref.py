@@ -76,14 +76,6 @@ def linearize(g: Geometry, c) -> int:
     return int(sum(int(c[j]) * g.strides[j] for j in range(g.d)))
 
 
-def delinearize(g: Geometry, lid: int) -> tuple:
-    out = []
-    for j in range(g.d):
-        out.append(lid % g.cpd[j])
-        lid //= g.cpd[j]
-    return tuple(out)
-
-
 @dataclass
 class Index:
     geom: Geometry

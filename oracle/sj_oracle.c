@@ -23,6 +23,15 @@
  *                       |x_j-y_j| + coordinate rounding (DESIGN.md "Oracle" section).
  *   orc_rows         -- for sampled query ids, the full neighbour row by brute force over all N
  *                       points (used for parity at full size, one query at a time).
+ *   orc_grid_digest  -- the grid join of orc_grid_join, but instead of storing S it returns
+ *                       |S|, per-query counts and order-independent fingerprints of the multiset S
+ *                       and of the count vector (full-size parity of results too large to hold:
+ *                       tens of GB of pairs).  Fingerprint definition:
+ *                         F_a(S) = sum over pairs x of mix_a(x)  (mod 2^64)
+ *                         F_b(S) = sum over pairs x of mix_b(x)  (mod 2^64)
+ *                         F_c(cnt) = sum over queries i of mix_a((uint64)i << 32 | cnt_i)
+ *                       mix_a = SplitMix64 output function of x + 0x9E3779B97F4A7C15,
+ *                       mix_b = MurmurHash3 fmix64 of x ^ 0xC2B2AE3D27D4EB4F.
  */
 #include <math.h>
 #include <pthread.h>
@@ -315,6 +324,104 @@ int64_t orc_grid_join(const double *pts, int64_t n, int d, double eps, int inclu
         }
         total += jobs[t].len;
         free(jobs[t].buf);
+    }
+    free(th); free(jobs);
+    grid_free(&g);
+    return total;
+}
+
+/* ---- order-independent fingerprints of S (full-size parity without storing S) ------------ */
+static uint64_t orc_mix_a(uint64_t x)
+{
+    uint64_t z = x + 0x9E3779B97F4A7C15ULL;               /* SplitMix64 (Steele, Lea, Flood 2014) */
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+static uint64_t orc_mix_b(uint64_t x)
+{
+    uint64_t k = x ^ 0xC2B2AE3D27D4EB4FULL;                /* MurmurHash3 fmix64 */
+    k ^= k >> 33;
+    k *= 0xFF51AFD7ED558CCDULL;
+    k ^= k >> 33;
+    k *= 0xC4CEB9FE1A85EC53ULL;
+    k ^= k >> 33;
+    return k;
+}
+
+/* exported so tests can pin the mixers against their published reference values */
+uint64_t orc_mix(int which, uint64_t x) { return which == 0 ? orc_mix_a(x) : orc_mix_b(x); }
+
+typedef struct {
+    const orc_grid *g; double E; int include_self;
+    int64_t q0, q1;
+    int64_t *counts; int64_t counts_base;
+    int64_t total; uint64_t fa, fb, fc;
+} digest_job;
+
+static void *digest_worker(void *arg)
+{
+    digest_job *J = (digest_job *)arg;
+    const orc_grid *g = J->g;
+    int d = g->d;
+    int64_t noff = 1;
+    for (int j = 0; j < d; ++j) noff *= 3;
+    int64_t nb[ORC_MAXD];
+    for (int64_t i = J->q0; i < J->q1; ++i) {
+        const int64_t *ci = g->cellc + i * d;
+        int64_t cnt = 0;
+        for (int64_t o = 0; o < noff; ++o) {          /* every cell of the 3^d neighbourhood */
+            int64_t r = o;
+            for (int j = 0; j < d; ++j) { nb[j] = ci[j] + (r % 3) - 1; r /= 3; }
+            const orc_cell *e = grid_find(g, nb);
+            if (!e) continue;
+            for (int64_t m = e->start; m < e->start + e->count; ++m) {
+                int64_t k = g->order[m];
+                if (k == i && !J->include_self) continue;
+                if (orc_within(g->pts + i * d, g->pts + k * d, d, J->E)) {
+                    uint64_t x = ((uint64_t)i << 32) | (uint64_t)k;
+                    J->fa += orc_mix_a(x);
+                    J->fb += orc_mix_b(x);
+                    ++cnt;
+                }
+            }
+        }
+        J->fc += orc_mix_a(((uint64_t)i << 32) | (uint64_t)cnt);
+        J->total += cnt;
+        if (J->counts) J->counts[i - J->counts_base] = cnt;
+    }
+    return NULL;
+}
+
+/* Fingerprints of the pairs of queries [q0,q1) against all N points (full 3^d grid scan, the
+ * same filter and predicate as orc_grid_join).  fp[0..2] = F_a, F_b, F_c over those queries;
+ * counts[q1-q0] (may be NULL) = per-query counts.  Returns the number of pairs, or -1/-2. */
+int64_t orc_grid_digest(const double *pts, int64_t n, int d, double eps, int include_self,
+                        int64_t q0, int64_t q1, int nthreads, int64_t *counts, uint64_t *fp)
+{
+    if (n < 0 || d < 1 || d > ORC_MAXD || !(eps > 0.0) || !fp) return -1;
+    if (q0 < 0 || q1 > n || q0 > q1) return -1;
+    if (nthreads < 1) nthreads = 1;
+    orc_grid g;
+    memset(&g, 0, sizeof g);
+    if (grid_build(&g, pts, n, d, eps) != 0) { grid_free(&g); return -2; }
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    digest_job *jobs = (digest_job *)calloc((size_t)nthreads, sizeof(digest_job));
+    /* many more chunks than threads would balance skewed inputs better; static chunks keep it plain */
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t].g = &g; jobs[t].E = eps * eps; jobs[t].include_self = include_self;
+        jobs[t].q0 = q0 + (q1 - q0) * t / nthreads;
+        jobs[t].q1 = q0 + (q1 - q0) * (t + 1) / nthreads;
+        jobs[t].counts = counts; jobs[t].counts_base = q0;
+        pthread_create(&th[t], NULL, digest_worker, &jobs[t]);
+    }
+    int64_t total = 0;
+    fp[0] = fp[1] = fp[2] = 0;
+    for (int t = 0; t < nthreads; ++t) {
+        pthread_join(th[t], NULL);
+        total += jobs[t].total;
+        fp[0] += jobs[t].fa; fp[1] += jobs[t].fb; fp[2] += jobs[t].fc;
     }
     free(th); free(jobs);
     grid_free(&g);

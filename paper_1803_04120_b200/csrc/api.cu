@@ -22,6 +22,9 @@ struct AllocHook {
 };
 AllocHook g_hook;
 std::mutex g_hook_mu;
+// provenance of hooked allocations: a pointer is released by the hook that produced it, whatever
+// hook is installed when it is freed (sj_set_allocator may change in between)
+std::map<void *, AllocHook> g_hooked;
 std::set<int> g_pool_configured;
 std::mutex g_pool_mu;
 
@@ -77,6 +80,7 @@ void *dev_alloc(size_t bytes, cudaStream_t s)
         if (g_hook.alloc) {
             void *p = g_hook.alloc(bytes, dev, s, g_hook.ctx);
             if (!p) fail(SJ_ERR_NOMEM, "allocator hook returned NULL");
+            g_hooked[p] = g_hook;
             return p;
         }
     }
@@ -95,14 +99,21 @@ void *dev_alloc(size_t bytes, cudaStream_t s)
 void dev_free(void *p, cudaStream_t s)
 {
     if (!p) return;
+    AllocHook h;
     {
         std::lock_guard<std::mutex> lk(g_hook_mu);
-        if (g_hook.release) {
-            // hooked memory is released stream-unordered: make prior work complete first
-            if (s) cudaStreamSynchronize(s);
-            g_hook.release(p, g_hook.ctx);
-            return;
+        auto it = g_hooked.find(p);
+        if (it != g_hooked.end()) {
+            h = it->second;
+            g_hooked.erase(it);
         }
+    }
+    if (h.alloc) {
+        // hooked memory is released stream-unordered: make prior work complete first
+        if (s) cudaStreamSynchronize(s);
+        else cudaDeviceSynchronize();
+        if (h.release) h.release(p, h.ctx);
+        return;
     }
     cudaFreeAsync(p, s);
 }
@@ -139,6 +150,16 @@ void *host_pinned_alloc(size_t bytes, size_t *granted)
     g_pin_size[p] = sz;
     if (granted) *granted = sz;
     return p;
+}
+
+void host_pinned_trim()
+{
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    for (auto &kv : g_pin_free) {
+        cudaFreeHost(kv.second);
+        g_pin_size.erase(kv.second);
+    }
+    g_pin_free.clear();
 }
 
 void host_pinned_free(void *p)
@@ -233,17 +254,43 @@ sj_status sj_self_join(const sj_index *idx, const sj_join_opts *opts, sj_result 
     SJ_API_END
 }
 
-void sj_free_result(sj_result *r)
+void sj_free_result_async(sj_result *r, void *stream)
 {
     if (!r) return;
     cudaSetDevice(r->device);
     sj::result_release_events(r);
     for (auto &b : r->batches) {
         if (!b.pairs) continue;
-        if (b.on_device) sj::result_buffer_put(r->device, b.pairs, nullptr);
+        if (b.on_device) sj::result_buffer_put(r->device, b.pairs, static_cast<cudaStream_t>(stream));
         else sj::host_pinned_free(b.pairs);
     }
     delete r;
+}
+
+void sj_free_result(sj_result *r) { sj_free_result_async(r, nullptr); }
+
+void sj_set_result_cache_limit(uint64_t bytes) { sj::set_result_cache_limit((size_t)bytes); }
+
+sj_status sj_trim(int device)
+{
+    SJ_API_BEGIN
+    sj::result_cache_trim(device);
+    sj::scratch_trim(device);
+    sj::host_pinned_trim();
+    const int n = sj::device_count();
+    for (int dv = 0; dv < n; ++dv) {
+        if (device >= 0 && dv != device) continue;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dv) == cudaSuccess) {
+            SJ_CUDA(cudaSetDevice(dv));
+            SJ_CUDA(cudaDeviceSynchronize());
+            SJ_CUDA(cudaMemPoolTrimTo(pool, 0));
+        } else {
+            cudaGetLastError();
+        }
+    }
+    return SJ_OK;
+    SJ_API_END
 }
 
 void sj_free_index(sj_index *idx) { sj::free_index_impl(idx); }
@@ -297,6 +344,22 @@ sj_status sj_result_to_csr(const sj_result *r, uint64_t n_points, uint64_t *row_
 {
     SJ_API_BEGIN
     sj::result_to_csr_impl(r, n_points, row_offsets, neighbors);
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_plan_shards(const sj_index *idx, uint32_t world, uint64_t *cuts)
+{
+    SJ_API_BEGIN
+    sj::plan_shards_impl(idx, world, cuts);
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_result_fingerprint(const sj_result *r, uint64_t fp[2], uint32_t *counts)
+{
+    SJ_API_BEGIN
+    sj::result_fingerprint_impl(r, fp, counts);
     return SJ_OK;
     SJ_API_END
 }

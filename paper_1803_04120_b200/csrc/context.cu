@@ -119,15 +119,54 @@ std::map<int, ScratchSlot> g_scr;
 
 // Device-resident result batches: a bounded per-device cache of freed batch buffers.  Joins with
 // results of tens of GB otherwise had the stream-ordered pool map fresh memory again (C4 2-D
-// eps=0.02: joins of 0.08 vs 0.8 s).  A freed result is complete (its join synchronised), so any
-// later join may reuse its buffers.  Holds at most kResultCacheBytes; the allocator hook bypasses it.
+// eps=0.02: joins of 0.08 vs 0.8 s).  Each cached buffer carries an event recorded on the stream
+// that freed it; the next owner's stream waits on it, so a buffer still read by the previous owner's
+// pending work (e.g. an async torch op on a zero-copy batch view) is never overwritten early.
+// Holds at most the limit (default 48 GB, env SJ_RESULT_CACHE_BYTES, sj_set_result_cache_limit);
+// sj_trim() empties it.  The allocator hook bypasses it.
 namespace {
-constexpr size_t kResultCacheBytes = 48ull << 30;
+struct CachedBuf { void *p; cudaEvent_t ev; };
 std::mutex g_rc_mu;
-std::map<int, std::multimap<size_t, void *>> g_rc;       // device -> (bytes -> buffer)
+std::map<int, std::multimap<size_t, CachedBuf>> g_rc;    // device -> (bytes -> buffer)
 std::map<void *, size_t> g_rc_size;                      // buffer -> bytes (cached or handed out)
 std::map<int, size_t> g_rc_held;
+size_t g_rc_limit = [] {
+    const char *e = std::getenv("SJ_RESULT_CACHE_BYTES");
+    return (e && *e) ? (size_t)std::strtoull(e, nullptr, 10) : (size_t)(48ull << 30);
+}();
 }  // namespace
+
+void set_result_cache_limit(size_t bytes)
+{
+    {
+        std::lock_guard<std::mutex> lk(g_rc_mu);
+        g_rc_limit = bytes;
+    }
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+        std::vector<CachedBuf> drop;
+        {
+            std::lock_guard<std::mutex> lk(g_rc_mu);
+            for (auto &kv : g_rc) {
+                auto &m = kv.second;
+                while (g_rc_held[kv.first] > g_rc_limit && !m.empty()) {
+                    auto it = std::prev(m.end());          // largest first
+                    g_rc_held[kv.first] -= it->first;
+                    g_rc_size.erase(it->second.p);
+                    drop.push_back(it->second);
+                    m.erase(it);
+                }
+            }
+        }
+        for (auto &c : drop) {
+            cudaEventSynchronize(c.ev);
+            cudaFree(c.p);
+            cudaEventDestroy(c.ev);
+        }
+    } else {
+        cudaGetLastError();
+    }
+}
 
 void *result_buffer_get(int dev, size_t bytes, cudaStream_t s)
 {
@@ -137,10 +176,12 @@ void *result_buffer_get(int dev, size_t bytes, cudaStream_t s)
         auto &m = g_rc[dev];
         auto it = m.lower_bound(bytes);
         if (it != m.end() && it->first <= 2 * bytes + (64u << 20)) {
-            void *p = it->second;
+            const CachedBuf c = it->second;
             g_rc_held[dev] -= it->first;
             m.erase(it);
-            return p;
+            SJ_CUDA(cudaStreamWaitEvent(s, c.ev, 0));       // the previous owner's reads are done
+            event_put(dev, c.ev);
+            return c.p;
         }
     }
     void *p = dev_alloc(bytes, s);
@@ -152,22 +193,44 @@ void *result_buffer_get(int dev, size_t bytes, cudaStream_t s)
 void result_buffer_put(int dev, void *p, cudaStream_t s)
 {
     if (!p) return;
-    size_t bytes = 0;
     {
         std::lock_guard<std::mutex> lk(g_rc_mu);
         auto it = g_rc_size.find(p);
-        if (it != g_rc_size.end() && g_rc_held[dev] + it->second <= kResultCacheBytes) {
-            g_rc[dev].emplace(it->second, p);
-            g_rc_held[dev] += it->second;
-            return;
+        if (it != g_rc_size.end() && g_rc_held[dev] + it->second <= g_rc_limit) {
+            cudaEvent_t ev = event_get(dev);
+            if (cudaEventRecord(ev, s ? s : cudaStreamLegacy) == cudaSuccess) {
+                g_rc[dev].emplace(it->second, CachedBuf{p, ev});
+                g_rc_held[dev] += it->second;
+                return;
+            }
+            cudaGetLastError();
+            event_put(dev, ev);
         }
-        if (it != g_rc_size.end()) {
-            bytes = it->second;
-            g_rc_size.erase(it);
+        if (it != g_rc_size.end()) g_rc_size.erase(it);
+    }
+    dev_free(p, s ? s : cudaStreamLegacy);
+}
+
+void result_cache_trim(int dev)
+{
+    std::vector<CachedBuf> drop;
+    {
+        std::lock_guard<std::mutex> lk(g_rc_mu);
+        for (auto &kv : g_rc) {
+            if (dev >= 0 && kv.first != dev) continue;
+            for (auto &e : kv.second) {
+                g_rc_size.erase(e.second.p);
+                drop.push_back(e.second);
+            }
+            kv.second.clear();
+            g_rc_held[kv.first] = 0;
         }
     }
-    (void)bytes;
-    dev_free(p, s);
+    for (auto &c : drop) {
+        cudaEventSynchronize(c.ev);
+        cudaFree(c.p);             // pool memory: cudaFree of a cudaMallocAsync block is synchronous and valid
+        cudaEventDestroy(c.ev);
+    }
 }
 
 int device_count()
@@ -201,6 +264,7 @@ int device_sm_count(int dev)
 
 void *scratch_acquire(int dev, size_t bytes)
 {
+    if (alloc_hook_set()) return nullptr;      // scratch goes through the hook (dev_alloc) too
     std::lock_guard<std::mutex> lk(g_scr_mu);
     ScratchSlot &sl = g_scr[dev];
     if (sl.busy) return nullptr;
@@ -225,6 +289,19 @@ void scratch_release(int dev, void *p)
     std::lock_guard<std::mutex> lk(g_scr_mu);
     ScratchSlot &sl = g_scr[dev];
     if (sl.p == p) sl.busy = false;
+}
+
+void scratch_trim(int dev)
+{
+    std::lock_guard<std::mutex> lk(g_scr_mu);
+    for (auto &kv : g_scr) {
+        if (dev >= 0 && kv.first != dev) continue;
+        ScratchSlot &sl = kv.second;
+        if (sl.busy || !sl.p) continue;
+        cudaFree(sl.p);
+        sl.p = nullptr;
+        sl.bytes = 0;
+    }
 }
 
 void set_max_dyn_smem(const void *func, int bytes)

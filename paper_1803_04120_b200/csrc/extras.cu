@@ -53,6 +53,7 @@ void result_to_csr_impl(const sj_result *r, uint64_t n_points, uint64_t *row_off
 {
     if (!r) fail(SJ_ERR_STATE, "result is NULL");
     if (n_points == 0 || n_points >= (1ull << 32)) fail(SJ_ERR_ARG, "n_points must satisfy 1 <= n < 2^32");
+    if (n_points < r->n_points) fail(SJ_ERR_ARG, "n_points is smaller than the N of the joined point set");
     if (!row_offsets || (!neighbors && r->total)) fail(SJ_ERR_ARG, "NULL output array");
     if (r->total >= (1ull << 32)) fail(SJ_ERR_ARG, "CSR of >= 2^32 pairs is not supported");
     SJ_CUDA(cudaSetDevice(r->device));
@@ -86,6 +87,93 @@ void result_to_csr_impl(const sj_result *r, uint64_t n_points, uint64_t *row_off
         SJ_LAUNCHED();
     }
     SJ_CUDA(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------------------ result fingerprints
+// Order-independent fingerprints of the pair multiset:
+//   F_a = sum_x mix_a(x), F_b = sum_x mix_b(x) (mod 2^64), mix_a = SplitMix64 output function of
+//   x + 0x9E3779B97F4A7C15, mix_b = MurmurHash3 fmix64 of x ^ 0xC2B2AE3D27D4EB4F;
+// optionally the per-key counts cnt[x >> 32].  One pass over every batch (device memory, or pinned
+// host memory read in place over PCIe through its UVA mapping).  The oracle computes the same
+// fingerprints from its own join (oracle/sj_oracle.c orc_grid_digest), so results of tens of GB
+// are compared without being held twice.
+namespace {
+__device__ __forceinline__ uint64_t fp_mix_a(uint64_t x)
+{
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t fp_mix_b(uint64_t x)
+{
+    uint64_t k = x ^ 0xC2B2AE3D27D4EB4Full;
+    k ^= k >> 33;
+    k *= 0xFF51AFD7ED558CCDull;
+    k ^= k >> 33;
+    k *= 0xC4CEB9FE1A85EC53ull;
+    k ^= k >> 33;
+    return k;
+}
+
+__global__ void __launch_bounds__(256)
+k_fingerprint(const uint64_t *__restrict__ pairs, uint64_t n, unsigned long long *__restrict__ acc,
+              uint32_t *__restrict__ counts, uint64_t n_points, uint32_t *__restrict__ bad)
+{
+    uint64_t fa = 0, fb = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = pairs[i];
+        fa += fp_mix_a(x);
+        fb += fp_mix_b(x);
+        if (counts) {
+            const uint64_t key = x >> 32;
+            if (key < n_points) atomicAdd(counts + key, 1u);
+            else atomicOr(bad, 1u);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        fa += __shfl_xor_sync(0xffffffffu, fa, o);
+        fb += __shfl_xor_sync(0xffffffffu, fb, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(acc + 0, (unsigned long long)fa);       // wraps mod 2^64: the definition
+        atomicAdd(acc + 1, (unsigned long long)fb);
+    }
+}
+}  // namespace
+
+void result_fingerprint_impl(const sj_result *r, uint64_t *fp, uint32_t *counts)
+{
+    if (!r) fail(SJ_ERR_STATE, "result is NULL");
+    if (!fp) fail(SJ_ERR_ARG, "fp is NULL");
+    SJ_CUDA(cudaSetDevice(r->device));
+    CtxGuard cg{acquire_ctx(r->device, 1, 0, 64)};
+    cudaStream_t s = cg.c->streams[0];
+    unsigned long long *dacc = static_cast<unsigned long long *>(cg.c->d_slots);
+    unsigned long long *hacc = static_cast<unsigned long long *>(cg.c->h_slots);
+    SJ_CUDA(cudaMemsetAsync(dacc, 0, 4 * sizeof(unsigned long long), s));
+    if (counts) SJ_CUDA(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * r->n_points, s));
+    const int nsm = device_sm_count(r->device);
+    uint32_t *bad = reinterpret_cast<uint32_t *>(dacc + 2);
+    for (const auto &b : r->batches) {
+        if (!b.n) continue;
+        const uint64_t *src = b.pairs;
+        if (!b.on_device) {
+            void *dp = nullptr;
+            SJ_CUDA(cudaHostGetDevicePointer(&dp, const_cast<uint64_t *>(b.pairs), 0));
+            src = static_cast<const uint64_t *>(dp);
+        }
+        const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((b.n + 255) / 256, (uint64_t)nsm * 8));
+        k_fingerprint<<<grid, 256, 0, s>>>(src, b.n, dacc, counts, r->n_points, bad);
+        SJ_LAUNCHED();
+    }
+    SJ_CUDA(cudaMemcpyAsync(hacc, dacc, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaStreamSynchronize(s));
+    if (hacc[2] & 0xffffffffull) fail(SJ_ERR_STATE, "a pair's key is >= the result's n_points (corrupt result)");
+    fp[0] = hacc[0];
+    fp[1] = hacc[1];
 }
 
 // ------------------------------------------------------------------ f3: brute force
@@ -185,6 +273,7 @@ sj_result *brute_force_impl(const double *points, uint64_t n, int d, double eps,
     Slot *dslot = static_cast<Slot *>(cg.c->d_slots), *hslot = static_cast<Slot *>(cg.c->h_slots);
     sj_result *res = new sj_result();
     res->device = bo.device;
+    res->n_points = n;
     try {
         uint64_t cap = std::max<uint64_t>(n * 8, 1024);
         for (int attempt = 0; attempt < 2; ++attempt) {

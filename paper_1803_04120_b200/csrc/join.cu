@@ -23,9 +23,11 @@ namespace {
 void launch_dense(const DevIndex &ix, const JoinArgs &ja, bool unicomp, cudaStream_t s)
 {
     if (!ja.dense_T || ix.n_dense_tasks == 0) return;
-    // tasks intersecting [q0, q1): at most (q1 - q0) / dense_T + 2 (each task holds >= dense_T queries
-    // of its cell, except cell tails), starting at t_lo found on the device
-    const uint64_t max_tasks = std::min<uint64_t>(ix.n_dense_tasks, (uint64_t)(ja.q1 - ja.q0) / ix.dense_T + 2);
+    // tasks intersecting [q0, q1): a whole cell of m >= dense_T points has ceil(m/32) <= m/dense_T
+    // tasks, and the two cells cut by the batch ends add at most 2 more each; the kernel strides
+    // over its task range anyway (k_refine_dense), so this only sizes the launch
+    const uint64_t max_tasks =
+        std::min<uint64_t>(ix.n_dense_tasks, (uint64_t)(ja.q1 - ja.q0 + ix.dense_T - 1) / ix.dense_T + 4);
     const dim3 grid((uint32_t)((max_tasks + kDenseWarps - 1) / kDenseWarps)), block(32 * kDenseWarps);
     const size_t smem = sizeof(uint64_t) * kDenseWarps * kWarpBufPairs;
 #define SJ_DENSE_CASE(DD)                                                                              \
@@ -329,6 +331,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     tr.mark("acquire ctx");
     sj_result *res = new sj_result();
     res->device = idx->device;
+    res->n_points = idx->view.n;
     sj_stats &stats = res->stats;
     // self pairs of a batch [a, b): written at fixed slots, counted on the host (see JoinArgs::nself)
     auto nself_of = [&](uint64_t a, uint64_t b) -> uint64_t { return o.include_self ? b - a : 0; };
@@ -573,6 +576,63 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     }
     stats.total_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
     return res;
+}
+
+// Multi-GPU shard plan (north_star "Partitioning"): contiguous A-order query ranges
+// balanced by the a5 sampled estimate -- per planning bucket, estimated pairs plus kQueryWeight per
+// query (the per-query search cost, in units of emitted pairs) -- cut where the cumulative weight
+// crosses multiples of total/world, interpolated by query count inside a bucket.  Uses the build's
+// estimate of the default join when it carries one, else runs the estimate now.
+void plan_shards_impl(const sj_index *idx, uint32_t world, uint64_t *cuts)
+{
+    if (!idx) fail(SJ_ERR_STATE, "index is NULL");
+    if (world < 1 || !cuts) fail(SJ_ERR_ARG, "world must be >= 1 and cuts non-NULL");
+    const uint64_t n = idx->view.n;
+    constexpr double kQueryWeight = 4.0;
+    EstimateShape es;
+    std::vector<unsigned long long> bk;
+    if (idx->spec_est_valid) {
+        es = idx->spec_shape;
+        bk = idx->spec_buckets;
+    } else {
+        SJ_CUDA(cudaSetDevice(idx->device));
+        es = estimate_shape(n);
+        const size_t bytes = 8 * (size_t)(es.nbk + 1);
+        CtxGuard cg{acquire_ctx(idx->device, 1, 0, bytes)};
+        cudaStream_t s = cg.c->streams[0];
+        auto *dbk = static_cast<unsigned long long *>(cg.c->d_slots);
+        SJ_CUDA(cudaMemsetAsync(dbk, 0, bytes, s));
+        sj_join_opts o;
+        sj_join_opts_default(&o);
+        launch_estimate(idx->dev, idx->device, o, 0, n, es, dbk, s);
+        SJ_CUDA(cudaMemcpyAsync(cg.c->h_slots, dbk, 8 * es.nbk, cudaMemcpyDeviceToHost, s));
+        SJ_CUDA(cudaStreamSynchronize(s));
+        const auto *h = static_cast<const unsigned long long *>(cg.c->h_slots);
+        bk.assign(h, h + es.nbk);
+    }
+    const uint64_t width = std::max<uint64_t>(1, es.step * es.group);
+    const uint64_t nbk = (n + width - 1) / width;
+    std::vector<double> cum(nbk + 1, 0.0);
+    for (uint64_t i = 0; i < nbk; ++i) {
+        const uint64_t a = i * width, b = std::min(n, a + width);
+        const double est = i < bk.size() ? (double)bk[i] * (double)es.step : 0.0;
+        cum[i + 1] = cum[i] + est + kQueryWeight * (double)(b - a);
+    }
+    const double W = cum[nbk];
+    cuts[0] = 0;
+    uint64_t i = 0;
+    for (uint32_t r = 1; r < world; ++r) {
+        const double t = W * (double)r / (double)world;
+        while (i < nbk && cum[i + 1] < t) ++i;
+        uint64_t c = n;
+        if (i < nbk) {
+            const uint64_t a = i * width, b = std::min(n, a + width);
+            const double f = cum[i + 1] > cum[i] ? (t - cum[i]) / (cum[i + 1] - cum[i]) : 0.0;
+            c = a + (uint64_t)std::llround(f * (double)(b - a));
+        }
+        cuts[r] = std::max(cuts[r - 1], std::min(c, n));
+    }
+    cuts[world] = n;
 }
 
 void neighbor_counts_impl(const sj_index *idx, const sj_join_opts &o, uint32_t *cnt, uint64_t *total)

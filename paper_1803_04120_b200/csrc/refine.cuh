@@ -678,27 +678,34 @@ k_refine_dense(const DevIndex ix, const JoinArgs ja)
     __shared__ TopTable tt;
     extern __shared__ __align__(16) uint64_t s_buf[];     // [kDenseWarps][kWarpBufPairs]
     if (ix.search_mode == kSearchCellScan) build_top_table<D>(ix, tt);
-    // the batch's tasks are the contiguous range [t_lo, t_hi) of the A-ordered task list: tasks
-    // with start + 32 > q0 and start < q1 (one binary search per CTA)
+    // the batch's tasks are the contiguous range of the A-ordered task list whose real end
+    // min(start + 32, end of its cell) lies after q0 and whose start lies before q1.  Task ends are
+    // monotone in the task index (tasks of a cell are consecutive, cells are in A-order), so t_lo
+    // is one binary search per CTA; the warps then stride over the tasks until start >= q1, so the
+    // launch size is only a hint (tails of cells make tasks shorter than dense_T queries).
     __shared__ uint32_t s_tlo;
     if (threadIdx.x == 0) {
         uint32_t lo = 0, hi = ja.n_dense_tasks;
         while (lo < hi) {
             const uint32_t mid = (lo + hi) >> 1;
-            if (__ldg(ja.dense_tasks + mid) + 32u <= ja.q0) lo = mid + 1;
+            const uint32_t st = __ldg(ja.dense_tasks + mid);
+            const uint32_t en = min(st + 32u, __ldg(ix.G + __ldg(ix.pcell + st) + 1));
+            if (en <= ja.q0) lo = mid + 1;
             else hi = mid;
         }
         s_tlo = lo;
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t task = s_tlo + blockIdx.x * kDenseWarps + warp;
     QueryState<D> q;
     q.G = 1u;
     q.sub = 0u;
     q.emitted = q.probes = q.tests = 0;
-    if (task < ja.n_dense_tasks) {                     // warp-uniform
+#pragma unroll 1
+    for (uint32_t task = s_tlo + blockIdx.x * kDenseWarps + warp; task < ja.n_dense_tasks;
+         task += gridDim.x * kDenseWarps) {            // warp-uniform
         const uint32_t start = __ldg(ja.dense_tasks + task);
+        if (start >= ja.q1) break;
         const uint32_t h = __ldg(ix.pcell + start);
         const uint32_t end = min(start + 32u, __ldg(ix.G + h + 1));
         const uint32_t a = max(start, ja.q0), b = min(end, ja.q1);

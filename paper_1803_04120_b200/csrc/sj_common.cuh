@@ -47,6 +47,7 @@ void *dev_alloc(size_t bytes, cudaStream_t s);
 void dev_free(void *p, cudaStream_t s);
 void *host_pinned_alloc(size_t bytes, size_t *granted);   // pooled pinned memory
 void host_pinned_free(void *p);
+void host_pinned_trim();              // release every cached pinned block
 
 template <class T>
 T *dalloc(size_t count, cudaStream_t s) { return static_cast<T *>(dev_alloc(count * sizeof(T), s)); }
@@ -202,6 +203,7 @@ struct sj_result {
     std::vector<sj_batch> batches;
     sj_stats stats{};
     uint64_t total = 0;
+    uint64_t n_points = 0;       // N of the index / point set the pairs' ids refer to
 };
 
 namespace sj {
@@ -220,8 +222,15 @@ DevCtx *acquire_ctx(int dev, int nstreams, int nevents, size_t slot_bytes);
 void set_max_dyn_smem(const void *func, int bytes);
 int device_count();                            // cached cudaGetDeviceCount (0 on error)
 bool alloc_hook_set();                         // api.cu: a user allocator hook is installed
-void *result_buffer_get(int dev, size_t bytes, cudaStream_t s);   // device batch buffers (cached)
+// device batch buffers, cached per device up to a limit (sj_set_result_cache_limit).  put() records
+// an event on the freeing stream (cudaStreamLegacy when none is given, which orders after the
+// caller's work on blocking streams such as torch's default stream); get() makes the new owner's
+// stream wait for it, so a reused buffer is never written while the old owner still reads it.
+void *result_buffer_get(int dev, size_t bytes, cudaStream_t s);
 void result_buffer_put(int dev, void *p, cudaStream_t s);
+void result_cache_trim(int dev);                 // free every cached buffer of dev (-1: all devices)
+void set_result_cache_limit(size_t bytes);
+void scratch_trim(int dev);
 int device_sm_count(int dev);                  // cached multiprocessor count
 void *scratch_acquire(int dev, size_t bytes);   // nullptr if busy (use the pool instead)
 void scratch_release(int dev, void *p);
@@ -260,12 +269,14 @@ void inclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStrea
 // extras.cu
 void sort_pairs_device(uint64_t *pairs, uint64_t n, uint64_t n_points, cudaStream_t s);
 void result_to_csr_impl(const sj_result *r, uint64_t n_points, uint64_t *row_offsets, uint32_t *neighbors);
+void result_fingerprint_impl(const sj_result *r, uint64_t *fp, uint32_t *counts);
 sj_result *brute_force_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &bo,
                             const sj_join_opts &jo);
 
 // join.cu
 sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o);
 void neighbor_counts_impl(const sj_index *idx, const sj_join_opts &o, uint32_t *cnt, uint64_t *total);
+void plan_shards_impl(const sj_index *idx, uint32_t world, uint64_t *cuts);
 EstimateShape estimate_shape(uint64_t nq);
 void launch_estimate(const DevIndex &ix, int device, const sj_join_opts &o, uint64_t q0, uint64_t q1,
                      const EstimateShape &es, unsigned long long *dbk, cudaStream_t s);

@@ -91,6 +91,16 @@ def load_library(path: str = LIB_PATH):
     L.sj_self_join.restype = i32
     L.sj_free_result.argtypes = [vp]
     L.sj_free_result.restype = None
+    L.sj_free_result_async.argtypes = [vp, vp]
+    L.sj_free_result_async.restype = None
+    L.sj_result_fingerprint.argtypes = [vp, vp, vp]
+    L.sj_result_fingerprint.restype = i32
+    L.sj_plan_shards.argtypes = [vp, u32, vp]
+    L.sj_plan_shards.restype = i32
+    L.sj_trim.argtypes = [i32]
+    L.sj_trim.restype = i32
+    L.sj_set_result_cache_limit.argtypes = [u64]
+    L.sj_set_result_cache_limit.restype = None
     L.sj_free_index.argtypes = [vp]
     L.sj_free_index.restype = None
     L.sj_result_info.argtypes = [vp, P(u64), P(u32), P(Stats)]
@@ -347,9 +357,31 @@ class Result:
                                                ctypes.c_void_p(nbrs.data_ptr())))
         return offsets, nbrs[:self.n_pairs]
 
-    def free(self):
+    def fingerprint(self, counts: bool = False, n_points: Optional[int] = None):
+        """sj_result_fingerprint -> (F_a, F_b) of the pair multiset, and with counts=True also the
+        per-key counts (torch uint32 on the device, n_points entries = the joined N)."""
+        fp = (ctypes.c_uint64 * 2)()
+        cnt = None
+        if counts:
+            import torch
+            dev = self.device if self.device is not None else 0
+            cnt = torch.empty(int(n_points), dtype=torch.uint32, device=f"cuda:{dev}")
+        _check(load_library().sj_result_fingerprint(self._h, fp, ctypes.c_void_p(cnt.data_ptr()) if counts else None))
+        return (int(fp[0]), int(fp[1]), cnt) if counts else (int(fp[0]), int(fp[1]))
+
+    def free(self, stream=None):
+        """Release the result; its device buffers are reused only after the work queued on
+        `stream` (default: torch's current stream of the result's device) completed."""
         if self._h and self._h.value:
-            load_library().sj_free_result(self._h)
+            L = load_library()
+            st = stream
+            if st is None and self.device is not None:
+                try:
+                    import torch
+                    st = torch.cuda.current_stream(self.device).cuda_stream
+                except Exception:
+                    st = None
+            L.sj_free_result_async(self._h, ctypes.c_void_p(st) if st else None)
             self._h = ctypes.c_void_p(0)
 
     def __del__(self):
@@ -357,6 +389,15 @@ class Result:
             self.free()
         except Exception:
             pass
+
+
+def trim(device: int = -1):
+    """sj_trim: release the library's caches (result batches, build scratch, pinned blocks, pool)."""
+    _check(load_library().sj_trim(int(device)))
+
+
+def set_result_cache_limit(nbytes: int):
+    load_library().sj_set_result_cache_limit(int(nbytes))
 
 
 def self_join(index: Index, unicomp: bool = True, include_self: bool = True,
@@ -420,6 +461,13 @@ def brute_force_join(points, eps: float, include_self: bool = True, result_on_ho
     r = Result(h.value)
     r.device = bo.device
     return r
+
+
+def plan_shards(index: Index, world: int) -> np.ndarray:
+    """sj_plan_shards: A-order query cuts (world + 1 entries) balanced by the sampled estimate."""
+    cuts = np.zeros(int(world) + 1, dtype=np.uint64)
+    _check(load_library().sj_plan_shards(index.handle, int(world), cuts.ctypes.data))
+    return cuts.astype(np.int64)
 
 
 def import_index(view: IndexView, device: int) -> Index:

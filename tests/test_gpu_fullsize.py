@@ -1,0 +1,150 @@
+"""Full-size parity on every BASELINE.json config and eps.
+
+The bar is bit-exactness of the pair SET S (PAPER.md:128-130 definition; the paper itself validates
+by total neighbour counts only):
+  * results small enough to hold twice (C2 3..6-D, C3 eps <= 12): the GPU's canonical-sorted pairs
+    are compared with the oracle's (oracle.grid_join) element by element;
+  * larger results (C2 2-D, C3 eps >= 16, every C4 eps, C5): |S|, the two order-independent
+    fingerprints F_a / F_b of the pair multiset and the fingerprint F_c of the per-key count
+    vector, computed on the device over all batches (sj_result_fingerprint), against the oracle's
+    (orc_grid_digest; stored in tests/golden/fingerprints.json by tools/make_golden_fingerprints.py,
+    which calls only oracle/ and datagen/);
+  * plus exact rows of the queries that stress the path most: the largest-count queries and the
+    queries of the most populous cell (oracle.rows: brute force over all N points).
+Every join runs in the launch configuration bench.py times (default options).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import datagen
+import fingerprints as F
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fingerprints.json")))
+
+
+@pytest.fixture(scope="module")
+def sj():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1803_04120_b200 as m
+    m.load_library()
+    return m
+
+
+_CACHE = {}
+
+
+def points(cfg, d):
+    """The config's seeded array (one dataset cached at a time: C4/C5 are 0.4-0.8 GB)."""
+    key = (cfg, d)
+    if key not in _CACHE:
+        _CACHE.clear()
+        P = datagen.skewed(15_228_633, d) if cfg == "C4" else datagen.uniform_config(cfg, d)
+        _CACHE[key] = (P, torch.from_numpy(P).cuda())
+    return _CACHE[key]
+
+
+def gpu_rows(res, qids):
+    """Rows (sorted pairs) of the given original query ids, gathered batch by batch on the device."""
+    qt = torch.from_numpy(np.asarray(qids, dtype=np.int64)).cuda()
+    got = []
+    for b in res.batches():
+        bt = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.asarray(b)).cuda()
+        b64 = bt.view(torch.int64)
+        sel = torch.isin(b64 >> 32, qt)
+        got.append(b64[sel].cpu().numpy().view(np.uint64))
+        del sel, b64
+    return np.sort(np.concatenate(got)) if got else np.empty(0, np.uint64)
+
+
+def stress_queries(idx, cnt, k=24, seed=0):
+    """Original ids of the k largest-count queries, up to k queries of the most populous cell and
+    k random ones (rows from the largest cells and largest counts, not uniform)."""
+    c = cnt.cpu().numpy()
+    top = np.argsort(c, kind="stable")[-k:]
+    arr = idx.arrays()
+    G = arr["G"].cpu().numpy().astype(np.int64)
+    h = int(np.argmax(np.diff(G)))
+    A = arr["A"].cpu().numpy().astype(np.int64)
+    dense = A[G[h]:G[h] + k]
+    rnd = np.random.default_rng(seed).integers(0, len(c), k)
+    return np.unique(np.concatenate([top, dense, rnd]))
+
+
+def check_rows(P, eps, res, idx, cnt):
+    q = stress_queries(idx, cnt)
+    want_cnt, want = oracle.rows(P, eps, q)
+    got = gpu_rows(res, q)
+    assert np.array_equal(got, want)
+    assert np.array_equal(cnt.cpu().numpy()[q].astype(np.int64), want_cnt)
+
+
+# ------------------------------------------------------------------ full pair sets
+FULL = [("C2", d, 1.0) for d in (3, 4, 5, 6)] + [("C3", 6, e) for e in (2.0, 4.0, 8.0, 12.0)]
+
+
+@pytest.mark.parametrize("cfg,d,eps", FULL, ids=[f"{c}-d{d}-eps{e:g}" for c, d, e in FULL])
+def test_full_pair_set_equals_oracle(sj, cfg, d, eps):
+    """Canonical-sorted GPU pairs == oracle.grid_join pairs, element by element (the headline
+    workload C2 6-D eps=1 included); the device fingerprints agree with the explicit set's."""
+    P, Pd = points(cfg, d)
+    idx = sj.build_index(Pd, eps)
+    res = sj.self_join(idx)
+    assert res.n_batches >= 3
+    got = res.to_numpy(sort=True)
+    want = oracle.grid_join(P, eps)
+    assert len(got) == len(want)
+    assert np.array_equal(got, want)
+    fa, fb, cnt = res.fingerprint(counts=True, n_points=len(P))
+    assert (fa, fb) == F.fingerprint(want)
+    assert np.array_equal(cnt.cpu().numpy().astype(np.int64), oracle.pair_counts(want, len(P)))
+    res.free()
+
+
+# ------------------------------------------------------------------ fingerprints vs golden
+@pytest.mark.parametrize("key", sorted(GOLD))
+def test_fingerprints_equal_oracle(sj, key):
+    """|S|, F_a, F_b (pair multiset) and F_c (per-key counts) of the whole GPU result == the
+    oracle's, plus exact stress rows.  C4 2-D eps=0.02 is the 3.0e9-pair, many-batch case."""
+    g = GOLD[key]
+    cfg, d, eps = g["config"], g["d"], g["eps"]
+    P, Pd = points(cfg, d)
+    assert len(P) == g["n"]
+    idx = sj.build_index(Pd, eps)
+    res = sj.self_join(idx)
+    assert res.n_pairs == g["pairs"]
+    assert res.n_batches >= 3
+    fa, fb, cnt = res.fingerprint(counts=True, n_points=len(P))
+    assert f"{fa:016x}" == g["fa"] and f"{fb:016x}" == g["fb"]
+    assert f"{F.count_fingerprint(cnt.cpu().numpy()):016x}" == g["fc"]
+    check_rows(P, eps, res, idx, cnt)
+    res.free()
+
+
+def test_c4_weighted_shards_union_equals_oracle(sj):
+    """Multi-GPU partitioning on skewed data: shards planned by the sampled estimate
+    (sj_plan_shards) are joined separately; their fingerprints add up to the oracle's S and the
+    estimated work is spread (no shard holds more than twice its share of the pairs)."""
+    g = GOLD["C4/d2/eps0.005"]
+    P, Pd = points("C4", 2)
+    idx = sj.build_index(Pd, g["eps"])
+    for world in (2, 4, 8):
+        cuts = sj.plan_shards(idx, world)
+        assert cuts[0] == 0 and cuts[-1] == len(P) and np.all(np.diff(cuts) >= 0)
+        fa = fb = n = 0
+        sizes = []
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            r = sj.self_join(idx, query_begin=int(a), query_end=int(b))
+            x, y = r.fingerprint()
+            fa, fb, n = (fa + x) % 2**64, (fb + y) % 2**64, n + r.n_pairs
+            sizes.append(r.n_pairs)
+            r.free()
+        assert n == g["pairs"] and f"{fa:016x}" == g["fa"] and f"{fb:016x}" == g["fb"]
+        assert max(sizes) <= 2.0 * g["pairs"] / world, sizes

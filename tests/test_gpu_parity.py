@@ -238,52 +238,6 @@ def test_c1_config_exact(sj):
         assert np.array_equal(got, want)
 
 
-# ------------------------------------------------------------------ full-size sampled parity
-def _sampled_rows_check(sj, pts, eps, nsample=64, seed=0, **kw):
-    n = len(pts)
-    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
-    res = sj.self_join(idx, **kw)
-    rng = np.random.default_rng(seed)
-    q = np.unique(rng.integers(0, n, nsample))
-    cnt, want = oracle.rows(pts, eps, q)
-    qt = torch.from_numpy(q.astype(np.int64)).cuda()
-    got = []
-    for b in res.batches():
-        bt = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.asarray(b)).cuda()
-        b64 = bt.view(torch.int64)
-        sel = torch.isin(b64 >> 32, qt)
-        got.append(b64[sel].cpu().numpy().view(np.uint64))
-    got = np.sort(np.concatenate(got)) if got else np.empty(0, np.uint64)
-    assert np.array_equal(got, want)
-    return res
-
-
-@pytest.mark.parametrize("d", [2, 3, 4, 5, 6])
-def test_c2_full_size_sampled_rows(sj, d):
-    """BASELINE.json configs[1] (Syn-dD 2M, eps=1) at full size, in the bench's launch
-    configuration: sampled neighbour rows == oracle brute-force rows; |S| vs P4 expectation."""
-    pts = datagen.uniform_config("C2", d)
-    res = _sampled_rows_check(sj, pts, 1.0, nsample=48, seed=d)
-    exp = oracle.expected_pairs_uniform(len(pts), d, 1.0)
-    assert abs(res.n_pairs - exp) / exp < 0.01
-
-
-def test_c2_6d_total_equals_oracle_count(sj):
-    """Total |S| for the bench workload equals the oracle's exact count (grid join)."""
-    pts = datagen.uniform_config("C2", 6)
-    want = int(oracle.grid_join(pts, 1.0, count_only=True).sum())
-    idx = sj.build_index(torch.from_numpy(pts).cuda(), 1.0)
-    assert sj.self_join(idx).n_pairs == want
-    cnt, tot = sj.neighbor_counts(idx)
-    assert tot == want
-
-
-def test_c3_eps8_sampled_rows(sj):
-    """C3 (Syn-6D 2M, eps=8): sampled rows exact."""
-    pts = datagen.uniform_config("C3", 6)
-    _sampled_rows_check(sj, pts, 8.0, nsample=32, seed=8)
-
-
 def _gapped(n, d, seed):
     """Points in separated slabs: whole coordinate columns of the grid are empty, so the
     masks M_j actually remove adjacent coordinates."""
@@ -343,40 +297,6 @@ def test_lanes_per_query_invariance(sj, d, n, eps):
             assert np.array_equal(got, want), (G, unicomp)
         cnt, tot = sj.neighbor_counts(idx, lanes_per_query=G)
         assert tot == len(want)
-
-
-# ------------------------------------------------------------------ full-size configs C3, C4, C5
-@pytest.mark.parametrize("eps", [16.0, 24.0])
-def test_c3_eps_sweep_sampled_rows(sj, eps):
-    """C3 (Syn-6D 2M): eps=16 (~1 buffer of 2^28 pairs) and eps=24 (~9.5 buffers, 20 GB):
-    sampled rows exact, batching engaged (k > 3 at eps=24), total within 1% of the P4
-    expectation."""
-    pts = datagen.uniform_config("C3", 6)
-    res = _sampled_rows_check(sj, pts, eps, nsample=24, seed=int(eps))
-    exp = oracle.expected_pairs_uniform(len(pts), 6, eps)
-    assert abs(res.n_pairs - exp) / exp < 0.01
-    if eps == 24.0:
-        assert res.n_batches > 3
-
-
-@pytest.mark.parametrize("d,eps", [(2, 0.005), (3, 0.1)])
-def test_c4_skewed_sampled_rows(sj, d, eps):
-    """C4 (skewed 15.2M-point cloud, real-data stand-in): sampled rows exact, including rows of
-    queries from the densest cells (heavy skew tail)."""
-    pts = datagen.skewed(15_228_633, d)
-    _sampled_rows_check(sj, pts, eps, nsample=48, seed=d)
-
-
-@pytest.mark.parametrize("d,eps", [(4, 2.0), (6, 8.0)])
-def test_c5_16m_sampled_rows_and_shards(sj, d, eps):
-    """C5 (16M uniform): sampled rows exact on the full join, and the union of 4 query shards
-    has exactly the full join's size (what each GPU of the scaling run computes)."""
-    pts = datagen.uniform_config("C5", d)
-    res = _sampled_rows_check(sj, pts, eps, nsample=24, seed=d)
-    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
-    cuts = np.linspace(0, len(pts), 5).astype(np.int64)
-    tot = sum(sj.self_join(idx, query_begin=int(a), query_end=int(b)).n_pairs for a, b in zip(cuts[:-1], cuts[1:]))
-    assert tot == res.n_pairs
 
 
 @pytest.mark.parametrize("kind,d,eps", [("uniform", 2, 3.0), ("uniform", 3, 9.0), ("clustered", 2, 0.4),
@@ -533,3 +453,74 @@ def test_tiny_inputs(sj, d):
             off, nb = res.to_csr(len(pts))
             keys = (want >> np.uint64(32)).astype(np.int64)
             assert np.array_equal(off.cpu().numpy(), np.concatenate([[0], np.cumsum(np.bincount(keys, minlength=len(pts)))]))
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_dense_tasks_small_batches(sj, host):
+    """Dense-cell tasks with batches of ~100 queries over runs of 16-25-point cells:
+    a batch intersects more tasks than (q1-q0)/dense_T when cell tails are short, and every one of
+    them must run (their self pairs sit in fixed slots)."""
+    n = 20000
+    pts = datagen.uniform(n, 2, seed=41)
+    eps = 3.16          # ~1000 cells of ~20 points (w ~ eps)
+    want = oracle.brute_force(pts, eps)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    per_query = len(want) / n
+    for nq in (37, 100, 230):
+        cap = int(nq * per_query * 1.3)
+        res = sj.self_join(idx, batch_capacity_pairs=cap, result_on_host=host)
+        assert res.n_batches > n // (2 * nq)
+        assert np.array_equal(res.to_numpy(), want), nq
+
+
+def test_fingerprint_device_and_host_batches(sj):
+    """sj_result_fingerprint over device batches and over pinned host batches (read through the UVA
+    mapping) equals the fingerprint of the oracle's explicit S; per-key counts too."""
+    import fingerprints as F
+    pts = datagen.clustered_small(6000, 3, seed=17)
+    eps = 0.5
+    want = oracle.brute_force(pts, eps)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+    for host in (False, True):
+        res = sj.self_join(idx, result_on_host=host, min_batches=4)
+        fa, fb, cnt = res.fingerprint(counts=True, n_points=len(pts))
+        assert (fa, fb) == F.fingerprint(want)
+        assert np.array_equal(cnt.cpu().numpy().astype(np.int64), oracle.pair_counts(want, len(pts)))
+        with pytest.raises(sj.SJError):
+            res.to_csr(len(pts) - 1)              # n_points below the joined N is rejected
+        res.free()
+
+
+def test_freed_buffers_reused_after_pending_reads(sj):
+    """A result freed while an async read of its zero-copy batch view is still queued: the next
+    join reuses the cached buffer only after that read completed (sj_free_result_async)."""
+    pts = datagen.uniform(300_000, 2, seed=8)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), 0.4)
+    # a different point set of the same shape: the next join writes different pairs into the buffers
+    idx2 = sj.build_index(torch.from_numpy(datagen.uniform(300_000, 2, seed=9)).cuda(), 0.4)
+    ref = sj.self_join(idx)
+    want = sum(int(b.view(torch.int64).sum().item()) for b in ref.batches())
+    ref.free()
+    side = torch.cuda.Stream()
+    for _ in range(3):
+        res = sj.self_join(idx)
+        with torch.cuda.stream(side):
+            torch.cuda._sleep(20_000_000)         # keep the side stream busy (~10 ms)
+            sums = [b.view(torch.int64).sum() for b in res.batches()]
+            res.free(stream=side.cuda_stream)
+        nxt = sj.self_join(idx2)                 # may get the same buffers from the cache
+        side.synchronize()
+        assert sum(int(x.item()) for x in sums) == want
+        nxt.free()
+
+
+def test_trim_and_cache_limit(sj):
+    pts = datagen.uniform(200_000, 3, seed=2)
+    idx = sj.build_index(torch.from_numpy(pts).cuda(), 2.0)
+    want = sj.self_join(idx).to_numpy()
+    sj.set_result_cache_limit(0)
+    r = sj.self_join(idx)
+    r.free()
+    sj.trim()
+    sj.set_result_cache_limit(48 << 30)
+    assert np.array_equal(sj.self_join(idx).to_numpy(), want)

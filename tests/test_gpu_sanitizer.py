@@ -1,0 +1,32 @@
+"""compute-sanitizer over the CUDA path (SURVEY §4 hygiene; PAPER.md:238 atomic emission):
+memcheck (out-of-bounds / misaligned global and shared accesses) and racecheck (shared-memory
+hazards: the dense kernel's per-warp emission buffers, the radix sort's warp counters, the bucket
+sorter) on C1 and two small 6-D clouds.  Each run must report 0 errors and its own parity check."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _sanitizer():
+    return shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+@pytest.mark.parametrize("case", ["c1", "clustered6", "sparse6"])
+def test_sanitizer_clean(tool, case):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "99", sys.executable,
+           os.path.join(ROOT, "tools", "sanitize_case.py"), case]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
+    assert f"sanitize case {case}: OK" in out

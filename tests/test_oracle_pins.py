@@ -228,6 +228,50 @@ def test_rows_and_query_ranges_match_full_join():
     assert np.array_equal(c, oracle.pair_counts(full, len(P)))                  # P6
 
 
+# ---------------------------------------------------------------- fingerprints (full-size parity)
+def test_fingerprint_mixers_match_published_values():
+    """mix_a is SplitMix64's output function: its first four outputs from state 0 are the
+    published e220a8397b1dcdaf, 6e789e6aa1b965f4, 06c45d188009454f, f88bb8a8724c81ec (Steele, Lea
+    & Flood 2014 reference implementation); mix_b is MurmurHash3's fmix64 (fmix64(0) = 0,
+    fmix64(1) = b456bcfc34c2cb2c) applied to x ^ 0xC2B2AE3D27D4EB4F."""
+    gamma = 0x9E3779B97F4A7C15
+    want = [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F, 0xF88BB8A8724C81EC]
+    assert [oracle.mix(0, (i * gamma) % 2**64) for i in range(4)] == want
+    assert oracle.mix(1, 0xC2B2AE3D27D4EB4F) == 0
+    assert oracle.mix(1, 1 ^ 0xC2B2AE3D27D4EB4F) == 0xB456BCFC34C2CB2C
+    import fingerprints
+    x = np.random.default_rng(1).integers(0, 2**63, 2000, dtype=np.uint64) * np.uint64(2) + np.uint64(1)
+    assert [int(v) for v in fingerprints.mix_a(x)] == [oracle.mix(0, int(v)) for v in x]
+    assert [int(v) for v in fingerprints.mix_b(x)] == [oracle.mix(1, int(v)) for v in x]
+
+
+@pytest.mark.parametrize("kind,d,n,eps", [("uniform", 2, 2000, 4.0), ("clustered", 3, 2500, 0.6),
+                                          ("knife", 4, 1500, 0.1), ("uniform", 6, 1500, 40.0)])
+def test_grid_digest_equals_brute_force_fingerprint(kind, d, n, eps):
+    """orc_grid_digest (|S|, F_a, F_b, F_c, per-query counts) equals the fingerprints of the brute
+    force's explicit S (P1), for any split of the queries (fingerprints add over query ranges)."""
+    P = {"uniform": datagen.uniform, "clustered": datagen.clustered_small}.get(kind, None)
+    P = P(n, d, 7 * n + d) if P else datagen.knife_edge(n, d, eps, 7 * n + d)
+    bf = oracle.brute_force(P, eps)
+    cnt = oracle.pair_counts(bf, n)
+    dg = oracle.grid_digest(P, eps, with_counts=True)
+    assert dg["pairs"] == len(bf) and np.array_equal(dg["counts"], cnt)
+    import fingerprints
+    assert (dg["fa"], dg["fb"]) == fingerprints.fingerprint(bf)
+    assert dg["fc"] == fingerprints.count_fingerprint(cnt)
+    parts = [oracle.grid_digest(P, eps, q0=a, q1=b) for a, b in ((0, n // 3), (n // 3, n - 1), (n - 1, n))]
+    M = 2**64
+    assert sum(p["pairs"] for p in parts) == dg["pairs"]
+    for key in ("fa", "fb", "fc"):
+        assert sum(p[key] for p in parts) % M == dg[key]
+    # a single dropped, added or altered pair changes both fingerprints
+    assert fingerprints.fingerprint(bf[1:]) != fingerprints.fingerprint(bf)
+    alt = bf.copy()
+    alt[len(alt) // 2] ^= np.uint64(1)
+    fa, fb = fingerprints.fingerprint(alt)
+    assert fa != dg["fa"] and fb != dg["fb"]
+
+
 # ---------------------------------------------------------------- expectation (P4)
 @pytest.mark.parametrize("d,eps,tol", [(2, 2.5, 0.01), (3, 8.0, 0.02), (4, 20.0, 0.03),
                                        (6, 40.0, 0.04)])

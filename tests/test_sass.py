@@ -1,0 +1,50 @@
+"""SASS hygiene of the built library (CPU only: cuobjdump reads the sm_100a cubins).
+
+The accept/reject decision s <= fl(eps^2) must be evaluated with one rounding per -, * and + in
+left-to-right order (PAPER.md:130 predicate; reading R1): a fused multiply-add (DFMA)
+anywhere in a kernel that evaluates the predicate would round differently from the oracle.  Every
+such kernel (refine, dense refine, brute force) must contain DADD/DMUL and no DFMA.  (k_keys may use
+DFMA: it sits inside __ddiv_rn's correctly rounded division, which is exact IEEE division.)
+"""
+import re
+import shutil
+import subprocess
+
+import pytest
+
+PREDICATE_KERNELS = re.compile(r"k_refine|k_refine_dense|k_brute_force")
+
+
+@pytest.fixture(scope="module")
+def sass():
+    from paper_1803_04120_b200 import build as b
+    lib = b.build()
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([tool, "-sass", lib], capture_output=True, text=True, check=True).stdout
+    funcs, cur = {}, None
+    for line in out.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+        elif cur:
+            funcs[cur].append(line)
+    return funcs
+
+
+def test_library_is_sm100a(sass):
+    assert len(sass) > 20
+
+
+def test_no_fma_in_predicate_kernels(sass):
+    checked = 0
+    for name, lines in sass.items():
+        if not PREDICATE_KERNELS.search(name):
+            continue
+        body = "\n".join(lines)
+        assert not re.search(r"\bDFMA\b", body), f"DFMA in {name}"
+        assert re.search(r"\bDADD\b", body) and re.search(r"\bDMUL\b", body), name
+        checked += 1
+    # refine: 5 dims x (emit/count-query/count-point) x unicomp on/off (+ 6-CTA variants);
+    # dense refine: 5 x 2; brute force: 5
+    assert checked >= 30, checked
