@@ -4,21 +4,27 @@ pairs/s, Syn-6D 2M pts, at 1/2/4/8 B200").
 
 Workload (config.workload): Syn-6D, N = 2,000,000 iid uniform points in [0,100]^6 (PAPER.md:357-358;
 datagen seed 1803_04120+100*6+1), eps = 1 (BASELINE.json configs[1], Fig. 1(a) set-up PAPER.md:66).
-One STEP = the whole hot path: index build (geometry, keys, radix sort,
-compaction/gather) + estimator + batch plan + refine/emission of every batch; N>1: rank-0 build,
-NCCL broadcast of the index, per-rank shard join, all-reduce of the counts.
+One STEP = the whole hot path: index build (geometry, keys, sort,
+compaction/gather) + estimator + batch plan + refine/emission of every batch; N>1: rank-0 build and
+shard plan, NCCL broadcast of the packed index, per-rank shard join, all-reduce of the counters.
 
   value : result pairs/s of the whole job, inputs resident in HBM, results left in HBM.
   e2e   : same metric through the C ABI with HOST buffers: pinned N x d input copied H2D and every
           result batch drained D2H to pinned host memory inside the timed region.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--dry-run]
+
+--gpus N without a torchrun environment re-launches itself under torch.distributed.run with N
+ranks (one per GPU; 127.0.0.1 rendezvous).  --dry-run runs the multi-rank plumbing on CPU (gloo):
+rank spawn, header + packed-buffer broadcast, counter all-reduce, max-over-ranks timing, one JSON
+line -- no GPU work (a launch test, not a measurement).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,7 +38,7 @@ METRIC = "self-join result pairs/s, Syn-6D 2M pts"
 UNIT = "pairs/s"
 
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -46,7 +52,13 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle sample duration")
     ap.add_argument("--phases", action="store_true", help="also print per-phase timings (stderr)")
     ap.add_argument("--also-eps", type=float, default=8.0, help="secondary eps of the same metric (0: off)")
-    return ap.parse_args()
+    ap.add_argument("--dry-run", action="store_true", help="CPU-only multi-rank plumbing test (gloo)")
+    ap.add_argument("--backend", default=None, choices=[None, "nccl", "gloo"],
+                    help="process-group backend for N>1 (default nccl; gloo when ranks share a GPU)")
+    ap.add_argument("--traffic", default="auto", choices=["auto", "on", "off"],
+                    help="measure the refine's DRAM traffic with an ncu child run (auto: N=1 only)")
+    ap.add_argument("--profile-child", action="store_true", help=argparse.SUPPRESS)
+    return ap.parse_args(argv)
 
 
 # --------------------------------------------------------------------------- helpers
@@ -107,6 +119,27 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
+def host_cpu():
+    """CPU model, sockets and logical CPUs of the host (reported with the oracle baseline)."""
+    info = {"logical_cpus": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "Model name":
+                info["model"] = v
+            elif k == "Socket(s)":
+                info["sockets"] = int(v) if v.isdigit() else v
+            elif k == "Core(s) per socket":
+                info["cores_per_socket"] = int(v) if v.isdigit() else v
+            elif k == "Thread(s) per core":
+                info["threads_per_core"] = int(v) if v.isdigit() else v
+    except Exception:
+        pass
+    return info
+
+
 def cpu_baseline(pts, eps, seconds: float):
     """The oracle (oracle/ grid join, plain C, all host threads) on a bounded query sample of the
     same workload: every sampled query is joined against all N points.  Two probes separate the
@@ -132,22 +165,25 @@ def cpu_baseline(pts, eps, seconds: float):
             "sample": f"queries [0,{q}) of the {n}-point workload joined against all {n} points "
                       f"(full 3^d hash-grid scan incl. its grid build over all points; count-only), "
                       f"{dt:.2f} s, {pairs} pairs",
-            "seconds": dt, "pairs": pairs}
+            "host_cpu": host_cpu(), "seconds": dt, "pairs": pairs}
 
 
-def dist_setup(gpus: int):
-    import torch
-    import torch.distributed as dist
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    return world, rank, local
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_distributed(args) -> int:
+    """--gpus N outside torchrun: re-exec this script under torch.distributed.run, N ranks."""
+    # the ranks get this invocation's arguments through the environment: torchrun's own parser would
+    # otherwise claim abbreviations such as --n
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)]
+    env = dict(os.environ, SJ_BENCH_ARGV=json.dumps(sys.argv[1:]))
+    return subprocess.call(cmd, env=env)
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -177,14 +213,163 @@ def run_reference(args):
             "config": {"workload": f"Syn-{args.d}D uniform [0,100]^{args.d}, N={args.n}, eps={args.eps}",
                        "sample": "bounded query sample per step (see cpu_baseline.sample)"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
-                             "sample": last["sample"]},
+                             "sample": last["sample"], "host_cpu": last["host_cpu"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-# --------------------------------------------------------------------------- our arm
-def run_ours(args):
+# --------------------------------------------------------------------------- dry run (CPU)
+def run_dry(args):
+    """Multi-rank plumbing on CPU: gloo process group, the header + packed-buffer broadcast of the
+    index format, the counter all-reduce and max-over-ranks timing; prints one JSON line."""
     import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1803_04120_b200 import distributed as sjd
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    dev = torch.device("cpu")
+    n = min(args.n, 100_000)
+    geom = dict(d=args.d, key_bits=41, eps=args.eps, eps2=args.eps * args.eps, w=args.eps,
+                mins=[0.0] * args.d, cpd=[102] * args.d, strides=[102 ** j for j in range(args.d)],
+                mask_offsets=[102 * j for j in range(args.d + 1)])
+    layout = {"X": 0, "A": 8 * args.d * n, "pcell": 8 * args.d * n + 4 * n, "G": 8 * args.d * n + 8 * n,
+              "masks": 8 * args.d * n + 12 * n + 4, "B": 8 * args.d * n + 16 * n + 256}
+    layout["packed_bytes"] = layout["B"] + 8 * n
+    times = []
+    got_ok = True
+    for _ in range(max(1, args.steps)):
+        t0 = time.perf_counter()
+        if rank == 0:
+            cuts = sjd.plan_shards(n, world)
+            meta = sjd.pack_meta(geom, n, n, geom["mask_offsets"][-1], layout, cuts)
+            buf = torch.arange(layout["packed_bytes"], dtype=torch.int64).to(torch.uint8)
+            args_b = (meta, buf, None)
+        else:
+            args_b = (None, None, None)
+        if world > 1:
+            meta, buf, _ = sjd.broadcast_index(*args_b, dev)
+        else:
+            meta, buf, _ = args_b
+        lay, cuts = sjd.unpack_layout(meta)
+        got_ok &= bool(torch.equal(buf[:4096], torch.arange(4096, dtype=torch.int64).to(torch.uint8)))
+        mine = int(cuts[rank + 1] - cuts[rank])
+        tot = sjd.allreduce_counts([mine, 0, 0, 0], dev) if world > 1 else np.array([mine, 0, 0, 0])
+        dt = (time.perf_counter() - t0) * 1e3
+        if world > 1:
+            dt = float(sjd.allreduce_counts([dt], dev, op="max")[0])
+        times.append(dt)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": statistics.mean(times), "higher_is_better": True,
+                          "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                          "dry_run": True, "broadcast_ok": got_ok, "queries_covered": int(tot[0]),
+                          "config": {"workload": f"dry run: packed-buffer broadcast of a {n}-point index image",
+                                     "parallelism": f"query-shard x{world} (gloo, CPU)"}}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------------- our arm
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    if ndev == 0:
+        raise RuntimeError("bench.py needs a CUDA device (use --dry-run for the CPU plumbing test)")
+    dev_index = local % ndev
+    backend = args.backend
+    torch.cuda.set_device(dev_index)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend is None:
+            backend = "nccl" if ndev >= world else "gloo"     # NCCL refuses two ranks on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, dev_index, backend
+
+
+def refine_traffic(args):
+    """DRAM bytes of the refine launches of ONE step of this exact workload, measured by an ncu child
+    run of bench.py (--profile-child: 2 steps, the second profiled) with --cache-control none, so the
+    counters see the step's real cache state; per-launch dram__bytes_read + dram__bytes_write and
+    sm issue / FP64-pipe utilisation are summed over the step's kEmit refine launches."""
+    import csv
+    import io
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found"
+    metrics = ("dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+               "sm__inst_issued.avg.pct_of_peak_sustained_active,"
+               "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+    cmd = [ncu, "--metrics", metrics, "--cache-control", "none", "--clock-control", "none", "--csv",
+           "-k", "regex:k_refine", sys.executable, os.path.abspath(__file__), "--profile-child",
+           "--d", str(args.d), "--n", str(args.n), "--eps", str(args.eps)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    except Exception as e:  # pragma: no cover
+        return None, f"ncu failed: {e}"
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith('"')]
+    if not lines:
+        return None, f"ncu produced no metrics (rc={r.returncode}): {r.stderr[-300:]}"
+    rows = list(csv.DictReader(io.StringIO("\n".join(lines))))
+    # group metrics by launch id; keep the kEmit refine launches (template arg MODE = 0) of the last step
+    launches = {}
+    for row in rows:
+        name = row.get("Kernel Name", "")
+        if "k_refine<" not in name and "k_refine_dense<" not in name:
+            continue
+        emit = "k_refine_dense<" in name or name.split("<")[1].split(",")[1].strip() == "0"
+        if not emit:
+            continue
+        lid = int(row["ID"])
+        v = float(row["Metric Value"].replace(",", "")) if row["Metric Value"] else 0.0
+        unit = row.get("Metric Unit", "")
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+                 "msecond": 1e-3}.get(unit, 1.0)
+        launches.setdefault(lid, {})[row["Metric Name"]] = v * scale
+    if not launches:
+        return None, "no refine launches in the ncu output"
+    ids = sorted(launches)
+    half = ids[len(ids) // 2:]                 # the second (profiled) step's launches
+    tot = sum(launches[i].get("dram__bytes_read.sum", 0) + launches[i].get("dram__bytes_write.sum", 0) for i in half)
+    dur = sum(launches[i].get("gpu__time_duration.sum", 0) for i in half)
+    w = lambda key: (sum(launches[i].get(key, 0) * launches[i].get("gpu__time_duration.sum", 0) for i in half)
+                     / dur if dur else None)
+    return {"dram_bytes_per_step": tot, "launches_per_step": len(half), "ncu_serial_time_s": dur,
+            "issue_slots_busy_pct": w("sm__inst_issued.avg.pct_of_peak_sustained_active"),
+            "fp64_pipe_pct": w("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")}, None
+
+
+def profile_child(args):
+    """The ncu child of refine_traffic(): one warm-up step and one profiled step, no output line."""
+    import torch
+    import datagen
+    import paper_1803_04120_b200 as sj
+    torch.cuda.set_device(0)
+    pts = torch.from_numpy(datagen.uniform(args.n, args.d, datagen.seed_for(args.d, "C2"))).cuda()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        flush.zero_()
+        torch.cuda.synchronize()
+        idx = sj.build_index(pts, args.eps)
+        res = sj.self_join(idx)
+        torch.cuda.synchronize()
+        res.free()
+        idx.free()
+
+
+def run_ours(args):
     import torch
     import torch.distributed as dist
 
@@ -192,23 +377,25 @@ def run_ours(args):
     import paper_1803_04120_b200 as sj
     from paper_1803_04120_b200 import distributed as sjd
 
-    world, rank, local = dist_setup(args.gpus)
+    world, rank, local, backend = dist_setup(args)
     dev = torch.device("cuda", local)
     sj.load_library()
 
     pts = datagen.uniform(args.n, args.d, datagen.seed_for(args.d, "C2"))
-    pts_dev = torch.from_numpy(pts).to(dev)
-    pts_pin = torch.from_numpy(pts).pin_memory()
+    pts_dev = torch.from_numpy(pts).to(dev) if rank == 0 else None
+    pts_pin = torch.from_numpy(pts).pin_memory() if rank == 0 else None
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
 
     def step(points, host_results=False):
-        res, total, idx = sjd.sharded_self_join(points, args.eps, local, result_on_host=host_results)
-        return res, total, idx
+        return sjd.sharded_self_join(points, args.eps, local, result_on_host=host_results, stats=True)
 
     def timed(points, host_results, k):
         total_ms = 0.0
@@ -221,13 +408,14 @@ def run_ours(args):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            res, total, idx = step(points, host_results)
+            res, total, idx, cnt = step(points, host_results)
             e1.record(stream)
             torch.cuda.synchronize(dev)
             barrier()
             total_ms += e0.elapsed_time(e1)
             pairs = total
-            info.append((res.stats if res is not None else None, idx.timings()))
+            info.append((res.stats if res is not None else None, idx.timings() if rank == 0 else None, cnt,
+                         idx.n_cells))
             if res is not None:
                 res.free()
             del idx
@@ -237,7 +425,7 @@ def run_ours(args):
 
     # warm-up (W >= 3 untimed steps)
     for _ in range(args.warmup):
-        res, total, idx = step(pts_dev)
+        res, total, idx, _ = step(pts_dev)
         if res is not None:
             res.free()
         del idx
@@ -254,7 +442,7 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         for _ in range(args.warmup):       # warm the host-drain path too (pinned result pool)
-            res, total, idx = step(pts_pin, True)
+            res, total, idx, _ = step(pts_pin, True)
             if res is not None:
                 res.free()
             del idx
@@ -266,48 +454,77 @@ def run_ours(args):
 
     # ---- per-phase device times (CUDA events recorded by the library on its launch streams)
     st = [i[0] for i in info if i[0] is not None]
-    bt = [i[1] for i in info]
-    mean = lambda xs: sum(xs) / len(xs)
-    phases = {
-        "build_total_ms": mean([b["total_ms"] for b in bt]),
-        "build_keys_ms": mean([b["keys_ms"] for b in bt]),
-        "build_sort_ms": mean([b["sort_ms"] for b in bt]),
-        "build_compact_ms": mean([b["compact_ms"] for b in bt]),
-        "build_geometry_ms": mean([b["geometry_ms"] for b in bt]),
-        "estimate_ms": mean([s["estimate_ms"] for s in st]),
-        "refine_ms_sum": mean([s["refine_ms"] for s in st]),
-        "refine_launch_max_ms": mean([s["refine_max_ms"] for s in st]),
-        "refine_launches": st[-1]["refine_launches"],
-        "join_total_ms": mean([s["total_ms"] for s in st]),
-        "cells_probed": st[-1]["cells_probed"],
-        "candidates_tested": st[-1]["candidates_tested"],
-        "batches": st[-1]["batches"],
-    }
+    bt = [i[1] for i in info if i[1] is not None]
+    counters = info[-1][2]
+    mean = lambda xs: sum(xs) / len(xs) if xs else None
     peaks, peak_src = measured_peaks()
+    phases = {}
+    if bt:
+        phases.update({
+            "build_total_ms": mean([b["total_ms"] for b in bt]),
+            "build_keys_ms": mean([b["keys_ms"] for b in bt]),
+            "build_sort_ms": mean([b["sort_ms"] for b in bt]),
+            "build_compact_ms": mean([b["compact_ms"] for b in bt]),
+            "build_geometry_ms": mean([b["geometry_ms"] for b in bt]),
+        })
+    if st:
+        phases.update({
+            "estimate_ms": mean([s["estimate_ms"] for s in st]),
+            "refine_ms_sum": mean([s["refine_ms"] for s in st]),
+            "refine_launch_max_ms": mean([s["refine_max_ms"] for s in st]),
+            "refine_launches": st[-1]["refine_launches"],
+            "join_total_ms": mean([s["total_ms"] for s in st]),
+            "batches": st[-1]["batches"],
+            "refine_span_ms": mean([s_["refine_span_ms"] for s_ in st]),
+        })
+    phases.update({k: counters[k] for k in sjd.COUNTERS})
 
-    # ---- roofline of the dominant kernel: the refine kernel (k_refine<6,kEmit,unicomp>)
-    # Algorithmic HBM bytes of the refine over the whole step: every query reads its
-    # own point, A id, cell and cell key (8d + 16 B); every candidate test reads the candidate's
-    # point and id (8d + 4 B); every emitted pair writes 8 B.  Time = the refine phase span on the
-    # device (first launch start -> last launch end, CUDA events on the launching streams).
-    n_local = args.n // world
-    span_ms = mean([s_["refine_span_ms"] for s_ in st])
-    cands = st[-1]["candidates_tested"]
+    # ---- roofline of the dominant kernel: the refine (k_refine<d,kEmit,unicomp> + k_refine_dense)
+    # Algorithmic HBM bytes of the refine over one step: every query reads its own
+    # point, A id, cell and cell key (8d + 16 B); every candidate test reads the candidate's point and
+    # id (8d + 4 B); every emitted pair writes 8 B.  Time = the refine phase span on the device (first
+    # launch start -> last launch end, CUDA events on the launching streams).
+    n_local = args.n / world
+    span_ms = phases.get("refine_span_ms") or float("nan")
+    cands = counters["candidates_tested"] / world
     alg_bytes = n_local * (8 * args.d + 16) + cands * (8 * args.d + 4) + (pairs / world) * 8
     achieved = alg_bytes / (span_ms / 1000.0) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01d_refine_traffic.json")
-    if args.d == 6 and args.eps == 1.0 and args.n == 2_000_000 and os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f)["dram_bytes_per_step"]      # ncu --set full, same workload
-    roof = {"kernel": f"k_refine<{args.d},kEmit,unicomp>", "bound": "hbm", "achieved": achieved,
+    fp64 = None
+    fp64_peak = None
+    try:
+        fp = sj.fp64_peak(local)
+        fp64_peak = min(fp["dadd_ops_per_s"], fp["dmul_ops_per_s"])
+        fp64 = (3 * args.d * cands) / (span_ms / 1000.0)
+    except Exception:
+        pass
+    traffic, traffic_note = None, None
+    want_traffic = args.traffic == "on" or (args.traffic == "auto" and world == 1)
+    if want_traffic and rank == 0:
+        traffic, traffic_note = refine_traffic(args)
+    roof = {"kernel": f"k_refine<{args.d},kEmit,unicomp> (+k_refine_dense)", "bound": "hbm", "achieved": achieved,
             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-            "traffic": traffic, "traffic_unit": "bytes per step (all refine launches)", "peak_source": peak_src,
+            "traffic": (traffic["dram_bytes_per_step"] if traffic else None),
+            "traffic_unit": "bytes per step (the step's kEmit refine launches; ncu --cache-control none, this run)",
+            "traffic_note": traffic_note, "peak_source": peak_src,
             "algorithmic_bytes_per_step": alg_bytes, "refine_span_ms": span_ms,
             "refine_share_of_step": span_ms / (ms / args.steps),
-            "note": "search-dominated workload (~1 neighbour/point): the kernel is issue/latency bound, "
-                    "not HBM bound; ncu evidence in profiles/"}
-    phases["refine_span_ms"] = span_ms
+            "fp64": {"achieved_ops_per_s": fp64, "peak_ops_per_s": fp64_peak,
+                     "frac": (fp64 / fp64_peak) if fp64 and fp64_peak else None,
+                     "ops": "3d per candidate test (d DSUB + d DMUL + (d-1) DADD + DSETP)",
+                     "peak_source": "sj_diag_fp64_peak (measured DADD/DMUL microbenchmark, min of the two)"},
+            "issue_slots_busy_pct": traffic.get("issue_slots_busy_pct") if traffic else None,
+            "fp64_pipe_pct_ncu": traffic.get("fp64_pipe_pct") if traffic else None,
+            "note": "~1 neighbour per point: the refine's work is the neighbour-cell search (issue/latency "
+                    "bound, not HBM bound); the HBM fraction is reported as the contract asks, with the "
+                    "issue-slot and FP64-pipe fractions beside it"}
+    # the build (a1-a4) as its own HBM roofline: read D (8dN) + write X (8dN) + A (4N) + B, G (16|G|)
+    if bt:
+        nG = info[-1][3]
+        build_bytes = 16 * args.d * args.n + 4 * args.n + 16 * nG
+        phases["build_roofline"] = {"bound": "hbm", "algorithmic_bytes": build_bytes,
+                                    "achieved_gbs": build_bytes / (phases["build_total_ms"] / 1e3) / 1e9,
+                                    "frac": build_bytes / (phases["build_total_ms"] / 1e3) / 1e9 / peaks["hbm_gbs"],
+                                    "bytes": "8dN read D + 8dN write X + 4N write A + 16|G| write B, G"}
 
     # ---- secondary workload of the same metric (Syn-6D 2 M at eps = 1 AND eps = 8)
     also = None
@@ -315,22 +532,24 @@ def run_ours(args):
         saved = args.eps
         args.eps = args.also_eps
         for _ in range(args.warmup):
-            res, total, idx = step(pts_dev)
+            res, total, idx, _ = step(pts_dev)
             if res is not None:
                 res.free()
             del idx
         ms2, pairs2, info2 = timed(pts_dev, False, args.steps)
         args.eps = saved
         st2 = [i[0] for i in info2 if i[0] is not None]
-        also = {"config": f"Syn-{args.d}D uniform, N={args.n}, eps={args.also_eps}", "value": pairs2 * args.steps / (ms2 / 1000.0),
-                "unit": UNIT, "ms_per_step": ms2 / args.steps, "pairs_per_step": pairs2,
-                "refine_span_ms": mean([s_["refine_span_ms"] for s_ in st2]),
-                "candidates_tested": st2[-1]["candidates_tested"]}
+        span2 = mean([s_["refine_span_ms"] for s_ in st2]) if st2 else None
+        c2 = info2[-1][2]["candidates_tested"]
+        also = {"config": f"Syn-{args.d}D uniform, N={args.n}, eps={args.also_eps}",
+                "value": pairs2 * args.steps / (ms2 / 1000.0), "unit": UNIT, "ms_per_step": ms2 / args.steps,
+                "pairs_per_step": pairs2, "refine_span_ms": span2, "candidates_tested": c2,
+                "fp64_frac": ((3 * args.d * c2 / world) / (span2 / 1e3) / fp64_peak) if (span2 and fp64_peak) else None}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(pts, args.eps, args.cpu_seconds)
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "host_cpu")}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -339,7 +558,8 @@ def run_ours(args):
                 "config": {"workload": f"Syn-{args.d}D uniform [0,100]^{args.d}, N={args.n}, eps={args.eps} "
                                        f"(BASELINE.json configs[1], 6-D member)",
                            "n": args.n, "d": args.d, "eps": args.eps, "pairs_per_step": pairs,
-                           "parallelism": f"query-shard x{world}, replicated index (NCCL broadcast)",
+                           "parallelism": f"query-shard x{world}, replicated index (packed broadcast, "
+                                          f"{backend or 'single process'}), shards balanced by the sampled estimate",
                            "l2": "flushed (512 MB write) before every timed step",
                            "results": "device-resident batches (value); pinned-host drained batches (e2e)"},
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
@@ -348,14 +568,23 @@ def run_ours(args):
         if args.phases:
             print(json.dumps(phases, indent=1), file=sys.stderr)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        barrier()
         dist.destroy_process_group()
 
 
 def main():
-    args = parse_args()
+    argv = json.loads(os.environ["SJ_BENCH_ARGV"]) if "SJ_BENCH_ARGV" in os.environ else None
+    args = parse_args(argv)
+    if args.profile_child:
+        profile_child(args)
+        return
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args))
+    if args.dry_run:
+        run_dry(args)
     else:
         run_ours(args)
 

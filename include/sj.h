@@ -133,6 +133,13 @@ typedef struct {
     const uint32_t *dir;         /* [dir_entries] dir[p] = first cell with top-dir_k prefix >= p   */
     /* build timings (CUDA events, ms) */
     float t_h2d_ms, t_geometry_ms, t_keys_ms, t_sort_ms, t_compact_ms, t_total_ms;
+    /* the index's arrays as ONE contiguous device buffer (multi-GPU broadcast):
+       packed_bytes bytes at `packed`; X, A, pcell, G, masks and B sit at the off_* byte offsets in it
+       (off_masks = UINT64_MAX when the masks live outside it, at `masks`).  NULL for an index whose
+       arrays are not contiguous (sj_index_import with copies).                                    */
+    const void *packed;
+    uint64_t packed_bytes;
+    uint64_t off_X, off_A, off_pcell, off_G, off_masks, off_B;
 } sj_index_view;
 
 /* Fill *o with the defaults above. */
@@ -164,6 +171,13 @@ sj_status sj_build_index(const double *points, uint64_t n, int d, double eps,
  * Errors: SJ_ERR_ARG (bad options / query range), SJ_ERR_STATE (NULL index), SJ_ERR_NOMEM,
  *         SJ_ERR_CUDA. */
 sj_status sj_self_join(const sj_index *idx, const sj_join_opts *opts, sj_result **out);
+
+/* Build + join in ONE call (the common path of a user holding points): sj_build_index followed by
+ * sj_self_join on the same device, with no return to the caller in between.  *out_index receives
+ * the index (free with sj_free_index) unless out_index is NULL, in which case it is freed here
+ * (after the join completed).  Errors: those of sj_build_index and sj_self_join. */
+sj_status sj_self_join_points(const double *points, uint64_t n, int d, double eps, const sj_build_opts *bopts,
+                              const sj_join_opts *jopts, sj_index **out_index, sj_result **out);
 
 /* Release a result and every batch buffer it owns.  NULL-safe.  Device batch buffers go to a
  * per-device cache reused by later joins; they are reused only after the work queued before this
@@ -241,8 +255,17 @@ sj_status sj_index_export(const sj_index *idx, sj_index_view *view);
 sj_status sj_index_timings(const sj_index *idx, sj_index_view *view);
 
 /* Build an index on `device` from a view whose array pointers are device memory on that device
- * (e.g. buffers received by an NCCL broadcast); the arrays are copied. */
+ * (e.g. buffers received by an NCCL broadcast); the arrays are copied.  Only the geometry fields
+ * (d, n, n_cells, eps, eps2, w, mins, cpd, strides, key_bits, mask_offsets) and the array pointers
+ * B, G, A, pcell, X, masks are read; the prefix directory, occupancy bitmaps and dense-cell tasks
+ * are rebuilt from B and G on the device. */
 sj_status sj_index_import(const sj_index_view *view, int device, sj_index **out);
+
+/* Same, but the arrays are BORROWED, not copied: the index reads B, G, A, pcell, X, masks in place,
+ * and the caller keeps that memory alive (and unmodified) until sj_free_index.  For a rank that
+ * received the packed buffer of sj_index_view.packed, this makes the import cost only the rebuild
+ * of the small derived tables. */
+sj_status sj_index_import_borrowed(const sj_index_view *view, int device, sj_index **out);
 
 /* Optional allocator hook for device memory (index arrays, result batches, scratch).
  * alloc(bytes, device, stream, ctx) returns a device pointer or NULL; release(ptr, ctx).
@@ -269,6 +292,12 @@ sj_status sj_plan_batches(const uint32_t *sample_counts, uint64_t n_samples, uin
                           uint64_t q_begin, uint64_t q_end, uint64_t capacity, int min_batches,
                           double margin, uint64_t *cuts, uint32_t max_cuts, uint32_t *k,
                           uint64_t *estimated_total);
+
+/* Measurement helper (bench.py roofline): throughput of the FP64 pipe for single DADD and DMUL
+ * instructions on `device`, in operations per second (a saturating microbenchmark, best of 3
+ * timed runs).  The predicate issues no FMA (reading R1), so this -- not the datasheet's
+ * FMA-counted FP64 figure -- is the refine's FP64 roofline.  Errors: SJ_ERR_CUDA. */
+sj_status sj_diag_fp64_peak(int device, double *dadd_ops_per_s, double *dmul_ops_per_s);
 
 /* Number of CUDA kernels this library has launched in the process (monotone counter). */
 uint64_t sj_kernel_launches(void);

@@ -4,10 +4,10 @@ The work runs in ``libsj.so`` (hand-written CUDA behind the C ABI of ``include/s
 package is its thin ctypes binding plus the multi-GPU glue.  There is no CPU fallback.
 """
 from .sj import (  # noqa: F401
-    Index, Result, SJError, build_index, self_join, neighbor_counts, import_index, plan_batches, plan_shards,
-    brute_force_join, kernel_launches, load_library, trim, set_result_cache_limit, LIB_PATH,
+    Index, Result, SJError, build_index, self_join, join_points, neighbor_counts, import_index, plan_batches, plan_shards,
+    brute_force_join, kernel_launches, load_library, trim, set_result_cache_limit, fp64_peak, LIB_PATH,
 )
 
-__all__ = ["Index", "Result", "SJError", "build_index", "self_join", "neighbor_counts", "import_index",
+__all__ = ["Index", "Result", "SJError", "build_index", "self_join", "join_points", "neighbor_counts", "import_index",
            "plan_batches", "plan_shards", "brute_force_join", "kernel_launches", "load_library", "trim",
-           "set_result_cache_limit", "LIB_PATH"]
+           "set_result_cache_limit", "fp64_peak", "LIB_PATH"]

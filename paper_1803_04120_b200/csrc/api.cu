@@ -254,6 +254,30 @@ sj_status sj_self_join(const sj_index *idx, const sj_join_opts *opts, sj_result 
     SJ_API_END
 }
 
+sj_status sj_self_join_points(const double *points, uint64_t n, int d, double eps, const sj_build_opts *bopts,
+                              const sj_join_opts *jopts, sj_index **out_index, sj_result **out)
+{
+    SJ_API_BEGIN
+    if (!out) sj::fail(SJ_ERR_ARG, "out is NULL");
+    sj_build_opts bo;
+    if (bopts) bo = *bopts;
+    else sj_build_opts_default(&bo);
+    sj_join_opts jo;
+    if (jopts) jo = *jopts;
+    else sj_join_opts_default(&jo);
+    sj_index *idx = sj::build_index_impl(points, n, d, eps, bo);
+    try {
+        *out = sj::self_join_impl(idx, jo);
+    } catch (...) {
+        sj::free_index_impl(idx);
+        throw;
+    }
+    if (out_index) *out_index = idx;
+    else sj::free_index_impl(idx);
+    return SJ_OK;
+    SJ_API_END
+}
+
 void sj_free_result_async(sj_result *r, void *stream)
 {
     if (!r) return;
@@ -417,7 +441,16 @@ sj_status sj_index_import(const sj_index_view *view, int device, sj_index **out)
 {
     SJ_API_BEGIN
     if (!view || !out) sj::fail(SJ_ERR_ARG, "NULL argument");
-    *out = sj::import_index_impl(*view, device);
+    *out = sj::import_index_impl(*view, device, false);
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_index_import_borrowed(const sj_index_view *view, int device, sj_index **out)
+{
+    SJ_API_BEGIN
+    if (!view || !out) sj::fail(SJ_ERR_ARG, "NULL argument");
+    *out = sj::import_index_impl(*view, device, true);
     return SJ_OK;
     SJ_API_END
 }

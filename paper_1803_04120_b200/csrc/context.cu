@@ -399,8 +399,9 @@ HostTrace::HostTrace(const char *w) : what(w)
 void HostTrace::dev(const char *stage, cudaStream_t s)
 {
     if (trace_level() < 2) return;
-    cudaEvent_t e;
-    if (cudaEventCreate(&e) != cudaSuccess) return;
+    int d = 0;
+    cudaGetDevice(&d);
+    cudaEvent_t e = event_get(d);       // pooled: recording costs ~1 us of host time, no creation
     cudaEventRecord(e, s);
     dev_ev.emplace_back(stage, e);
 }
@@ -414,7 +415,9 @@ HostTrace::~HostTrace()
         cudaEventElapsedTime(&ms, dev_ev[i - 1].second, dev_ev[i].second);
         std::fprintf(stderr, "[sj-dev]   %-10s %-28s +%8.1f us (GPU)\n", what, dev_ev[i].first, 1000.0 * ms);
     }
-    for (auto &pr : dev_ev) cudaEventDestroy(pr.second);
+    int d = 0;
+    cudaGetDevice(&d);
+    for (auto &pr : dev_ev) event_put(d, pr.second);
 }
 
 void HostTrace::mark(const char *stage)

@@ -650,6 +650,8 @@ k_occ_bits(const uint64_t *__restrict__ B, const uint32_t *__restrict__ nG, uint
 }
 
 // second bitmap: bit prefix * |g_{d-k-2}| + c_{d-k-2}, c = (key / stride_{d-k-2}) mod |g_{d-k-2}|
+// (the low part key - prefix * div divided by stride_{d-k-2} still carries c_{d-k-1} * |g_{d-k-2}|:
+// the mod removes it)
 __global__ void __launch_bounds__(kThreads)
 k_occ2_bits(const uint64_t *__restrict__ B, const uint32_t *__restrict__ nG, uint64_t div, double inv,
             uint64_t st2, double inv2, uint64_t cpd2, uint32_t *__restrict__ occ2)
@@ -658,7 +660,8 @@ k_occ2_bits(const uint64_t *__restrict__ B, const uint32_t *__restrict__ nG, uin
     if (h >= *nG) return;
     const uint64_t key = B[h];
     const uint64_t prefix = div_small_quot(key, div, inv);
-    const uint64_t c2 = div_small_quot(key - prefix * div, st2, inv2);
+    const uint64_t q2 = div_small_quot(key - prefix * div, st2, inv2);
+    const uint64_t c2 = q2 % cpd2;
     occ_set_window(occ2, prefix * cpd2 + c2);
 }
 
@@ -810,25 +813,29 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         }
         ev.rec(1, s);
 
-        // every N-sized array in two arenas (one owned by the index: A, pcell, B, G, X, cell
-        // coordinates/masks, the small mask bitmap, aux; one scratch: keys, sort buffers, bucket
-        // histogram sized for the largest possible prefix count)
+        // every N-sized array in two arenas.  The index's arena is laid out for the multi-GPU
+        // broadcast (sj_index_view.packed): [X | A | pcell | G | small masks | aux | B]; with B last,
+        // the bytes up to B + 8|G| are the whole index (B is sized for the upper bound N cells so
+        // that no host round trip for |G| is needed during the build).  The scratch arena holds the
+        // keys, sort buffers and bucket histogram.
         auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
         const size_t b_A = al(4 * n), b_pc = al(4 * n), b_B = al(8 * n), b_G = al(4 * (n + 1)), b_X = al(8 * n * d),
-                     b_cc = 0, b_cm = 0, b_mk = al(4 * kSmemMaskWords),
+                     b_mk = al(4 * kSmemMaskWords),
                      b_aux = al(kAuxEstOffset + 8 * kMaxEstBuckets);   // aux + the build's estimate buckets
-        char *arena =
-            static_cast<char *>(own(dev_alloc(b_A + b_pc + b_B + b_G + b_X + b_cc + b_cm + b_mk + b_aux, s)));
-        uint32_t *A = reinterpret_cast<uint32_t *>(arena);
-        uint32_t *pcell = reinterpret_cast<uint32_t *>(arena + b_A);
-        uint64_t *B = reinterpret_cast<uint64_t *>(arena + b_A + b_pc);
-        uint32_t *G = reinterpret_cast<uint32_t *>(arena + b_A + b_pc + b_B);
-        double *X = reinterpret_cast<double *>(arena + b_A + b_pc + b_B + b_G);
-        uint64_t *ccoord = reinterpret_cast<uint64_t *>(arena + b_A + b_pc + b_B + b_G + b_X);
-        uint32_t *cmask = reinterpret_cast<uint32_t *>(arena + b_A + b_pc + b_B + b_G + b_X + b_cc);
-        uint32_t *small_masks = reinterpret_cast<uint32_t *>(arena + b_A + b_pc + b_B + b_G + b_X + b_cc + b_cm);
+        const size_t o_X = 0, o_A = o_X + b_X, o_pc = o_A + b_A, o_G = o_pc + b_pc, o_mk = o_G + b_G,
+                     o_aux = o_mk + b_mk, o_B = o_aux + b_aux;
+        char *arena = static_cast<char *>(own(dev_alloc(o_B + b_B, s)));
+        idx->arena = arena;
+        uint32_t *A = reinterpret_cast<uint32_t *>(arena + o_A);
+        uint32_t *pcell = reinterpret_cast<uint32_t *>(arena + o_pc);
+        uint64_t *B = reinterpret_cast<uint64_t *>(arena + o_B);
+        uint32_t *G = reinterpret_cast<uint32_t *>(arena + o_G);
+        double *X = reinterpret_cast<double *>(arena + o_X);
+        uint64_t *ccoord = nullptr;
+        uint32_t *cmask = nullptr;
+        uint32_t *small_masks = reinterpret_cast<uint32_t *>(arena + o_mk);
         // aux: [0] = |G|, [1] = #dense tasks, [2] = #populous cells, [3] = bucket-sort overflow
-        uint32_t *aux = reinterpret_cast<uint32_t *>(arena + b_A + b_pc + b_B + b_G + b_X + b_cc + b_cm + b_mk);
+        uint32_t *aux = reinterpret_cast<uint32_t *>(arena + o_aux);
         const uint64_t hcap = std::max<uint64_t>(4ull * n, 1ull << 16);
         const size_t s_k = al(8 * n), s_i = al(4 * n), s_h = al(4 * (hcap + 1));
         // the build's temporaries: the per-device cached scratch buffer (released after the final
@@ -1095,6 +1102,18 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         }
         finish_aux(idx, s, aux, dp, nullptr, false, h_aux, h_stage,
                    kAuxEstOffset + (spec ? 8 * es_spec.nbk : 0));     // the build's late host sync
+        {
+            sj_index_view &vv = idx->view;
+            const uint64_t nGf = vv.n_cells;
+            vv.packed = arena;
+            vv.off_X = o_X;
+            vv.off_A = o_A;
+            vv.off_pcell = o_pc;
+            vv.off_G = o_G;
+            vv.off_masks = (masks == small_masks) ? o_mk : UINT64_MAX;
+            vv.off_B = o_B;
+            vv.packed_bytes = o_B + 8 * std::min<uint64_t>(nGf + 1, n);
+        }
         if (spec && !h_aux[3] && idx->dev.search_mode == prov_mode) {
             idx->spec_est_valid = true;
             idx->spec_shape = es_spec;
@@ -1133,7 +1152,7 @@ void free_index_impl(sj_index *idx)
 }
 
 
-sj_index *import_index_impl(const sj_index_view &src, int device)
+sj_index *import_index_impl(const sj_index_view &src, int device, bool borrow)
 {
     if (src.d < 2 || src.d > SJ_MAX_DIM) fail(SJ_ERR_DIM, "d must be in [2,6]");
     if (src.n == 0 || src.n >= (1ull << 32) || src.n_cells == 0 || src.n_cells > src.n)
@@ -1150,21 +1169,34 @@ sj_index *import_index_impl(const sj_index_view &src, int device)
         const int d = src.d;
         sj_index_view v = src;
         v.device = device;
-        uint64_t *B = static_cast<uint64_t *>(own(8 * nG));
-        uint32_t *G = static_cast<uint32_t *>(own(4 * (nG + 1)));
-        uint32_t *A = static_cast<uint32_t *>(own(4 * n));
-        uint32_t *pcell = static_cast<uint32_t *>(own(4 * n));
-        double *X = static_cast<double *>(own(8 * n * d));
-        uint32_t *masks = nullptr;
-        SJ_CUDA(cudaMemcpyAsync(B, src.B, 8 * nG, cudaMemcpyDefault, s));
-        SJ_CUDA(cudaMemcpyAsync(G, src.G, 4 * (nG + 1), cudaMemcpyDefault, s));
-        SJ_CUDA(cudaMemcpyAsync(A, src.A, 4 * n, cudaMemcpyDefault, s));
-        SJ_CUDA(cudaMemcpyAsync(pcell, src.pcell, 4 * n, cudaMemcpyDefault, s));
-        SJ_CUDA(cudaMemcpyAsync(X, src.X, 8 * n * d, cudaMemcpyDefault, s));
-        if (src.masks && src.mask_offsets[d] > 0) {
-            const size_t mb = 4 * ((src.mask_offsets[d] + 31) / 32);
-            masks = static_cast<uint32_t *>(own(mb));
-            SJ_CUDA(cudaMemcpyAsync(masks, src.masks, mb, cudaMemcpyDefault, s));
+        uint64_t *B;
+        uint32_t *G, *A, *pcell, *masks = nullptr;
+        double *X;
+        if (borrow) {
+            B = const_cast<uint64_t *>(src.B);
+            G = const_cast<uint32_t *>(src.G);
+            A = const_cast<uint32_t *>(src.A);
+            pcell = const_cast<uint32_t *>(src.pcell);
+            X = const_cast<double *>(src.X);
+            if (src.masks && src.mask_offsets[d] > 0) masks = const_cast<uint32_t *>(src.masks);
+        } else {
+            B = static_cast<uint64_t *>(own(8 * nG));
+            G = static_cast<uint32_t *>(own(4 * (nG + 1)));
+            A = static_cast<uint32_t *>(own(4 * n));
+            pcell = static_cast<uint32_t *>(own(4 * n));
+            X = static_cast<double *>(own(8 * n * d));
+            SJ_CUDA(cudaMemcpyAsync(B, src.B, 8 * nG, cudaMemcpyDefault, s));
+            SJ_CUDA(cudaMemcpyAsync(G, src.G, 4 * (nG + 1), cudaMemcpyDefault, s));
+            SJ_CUDA(cudaMemcpyAsync(A, src.A, 4 * n, cudaMemcpyDefault, s));
+            SJ_CUDA(cudaMemcpyAsync(pcell, src.pcell, 4 * n, cudaMemcpyDefault, s));
+            SJ_CUDA(cudaMemcpyAsync(X, src.X, 8 * n * d, cudaMemcpyDefault, s));
+            if (src.masks && src.mask_offsets[d] > 0) {
+                const size_t mb = 4 * ((src.mask_offsets[d] + 31) / 32);
+                masks = static_cast<uint32_t *>(own(mb));
+                SJ_CUDA(cudaMemcpyAsync(masks, src.masks, mb, cudaMemcpyDefault, s));
+            }
+            v.packed = nullptr;
+            v.packed_bytes = 0;
         }
         v.B = B; v.G = G; v.A = A; v.pcell = pcell; v.X = X; v.masks = masks;
         DevIndex ix{};

@@ -14,7 +14,7 @@
 #include <cstring>
 #include <deque>
 
-#include "refine.cuh"
+#include "refine_launch.cuh"
 
 namespace sj {
 
@@ -28,27 +28,15 @@ void launch_dense(const DevIndex &ix, const JoinArgs &ja, bool unicomp, cudaStre
     // over its task range anyway (k_refine_dense), so this only sizes the launch
     const uint64_t max_tasks =
         std::min<uint64_t>(ix.n_dense_tasks, (uint64_t)(ja.q1 - ja.q0 + ix.dense_T - 1) / ix.dense_T + 4);
-    const dim3 grid((uint32_t)((max_tasks + kDenseWarps - 1) / kDenseWarps)), block(32 * kDenseWarps);
-    const size_t smem = sizeof(uint64_t) * kDenseWarps * kWarpBufPairs;
-#define SJ_DENSE_CASE(DD)                                                                              \
-    case DD:                                                                                           \
-        if (unicomp) {                                                                                 \
-            set_max_dyn_smem(reinterpret_cast<const void *>(k_refine_dense<DD, true>), (int)smem);     \
-            k_refine_dense<DD, true><<<grid, block, smem, s>>>(ix, ja);                               \
-        } else {                                                                                       \
-            set_max_dyn_smem(reinterpret_cast<const void *>(k_refine_dense<DD, false>), (int)smem);     \
-            k_refine_dense<DD, false><<<grid, block, smem, s>>>(ix, ja);                              \
-        }                                                                                              \
-        break;
+    const dim3 grid((uint32_t)((max_tasks + kDenseWarps - 1) / kDenseWarps));
     switch (ix.d) {
-        SJ_DENSE_CASE(2)
-        SJ_DENSE_CASE(3)
-        SJ_DENSE_CASE(4)
-        SJ_DENSE_CASE(5)
-        SJ_DENSE_CASE(6)
+    case 2: launch_dense_d<2>(ix, ja, unicomp, grid, s); break;
+    case 3: launch_dense_d<3>(ix, ja, unicomp, grid, s); break;
+    case 4: launch_dense_d<4>(ix, ja, unicomp, grid, s); break;
+    case 5: launch_dense_d<5>(ix, ja, unicomp, grid, s); break;
+    case 6: launch_dense_d<6>(ix, ja, unicomp, grid, s); break;
     default: fail(SJ_ERR_DIM, "bad d");
     }
-#undef SJ_DENSE_CASE
     SJ_LAUNCHED();
 }
 
@@ -59,27 +47,16 @@ void launch_refine(const DevIndex &ix, const JoinArgs &ja, bool unicomp, uint32_
     const uint64_t nthreads64 = (uint64_t)nqueries << ja.lanes_log2;
     if (nthreads64 >= (1ull << 32)) fail(SJ_ERR_ARG, "too many queries x lanes for one launch");
     const uint32_t nthreads = (uint32_t)nthreads64;
-    const dim3 grid((nthreads + kRefineThreads - 1) / kRefineThreads), block(kRefineThreads);
+    const dim3 grid((nthreads + kRefineThreads - 1) / kRefineThreads);
     const bool occ6 = MODE == kEmit && ix.search_mode == kSearchCellScan && !ix.occ && ix.dir_ntop >= 81;
-#define SJ_REFINE_CASE(DD)                                                                       \
-    case DD:                                                                                     \
-        if (occ6) {                                                                              \
-            if (unicomp) k_refine<DD, MODE, true, 6><<<grid, block, 0, s>>>(ix, ja);            \
-            else k_refine<DD, MODE, false, 6><<<grid, block, 0, s>>>(ix, ja);                   \
-        } else {                                                                                 \
-            if (unicomp) k_refine<DD, MODE, true><<<grid, block, 0, s>>>(ix, ja);               \
-            else k_refine<DD, MODE, false><<<grid, block, 0, s>>>(ix, ja);                      \
-        }                                                                                        \
-        break;
     switch (ix.d) {
-        SJ_REFINE_CASE(2)
-        SJ_REFINE_CASE(3)
-        SJ_REFINE_CASE(4)
-        SJ_REFINE_CASE(5)
-        SJ_REFINE_CASE(6)
+    case 2: launch_refine_d<2>(MODE, ix, ja, unicomp, occ6, grid, s); break;
+    case 3: launch_refine_d<3>(MODE, ix, ja, unicomp, occ6, grid, s); break;
+    case 4: launch_refine_d<4>(MODE, ix, ja, unicomp, occ6, grid, s); break;
+    case 5: launch_refine_d<5>(MODE, ix, ja, unicomp, occ6, grid, s); break;
+    case 6: launch_refine_d<6>(MODE, ix, ja, unicomp, occ6, grid, s); break;
     default: fail(SJ_ERR_DIM, "bad d");
     }
-#undef SJ_REFINE_CASE
     SJ_LAUNCHED();
 }
 
@@ -283,7 +260,10 @@ void launch_estimate(const DevIndex &ix, int device, const sj_join_opts &o, uint
     const bool heavy = ix.search_mode == kSearchCellScan && ix.dir_ntop >= 81;
     const uint32_t lanes_max = heavy ? 4u : 3u;
     const uint64_t threads_per_sm = heavy ? 4096 : 1024;
-    if (o.lanes_per_query == 0) {
+    // the bitmap-filtered sparse search runs one lane per query (refine_query takes it for G = 1
+    // only): spreading the sample over lanes would switch it to the unfiltered offset scan
+    const bool sparse = ix.search_mode == kSearchCellScan && ix.occ && ix.dir_k <= 3;
+    if (o.lanes_per_query == 0 && !sparse) {
         const int nsm = device_sm_count(device);
         while (ja.lanes_log2 < lanes_max && (es.ns << (ja.lanes_log2 + 1)) <= (uint64_t)nsm * threads_per_sm)
             ++ja.lanes_log2;

@@ -343,6 +343,58 @@ __device__ __forceinline__ void test_low_cell(const DevIndex &ix, const JoinArgs
 // needs no directory lookup: its adjacent cells are the run of B within +-lowR[L] of the home
 // key around h (B is sorted and |key difference| <= lowR[L] < stride_L keeps the run inside
 // the prefix).
+// One block of search_cell_scan_sparse: the 2 * 3^JT top offsets whose highest moved top dimension is
+// L + JT (that dimension moved by -1 or +1, the top dimensions below it by -1/0/+1, the ones above
+// it unmoved).  JT is a compile-time constant so the filter loop has exactly the block's offsets.
+template <int D, int MODE, bool UNICOMP, int JT>
+__device__ __forceinline__ void sparse_block(const DevIndex &ix, const JoinArgs &ja, QueryState<D> &q, uint64_t key,
+                                             uint32_t bad, const TopTable &tt, uint64_t ph, uint64_t qc,
+                                             uint64_t qc2, int64_t Rl, uint32_t pow3k, int L)
+{
+    constexpr uint32_t p3 = JT == 2 ? 9u : (JT == 1 ? 3u : 1u);   // 3^JT
+    constexpr uint32_t nb = 2u * p3;
+    const uint32_t tbase = (pow3k - 3u * p3) / 2u;               // digits above JT = "0 move"
+    uint32_t live = 0;
+#pragma unroll
+    for (uint32_t i = 0; i < nb; ++i) {
+        const uint32_t t = tbase + (i >> 1) + ((i & 1u) ? 2u * p3 : 0u);
+        if (!(tt.bits[t] & bad)) {
+            // both bitmaps' loads are issued together (no dependent second round)
+            const uint64_t qb = qc + (uint64_t)tt.dq[t];
+            uint32_t ok = __ldg(ix.occ + (qb >> 5)) >> (qb & 31);
+            if (ix.occ2) {
+                const uint64_t qb2 = qc2 + (uint64_t)tt.dq2[t];
+                ok &= __ldg(ix.occ2 + (qb2 >> 5)) >> (qb2 & 31);
+            }
+            if (ok & 1u) live |= 1u << i;
+        }
+    }
+    const int dim = L + JT;
+#pragma unroll 1
+    while (live) {
+        const uint32_t i = __ffs(live) - 1;
+        live &= live - 1u;
+        const uint32_t t = tbase + (i >> 1) + ((i & 1u) ? 2u * p3 : 0u);
+        const uint64_t p = ph + (uint64_t)tt.dp[t];
+        ++q.probes;
+        const uint32_t lo = __ldg(ix.dir + p), hi = __ldg(ix.dir + p + 1);
+        const uint64_t kal = key + (uint64_t)tt.dk[t];
+#pragma unroll 1
+        for (uint32_t hh = lo; hh < hi; ++hh) {
+            const int64_t dlt = (int64_t)(__ldg(ix.B + hh) - kal);
+            if (dlt > Rl || dlt < -Rl) continue;
+            test_low_cell<D, MODE, UNICOMP, false>(ix, ja, q, hh, dlt, dim, L, 0u, nullptr);
+        }
+    }
+}
+
+// Sparse regime with k <= 3 top dimensions (the occupancy bitmap is built): the top offsets are
+// visited in blocks by their highest moved top dimension, so a block that unicomp rejects (that
+// dimension's coordinate even -- warp-uniform for the slow dimensions of A-ordered queries) is
+// skipped with one branch; the bitmap loads of a block are issued together; the home top offset
+// needs no directory lookup: its adjacent cells are the run of B within +-lowR[L] of the home
+// key around h (B is sorted and |key difference| <= lowR[L] < stride_L keeps the run inside
+// the prefix).
 template <int D, int MODE, bool UNICOMP>
 __device__ __forceinline__ void search_cell_scan_sparse(const DevIndex &ix, const JoinArgs &ja, QueryState<D> &q,
                                                         uint32_t h, uint64_t key, uint32_t bad, const TopTable &tt,
@@ -363,48 +415,14 @@ __device__ __forceinline__ void search_cell_scan_sparse(const DevIndex &ix, cons
     }
     const int64_t Rl = ix.lowR[L];
     const uint32_t pow3k = k == 3 ? 27u : (k == 2 ? 9u : 3u);
-#pragma unroll 1
-    for (int jt = k - 1; jt >= 0; --jt) {
-        __syncwarp(wmask);
-        if (UNICOMP && !((q.odd >> (L + jt)) & 1u)) continue;
-        const uint32_t p3 = jt == 2 ? 9u : (jt == 1 ? 3u : 1u);     // 3^jt
-        const uint32_t nb = 2u * p3;
-        const uint32_t tbase = (pow3k - 3u * p3) / 2u;               // digits above jt = "0 move"
-        uint32_t live = 0;
-#pragma unroll
-        for (uint32_t i = 0; i < 18u; ++i) {
-            if (i < nb) {
-                const uint32_t t = tbase + (i >> 1) + ((i & 1u) ? 2u * p3 : 0u);
-                if (!(tt.bits[t] & bad)) {
-                    // both bitmaps' loads are issued together (no dependent second round)
-                    const uint64_t qb = qc + (uint64_t)tt.dq[t];
-                    uint32_t ok = __ldg(ix.occ + (qb >> 5)) >> (qb & 31);
-                    if (ix.occ2) {
-                        const uint64_t qb2 = qc2 + (uint64_t)tt.dq2[t];
-                        ok &= __ldg(ix.occ2 + (qb2 >> 5)) >> (qb2 & 31);
-                    }
-                    if (ok & 1u) live |= 1u << i;
-                }
-            }
-        }
-        const int dim = L + jt;
-#pragma unroll 1
-        while (live) {
-            const uint32_t i = __ffs(live) - 1;
-            live &= live - 1u;
-            const uint32_t t = tbase + (i >> 1) + ((i & 1u) ? 2u * p3 : 0u);
-            const uint64_t p = ph + (uint64_t)tt.dp[t];
-            ++q.probes;
-            const uint32_t lo = __ldg(ix.dir + p), hi = __ldg(ix.dir + p + 1);
-            const uint64_t kal = key + (uint64_t)tt.dk[t];
-#pragma unroll 1
-            for (uint32_t hh = lo; hh < hi; ++hh) {
-                const int64_t dlt = (int64_t)(__ldg(ix.B + hh) - kal);
-                if (dlt > Rl || dlt < -Rl) continue;
-                test_low_cell<D, MODE, UNICOMP, false>(ix, ja, q, hh, dlt, dim, L, wmask, nullptr);
-            }
-        }
-    }
+    if (k >= 3 && (!UNICOMP || ((q.odd >> (L + 2)) & 1u)))
+        sparse_block<D, MODE, UNICOMP, 2>(ix, ja, q, key, bad, tt, ph, qc, qc2, Rl, pow3k, L);
+    __syncwarp(wmask);
+    if (k >= 2 && (!UNICOMP || ((q.odd >> (L + 1)) & 1u)))
+        sparse_block<D, MODE, UNICOMP, 1>(ix, ja, q, key, bad, tt, ph, qc, qc2, Rl, pow3k, L);
+    __syncwarp(wmask);
+    if (!UNICOMP || ((q.odd >> L) & 1u))
+        sparse_block<D, MODE, UNICOMP, 0>(ix, ja, q, key, bad, tt, ph, qc, qc2, Rl, pow3k, L);
     // home top offset: outward from h while |B[hh] - key| <= lowR[L]
     __syncwarp(wmask);
     ++q.probes;

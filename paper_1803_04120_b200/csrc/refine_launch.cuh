@@ -1,0 +1,16 @@
+// refine_launch.cuh -- host-side launchers of the refine kernels, one explicit instantiation per
+// dimension (refine_d2.cu .. refine_d6.cu), so the kernels of different d compile in parallel.
+#pragma once
+
+#include "refine.cuh"
+
+namespace sj {
+
+// MODE: kEmit / kCountQuery / kCountPoint; occ6: the 6-CTA/SM variant of the many-offset cell scan
+template <int D>
+void launch_refine_d(int mode, const DevIndex &ix, const JoinArgs &ja, bool unicomp, bool occ6, dim3 grid,
+                     cudaStream_t s);
+template <int D>
+void launch_dense_d(const DevIndex &ix, const JoinArgs &ja, bool unicomp, dim3 grid, cudaStream_t s);
+
+}  // namespace sj

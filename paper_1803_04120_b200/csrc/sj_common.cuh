@@ -183,6 +183,7 @@ struct sj_index {
     sj::DevIndex dev{};          // same, in kernel form
     void *bufs[16] = {nullptr};  // owned device allocations
     int nbufs = 0;
+    char *arena = nullptr;       // the build's contiguous arena (sj_index_view.packed), if any
 };
 
 struct sj_batch {
@@ -253,7 +254,7 @@ struct CtxGuard {
 
 // index_build.cu
 sj_index *build_index_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &o);
-sj_index *import_index_impl(const sj_index_view &v, int device);
+sj_index *import_index_impl(const sj_index_view &v, int device, bool borrow);
 void free_index_impl(sj_index *idx);
 
 // radix_sort.cu

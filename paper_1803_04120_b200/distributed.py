@@ -1,26 +1,37 @@
-"""Multi-GPU glue: query sharding with a replicated index (north_star "Partitioning").
+"""Multi-GPU glue: query sharding with a replicated index (north_star "Partitioning", SURVEY §8(e)).
 
 One process per GPU (torchrun), ``torch.distributed`` for the plumbing:
-  1. rank 0 builds the index (sj_build_index);
-  2. the index arrays (B, G, A, pcell, X, masks) and its geometry are broadcast from rank 0
-     (NCCL over NVLink on B200; gloo in the CPU tests) -- the one exchange step of the path;
-  3. every rank imports the arrays (sj_index_import) and joins its own contiguous A-order
-     query range (sj_self_join with query_begin/query_end); with unicomp a rank emits both
+  1. rank 0 builds the index (sj_build_index) and plans the shards from the build's sampled
+     result-size estimate (sj_plan_shards: contiguous A-order query ranges of equal estimated work);
+  2. rank 0 broadcasts a small int64 header (geometry, sizes, array offsets, shard cuts) and then the
+     index's arrays as ONE packed device buffer (sj_index_view.packed: X, A, pcell, G, masks, B) --
+     the one exchange step of the path (NCCL over NVLink on B200; gloo in the CPU tests);
+  3. every other rank imports the received buffer in place (sj_index_import_borrowed: no copy; the
+     prefix directory, occupancy bitmaps and dense-cell tasks are rebuilt from B and G) and joins its
+     own query range (sj_self_join with query_begin/query_end); with unicomp a rank emits both
      orientations of every pair its queries decide, so the shards partition S exactly;
-  4. pair counts are combined with an all-reduce (SUM); pairs stay on their rank.
+  4. [pairs, cells_probed, candidates_tested, retries] are all-reduced (SUM); pairs stay on their rank.
 
 Everything here is marshalling: no step of the method runs in Python.
 """
 from __future__ import annotations
 
 import struct
-from typing import Dict, Optional, Sequence, Tuple
+from typing import Optional, Sequence, Tuple
 
 import numpy as np
 
 SJ_MAX_DIM = 6
-# meta layout (int64 words): n, d, n_cells, key_bits, mask_bits, device-independent geometry
-_META_WORDS = 5 + 3 + SJ_MAX_DIM * 3 + (SJ_MAX_DIM + 1)
+MAX_WORLD = 64
+# header layout (int64 words):
+#   [0:5]   n, d, n_cells, key_bits, mask_bits
+#   [5:8]   eps, eps2, w (float64 bit patterns)
+#   [8:26]  mins (bits), cpd, strides (SJ_MAX_DIM each)
+#   [26:33] mask_offsets (SJ_MAX_DIM + 1)
+#   [33:41] packed_bytes, off_X, off_A, off_pcell, off_G, off_masks (-1: separate), off_B, world
+#   [41:41+MAX_WORLD+1] shard cuts
+_GEOM_WORDS = 5 + 3 + SJ_MAX_DIM * 3 + (SJ_MAX_DIM + 1)
+_META_WORDS = _GEOM_WORDS + 8 + MAX_WORLD + 1
 
 
 def _f2i(x: float) -> int:
@@ -31,8 +42,18 @@ def _i2f(x: int) -> float:
     return struct.unpack("<d", struct.pack("<q", int(x)))[0]
 
 
-def pack_meta(geom: dict, n: int, n_cells: int, mask_bits: int) -> np.ndarray:
-    """Geometry of an index as int64 words (float64 fields bit-cast, so transfer is exact)."""
+def _u2i(x: int) -> int:
+    return int(np.uint64(x).astype(np.int64))
+
+
+def _i2u(x) -> int:
+    return int(np.int64(x).astype(np.uint64))
+
+
+def pack_meta(geom: dict, n: int, n_cells: int, mask_bits: int, layout: Optional[dict] = None,
+              cuts: Optional[Sequence[int]] = None) -> np.ndarray:
+    """Geometry, packed-buffer layout and shard cuts of an index as int64 words (float64 fields
+    bit-cast, so the transfer is exact)."""
     d = int(geom["d"])
     m = np.zeros(_META_WORDS, dtype=np.int64)
     m[0:5] = [n, d, n_cells, geom["key_bits"], mask_bits]
@@ -40,11 +61,21 @@ def pack_meta(geom: dict, n: int, n_cells: int, mask_bits: int) -> np.ndarray:
     o = 8
     for j in range(d):
         m[o + j] = _f2i(geom["mins"][j])
-        m[o + SJ_MAX_DIM + j] = np.uint64(geom["cpd"][j]).astype(np.int64)
-        m[o + 2 * SJ_MAX_DIM + j] = np.uint64(geom["strides"][j]).astype(np.int64)
+        m[o + SJ_MAX_DIM + j] = _u2i(geom["cpd"][j])
+        m[o + 2 * SJ_MAX_DIM + j] = _u2i(geom["strides"][j])
     o += 3 * SJ_MAX_DIM
     for j in range(d + 1):
         m[o + j] = geom["mask_offsets"][j]
+    o = _GEOM_WORDS
+    if layout is not None:
+        m[o:o + 7] = [layout["packed_bytes"], layout["X"], layout["A"], layout["pcell"], layout["G"],
+                      layout.get("masks", -1), layout["B"]]
+    if cuts is not None:
+        w = len(cuts) - 1
+        if w > MAX_WORLD:
+            raise ValueError(f"world > {MAX_WORLD}")
+        m[o + 7] = w
+        m[o + 8:o + 8 + w + 1] = np.asarray(cuts, dtype=np.int64)
     return m
 
 
@@ -54,70 +85,45 @@ def unpack_meta(m: np.ndarray) -> Tuple[dict, int, int, int]:
     geom = dict(d=d, key_bits=key_bits, eps=_i2f(m[5]), eps2=_i2f(m[6]), w=_i2f(m[7]))
     o = 8
     geom["mins"] = [_i2f(m[o + j]) for j in range(d)]
-    geom["cpd"] = [int(np.int64(m[o + SJ_MAX_DIM + j]).astype(np.uint64)) for j in range(d)]
-    geom["strides"] = [int(np.int64(m[o + 2 * SJ_MAX_DIM + j]).astype(np.uint64)) for j in range(d)]
+    geom["cpd"] = [_i2u(m[o + SJ_MAX_DIM + j]) for j in range(d)]
+    geom["strides"] = [_i2u(m[o + 2 * SJ_MAX_DIM + j]) for j in range(d)]
     o += 3 * SJ_MAX_DIM
     geom["mask_offsets"] = [int(m[o + j]) for j in range(d + 1)]
     return geom, n, n_cells, mask_bits
 
 
-ARRAY_SPECS = ("B", "G", "A", "pcell", "X", "masks")
+def unpack_layout(m: np.ndarray) -> Tuple[dict, np.ndarray]:
+    m = np.asarray(m, dtype=np.int64)
+    o = _GEOM_WORDS
+    keys = ("packed_bytes", "X", "A", "pcell", "G", "masks", "B")
+    layout = {k: int(v) for k, v in zip(keys, m[o:o + 7])}
+    w = int(m[o + 7])
+    cuts = m[o + 8:o + 8 + w + 1].copy() if w > 0 else np.zeros(0, dtype=np.int64)
+    return layout, cuts
 
 
-def _shapes(n: int, d: int, n_cells: int, mask_bits: int) -> Dict[str, Tuple[tuple, str]]:
-    # torch has no unsigned 64/32-bit collectives: int64/int32 carry the same bits
-    return {"B": ((n_cells,), "int64"), "G": ((n_cells + 1,), "int32"), "A": ((n,), "int32"),
-            "pcell": ((n,), "int32"), "X": ((d, n), "float64"), "masks": (((mask_bits + 31) // 32,), "int32")}
-
-
-def broadcast_index_arrays(arrays: Optional[Dict[str, "torch.Tensor"]], meta: Optional[np.ndarray],
-                           device, group=None, src: int = 0):
-    """Broadcast geometry + index arrays from `src`.  Returns (meta, arrays) on every rank.
-
-    `arrays` (rank src only): B, G, A, pcell, X[, masks] as tensors on `device` (dtype bits as in
-    ``_shapes``).  Other ranks pass None and receive freshly allocated tensors.
-    """
-    import torch
-    import torch.distributed as dist
-    rank = dist.get_rank(group)
-    mt = torch.zeros(_META_WORDS, dtype=torch.int64, device=device)
-    if rank == src:
-        mt.copy_(torch.from_numpy(np.asarray(meta, dtype=np.int64)))
-    dist.broadcast(mt, src=src, group=group)
-    meta = mt.cpu().numpy()
-    geom, n, n_cells, mask_bits = unpack_meta(meta)
-    out = {}
-    for name, (shape, dt) in _shapes(n, geom["d"], n_cells, mask_bits).items():
-        if name == "masks" and mask_bits == 0:
-            continue
-        if rank == src:
-            t = arrays[name]
-            t = t.view(getattr(torch, dt)) if t.dtype != getattr(torch, dt) else t
-            t = t.reshape(shape).contiguous()
-        else:
-            t = torch.empty(shape, dtype=getattr(torch, dt), device=device)
-        dist.broadcast(t, src=src, group=group)
-        out[name] = t
-    return meta, out
-
-
-def index_to_arrays(idx) -> Tuple[np.ndarray, Dict[str, "torch.Tensor"]]:
-    """(meta, arrays) of a built sj index, arrays as zero-copy device tensors."""
-    import torch
+def index_meta(idx, cuts=None) -> Tuple[np.ndarray, "torch.Tensor", Optional["torch.Tensor"]]:
+    """(header words, packed uint8 device buffer, separate masks tensor or None) of a built index."""
+    v = idx.view
     g = idx.geometry()
-    arr = idx.arrays()
-    mask_bits = int(g["mask_offsets"][-1]) if "masks" in arr else 0
-    meta = pack_meta(g, idx.n, idx.n_cells, mask_bits)
-    conv = {"B": torch.int64, "G": torch.int32, "A": torch.int32, "pcell": torch.int32, "masks": torch.int32}
-    out = {k: (v.view(conv[k]) if k in conv else v) for k, v in arr.items()}
-    return meta, out
+    has_masks = bool(v.masks)
+    mask_bits = int(g["mask_offsets"][-1]) if has_masks else 0
+    sep = has_masks and int(v.off_masks) == 0xFFFFFFFFFFFFFFFF
+    layout = {"packed_bytes": int(v.packed_bytes), "X": int(v.off_X), "A": int(v.off_A),
+              "pcell": int(v.off_pcell), "G": int(v.off_G), "B": int(v.off_B),
+              "masks": -1 if (sep or not has_masks) else int(v.off_masks)}
+    meta = pack_meta(g, idx.n, idx.n_cells, mask_bits, layout, cuts)
+    buf = idx.packed()
+    masks = idx.arrays()["masks"] if sep else None
+    return meta, buf, masks
 
 
-def arrays_to_index(meta: np.ndarray, arrays: Dict[str, "torch.Tensor"], device: int):
-    """sj_index_import of broadcast arrays (copied into a library-owned index)."""
+def view_from_packed(meta: np.ndarray, buf, masks, device: int):
+    """sj_index_view whose arrays point into the received packed buffer (+ separate masks)."""
     import ctypes
     from . import sj
     geom, n, n_cells, mask_bits = unpack_meta(meta)
+    layout, _ = unpack_layout(meta)
     v = sj.IndexView()
     d = geom["d"]
     v.d, v.device, v.n, v.n_cells = d, device, n, n_cells
@@ -129,17 +135,47 @@ def arrays_to_index(meta: np.ndarray, arrays: Dict[str, "torch.Tensor"], device:
     v.key_bits = geom["key_bits"]
     for j in range(d + 1):
         v.mask_offsets[j] = geom["mask_offsets"][j]
+    base = buf.data_ptr()
     for name in ("B", "G", "A", "pcell", "X"):
-        setattr(v, name, ctypes.c_void_p(arrays[name].data_ptr()))
-    v.masks = ctypes.c_void_p(arrays["masks"].data_ptr()) if mask_bits and "masks" in arrays else None
-    return sj.import_index(v, device)
+        setattr(v, name, ctypes.c_void_p(base + layout[name]))
+    if mask_bits:
+        v.masks = ctypes.c_void_p(masks.data_ptr() if layout["masks"] < 0 else base + layout["masks"])
+    else:
+        v.masks = None
+    v.packed = ctypes.c_void_p(base)
+    v.packed_bytes = layout["packed_bytes"]
+    return v
+
+
+def broadcast_index(meta: Optional[np.ndarray], buf, masks, device, group=None, src: int = 0):
+    """Broadcast the header, then the packed index buffer (and, rarely, masks too large for the
+    packed buffer) from `src`.  Non-src ranks pass None and receive fresh tensors on `device`.
+    Returns (meta, buf, masks) on every rank."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    mt = torch.zeros(_META_WORDS, dtype=torch.int64, device=device)
+    if rank == src:
+        mt.copy_(torch.from_numpy(np.asarray(meta, dtype=np.int64)))
+    dist.broadcast(mt, src=src, group=group)
+    meta = mt.cpu().numpy()
+    geom, n, n_cells, mask_bits = unpack_meta(meta)
+    layout, _ = unpack_layout(meta)
+    if rank != src:
+        buf = torch.empty(layout["packed_bytes"], dtype=torch.uint8, device=device)
+    dist.broadcast(buf, src=src, group=group)
+    if mask_bits and layout["masks"] < 0:
+        if rank != src:
+            masks = torch.empty((mask_bits + 31) // 32, dtype=torch.int32, device=device)
+        else:
+            masks = masks.view(torch.int32)
+        dist.broadcast(masks, src=src, group=group)
+    return meta, buf, masks
 
 
 def plan_shards(n: int, world: int, weights: Optional[Sequence[float]] = None) -> np.ndarray:
-    """Contiguous A-order query ranges [cuts[r], cuts[r+1]) for `world` ranks.
-
-    With per-query work weights (e.g. sampled estimator counts expanded to queries), ranges are
-    cut at equal cumulative weight; otherwise at equal query counts."""
+    """Host-side shard cuts for tests and the dry run: equal query counts, or equal cumulative
+    weight.  (The GPU path uses sj_plan_shards, balanced by the sampled estimate.)"""
     if world < 1:
         raise ValueError("world must be >= 1")
     if weights is None:
@@ -153,8 +189,7 @@ def plan_shards(n: int, world: int, weights: Optional[Sequence[float]] = None) -
     for r in range(1, world):
         cuts.append(int(np.searchsorted(c, tot * r / world, side="left")))
     cuts.append(n)
-    cuts = np.maximum.accumulate(np.array(cuts, dtype=np.int64))
-    return cuts
+    return np.maximum.accumulate(np.array(cuts, dtype=np.int64))
 
 
 def allreduce_counts(values: Sequence[int], device, op: str = "sum", group=None) -> np.ndarray:
@@ -165,10 +200,15 @@ def allreduce_counts(values: Sequence[int], device, op: str = "sum", group=None)
     return t.cpu().numpy()
 
 
-def sharded_self_join(points, eps: float, device: int, group=None, **join_kw):
-    """Full multi-GPU step: rank-0 build -> broadcast -> import -> shard join -> all-reduce.
+COUNTERS = ("pairs", "cells_probed", "candidates_tested", "retries")
 
-    Returns (local Result, global pair count, local index)."""
+
+def sharded_self_join(points, eps: float, device: int, group=None, stats: bool = False, **join_kw):
+    """Full multi-GPU step: rank-0 build + shard plan -> broadcast (header + packed buffer) ->
+    borrowed import -> shard join -> all-reduce of the work counters.
+
+    Returns (local Result or None, global pair count, local Index) -- and with stats=True also the
+    dict of all-reduced counters."""
     import torch
     import torch.distributed as dist
     from . import sj
@@ -180,18 +220,28 @@ def sharded_self_join(points, eps: float, device: int, group=None, **join_kw):
     if world == 1:
         idx = sj.build_index(points, eps, device=device)
         res = sj.self_join(idx, **join_kw)
+        if stats:
+            st = res.stats
+            return res, res.n_pairs, idx, {k: int(st[k]) for k in COUNTERS}
         return res, res.n_pairs, idx
     if rank == 0:
-        idx0 = sj.build_index(points, eps, device=device)
-        meta, arrays = index_to_arrays(idx0)
+        idx = sj.build_index(points, eps, device=device)
+        cuts = sj.plan_shards(idx, world)
+        meta, buf, masks = index_meta(idx, cuts)
     else:
-        idx0, meta, arrays = None, None, None
-    meta, arrays = broadcast_index_arrays(arrays, meta, dev, group=group)
-    idx = idx0 if rank == 0 else arrays_to_index(meta, arrays, device)
-    n = idx.n
-    cuts = plan_shards(n, world)
+        idx, meta, buf, masks = None, None, None, None
+    meta, buf, masks = broadcast_index(meta, buf, masks, dev, group=group)
+    if rank != 0:
+        idx = sj.import_index(view_from_packed(meta, buf, masks, device), device, borrow=(buf, masks))
+    _, cuts = unpack_layout(meta)
     a, b = int(cuts[rank]), int(cuts[rank + 1])
     res = sj.self_join(idx, query_begin=a, query_end=b, **join_kw) if b > a else None
-    local = res.n_pairs if res is not None else 0
-    total = int(allreduce_counts([local], dev, group=group)[0])
-    return res, total, idx
+    if res is not None:
+        st = res.stats
+        local = [int(st[k]) for k in COUNTERS]
+    else:
+        local = [0] * len(COUNTERS)
+    tot = allreduce_counts(local, dev, group=group)
+    if stats:
+        return res, int(tot[0]), idx, dict(zip(COUNTERS, (int(x) for x in tot)))
+    return res, int(tot[0]), idx

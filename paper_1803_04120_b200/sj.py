@@ -57,7 +57,9 @@ class IndexView(ctypes.Structure):
                 ("B", vp), ("G", vp), ("A", vp), ("pcell", vp), ("X", vp), ("masks", vp),
                 ("dir_k", i32), ("dir_entries", u64), ("dir", vp),
                 ("t_h2d_ms", f32), ("t_geometry_ms", f32), ("t_keys_ms", f32), ("t_sort_ms", f32),
-                ("t_compact_ms", f32), ("t_total_ms", f32)]
+                ("t_compact_ms", f32), ("t_total_ms", f32),
+                ("packed", vp), ("packed_bytes", u64), ("off_X", u64), ("off_A", u64), ("off_pcell", u64),
+                ("off_G", u64), ("off_masks", u64), ("off_B", u64)]
 
 
 class SJError(RuntimeError):
@@ -89,6 +91,8 @@ def load_library(path: str = LIB_PATH):
     L.sj_build_index.restype = i32
     L.sj_self_join.argtypes = [vp, P(JoinOpts), P(vp)]
     L.sj_self_join.restype = i32
+    L.sj_self_join_points.argtypes = [vp, u64, i32, dbl, P(BuildOpts), P(JoinOpts), P(vp), P(vp)]
+    L.sj_self_join_points.restype = i32
     L.sj_free_result.argtypes = [vp]
     L.sj_free_result.restype = None
     L.sj_free_result_async.argtypes = [vp, vp]
@@ -97,6 +101,8 @@ def load_library(path: str = LIB_PATH):
     L.sj_result_fingerprint.restype = i32
     L.sj_plan_shards.argtypes = [vp, u32, vp]
     L.sj_plan_shards.restype = i32
+    L.sj_diag_fp64_peak.argtypes = [i32, P(dbl), P(dbl)]
+    L.sj_diag_fp64_peak.restype = i32
     L.sj_trim.argtypes = [i32]
     L.sj_trim.restype = i32
     L.sj_set_result_cache_limit.argtypes = [u64]
@@ -121,6 +127,8 @@ def load_library(path: str = LIB_PATH):
     L.sj_index_timings.restype = i32
     L.sj_index_import.argtypes = [P(IndexView), i32, P(vp)]
     L.sj_index_import.restype = i32
+    L.sj_index_import_borrowed.argtypes = [P(IndexView), i32, P(vp)]
+    L.sj_index_import_borrowed.restype = i32
     L.sj_set_allocator.argtypes = [vp, vp, vp]
     L.sj_set_allocator.restype = None
     L.sj_plan_batches.argtypes = [vp, u64, u64, u64, u64, u64, i32, dbl, vp, u32, P(u32), P(u64)]
@@ -220,10 +228,20 @@ class Index:
             out["dir"] = _device_tensor(v.dir, (int(v.dir_entries),), torch.uint32, self.device, self)
         return out
 
+    def packed(self):
+        """Zero-copy uint8 device tensor of the index's contiguous array buffer
+        (sj_index_view.packed: X, A, pcell, G, masks, B at the view's off_* offsets), or None."""
+        import torch
+        v = self.view
+        if not v.packed:
+            return None
+        return _device_tensor(v.packed, (int(v.packed_bytes),), torch.uint8, self.device, self)
+
     def free(self):
         if self._h and self._h.value:
             load_library().sj_free_index(self._h)
             self._h = ctypes.c_void_p(0)
+        self._keep = None
 
     def __del__(self):
         try:
@@ -253,15 +271,13 @@ def _device_tensor(ptr, shape, dtype, device, owner):
     return t
 
 
-def build_index(points, eps: float, device: Optional[int] = None, stream=None, build_masks: bool = True,
-                speculative_estimate: bool = True) -> Index:
-    """sj_build_index.  points: N x d float64 (torch cuda/cpu tensor or numpy array)."""
+def _points_arg(points, device, stream, build_masks=True, speculative_estimate=True):
+    """(BuildOpts, pointer, n, d, keepalive) for sj_build_index / sj_self_join_points."""
     L = load_library()
     o = BuildOpts()
     L.sj_build_opts_default(ctypes.byref(o))
     o.build_masks = int(build_masks)
     o.speculative_estimate = int(speculative_estimate)
-    keep = None
     try:
         import torch
         is_torch = isinstance(points, torch.Tensor)
@@ -272,9 +288,7 @@ def build_index(points, eps: float, device: Optional[int] = None, stream=None, b
         if t.dtype != torch.float64 or t.dim() != 2:
             raise TypeError("points must be a 2-D float64 tensor")
         t = t.contiguous()
-        keep = t
         n, d = t.shape
-        ptr = t.data_ptr()
         if t.is_cuda:
             o.points_on_device = 1
             o.device = t.device.index if device is None else device
@@ -283,19 +297,40 @@ def build_index(points, eps: float, device: Optional[int] = None, stream=None, b
         else:
             o.points_on_device = 0
             o.device = 0 if device is None else device
-    else:
-        a = np.ascontiguousarray(points, dtype=np.float64)
-        if a.ndim != 2:
-            raise TypeError("points must be N x d")
-        keep = a
-        n, d = a.shape
-        ptr = a.ctypes.data
-        o.points_on_device = 0
-        o.device = 0 if device is None else device
+        return o, t.data_ptr(), n, d, t
+    a = np.ascontiguousarray(points, dtype=np.float64)
+    if a.ndim != 2:
+        raise TypeError("points must be N x d")
+    n, d = a.shape
+    o.points_on_device = 0
+    o.device = 0 if device is None else device
+    return o, a.ctypes.data, n, d, a
+
+
+def build_index(points, eps: float, device: Optional[int] = None, stream=None, build_masks: bool = True,
+                speculative_estimate: bool = True) -> Index:
+    """sj_build_index.  points: N x d float64 (torch cuda/cpu tensor or numpy array)."""
+    L = load_library()
+    o, ptr, n, d, keep = _points_arg(points, device, stream, build_masks, speculative_estimate)
     h = ctypes.c_void_p()
     _check(L.sj_build_index(ctypes.c_void_p(ptr), n, d, float(eps), ctypes.byref(o), ctypes.byref(h)))
     del keep
     return Index(h.value)
+
+
+def join_points(points, eps: float, device: Optional[int] = None, stream=None, keep_index: bool = True,
+                **join_kw):
+    """sj_self_join_points: build + join in one library call -> (Result, Index or None)."""
+    L = load_library()
+    o, ptr, n, d, keep = _points_arg(points, device, stream)
+    jo = join_opts(**join_kw)
+    hi, hr = ctypes.c_void_p(), ctypes.c_void_p()
+    _check(L.sj_self_join_points(ctypes.c_void_p(ptr), n, d, float(eps), ctypes.byref(o), ctypes.byref(jo),
+                                 ctypes.byref(hi) if keep_index else None, ctypes.byref(hr)))
+    del keep
+    r = Result(hr.value)
+    r.device = o.device
+    return r, (Index(hi.value) if keep_index else None)
 
 
 class Result:
@@ -391,6 +426,13 @@ class Result:
             pass
 
 
+def fp64_peak(device: int = 0) -> dict:
+    """sj_diag_fp64_peak: measured DADD / DMUL throughput (operations/s) of the FP64 pipe."""
+    a, m = dbl(), dbl()
+    _check(load_library().sj_diag_fp64_peak(int(device), ctypes.byref(a), ctypes.byref(m)))
+    return {"dadd_ops_per_s": a.value, "dmul_ops_per_s": m.value}
+
+
 def trim(device: int = -1):
     """sj_trim: release the library's caches (result batches, build scratch, pinned blocks, pool)."""
     _check(load_library().sj_trim(int(device)))
@@ -470,11 +512,16 @@ def plan_shards(index: Index, world: int) -> np.ndarray:
     return cuts.astype(np.int64)
 
 
-def import_index(view: IndexView, device: int) -> Index:
+def import_index(view: IndexView, device: int, borrow=None) -> Index:
+    """sj_index_import (arrays copied), or with borrow=<object owning the arrays>
+    sj_index_import_borrowed: the index reads the view's arrays in place and keeps `borrow` alive."""
     L = load_library()
     h = ctypes.c_void_p()
-    _check(L.sj_index_import(ctypes.byref(view), device, ctypes.byref(h)))
-    return Index(h.value)
+    if borrow is None:
+        _check(L.sj_index_import(ctypes.byref(view), device, ctypes.byref(h)))
+        return Index(h.value)
+    _check(L.sj_index_import_borrowed(ctypes.byref(view), device, ctypes.byref(h)))
+    return Index(h.value, keepalive=borrow)
 
 
 def plan_batches(sample_counts, step: int, q_begin: int, q_end: int, capacity: int, min_batches: int = 3,

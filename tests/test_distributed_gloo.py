@@ -21,8 +21,9 @@ def _free_port():
     return p
 
 
-def _ref_arrays():
-    """Index arrays of a small dataset, from the oracle's statement of the index (test-side)."""
+def _ref_index():
+    """Index arrays of a small dataset from the oracle's statement of the index (test-side), laid
+    out in ONE packed byte buffer the way sj_index_view.packed is (X, A, pcell, G, masks, B)."""
     import datagen
     from oracle import index_ref as ir
     pts = datagen.uniform(500, 3, seed=3)
@@ -31,13 +32,23 @@ def _ref_arrays():
     geom = dict(d=3, key_bits=int(g.n_cells - 1).bit_length(), eps=9.0, eps2=81.0, w=g.w,
                 mins=g.mins.tolist(), cpd=g.cpd, strides=g.strides, mask_offsets=[0, 7, 14, 21])
     n, nG = len(pts), len(idx.B)
-    pcell = np.repeat(np.arange(nG), np.diff(idx.G)).astype(np.int32)
-    arrays = {"B": torch.tensor(np.array(idx.B, dtype=np.uint64).view(np.int64)),
-              "G": torch.tensor(idx.G.astype(np.int32)), "A": torch.tensor(idx.A.astype(np.int32)),
-              "pcell": torch.tensor(pcell), "X": torch.tensor(pts[idx.A].T.copy()),
-              "masks": torch.tensor(np.array([0x12345], dtype=np.int32))}   # 21 mask bits = 1 word
-    meta = sjd.pack_meta(geom, n, nG, 21)
-    return meta, arrays, geom
+    parts = {"X": pts[idx.A].T.copy().view(np.uint8).ravel(),
+             "A": idx.A.astype(np.uint32).view(np.uint8),
+             "pcell": np.repeat(np.arange(nG), np.diff(idx.G)).astype(np.uint32).view(np.uint8),
+             "G": idx.G.astype(np.uint32).view(np.uint8),
+             "masks": np.array([0x12345], dtype=np.uint32).view(np.uint8),
+             "B": np.array(idx.B, dtype=np.uint64).view(np.uint8)}
+    layout, off = {}, 0
+    for k, v in parts.items():
+        layout[k] = off
+        off += (len(v) + 255) // 256 * 256
+    buf = np.zeros(off, dtype=np.uint8)
+    for k, v in parts.items():
+        buf[layout[k]:layout[k] + len(v)] = v
+    layout["packed_bytes"] = off
+    cuts = sjd.plan_shards(n, 2)
+    meta = sjd.pack_meta(geom, n, nG, 21, layout, cuts)
+    return meta, torch.from_numpy(buf), geom, parts, layout
 
 
 def _worker(rank, world, port, out_q):
@@ -45,23 +56,22 @@ def _worker(rank, world, port, out_q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        meta, arrays, geom = _ref_arrays()
-        if rank != 0:
-            meta_in, arr_in = None, None
-        else:
-            meta_in, arr_in = meta, arrays
-        m, got = sjd.broadcast_index_arrays(arr_in, meta_in, torch.device("cpu"))
-        ok = np.array_equal(m, meta)
-        for k, v in arrays.items():
-            ok &= torch.equal(got[k], v)
+        meta, buf, geom, parts, layout = _ref_index()
+        args = (meta, buf, None) if rank == 0 else (None, None, None)
+        m, got, masks = sjd.broadcast_index(*args, torch.device("cpu"))
+        ok = np.array_equal(m, meta) and masks is None
+        lay, cuts = sjd.unpack_layout(m)
+        ok &= lay == {k: (layout[k] if k in layout else -1) for k in lay}
+        g = got.numpy()
+        for k, v in parts.items():
+            ok &= np.array_equal(g[lay[k]:lay[k] + len(v)], v)
         g2, n2, nG2, mb2 = sjd.unpack_meta(m)
         ok &= g2["w"] == geom["w"] and g2["cpd"] == geom["cpd"] and g2["mins"] == geom["mins"]
-        # shard plan + count all-reduce: the shards partition [0, n)
-        cuts = sjd.plan_shards(n2, world)
+        # shard cuts travel in the header; the count all-reduce sums the shards
         mine = int(cuts[rank + 1] - cuts[rank])
-        tot = sjd.allreduce_counts([mine], torch.device("cpu"))[0]
+        tot = sjd.allreduce_counts([mine, 1, 2, 3], torch.device("cpu"))
         mx = sjd.allreduce_counts([float(rank + 0.5)], torch.device("cpu"), op="max")[0]
-        out_q.put((rank, bool(ok), int(tot), float(mx)))
+        out_q.put((rank, bool(ok), int(tot[0]), float(mx), tot[1:].tolist()))
     finally:
         dist.destroy_process_group()
 
@@ -81,14 +91,18 @@ def test_broadcast_and_allreduce_world2():
     assert all(r[1] for r in res), res
     assert all(r[2] == 500 for r in res)
     assert all(r[3] == 1.5 for r in res)
+    assert all(r[4] == [2, 4, 6] for r in res)
 
 
 def test_meta_roundtrip_is_bit_exact():
     geom = dict(d=6, key_bits=41, eps=1.0, eps2=1.0, w=1.0000000000000069, mins=[-0.0, 5e-324, 1e308, -3.5, 0.1, 2.0],
                 cpd=[102, 2 ** 40, 3, 4, 5, 6], strides=[1, 102, 2 ** 47, 2 ** 62 + 5, 7, 8],
                 mask_offsets=[0, 1, 2, 3, 4, 5, 6])
-    m = sjd.pack_meta(geom, 123, 45, 6)
+    m = sjd.pack_meta(geom, 123, 45, 6, {"packed_bytes": 4096, "X": 0, "A": 512, "pcell": 1024, "G": 1536,
+                                          "masks": -1, "B": 2048}, [0, 50, 123])
     g, n, nG, mb = sjd.unpack_meta(m)
+    lay, cuts = sjd.unpack_layout(m)
+    assert lay["masks"] == -1 and lay["B"] == 2048 and cuts.tolist() == [0, 50, 123]
     assert (n, nG, mb) == (123, 45, 6)
     for k in ("eps", "eps2", "w"):
         assert np.float64(g[k]).tobytes() == np.float64(geom[k]).tobytes()

@@ -524,3 +524,36 @@ def test_trim_and_cache_limit(sj):
     sj.trim()
     sj.set_result_cache_limit(48 << 30)
     assert np.array_equal(sj.self_join(idx).to_numpy(), want)
+
+
+@pytest.mark.parametrize("d,n,eps", [(6, 2_000_000, 1.0), (6, 2_000_000, 4.0), (5, 2_000_000, 1.0),
+                                     (4, 300_000, 3.0), (2, 200_000, 0.5)])
+def test_imported_index_equals_built(sj, d, n, eps):
+    """The multi-GPU import path: an index imported from the exported arrays (copied)
+    and one imported in place from the packed buffer (sj_index_import_borrowed, what a non-zero rank
+    does with the broadcast buffer) join to the same S as the built index -- same |S| and
+    fingerprints -- in the sparse regimes whose occupancy bitmaps (occ, occ2) are rebuilt on import."""
+    from paper_1803_04120_b200 import distributed as sjd
+    pts = torch.from_numpy(datagen.uniform(n, d, seed=91 + d)).cuda()
+    idx = sj.build_index(pts, eps)
+    r0 = sj.self_join(idx)
+    want = (r0.n_pairs, r0.fingerprint())
+    r0.free()
+    copied = sj.import_index(idx.view, 0)
+    meta, buf, masks = sjd.index_meta(idx, sj.plan_shards(idx, 3))
+    buf2 = buf.clone()                         # stands for the received broadcast buffer
+    borrowed = sj.import_index(sjd.view_from_packed(meta, buf2, masks, 0), 0, borrow=(buf2, masks))
+    for imp in (copied, borrowed):
+        assert imp.n_cells == idx.n_cells
+        r = sj.self_join(imp)
+        assert (r.n_pairs, r.fingerprint()) == want
+        r.free()
+        # and sharded: the three ranges of the plan
+        _, cuts = sjd.unpack_layout(meta)
+        fa = fb = tot = 0
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            r = sj.self_join(imp, query_begin=int(a), query_end=int(b))
+            x, y = r.fingerprint()
+            fa, fb, tot = (fa + x) % 2**64, (fb + y) % 2**64, tot + r.n_pairs
+            r.free()
+        assert (tot, (fa, fb)) == want
