@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -390,10 +391,59 @@ static int trace_level()
     return lvl;
 }
 
+namespace {
+struct TraceEntry {
+    const char *what, *stage;
+    double host_us;
+    cudaEvent_t ev;
+};
+std::mutex g_tr_mu;
+std::vector<TraceEntry> g_tr;
+double g_tr_h0 = 0;
+cudaEvent_t g_tr_e0 = nullptr;
+int g_tr_dev = 0;
+
+void trace_dump()
+{
+    std::vector<TraceEntry> v;
+    cudaEvent_t e0;
+    double h0;
+    {
+        std::lock_guard<std::mutex> lk(g_tr_mu);
+        v.swap(g_tr);
+        e0 = g_tr_e0;
+        h0 = g_tr_h0;
+        g_tr_e0 = nullptr;
+    }
+    if (v.empty()) return;
+    for (auto &e : v)
+        if (e.ev) cudaEventSynchronize(e.ev);
+    std::fprintf(stderr, "[sj-timeline] %-7s %-34s %10s %10s\n", "", "stage", "host us", "gpu us");
+    for (auto &e : v) {
+        float ms = 0;
+        if (e.ev && e0) cudaEventElapsedTime(&ms, e0, e.ev);
+        if (e.ev)
+            std::fprintf(stderr, "[sj-timeline] %-7s %-34s %10.1f %10.1f\n", e.what, e.stage, e.host_us - h0,
+                         1000.0 * ms);
+        else
+            std::fprintf(stderr, "[sj-timeline] %-7s %-34s %10.1f %10s\n", e.what, e.stage, e.host_us - h0, "");
+    }
+    for (auto &e : v)
+        if (e.ev) event_put(g_tr_dev, e.ev);
+}
+}  // namespace
+
 HostTrace::HostTrace(const char *w) : what(w)
 {
     on = trace_level() > 0;
     t0 = last = on ? now_us() : 0.0;
+    if (trace_level() >= 2 && std::strcmp(w, "build") == 0) {
+        std::lock_guard<std::mutex> lk(g_tr_mu);
+        for (auto &e : g_tr)
+            if (e.ev) event_put(g_tr_dev, e.ev);
+        g_tr.clear();
+        g_tr_e0 = nullptr;
+    }
 }
 
 void HostTrace::dev(const char *stage, cudaStream_t s)
@@ -402,29 +452,32 @@ void HostTrace::dev(const char *stage, cudaStream_t s)
     int d = 0;
     cudaGetDevice(&d);
     cudaEvent_t e = event_get(d);       // pooled: recording costs ~1 us of host time, no creation
+    const double h = now_us();
     cudaEventRecord(e, s);
-    dev_ev.emplace_back(stage, e);
+    std::lock_guard<std::mutex> lk(g_tr_mu);
+    if (!g_tr_e0) {
+        g_tr_e0 = e;
+        g_tr_h0 = h;
+        g_tr_dev = d;
+    }
+    g_tr.push_back({what, stage, h, e});
 }
 
 HostTrace::~HostTrace()
 {
-    if (dev_ev.empty()) return;
-    cudaEventSynchronize(dev_ev.back().second);
-    for (size_t i = 1; i < dev_ev.size(); ++i) {
-        float ms = 0;
-        cudaEventElapsedTime(&ms, dev_ev[i - 1].second, dev_ev[i].second);
-        std::fprintf(stderr, "[sj-dev]   %-10s %-28s +%8.1f us (GPU)\n", what, dev_ev[i].first, 1000.0 * ms);
-    }
-    int d = 0;
-    cudaGetDevice(&d);
-    for (auto &pr : dev_ev) event_put(d, pr.second);
+    if (trace_level() >= 2 && std::strcmp(what, "join") == 0) trace_dump();
 }
 
 void HostTrace::mark(const char *stage)
 {
     if (!on) return;
     const double t = now_us();
-    std::fprintf(stderr, "[sj-trace] %-10s %-28s +%8.1f us  (t=%8.1f us)\n", what, stage, t - last, t - t0);
+    if (trace_level() >= 2) {
+        std::lock_guard<std::mutex> lk(g_tr_mu);
+        if (g_tr_e0) g_tr.push_back({what, stage, t, nullptr});
+    } else {
+        std::fprintf(stderr, "[sj-trace] %-10s %-28s +%8.1f us  (t=%8.1f us)\n", what, stage, t - last, t - t0);
+    }
     last = t;
 }
 

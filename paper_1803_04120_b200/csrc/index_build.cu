@@ -885,6 +885,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         tr.dev("minmax", s);
         k_geometry<<<1, 256, 0, s>>>(part, parts, d, eps, N, allow_bucket ? 1 : 0, o.build_masks ? 1 : 0, dgeom);
         SJ_LAUNCHED();
+        tr.dev("geometry", s);
         // the host's copy of the geometry travels on a side stream, so the key pass does not queue
         // behind the small D2H copy's latency
         DevGeom *hgeom = static_cast<DevGeom *>(cg.c->h_slots);
@@ -910,7 +911,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ba.bhist = bhist;
         launch(d, 1, grid, s, ix, ba);
         ev.rec(3, s);
-        tr.dev("geometry + keys", s);
+        tr.dev("keys", s);
         tr.mark("minmax/geometry/keys enqueued");
         SJ_CUDA(cudaEventSynchronize(cg.c->events[0]));
         tr.mark("geometry read");
@@ -1000,6 +1001,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         tr.mark("geometry + allocs");
         idx->view = v;
         alloc_dir(idx, dp, s);
+        tr.dev("alloc dir", s);
         uint32_t *dir = const_cast<uint32_t *>(idx->dev.dir);
 
         // ---- a3: sort of (key, id) into (key, id)-ascending order (= stable sort by key, R14)
@@ -1075,6 +1077,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         idx->dev = ix;
         // LSD path: the directory from its histogram (the bucket path scanned it before compaction)
         if (dirhist.p) exclusive_scan_u32(dirhist.p, dir, (uint64_t)dp.P + 1, s);
+        tr.mark("compaction enqueued");
         // a5 for the default join, speculatively, before the final sync: the provisional index
         // bounds cell ranges by N (B carries a sentinel after the last cell) and chooses the search
         // mode from N; the result is kept only if the mode from |G| is the same

@@ -333,6 +333,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             SJ_CUDA(cudaMemcpyAsync(hbk, dbk, nbk * 8, cudaMemcpyDeviceToHost, s0));
             SJ_CUDA(cudaStreamSynchronize(s0));
         }
+        tr.dev("join start", s0);
         tr.mark("estimate (synced)");
 
         // ---- plan (k >= min_batches contiguous A-order ranges)
@@ -374,9 +375,11 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 ja.n_dense_tasks = ix.n_dense_tasks;
             }
             SJ_CUDA(cudaEventRecord(e0, s));
+            tr.dev("refine launch", s);
             launch_refine<kEmit>(ix, ja, o.unicomp != 0, (uint32_t)(b - a), s);
             launch_dense(ix, ja, o.unicomp != 0, s);
             SJ_CUDA(cudaEventRecord(e1, s));
+            tr.dev("refine done", s);
             ++launches;
         };
 

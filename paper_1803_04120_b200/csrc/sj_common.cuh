@@ -29,13 +29,16 @@ inline void count_launch(uint64_t k = 1) { g_kernel_launches.fetch_add(k, std::m
 // Checks the launch configuration error right after a <<<>>> launch.
 #define SJ_LAUNCHED() do { ::sj::count_launch(); SJ_CUDA(cudaGetLastError()); } while (0)
 
-// ---------------------------------------------------------------- host tracing (SJ_TRACE=1)
+// ---------------------------------------------------------------- host tracing (SJ_TRACE=1..2)
+// SJ_TRACE=1: host marks printed as they happen.  SJ_TRACE=2: one step's timeline (from the start of
+// a build to the end of the following join): every mark() with its host time and every dev() with
+// its host enqueue time AND the GPU time its stream reached that point (pooled events), printed
+// together when the join's trace ends -- a GPU time well after the host time means the GPU was busy,
+// one just after it means the GPU waited for the host.
 struct HostTrace {
     bool on;
     const char *what;
     double t0, last;
-    // device timeline (SJ_TRACE=2): an event per dev() call; printed as GPU-side deltas at exit
-    std::vector<std::pair<const char *, cudaEvent_t>> dev_ev;
     explicit HostTrace(const char *w);
     ~HostTrace();
     void mark(const char *stage);
