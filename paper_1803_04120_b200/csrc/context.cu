@@ -41,6 +41,7 @@ static void ensure(DevCtx *c, int nstreams, int nevents, size_t slot_bytes)
         size_t b = 4096;
         while (b < slot_bytes) b <<= 1;
         SJ_CUDA(cudaMalloc(&c->d_slots, b));
+        SJ_CUDA(cudaMemset(c->d_slots, 0, b));       // (the build's last-CTA counter starts at 0)
         SJ_CUDA(cudaHostAlloc(&c->h_slots, b, cudaHostAllocPortable));
         c->slot_bytes = b;
     }
@@ -113,7 +114,7 @@ void event_put(int dev, cudaEvent_t e)
 // gigabytes of result batches on another stream (measured 0.36 ms per build on 2-D eps=1).  A build
 // holds it from allocation to its final stream sync; a concurrent build falls back to the pool.
 namespace {
-struct ScratchSlot { void *p = nullptr; size_t bytes = 0; bool busy = false; };
+struct ScratchSlot { void *p = nullptr; size_t bytes = 0; bool busy = false; size_t zero = 0; };
 std::mutex g_scr_mu;
 std::map<int, ScratchSlot> g_scr;
 }  // namespace
@@ -263,8 +264,9 @@ int device_sm_count(int dev)
     return nsm;
 }
 
-void *scratch_acquire(int dev, size_t bytes)
+void *scratch_acquire(int dev, size_t bytes, size_t *zero_prefix)
 {
+    *zero_prefix = 0;
     if (alloc_hook_set()) return nullptr;      // scratch goes through the hook (dev_alloc) too
     std::lock_guard<std::mutex> lk(g_scr_mu);
     ScratchSlot &sl = g_scr[dev];
@@ -273,6 +275,7 @@ void *scratch_acquire(int dev, size_t bytes)
         if (sl.p) cudaFree(sl.p);
         sl.p = nullptr;
         sl.bytes = 0;
+        sl.zero = 0;
         const size_t b = bytes + bytes / 4;
         if (cudaMalloc(&sl.p, b) != cudaSuccess) {
             cudaGetLastError();
@@ -282,14 +285,19 @@ void *scratch_acquire(int dev, size_t bytes)
         sl.bytes = b;
     }
     sl.busy = true;
+    *zero_prefix = sl.zero;
+    sl.zero = 0;                               // unknown while the build runs
     return sl.p;
 }
 
-void scratch_release(int dev, void *p)
+void scratch_release(int dev, void *p, size_t zero_prefix)
 {
     std::lock_guard<std::mutex> lk(g_scr_mu);
     ScratchSlot &sl = g_scr[dev];
-    if (sl.p == p) sl.busy = false;
+    if (sl.p == p) {
+        sl.busy = false;
+        sl.zero = zero_prefix;
+    }
 }
 
 void scratch_trim(int dev)

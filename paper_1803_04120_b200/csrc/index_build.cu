@@ -17,8 +17,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <set>
 
-#include "sj_common.cuh"
+#include "scan.cuh"
 
 namespace sj {
 
@@ -31,52 +33,6 @@ __device__ __forceinline__ unsigned long long ord_key(double x)
 {
     const unsigned long long u = (unsigned long long)__double_as_longlong(x);
     return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
-}
-
-// a1: exact per-dimension min/max (+ non-finite flag) in ONE pass: each block reduces its points
-// and writes its partial (order-preserving integer images, no atomics, no initialisation):
-// part[b][0..D) = ord(min), part[b][D..2D) = ord(max), part[b][2D] = non-finite flag.  k_geometry
-// reduces the partials.
-template <int D>
-__global__ void __launch_bounds__(kThreads)
-k_minmax(const double *__restrict__ pts, uint32_t n, unsigned long long *__restrict__ part)
-{
-    double mn[D], mx[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) { mn[j] = INFINITY; mx[j] = -INFINITY; }
-    bool bad = false;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            const double x = pts[i * D + j];
-            bad |= !isfinite(x);
-            mn[j] = fmin(mn[j], x);
-            mx[j] = fmax(mx[j], x);
-        }
-    }
-    const bool any_bad = __syncthreads_or(bad);
-    __shared__ double s_mn[kThreads / 32][D], s_mx[kThreads / 32][D];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        double a = mn[j], b = mx[j];
-        for (int o = 16; o; o >>= 1) {
-            a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
-            b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
-        }
-        if (lane == 0) { s_mn[warp][j] = a; s_mx[warp][j] = b; }
-    }
-    __syncthreads();
-    unsigned long long *out = part + (uint64_t)blockIdx.x * (2 * D + 1);
-    if (threadIdx.x < D) {
-        const int j = threadIdx.x;
-        double a = INFINITY, b = -INFINITY;
-        for (int w = 0; w < kThreads / 32; ++w) { a = fmin(a, s_mn[w][j]); b = fmax(b, s_mx[w][j]); }
-        out[j] = ord_key(a);            // +inf / -inf when the block saw no point
-        out[D + j] = ord_key(b);
-    }
-    if (threadIdx.x == 0) out[2 * D] = any_bad ? 1ull : 0ull;
 }
 
 // Geometry computed ON THE DEVICE from the min/max (same IEEE operations as host_geometry, so the
@@ -108,12 +64,32 @@ constexpr size_t kMaxEstBuckets = 1100;
 constexpr size_t kAuxEstOffset = 64;                       // estimate buckets, bytes after aux
 constexpr size_t kBuildSlotBytes = kEstOffset + kAuxEstOffset + 8 * kMaxEstBuckets;
 
+// prefix-bucket items travel packed as ONE 64-bit word ((key - prefix*div) << idb | id): possible when
+// the low key part and the point id fit together (bits(div - 1) + bits(n - 1) <= 64)
+__host__ __device__ __forceinline__ int id_bits(uint32_t n)
+{
+    int b = 1;
+    while (b < 32 && ((uint64_t)(n - 1) >> b)) ++b;
+    return b;
+}
+__host__ __device__ __forceinline__ int low_bits(uint64_t div)
+{
+    int b = 0;
+    while (b < 64 && ((div - 1) >> b)) ++b;
+    return b;
+}
+__host__ __device__ __forceinline__ bool bucket_items_pack(uint64_t div, uint32_t n)
+{
+    return low_bits(div) + id_bits(n) <= 64;
+}
+
 __device__ __noinline__ void geometry_products(const uint64_t *cpd, int d, uint32_t n, int allow_bucket,
                                                int want_masks, DevGeom &G);
 
-__global__ void __launch_bounds__(256)
-k_geometry(const unsigned long long *__restrict__ part, uint32_t parts, int d, double eps, uint32_t n,
-           int allow_bucket, int want_masks, DevGeom *__restrict__ g)
+// executed by the whole (last) CTA of k_minmax_geom (256 threads)
+__device__ __forceinline__ void geometry_block(const unsigned long long *__restrict__ part, uint32_t parts, int d,
+                                               double eps, uint32_t n, int allow_bucket, int want_masks,
+                                               DevGeom *__restrict__ g)
 {
     // reduce the per-block partials of k_minmax: min over [0, d), max over [d, 2d), or of [2d];
     // each thread folds whole rows (independent loads in flight), then warp and CTA reductions
@@ -127,7 +103,7 @@ k_geometry(const unsigned long long *__restrict__ part, uint32_t parts, int d, d
 #pragma unroll
         for (int v = 0; v <= 2 * SJ_MAX_DIM; ++v) {
             if (v > 2 * d) break;
-            const unsigned long long x = row[v];
+            const unsigned long long x = __ldcg(row + v);     // written by other CTAs: bypass L1
             acc[v] = v < d ? min(acc[v], x) : max(acc[v], x);
         }
     }
@@ -189,6 +165,72 @@ k_geometry(const unsigned long long *__restrict__ part, uint32_t parts, int d, d
     for (size_t i2 = lane; i2 < sizeof(DevGeom) / 8; i2 += 32) dst[i2] = src[i2];
 }
 
+// a1: exact per-dimension min/max + non-finite flag, then -- in the LAST CTA to finish -- the geometry
+// (geometry_block) and the zeroing of the index's small masks / aux / estimate buckets.  D is read as
+// ONE flat array of n*D doubles, fully coalesced: the grid's thread count is a multiple of D (host),
+// so every element a thread visits has the same dimension t mod D.  Each CTA writes its partial
+// (order-preserving integer images): part[b][0..D) = ord(min), [D..2D) = ord(max), [2D] = non-finite.
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+k_minmax_geom(const double *__restrict__ pts, uint32_t n, unsigned long long *__restrict__ part,
+              unsigned int *__restrict__ done, double eps, int allow_bucket, int want_masks,
+              DevGeom *__restrict__ g, uint32_t *__restrict__ zero_words, uint32_t nzero)
+{
+    const uint64_t total = (uint64_t)n * D;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
+    double mn = INFINITY, mx = -INFINITY;
+    bool bad = false;
+    uint64_t e = t;
+    constexpr int U = 8;                              // independent loads in flight per thread
+    for (; e + (U - 1) * S < total; e += U * S) {
+        double x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = pts[e + u * S];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            bad |= !isfinite(x[u]);
+            mn = fmin(mn, x[u]);
+            mx = fmax(mx, x[u]);
+        }
+    }
+    for (; e < total; e += S) {
+        const double x = pts[e];
+        bad |= !isfinite(x);
+        mn = fmin(mn, x);
+        mx = fmax(mx, x);
+    }
+    const bool any_bad = __syncthreads_or(bad);
+    __shared__ double s_mn[kThreads], s_mx[kThreads];
+    s_mn[threadIdx.x] = mn;
+    s_mx[threadIdx.x] = mx;
+    __syncthreads();
+    unsigned long long *out = part + (uint64_t)blockIdx.x * (2 * D + 1);
+    if (threadIdx.x < D) {
+        const int j = threadIdx.x;
+        const uint32_t base = (uint32_t)(((uint64_t)blockIdx.x * kThreads) % D);
+        double a = INFINITY, b = -INFINITY;
+        for (uint32_t l = (uint32_t)((j + D - (int)base) % D); l < kThreads; l += D) {
+            a = fmin(a, s_mn[l]);
+            b = fmax(b, s_mx[l]);
+        }
+        out[j] = ord_key(a);            // +inf / -inf when the CTA saw no element of dimension j
+        out[D + j] = ord_key(b);
+    }
+    if (threadIdx.x == 0) out[2 * D] = any_bad ? 1ull : 0ull;
+    // last CTA: geometry from all partials
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (uint32_t i = threadIdx.x; i < nzero; i += blockDim.x) zero_words[i] = 0u;
+    geometry_block(part, gridDim.x, D, eps, n, allow_bucket, want_masks, g);
+    if (threadIdx.x == 0) *done = 0u;                 // ready for the next build on this context
+}
+
 // lane 0 of k_geometry: everything that needs only products and sums of the |g_j|
 __device__ __noinline__ void geometry_products(const uint64_t *cpd, int d, uint32_t n, int allow_bucket,
                                                int want_masks, DevGeom &G)
@@ -222,21 +264,11 @@ __device__ __noinline__ void geometry_products(const uint64_t *cpd, int d, uint3
         if (j >= d - G.k) ps *= cpd[j];
     }
     G.use_bucket = allow_bucket && G.k >= 1 && (double)n <= 2.0 * (double)G.P && G.P <= (1ull << 22) &&
-                   G.key_bits <= 62;
+                   G.key_bits <= 62 && bucket_items_pack(G.div, n);
     uint64_t mt = 0;
     for (int j = 0; j < d; ++j) { G.mask_off[j] = mt; mt += cpd[j]; }
     G.mask_off[d] = mt;
     G.masks_on = want_masks && mt <= 32ull * kSmemMaskWords;
-}
-
-// zero bhist[0, P] (P known on the device only)
-__global__ void __launch_bounds__(kThreads)
-k_zero_prefix_hist(uint32_t *__restrict__ h, const DevGeom *__restrict__ g)
-{
-    if (!g->use_bucket) return;
-    const uint64_t P = g->P;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= P; i += (uint64_t)gridDim.x * blockDim.x)
-        h[i] = 0;
 }
 
 // Cell coordinate c_j = 1 + floor(fl(fl(x_j - min_j) / w))  (reading R7), linear id with
@@ -267,9 +299,11 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
     }
     if (use_masks)
         for (uint32_t w2 = threadIdx.x; w2 < mask_words; w2 += blockDim.x) s_mask[w2] = 0;
+    const uint64_t base = (uint64_t)blockIdx.x * kThreads;
+    const uint32_t cnt = (uint32_t)min((uint64_t)kThreads, (uint64_t)n - base);
     __syncthreads();
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
+    const uint64_t i = base + threadIdx.x;
+    if (threadIdx.x < cnt) {
         uint64_t key = 0, prefix = 0;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
@@ -285,8 +319,8 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
             }
         }
         keys[i] = key;
-        ids[i] = (uint32_t)i;
         if (use_hist) atomicAdd(bhist + prefix, 1u);
+        else ids[i] = (uint32_t)i;                  // the LSD sort's values (the bucket path's ids are implicit)
     }
     if (use_masks) {
         __syncthreads();
@@ -423,6 +457,11 @@ struct BuildArgs {
     const double *pts = nullptr;
     uint32_t n = 0;
     unsigned long long *mm = nullptr;
+    unsigned int *done = nullptr;
+    double eps = 0.0;
+    int allow_bucket = 0, want_masks = 0;
+    uint32_t *zero_words = nullptr;
+    uint32_t nzero = 0;
     uint32_t *nonfinite = nullptr;
     uint64_t *keys = nullptr;
     uint32_t *ids = nullptr;
@@ -447,7 +486,8 @@ template <int D>
 void launch_dim(int which, dim3 g, cudaStream_t s, const DevIndex &ix, const BuildArgs &a)
 {
     if (which == 0) {
-        k_minmax<D><<<g, kThreads, 0, s>>>(a.pts, a.n, a.mm);
+        k_minmax_geom<D><<<g, kThreads, 0, s>>>(a.pts, a.n, a.mm, a.done, a.eps, a.allow_bucket, a.want_masks,
+                                                 const_cast<DevGeom *>(a.geom), a.zero_words, a.nzero);
     } else if (which == 1) {
         k_keys<D><<<g, kThreads, 0, s>>>(a.pts, a.n, a.geom, a.keys, a.ids, a.masks, a.bhist);
     } else if (which == 3) {
@@ -783,6 +823,13 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
     static_assert(sizeof(DevGeom) <= 4096, "DevGeom fits its slot");
     CtxGuard cg{acquire_ctx(o.device, 2, 2, kBuildSlotBytes)};   // stream 1: the geometry read-back
     cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : cg.c->streams[0];
+    if (!o.stream) {
+        // NULL = the library stream, ordered after the work already queued on the legacy default
+        // stream (e.g. torch's default stream producing the points), which a non-blocking library
+        // stream would not otherwise wait for
+        SJ_CUDA(cudaEventRecord(cg.c->events[1], cudaStreamLegacy));
+        SJ_CUDA(cudaStreamWaitEvent(s, cg.c->events[1], 0));
+    }
 
     const uint32_t N = (uint32_t)n;
     // phase events (pooled); handed to the index, which turns them into timings on request
@@ -837,43 +884,55 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         // aux: [0] = |G|, [1] = #dense tasks, [2] = #populous cells, [3] = bucket-sort overflow
         uint32_t *aux = reinterpret_cast<uint32_t *>(arena + o_aux);
         const uint64_t hcap = std::max<uint64_t>(4ull * n, 1ull << 16);
-        const size_t s_k = al(8 * n), s_i = al(4 * n), s_h = al(4 * (hcap + 1));
+        const size_t s_k = al(8 * n), s_i = al(4 * n), s_h = al(4 * (hcap + 2));
         // the build's temporaries: the per-device cached scratch buffer (released after the final
-        // stream sync below), else pool memory
+        // stream sync below), else pool memory.  Layout: [bucket histogram | keys | keys_tmp/items |
+        // ids_tmp | flags].  The histogram sits at
+        // offset 0 and every build leaves it zero (the bucket path's finish kernel re-zeroes the cursors
+        // it used), so a reused scratch buffer needs no zeroing pass; `zero` is the known-zero prefix.
+        // (The bucket path leaves cells-per-bucket there; the directory scan consumes and zeroes it.)
         struct BuildScratch {
             int dev;
             char *p = nullptr;
             bool cached = false;
+            size_t zero = 0, leave_zero = 0;
             cudaStream_t s;
             BuildScratch(int d, size_t bytes, cudaStream_t st) : dev(d), s(st)
             {
-                p = static_cast<char *>(scratch_acquire(dev, bytes));
+                p = static_cast<char *>(scratch_acquire(dev, bytes, &zero));
                 cached = p != nullptr;
-                if (!cached) p = static_cast<char *>(dev_alloc(bytes, s));
+                if (!cached) {
+                    p = static_cast<char *>(dev_alloc(bytes, s));
+                    zero = 0;
+                }
             }
             ~BuildScratch()
             {
                 if (cached) {
-                    cudaStreamSynchronize(s);      // (normally already idle: the build ends synced)
-                    scratch_release(dev, p);
+                    if (!leave_zero) cudaStreamSynchronize(s);   // (a completed build ends synced)
+                    scratch_release(dev, p, leave_zero);
                 } else {
                     dev_free(p, s);
                 }
             }
-        } scratch(o.device, 2 * s_k + 2 * s_i + s_h, s);
-        uint64_t *keys = reinterpret_cast<uint64_t *>(scratch.p);
-        uint64_t *keys_tmp = reinterpret_cast<uint64_t *>(scratch.p + s_k);
-        uint32_t *ids_tmp = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k);
-        uint32_t *flags = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k + s_i);
-        uint32_t *bhist = reinterpret_cast<uint32_t *>(scratch.p + 2 * s_k + 2 * s_i);
+        } scratch(o.device, s_h + 2 * s_k + 2 * s_i, s);
+        uint32_t *bhist = reinterpret_cast<uint32_t *>(scratch.p);
+        uint64_t *keys = reinterpret_cast<uint64_t *>(scratch.p + s_h);
+        uint64_t *keys_tmp = reinterpret_cast<uint64_t *>(scratch.p + s_h + s_k);
+        uint32_t *ids_tmp = reinterpret_cast<uint32_t *>(scratch.p + s_h + 2 * s_k);
+        uint32_t *flags = reinterpret_cast<uint32_t *>(scratch.p + s_h + 2 * s_k + s_i);
+        if (scratch.zero < s_h) SJ_CUDA(cudaMemsetAsync(bhist, 0, s_h, s));
         // ---- a1: exact per-dimension min/max + finiteness (one kernel, integer atomics), then the
         // geometry on the device (k_geometry) and the key pass right behind it; the host reads the
         // geometry (one small D2H copy, waited on by an event) while the key pass runs.
-        const uint32_t parts =
-            (uint32_t)std::min<uint64_t>(std::min<uint64_t>((n + kThreads - 1) / kThreads, (uint64_t)nsm * 4), 1024);
-        // min/max partials and the device geometry live in the context's slot memory
+        // grid: a multiple of 3 and 5 CTAs (so the thread count is a multiple of d), <= 1020 partials
+        uint32_t parts = (uint32_t)std::min<uint64_t>((n * d + kThreads * 16 - 1) / (kThreads * 16), 1020u);
+        parts = std::max<uint32_t>(15u, (parts + 14u) / 15u * 15u);
+        parts = std::min<uint32_t>(parts, 1020u);
+        // min/max partials, the device geometry and the last-CTA counter live in the context's slots
         unsigned long long *part = static_cast<unsigned long long *>(cg.c->d_slots);
         DevGeom *dgeom = reinterpret_cast<DevGeom *>(static_cast<char *>(cg.c->d_slots) + kGeomOffset);
+        unsigned int *done = reinterpret_cast<unsigned int *>(static_cast<char *>(cg.c->d_slots) + kGeomOffset + 4096 - 16);
         DevIndex ix{};
         ix.d = d;
         ix.n = N;
@@ -881,11 +940,15 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ba.pts = pts;
         ba.n = N;
         ba.mm = part;
+        ba.done = done;
+        ba.eps = eps;
+        ba.allow_bucket = allow_bucket ? 1 : 0;
+        ba.want_masks = o.build_masks ? 1 : 0;
+        ba.geom = dgeom;
+        ba.zero_words = small_masks;            // small masks, aux and the build's estimate buckets
+        ba.nzero = (uint32_t)((b_mk + b_aux) / 4);
         launch(d, 0, dim3(parts), s, ix, ba);
-        tr.dev("minmax", s);
-        k_geometry<<<1, 256, 0, s>>>(part, parts, d, eps, N, allow_bucket ? 1 : 0, o.build_masks ? 1 : 0, dgeom);
-        SJ_LAUNCHED();
-        tr.dev("geometry", s);
+        tr.dev("minmax + geometry", s);
         // the host's copy of the geometry travels on a side stream, so the key pass does not queue
         // behind the small D2H copy's latency
         DevGeom *hgeom = static_cast<DevGeom *>(cg.c->h_slots);
@@ -897,10 +960,6 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ev.rec(2, s);
 
         tr.mark("minmax + geometry enqueued");
-        SJ_CUDA(cudaMemsetAsync(small_masks, 0, b_mk + 4 * sizeof(uint32_t), s));   // small masks + aux
-        k_zero_prefix_hist<<<(unsigned)std::min<uint64_t>((hcap + kThreads) / kThreads, (uint64_t)nsm * 8), kThreads, 0,
-                             s>>>(bhist, dgeom);
-        SJ_LAUNCHED();
         const dim3 grid((unsigned)((n + kThreads - 1) / kThreads));
 
         // ---- a2: keys (+ small masks, + prefix histogram of the bucket sort)
@@ -982,7 +1041,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         // bucket arrays stay L2-sized; measured slower than LSD at P = 11.4 M) -> prefix buckets +
         // per-bucket sort; otherwise stable LSD radix sort.  (Same rule as k_geometry's.)
         const bool use_bucket = allow_bucket && dp.k >= 1 && (double)n <= 2.0 * (double)dp.P &&
-                                dp.P <= (1ull << 22) && v.key_bits <= 62;
+                                dp.P <= (1ull << 22) && v.key_bits <= 62 && bucket_items_pack(dp.div, N);
         if (use_bucket != (hg.use_bucket != 0) || dp.P != hg.P || dp.k != hg.k)
             fail(SJ_ERR_CUDA, "device and host directory plans disagree (internal error)");
         uint32_t *masks = nullptr;
@@ -1004,28 +1063,48 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         tr.dev("alloc dir", s);
         uint32_t *dir = const_cast<uint32_t *>(idx->dev.dir);
 
-        // ---- a3: sort of (key, id) into (key, id)-ascending order (= stable sort by key, R14)
-        bool in_tmp = false;
         Scratch<uint32_t> dirhist;
+        ix.masks = masks;
+        ix.occ = idx->dev.occ;
+        ix.occ2 = idx->dev.occ2;
+        ix.dir = idx->dev.dir;
         if (use_bucket) {
-            // the bucket sort also numbers each bucket's cells: pcell = cell index within the
-            // bucket, bhist = cells per bucket, whose exclusive scan IS the prefix directory
+            // ---- a3, prefix buckets: scatter by top-k prefix, each bucket sorted by (key, id) (=
+            // the stable order, R14); the sort also numbers each bucket's cells: pcell = cell index
+            // within the bucket, bhist = cells per bucket, whose exclusive scan IS the directory
             bucket_sort_pairs(keys, A, keys_tmp, ids_tmp, N, dp.div, dp.P, bhist, aux + 3, pcell, bhist, s);
-            exclusive_scan_u32(bhist, dir, (uint64_t)dp.P + 1, s);
-            tr.dev("dir scan", s);
+            exclusive_scan_u32_consume(bhist, dir, (uint64_t)dp.P + 1, s);    // (leaves bhist zero)
+            tr.dev("bucket sort + dir scan", s);
             SJ_CUDA(cudaMemcpyAsync(aux, dir + dp.P, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+            ev.rec(4, s);
+            // ---- a4: compaction (cell = directory entry of its prefix + index within the bucket),
+            // B, G, SoA gather, occupancy bits
+            ba.keys = keys;
+            ba.A = A;
+            ba.pcell = pcell;
+            ba.B = B;
+            ba.G = G;
+            ba.X = X;
+            ba.ccoord = ccoord;
+            ba.cmask = cmask;
+            ba.ndense = aux + 2;
+            ba.dirhist = nullptr;
+            ba.bucket_cells = true;
+            ba.dir_inv = 1.0 / (double)dp.div;
+            ba.occ = const_cast<uint32_t *>(ix.occ);
+            launch(d, 2, grid, s, ix, ba);
+            tr.dev("compact", s);
         } else {
+            // ---- a3: stable LSD radix sort of (key, id) (reading R14)
+            bool in_tmp = false;
             radix_sort_pairs(keys, A, keys_tmp, ids_tmp, N, v.key_bits, s, &in_tmp);
-        }
-        const uint64_t *skeys = in_tmp ? keys_tmp : keys;
-        if (in_tmp) SJ_CUDA(cudaMemcpyAsync(A, ids_tmp, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
-        ev.rec(4, s);
-        tr.mark("sort enqueued");
-
-        // ---- a4: cell numbering (LSD path: heads + scan), compaction, SoA gather, directory
-        // histogram (LSD path), occupancy bits.  B and G are sized for the upper bound N cells so no
-        // host round trip is needed here; |G| is read back by the single sync of finish_aux.
-        if (!use_bucket) {
+            const uint64_t *skeys = in_tmp ? keys_tmp : keys;
+            if (in_tmp) SJ_CUDA(cudaMemcpyAsync(A, ids_tmp, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
+            ev.rec(4, s);
+            tr.mark("sort enqueued");
+            // ---- a4: cell numbering (heads + scan), compaction, SoA gather, directory histogram,
+            // occupancy bits.  B and G are sized for the upper bound N cells so no host round trip is
+            // needed here; |G| is read back by the single sync of finish_aux.
             k_heads<<<grid, kThreads, 0, s>>>(skeys, N, flags);
             SJ_LAUNCHED();
             inclusive_scan_u32(flags, pcell, n, s);
@@ -1033,31 +1112,26 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
             dirhist.p = dalloc<uint32_t>((size_t)dp.P + 1, s);
             dirhist.s = s;
             SJ_CUDA(cudaMemsetAsync(dirhist.p, 0, sizeof(uint32_t) * ((size_t)dp.P + 1), s));
+            ba.keys = const_cast<uint64_t *>(skeys);
+            ba.A = A;
+            ba.pcell = pcell;
+            ba.B = B;
+            ba.G = G;
+            ba.X = X;
+            ba.ccoord = ccoord;
+            ba.cmask = cmask;
+            ba.ndense = aux + 2;
+            ba.dirhist = dirhist.p;
+            ba.bucket_cells = false;
+            ba.dir_inv = 1.0 / (double)dp.div;
+            ba.occ = const_cast<uint32_t *>(ix.occ);
+            launch(d, 2, grid, s, ix, ba);
+            tr.dev("compact", s);
         }
-        ix.masks = masks;
-        ix.occ = idx->dev.occ;
-        ix.occ2 = idx->dev.occ2;
-        ix.dir = idx->dev.dir;
-        ba.keys = const_cast<uint64_t *>(skeys);
-        ba.A = A;
-        ba.pcell = pcell;
-        ba.B = B;
-        ba.G = G;
-        ba.X = X;
-        ba.ccoord = ccoord;
-        ba.cmask = cmask;
-        ba.ndense = aux + 2;
-        ba.dirhist = dirhist.p;
-        ba.bucket_cells = use_bucket;
-        ba.dir_inv = 1.0 / (double)dp.div;
-        ba.occ = const_cast<uint32_t *>(ix.occ);
-        tr.dev("pre-compact", s);
-        launch(d, 2, grid, s, ix, ba);
-        tr.dev("compact", s);
         ix.ccoord = ccoord;
         ix.cmask = cmask;
         ev.rec(5, s);
-        tr.mark("compact enqueued");
+        tr.mark("compaction enqueued");
 
         v.n_cells = n;            // provisional upper bound until finish_aux() reads |G|
         v.B = B;
@@ -1077,7 +1151,6 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         idx->dev = ix;
         // LSD path: the directory from its histogram (the bucket path scanned it before compaction)
         if (dirhist.p) exclusive_scan_u32(dirhist.p, dir, (uint64_t)dp.P + 1, s);
-        tr.mark("compaction enqueued");
         // a5 for the default join, speculatively, before the final sync: the provisional index
         // bounds cell ranges by N (B carries a sentinel after the last cell) and chooses the search
         // mode from N; the result is kept only if the mode from |G| is the same
@@ -1097,7 +1170,6 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
             es_spec = estimate_shape(n);
             if (es_spec.nbk > kMaxEstBuckets) fail(SJ_ERR_CUDA, "estimate bucket count out of range (internal error)");
             unsigned long long *dbk = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(aux) + kAuxEstOffset);
-            SJ_CUDA(cudaMemsetAsync(dbk, 0, 8 * es_spec.nbk, s));
             sj_join_opts jo;
             sj_join_opts_default(&jo);
             launch_estimate(px, o.device, jo, 0, n, es_spec, dbk, s);
@@ -1105,6 +1177,8 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         }
         finish_aux(idx, s, aux, dp, nullptr, false, h_aux, h_stage,
                    kAuxEstOffset + (spec ? 8 * es_spec.nbk : 0));     // the build's late host sync
+        scratch.leave_zero = s_h;            // the histogram region is zero again (see BuildScratch)
+        cg.idle = true;                      // s synced by finish_aux, the side stream by the geometry event
         {
             sj_index_view &vv = idx->view;
             const uint64_t nGf = vv.n_cells;

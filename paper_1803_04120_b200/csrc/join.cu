@@ -557,6 +557,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         delete res;
         throw;
     }
+    cg.idle = true;                          // every stream was synchronised above
     stats.total_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
     return res;
 }

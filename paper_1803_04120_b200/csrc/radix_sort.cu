@@ -11,7 +11,7 @@
 //   scatter : each warp ranks its 512 consecutive items in registers (__match_any_sync + warp
 //             private digit counters, no CTA barrier per round), one CTA prefix over the warps,
 //             then every item goes to base[digit][cta] + its stable rank.
-#include "sj_common.cuh"
+#include "scan.cuh"
 
 namespace sj {
 
@@ -111,34 +111,6 @@ constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 4;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *s_warp, uint32_t *total)
-{
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) s_warp[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t w = (lane < (int)(blockDim.x >> 5)) ? s_warp[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
-        }
-        s_warp[lane] = w;  // inclusive prefix of warp totals
-    }
-    __syncthreads();
-    const uint32_t warp_off = warp ? s_warp[warp - 1] : 0;
-    if (total) *total = s_warp[(blockDim.x >> 5) - 1];
-    const uint32_t r = warp_off + x - v;
-    __syncthreads();
-    return r;
-}
-
 __global__ void __launch_bounds__(kScanThreads)
 k_scan_reduce(const uint32_t *__restrict__ in, uint64_t n, uint32_t *__restrict__ block_sums)
 {
@@ -158,7 +130,7 @@ k_scan_reduce(const uint32_t *__restrict__ in, uint64_t n, uint32_t *__restrict_
 template <bool INCLUSIVE>
 __global__ void __launch_bounds__(kScanThreads)
 k_scan_apply(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, uint64_t n,
-             const uint32_t *__restrict__ block_off, uint32_t *__restrict__ out2)
+             const uint32_t *__restrict__ block_off, uint32_t *__restrict__ out2, uint32_t *__restrict__ zero_in)
 {
     __shared__ uint32_t s_warp[32];
     // each thread owns kScanItems consecutive items
@@ -170,6 +142,11 @@ k_scan_apply(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, uint64
         uint64_t i = base + r;
         v[r] = (i < n) ? in[i] : 0;
         acc += v[r];
+    }
+    if (zero_in) {                       // consume: leave the input zero (each thread its own items)
+#pragma unroll
+        for (int r = 0; r < kScanItems; ++r)
+            if (base + r < n) zero_in[base + r] = 0u;
     }
     // this block's offset = sum of the preceding blocks' totals (<= a few thousand: every block
     // reduces them itself, so no separate kernel scans the block sums)
@@ -196,7 +173,7 @@ k_scan_apply(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, uint64
 }
 
 void scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, bool inclusive, cudaStream_t s,
-              uint32_t *out2 = nullptr)
+              uint32_t *out2 = nullptr, uint32_t *zero_in = nullptr)
 {
     if (n == 0) return;
     const uint64_t nb = (n + kScanTile - 1) / kScanTile;
@@ -204,9 +181,9 @@ void scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, bool inclusive, cud
     k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, sums.p);
     SJ_LAUNCHED();
     if (inclusive)
-        k_scan_apply<true><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, sums.p, out2);
+        k_scan_apply<true><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, sums.p, out2, zero_in);
     else
-        k_scan_apply<false><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, sums.p, out2);
+        k_scan_apply<false><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, sums.p, out2, zero_in);
     SJ_LAUNCHED();
 }
 
@@ -215,6 +192,11 @@ void scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, bool inclusive, cud
 void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s)
 {
     scan_u32(in, out, n, false, s);
+}
+
+void exclusive_scan_u32_consume(uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s)
+{
+    scan_u32(in, out, n, false, s, nullptr, in);
 }
 
 void exclusive_scan_u32_dup(const uint32_t *in, uint32_t *out, uint32_t *out2, uint64_t n, cudaStream_t s)
@@ -303,7 +285,7 @@ k_bucket_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ 
     else if ((q + 1) * div <= k) ++q;
     const uint32_t pos = atomicAdd(cursor + q, 1u);
     if (idb) {
-        kout[pos] = ((k - q * div) << idb) | vin[i];
+        kout[pos] = ((k - q * div) << idb) | i;       // ids are the input positions (k_keys writes none)
     } else {
         kout[pos] = k;
         vout[pos] = vin[i];
@@ -525,7 +507,7 @@ void bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint3
     while (lowb < 64 && ((div - 1) >> lowb)) ++lowb;
     while (idb < 32 && ((uint64_t)(n - 1) >> idb)) ++idb;
     if (idb == 0) idb = 1;
-    if (lowb + idb > 64) idb = 0;
+    if (lowb + idb > 64) fail(SJ_ERR_CUDA, "bucket sort needs packed items (internal error)");
     k_bucket_scatter<<<g, 256, 0, s>>>(keys, vals, n, div, inv, hist, keys_tmp, vals_tmp, idb);
     SJ_LAUNCHED();
     tr.dev("scatter", s);

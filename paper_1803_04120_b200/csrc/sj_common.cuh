@@ -236,8 +236,10 @@ void result_cache_trim(int dev);                 // free every cached buffer of 
 void set_result_cache_limit(size_t bytes);
 void scratch_trim(int dev);
 int device_sm_count(int dev);                  // cached multiprocessor count
-void *scratch_acquire(int dev, size_t bytes);   // nullptr if busy (use the pool instead)
-void scratch_release(int dev, void *p);
+// the build's scratch buffer (nullptr if busy: use the pool instead); *zero_prefix = leading bytes known
+// to be zero; the releasing build states how many leading bytes it leaves zero
+void *scratch_acquire(int dev, size_t bytes, size_t *zero_prefix);
+void scratch_release(int dev, void *p, size_t zero_prefix);
 // pooled timing events (cudaEventCreate / elapsed-time queries stay off the critical path)
 cudaEvent_t event_get(int dev);
 void event_put(int dev, cudaEvent_t e);
@@ -247,10 +249,12 @@ void index_finalize_timing(sj_index *idx);
 void release_ctx(DevCtx *c);
 struct CtxGuard {
     DevCtx *c;
+    bool idle = false;           // the owner already synchronised every stream it used
     ~CtxGuard()
     {
         if (!c) return;
-        for (auto s : c->streams) cudaStreamSynchronize(s);
+        if (!idle)
+            for (auto s : c->streams) cudaStreamSynchronize(s);
         release_ctx(c);
     }
 };
@@ -263,10 +267,12 @@ void free_index_impl(sj_index *idx);
 // radix_sort.cu
 void radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp,
                       uint32_t n, int key_bits, cudaStream_t s, bool *result_in_tmp);
+
 void bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp, uint32_t n,
                        uint64_t div, uint64_t P, uint32_t *hist, uint32_t *overflow, uint32_t *local,
                        uint32_t *cellcnt, cudaStream_t s);
 void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s);
+void exclusive_scan_u32_consume(uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s);   // zeroes in
 void exclusive_scan_u32_dup(const uint32_t *in, uint32_t *out, uint32_t *out2, uint64_t n, cudaStream_t s);
 void inclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStream_t s);
 
