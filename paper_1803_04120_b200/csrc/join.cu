@@ -44,17 +44,20 @@ template <int MODE>
 void launch_refine(const DevIndex &ix, const JoinArgs &ja, bool unicomp, uint32_t nqueries, cudaStream_t s)
 {
     if (nqueries == 0) return;
+    // cell scan without occupancy bitmaps: the queued kernel (candidate ranges tested by converged warps)
+    static const bool no_queue = getenv_flag("SJ_NO_QUEUE");
+    const bool queued = ix.search_mode == kSearchCellScan && !ix.occ && !no_queue;
     const uint64_t nthreads64 = (uint64_t)nqueries << ja.lanes_log2;
     if (nthreads64 >= (1ull << 32)) fail(SJ_ERR_ARG, "too many queries x lanes for one launch");
     const uint32_t nthreads = (uint32_t)nthreads64;
     const dim3 grid((nthreads + kRefineThreads - 1) / kRefineThreads);
     const bool occ6 = MODE == kEmit && ix.search_mode == kSearchCellScan && !ix.occ && ix.dir_ntop >= 81;
     switch (ix.d) {
-    case 2: launch_refine_d<2>(MODE, ix, ja, unicomp, occ6, grid, s); break;
-    case 3: launch_refine_d<3>(MODE, ix, ja, unicomp, occ6, grid, s); break;
-    case 4: launch_refine_d<4>(MODE, ix, ja, unicomp, occ6, grid, s); break;
-    case 5: launch_refine_d<5>(MODE, ix, ja, unicomp, occ6, grid, s); break;
-    case 6: launch_refine_d<6>(MODE, ix, ja, unicomp, occ6, grid, s); break;
+    case 2: launch_refine_d<2>(MODE, ix, ja, unicomp, occ6, queued, grid, s); break;
+    case 3: launch_refine_d<3>(MODE, ix, ja, unicomp, occ6, queued, grid, s); break;
+    case 4: launch_refine_d<4>(MODE, ix, ja, unicomp, occ6, queued, grid, s); break;
+    case 5: launch_refine_d<5>(MODE, ix, ja, unicomp, occ6, queued, grid, s); break;
+    case 6: launch_refine_d<6>(MODE, ix, ja, unicomp, occ6, queued, grid, s); break;
     default: fail(SJ_ERR_DIM, "bad d");
     }
     SJ_LAUNCHED();

@@ -789,4 +789,295 @@ k_refine(const DevIndex ix, const JoinArgs ja)
     flush_work(ja, q.probes, q.tests, q.emitted);
 }
 
+// ---------------------------------------------------------------- queued cell scan (many offsets)
+// The cell-scan search without occupancy bitmaps (6-D eps = 8: 243 top offsets per query) spent about
+// half its issue slots in the candidate loop and the low-coordinate adjacency test with 4-5 of 32
+// lanes active (every lane walks its own query's cells; ncu: 9.4 active threads per warp).  Here the
+// search only FINDS the adjacent cells: each lane pushes the point range of every adjacent cell its
+// query must test into a per-warp queue in shared memory, and the warp drains the queue with all 32
+// lanes -- candidate t of the flattened ranges goes to lane t mod 32 (owner range by a binary search
+// over the ranges' prefix sums held in registers), the query's coordinates come from shared memory,
+// and hits are emitted warp-aggregated (ballot/popc, one cursor atomic per warp round).  The set of
+// (query, candidate) tests is exactly the inline path's, so S is unchanged.
+constexpr int kQCap = 192;             // queue entries per warp (1.5 KB)
+constexpr int kQDrainAt = 96;           // drain once this many are queued (one round pushes <= 32 * 3^L)
+constexpr int kQWarps = kRefineThreads / 32;
+
+struct QEntry {
+    uint32_t start;                     // first A-position of the range
+    uint32_t len_lane;                  // length (< 2^24) | pushing lane << 24
+};
+
+template <int D>
+struct WarpQueue {
+    QEntry *e;                          // [kQCap]
+    uint32_t *cnt;                      // entries queued
+    double *qx;                         // [32][D] the lanes' query coordinates
+    uint32_t *qid;                      // [32] the lanes' query ids (original)
+    uint32_t *qem;                      // [32] pairs emitted for each lane's query (count modes)
+};
+
+template <int D>
+struct QueueSmem {
+    QEntry e[kQWarps][kQCap];
+    uint32_t cnt[kQWarps];
+    double qx[kQWarps][32 * D];
+    uint32_t qid[kQWarps][32];
+    uint32_t qem[kQWarps][32];
+};
+
+// Push a candidate range for the calling lane's query; false when the queue is full (the caller
+// then tests the range inline).
+template <int D>
+__device__ __forceinline__ bool q_push(const WarpQueue<D> &w, uint32_t start, uint32_t len)
+{
+    if (len == 0) return true;
+    if (len >= (1u << 24)) return false;
+    const uint32_t slot = atomicAdd(w.cnt, 1u);
+    if (slot >= (uint32_t)kQCap) {
+        atomicSub(w.cnt, 1u);
+        return false;
+    }
+    w.e[slot] = QEntry{start, len | ((uint32_t)(threadIdx.x & 31) << 24)};
+    return true;
+}
+
+// Drain the queue (all 32 lanes, converged): while >= 32 entries are queued, or until empty when
+// `final`.  Entries are taken from the top, 32 at a time.
+template <int D, int MODE, bool BOTH>
+__device__ __forceinline__ void q_drain(const DevIndex &ix, const JoinArgs &ja, const WarpQueue<D> &w, bool final,
+                                     uint32_t &tests, uint32_t &emitted)
+{
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    uint32_t cnt = *(volatile uint32_t *)w.cnt;
+    const uint32_t n = ix.n;
+    while (cnt >= 32u || (final && cnt > 0u)) {
+        const uint32_t nb = min(32u, cnt);
+        QEntry en{0u, 0u};
+        if ((uint32_t)lane < nb) en = w.e[cnt - nb + lane];
+        const uint32_t len = en.len_lane & 0xFFFFFFu;
+        uint32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
+        for (uint32_t t0 = 0; t0 < T; t0 += 32u) {
+            const uint32_t t = t0 + lane;
+            // owner range: the number of ranges whose inclusive end is <= t
+            uint32_t l = 0;
+#pragma unroll
+            for (uint32_t step = 16; step; step >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, incl, l + step - 1);
+                if (v <= t) l += step;
+            }
+            l = min(l, 31u);
+            const uint32_t ex = __shfl_sync(0xffffffffu, incl - len, l);
+            const uint32_t st = __shfl_sync(0xffffffffu, en.start, l);
+            const uint32_t ql = __shfl_sync(0xffffffffu, en.len_lane, l) >> 24;
+            const bool valid = t < T;
+            bool hit = false;
+            uint32_t cid = 0;
+            if (valid) {
+                const uint32_t m = st + (t - ex);
+                const double *qx = w.qx + ql * D;
+                double s;
+                {
+                    const double d0 = __dsub_rn(qx[0], __ldg(ix.X + m));
+                    s = __dmul_rn(d0, d0);
+                }
+#pragma unroll
+                for (int j = 1; j < D; ++j) {
+                    const double dj = __dsub_rn(qx[j], __ldg(ix.X + (uint64_t)j * n + m));
+                    s = __dadd_rn(s, __dmul_rn(dj, dj));
+                }
+                ++tests;
+                hit = s <= ix.eps2;
+                if (MODE != kCountQuery && hit) cid = __ldg(ix.A + m);
+            }
+            const uint32_t pid = w.qid[ql];
+            if constexpr (MODE == kCountQuery) {
+                if (hit) atomicAdd(w.qem + ql, BOTH ? 2u : 1u);
+            } else {
+                uint32_t dummy = 0;
+                emit<MODE, BOTH>(ja, hit, pid, cid, dummy);
+                emitted += dummy;
+            }
+        }
+        cnt -= nb;
+        __syncwarp();
+        if (lane == 0) *w.cnt = cnt;
+        __syncwarp();
+    }
+}
+
+template <int D, bool UNICOMP>
+__device__ __forceinline__ bool low_cell_adjacent_odd(const DevIndex &ix, uint32_t odd, int64_t dlt, int jtop, int L)
+{
+    int jlow = -1;
+#pragma unroll
+    for (int i = D - 2; i >= 0; --i) {
+        if (i >= L) continue;
+        const int64_t R = ix.lowR[i], st = (int64_t)ix.strides[i];
+        if (dlt > R) { dlt -= st; if (jlow < 0) jlow = i; }
+        else if (dlt < -R) { dlt += st; if (jlow < 0) jlow = i; }
+    }
+    if (dlt != 0) return false;
+    const int j = jtop >= 0 ? jtop : jlow;
+    return !(UNICOMP && !((odd >> j) & 1u));
+}
+
+// kSearchCellScan without the bitmap filter, queued.  Every lane of the warp runs this (lanes without
+// a query have `bad` = all ones: no live offsets) so the drains see a converged warp.  A lane whose
+// push finds the queue full stops its cell walk there and resumes it after the warp drained, so no
+// range is ever tested inline (the query's coordinates live only in the queue's shared memory).
+// (Dealing the warp's live (query, offset) pairs out to all lanes instead of iterating the union of
+// the lanes' live offsets measured slower: 11.5 vs 8.6 ms on 6-D eps = 8.)
+template <int D, int MODE, bool UNICOMP>
+__device__ __forceinline__ void search_cell_scan_q(const DevIndex &ix, const JoinArgs &ja, QueryState<D> &q,
+                                                   bool active, uint32_t h, uint64_t key, uint32_t bad,
+                                                   const TopTable &tt, const WarpQueue<D> &w)
+{
+    const int L = D - ix.dir_k;
+    uint64_t ph = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) ph += q.c[j] * ix.pstride[j];
+    const int64_t Rl = ix.lowR[L];
+    constexpr int kChunk = 27;
+    const uint32_t ntop = ix.dir_ntop;
+    const uint32_t step = q.G * kChunk;
+#pragma unroll 1
+    for (uint32_t t0 = 0; t0 < ntop; t0 += step) {
+        uint32_t live = 0;
+        if (active) {
+#pragma unroll
+            for (int u = 0; u < kChunk; ++u) {
+                const uint32_t t = t0 + q.sub + (uint32_t)u * q.G;
+                if (t < ntop && !(tt.bits[t] & bad)) live |= 1u << u;
+            }
+        }
+        uint32_t any = __reduce_or_sync(0xffffffffu, live);
+#pragma unroll 1
+        while (any) {
+            const int u = __ffs(any) - 1;
+            any &= any - 1u;
+            bool pending = (live >> u) & 1u;
+            uint32_t hh = 0, hi = 0;
+            uint64_t kal = 0;
+            int jtop = -1;
+            if (pending) {
+                const uint32_t t = t0 + q.sub + (uint32_t)u * q.G;
+                const uint32_t bits = tt.bits[t];
+                jtop = (bits >> 16) ? (__ffs(bits >> 16) - 1) : -1;
+                const uint64_t p = ph + (uint64_t)tt.dp[t];
+                ++q.probes;
+                hh = __ldg(ix.dir + p);
+                hi = __ldg(ix.dir + p + 1);
+                kal = key + (uint64_t)tt.dk[t];
+            }
+#pragma unroll 1
+            while (true) {
+                if (pending) {
+#pragma unroll 1
+                    for (; hh < hi; ++hh) {
+                        if (hh == h) continue;                   // home cell handled separately
+                        const int64_t dlt = (int64_t)(__ldg(ix.B + hh) - kal);
+                        if (dlt > Rl || dlt < -Rl) continue;     // outside the +-1 box
+                        if (!low_cell_adjacent_odd<D, UNICOMP>(ix, q.odd, dlt, jtop, L)) continue;
+                        const uint32_t a = __ldg(ix.G + hh), b = __ldg(ix.G + hh + 1);
+                        if (!q_push<D>(w, a, b - a)) break;      // queue full: resume at hh
+                    }
+                    pending = hh < hi;
+                }
+                const bool again = __any_sync(0xffffffffu, pending);
+                if (again || *(volatile uint32_t *)w.cnt >= (uint32_t)kQDrainAt)
+                    q_drain<D, MODE, UNICOMP>(ix, ja, w, false, q.tests, q.emitted);
+                if (!again) break;
+            }
+        }
+    }
+    q_drain<D, MODE, UNICOMP>(ix, ja, w, true, q.tests, q.emitted);
+}
+
+// The refine for kSearchCellScan indexes without occupancy bitmaps (launch_refine picks it), queued.
+template <int D, int MODE, bool UNICOMP, int MINB = kRefineMinBlocks>
+__global__ void __launch_bounds__(kRefineThreads, MINB)
+k_refine_q(const DevIndex ix, const JoinArgs ja)
+{
+    __shared__ TopTable tt;
+    __shared__ QueueSmem<D> qs;
+    build_top_table<D>(ix, tt);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) qs.cnt[warp] = 0;
+    __syncthreads();
+    WarpQueue<D> w{qs.e[warp], qs.cnt + warp, qs.qx[warp], qs.qid[warp], qs.qem[warp]};
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t qi = t >> ja.lanes_log2;            // G lanes split a query's top offsets
+    QueryState<D> q;
+    q.valid = true;
+    q.G = 1u << ja.lanes_log2;
+    q.sub = t & (q.G - 1u);
+    q.emitted = q.probes = q.tests = 0;
+    uint32_t k;
+    bool active;
+    if constexpr (MODE == kCountQuery) {
+        k = ja.q0 + (qi >> 5) * (32u * ja.step) + (qi & 31u);
+        active = qi < ja.nsamples && k < ja.q1;
+    } else {
+        k = ja.q0 + qi;
+        active = k < ja.q1;
+    }
+    uint32_t h = 0, cs = 0, ce = 0;
+    if (active) {
+        h = __ldg(ix.pcell + k);
+        cs = __ldg(ix.G + h);
+        ce = __ldg(ix.G + h + 1);
+        if (MODE == kEmit && ja.dense_T && ce - cs >= ja.dense_T) active = false;
+    }
+    uint64_t key = 0;
+    uint32_t bad = 0xFFFFFFFFu;
+    if (active) {
+        q.k = k;
+        q.pid = __ldg(ix.A + k);
+#pragma unroll
+        for (int j = 0; j < D; ++j) q.x[j] = __ldg(ix.X + (uint64_t)j * ix.n + k);
+        key = __ldg(ix.B + h);
+        key_to_coords<D>(ix, key, q.c);
+        q.odd = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) q.odd |= (uint32_t)(q.c[j] & 1ull) << j;
+#pragma unroll
+        for (int j = 0; j < D; ++j) w.qx[lane * D + j] = q.x[j];
+        w.qid[lane] = q.pid;
+    } else {
+        q.pid = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) { q.x[j] = 0.0; q.c[j] = 0; }
+        q.odd = 0;
+    }
+    w.qem[lane] = 0;
+    __syncwarp();
+    if (active && q.sub == 0) {
+        // home cell: (p,p) once; unicomp: q after p in A-order, both orientations (R10); full: all others.
+        // (The queue is empty here and a lane pushes <= 2 ranges; ranges of >= 2^24 points -- only with
+        // dense_cells = 0 -- go in pieces.)
+        if (ja.include_self) emit_self<MODE>(ja, q.k, q.pid, q.emitted);
+        for (uint32_t a = k + 1; a < ce; a += (1u << 24) - 1u) q_push<D>(w, a, min(ce - a, (1u << 24) - 1u));
+        if (!UNICOMP)
+            for (uint32_t a = cs; a < k; a += (1u << 24) - 1u) q_push<D>(w, a, min(k - a, (1u << 24) - 1u));
+    }
+    if (active) bad = bad_moves<D, UNICOMP>(ix, ja, q, h);
+    search_cell_scan_q<D, MODE, UNICOMP>(ix, ja, q, active, h, key, bad, tt, w);
+    if constexpr (MODE == kCountQuery) {
+        __syncwarp();
+        q.emitted += w.qem[lane];                    // hits of the ranges this lane queued
+        uint32_t e = q.emitted;
+        for (uint32_t o = 1; o < q.G; o <<= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        if (active && q.sub == 0) atomicAdd(ja.qbucket + qi / ja.group, (unsigned long long)e);
+    }
+    flush_work(ja, q.probes, q.tests, q.emitted);
+}
+
 }  // namespace sj

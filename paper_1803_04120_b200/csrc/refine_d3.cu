@@ -4,12 +4,17 @@
 namespace sj {
 
 template <>
-void launch_refine_d<3>(int mode, const DevIndex &ix, const JoinArgs &ja, bool unicomp, bool occ6, dim3 grid,
-                        cudaStream_t s)
+void launch_refine_d<3>(int mode, const DevIndex &ix, const JoinArgs &ja, bool unicomp, bool occ6, bool queued,
+                        dim3 grid, cudaStream_t s)
 {
     const dim3 block(kRefineThreads);
 #define SJ_MODE_CASE(M)                                                                          \
     case M:                                                                                      \
+        if (queued) {                                                                            \
+            if (unicomp) k_refine_q<3, M, true><<<grid, block, 0, s>>>(ix, ja);                  \
+            else k_refine_q<3, M, false><<<grid, block, 0, s>>>(ix, ja);                         \
+            break;                                                                               \
+        }                                                                                        \
         if constexpr (M == kEmit) {                                                              \
             if (occ6) {                                                                          \
                 if (unicomp) k_refine<3, M, true, 6><<<grid, block, 0, s>>>(ix, ja);             \
