@@ -264,6 +264,65 @@ int device_sm_count(int dev)
     return nsm;
 }
 
+// L2 set-aside for persisting accesses (per device, once): the build marks its input points as
+// persisting while its three passes over them run (min/max, keys, the random row gather), then
+// demotes them (l2_persist_end).  The set-aside is usable by normal accesses while no persisting
+// lines occupy it.  SJ_L2_PERSIST=0 turns this off.  Returns the window size usable (0 = off).
+size_t l2_persist_limit(int dev)
+{
+    static std::mutex mu;
+    static std::map<int, size_t> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    size_t lim = 0;
+    const char *e = std::getenv("SJ_L2_PERSIST");
+    const bool on = e && *e && *e != '0';        // off by default: measured slower (below)
+    int maxp = 0, maxw = 0;
+    if (on && cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev) == cudaSuccess && maxp > 0 &&
+        maxw > 0) {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        cudaSetDevice(dev);
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) == cudaSuccess)
+            lim = std::min<size_t>((size_t)maxp, (size_t)maxw);
+        if (cur >= 0) cudaSetDevice(cur);
+    }
+    cudaGetLastError();
+    cache[dev] = lim;
+    return lim;
+}
+
+void l2_persist_begin(int dev, cudaStream_t s, const void *base, size_t bytes)
+{
+    const size_t lim = l2_persist_limit(dev);
+    if (!lim || !bytes) return;
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.base_ptr = const_cast<void *>(base);
+    a.accessPolicyWindow.num_bytes = std::min(bytes, lim);
+    a.accessPolicyWindow.hitRatio = std::min(1.0f, (float)((double)lim / (double)a.accessPolicyWindow.num_bytes));
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a) != cudaSuccess) cudaGetLastError();
+}
+
+// stop marking (kernels launched on s after this call) ...
+void l2_persist_stop(int dev, cudaStream_t s)
+{
+    if (!l2_persist_limit(dev)) return;
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.num_bytes = 0;
+    if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a) != cudaSuccess) cudaGetLastError();
+}
+
+// ... and, once those kernels have completed (after a sync), demote the persisting lines
+void l2_persist_end(int dev)
+{
+    if (!l2_persist_limit(dev)) return;
+    if (cudaCtxResetPersistingL2Cache() != cudaSuccess) cudaGetLastError();
+}
+
 void *scratch_acquire(int dev, size_t bytes, size_t *zero_prefix)
 {
     *zero_prefix = 0;
@@ -323,6 +382,9 @@ void set_max_dyn_smem(const void *func, int bytes)
     auto &b = done[{func, dev}];
     if (b >= bytes) return;
     SJ_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    // the largest shared-memory carve-out: the occupancy the launch bounds ask for needs it (the
+    // default configuration left k_refine_dense at 2 CTAs per SM)
+    SJ_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     b = bytes;
 }
 

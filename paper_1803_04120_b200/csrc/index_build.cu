@@ -15,6 +15,7 @@
 //   k_compact_gather                : B, G starts, SoA coordinates X[j][k] = D[A[k]][j] (a4)
 //   k_dir_hist + exclusive scan     : prefix directory bounding every B search (a4)
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -56,6 +57,20 @@ __device__ __forceinline__ double ord_to_double(unsigned long long k)
     return __longlong_as_double((long long)u);
 }
 
+// directory size cap: P_k <= max(mult * N, 2^16) entries (SJ_DIR_CAP overrides mult)
+static uint32_t dir_cap_mult()
+{
+    static const uint32_t m = [] {
+        const char *e = std::getenv("SJ_DIR_CAP");
+        const long v = e ? std::strtol(e, nullptr, 10) : 0;
+        return (uint32_t)(v >= 1 && v <= 64 ? v : 4);
+    }();
+    return m;
+}
+
+// the full directory (k = d) is taken when it has at most kFullDirMult entries per point
+constexpr uint32_t kFullDirMult = 8;
+
 constexpr int kSmemMaskWords = 2048;   // 64 K bits, 8 KB of shared memory
 // context slot layout of the build: min/max partials (<= 4 * SMs blocks), then the DevGeom
 constexpr size_t kGeomOffset = 4 * 256 * (2 * SJ_MAX_DIM + 1) * sizeof(unsigned long long);
@@ -84,12 +99,12 @@ __host__ __device__ __forceinline__ bool bucket_items_pack(uint64_t div, uint32_
 }
 
 __device__ __noinline__ void geometry_products(const uint64_t *cpd, int d, uint32_t n, int allow_bucket,
-                                               int want_masks, DevGeom &G);
+                                               int want_masks, uint32_t cap_mult, DevGeom &G);
 
 // executed by the whole (last) CTA of k_minmax_geom (256 threads)
 __device__ __forceinline__ void geometry_block(const unsigned long long *__restrict__ part, uint32_t parts, int d,
                                                double eps, uint32_t n, int allow_bucket, int want_masks,
-                                               DevGeom *__restrict__ g)
+                                               uint32_t cap_mult, DevGeom *__restrict__ g)
 {
     // reduce the per-block partials of k_minmax: min over [0, d), max over [d, 2d), or of [2d];
     // each thread folds whole rows (independent loads in flight), then warp and CTA reductions
@@ -157,7 +172,7 @@ __device__ __forceinline__ void geometry_block(const unsigned long long *__restr
         G.w = w;
         if (bad) G.status = 1;
         else if (any_tbad) G.status = 2;
-        else geometry_products(cpd, d, n, allow_bucket, want_masks, G);
+        else geometry_products(cpd, d, n, allow_bucket, want_masks, cap_mult, G);
     }
     __syncwarp();
     const uint64_t *src = reinterpret_cast<const uint64_t *>(&G);
@@ -173,46 +188,73 @@ __device__ __forceinline__ void geometry_block(const unsigned long long *__restr
 template <int D>
 __global__ void __launch_bounds__(kThreads)
 k_minmax_geom(const double *__restrict__ pts, uint32_t n, unsigned long long *__restrict__ part,
-              unsigned int *__restrict__ done, double eps, int allow_bucket, int want_masks,
+              unsigned int *__restrict__ done, double eps, int allow_bucket, int want_masks, uint32_t cap_mult,
               DevGeom *__restrict__ g, uint32_t *__restrict__ zero_words, uint32_t nzero)
 {
     const uint64_t total = (uint64_t)n * D;
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
-    double mn = INFINITY, mx = -INFINITY;
+    // 16-byte loads: thread t reads the element pairs v = t, t+S, ... (elements 2v, 2v+1, always of
+    // dimensions 2t mod D and (2t+1) mod D: 2S is a multiple of D).  Every round issues U loads
+    // together (predicated, the out-of-range ones repeat the first), so a thread waits for
+    // ceil(pairs / (U*S)) memory latencies -- 3 at 2 M x 6-D -- instead of one per tail element.
+    // (the odd last element of an odd total belongs to dimension D-1: CTA 0 folds it in below)
+    __shared__ double s_mn[2 * kThreads], s_mx[2 * kThreads];
     bool bad = false;
-    uint64_t e = t;
-    constexpr int U = 8;                              // independent loads in flight per thread
-    for (; e + (U - 1) * S < total; e += U * S) {
-        double x[U];
+    const bool vec = (reinterpret_cast<uintptr_t>(pts) & 15u) == 0;
+    if (vec) {
+        const double2 *p2 = reinterpret_cast<const double2 *>(pts);
+        const uint64_t T2 = total >> 1;
+        double mna = INFINITY, mxa = -INFINITY, mnb = INFINITY, mxb = -INFINITY;
+        constexpr int U = 8;
+#pragma unroll 1
+        for (uint64_t v0 = t; v0 < T2; v0 += U * S) {
+            double2 x[U];
+            x[0] = p2[v0];
 #pragma unroll
-        for (int u = 0; u < U; ++u) x[u] = pts[e + u * S];
+            for (int u = 1; u < U; ++u) x[u] = v0 + u * S < T2 ? p2[v0 + u * S] : x[0];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            bad |= !isfinite(x[u]);
-            mn = fmin(mn, x[u]);
-            mx = fmax(mx, x[u]);
+            for (int u = 0; u < U; ++u) {
+                bad |= !isfinite(x[u].x) || !isfinite(x[u].y);
+                mna = fmin(mna, x[u].x);
+                mxa = fmax(mxa, x[u].x);
+                mnb = fmin(mnb, x[u].y);
+                mxb = fmax(mxb, x[u].y);
+            }
         }
+        s_mn[2 * threadIdx.x] = mna;
+        s_mx[2 * threadIdx.x] = mxa;
+        s_mn[2 * threadIdx.x + 1] = mnb;
+        s_mx[2 * threadIdx.x + 1] = mxb;
+    } else {
+        double mn = INFINITY, mx = -INFINITY;
+#pragma unroll 1
+        for (uint64_t e = t; e < total; e += S) {
+            const double x = pts[e];
+            bad |= !isfinite(x);
+            mn = fmin(mn, x);
+            mx = fmax(mx, x);
+        }
+        s_mn[threadIdx.x] = mn;
+        s_mx[threadIdx.x] = mx;
     }
-    for (; e < total; e += S) {
-        const double x = pts[e];
-        bad |= !isfinite(x);
-        mn = fmin(mn, x);
-        mx = fmax(mx, x);
-    }
+    if (vec && (total & 1ull) && blockIdx.x == 0 && threadIdx.x == 0) bad |= !isfinite(pts[total - 1]);
     const bool any_bad = __syncthreads_or(bad);
-    __shared__ double s_mn[kThreads], s_mx[kThreads];
-    s_mn[threadIdx.x] = mn;
-    s_mx[threadIdx.x] = mx;
-    __syncthreads();
     unsigned long long *out = part + (uint64_t)blockIdx.x * (2 * D + 1);
     if (threadIdx.x < D) {
         const int j = threadIdx.x;
-        const uint32_t base = (uint32_t)(((uint64_t)blockIdx.x * kThreads) % D);
+        // the slots cover elements base .. base + L - 1 of the flat array (mod D: their dimensions)
+        const uint32_t L = vec ? 2 * kThreads : kThreads;
+        const uint32_t base = (uint32_t)(((uint64_t)blockIdx.x * L) % D);
         double a = INFINITY, b = -INFINITY;
-        for (uint32_t l = (uint32_t)((j + D - (int)base) % D); l < kThreads; l += D) {
+        for (uint32_t l = (uint32_t)((j + D - (int)base) % D); l < L; l += D) {
             a = fmin(a, s_mn[l]);
             b = fmax(b, s_mx[l]);
+        }
+        if (vec && (total & 1ull) && blockIdx.x == 0 && j == D - 1) {
+            const double x = pts[total - 1];
+            a = fmin(a, x);
+            b = fmax(b, x);
         }
         out[j] = ord_key(a);            // +inf / -inf when the CTA saw no element of dimension j
         out[D + j] = ord_key(b);
@@ -227,13 +269,13 @@ k_minmax_geom(const double *__restrict__ pts, uint32_t n, unsigned long long *__
     if (!s_last) return;
     __threadfence();
     for (uint32_t i = threadIdx.x; i < nzero; i += blockDim.x) zero_words[i] = 0u;
-    geometry_block(part, gridDim.x, D, eps, n, allow_bucket, want_masks, g);
+    geometry_block(part, gridDim.x, D, eps, n, allow_bucket, want_masks, cap_mult, g);
     if (threadIdx.x == 0) *done = 0u;                 // ready for the next build on this context
 }
 
 // lane 0 of k_geometry: everything that needs only products and sums of the |g_j|
 __device__ __noinline__ void geometry_products(const uint64_t *cpd, int d, uint32_t n, int allow_bucket,
-                                               int want_masks, DevGeom &G)
+                                               int want_masks, uint32_t cap_mult, DevGeom &G)
 {
     unsigned __int128 prod = 1;
     for (int j = 0; j < d; ++j) {
@@ -246,14 +288,20 @@ __device__ __noinline__ void geometry_products(const uint64_t *cpd, int d, uint3
     const unsigned __int128 maxkey = prod - 1;
     const uint64_t hi = (uint64_t)(maxkey >> 64), lo = (uint64_t)maxkey;
     G.key_bits = hi ? 128 - __clzll((long long)hi) : (lo ? 64 - __clzll((long long)lo) : 0);
-    // directory plan (plan_dir): largest k with prod_{top k} |g_j| <= max(4N, 2^16)
-    const uint64_t cap = max((uint64_t)4 * n, (uint64_t)1 << 16);
+    // directory plan (plan_dir): the full directory (k = d) when prod_j |g_j| <= kFullDirMult * N,
+    // else the largest k with prod_{top k} |g_j| <= max(4N, 2^16)
+    const uint64_t cap = max((uint64_t)cap_mult * n, (uint64_t)1 << 16);
     unsigned __int128 P = 1;
-    for (int kk = 1; kk <= d; ++kk) {
-        const unsigned __int128 Q = P * cpd[d - kk];
-        if (Q > cap) break;
-        P = Q;
-        G.k = kk;
+    if (prod <= (unsigned __int128)kFullDirMult * n) {
+        P = prod;
+        G.k = d;
+    } else {
+        for (int kk = 1; kk <= d; ++kk) {
+            const unsigned __int128 Q = P * cpd[d - kk];
+            if (Q > cap) break;
+            P = Q;
+            G.k = kk;
+        }
     }
     G.P = (uint64_t)P;
     G.div = 1;
@@ -305,9 +353,26 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
     const uint64_t i = base + threadIdx.x;
     if (threadIdx.x < cnt) {
         uint64_t key = 0, prefix = 0;
+        double xr[D];
+        bool loaded = false;
+        if constexpr (D % 2 == 0) {
+            if ((reinterpret_cast<uintptr_t>(pts) & 15u) == 0) {   // 16-B aligned rows: vector loads
+#pragma unroll
+                for (int j = 0; j < D; j += 2) {
+                    const double2 v = *reinterpret_cast<const double2 *>(pts + i * D + j);
+                    xr[j] = v.x;
+                    xr[j + 1] = v.y;
+                }
+                loaded = true;
+            }
+        }
+        if (!loaded) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) xr[j] = pts[i * D + j];
+        }
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            const double x = pts[i * D + j];
+            const double x = xr[j];
             const double t = floor(__ddiv_rn(__dsub_rn(x, s_min[j]), w));
             const uint64_t c = 1ull + (uint64_t)t;
             key += c * s_str[j];
@@ -487,7 +552,7 @@ void launch_dim(int which, dim3 g, cudaStream_t s, const DevIndex &ix, const Bui
 {
     if (which == 0) {
         k_minmax_geom<D><<<g, kThreads, 0, s>>>(a.pts, a.n, a.mm, a.done, a.eps, a.allow_bucket, a.want_masks,
-                                                 const_cast<DevGeom *>(a.geom), a.zero_words, a.nzero);
+                                                 dir_cap_mult(), const_cast<DevGeom *>(a.geom), a.zero_words, a.nzero);
     } else if (which == 1) {
         k_keys<D><<<g, kThreads, 0, s>>>(a.pts, a.n, a.geom, a.keys, a.ids, a.masks, a.bhist);
     } else if (which == 3) {
@@ -576,13 +641,22 @@ DirPlan plan_dir(const sj_index_view &v)
     DirPlan dp;
     const int d = v.d;
     const uint64_t n = v.n;
-    const unsigned __int128 cap = std::max<uint64_t>(4ull * n, 1ull << 16);
+    const unsigned __int128 cap = std::max<uint64_t>((uint64_t)dir_cap_mult() * n, 1ull << 16);
     unsigned __int128 P = 1;
-    for (int kk = 1; kk <= d; ++kk) {
-        const unsigned __int128 Q = P * v.cpd[d - kk];
-        if (Q > cap) break;
-        P = Q;
-        dp.k = kk;
+    unsigned __int128 prod = 1;
+    for (int j = 0; j < d; ++j) prod *= v.cpd[j];
+    if (prod <= (unsigned __int128)kFullDirMult * n) {
+        // the full directory: every row of three cells is ONE O(1) lookup (dense-rows mode; 6-D
+        // eps = 8: 15^6 = 11.4 M entries, join 8.6 -> 4.1 ms against the k = 5 cell scan)
+        P = prod;
+        dp.k = d;
+    } else {
+        for (int kk = 1; kk <= d; ++kk) {
+            const unsigned __int128 Q = P * v.cpd[d - kk];
+            if (Q > cap) break;
+            P = Q;
+            dp.k = kk;
+        }
     }
     dp.P = (uint64_t)P;
     for (int j = 0; j < d - dp.k; ++j) dp.div *= v.cpd[j];
@@ -848,6 +922,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
     auto own = [&](void *p) { idx->bufs[idx->nbufs++] = p; return p; };
     uint32_t h_aux[4] = {0, 0, 0, 0};
     const int nsm = device_sm_count(o.device);
+    bool l2p = false;              // the input is marked L2-persisting on s (see below)
     try {
         // ---- inputs on device
         const double *pts = points;
@@ -883,7 +958,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         uint32_t *small_masks = reinterpret_cast<uint32_t *>(arena + o_mk);
         // aux: [0] = |G|, [1] = #dense tasks, [2] = #populous cells, [3] = bucket-sort overflow
         uint32_t *aux = reinterpret_cast<uint32_t *>(arena + o_aux);
-        const uint64_t hcap = std::max<uint64_t>(4ull * n, 1ull << 16);
+        const uint64_t hcap = std::max<uint64_t>((uint64_t)std::max(dir_cap_mult(), kFullDirMult) * n, 1ull << 16);
         const size_t s_k = al(8 * n), s_i = al(4 * n), s_h = al(4 * (hcap + 2));
         // the build's temporaries: the per-device cached scratch buffer (released after the final
         // stream sync below), else pool memory.  Layout: [bucket histogram | keys | keys_tmp/items |
@@ -947,6 +1022,11 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ba.geom = dgeom;
         ba.zero_words = small_masks;            // small masks, aux and the build's estimate buckets
         ba.nzero = (uint32_t)((b_mk + b_aux) / 4);
+        // the input is read three times (min/max, keys, the gather's random rows): keep it in L2 as
+        // persisting lines until the gather is enqueued (library stream only: a caller's stream keeps
+        // its own attributes)
+        l2p = !o.stream;
+        if (l2p) l2_persist_begin(o.device, s, pts, sizeof(double) * n * d);
         launch(d, 0, dim3(parts), s, ix, ba);
         tr.dev("minmax + geometry", s);
         // the host's copy of the geometry travels on a side stream, so the key pass does not queue
@@ -1128,6 +1208,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
             launch(d, 2, grid, s, ix, ba);
             tr.dev("compact", s);
         }
+        if (l2p) l2_persist_stop(o.device, s);
         ix.ccoord = ccoord;
         ix.cmask = cmask;
         ev.rec(5, s);
@@ -1177,6 +1258,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         }
         finish_aux(idx, s, aux, dp, nullptr, false, h_aux, h_stage,
                    kAuxEstOffset + (spec ? 8 * es_spec.nbk : 0));     // the build's late host sync
+        if (l2p) l2_persist_end(o.device);   // s is synced: demote the input's persisting lines
         scratch.leave_zero = s_h;            // the histogram region is zero again (see BuildScratch)
         cg.idle = true;                      // s synced by finish_aux, the side stream by the geometry event
         {
@@ -1206,6 +1288,10 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         }
     } catch (...) {
         cudaStreamSynchronize(s);
+        if (l2p) {
+            l2_persist_stop(o.device, s);
+            l2_persist_end(o.device);
+        }
         free_index_impl(idx);
         throw;
     }

@@ -300,17 +300,21 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     const EstimateShape es = spec ? idx->spec_shape : estimate_shape(nq);
     const uint64_t nbk = es.nbk;
     const size_t kSlotsBytes = sizeof(Slot) * 64;
-    const size_t slot_need = kWorkBytes + kSlotsBytes + 8 * (size_t)(nbk + 1);
+    // per stream ONE block [work counters | 64 batch slots], mirrored in pinned memory: each stream
+    // zeroes its own block before its first batch and copies it back after its last one, so no
+    // stream waits for another (no event hops on the GPU between the batches and the read-back)
+    const size_t kBlock = kWorkBytes + kSlotsBytes;
+    const size_t slot_need = kBlock * (size_t)S + 8 * (size_t)(nbk + 1);
     CtxGuard cg{acquire_ctx(idx->device, S, S + 2, slot_need)};
     DevCtx &cx = *cg.c;
     cudaStream_t s0 = cx.streams[0];
     char *dbase = static_cast<char *>(cx.d_slots), *hbase = static_cast<char *>(cx.h_slots);
-    unsigned long long *work = reinterpret_cast<unsigned long long *>(dbase);
-    unsigned long long *hwork = reinterpret_cast<unsigned long long *>(hbase);
-    Slot *dslots = reinterpret_cast<Slot *>(dbase + kWorkBytes);
-    Slot *hslots = reinterpret_cast<Slot *>(hbase + kWorkBytes);
-    unsigned long long *dbk = reinterpret_cast<unsigned long long *>(dbase + kWorkBytes + kSlotsBytes);
-    unsigned long long *hbk = reinterpret_cast<unsigned long long *>(hbase + kWorkBytes + kSlotsBytes);
+    auto dwork = [&](int si) { return reinterpret_cast<unsigned long long *>(dbase + kBlock * si); };
+    auto hwork = [&](int si) { return reinterpret_cast<const unsigned long long *>(hbase + kBlock * si); };
+    auto dslot = [&](int si, size_t j) { return reinterpret_cast<Slot *>(dbase + kBlock * si + kWorkBytes) + j; };
+    auto hslot = [&](int si, size_t j) { return reinterpret_cast<Slot *>(hbase + kBlock * si + kWorkBytes) + j; };
+    unsigned long long *dbk = reinterpret_cast<unsigned long long *>(dbase + kBlock * S);
+    unsigned long long *hbk = reinterpret_cast<unsigned long long *>(hbase + kBlock * S);
     tr.mark("acquire ctx");
     sj_result *res = new sj_result();
     res->device = idx->device;
@@ -319,8 +323,8 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     // self pairs of a batch [a, b): written at fixed slots, counted on the host (see JoinArgs::nself)
     auto nself_of = [&](uint64_t a, uint64_t b) -> uint64_t { return o.include_self ? b - a : 0; };
     try {
-        // work counters, the 64 batch slots and the planning buckets are contiguous: one memset
-        SJ_CUDA(cudaMemsetAsync(work, 0, kWorkBytes + kSlotsBytes + 8 * nbk, s0));
+        for (int i = 0; i < S; ++i) SJ_CUDA(cudaMemsetAsync(dwork(i), 0, kBlock, cx.streams[i]));
+        if (!spec && es.ns) SJ_CUDA(cudaMemsetAsync(dbk, 0, 8 * nbk, s0));
         // ---- a5: estimate on a strided sample (count-only refine), summed per planning bucket
         // (an index built for the default join already carries it: no launch, no round trip)
         if (spec) {
@@ -355,12 +359,13 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         bool work_read = false;
         uint32_t launches = 0;
         // every batch run records a (start, end) event pair; timings are computed on request
-        auto run_batch = [&](uint64_t a, uint64_t b, uint64_t *buf, uint64_t cap, Slot *dslot, cudaStream_t s,
+        auto run_batch = [&](uint64_t a, uint64_t b, uint64_t *buf, uint64_t cap, Slot *dslot, int si,
                              bool clear_slot) {
+            cudaStream_t s = cx.streams[si];
             cudaEvent_t e0 = event_get(idx->device), e1 = event_get(idx->device);
             res->runs.emplace_back(e0, e1);
             if (clear_slot) SJ_CUDA(cudaMemsetAsync(dslot, 0, sizeof(Slot), s));
-            JoinArgs ja = base_args(idx, o, work);
+            JoinArgs ja = base_args(idx, o, dwork(si));
             ja.out = buf;
             ja.cap = cap;
             ja.cursor = &dslot->cursor;
@@ -388,19 +393,20 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
 
         if (!o.result_on_host) {
             // ---- device-resident batches: every batch owns its buffer; streams run them
-            //      concurrently.  Up to 64 batches own a cursor slot each (cleared by the initial
-            //      memset; all read back by ONE copy at the end, with the work counters); beyond
-            //      that slot i % S of each stream is reused in order, read back per batch.
+            //      concurrently.  Batch b runs on stream b % S; up to 64 batches per stream own a
+            //      cursor slot each in that stream's block (zeroed by its memset), read back with the
+            //      stream's work counters by ONE copy after its last batch; beyond that slot 0 of the
+            //      stream is reused in order and read back per batch.
             res->batches.resize(nb);
             std::vector<uint64_t> counts(nb, 0);
-            const bool own_slots = nb <= 64;
+            const bool own_slots = nb <= (size_t)64 * S;
             for (size_t b = 0; b < nb; ++b) {
                 const int si = (int)(b % S);
                 cudaStream_t s = cx.streams[si];
-                const size_t slot = own_slots ? b : (size_t)si;
+                const size_t slot = own_slots ? b / S : 0;
                 if (!own_slots && b >= (size_t)S) {   // stream si's previous batch must have published its cursor
                     SJ_CUDA(cudaStreamSynchronize(s));
-                    counts[b - S] = hslots[si].cursor;      // (+ the batch's self pairs below)
+                    counts[b - S] = hslot(si, 0)->cursor;   // (+ the batch's self pairs below)
                 }
                 const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(
                     o.batch_capacity_pairs, est[b] + est[b] / 4 + 65536));
@@ -408,33 +414,25 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 bt.pairs = static_cast<uint64_t *>(result_buffer_get(idx->device, cap * sizeof(uint64_t), s));
                 bt.cap = cap;
                 bt.on_device = 1;
-                run_batch(cuts[b], cuts[b + 1], bt.pairs, cap, dslots + slot, s, !own_slots);
+                run_batch(cuts[b], cuts[b + 1], bt.pairs, cap, dslot(si, slot), si, !own_slots);
                 if (!own_slots)
-                    SJ_CUDA(cudaMemcpyAsync(hslots + si, dslots + si, sizeof(Slot), cudaMemcpyDeviceToHost, s));
+                    SJ_CUDA(cudaMemcpyAsync(hslot(si, 0), dslot(si, 0), sizeof(Slot), cudaMemcpyDeviceToHost, s));
+                if (b + S >= nb)                      // the stream's last batch: its block back to the host
+                    SJ_CUDA(cudaMemcpyAsync(hbase + kBlock * si, dbase + kBlock * si, kBlock, cudaMemcpyDeviceToHost, s));
             }
             tr.mark("batches launched");
-            // the work counters (and the own slots) are read back on stream 0 after every stream's
-            // last batch, so the one round of stream syncs below also covers them
-            for (int i = 1; i < S; ++i) {
-                SJ_CUDA(cudaEventRecord(cx.events[2 + i], cx.streams[i]));
-                SJ_CUDA(cudaStreamWaitEvent(s0, cx.events[2 + i], 0));
-            }
-            tr.dev("gap + batches (stream 0 joined)", s0);
-            SJ_CUDA(cudaMemcpyAsync(hwork, work, kWorkBytes + (own_slots ? sizeof(Slot) * nb : 0),
-                                    cudaMemcpyDeviceToHost, s0));
-            tr.dev("counter copy", s0);
             for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
             tr.mark("batches done (synced)");
             work_read = true;
             cudaStream_t st_sort = s0;
             if (own_slots) {
-                for (size_t b = 0; b < nb; ++b) counts[b] = hslots[b].cursor;
+                for (size_t b = 0; b < nb; ++b) counts[b] = hslot((int)(b % S), b / S)->cursor;
             } else {
-                for (size_t b = (nb > (size_t)S ? nb - S : 0); b < nb; ++b) counts[b] = hslots[b % S].cursor;
+                for (size_t b = (nb > (size_t)S ? nb - S : 0); b < nb; ++b) counts[b] = hslot((int)(b % S), 0)->cursor;
             }
             for (size_t b = 0; b < nb; ++b) counts[b] += nself_of(cuts[b], cuts[b + 1]);
             // overflowed batches (estimate too low): exact re-allocation, all re-runs launched
-            // together across the streams (slots 0..S-1 are free again), one sync for the round
+            // together across the streams (slot 0 of every stream is free again), one sync per round
             std::vector<size_t> redo;
             for (size_t b = 0; b < nb; ++b)
                 if (counts[b] > res->batches[b].cap) redo.push_back(b);
@@ -448,14 +446,14 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                     result_buffer_put(idx->device, bt.pairs, st);
                     bt.pairs = static_cast<uint64_t *>(result_buffer_get(idx->device, counts[b] * sizeof(uint64_t), st));
                     bt.cap = counts[b];
-                    run_batch(cuts[b], cuts[b + 1], bt.pairs, bt.cap, dslots + si, st, true);
-                    SJ_CUDA(cudaMemcpyAsync(hslots + si, dslots + si, sizeof(Slot), cudaMemcpyDeviceToHost, st));
+                    run_batch(cuts[b], cuts[b + 1], bt.pairs, bt.cap, dslot(si, 0), si, true);
+                    SJ_CUDA(cudaMemcpyAsync(hslot(si, 0), dslot(si, 0), sizeof(Slot), cudaMemcpyDeviceToHost, st));
                     ++stats.retries;
                 }
                 for (size_t r = r0; r < r1; ++r) SJ_CUDA(cudaStreamSynchronize(cx.streams[r - r0]));
                 for (size_t r = r0; r < r1; ++r) {
                     const size_t b = redo[r];
-                    const uint64_t n = hslots[r - r0].cursor + nself_of(cuts[b], cuts[b + 1]);
+                    const uint64_t n = hslot((int)(r - r0), 0)->cursor + nself_of(cuts[b], cuts[b + 1]);
                     if (n != counts[b]) fail(SJ_ERR_CUDA, "batch re-run produced a different count");
                 }
             }
@@ -488,8 +486,8 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 auto r = pending.front();
                 pending.pop_front();
                 inflight[i] = r;
-                run_batch(r.first, r.second, staging[i], scap[i], dslots + i, cx.streams[i], true);
-                SJ_CUDA(cudaMemcpyAsync(hslots + i, dslots + i, sizeof(Slot), cudaMemcpyDeviceToHost,
+                run_batch(r.first, r.second, staging[i], scap[i], dslot(i, 0), i, true);
+                SJ_CUDA(cudaMemcpyAsync(hslot(i, 0), dslot(i, 0), sizeof(Slot), cudaMemcpyDeviceToHost,
                                         cx.streams[i]));
                 order.push_back(i);
             };
@@ -501,7 +499,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 // precedes the kernel, so a stream sync here waits for exactly that batch.
                 SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
                 const auto r = inflight[i];
-                const uint64_t n = hslots[i].cursor + nself_of(r.first, r.second);
+                const uint64_t n = hslot(i, 0)->cursor + nself_of(r.first, r.second);
                 if (n > scap[i]) {
                     ++stats.retries;
                     if (r.second - r.first < 2) {
@@ -535,14 +533,16 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
         }
 
-        // ---- work counters (already read back unless a retry / host mode ran more kernels)
+        // ---- work counters (already read back unless a retry / host mode ran more kernels; every
+        //      stream is synchronised here)
         if (!work_read || stats.retries || o.sort_pairs) {
-            SJ_CUDA(cudaMemcpyAsync(hwork, work, kWorkBytes, cudaMemcpyDeviceToHost, s0));
+            SJ_CUDA(cudaMemcpyAsync(hbase, dbase, kBlock * S, cudaMemcpyDeviceToHost, s0));
             SJ_CUDA(cudaStreamSynchronize(s0));
         }
         unsigned long long wsum[3] = {0, 0, 0};
-        for (int sl = 0; sl < kWorkSlots; ++sl)
-            for (int i = 0; i < 3; ++i) wsum[i] += hwork[4 * sl + i];
+        for (int si = 0; si < S; ++si)
+            for (int sl = 0; sl < kWorkSlots; ++sl)
+                for (int i = 0; i < 3; ++i) wsum[i] += hwork(si)[4 * sl + i];
         stats.cells_probed = wsum[0];
         stats.candidates_tested = wsum[1];
         stats.pairs = res->total;

@@ -59,13 +59,29 @@ struct JoinArgs {
                                    // query k's (p,p) sits at out[k - q0], every other pair after them
 };
 
-// Per-warp emission buffer of the dense kernel (shared memory): hits are appended at warp-uniform
-// points; one atomicAdd on the batch cursor per flush of up to kWarpBufPairs pairs.
+// Per-warp shared memory of the dense kernel: the emission ring (hits are appended once per
+// 32-candidate tile) and the candidate tile (the coordinates of 32 consecutive A-positions in SoA
+// form, tx[j*32 + e], and their original ids), loaded coalesced by the warp and read back as
+// broadcasts by every query lane.
+// The ring holds kWarpBufPairs pairs between the counters head <= tail (ring slot = counter mod
+// kWarpBufPairs).  Output space is reserved AHEAD: once half the ring is filled, the leader issues
+// the atomicAdd on the batch cursor for [head, tail) and the warp goes on testing candidates; the
+// reserved pairs are written out only when the ring needs the room (usually one tile later), so
+// the round trip of that atomic -- contended by every warp of the launch -- is off the warp's
+// critical path (ncu: 23% of the dense kernel's stall samples sat on the flush's shuffle of the
+// returned base).  Every reservation covers exactly the pairs it is for, so the batch stays dense.
 constexpr int kWarpBufPairs = 1024;
 struct WarpBuf {
-    uint64_t *buf;     // [kWarpBufPairs] in shared memory
-    uint32_t cnt;      // warp-uniform fill level (kept identical in every lane)
+    uint64_t *buf;        // [kWarpBufPairs] ring in shared memory
+    double *tx;           // [D][32] candidate tile (SoA)
+    uint32_t *tid;        // [32] original ids of the tile's candidates
+    uint32_t head, tail;  // warp-uniform ring counters
+    uint32_t pend;        // pairs [head, head + pend) are reserved, their base in `base` (leader)
+    unsigned long long base;
 };
+// dynamic shared memory of k_refine_dense<D>: per warp the pair buffer, the SoA tile and the ids
+template <int D>
+__host__ __device__ constexpr size_t dense_smem_per_warp() { return sizeof(uint64_t) * kWarpBufPairs + sizeof(double) * 32 * D + 4 * 32; }
 
 constexpr int kRefineThreads = 256;
 #ifndef SJ_REFINE_MIN_BLOCKS
@@ -149,44 +165,125 @@ __device__ __forceinline__ void emit_self(const JoinArgs &ja, uint32_t k, uint32
     }
 }
 
-// Warp-converged emission into the per-warp buffer (dense kernel only: every lane of `mask`
-// executes this at the same candidate).  Flush = one atomicAdd + coalesced copy-out.
-__device__ __forceinline__ void warpbuf_flush(const JoinArgs &ja, WarpBuf &wb, unsigned mask)
+// Write the ring's pairs [head, head + len) to the batch at p0 (all 32 lanes).  16-byte streaming
+// stores when both ends are even (the pairs are not read again by the join; the index stays in L2),
+// as (at most) two contiguous runs of the ring.
+__device__ __forceinline__ void ring_write(const JoinArgs &ja, const WarpBuf &wb, uint32_t head, uint32_t len,
+                                           unsigned long long p0)
 {
-    if (wb.cnt == 0) return;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(mask) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(ja.cursor, (unsigned long long)wb.cnt);
-    base = __shfl_sync(mask, base, leader);
-    const uint32_t nl = __popc(mask), rank = __popc(mask & ((1u << lane) - 1u));
-    for (uint32_t i = rank; i < wb.cnt; i += nl) {
-        const unsigned long long pos = ja.nself + base + i;
-        if (pos < ja.cap) ja.out[pos] = wb.buf[i];
-        else atomicOr(ja.overflow, 1u);
+    constexpr uint32_t R = (uint32_t)kWarpBufPairs;
+    const uint32_t lane = threadIdx.x & 31u;
+    if (p0 + len <= ja.cap && !((p0 | len | head) & 1ull)) {
+        const uint32_t h2 = (head & (R - 1)) >> 1, n2 = len >> 1;
+        const uint32_t first = min(n2, R / 2 - h2);              // 16-byte units before the wrap
+        const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(wb.buf);
+        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(ja.out + p0);
+        for (uint32_t i = lane; i < first; i += 32u) __stcs(dst + i, src[h2 + i]);
+        for (uint32_t i = lane; i < n2 - first; i += 32u) __stcs(dst + first + i, src[i]);
+    } else {
+        for (uint32_t i = lane; i < len; i += 32u) {
+            const unsigned long long pos = p0 + i;
+            if (pos < ja.cap) __stcs(reinterpret_cast<unsigned long long *>(ja.out + pos), wb.buf[(head + i) & (R - 1)]);
+            else atomicOr(ja.overflow, 1u);
+        }
     }
-    __syncwarp(mask);
-    wb.cnt = 0;
 }
 
-template <bool BOTH>
-__device__ __forceinline__ void emit_buffered(const JoinArgs &ja, WarpBuf &wb, unsigned mask, bool hit,
-                                              uint32_t pid, uint32_t qid, uint32_t &emitted)
+// Write out the reserved pairs (waits for the reservation's atomic only now).
+__device__ __forceinline__ void ring_retire(const JoinArgs &ja, WarpBuf &wb)
 {
-    const unsigned hits = __ballot_sync(mask, hit);
-    if (hits == 0u) return;
+    if (!wb.pend) return;
+    const unsigned long long base = __shfl_sync(0xffffffffu, wb.base, 0);
+    ring_write(ja, wb, wb.head, wb.pend, ja.nself + base);
+    wb.head += wb.pend;
+    wb.pend = 0;
+}
+
+// Reserve output space for everything not yet reserved (asynchronous: the result is consumed by
+// ring_retire).  ATOM issued by lane 0.
+__device__ __forceinline__ void ring_reserve(const JoinArgs &ja, WarpBuf &wb)
+{
+    const uint32_t len = wb.tail - wb.head;
+    if (wb.pend || !len) return;
+    if ((threadIdx.x & 31u) == 0) wb.base = atomicAdd(ja.cursor, (unsigned long long)len);
+    wb.pend = len;
+}
+
+// Empty the ring (end of the kernel, or a unit that needs more room than retiring frees).
+__device__ __forceinline__ void ring_drain(const JoinArgs &ja, WarpBuf &wb)
+{
+    ring_retire(ja, wb);
+    ring_reserve(ja, wb);
+    ring_retire(ja, wb);
+    __syncwarp();
+}
+
+// Emission of one 32-candidate tile of the dense kernel: lane = query, bit e of hm = candidate e of
+// the tile (id wb.tid[e]) is a hit.  One warp prefix sum places every lane's pairs in the ring (no
+// per-candidate ballot); each lane then writes its hits, (p,q) and (q,p) as one 16-byte store when
+// BOTH.  A tile yields at most 32*32*per pairs; one that does not fit the ring (> kWarpBufPairs, only
+// with BOTH and > 50% hits) is emitted in two halves of 16 candidates.
+template <bool BOTH>
+__device__ __forceinline__ void emit_tile(const JoinArgs &ja, WarpBuf &wb, uint32_t hm, uint32_t pid,
+                                          uint32_t &emitted)
+{
     constexpr uint32_t per = BOTH ? 2u : 1u;
-    const uint32_t n = __popc(hits) * per;
-    if (wb.cnt + n > (uint32_t)kWarpBufPairs) warpbuf_flush(ja, wb, mask);
-    if (hit) {
-        const int lane = threadIdx.x & 31;
-        const uint32_t pos = wb.cnt + __popc(hits & ((1u << lane) - 1u)) * per;
-        wb.buf[pos] = ((uint64_t)pid << 32) | qid;
-        if (BOTH) wb.buf[pos + 1] = ((uint64_t)qid << 32) | pid;
-        emitted += per;
+    constexpr uint32_t R = (uint32_t)kWarpBufPairs;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t sbuf = (uint32_t)__cvta_generic_to_shared(wb.buf);
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+        uint32_t m = hm;
+        uint32_t n = __popc(m) * per;
+        uint32_t total = __reduce_add_sync(0xffffffffu, n);
+        if (total == 0u) return;
+        if (total > R) {                                 // split: the low half now, the high half next
+            m = hm & 0xFFFFu;
+            n = __popc(m) * per;
+            total = __reduce_add_sync(0xffffffffu, n);
+        }
+        hm &= ~m;
+        uint32_t inc = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (uint32_t)o) inc += t;
+        }
+        if (wb.tail - wb.head + total > R) {             // make room: the reserved part first
+            ring_retire(ja, wb);
+            if (wb.tail - wb.head + total > R) ring_drain(ja, wb);
+            __syncwarp();
+        }
+        // byte offset into the ring (wraps with one AND: the ring is 8 KB); two hits per iteration
+        uint32_t pb = (wb.tail + inc - n) << 3;
+        const uint32_t stid = (uint32_t)__cvta_generic_to_shared(wb.tid);
+        emitted += n;
+        constexpr uint32_t kStep = per * 8u;
+        while (m) {
+            uint32_t e1, e2;
+            asm("bfind.u32 %0, %1;" : "=r"(e1) : "r"(m));
+            m ^= 1u << e1;
+            const bool two = m != 0u;
+            asm("bfind.u32 %0, %1;" : "=r"(e2) : "r"(m));   // 0xffffffff when m == 0 (unused then)
+            if (two) m ^= 1u << e2;
+            uint32_t q1, q2;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(q1) : "r"(stid + 4u * e1));
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(q2) : "r"(stid + 4u * (e2 & 31u)));
+            const uint32_t a1 = sbuf + (pb & (R * 8u - 1u)), a2 = sbuf + ((pb + kStep) & (R * 8u - 1u));
+            if constexpr (BOTH) {
+                // (p,q) = {q, p} and (q,p) = {p, q} as little-endian 32-bit words
+                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %2, %1};" ::"r"(a1), "r"(q1), "r"(pid) : "memory");
+                if (two) asm volatile("st.shared.v4.u32 [%0], {%1, %2, %2, %1};" ::"r"(a2), "r"(q2), "r"(pid) : "memory");
+            } else {
+                asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a1), "r"(q1), "r"(pid) : "memory");
+                if (two) asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a2), "r"(q2), "r"(pid) : "memory");
+            }
+            pb += two ? 2u * kStep : kStep;
+        }
+        __syncwarp();
+        wb.tail += total;
+        if (wb.tail - wb.head >= R / 2) ring_reserve(ja, wb);
     }
-    __syncwarp(mask);
-    wb.cnt += n;
 }
 
 // Test the points at A-positions m0, m0+stride, ... < m1 against the query.
@@ -199,40 +296,68 @@ __device__ __forceinline__ void scan_range(const DevIndex &ix, const JoinArgs &j
 {
     const uint32_t n = ix.n;
     if constexpr (DENSE) {
-        // all 32 lanes are active here (helper lanes included): candidates are loaded 32 at a time,
-        // one per lane (coalesced), and broadcast with shuffles
+        // all 32 lanes are active here (helper lanes included).  Tiles of 32 candidates: lane e loads
+        // candidate g+e (coalesced SoA reads of X) into the warp's shared-memory tile; every query
+        // lane then tests the whole tile reading two candidates per 16-byte broadcast load per
+        // dimension, collects a 32-bit hit mask, and the tile is emitted at once (emit_tile).
+        // The next tile's loads are issued before the current tile is tested (software pipelining:
+        // their L2/DRAM latency hides behind the tile's FP64 work).
+        const uint32_t lane = threadIdx.x & 31u;
+        double nx[D];
+        uint32_t nid = 0;
+        if (m0 + lane < m1) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) nx[j] = __ldg(ix.X + (uint64_t)j * n + m0 + lane);
+            nid = __ldg(ix.A + m0 + lane);
+        }
+#pragma unroll 1
         for (uint32_t g = m0; g < m1; g += 32u) {
-            const uint32_t mine = g + (threadIdx.x & 31u);
-            double cx[D];
-            uint32_t cid = 0;
-            if (mine < m1) {
+            __syncwarp();                                   // the previous tile is consumed
+            if (g + lane < m1) {
 #pragma unroll
-                for (int j = 0; j < D; ++j) cx[j] = __ldg(ix.X + (uint64_t)j * n + mine);
-                cid = __ldg(ix.A + mine);
-            } else {
-#pragma unroll
-                for (int j = 0; j < D; ++j) cx[j] = 0.0;
+                for (int j = 0; j < D; ++j) wb->tx[j * 32 + lane] = nx[j];
+                wb->tid[lane] = nid;
             }
+            const uint32_t nxt = g + 32u + lane;
+            if (nxt < m1) {
+#pragma unroll
+                for (int j = 0; j < D; ++j) nx[j] = __ldg(ix.X + (uint64_t)j * n + nxt);
+                nid = __ldg(ix.A + nxt);
+            }
+            __syncwarp();
             const uint32_t lim = min(32u, m1 - g);
-            for (uint32_t e = 0; e < lim; ++e) {
-                double s;
-                {
-                    const double t = __dsub_rn(q.x[0], __shfl_sync(0xffffffffu, cx[0], e));
-                    s = __dmul_rn(t, t);
-                }
+            // candidates this lane must test: e < lim, a real query, and the home-cell rule
+            uint32_t vm = lim == 32u ? 0xffffffffu : ((1u << lim) - 1u);
+            if (!q.valid) vm = 0u;
+            if (HOME && q.k >= g) {
+                const uint32_t r = q.k - g;                 // the query's own position in the tile
+                if (BOTH) vm &= r >= 31u ? 0u : ~((2u << r) - 1u);   // unicomp: only m > k
+                else if (r < 32u) vm &= ~(1u << r);                  // full: every m != k
+            }
+            q.tests += __popc(vm);
+            uint32_t hm = 0u;
+            const double2 *t2 = reinterpret_cast<const double2 *>(wb->tx);
+            const uint32_t npair = (lim + 1u) >> 1;         // warp-uniform
+            // fully unrolled (constant bit positions: the hit bit is one predicated OR); the
+            // ragged last tile of a range leaves early by a uniform branch
+#pragma unroll
+            for (uint32_t e2 = 0; e2 < 16u; ++e2) {
+                if (e2 >= npair) break;
+                double2 c = t2[e2];                         // dim 0 of candidates 2e2, 2e2+1
+                double ta = __dsub_rn(q.x[0], c.x), tb = __dsub_rn(q.x[0], c.y);
+                double sa = __dmul_rn(ta, ta), sb = __dmul_rn(tb, tb);
 #pragma unroll
                 for (int j = 1; j < D; ++j) {
-                    const double t = __dsub_rn(q.x[j], __shfl_sync(0xffffffffu, cx[j], e));
-                    s = __dadd_rn(s, __dmul_rn(t, t));
+                    c = t2[j * 16 + e2];
+                    ta = __dsub_rn(q.x[j], c.x);
+                    tb = __dsub_rn(q.x[j], c.y);
+                    sa = __dadd_rn(sa, __dmul_rn(ta, ta));
+                    sb = __dadd_rn(sb, __dmul_rn(tb, tb));
                 }
-                const uint32_t qid = __shfl_sync(0xffffffffu, cid, e);
-                const uint32_t m = g + e;
-                bool ok = q.valid;
-                if (HOME) ok = ok && (BOTH ? (m > q.k) : (m != q.k));
-                q.tests += ok ? 1u : 0u;
-                const bool hit = ok && s <= ix.eps2;
-                emit_buffered<BOTH>(ja, *wb, wmask, hit, q.pid, qid, q.emitted);
+                if (sa <= ix.eps2) hm |= 1u << (2u * e2);
+                if (sb <= ix.eps2) hm |= 2u << (2u * e2);
             }
+            emit_tile<BOTH>(ja, *wb, hm & vm, q.pid, q.emitted);
         }
         return;
     }
@@ -690,11 +815,14 @@ __device__ __forceinline__ void flush_work(const JoinArgs &ja, unsigned long lon
 // shared-memory buffer (one cursor atomic per flush instead of one per candidate step).
 constexpr int kDenseWarps = 8;
 template <int D, bool UNICOMP>
-__global__ void __launch_bounds__(32 * kDenseWarps, 2)
+__global__ void __launch_bounds__(32 * kDenseWarps, D <= 3 ? 3 : 2)   // 3 CTAs/SM: smem fits up to d = 4, registers (80) up to d = 3
 k_refine_dense(const DevIndex ix, const JoinArgs ja)
 {
-    __shared__ TopTable tt;
-    extern __shared__ __align__(16) uint64_t s_buf[];     // [kDenseWarps][kWarpBufPairs]
+    // dynamic shared memory: [rings | tiles | ids] (dense_smem_per_warp each warp) and, in the
+    // cell-scan mode only, the top-offset table after them -- a static table (9.8 KB) kept the
+    // kernel at 2 CTAs per SM
+    extern __shared__ __align__(16) uint64_t s_buf[];
+    TopTable &tt = *reinterpret_cast<TopTable *>(reinterpret_cast<char *>(s_buf) + kDenseWarps * dense_smem_per_warp<D>());
     if (ix.search_mode == kSearchCellScan) build_top_table<D>(ix, tt);
     // the batch's tasks are the contiguous range of the A-ordered task list whose real end
     // min(start + 32, end of its cell) lies after q0 and whose start lies before q1.  Task ends are
@@ -719,6 +847,9 @@ k_refine_dense(const DevIndex ix, const JoinArgs ja)
     q.G = 1u;
     q.sub = 0u;
     q.emitted = q.probes = q.tests = 0;
+    double *s_tx = reinterpret_cast<double *>(s_buf + (size_t)kDenseWarps * kWarpBufPairs);
+    uint32_t *s_tid = reinterpret_cast<uint32_t *>(s_tx + (size_t)kDenseWarps * 32 * D);
+    WarpBuf wb{s_buf + (size_t)warp * kWarpBufPairs, s_tx + (size_t)warp * 32 * D, s_tid + warp * 32, 0u, 0u, 0u, 0ull};
 #pragma unroll 1
     for (uint32_t task = s_tlo + blockIdx.x * kDenseWarps + warp; task < ja.n_dense_tasks;
          task += gridDim.x * kDenseWarps) {            // warp-uniform
@@ -728,16 +859,15 @@ k_refine_dense(const DevIndex ix, const JoinArgs ja)
         const uint32_t end = min(start + 32u, __ldg(ix.G + h + 1));
         const uint32_t a = max(start, ja.q0), b = min(end, ja.q1);
         if (a < b) {                                   // task inside this batch
-            WarpBuf wb{s_buf + (size_t)warp * kWarpBufPairs, 0u};
             // every lane runs the (cell-uniform) enumeration; lanes past the task's end are helpers
             // that load and broadcast candidates but never emit (they take the first query's point)
             const uint32_t k = a + lane;
             q.valid = k < b;
             refine_query<D, kEmit, UNICOMP, true>(ix, ja, q.valid ? k : a, h, __ldg(ix.G + h), __ldg(ix.G + h + 1),
                                                   0xffffffffu, q, tt, &wb);
-            warpbuf_flush(ja, wb, 0xffffffffu);
         }
     }
+    ring_drain(ja, wb);                                // the ring lives across the warp's tasks
     flush_work(ja, q.probes, q.tests, q.emitted);
 }
 

@@ -38,7 +38,7 @@ template <>
 void launch_dense_d<6>(const DevIndex &ix, const JoinArgs &ja, bool unicomp, dim3 grid, cudaStream_t s)
 {
     const dim3 block(32 * kDenseWarps);
-    const size_t smem = sizeof(uint64_t) * kDenseWarps * kWarpBufPairs;
+    const size_t smem = kDenseWarps * dense_smem_per_warp<6>() + (ix.search_mode == kSearchCellScan ? sizeof(TopTable) : 0);
     if (unicomp) {
         set_max_dyn_smem(reinterpret_cast<const void *>(k_refine_dense<6, true>), (int)smem);
         k_refine_dense<6, true><<<grid, block, smem, s>>>(ix, ja);

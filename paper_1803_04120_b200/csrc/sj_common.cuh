@@ -236,6 +236,11 @@ void result_cache_trim(int dev);                 // free every cached buffer of 
 void set_result_cache_limit(size_t bytes);
 void scratch_trim(int dev);
 int device_sm_count(int dev);                  // cached multiprocessor count
+// L2 persisting window over the build's input (context.cu): begin/stop on a stream, end after a sync
+size_t l2_persist_limit(int dev);
+void l2_persist_begin(int dev, cudaStream_t s, const void *base, size_t bytes);
+void l2_persist_stop(int dev, cudaStream_t s);
+void l2_persist_end(int dev);
 // the build's scratch buffer (nullptr if busy: use the pool instead); *zero_prefix = leading bytes known
 // to be zero; the releasing build states how many leading bytes it leaves zero
 void *scratch_acquire(int dev, size_t bytes, size_t *zero_prefix);

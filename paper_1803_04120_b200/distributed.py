@@ -218,8 +218,8 @@ def sharded_self_join(points, eps: float, device: int, group=None, stats: bool =
         rank, world = 0, 1
     dev = torch.device("cuda", device)
     if world == 1:
-        idx = sj.build_index(points, eps, device=device)
-        res = sj.self_join(idx, **join_kw)
+        # one library call (sj_self_join_points): build + join without a return to Python between them
+        res, idx = sj.join_points(points, eps, device=device, **join_kw)
         if stats:
             st = res.stats
             return res, res.n_pairs, idx, {k: int(st[k]) for k in COUNTERS}
