@@ -91,6 +91,13 @@ typedef struct {
                                       warp per 32 queries with warp-buffered emission; 0: off     */
     int sort_pairs;                /* 0 (default); 1: each batch is sorted by (key, value) on the
                                       device before it is returned / drained       */
+    int drain_csr;                 /* 0 (default); 1 (requires result_on_host): each batch crosses
+                                      PCIe as CSR neighbour lists -- uint32 row offsets over all N
+                                      keys + one uint32 neighbour per pair, 4 B/pair instead of 8
+                                      (PAPER.md:209 sorted key/value pairs; the D2H drain is the
+                                      bottleneck PAPER.md:262/601 names).  Rows are in arbitrary
+                                      order unless sort_pairs = 1 (then ascending).  Read with
+                                      sj_result_batch_csr; sj_result_copy_to_host expands them.  */
 } sj_join_opts;
 
 typedef struct {
@@ -200,6 +207,14 @@ sj_status sj_result_info(const sj_result *r, uint64_t *n_pairs, uint32_t *n_batc
  * on the index's device) or pinned host memory (*on_device=0); owned by the result. */
 sj_status sj_result_batch(const sj_result *r, uint32_t b, const uint64_t **pairs, uint64_t *n,
                           int *on_device);
+
+/* Batch b of a drain_csr result: row_offsets[i] .. row_offsets[i+1] index the neighbours (original
+ * ids) that batch b holds for key i in `neighbors`; *n_rows = N of the joined index (row_offsets has
+ * N + 1 entries), *n = pairs in the batch.  Pinned host memory owned by the result.  Errors:
+ * SJ_ERR_STATE if the batch is not in CSR form (sj_result_batch then returns its pairs; for a CSR
+ * batch sj_result_batch fails with SJ_ERR_STATE), SJ_ERR_ARG for a bad index. */
+sj_status sj_result_batch_csr(const sj_result *r, uint32_t b, const uint32_t **row_offsets,
+                              const uint32_t **neighbors, uint64_t *n_rows, uint64_t *n);
 
 /* Copy all pairs of a result, batch after batch, into host memory dst (capacity cap pairs).
  * Errors: SJ_ERR_ARG if cap < total. */

@@ -339,9 +339,27 @@ sj_status sj_result_batch(const sj_result *r, uint32_t b, const uint64_t **pairs
     if (!r) sj::fail(SJ_ERR_STATE, "result is NULL");
     if (b >= r->batches.size()) sj::fail(SJ_ERR_ARG, "batch index out of range");
     const sj_batch &bt = r->batches[b];
+    if (bt.csr) sj::fail(SJ_ERR_STATE, "batch is in CSR form (drain_csr): use sj_result_batch_csr");
     if (pairs) *pairs = bt.pairs;
     if (n) *n = bt.n;
     if (on_device) *on_device = bt.on_device;
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_result_batch_csr(const sj_result *r, uint32_t b, const uint32_t **row_offsets, const uint32_t **neighbors,
+                              uint64_t *n_rows, uint64_t *n)
+{
+    SJ_API_BEGIN
+    if (!r) sj::fail(SJ_ERR_STATE, "result is NULL");
+    if (b >= r->batches.size()) sj::fail(SJ_ERR_ARG, "batch index out of range");
+    const sj_batch &bt = r->batches[b];
+    if (!bt.csr) sj::fail(SJ_ERR_STATE, "batch is not in CSR form: use sj_result_batch");
+    const uint32_t *blk = reinterpret_cast<const uint32_t *>(bt.pairs);
+    if (row_offsets) *row_offsets = blk;
+    if (neighbors) *neighbors = blk ? blk + bt.rows + 1 : nullptr;
+    if (n_rows) *n_rows = bt.rows;
+    if (n) *n = bt.n;
     return SJ_OK;
     SJ_API_END
 }
@@ -356,8 +374,15 @@ sj_status sj_result_copy_to_host(const sj_result *r, uint64_t *dst, uint64_t cap
     uint64_t off = 0;
     for (const auto &b : r->batches) {
         if (!b.n) continue;
-        if (b.on_device) SJ_CUDA(cudaMemcpy(dst + off, b.pairs, b.n * 8, cudaMemcpyDeviceToHost));
-        else std::memcpy(dst + off, b.pairs, b.n * 8);
+        if (b.csr) {                       // expand the CSR block: (row << 32) | neighbour
+            const uint32_t *offs = reinterpret_cast<const uint32_t *>(b.pairs), *nb = offs + b.rows + 1;
+            for (uint64_t i = 0; i < b.rows; ++i)
+                for (uint32_t e = offs[i]; e < offs[i + 1]; ++e) dst[off + e] = (i << 32) | nb[e];
+        } else if (b.on_device) {
+            SJ_CUDA(cudaMemcpy(dst + off, b.pairs, b.n * 8, cudaMemcpyDeviceToHost));
+        } else {
+            std::memcpy(dst + off, b.pairs, b.n * 8);
+        }
         off += b.n;
     }
     return SJ_OK;

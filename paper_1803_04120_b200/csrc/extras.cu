@@ -62,6 +62,8 @@ void result_to_csr_impl(const sj_result *r, uint64_t n_points, uint64_t *row_off
     const uint64_t n = r->total;
     const int nsm = device_sm_count(r->device);
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)nsm * 8));
+    for (const auto &b : r->batches)
+        if (b.csr) fail(SJ_ERR_STATE, "the result's batches are already CSR (drain_csr): read them with sj_result_batch_csr");
     Scratch<uint64_t> all(n ? n : 1, s);
     uint64_t off = 0;
     for (const auto &b : r->batches) {
@@ -87,6 +89,68 @@ void result_to_csr_impl(const sj_result *r, uint64_t n_points, uint64_t *row_off
         SJ_LAUNCHED();
     }
     SJ_CUDA(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------------------ a8 + f2: CSR drain of a batch
+// One finished batch (device pairs) -> CSR over all N keys in device memory: counts by key (one
+// atomic per distinct key per warp: __match_any_sync groups a warp's equal keys -- a query's
+// pairs sit together in the batch), exclusive scan, then every pair's value is placed at its row's
+// running cursor (rows in arbitrary order), or -- for a batch sorted by (key, value) -- at its own
+// index (rows ascending, no atomics).  The caller copies [offsets | neighbours] to the host.
+namespace {
+__global__ void __launch_bounds__(256)
+k_drain_hist(const uint64_t *__restrict__ pairs, uint64_t n, uint32_t *__restrict__ counts)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {   // warp-uniform trips
+        const uint64_t i = i0 + threadIdx.x;
+        const bool ok = i < n;
+        const uint32_t key = ok ? (uint32_t)(pairs[i] >> 32) : 0xffffffffu;
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        if (ok && (threadIdx.x & 31) == (unsigned)(__ffs(grp) - 1)) atomicAdd(counts + key, (uint32_t)__popc(grp));
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_drain_scatter(const uint64_t *__restrict__ pairs, uint64_t n, uint32_t *__restrict__ cursor,
+                uint32_t *__restrict__ nbrs)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const unsigned lane = threadIdx.x & 31;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+        const uint64_t i = i0 + threadIdx.x;
+        const bool ok = i < n;
+        const uint64_t x = ok ? pairs[i] : ~0ull;
+        const uint32_t key = (uint32_t)(x >> 32);
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        const int leader = __ffs(grp) - 1;
+        uint32_t base = 0;
+        if (ok && lane == (unsigned)leader) base = atomicAdd(cursor + key, (uint32_t)__popc(grp));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (ok) nbrs[base + __popc(grp & ((1u << lane) - 1u))] = (uint32_t)x;
+    }
+}
+}  // namespace
+
+// pairs (device, n) -> dst_offs[rows + 1] and dst_nbrs[n] (device); counts / cursor: rows + 1 uint32
+// scratch (device).  sorted: the batch is in (key, value) order.
+void batch_to_csr_device(const uint64_t *pairs, uint64_t n, uint64_t rows, bool sorted, uint32_t *counts,
+                         uint32_t *cursor, uint32_t *dst_offs, uint32_t *dst_nbrs, cudaStream_t s, int nsm)
+{
+    SJ_CUDA(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * (rows + 1), s));
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)nsm * 16));
+    if (n) {
+        k_drain_hist<<<grid, 256, 0, s>>>(pairs, n, counts);
+        SJ_LAUNCHED();
+    }
+    exclusive_scan_u32_dup(counts, dst_offs, cursor, rows + 1, s);
+    if (!n) return;
+    if (sorted) {
+        k_csr_values<<<grid, 256, 0, s>>>(pairs, n, dst_nbrs);
+    } else {
+        k_drain_scatter<<<grid, 256, 0, s>>>(pairs, n, cursor, dst_nbrs);
+    }
+    SJ_LAUNCHED();
 }
 
 // ------------------------------------------------------------------ result fingerprints
@@ -142,6 +206,36 @@ k_fingerprint(const uint64_t *__restrict__ pairs, uint64_t n, unsigned long long
         atomicAdd(acc + 1, (unsigned long long)fb);
     }
 }
+
+// the same fingerprints over a CSR batch (drain_csr): one thread per row, x = (row << 32) | neighbour
+__global__ void __launch_bounds__(256)
+k_fingerprint_csr(const uint32_t *__restrict__ offs, const uint32_t *__restrict__ nbrs, uint64_t rows,
+                  unsigned long long *__restrict__ acc, uint32_t *__restrict__ counts, uint64_t n_points,
+                  uint32_t *__restrict__ bad)
+{
+    uint64_t fa = 0, fb = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = offs[i], b = offs[i + 1];
+        for (uint32_t e = a; e < b; ++e) {
+            const uint64_t x = (i << 32) | nbrs[e];
+            fa += fp_mix_a(x);
+            fb += fp_mix_b(x);
+        }
+        if (counts && b > a) {
+            if (i < n_points) atomicAdd(counts + i, b - a);
+            else atomicOr(bad, 1u);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        fa += __shfl_xor_sync(0xffffffffu, fa, o);
+        fb += __shfl_xor_sync(0xffffffffu, fb, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(acc + 0, (unsigned long long)fa);
+        atomicAdd(acc + 1, (unsigned long long)fb);
+    }
+}
 }  // namespace
 
 void result_fingerprint_impl(const sj_result *r, uint64_t *fp, uint32_t *counts)
@@ -159,6 +253,15 @@ void result_fingerprint_impl(const sj_result *r, uint64_t *fp, uint32_t *counts)
     uint32_t *bad = reinterpret_cast<uint32_t *>(dacc + 2);
     for (const auto &b : r->batches) {
         if (!b.n) continue;
+        if (b.csr) {
+            void *dp = nullptr;
+            SJ_CUDA(cudaHostGetDevicePointer(&dp, const_cast<uint64_t *>(b.pairs), 0));
+            const uint32_t *offs = static_cast<const uint32_t *>(dp);
+            const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((b.rows + 255) / 256, (uint64_t)nsm * 8));
+            k_fingerprint_csr<<<grid, 256, 0, s>>>(offs, offs + b.rows + 1, b.rows, dacc, counts, r->n_points, bad);
+            SJ_LAUNCHED();
+            continue;
+        }
         const uint64_t *src = b.pairs;
         if (!b.on_device) {
             void *dp = nullptr;

@@ -72,6 +72,7 @@ void validate(const sj_index *idx, const sj_join_opts &o, uint64_t *qb, uint64_t
     if (o.min_batches < 1 || o.min_batches > 1 << 20) fail(SJ_ERR_ARG, "min_batches must be >= 1");
     if (o.n_streams < 1 || o.n_streams > 32) fail(SJ_ERR_ARG, "n_streams must be in [1,32]");
     if (o.batch_capacity_pairs < 1) fail(SJ_ERR_ARG, "batch_capacity_pairs must be >= 1");
+    if (o.drain_csr && !o.result_on_host) fail(SJ_ERR_ARG, "drain_csr requires result_on_host = 1");
     const uint64_t n = idx->view.n;
     uint64_t b = o.query_begin, e = o.query_end;
     if (b == 0 && e == 0) e = n;
@@ -469,8 +470,9 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             //      the D2H of batch b (stream order), while other streams compute.
             uint64_t maxest = 0;
             for (auto e : est) maxest = std::max(maxest, e);
-            const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(o.batch_capacity_pairs,
-                                                                          maxest + maxest / 4 + 65536));
+            uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(o.batch_capacity_pairs,
+                                                                    maxest + maxest / 4 + 65536));
+            if (o.drain_csr) cap = std::min<uint64_t>(cap, 0xffffffffull);   // uint32 row offsets
             std::vector<uint64_t *> staging(S, nullptr);
             std::vector<uint64_t> scap(S, cap);           // per-stream staging capacity
             struct StagingGuard {
@@ -478,6 +480,26 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 ~StagingGuard() { for (size_t i = 0; i < v.size(); ++i) if (v[i]) dev_free(v[i], cx.streams[i]); }
             } sg{staging, cx};
             for (int i = 0; i < S; ++i) staging[i] = dalloc<uint64_t>(cap, cx.streams[i]);
+            // drain_csr: per stream the CSR of the finished batch is built in device memory
+            // ([offsets | neighbours] contiguous, one D2H copy) with two N+1 scratch arrays
+            const uint64_t rows = ix.n;
+            std::vector<uint32_t *> csr_blk(S, nullptr), csr_tmp(S, nullptr);
+            struct CsrGuard {
+                std::vector<uint32_t *> &a, &b; DevCtx &cx;
+                ~CsrGuard() {
+                    for (size_t i = 0; i < a.size(); ++i) {
+                        if (a[i]) dev_free(a[i], cx.streams[i]);
+                        if (b[i]) dev_free(b[i], cx.streams[i]);
+                    }
+                }
+            } cgd{csr_blk, csr_tmp, cx};
+            if (o.drain_csr) {
+                for (int i = 0; i < S; ++i) {
+                    csr_blk[i] = dalloc<uint32_t>(rows + 1 + cap, cx.streams[i]);
+                    csr_tmp[i] = dalloc<uint32_t>(2 * (rows + 1), cx.streams[i]);
+                }
+            }
+            const int nsm = device_sm_count(idx->device);
             std::deque<std::pair<uint64_t, uint64_t>> pending;
             for (size_t b = 0; b < nb; ++b) pending.emplace_back(cuts[b], cuts[b + 1]);
             std::vector<std::pair<uint64_t, uint64_t>> inflight(S, {0, 0});
@@ -504,9 +526,15 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                     ++stats.retries;
                     if (r.second - r.first < 2) {
                         // one query emits more than the staging buffer holds: grow it to fit
+                        if (o.drain_csr && n > 0xffffffffull)
+                            fail(SJ_ERR_ARG, "drain_csr: one query emits >= 2^32 pairs");
                         dev_free(staging[i], cx.streams[i]);
                         staging[i] = dalloc<uint64_t>(n, cx.streams[i]);
                         scap[i] = n;
+                        if (o.drain_csr) {
+                            dev_free(csr_blk[i], cx.streams[i]);
+                            csr_blk[i] = dalloc<uint32_t>(rows + 1 + n, cx.streams[i]);
+                        }
                         pending.emplace_front(r);
                     } else {
                         // overflow: split the query range and re-run both halves first
@@ -519,7 +547,17 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                     bt.on_device = 0;
                     bt.n = n;
                     bt.cap = n;
-                    if (n) {
+                    if (o.drain_csr) {
+                        // 4 B per pair + 4 B per row cross PCIe instead of 8 B per pair
+                        if (n && o.sort_pairs) sort_pairs_device(staging[i], n, ix.n, cx.streams[i]);
+                        batch_to_csr_device(staging[i], n, rows, o.sort_pairs != 0, csr_tmp[i], csr_tmp[i] + rows + 1,
+                                            csr_blk[i], csr_blk[i] + rows + 1, cx.streams[i], nsm);
+                        const size_t bytes = sizeof(uint32_t) * (rows + 1 + n);
+                        bt.pairs = static_cast<uint64_t *>(host_pinned_alloc(bytes, nullptr));
+                        bt.csr = 1;
+                        bt.rows = rows;
+                        SJ_CUDA(cudaMemcpyAsync(bt.pairs, csr_blk[i], bytes, cudaMemcpyDeviceToHost, cx.streams[i]));
+                    } else if (n) {
                         if (o.sort_pairs) sort_pairs_device(staging[i], n, ix.n, cx.streams[i]);
                         bt.pairs = static_cast<uint64_t *>(host_pinned_alloc(n * sizeof(uint64_t), nullptr));
                         SJ_CUDA(cudaMemcpyAsync(bt.pairs, staging[i], n * sizeof(uint64_t), cudaMemcpyDeviceToHost,

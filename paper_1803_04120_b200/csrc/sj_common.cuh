@@ -194,6 +194,10 @@ struct sj_batch {
     uint64_t n = 0;
     uint64_t cap = 0;
     int on_device = 1;
+    // drain_csr: the batch is held in pinned host memory as CSR, one block [row offsets (rows + 1
+    // uint32) | neighbours (n uint32)] at `pairs` (reinterpreted); rows = N of the joined index
+    int csr = 0;
+    uint64_t rows = 0;
 };
 
 struct sj_result {
@@ -284,6 +288,8 @@ void inclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStrea
 // extras.cu
 void sort_pairs_device(uint64_t *pairs, uint64_t n, uint64_t n_points, cudaStream_t s);
 void result_to_csr_impl(const sj_result *r, uint64_t n_points, uint64_t *row_offsets, uint32_t *neighbors);
+void batch_to_csr_device(const uint64_t *pairs, uint64_t n, uint64_t rows, bool sorted, uint32_t *counts,
+                         uint32_t *cursor, uint32_t *dst_offs, uint32_t *dst_nbrs, cudaStream_t s, int nsm);
 void result_fingerprint_impl(const sj_result *r, uint64_t *fp, uint32_t *counts);
 sj_result *brute_force_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &bo,
                             const sj_join_opts &jo);

@@ -36,7 +36,7 @@ class JoinOpts(ctypes.Structure):
     _fields_ = [("unicomp", i32), ("include_self", i32), ("batch_capacity_pairs", u64),
                 ("min_batches", i32), ("n_streams", i32), ("result_on_host", i32),
                 ("query_begin", u64), ("query_end", u64), ("use_masks", i32), ("lanes_per_query", i32),
-                ("dense_cells", i32), ("sort_pairs", i32)]
+                ("dense_cells", i32), ("sort_pairs", i32), ("drain_csr", i32)]
 
 
 class Stats(ctypes.Structure):
@@ -113,6 +113,8 @@ def load_library(path: str = LIB_PATH):
     L.sj_result_info.restype = i32
     L.sj_result_batch.argtypes = [vp, u32, P(vp), P(u64), P(i32)]
     L.sj_result_batch.restype = i32
+    L.sj_result_batch_csr.argtypes = [vp, u32, P(vp), P(vp), P(u64), P(u64)]
+    L.sj_result_batch_csr.restype = i32
     L.sj_result_copy_to_host.argtypes = [vp, vp, u64]
     L.sj_result_copy_to_host.restype = i32
     L.sj_result_to_csr.argtypes = [vp, u64, vp, vp]
@@ -371,6 +373,21 @@ class Result:
         arr.flags.writeable = False
         return arr
 
+    def batch_csr(self, b: int):
+        """sj_result_batch_csr (drain_csr results) -> (row_offsets uint32[N+1], neighbors uint32[n]):
+        zero-copy numpy views of the pinned host block; the neighbours of key i held by batch b are
+        neighbors[row_offsets[i]:row_offsets[i+1]]."""
+        L = load_library()
+        po, pn, rows, n = vp(), vp(), u64(), u64()
+        _check(L.sj_result_batch_csr(self._h, b, ctypes.byref(po), ctypes.byref(pn), ctypes.byref(rows),
+                                     ctypes.byref(n)))
+        offs = np.ctypeslib.as_array((ctypes.c_uint32 * (int(rows.value) + 1)).from_address(po.value))
+        nb = (np.ctypeslib.as_array((ctypes.c_uint32 * int(n.value)).from_address(pn.value)) if n.value
+              else np.empty(0, dtype=np.uint32))
+        offs.flags.writeable = False
+        nb.flags.writeable = False
+        return offs, nb
+
     def batches(self):
         return [self.batch(b) for b in range(self.n_batches)]
 
@@ -433,6 +450,41 @@ def fp64_peak(device: int = 0) -> dict:
     return {"dadd_ops_per_s": a.value, "dmul_ops_per_s": m.value}
 
 
+_ALLOC_CB = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p)
+_RELEASE_CB = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+_hook_refs = None
+
+
+def use_torch_allocator(enable: bool = True):
+    """sj_set_allocator wired to PyTorch's caching allocator: every device allocation of the library
+    (index arrays, result batches, build scratch) then comes from -- and returns to -- torch's pool,
+    so the library and the surrounding PyTorch program share one device-memory budget
+    (north_star: "PyTorch used only for device memory, streams and process groups").  enable=False
+    restores the library's own stream-ordered pool.  Allocations made under one allocator are
+    released by the same one (the library records each allocation's provenance)."""
+    global _hook_refs
+    L = load_library()
+    if not enable:
+        L.sj_set_allocator(None, None, None)
+        _hook_refs = None
+        return
+    import torch
+
+    def _alloc(nbytes, dev, stream, ctx):
+        try:
+            return int(torch.cuda.caching_allocator_alloc(int(nbytes), int(dev), int(stream or 0)))
+        except Exception:
+            return None
+
+    def _release(ptr, ctx):
+        if ptr:
+            torch.cuda.caching_allocator_delete(int(ptr))
+
+    a, r = _ALLOC_CB(_alloc), _RELEASE_CB(_release)
+    _hook_refs = (a, r)                       # the C library keeps raw pointers to these thunks
+    L.sj_set_allocator(ctypes.cast(a, ctypes.c_void_p), ctypes.cast(r, ctypes.c_void_p), None)
+
+
 def trim(device: int = -1):
     """sj_trim: release the library's caches (result batches, build scratch, pinned blocks, pool)."""
     _check(load_library().sj_trim(int(device)))
@@ -446,13 +498,15 @@ def self_join(index: Index, unicomp: bool = True, include_self: bool = True,
               batch_capacity_pairs: Optional[int] = None, min_batches: Optional[int] = None,
               n_streams: Optional[int] = None, result_on_host: bool = False,
               query_begin: int = 0, query_end: int = 0, use_masks: bool = True,
-              lanes_per_query: int = 0, dense_cells: bool = True, sort_pairs: bool = False) -> Result:
+              lanes_per_query: int = 0, dense_cells: bool = True, sort_pairs: bool = False,
+              drain_csr: bool = False) -> Result:
     """sj_self_join over the index; see include/sj.h for the option semantics."""
     L = load_library()
     o = join_opts(unicomp=unicomp, include_self=include_self, batch_capacity_pairs=batch_capacity_pairs,
                   min_batches=min_batches, n_streams=n_streams, result_on_host=result_on_host,
                   query_begin=query_begin, query_end=query_end, use_masks=use_masks,
-                  lanes_per_query=lanes_per_query, dense_cells=dense_cells, sort_pairs=sort_pairs)
+                  lanes_per_query=lanes_per_query, dense_cells=dense_cells, sort_pairs=sort_pairs,
+                  drain_csr=drain_csr)
     h = ctypes.c_void_p()
     _check(L.sj_self_join(index.handle, ctypes.byref(o), ctypes.byref(h)))
     r = Result(h.value)

@@ -557,3 +557,31 @@ def test_imported_index_equals_built(sj, d, n, eps):
             fa, fb, tot = (fa + x) % 2**64, (fb + y) % 2**64, tot + r.n_pairs
             r.free()
         assert (tot, (fa, fb)) == want
+
+
+def test_torch_allocator_hook(sj):
+    """sj_set_allocator wired to torch's caching allocator (sj.use_torch_allocator): the index and
+    the device result batches are carved from torch's pool (torch.cuda.memory_allocated grows by at
+    least the index's SoA copy while they live, and returns when they are freed); S is unchanged."""
+    pts = datagen.uniform(20_000, 3, seed=77)
+    want = oracle.grid_join(pts, 4.0)
+    P = torch.from_numpy(pts).cuda()
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    sj.use_torch_allocator(True)
+    try:
+        idx = sj.build_index(P, 4.0)
+        res = sj.self_join(idx)
+        torch.cuda.synchronize()
+        during = torch.cuda.memory_allocated()
+        assert during - base >= pts.nbytes          # X (8dN) alone lives in torch's pool
+        assert np.array_equal(res.to_numpy(), want)
+        res.free()
+        idx.free()
+        torch.cuda.synchronize()
+        assert torch.cuda.memory_allocated() == base
+    finally:
+        sj.use_torch_allocator(False)
+    # and the library's own pool again
+    idx = sj.build_index(P, 4.0)
+    assert np.array_equal(sj.self_join(idx).to_numpy(), want)
