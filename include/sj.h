@@ -203,6 +203,9 @@ void sj_free_index(sj_index *idx);   /* NULL-safe */
  * *stats are computed from the join's CUDA events on the first call that asks for stats. */
 sj_status sj_result_info(const sj_result *r, uint64_t *n_pairs, uint32_t *n_batches, sj_stats *stats);
 
+/* N of the point set the result's ids refer to (the joined index's N).  Errors: SJ_ERR_STATE (NULL). */
+sj_status sj_result_n_points(const sj_result *r, uint64_t *n_points);
+
 /* Batch b of a result: *pairs points to *n packed uint64 pairs in device memory (*on_device=1,
  * on the index's device) or pinned host memory (*on_device=0); owned by the result. */
 sj_status sj_result_batch(const sj_result *r, uint32_t b, const uint64_t **pairs, uint64_t *n,
@@ -215,6 +218,18 @@ sj_status sj_result_batch(const sj_result *r, uint32_t b, const uint64_t **pairs
  * batch sj_result_batch fails with SJ_ERR_STATE), SJ_ERR_ARG for a bad index. */
 sj_status sj_result_batch_csr(const sj_result *r, uint32_t b, const uint32_t **row_offsets,
                               const uint32_t **neighbors, uint64_t *n_rows, uint64_t *n);
+
+/* DBSCAN (Ester et al. 1996) read off a whole self-join result -- the epsilon-
+ * neighbourhood table N_eps(p) = {q : (p,q) in S}.  core(p) <=> |N_eps(p)| >= min_pts (p counts
+ * itself); clusters = connected components of the core points under S, labelled by their
+ * smallest core id; a non-core point with core neighbours takes the smallest of their labels
+ * (border), else -1 (noise) -- DESIGN.md reading R17.  labels: int32[N] in DEVICE memory on the
+ * result's device (caller-owned), indexed by original id.  Optional outputs: number of clusters,
+ * core points, noise points.  The result must cover the full query range, in pair batches (not
+ * drain_csr); device or pinned-host batches.  Blocks until written.  Errors: SJ_ERR_ARG (NULL
+ * labels, min_pts < 1, partial result, N >= 2^31), SJ_ERR_STATE (CSR batches), SJ_ERR_CUDA. */
+sj_status sj_dbscan(const sj_result *r, uint32_t min_pts, int32_t *labels, uint64_t *n_clusters,
+                    uint64_t *n_core, uint64_t *n_noise);
 
 /* Copy all pairs of a result, batch after batch, into host memory dst (capacity cap pairs).
  * Errors: SJ_ERR_ARG if cap < total. */

@@ -389,6 +389,24 @@ sj_status sj_result_copy_to_host(const sj_result *r, uint64_t *dst, uint64_t cap
     SJ_API_END
 }
 
+sj_status sj_result_n_points(const sj_result *r, uint64_t *n_points)
+{
+    SJ_API_BEGIN
+    if (!r) sj::fail(SJ_ERR_STATE, "result is NULL");
+    if (n_points) *n_points = r->n_points;
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_dbscan(const sj_result *r, uint32_t min_pts, int32_t *labels, uint64_t *n_clusters, uint64_t *n_core,
+                    uint64_t *n_noise)
+{
+    SJ_API_BEGIN
+    sj::dbscan_impl(r, min_pts, labels, n_clusters, n_core, n_noise);
+    return SJ_OK;
+    SJ_API_END
+}
+
 sj_status sj_result_to_csr(const sj_result *r, uint64_t n_points, uint64_t *row_offsets, uint32_t *neighbors)
 {
     SJ_API_BEGIN

@@ -377,6 +377,10 @@ sj_result *brute_force_impl(const double *points, uint64_t n, int d, double eps,
     sj_result *res = new sj_result();
     res->device = bo.device;
     res->n_points = n;
+    res->q0 = 0;
+    res->q1 = n;
+    res->include_self = jo.include_self;
+    res->unicomp = 0;
     try {
         uint64_t cap = std::max<uint64_t>(n * 8, 1024);
         for (int attempt = 0; attempt < 2; ++attempt) {

@@ -320,6 +320,10 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     sj_result *res = new sj_result();
     res->device = idx->device;
     res->n_points = idx->view.n;
+    res->q0 = q0;
+    res->q1 = q1;
+    res->include_self = o.include_self;
+    res->unicomp = o.unicomp;
     sj_stats &stats = res->stats;
     // self pairs of a batch [a, b): written at fixed slots, counted on the host (see JoinArgs::nself)
     auto nself_of = [&](uint64_t a, uint64_t b) -> uint64_t { return o.include_self ? b - a : 0; };

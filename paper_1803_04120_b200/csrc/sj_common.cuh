@@ -212,6 +212,10 @@ struct sj_result {
     sj_stats stats{};
     uint64_t total = 0;
     uint64_t n_points = 0;       // N of the index / point set the pairs' ids refer to
+    // what the pairs cover (sj_dbscan needs the whole self-join): the A-order query range and the
+    // predicate options of the join that produced them
+    uint64_t q0 = 0, q1 = 0;
+    int include_self = 1, unicomp = 1;
 };
 
 namespace sj {
@@ -288,6 +292,8 @@ void inclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, cudaStrea
 // extras.cu
 void sort_pairs_device(uint64_t *pairs, uint64_t n, uint64_t n_points, cudaStream_t s);
 void result_to_csr_impl(const sj_result *r, uint64_t n_points, uint64_t *row_offsets, uint32_t *neighbors);
+void dbscan_impl(const sj_result *r, uint32_t min_pts, int32_t *labels, uint64_t *n_clusters, uint64_t *n_core,
+                 uint64_t *n_noise);
 void batch_to_csr_device(const uint64_t *pairs, uint64_t n, uint64_t rows, bool sorted, uint32_t *counts,
                          uint32_t *cursor, uint32_t *dst_offs, uint32_t *dst_nbrs, cudaStream_t s, int nsm);
 void result_fingerprint_impl(const sj_result *r, uint64_t *fp, uint32_t *counts);

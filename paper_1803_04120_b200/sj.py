@@ -115,6 +115,10 @@ def load_library(path: str = LIB_PATH):
     L.sj_result_batch.restype = i32
     L.sj_result_batch_csr.argtypes = [vp, u32, P(vp), P(vp), P(u64), P(u64)]
     L.sj_result_batch_csr.restype = i32
+    L.sj_dbscan.argtypes = [vp, u32, vp, P(u64), P(u64), P(u64)]
+    L.sj_dbscan.restype = i32
+    L.sj_result_n_points.argtypes = [vp, P(u64)]
+    L.sj_result_n_points.restype = i32
     L.sj_result_copy_to_host.argtypes = [vp, vp, u64]
     L.sj_result_copy_to_host.restype = i32
     L.sj_result_to_csr.argtypes = [vp, u64, vp, vp]
@@ -420,6 +424,23 @@ class Result:
             cnt = torch.empty(int(n_points), dtype=torch.uint32, device=f"cuda:{dev}")
         _check(load_library().sj_result_fingerprint(self._h, fp, ctypes.c_void_p(cnt.data_ptr()) if counts else None))
         return (int(fp[0]), int(fp[1]), cnt) if counts else (int(fp[0]), int(fp[1]))
+
+    def dbscan(self, min_pts: int):
+        """sj_dbscan -> (labels torch.int32[N] on the device, {clusters, core, noise}): DBSCAN read off
+        this (whole) self-join result; see include/sj.h for the label conventions."""
+        import torch
+        dev = self.device if self.device is not None else 0
+        npts = self._n_points()
+        labels = torch.empty(max(npts, 1), dtype=torch.int32, device=f"cuda:{dev}")
+        nc, ncore, nn = u64(), u64(), u64()
+        _check(load_library().sj_dbscan(self._h, int(min_pts), ctypes.c_void_p(labels.data_ptr()), ctypes.byref(nc),
+                                        ctypes.byref(ncore), ctypes.byref(nn)))
+        return labels[:npts], {"clusters": int(nc.value), "core": int(ncore.value), "noise": int(nn.value)}
+
+    def _n_points(self) -> int:
+        n = u64()
+        _check(load_library().sj_result_n_points(self._h, ctypes.byref(n)))
+        return int(n.value)
 
     def free(self, stream=None):
         """Release the result; its device buffers are reused only after the work queued on

@@ -477,3 +477,68 @@ def test_generators_deterministic():
     assert np.array_equal(a, b) and a.min() >= 0 and a.max() < 100
     s = datagen.skewed(20000, 3, seed=5)
     assert s.shape == (20000, 3) and s.min() >= 0 and s.max() <= 100
+
+
+# ------------------------------------------------------------------ f4: DBSCAN on the join (R17)
+def _sk_dbscan(pairs, n, min_pts):
+    """scikit-learn's DBSCAN (an independent implementation) on the same eps-neighbourhood graph:
+    a sparse precomputed 'distance' matrix whose stored entries are exactly the pairs of S."""
+    from scipy.sparse import csr_matrix
+    from sklearn.cluster import DBSCAN
+    p = (pairs >> np.uint64(32)).astype(np.int64)
+    q = (pairs & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    G = csr_matrix((np.full(len(p), 0.1), (p, q)), shape=(n, n))
+    m = DBSCAN(eps=0.5, min_samples=min_pts, metric="precomputed").fit(G)
+    core = np.zeros(n, bool)
+    core[m.core_sample_indices_] = True
+    return m.labels_, core
+
+
+@pytest.mark.parametrize("seed,d,n,eps,min_pts", [(1, 2, 1500, 0.35, 4), (2, 2, 2000, 0.5, 8),
+                                                  (3, 3, 1200, 0.8, 5), (4, 2, 800, 2.0, 3),
+                                                  (5, 4, 1000, 1.2, 6)])
+def test_dbscan_oracle_matches_sklearn(seed, d, n, eps, min_pts):
+    """oracle.dbscan against scikit-learn on the same neighbourhood table: the core set and the
+    noise set exactly, the core partition up to relabelling; every border label is the smallest
+    label among the point's core neighbours (reading R17: the unique choice)."""
+    from oracle.dbscan import dbscan_from_pairs
+    pts = datagen.clustered_small(n, d, seed=seed) if seed % 2 else datagen.uniform(n, d, seed=seed, hi=12.0)
+    pairs = oracle.brute_force(pts, eps)
+    lab = dbscan_from_pairs(pairs, n, min_pts)
+    sk_lab, sk_core = _sk_dbscan(pairs, n, min_pts)
+    cnt = np.bincount((pairs >> np.uint64(32)).astype(np.int64), minlength=n)
+    core = cnt >= min_pts
+    assert np.array_equal(core, sk_core)
+    assert np.array_equal(lab == -1, sk_lab == -1)                   # noise: no core neighbour
+    # core partition identical up to relabelling (a bijection between label sets on core points)
+    pairs_cl = set(zip(lab[core].tolist(), sk_lab[core].tolist()))
+    assert len(pairs_cl) == len(set(lab[core].tolist())) == len(set(sk_lab[core].tolist()))
+    # labels are the smallest core id of each cluster
+    for c in set(lab[core].tolist()):
+        assert c == np.flatnonzero(core & (lab == c)).min()
+    # border: smallest label among core neighbours
+    p = (pairs >> np.uint64(32)).astype(np.int64)
+    q = (pairs & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    for i in np.flatnonzero(~core & (lab != -1)):
+        nb = q[(p == i)]
+        assert lab[i] == min(lab[j] for j in nb if core[j])
+    assert np.any(core) and len(set(lab[core].tolist())) >= 1
+
+
+def test_dbscan_oracle_fixture():
+    """Hand-built, on a line (y = 0), eps = 1 (ties included), min_pts = 4: two clusters of five
+    points 0.25 apart, a bridge point at x = 2 seeing 1.0, 2.0 and 3.0 only (3 < 4: not core, but a
+    border of BOTH clusters -> the smaller label, reading R17), and an isolated point (noise).
+    Neighbourhood sizes by hand: [5,5,5,5,6, 3, 6,5,5,5,5, 1]."""
+    from oracle.dbscan import dbscan_from_pairs
+    xs = [0.0, 0.25, 0.5, 0.75, 1.0, 2.0, 3.0, 3.25, 3.5, 3.75, 4.0, 10.0]
+    pts = np.array([[x, 0.0] for x in xs])
+    pairs = oracle.brute_force(pts, 1.0)
+    cnt = np.bincount((pairs >> np.uint64(32)).astype(np.int64), minlength=len(pts))
+    assert list(cnt) == [5, 5, 5, 5, 6, 3, 6, 5, 5, 5, 5, 1]
+    lab = dbscan_from_pairs(pairs, len(pts), 4)
+    assert list(lab) == [0, 0, 0, 0, 0, 0, 6, 6, 6, 6, 6, -1]
+    # min_pts = 6: only 1.0 and 3.0 are core, each its own cluster; the rest are their borders
+    # (the bridge takes the smaller label) or noise
+    lab6 = dbscan_from_pairs(pairs, len(pts), 6)
+    assert list(lab6) == [4, 4, 4, 4, 4, 4, 6, 6, 6, 6, 6, -1]
