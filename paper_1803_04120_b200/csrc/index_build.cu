@@ -417,16 +417,36 @@ k_heads(const uint64_t *__restrict__ keys, uint32_t n, uint32_t *__restrict__ fl
     flags[k] = (k == 0 || keys[k] != keys[k - 1]) ? 1u : 0u;
 }
 
-// Occupancy bitmap over the top-(k+1) prefixes, stored DILATED along dimension d-k-1: a cell with
-// top-(k+1) prefix q sets bits q-1, q, q+1, so the refine asks "is any of the three windows
-// c_{d-k-1} + {-1,0,1} occupied?" with one bit test.  (q-1 and q+1 stay inside q's top-k prefix:
-// c is in [1, |g|-2] and the pad cells are empty.)
-__device__ __forceinline__ void occ_set_window(uint32_t *occ, uint64_t q)
+// Occupancy bitmaps over (top-k prefix, c_lo), lo = d-k-1 (occ) / d-k-2 (occ2), stored DILATED along
+// c_lo: a cell sets the bits of c_lo - 1, c_lo, c_lo + 1 (index(c) +- the stride of c_lo, see
+// apply_dir_geometry), so the refine asks "is any cell of that prefix in the window c_lo + {-1,0,1}?"
+// with one bit test -- and, the lowest top dimension being the fastest index, for the three top
+// offsets that differ only in c_{d-k} with one load.  (c_lo is in [1, |g|-2]: the window never
+// leaves the prefix; the pad cells are empty.)
+template <int D>
+__device__ __forceinline__ void occ_set_cell(const DevIndex &ix, const uint64_t (&c)[D], uint32_t *occ, uint32_t *occ2)
 {
-    const uint64_t a = q - 1ull;
-    const uint32_t sh = (uint32_t)(a & 31u);
-    atomicOr(occ + (a >> 5), 7u << sh);
-    if (sh > 29) atomicOr(occ + (a >> 5) + 1, 7u >> (32 - sh));
+    const int L = D - ix.dir_k;
+    uint64_t q = 0, q2 = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        q += c[j] * ix.occ_mul[j];
+        q2 += c[j] * ix.occ2_mul[j];
+    }
+    uint64_t st = 0, st2 = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        if (j == L - 1) st = ix.occ_mul[j];
+        if (j == L - 2) st2 = ix.occ2_mul[j];
+    }
+    atomicOr(occ + ((q - st) >> 5), 1u << ((q - st) & 31));
+    atomicOr(occ + (q >> 5), 1u << (q & 31));
+    atomicOr(occ + ((q + st) >> 5), 1u << ((q + st) & 31));
+    if (occ2) {
+        atomicOr(occ2 + ((q2 - st2) >> 5), 1u << ((q2 - st2) & 31));
+        atomicOr(occ2 + (q2 >> 5), 1u << (q2 & 31));
+        atomicOr(occ2 + ((q2 + st2) >> 5), 1u << ((q2 + st2) & 31));
+    }
 }
 
 // pcell holds the inclusive scan of head flags on entry (1-based cell number) and the
@@ -485,19 +505,7 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
 #pragma unroll
         for (int j = 0; j < D; ++j) prefix += c[j] * ix.pstride[j];
         if (dirhist) atomicAdd(dirhist + prefix, 1u);
-        if (occ) {
-            const int jo = D - ix.dir_k - 1;             // dimension d-k-1 (0-based), >= 0 when occ exists
-            uint64_t cl = c[0];
-#pragma unroll
-            for (int j = 1; j < D; ++j) if (j == jo) cl = c[j];
-            occ_set_window(occ, prefix * ix.occ_cpd + cl);
-            if (ix.occ2) {
-                uint64_t c2 = c[0];
-#pragma unroll
-                for (int j = 1; j < D; ++j) if (j == jo - 1) c2 = c[j];
-                occ_set_window(const_cast<uint32_t *>(ix.occ2), prefix * ix.occ2_cpd + c2);
-            }
-        }
+        if (occ) occ_set_cell<D>(ix, c, occ, const_cast<uint32_t *>(ix.occ2));
     }
     if (k == n - 1) {
         G[h + 1] = n;
@@ -667,13 +675,13 @@ DirPlan plan_dir(const sj_index_view &v)
             dp.occ = true;
             dp.occ_cpd = v.cpd[d - dp.k - 1];
             dp.occ_div = dp.div / dp.occ_cpd;
-            dp.occ_words = (size_t)((P1 + 31) / 32);
+            dp.occ_words = (size_t)((P1 + 31) / 32) + 2;     // +2: the refine's 64-bit window loads
             if (d - dp.k >= 2) {
                 const unsigned __int128 P2 = P * v.cpd[d - dp.k - 2];
                 if (P2 <= (unsigned __int128)64 * std::max<uint64_t>(n, 1ull << 16)) {
                     dp.occ2 = true;
                     dp.occ2_cpd = v.cpd[d - dp.k - 2];
-                    dp.occ2_words = (size_t)((P2 + 31) / 32);
+                    dp.occ2_words = (size_t)((P2 + 31) / 32) + 2;
                 }
             }
         }
@@ -698,10 +706,15 @@ void apply_dir_geometry(DevIndex &ix, const sj_index_view &v, const DirPlan &dp)
     ix.occ_div = dp.occ ? dp.occ_div : 0;
     ix.occ_cpd = dp.occ ? dp.occ_cpd : 0;
     ix.occ2_cpd = dp.occ2 ? dp.occ2_cpd : 0;
+    // bitmap index = c_L + |g_L| * (c_lo + |g_lo| * (prefix - c_L) / |g_L|), L = d-k (the lowest top
+    // dimension), lo = L-1 (occ) or L-2 (occ2): the three top offsets that differ only in c_L are
+    // ADJACENT bits, so the refine tests them with one load (DESIGN.md §6 "grouped occupancy")
+    const int Lt = d - dp.k;
     for (int j = 0; j < SJ_MAX_DIM; ++j) {
-        const bool top = j < d && j >= d - dp.k;
-        ix.occ_mul[j] = top ? ix.pstride[j] * ix.occ_cpd : (dp.occ && j == d - dp.k - 1 ? 1 : 0);
-        ix.occ2_mul[j] = top ? ix.pstride[j] * ix.occ2_cpd : (dp.occ2 && j == d - dp.k - 2 ? 1 : 0);
+        const bool top = j < d && j >= Lt;
+        const uint64_t cL = dp.k >= 1 ? v.cpd[Lt] : 1;
+        ix.occ_mul[j] = !dp.occ ? 0 : (j == Lt ? 1 : (top ? ix.pstride[j] * ix.occ_cpd : (j == Lt - 1 ? cL : 0)));
+        ix.occ2_mul[j] = !dp.occ2 ? 0 : (j == Lt ? 1 : (top ? ix.pstride[j] * ix.occ2_cpd : (j == Lt - 2 ? cL : 0)));
     }
     // key -> coordinates by double reciprocals when every quotient < 2^50 and keys < 2^63
     bool fast = v.key_bits <= 63;
@@ -753,30 +766,24 @@ k_dir_hist(const uint64_t *__restrict__ B, const uint32_t *__restrict__ nG, uint
     atomicAdd(hist + div_small_quot(B[h], div, inv), 1u);
 }
 
-// occupancy bits of the top-(k+1) prefixes: bit q = key / occ_div
+// occupancy bits of an imported index (the build sets them in its compaction): coordinates
+// decoded from each cell's key, then occ_set_cell
+template <int D>
 __global__ void __launch_bounds__(kThreads)
-k_occ_bits(const uint64_t *__restrict__ B, const uint32_t *__restrict__ nG, uint64_t div, double inv,
-           uint32_t *__restrict__ occ)
+k_occ_import(const DevIndex ix, const uint64_t *__restrict__ B, const uint32_t *__restrict__ nG, uint32_t *occ,
+             uint32_t *occ2)
 {
     const uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (h >= *nG) return;
-    occ_set_window(occ, div_small_quot(B[h], div, inv));
-}
-
-// second bitmap: bit prefix * |g_{d-k-2}| + c_{d-k-2}, c = (key / stride_{d-k-2}) mod |g_{d-k-2}|
-// (the low part key - prefix * div divided by stride_{d-k-2} still carries c_{d-k-1} * |g_{d-k-2}|:
-// the mod removes it)
-__global__ void __launch_bounds__(kThreads)
-k_occ2_bits(const uint64_t *__restrict__ B, const uint32_t *__restrict__ nG, uint64_t div, double inv,
-            uint64_t st2, double inv2, uint64_t cpd2, uint32_t *__restrict__ occ2)
-{
-    const uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (h >= *nG) return;
-    const uint64_t key = B[h];
-    const uint64_t prefix = div_small_quot(key, div, inv);
-    const uint64_t q2 = div_small_quot(key - prefix * div, st2, inv2);
-    const uint64_t c2 = q2 % cpd2;
-    occ_set_window(occ2, prefix * cpd2 + c2);
+    uint64_t c[D];
+    uint64_t rem = B[h];
+#pragma unroll
+    for (int j = D - 1; j >= 1; --j) {
+        c[j] = rem / ix.strides[j];
+        rem -= c[j] * ix.strides[j];
+    }
+    c[0] = rem;
+    occ_set_cell<D>(ix, c, occ, occ2);
 }
 
 // dense tasks, in A-order: cells with >= T points are cut into <= 32-query tasks; count, exclusive
@@ -1390,14 +1397,14 @@ sj_index *import_index_impl(const sj_index_view &src, int device, bool borrow)
         k_dir_hist<<<gN, kThreads, 0, s>>>(B, aux, dp.div, 1.0 / (double)dp.div, hist.p);
         SJ_LAUNCHED();
         if (idx->dev.occ) {
-            k_occ_bits<<<gN, kThreads, 0, s>>>(B, aux, dp.occ_div, 1.0 / (double)dp.occ_div,
-                                               const_cast<uint32_t *>(idx->dev.occ));
-            SJ_LAUNCHED();
-        }
-        if (idx->dev.occ2) {
-            const uint64_t st2 = v.strides[d - dp.k - 2];
-            k_occ2_bits<<<gN, kThreads, 0, s>>>(B, aux, dp.div, 1.0 / (double)dp.div, st2, 1.0 / (double)st2,
-                                                dp.occ2_cpd, const_cast<uint32_t *>(idx->dev.occ2));
+            uint32_t *o1 = const_cast<uint32_t *>(idx->dev.occ), *o2 = const_cast<uint32_t *>(idx->dev.occ2);
+            switch (d) {
+            case 2: k_occ_import<2><<<gN, kThreads, 0, s>>>(idx->dev, B, aux, o1, o2); break;
+            case 3: k_occ_import<3><<<gN, kThreads, 0, s>>>(idx->dev, B, aux, o1, o2); break;
+            case 4: k_occ_import<4><<<gN, kThreads, 0, s>>>(idx->dev, B, aux, o1, o2); break;
+            case 5: k_occ_import<5><<<gN, kThreads, 0, s>>>(idx->dev, B, aux, o1, o2); break;
+            default: k_occ_import<6><<<gN, kThreads, 0, s>>>(idx->dev, B, aux, o1, o2); break;
+            }
             SJ_LAUNCHED();
         }
         uint32_t h_aux[4];

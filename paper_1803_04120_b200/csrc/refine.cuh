@@ -392,6 +392,13 @@ struct TopTable {
     uint32_t bits[kMaxTop];  // [0:6) dims at -1, [8:14) dims at +1, [16:22) one-hot highest moved dim
 };
 
+__device__ __forceinline__ uint32_t kPow3i(int e)
+{
+    uint32_t r = 1;
+    for (int i = 0; i < e; ++i) r *= 3u;
+    return r;
+}
+
 template <int D>
 __device__ __forceinline__ void build_top_table(const DevIndex &ix, TopTable &tt)
 {
@@ -407,8 +414,16 @@ __device__ __forceinline__ void build_top_table(const DevIndex &ix, TopTable &tt
         }
         tt.dp[t] = dp;
         tt.dk[t] = dp * (int64_t)ix.dir_div;
-        tt.dq[t] = dp * (int64_t)ix.occ_cpd;
-        tt.dq2[t] = dp * (int64_t)ix.occ2_cpd;
+        // bitmap index deltas in the grouped layout (apply_dir_geometry): the lowest top dim moves
+        // the index by 1, the others by pstride_i * |g_lo|
+        int64_t dq = 0, dq2 = 0;
+        for (int i = L; i < D; ++i) {
+            const int dl = (int)((t / kPow3i(i - L)) % 3u) - 1;
+            dq += dl * (int64_t)ix.occ_mul[i];
+            dq2 += dl * (int64_t)ix.occ2_mul[i];
+        }
+        tt.dq[t] = dq;
+        tt.dq2[t] = dq2;
         tt.bits[t] = neg | (pos << 8) | (top << 16);
     }
 }
@@ -471,6 +486,17 @@ __device__ __forceinline__ void test_low_cell(const DevIndex &ix, const JoinArgs
 // One block of search_cell_scan_sparse: the 2 * 3^JT top offsets whose highest moved top dimension is
 // L + JT (that dimension moved by -1 or +1, the top dimensions below it by -1/0/+1, the ones above
 // it unmoved).  JT is a compile-time constant so the filter loop has exactly the block's offsets.
+// Three bits of a bitmap starting at bit index b0 (the window c_L - 1 .. c_L + 1 of the grouped
+// layout): one 64-bit load (a second only when the three straddle a 64-bit word, 3 in 64)
+__device__ __forceinline__ uint32_t bits3(const uint32_t *bm, uint64_t b0)
+{
+    const uint64_t *w = reinterpret_cast<const uint64_t *>(bm) + (b0 >> 6);
+    const uint32_t sh = (uint32_t)(b0 & 63u);
+    uint64_t v = __ldg(w) >> sh;
+    if (sh > 61) v |= __ldg(w + 1) << (64u - sh);
+    return (uint32_t)v & 7u;
+}
+
 template <int D, int MODE, bool UNICOMP, int JT>
 __device__ __forceinline__ void sparse_block(const DevIndex &ix, const JoinArgs &ja, QueryState<D> &q, uint64_t key,
                                              uint32_t bad, const TopTable &tt, uint64_t ph, uint64_t qc,
@@ -479,19 +505,39 @@ __device__ __forceinline__ void sparse_block(const DevIndex &ix, const JoinArgs 
     constexpr uint32_t p3 = JT == 2 ? 9u : (JT == 1 ? 3u : 1u);   // 3^JT
     constexpr uint32_t nb = 2u * p3;
     const uint32_t tbase = (pow3k - 3u * p3) / 2u;               // digits above JT = "0 move"
+    // bit i of live <-> offset t(i) = tbase + (i >> 1) + (i & 1 ? 2 p3 : 0).  The offsets come in
+    // groups of three consecutive t (the lowest top dim at -1, 0, +1: adjacent bits of both bitmaps
+    // in the grouped layout), so each group costs ONE window load per bitmap instead of three.
     uint32_t live = 0;
+    if constexpr (JT == 0) {
+        // the pair c_L - 1, c_L + 1 (t = tbase, tbase + 2): one window of the home group
+        const uint32_t tm = tbase + 1u;                          // the home offset (all top dims 0)
+        uint32_t w = bits3(ix.occ, qc + (uint64_t)tt.dq[tm] - 1ull);
+        if (ix.occ2) w &= bits3(ix.occ2, qc2 + (uint64_t)tt.dq2[tm] - 1ull);
+        if ((w & 1u) && !(tt.bits[tbase] & bad)) live |= 1u;
+        if ((w & 4u) && !(tt.bits[tbase + 2u] & bad)) live |= 2u;
+    } else {
 #pragma unroll
-    for (uint32_t i = 0; i < nb; ++i) {
-        const uint32_t t = tbase + (i >> 1) + ((i & 1u) ? 2u * p3 : 0u);
-        if (!(tt.bits[t] & bad)) {
-            // both bitmaps' loads are issued together (no dependent second round)
-            const uint64_t qb = qc + (uint64_t)tt.dq[t];
-            uint32_t ok = __ldg(ix.occ + (qb >> 5)) >> (qb & 31);
-            if (ix.occ2) {
-                const uint64_t qb2 = qc2 + (uint64_t)tt.dq2[t];
-                ok &= __ldg(ix.occ2 + (qb2 >> 5)) >> (qb2 & 31);
+        for (uint32_t g = 0; g < nb / 3u; ++g) {
+            // group g: members i = 3g .. 3g+2 are consecutive t (i>>1 and the +2p3 half alternate, so
+            // enumerate groups in t order instead): t0 = first t of the group
+            const uint32_t half = g / (p3 / 3u), gi = g % (p3 / 3u);
+            const uint32_t t0 = tbase + half * 2u * p3 + 3u * gi;
+            const uint32_t tm = t0 + 1u;
+            uint32_t ok3 = 0;
+#pragma unroll
+            for (uint32_t m = 0; m < 3u; ++m) ok3 |= (tt.bits[t0 + m] & bad) ? 0u : (1u << m);
+            if (!ok3) continue;
+            uint32_t w = bits3(ix.occ, qc + (uint64_t)tt.dq[tm] - 1ull);
+            if (ix.occ2) w &= bits3(ix.occ2, qc2 + (uint64_t)tt.dq2[tm] - 1ull);
+            w &= ok3;
+            // member m of the group is offset t0 + m -> live bit index i with t(i) = t0 + m
+#pragma unroll
+            for (uint32_t m = 0; m < 3u; ++m) {
+                const uint32_t t = t0 + m - tbase;               // position in the block
+                const uint32_t i = t < p3 ? 2u * t : 2u * (t - 2u * p3) + 1u;
+                if ((w >> m) & 1u) live |= 1u << i;
             }
-            if (ok & 1u) live |= 1u << i;
         }
     }
     const int dim = L + JT;
