@@ -76,12 +76,22 @@ k_db_union(const uint64_t *__restrict__ pairs, uint64_t n, uint32_t *parent)
     }
 }
 
+// Every core point's entry becomes its root.  The walk is read-only: the only write to parent[i]
+// is thread i's own (a path-halving write by another thread could store a non-root ancestor over
+// it after thread i wrote the root).
 __global__ void __launch_bounds__(256)
 k_db_flatten(uint32_t *parent, uint32_t n)
 {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || parent[i] == 0xffffffffu) return;
-    parent[i] = db_find(parent, i);
+    if (i >= n) return;
+    uint32_t x = __ldcg(parent + i);
+    if (x == 0xffffffffu) return;
+    uint32_t p = __ldcg(parent + x);
+    while (p != x) {
+        x = p;
+        p = __ldcg(parent + x);
+    }
+    parent[i] = x;
 }
 
 __global__ void __launch_bounds__(256)

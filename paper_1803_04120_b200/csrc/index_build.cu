@@ -77,6 +77,7 @@ constexpr size_t kGeomOffset = 4 * 256 * (2 * SJ_MAX_DIM + 1) * sizeof(unsigned 
 constexpr size_t kEstOffset = kGeomOffset + 4096;          // pinned staging of aux + estimate buckets
 constexpr size_t kMaxEstBuckets = 1100;
 constexpr size_t kAuxEstOffset = 64;                       // estimate buckets, bytes after aux
+constexpr int kAuxWords = 8;                               // aux: |G|, tasks, populous, overflow, masks-trivial
 constexpr size_t kBuildSlotBytes = kEstOffset + kAuxEstOffset + 8 * kMaxEstBuckets;
 
 // prefix-bucket items travel packed as ONE 64-bit word ((key - prefix*div) << idb | id): possible when
@@ -786,6 +787,23 @@ k_occ_import(const DevIndex ix, const uint64_t *__restrict__ B, const uint32_t *
     occ_set_cell<D>(ix, c, occ, occ2);
 }
 
+// Are the masks M_j trivial (every coordinate c in [1, |g_j|-2] occupied, in every dimension)?  Then
+// they exclude no adjacent cell (uniform data) and the refine need not consult them (*flag = 1).
+__global__ void __launch_bounds__(256)
+k_masks_full(const DevIndex ix, uint32_t *__restrict__ flag)
+{
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    for (int j = 0; j < ix.d; ++j) {
+        const uint64_t lo = ix.mask_off[j] + 1, hi = ix.mask_off[j] + ix.cpd[j] - 2;   // inclusive
+        for (uint64_t b = lo + threadIdx.x; b <= hi; b += blockDim.x)
+            if (!((__ldcg(ix.masks + (b >> 5)) >> (b & 31)) & 1u)) s_bad = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *flag = s_bad ? 0u : 1u;
+}
+
 // dense tasks, in A-order: cells with >= T points are cut into <= 32-query tasks; count, exclusive
 // scan (over the N upper bound, zero past |G|), fill
 __global__ void __launch_bounds__(kThreads)
@@ -817,22 +835,33 @@ k_dense_fill(const uint32_t *__restrict__ G, const uint32_t *__restrict__ nG, ui
 // one warp each in k_refine_dense) are built in A-order when the compaction saw populous cells (the
 // import path, which has no such count, always builds them).
 constexpr uint32_t kDenseT = 16;
+void launch_masks_full(const DevIndex &ix, uint32_t *flag, cudaStream_t s)
+{
+    k_masks_full<<<1, 256, 0, s>>>(ix, flag);
+    SJ_LAUNCHED();
+}
+
 void finish_aux(sj_index *idx, cudaStream_t s, uint32_t *aux, const DirPlan &dp, const uint32_t *dirhist,
-                bool force_dense, uint32_t *h_aux, void *h_stage = nullptr, size_t stage_bytes = 0)
+                bool force_dense, uint32_t *h_aux, void *h_stage = nullptr, size_t stage_bytes = 0,
+                bool check_masks = true)
 {
     sj_index_view &v = idx->view;
     DevIndex &ix = idx->dev;
     if (dirhist) exclusive_scan_u32(dirhist, const_cast<uint32_t *>(ix.dir), (uint64_t)dp.P + 1, s);
+    // aux[4]: the masks exclude nothing (the build checks on its side stream; the import here)
+    if (check_masks && ix.masks && v.mask_offsets[v.d] <= 32ull * kSmemMaskWords) launch_masks_full(ix, aux + 4, s);
     if (h_stage) {
         // one copy into pinned memory: aux and whatever the caller placed after it (the build's
         // estimate buckets)
         SJ_CUDA(cudaMemcpyAsync(h_stage, aux, stage_bytes, cudaMemcpyDeviceToHost, s));
         SJ_CUDA(cudaStreamSynchronize(s));
-        std::memcpy(h_aux, h_stage, 4 * sizeof(uint32_t));
+        std::memcpy(h_aux, h_stage, kAuxWords * sizeof(uint32_t));
     } else {
-        SJ_CUDA(cudaMemcpyAsync(h_aux, aux, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        SJ_CUDA(cudaMemcpyAsync(h_aux, aux, kAuxWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         SJ_CUDA(cudaStreamSynchronize(s));
     }
+    // trivial masks: the kernels skip them (the view keeps them: S never depends on masks)
+    if (h_aux[4]) ix.masks = nullptr;
     uint32_t *tasks = nullptr;
     uint32_t ntasks = 0;
     if (!h_aux[3] && (h_aux[2] > 0 || force_dense)) {
@@ -902,7 +931,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
     // the build runs on the caller's stream, or on a pooled library stream; the pooled context also
     // lends its pinned slot memory and an event (device geometry read-back)
     static_assert(sizeof(DevGeom) <= 4096, "DevGeom fits its slot");
-    CtxGuard cg{acquire_ctx(o.device, 2, 2, kBuildSlotBytes)};   // stream 1: the geometry read-back
+    CtxGuard cg{acquire_ctx(o.device, 2, 4, kBuildSlotBytes)};   // stream 1: geometry read-back, mask check
     cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : cg.c->streams[0];
     if (!o.stream) {
         // NULL = the library stream, ordered after the work already queued on the legacy default
@@ -927,7 +956,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
     sj_index *idx = new sj_index();
     idx->device = o.device;
     auto own = [&](void *p) { idx->bufs[idx->nbufs++] = p; return p; };
-    uint32_t h_aux[4] = {0, 0, 0, 0};
+    uint32_t h_aux[kAuxWords] = {0, 0, 0, 0, 0, 0, 0, 0};
     const int nsm = device_sm_count(o.device);
     bool l2p = false;              // the input is marked L2-persisting on s (see below)
     try {
@@ -1057,6 +1086,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ba.bhist = bhist;
         launch(d, 1, grid, s, ix, ba);
         ev.rec(3, s);
+        SJ_CUDA(cudaEventRecord(cg.c->events[2], s));          // keys (and the small masks) done
         tr.dev("keys", s);
         tr.mark("minmax/geometry/keys enqueued");
         SJ_CUDA(cudaEventSynchronize(cg.c->events[0]));
@@ -1143,6 +1173,17 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
                 ba.masks = masks;
                 launch(d, 3, grid, s, ix, ba);
             }
+        }
+        // are the masks trivial (finish_aux reads aux[4])?  A one-CTA check on the side stream,
+        // off the critical path; s joins it before its final copy
+        bool mask_check = false;
+        if (masks && masks == small_masks) {
+            DevIndex mx = ix;
+            mx.masks = masks;
+            SJ_CUDA(cudaStreamWaitEvent(s_side, cg.c->events[2], 0));
+            launch_masks_full(mx, aux + 4, s_side);
+            SJ_CUDA(cudaEventRecord(cg.c->events[3], s_side));
+            mask_check = true;
         }
         tr.mark("geometry + allocs");
         idx->view = v;
@@ -1263,8 +1304,9 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
             launch_estimate(px, o.device, jo, 0, n, es_spec, dbk, s);
             tr.dev("speculative estimate", s);
         }
+        if (mask_check) SJ_CUDA(cudaStreamWaitEvent(s, cg.c->events[3], 0));
         finish_aux(idx, s, aux, dp, nullptr, false, h_aux, h_stage,
-                   kAuxEstOffset + (spec ? 8 * es_spec.nbk : 0));     // the build's late host sync
+                   kAuxEstOffset + (spec ? 8 * es_spec.nbk : 0), !mask_check);     // the build's late host sync
         if (l2p) l2_persist_end(o.device);   // s is synced: demote the input's persisting lines
         scratch.leave_zero = s_h;            // the histogram region is zero again (see BuildScratch)
         cg.idle = true;                      // s synced by finish_aux, the side stream by the geometry event
@@ -1387,8 +1429,8 @@ sj_index *import_index_impl(const sj_index_view &src, int device, bool borrow)
         idx->view = v;
         idx->dev = ix;
         alloc_dir(idx, dp, s);
-        uint32_t *aux = static_cast<uint32_t *>(own(4 * 4));
-        const uint32_t hn[4] = {(uint32_t)nG, 0u, 0u, 0u};
+        uint32_t *aux = static_cast<uint32_t *>(own(4 * kAuxWords));
+        const uint32_t hn[kAuxWords] = {(uint32_t)nG, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
         SJ_CUDA(cudaMemcpyAsync(aux, hn, sizeof(hn), cudaMemcpyHostToDevice, s));
         // directory histogram and occupancy bits from B (the build fuses these into its compaction)
         Scratch<uint32_t> hist((size_t)dp.P + 1, s);
@@ -1407,7 +1449,7 @@ sj_index *import_index_impl(const sj_index_view &src, int device, bool borrow)
             }
             SJ_LAUNCHED();
         }
-        uint32_t h_aux[4];
+        uint32_t h_aux[kAuxWords];
         finish_aux(idx, s, aux, dp, hist.p, true, h_aux);
     } catch (...) {
         cudaStreamDestroy(s);

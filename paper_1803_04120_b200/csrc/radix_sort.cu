@@ -106,69 +106,91 @@ k_radix_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ v
     }
 }
 
-// ---------------------------------------------------------------- u32 scans (3-phase)
+// ---------------------------------------------------------------- u32 scans (single pass)
 constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 4;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-__global__ void __launch_bounds__(kScanThreads)
-k_scan_reduce(const uint32_t *__restrict__ in, uint64_t n, uint32_t *__restrict__ block_sums)
-{
-    __shared__ uint32_t s_warp[32];
-    const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
-    uint32_t acc = 0;
-#pragma unroll
-    for (int r = 0; r < kScanItems; ++r) {
-        uint64_t i = base + (uint64_t)r * kScanThreads + threadIdx.x;
-        if (i < n) acc += in[i];
-    }
-    uint32_t tot;
-    block_exclusive_scan(acc, s_warp, &tot);
-    if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
-}
-
+// Single-pass scan with decoupled look-back (one launch instead of reduce + apply): CTA c handles
+// tiles c, c + grid, ... in order (grid <= resident CTAs, so every tile a look-back waits for is
+// being processed by a running CTA); tile t publishes its aggregate, looks back over the tiles
+// before it (a warp reads 32 statuses at a time, stopping at the first inclusive prefix), then
+// publishes its inclusive prefix.  status[t] = flag << 32 | value (flag 1: aggregate, 2:
+// inclusive prefix; the array is zeroed first).
 template <bool INCLUSIVE>
-__global__ void __launch_bounds__(kScanThreads)
-k_scan_apply(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, uint64_t n,
-             const uint32_t *__restrict__ block_off, uint32_t *__restrict__ out2, uint32_t *__restrict__ zero_in)
+__global__ void __launch_bounds__(kScanThreads, 2)
+k_scan_1pass(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, uint64_t n, uint64_t ntiles,
+             unsigned long long *status, uint32_t *__restrict__ out2, uint32_t *__restrict__ zero_in)
 {
     __shared__ uint32_t s_warp[32];
-    // each thread owns kScanItems consecutive items
-    const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
-    uint32_t v[kScanItems];
-    uint32_t acc = 0;
+    __shared__ uint32_t s_excl;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t base = t * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+        uint32_t v[kScanItems];
+        uint32_t acc = 0;
+        if (base + kScanItems <= n && !(reinterpret_cast<uintptr_t>(in + base) & 15u)) {
+            const uint4 q = *reinterpret_cast<const uint4 *>(in + base);
+            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        } else {
 #pragma unroll
-    for (int r = 0; r < kScanItems; ++r) {
-        uint64_t i = base + r;
-        v[r] = (i < n) ? in[i] : 0;
-        acc += v[r];
-    }
-    if (zero_in) {                       // consume: leave the input zero (each thread its own items)
-#pragma unroll
-        for (int r = 0; r < kScanItems; ++r)
-            if (base + r < n) zero_in[base + r] = 0u;
-    }
-    // this block's offset = sum of the preceding blocks' totals (<= a few thousand: every block
-    // reduces them itself, so no separate kernel scans the block sums)
-    uint32_t pre = 0;
-    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) pre += block_off[b];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
-    __shared__ uint32_t s_pre[kScanThreads / 32];
-    if ((threadIdx.x & 31) == 0) s_pre[threadIdx.x >> 5] = pre;
-    __syncthreads();
-    uint32_t off = 0;
-    for (int w = 0; w < kScanThreads / 32; ++w) off += s_pre[w];
-    uint32_t run = off + block_exclusive_scan(acc, s_warp, nullptr);
-#pragma unroll
-    for (int r = 0; r < kScanItems; ++r) {
-        uint64_t i = base + r;
-        if (INCLUSIVE) run += v[r];
-        if (i < n) {
-            out[i] = run;
-            if (out2) out2[i] = run;
+            for (int r = 0; r < kScanItems; ++r) v[r] = (base + r < n) ? in[base + r] : 0u;
         }
-        if (!INCLUSIVE) run += v[r];
+#pragma unroll
+        for (int r = 0; r < kScanItems; ++r) acc += v[r];
+        if (zero_in) {
+#pragma unroll
+            for (int r = 0; r < kScanItems; ++r)
+                if (base + r < n) zero_in[base + r] = 0u;
+        }
+        uint32_t tot;
+        const uint32_t excl = block_exclusive_scan(acc, s_warp, &tot);
+        if (threadIdx.x < 32) {
+            // warp 0: publish, look back, publish the inclusive prefix
+            const unsigned lane = threadIdx.x;
+            if (lane == 0)
+                atomicExch(status + t, ((unsigned long long)(t == 0 ? 2u : 1u) << 32) | tot);
+            uint32_t prefix = 0;
+            if (t > 0) {
+                int64_t j = (int64_t)t - 1;
+                while (true) {
+                    // statuses j - lane (lane 0 nearest); spin until none up to the nearest
+                    // inclusive prefix is empty
+                    unsigned long long st = 0;
+                    const int64_t k = j - (int64_t)lane;
+                    unsigned incl = 0;
+                    while (true) {
+                        st = k >= 0 ? __ldcg(status + k) : (2ull << 32);
+                        const unsigned empty = __ballot_sync(0xffffffffu, (st >> 32) == 0);
+                        incl = __ballot_sync(0xffffffffu, (st >> 32) == 2);
+                        const unsigned need = incl ? ((2u << (__ffs(incl) - 1)) - 1u) : 0xffffffffu;
+                        if (!(empty & need)) break;
+                    }
+                    // sum lanes 0 .. first inclusive lane (inclusive), all aggregates before it
+                    const int stop = incl ? __ffs(incl) - 1 : 31;
+                    uint32_t val = (lane <= (unsigned)stop) ? (uint32_t)st : 0u;
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                    prefix += val;
+                    if (incl) break;
+                    j -= 32;
+                }
+                if (lane == 0) atomicExch(status + t, (2ull << 32) | (uint32_t)(prefix + tot));
+            }
+            if (lane == 0) s_excl = prefix;
+        }
+        __syncthreads();
+        uint32_t run = s_excl + excl;
+        __syncthreads();                                       // s_excl / s_warp reused next tile
+#pragma unroll
+        for (int r = 0; r < kScanItems; ++r) {
+            const uint64_t i = base + r;
+            if (INCLUSIVE) run += v[r];
+            if (i < n) {
+                out[i] = run;
+                if (out2) out2[i] = run;
+            }
+            if (!INCLUSIVE) run += v[r];
+        }
     }
 }
 
@@ -177,13 +199,16 @@ void scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, bool inclusive, cud
 {
     if (n == 0) return;
     const uint64_t nb = (n + kScanTile - 1) / kScanTile;
-    Scratch<uint32_t> sums(nb, s);
-    k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, sums.p);
-    SJ_LAUNCHED();
+    int dev = 0;
+    SJ_CUDA(cudaGetDevice(&dev));
+    const uint64_t resident = 2ull * (uint64_t)device_sm_count(dev);       // __launch_bounds__(1024, 2)
+    const unsigned grid = (unsigned)std::min<uint64_t>(nb, resident);
+    Scratch<unsigned long long> status(nb, s);
+    SJ_CUDA(cudaMemsetAsync(status.p, 0, sizeof(unsigned long long) * nb, s));
     if (inclusive)
-        k_scan_apply<true><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, sums.p, out2, zero_in);
+        k_scan_1pass<true><<<grid, kScanThreads, 0, s>>>(in, out, n, nb, status.p, out2, zero_in);
     else
-        k_scan_apply<false><<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, sums.p, out2, zero_in);
+        k_scan_1pass<false><<<grid, kScanThreads, 0, s>>>(in, out, n, nb, status.p, out2, zero_in);
     SJ_LAUNCHED();
 }
 
