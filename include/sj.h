@@ -138,7 +138,9 @@ typedef struct {
                                     binary search of B; rebuilt from B on import)                  */
     uint64_t dir_entries;        /* entries of dir (= number of prefixes + 1)                     */
     const uint32_t *dir;         /* [dir_entries] dir[p] = first cell with top-dir_k prefix >= p   */
-    /* build timings (CUDA events, ms) */
+    /* build timings (CUDA events, ms).  t_geometry_ms covers the min/max pass, the geometry AND the
+       key pass: the key pass is a programmatic dependent launch that overlaps the geometry tail, so
+       there is no event between them (t_keys_ms = 0) */
     float t_h2d_ms, t_geometry_ms, t_keys_ms, t_sort_ms, t_compact_ms, t_total_ms;
     /* the index's arrays as ONE contiguous device buffer (multi-GPU broadcast):
        packed_bytes bytes at `packed`; X, A, pcell, G, masks and B sit at the off_* byte offsets in it
@@ -202,6 +204,11 @@ void sj_free_index(sj_index *idx);   /* NULL-safe */
 /* Totals and work counters of a result. Any out pointer may be NULL.  The device timings in
  * *stats are computed from the join's CUDA events on the first call that asks for stats. */
 sj_status sj_result_info(const sj_result *r, uint64_t *n_pairs, uint32_t *n_batches, sj_stats *stats);
+
+/* The work counters alone -- [pairs, cells_probed, candidates_tested, retries] -- without the lazy
+ * event-timing evaluation sj_result_info(stats) performs (the multi-GPU step all-reduces them).
+ * Errors: SJ_ERR_STATE (NULL result), SJ_ERR_ARG (NULL counters). */
+sj_status sj_result_counters(const sj_result *r, uint64_t counters[4]);
 
 /* N of the point set the result's ids refer to (the joined index's N).  Errors: SJ_ERR_STATE (NULL). */
 sj_status sj_result_n_points(const sj_result *r, uint64_t *n_points);

@@ -333,6 +333,19 @@ sj_status sj_result_info(const sj_result *r, uint64_t *n_pairs, uint32_t *n_batc
     SJ_API_END
 }
 
+sj_status sj_result_counters(const sj_result *r, uint64_t counters[4])
+{
+    SJ_API_BEGIN
+    if (!r) sj::fail(SJ_ERR_STATE, "result is NULL");
+    if (!counters) sj::fail(SJ_ERR_ARG, "counters is NULL");
+    counters[0] = r->total;
+    counters[1] = r->stats.cells_probed;
+    counters[2] = r->stats.candidates_tested;
+    counters[3] = r->stats.retries;
+    return SJ_OK;
+    SJ_API_END
+}
+
 sj_status sj_result_batch(const sj_result *r, uint32_t b, const uint64_t **pairs, uint64_t *n, int *on_device)
 {
     SJ_API_BEGIN

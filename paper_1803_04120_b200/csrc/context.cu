@@ -42,7 +42,7 @@ static void ensure(DevCtx *c, int nstreams, int nevents, size_t slot_bytes)
         while (b < slot_bytes) b <<= 1;
         SJ_CUDA(cudaMalloc(&c->d_slots, b));
         SJ_CUDA(cudaMemset(c->d_slots, 0, b));       // (the build's last-CTA counter starts at 0)
-        SJ_CUDA(cudaHostAlloc(&c->h_slots, b, cudaHostAllocPortable));
+        SJ_CUDA(cudaHostAlloc(&c->h_slots, b, cudaHostAllocPortable | cudaHostAllocMapped));
         c->slot_bytes = b;
     }
 }

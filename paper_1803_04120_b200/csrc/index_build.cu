@@ -14,6 +14,7 @@
 //   k_heads + inclusive scan        : cell index of every A-position (a4)
 //   k_compact_gather                : B, G starts, SoA coordinates X[j][k] = D[A[k]][j] (a4)
 //   k_dir_hist + exclusive scan     : prefix directory bounding every B search (a4)
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -50,6 +51,7 @@ struct DevGeom {
     int status;                  // 0 ok, 1 non-finite coordinate, 2 key overflow
 };
 static_assert(sizeof(DevGeom) % 8 == 0, "DevGeom is copied as 64-bit words");
+static_assert(sizeof(DevGeom) <= 2048, "DevGeom fits below the doorbell");
 
 __device__ __forceinline__ double ord_to_double(unsigned long long k)
 {
@@ -75,6 +77,7 @@ constexpr int kSmemMaskWords = 2048;   // 64 K bits, 8 KB of shared memory
 // context slot layout of the build: min/max partials (<= 4 * SMs blocks), then the DevGeom
 constexpr size_t kGeomOffset = 4 * 256 * (2 * SJ_MAX_DIM + 1) * sizeof(unsigned long long);
 constexpr size_t kEstOffset = kGeomOffset + 4096;          // pinned staging of aux + estimate buckets
+constexpr size_t kBellOffset = 2048;                       // host slots: DevGeom at 0, the doorbell here
 constexpr size_t kMaxEstBuckets = 1100;
 constexpr size_t kAuxEstOffset = 64;                       // estimate buckets, bytes after aux
 constexpr int kAuxWords = 8;                               // aux: |G|, tasks, populous, overflow, masks-trivial
@@ -105,7 +108,8 @@ __device__ __noinline__ void geometry_products(const uint64_t *cpd, int d, uint3
 // executed by the whole (last) CTA of k_minmax_geom (256 threads)
 __device__ __forceinline__ void geometry_block(const unsigned long long *__restrict__ part, uint32_t parts, int d,
                                                double eps, uint32_t n, int allow_bucket, int want_masks,
-                                               uint32_t cap_mult, DevGeom *__restrict__ g)
+                                               uint32_t cap_mult, DevGeom *__restrict__ g, DevGeom *hgeom,
+                                               volatile uint32_t *hbell, uint32_t epoch)
 {
     // reduce the per-block partials of k_minmax: min over [0, d), max over [d, 2d), or of [2d];
     // each thread folds whole rows (independent loads in flight), then warp and CTA reductions
@@ -179,6 +183,16 @@ __device__ __forceinline__ void geometry_block(const unsigned long long *__restr
     const uint64_t *src = reinterpret_cast<const uint64_t *>(&G);
     uint64_t *dst = reinterpret_cast<uint64_t *>(g);
     for (size_t i2 = lane; i2 < sizeof(DevGeom) / 8; i2 += 32) dst[i2] = src[i2];
+    if (hgeom) {
+        // the host's copy straight into mapped pinned memory, then the doorbell: the host polls it
+        // instead of an event + D2H copy between this kernel and the key pass (which would stop the
+        // key pass from launching programmatically behind this one)
+        uint64_t *hdst = reinterpret_cast<uint64_t *>(hgeom);
+        for (size_t i2 = lane; i2 < sizeof(DevGeom) / 8; i2 += 32) hdst[i2] = src[i2];
+        __threadfence_system();
+        __syncwarp();
+        if (lane == 0) *hbell = epoch;
+    }
 }
 
 // a1: exact per-dimension min/max + non-finite flag, then -- in the LAST CTA to finish -- the geometry
@@ -190,8 +204,10 @@ template <int D>
 __global__ void __launch_bounds__(kThreads)
 k_minmax_geom(const double *__restrict__ pts, uint32_t n, unsigned long long *__restrict__ part,
               unsigned int *__restrict__ done, double eps, int allow_bucket, int want_masks, uint32_t cap_mult,
-              DevGeom *__restrict__ g, uint32_t *__restrict__ zero_words, uint32_t nzero)
+              DevGeom *__restrict__ g, uint32_t *__restrict__ zero_words, uint32_t nzero, DevGeom *hgeom,
+              volatile uint32_t *hbell, uint32_t epoch)
 {
+    pdl_trigger();                   // the key pass may launch now (it loads its rows, then waits)
     const uint64_t total = (uint64_t)n * D;
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
@@ -270,7 +286,7 @@ k_minmax_geom(const double *__restrict__ pts, uint32_t n, unsigned long long *__
     if (!s_last) return;
     __threadfence();
     for (uint32_t i = threadIdx.x; i < nzero; i += blockDim.x) zero_words[i] = 0u;
-    geometry_block(part, gridDim.x, D, eps, n, allow_bucket, want_masks, cap_mult, g);
+    geometry_block(part, gridDim.x, D, eps, n, allow_bucket, want_masks, cap_mult, g, hgeom, hbell, epoch);
     if (threadIdx.x == 0) *done = 0u;                 // ready for the next build on this context
 }
 
@@ -335,26 +351,13 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
     __shared__ uint32_t s_mask[kSmemMaskWords];
     __shared__ double s_min[D];
     __shared__ uint64_t s_str[D], s_pstr[D], s_moff[D];
-    if (g->status) return;
-    const bool use_masks = g->masks_on != 0;
-    const bool use_hist = g->use_bucket != 0;
-    const double w = g->w;
-    const uint32_t mask_words = (uint32_t)((g->mask_off[D] + 31) / 32);
-    if (threadIdx.x < D) {
-        s_min[threadIdx.x] = g->mins[threadIdx.x];
-        s_str[threadIdx.x] = g->strides[threadIdx.x];
-        s_pstr[threadIdx.x] = g->pstride[threadIdx.x];
-        s_moff[threadIdx.x] = g->mask_off[threadIdx.x];
-    }
-    if (use_masks)
-        for (uint32_t w2 = threadIdx.x; w2 < mask_words; w2 += blockDim.x) s_mask[w2] = 0;
+    // the point's row does not depend on the min/max pass: under programmatic dependent launch it is
+    // loaded while k_minmax_geom's last CTA still computes the geometry, then we wait for that grid
     const uint64_t base = (uint64_t)blockIdx.x * kThreads;
     const uint32_t cnt = (uint32_t)min((uint64_t)kThreads, (uint64_t)n - base);
-    __syncthreads();
     const uint64_t i = base + threadIdx.x;
+    double xr[D];
     if (threadIdx.x < cnt) {
-        uint64_t key = 0, prefix = 0;
-        double xr[D];
         bool loaded = false;
         if constexpr (D % 2 == 0) {
             if ((reinterpret_cast<uintptr_t>(pts) & 15u) == 0) {   // 16-B aligned rows: vector loads
@@ -371,6 +374,24 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
 #pragma unroll
             for (int j = 0; j < D; ++j) xr[j] = pts[i * D + j];
         }
+    }
+    pdl_wait();
+    if (g->status) return;
+    const bool use_masks = g->masks_on != 0;
+    const bool use_hist = g->use_bucket != 0;
+    const double w = g->w;
+    const uint32_t mask_words = (uint32_t)((g->mask_off[D] + 31) / 32);
+    if (threadIdx.x < D) {
+        s_min[threadIdx.x] = g->mins[threadIdx.x];
+        s_str[threadIdx.x] = g->strides[threadIdx.x];
+        s_pstr[threadIdx.x] = g->pstride[threadIdx.x];
+        s_moff[threadIdx.x] = g->mask_off[threadIdx.x];
+    }
+    if (use_masks)
+        for (uint32_t w2 = threadIdx.x; w2 < mask_words; w2 += blockDim.x) s_mask[w2] = 0;
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+        uint64_t key = 0, prefix = 0;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             const double x = xr[j];
@@ -554,6 +575,9 @@ struct BuildArgs {
     bool bucket_cells = false;   // pcell holds the cell index within the top-k prefix; dir is final
     double dir_inv = 0.0;
     uint32_t *occ = nullptr;
+    DevGeom *hgeom = nullptr;              // mapped pinned copy of the geometry + its doorbell
+    volatile uint32_t *hbell = nullptr;
+    uint32_t epoch = 0;
 };
 
 template <int D>
@@ -561,9 +585,10 @@ void launch_dim(int which, dim3 g, cudaStream_t s, const DevIndex &ix, const Bui
 {
     if (which == 0) {
         k_minmax_geom<D><<<g, kThreads, 0, s>>>(a.pts, a.n, a.mm, a.done, a.eps, a.allow_bucket, a.want_masks,
-                                                 dir_cap_mult(), const_cast<DevGeom *>(a.geom), a.zero_words, a.nzero);
+                                                 dir_cap_mult(), const_cast<DevGeom *>(a.geom), a.zero_words, a.nzero,
+                                                 a.hgeom, a.hbell, a.epoch);
     } else if (which == 1) {
-        k_keys<D><<<g, kThreads, 0, s>>>(a.pts, a.n, a.geom, a.keys, a.ids, a.masks, a.bhist);
+        launch_pdl(k_keys<D>, g, dim3(kThreads), 0, s, a.pts, a.n, a.geom, a.keys, a.ids, a.masks, a.bhist);
     } else if (which == 3) {
         k_masks_global<D><<<g, kThreads, 0, s>>>(a.pts, a.n, ix, a.masks);
     } else {
@@ -1063,17 +1088,20 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         // its own attributes)
         l2p = !o.stream;
         if (l2p) l2_persist_begin(o.device, s, pts, sizeof(double) * n * d);
+        // the geometry comes back through mapped pinned memory + a doorbell the host polls (no
+        // stream operation between the min/max pass and the key pass: see geometry_block)
+        DevGeom *hgeom = static_cast<DevGeom *>(cg.c->h_slots);
+        volatile uint32_t *hbell = reinterpret_cast<volatile uint32_t *>(static_cast<char *>(cg.c->h_slots) + kBellOffset);
+        {
+            void *dh = nullptr;
+            SJ_CUDA(cudaHostGetDevicePointer(&dh, cg.c->h_slots, 0));
+            ba.hgeom = static_cast<DevGeom *>(dh);
+            ba.hbell = reinterpret_cast<volatile uint32_t *>(static_cast<char *>(dh) + kBellOffset);
+            ba.epoch = ++cg.c->doorbell;
+        }
+        cudaStream_t s_side = cg.c->streams[1];
         launch(d, 0, dim3(parts), s, ix, ba);
         tr.dev("minmax + geometry", s);
-        // the host's copy of the geometry travels on a side stream, so the key pass does not queue
-        // behind the small D2H copy's latency
-        DevGeom *hgeom = static_cast<DevGeom *>(cg.c->h_slots);
-        cudaStream_t s_side = cg.c->streams[1];
-        SJ_CUDA(cudaEventRecord(cg.c->events[1], s));
-        SJ_CUDA(cudaStreamWaitEvent(s_side, cg.c->events[1], 0));
-        SJ_CUDA(cudaMemcpyAsync(hgeom, dgeom, sizeof(DevGeom), cudaMemcpyDeviceToHost, s_side));
-        SJ_CUDA(cudaEventRecord(cg.c->events[0], s_side));
-        ev.rec(2, s);
 
         tr.mark("minmax + geometry enqueued");
         const dim3 grid((unsigned)((n + kThreads - 1) / kThreads));
@@ -1085,13 +1113,29 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ba.geom = dgeom;
         ba.bhist = bhist;
         launch(d, 1, grid, s, ix, ba);
+        ev.rec(2, s);
         ev.rec(3, s);
         SJ_CUDA(cudaEventRecord(cg.c->events[2], s));          // keys (and the small masks) done
         tr.dev("keys", s);
         tr.mark("minmax/geometry/keys enqueued");
-        SJ_CUDA(cudaEventSynchronize(cg.c->events[0]));
+        {
+            // poll the doorbell (the stream is queried now and then, so a failed launch is reported
+            // instead of waited for)
+            uint64_t spins = 0;
+            while (*hbell != ba.epoch) {
+                if ((++spins & 255u) == 0) {
+                    const cudaError_t e = cudaStreamQuery(s);
+                    if (e == cudaSuccess) break;
+                    if (e != cudaErrorNotReady) SJ_CUDA(e);
+                }
+            }
+            if (*hbell != ba.epoch) {           // (the stream drained without ringing: read it back)
+                SJ_CUDA(cudaMemcpy(hgeom, dgeom, sizeof(DevGeom), cudaMemcpyDeviceToHost));
+            }
+            std::atomic_thread_fence(std::memory_order_acquire);
+        }
         tr.mark("geometry read");
-        const DevGeom hg = *hgeom;
+        const DevGeom hg = *const_cast<const DevGeom *>(hgeom);
         if (hg.status == 1) fail(SJ_ERR_NONFINITE, "a coordinate is NaN or infinite");
 
         sj_index_view v{};

@@ -6,6 +6,8 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -28,6 +30,32 @@ extern std::atomic<uint64_t> g_kernel_launches;
 inline void count_launch(uint64_t k = 1) { g_kernel_launches.fetch_add(k, std::memory_order_relaxed); }
 // Checks the launch configuration error right after a <<<>>> launch.
 #define SJ_LAUNCHED() do { ::sj::count_launch(); SJ_CUDA(cudaGetLastError()); } while (0)
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// A kernel launched with launch_pdl may start while the previous kernel on its stream is still
+// running (its CTAs fill the SM slots the predecessor leaves free); it must call pdl_wait() before
+// it touches anything the predecessor writes -- the wait returns once the predecessor grid has
+// completed and its memory is visible.  A predecessor calls pdl_trigger() to let the dependent
+// launch early.  Both are no-ops when the launch did not ask for it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args &&...args)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    static const bool off = [] { const char *e = std::getenv("SJ_NO_PDL"); return e && *e && *e != '0'; }();
+    cfg.attrs = at;
+    cfg.numAttrs = off ? 0 : 1;
+    SJ_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 // ---------------------------------------------------------------- host tracing (SJ_TRACE=1..2)
 // SJ_TRACE=1: host marks printed as they happen.  SJ_TRACE=2: one step's timeline (from the start of
@@ -225,8 +253,9 @@ struct DevCtx {
     std::vector<cudaStream_t> streams;
     std::vector<cudaEvent_t> events;
     void *d_slots = nullptr;     // device scratch for cursors / counters
-    void *h_slots = nullptr;     // pinned mirror
+    void *h_slots = nullptr;     // pinned mirror (mapped: kernels may write it directly)
     size_t slot_bytes = 0;
+    uint32_t doorbell = 0;       // epoch of the last device -> host doorbell written into h_slots
 };
 DevCtx *acquire_ctx(int dev, int nstreams, int nevents, size_t slot_bytes);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the call costs

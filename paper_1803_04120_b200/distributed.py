@@ -221,8 +221,7 @@ def sharded_self_join(points, eps: float, device: int, group=None, stats: bool =
         # one library call (sj_self_join_points): build + join without a return to Python between them
         res, idx = sj.join_points(points, eps, device=device, **join_kw)
         if stats:
-            st = res.stats
-            return res, res.n_pairs, idx, {k: int(st[k]) for k in COUNTERS}
+            return res, res.n_pairs, idx, res.counters
         return res, res.n_pairs, idx
     if rank == 0:
         idx = sj.build_index(points, eps, device=device)
@@ -237,8 +236,8 @@ def sharded_self_join(points, eps: float, device: int, group=None, stats: bool =
     a, b = int(cuts[rank]), int(cuts[rank + 1])
     res = sj.self_join(idx, query_begin=a, query_end=b, **join_kw) if b > a else None
     if res is not None:
-        st = res.stats
-        local = [int(st[k]) for k in COUNTERS]
+        c = res.counters
+        local = [c[k] for k in COUNTERS]
     else:
         local = [0] * len(COUNTERS)
     tot = allreduce_counts(local, dev, group=group)

@@ -119,6 +119,8 @@ def load_library(path: str = LIB_PATH):
     L.sj_dbscan.restype = i32
     L.sj_result_n_points.argtypes = [vp, P(u64)]
     L.sj_result_n_points.restype = i32
+    L.sj_result_counters.argtypes = [vp, P(u64)]
+    L.sj_result_counters.restype = i32
     L.sj_result_copy_to_host.argtypes = [vp, vp, u64]
     L.sj_result_copy_to_host.restype = i32
     L.sj_result_to_csr.argtypes = [vp, u64, vp, vp]
@@ -361,6 +363,13 @@ class Result:
             _check(load_library().sj_result_info(self._h, None, None, ctypes.byref(st)))
             self._stats = st.as_dict()
         return self._stats
+
+    @property
+    def counters(self) -> dict:
+        """sj_result_counters: pairs, cells_probed, candidates_tested, retries (no event queries)."""
+        c = (u64 * 4)()
+        _check(load_library().sj_result_counters(self._h, c))
+        return {"pairs": int(c[0]), "cells_probed": int(c[1]), "candidates_tested": int(c[2]), "retries": int(c[3])}
 
     def batch(self, b: int):
         L = load_library()
