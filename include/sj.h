@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SJ_ABI_VERSION 3
+#define SJ_ABI_VERSION 4   /* 4: sj_join_opts.drain_csr, CSR batches, sj_dbscan, sj_result_counters */
 #define SJ_MAX_DIM 6
 
 typedef enum {
