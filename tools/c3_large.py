@@ -1,20 +1,31 @@
-"""C3 large-eps joins (result sets beyond one batch buffer): device- and host-resident results."""
-import os, sys, time
+"""C3 large-eps joins (result sets beyond one batch buffer): device-resident results, host-drained
+pairs (8 B/pair over PCIe) and the CSR host drain (4 B/pair + 4 B/row).  Build + join per call, best of 2."""
+import os
+import sys
+import time
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import torch, datagen, paper_1803_04120_b200 as sj
+import torch  # noqa: E402
+
+import datagen  # noqa: E402
+import paper_1803_04120_b200 as sj  # noqa: E402
+
 P = torch.from_numpy(datagen.uniform_config("C3", 6)).cuda()
 for eps in [float(e) for e in (sys.argv[1:] or ["20", "24"])]:
-    for host in (False, True):
+    for mode in ("device", "host", "csr"):
         best = None
         for _ in range(2):
-            torch.cuda.synchronize(); t0 = time.perf_counter()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
             idx = sj.build_index(P, eps)
-            res = sj.self_join(idx, result_on_host=host)
-            torch.cuda.synchronize(); dt = time.perf_counter() - t0
+            res = sj.self_join(idx, result_on_host=(mode != "device"), drain_csr=(mode == "csr"))
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
             st = res.stats
             row = (dt, res.n_pairs, res.n_batches, st["retries"], st["refine_ms"])
             best = row if best is None or dt < best[0] else best
-            res.free(); idx.free()
+            res.free()
+            idx.free()
         dt, n, nb, rt, rs = best
-        print(f"C3 eps={eps} host={int(host)} pairs={n} batches={nb} retries={rt} total={dt*1e3:.1f}ms "
+        print(f"C3 eps={eps} {mode:6s} pairs={n} batches={nb} retries={rt} total={dt*1e3:.1f}ms "
               f"refine_sum={rs:.1f}ms pairs/s={n/dt:.3e}", flush=True)
