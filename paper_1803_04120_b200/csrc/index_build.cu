@@ -105,8 +105,9 @@ __host__ __device__ __forceinline__ bool bucket_items_pack(uint64_t div, uint32_
 __device__ __noinline__ void geometry_products(const uint64_t *cpd, int d, uint32_t n, int allow_bucket,
                                                int want_masks, uint32_t cap_mult, DevGeom &G);
 
-// executed by the whole (last) CTA of k_minmax_geom (256 threads)
-__device__ __forceinline__ void geometry_block(const unsigned long long *__restrict__ part, uint32_t parts, int d,
+// executed by the whole (last) CTA of k_minmax_geom (256 threads); not inlined, so its registers
+// do not limit the occupancy of the min/max loop
+__device__ __noinline__ void geometry_block(const unsigned long long *__restrict__ part, uint32_t parts, int d,
                                                double eps, uint32_t n, int allow_bucket, int want_masks,
                                                uint32_t cap_mult, DevGeom *__restrict__ g, DevGeom *hgeom,
                                                volatile uint32_t *hbell, uint32_t epoch)
@@ -201,7 +202,7 @@ __device__ __forceinline__ void geometry_block(const unsigned long long *__restr
 // so every element a thread visits has the same dimension t mod D.  Each CTA writes its partial
 // (order-preserving integer images): part[b][0..D) = ord(min), [D..2D) = ord(max), [2D] = non-finite.
 template <int D>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
 k_minmax_geom(const double *__restrict__ pts, uint32_t n, unsigned long long *__restrict__ part,
               unsigned int *__restrict__ done, double eps, int allow_bucket, int want_masks, uint32_t cap_mult,
               DevGeom *__restrict__ g, uint32_t *__restrict__ zero_words, uint32_t nzero, DevGeom *hgeom,
@@ -379,6 +380,7 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
     if (g->status) return;
     const bool use_masks = g->masks_on != 0;
     const bool use_hist = g->use_bucket != 0;
+    const int dir_k = g->k;
     const double w = g->w;
     const uint32_t mask_words = (uint32_t)((g->mask_off[D] + 31) / 32);
     if (threadIdx.x < D) {
@@ -392,13 +394,19 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
     __syncthreads();
     if (threadIdx.x < cnt) {
         uint64_t key = 0, prefix = 0;
+        uint32_t rank = (uint32_t)i;
+        // top dimension first: the prefix is complete after the dir_k top dims, so the bucket path's
+        // histogram atomic -- whose old value is the point's rank in its bucket (the scatter then
+        // needs no atomic of its own) -- is in flight while the low dimensions are divided
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
+        for (int jj = 0; jj < D; ++jj) {
+            const int j = D - 1 - jj;
             const double x = xr[j];
             const double t = floor(__ddiv_rn(__dsub_rn(x, s_min[j]), w));
             const uint64_t c = 1ull + (uint64_t)t;
             key += c * s_str[j];
             prefix += c * s_pstr[j];
+            if (use_hist && jj == dir_k - 1) rank = atomicAdd(bhist + prefix, 1u);
             if (use_masks) {
                 const uint64_t bit = s_moff[j] + c;
                 const uint32_t m = 1u << (bit & 31);
@@ -406,8 +414,7 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
             }
         }
         keys[i] = key;
-        if (use_hist) atomicAdd(bhist + prefix, 1u);
-        else ids[i] = (uint32_t)i;                  // the LSD sort's values (the bucket path's ids are implicit)
+        ids[i] = rank;                      // bucket path: the rank; LSD: the values (input positions)
     }
     if (use_masks) {
         __syncthreads();
@@ -437,6 +444,41 @@ k_heads(const uint64_t *__restrict__ keys, uint32_t n, uint32_t *__restrict__ fl
     const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     flags[k] = (k == 0 || keys[k] != keys[k - 1]) ? 1u : 0u;
+}
+
+__device__ __forceinline__ uint64_t quot_small(uint64_t x, uint64_t d, double inv)   // floor(x/d), x/d < 2^50
+{
+    uint64_t q = (uint64_t)((double)x * inv);
+    if (q * d > x) --q;
+    else if ((q + 1) * d <= x) ++q;
+    return q;
+}
+
+// occ_set_cell (below) from the key and its top-k prefix alone, no full key decode: the grouped
+// index c_L + |g_L| (c_lo + |g_lo| rest) with prefix = c_L + |g_L| rest and c_lo (c_lo2) the
+// digits of the key's low part key - prefix * dir_div
+__device__ __forceinline__ void occ_set_prefix(const DevIndex &ix, uint64_t key, uint64_t prefix, uint32_t *occ,
+                                               uint32_t *occ2)
+{
+    const int L = ix.d - ix.dir_k;
+    const uint64_t gL = ix.cpd[L], glo = ix.cpd[L - 1];
+    const uint64_t rest = quot_small(prefix, gL, ix.inv_cpd[L]);
+    const uint64_t cL = prefix - rest * gL;
+    const uint64_t low = key - prefix * ix.dir_div;
+    const uint64_t clo = quot_small(low, ix.strides[L - 1], ix.inv_stride[L - 1]);
+    const uint64_t q = cL + gL * (clo + glo * rest);
+    atomicOr(occ + ((q - gL) >> 5), 1u << ((q - gL) & 31));
+    atomicOr(occ + (q >> 5), 1u << (q & 31));
+    atomicOr(occ + ((q + gL) >> 5), 1u << ((q + gL) & 31));
+    if (occ2) {
+        const uint64_t glo2 = ix.cpd[L - 2];
+        const uint64_t low2 = low - clo * ix.strides[L - 1];
+        const uint64_t clo2 = quot_small(low2, ix.strides[L - 2], ix.inv_stride[L - 2]);
+        const uint64_t q2 = cL + gL * (clo2 + glo2 * rest);
+        atomicOr(occ2 + ((q2 - gL) >> 5), 1u << ((q2 - gL) & 31));
+        atomicOr(occ2 + (q2 >> 5), 1u << (q2 & 31));
+        atomicOr(occ2 + ((q2 + gL) >> 5), 1u << ((q2 + gL) & 31));
+    }
 }
 
 // Occupancy bitmaps over (top-k prefix, c_lo), lo = d-k-1 (occ) / d-k-2 (occ2), stored DILATED along
@@ -491,10 +533,11 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
     const uint32_t a = A[k];
     const uint64_t key = keys[k];
     uint32_t h;
+    // the key's top-k prefix (exact quotient: double estimate + one integer correction)
+    uint64_t b = (uint64_t)((double)key * dir_inv);
+    if (b * ix.dir_div > key) --b;
+    else if ((b + 1) * ix.dir_div <= key) ++b;
     if (bucket_cells) {             // cell = directory start of the key's top-k prefix + index within it
-        uint64_t b = (uint64_t)((double)key * dir_inv);
-        if (b * ix.dir_div > key) --b;
-        else if ((b + 1) * ix.dir_div <= key) ++b;
         h = __ldg(ix.dir + b) + pcell[k];
         if (h >= n) return;         // only after a flagged bucket overflow (the build is redone)
     } else {                        // inclusive scan of head flags (1-based)
@@ -506,9 +549,9 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
         G[h] = (uint32_t)k;
         // populous cell (>= dense_T points)?  one extra load: its (dense_T-1)-th successor
         if (n_dense_cells && k + dense_T - 1 < n && keys[k + dense_T - 1] == key) atomicAdd(n_dense_cells, 1u);
-        uint64_t c[D];
-        key_to_coords<D>(ix, key, c);
         if (ccoord) {
+            uint64_t c[D];
+            key_to_coords<D>(ix, key, c);
             uint64_t packed = 0;
             uint32_t mb = 0;
 #pragma unroll
@@ -523,11 +566,8 @@ k_compact_gather(const uint64_t *__restrict__ keys, const uint32_t *__restrict__
             ccoord[h] = packed;
             cmask[h] = mb;
         }
-        uint64_t prefix = 0;
-#pragma unroll
-        for (int j = 0; j < D; ++j) prefix += c[j] * ix.pstride[j];
-        if (dirhist) atomicAdd(dirhist + prefix, 1u);
-        if (occ) occ_set_cell<D>(ix, c, occ, const_cast<uint32_t *>(ix.occ2));
+        if (dirhist) atomicAdd(dirhist + b, 1u);
+        if (occ) occ_set_prefix(ix, key, b, occ, const_cast<uint32_t *>(ix.occ2));
     }
     if (k == n - 1) {
         G[h + 1] = n;
@@ -1062,9 +1102,11 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         // geometry on the device (k_geometry) and the key pass right behind it; the host reads the
         // geometry (one small D2H copy, waited on by an event) while the key pass runs.
         // grid: a multiple of 3 and 5 CTAs (so the thread count is a multiple of d), <= 1020 partials
-        uint32_t parts = (uint32_t)std::min<uint64_t>((n * d + kThreads * 16 - 1) / (kThreads * 16), 1020u);
+        // one wave: <= 4 resident CTAs per SM (__launch_bounds__(256, 4)), a multiple of 15
+        const uint32_t pcap = std::max<uint32_t>(15u, std::min<uint32_t>(1020u, (uint32_t)(4 * nsm) / 15u * 15u));
+        uint32_t parts = (uint32_t)std::min<uint64_t>((n * d + kThreads * 16 - 1) / (kThreads * 16), pcap);
         parts = std::max<uint32_t>(15u, (parts + 14u) / 15u * 15u);
-        parts = std::min<uint32_t>(parts, 1020u);
+        parts = std::min<uint32_t>(parts, pcap);
         // min/max partials, the device geometry and the last-CTA counter live in the context's slots
         unsigned long long *part = static_cast<unsigned long long *>(cg.c->d_slots);
         DevGeom *dgeom = reinterpret_cast<DevGeom *>(static_cast<char *>(cg.c->d_slots) + kGeomOffset);

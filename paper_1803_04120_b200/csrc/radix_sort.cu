@@ -297,10 +297,11 @@ constexpr int kBigThreads = 512;
 // Packed mode (idb > 0): the item travels as ONE 64-bit word (key - prefix*div) << idb | id -- within
 // a bucket the prefix is common, so u64 order == (key, id) order -- instead of a key and an id
 // written to two random places.
+// The position of item i is start[prefix] + rank[i]: the rank came back from the key pass's histogram
+// atomic, so this pass is a plain streaming scatter (no atomic round trip per item).
 __global__ void __launch_bounds__(256)
-k_bucket_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t n, uint64_t div,
-                 double inv, uint32_t *__restrict__ cursor, uint64_t *__restrict__ kout, uint32_t *__restrict__ vout,
-                 int idb)
+k_bucket_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ rank, uint32_t n, uint64_t div,
+                 double inv, const uint32_t *__restrict__ start, uint64_t *__restrict__ kout, int idb)
 {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -308,13 +309,8 @@ k_bucket_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ 
     uint64_t q = (uint64_t)((double)k * inv);          // prefix = k / div (double estimate, corrected)
     if (q * div > k) --q;
     else if ((q + 1) * div <= k) ++q;
-    const uint32_t pos = atomicAdd(cursor + q, 1u);
-    if (idb) {
-        kout[pos] = ((k - q * div) << idb) | i;       // ids are the input positions (k_keys writes none)
-    } else {
-        kout[pos] = k;
-        vout[pos] = vin[i];
-    }
+    const uint32_t pos = __ldg(start + q) + rank[i];
+    kout[pos] = ((k - q * div) << idb) | i;           // ids are the input positions
 }
 
 // big[0] = number of queued big buckets, big[1..] = their ids.
@@ -508,7 +504,8 @@ k_bucket_sort_big(const uint64_t *__restrict__ kin, const uint32_t *__restrict__
 }
 }  // namespace
 
-// hist: per-prefix point counts (P + 1 entries, the last one 0), consumed (it becomes the cursor).
+// hist: per-prefix point counts (P + 1 entries, the last one 0); vals holds every point's rank in its
+// bucket (from the key pass's histogram atomic) on entry and the sorted ids on exit.
 // local[n]: cell index of each sorted item within its bucket; cellcnt[P+1]: cells per bucket (the
 // caller scans it into the prefix directory).
 void bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp, uint32_t n,
@@ -524,7 +521,7 @@ void bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint3
     SJ_CUDA(cudaMemsetAsync(big.p, 0, sizeof(uint32_t), s));
     SJ_CUDA(cudaMemsetAsync(cellcnt + P, 0, sizeof(uint32_t), s));
     tr.dev("start", s);
-    exclusive_scan_u32_dup(hist, start.p, hist, (uint64_t)P + 1, s);
+    exclusive_scan_u32(hist, start.p, (uint64_t)P + 1, s);
     tr.dev("bucket scan", s);
     const uint32_t g = (n + 255) / 256;
     // packed items when (bits of key - prefix*div) + (bits of an id) <= 64
@@ -533,7 +530,7 @@ void bucket_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint3
     while (idb < 32 && ((uint64_t)(n - 1) >> idb)) ++idb;
     if (idb == 0) idb = 1;
     if (lowb + idb > 64) fail(SJ_ERR_CUDA, "bucket sort needs packed items (internal error)");
-    k_bucket_scatter<<<g, 256, 0, s>>>(keys, vals, n, div, inv, hist, keys_tmp, vals_tmp, idb);
+    k_bucket_scatter<<<g, 256, 0, s>>>(keys, vals, n, div, inv, start.p, keys_tmp, idb);
     SJ_LAUNCHED();
     tr.dev("scatter", s);
     k_bucket_sort<<<(uint32_t)((P + 255) / 256), 256, 0, s>>>(keys_tmp, vals_tmp, start.p, P, keys, vals, big.p,
