@@ -47,6 +47,21 @@ static void ensure(DevCtx *c, int nstreams, int nevents, size_t slot_bytes)
     }
 }
 
+void ensure_join_blocks(DevCtx *c, size_t bytes)
+{
+    if (bytes <= c->jb_bytes) return;
+    if (c->jb_d) cudaFree(c->jb_d);
+    if (c->jb_h) cudaFreeHost(c->jb_h);
+    c->jb_d = c->jb_h = nullptr;
+    c->jb_bytes = 0;
+    c->jb_clean = false;
+    size_t b = 4096;
+    while (b < bytes) b <<= 1;
+    SJ_CUDA(cudaMalloc(&c->jb_d, b));
+    SJ_CUDA(cudaHostAlloc(&c->jb_h, b, cudaHostAllocPortable));
+    c->jb_bytes = b;
+}
+
 DevCtx *acquire_ctx(int dev, int nstreams, int nevents, size_t slot_bytes)
 {
     DevCtx *c = nullptr;

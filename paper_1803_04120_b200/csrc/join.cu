@@ -305,17 +305,18 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     // zeroes its own block before its first batch and copies it back after its last one, so no
     // stream waits for another (no event hops on the GPU between the batches and the read-back)
     const size_t kBlock = kWorkBytes + kSlotsBytes;
-    const size_t slot_need = kBlock * (size_t)S + 8 * (size_t)(nbk + 1);
+    const size_t slot_need = 8 * (size_t)(nbk + 1);
     CtxGuard cg{acquire_ctx(idx->device, S, S + 2, slot_need)};
     DevCtx &cx = *cg.c;
     cudaStream_t s0 = cx.streams[0];
-    char *dbase = static_cast<char *>(cx.d_slots), *hbase = static_cast<char *>(cx.h_slots);
+    ensure_join_blocks(&cx, kBlock * (size_t)S);
+    char *dbase = static_cast<char *>(cx.jb_d), *hbase = static_cast<char *>(cx.jb_h);
     auto dwork = [&](int si) { return reinterpret_cast<unsigned long long *>(dbase + kBlock * si); };
     auto hwork = [&](int si) { return reinterpret_cast<const unsigned long long *>(hbase + kBlock * si); };
     auto dslot = [&](int si, size_t j) { return reinterpret_cast<Slot *>(dbase + kBlock * si + kWorkBytes) + j; };
     auto hslot = [&](int si, size_t j) { return reinterpret_cast<Slot *>(hbase + kBlock * si + kWorkBytes) + j; };
-    unsigned long long *dbk = reinterpret_cast<unsigned long long *>(dbase + kBlock * S);
-    unsigned long long *hbk = reinterpret_cast<unsigned long long *>(hbase + kBlock * S);
+    unsigned long long *dbk = static_cast<unsigned long long *>(cx.d_slots);
+    unsigned long long *hbk = static_cast<unsigned long long *>(cx.h_slots);
     tr.mark("acquire ctx");
     sj_result *res = new sj_result();
     res->device = idx->device;
@@ -328,12 +329,16 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     // self pairs of a batch [a, b): written at fixed slots, counted on the host (see JoinArgs::nself)
     auto nself_of = [&](uint64_t a, uint64_t b) -> uint64_t { return o.include_self ? b - a : 0; };
     try {
-        for (int i = 0; i < S; ++i) SJ_CUDA(cudaMemsetAsync(dwork(i), 0, kBlock, cx.streams[i]));
+        // the blocks are zero when the previous join on this context re-zeroed them after reading them
+        if (!cx.jb_clean)
+            for (int i = 0; i < S; ++i) SJ_CUDA(cudaMemsetAsync(dwork(i), 0, kBlock, cx.streams[i]));
+        cx.jb_clean = false;
         if (!spec && es.ns) SJ_CUDA(cudaMemsetAsync(dbk, 0, 8 * nbk, s0));
         // ---- a5: estimate on a strided sample (count-only refine), summed per planning bucket
         // (an index built for the default join already carries it: no launch, no round trip)
+        const unsigned long long *bk = hbk;
         if (spec) {
-            std::copy(idx->spec_buckets.begin(), idx->spec_buckets.end(), hbk);
+            bk = idx->spec_buckets.data();          // the build's counts: no copy
         } else if (es.ns) {
             res->est_ev[0] = event_get(idx->device);
             res->est_ev[1] = event_get(idx->device);
@@ -353,7 +358,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         uint64_t est_total = 0;
         {
             std::vector<double> be(nbk);
-            for (uint64_t i = 0; i < nbk; ++i) be[i] = (double)hbk[i] * (double)es.step;
+            for (uint64_t i = 0; i < nbk; ++i) be[i] = (double)bk[i] * (double)es.step;
             plan_from_buckets(be.data(), nbk, es.step * es.group, q0, q1, o.batch_capacity_pairs, o.min_batches, 0.25,
                               cuts, est, &est_total);
         }
@@ -363,6 +368,12 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
 
         bool work_read = false;
         uint32_t launches = 0;
+        unsigned long long wsum[3] = {0, 0, 0};
+        auto add_work = [&]() {
+            for (int si = 0; si < S; ++si)
+                for (int sl = 0; sl < kWorkSlots; ++sl)
+                    for (int i = 0; i < 3; ++i) wsum[i] += hwork(si)[4 * sl + i];
+        };
         // every batch run records a (start, end) event pair; timings are computed on request
         auto run_batch = [&](uint64_t a, uint64_t b, uint64_t *buf, uint64_t cap, Slot *dslot, int si,
                              bool clear_slot) {
@@ -422,12 +433,16 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 run_batch(cuts[b], cuts[b + 1], bt.pairs, cap, dslot(si, slot), si, !own_slots);
                 if (!own_slots)
                     SJ_CUDA(cudaMemcpyAsync(hslot(si, 0), dslot(si, 0), sizeof(Slot), cudaMemcpyDeviceToHost, s));
-                if (b + S >= nb)                      // the stream's last batch: its block back to the host
+                if (b + S >= nb) {                    // the stream's last batch: its block back to the host,
                     SJ_CUDA(cudaMemcpyAsync(hbase + kBlock * si, dbase + kBlock * si, kBlock, cudaMemcpyDeviceToHost, s));
+                    // then zeroed for the next join on this context (off the critical path)
+                    SJ_CUDA(cudaMemsetAsync(dbase + kBlock * si, 0, kBlock, s));
+                }
             }
             tr.mark("batches launched");
             for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
             tr.mark("batches done (synced)");
+            add_work();                           // (the device blocks are being zeroed behind the copies)
             work_read = true;
             cudaStream_t st_sort = s0;
             if (own_slots) {
@@ -575,16 +590,14 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
         }
 
-        // ---- work counters (already read back unless a retry / host mode ran more kernels; every
-        //      stream is synchronised here)
-        if (!work_read || stats.retries || o.sort_pairs) {
+        // ---- work counters: the device path read them with its first round; re-runs (which counted
+        //      into the re-zeroed blocks) and the host path are read here (every stream is synced)
+        if (!work_read || stats.retries) {
             SJ_CUDA(cudaMemcpyAsync(hbase, dbase, kBlock * S, cudaMemcpyDeviceToHost, s0));
             SJ_CUDA(cudaStreamSynchronize(s0));
+            add_work();
         }
-        unsigned long long wsum[3] = {0, 0, 0};
-        for (int si = 0; si < S; ++si)
-            for (int sl = 0; sl < kWorkSlots; ++sl)
-                for (int i = 0; i < 3; ++i) wsum[i] += hwork(si)[4 * sl + i];
+        cx.jb_clean = work_read && !stats.retries;   // zeroed behind the device path's read-back copies
         stats.cells_probed = wsum[0];
         stats.candidates_tested = wsum[1];
         stats.pairs = res->total;

@@ -256,7 +256,15 @@ struct DevCtx {
     void *h_slots = nullptr;     // pinned mirror (mapped: kernels may write it directly)
     size_t slot_bytes = 0;
     uint32_t doorbell = 0;       // epoch of the last device -> host doorbell written into h_slots
+    // the join's per-stream counter blocks (only joins touch them): device + pinned mirror, and whether
+    // the previous join left them zero (it re-zeroes them on each stream right after reading them back)
+    void *jb_d = nullptr;
+    void *jb_h = nullptr;
+    size_t jb_bytes = 0;
+    bool jb_clean = false;
 };
+// grow the join blocks to `bytes` (a fresh allocation is not clean)
+void ensure_join_blocks(DevCtx *c, size_t bytes);
 DevCtx *acquire_ctx(int dev, int nstreams, int nevents, size_t slot_bytes);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the call costs
 // tens of microseconds of host time, on the build's / join's critical path if repeated.

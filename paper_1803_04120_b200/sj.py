@@ -161,10 +161,16 @@ def kernel_launches() -> int:
     return int(load_library().sj_kernel_launches())
 
 
+_JOIN_DEFAULTS = None
+
+
 def join_opts(**kw) -> JoinOpts:
-    L = load_library()
-    o = JoinOpts()
-    L.sj_join_opts_default(ctypes.byref(o))
+    global _JOIN_DEFAULTS
+    if _JOIN_DEFAULTS is None:
+        d0 = JoinOpts()
+        load_library().sj_join_opts_default(ctypes.byref(d0))
+        _JOIN_DEFAULTS = bytes(d0)
+    o = JoinOpts.from_buffer_copy(_JOIN_DEFAULTS)
     for k, v in kw.items():
         if v is None:
             continue
@@ -279,29 +285,46 @@ def _device_tensor(ptr, shape, dtype, device, owner):
     return t
 
 
+_BUILD_DEFAULTS = None
+_torch = None
+
+
+def _current_stream(dev: int) -> int:
+    """torch's current CUDA stream of a device as a raw handle (the cheap accessor when present: this
+    sits in every step's host path)."""
+    raw = getattr(_torch._C, "_cuda_getCurrentRawStream", None)
+    return raw(dev) if raw is not None else _torch.cuda.current_stream(dev).cuda_stream
+
+
 def _points_arg(points, device, stream, build_masks=True, speculative_estimate=True):
     """(BuildOpts, pointer, n, d, keepalive) for sj_build_index / sj_self_join_points."""
-    L = load_library()
-    o = BuildOpts()
-    L.sj_build_opts_default(ctypes.byref(o))
+    global _BUILD_DEFAULTS, _torch
+    if _BUILD_DEFAULTS is None:
+        d0 = BuildOpts()
+        load_library().sj_build_opts_default(ctypes.byref(d0))
+        _BUILD_DEFAULTS = bytes(d0)
+    o = BuildOpts.from_buffer_copy(_BUILD_DEFAULTS)
     o.build_masks = int(build_masks)
     o.speculative_estimate = int(speculative_estimate)
-    try:
-        import torch
-        is_torch = isinstance(points, torch.Tensor)
-    except ImportError:  # pragma: no cover
-        is_torch = False
+    if _torch is None:
+        try:
+            import torch
+            _torch = torch
+        except ImportError:  # pragma: no cover
+            _torch = False
+    is_torch = bool(_torch) and isinstance(points, _torch.Tensor)
     if is_torch:
         t = points
-        if t.dtype != torch.float64 or t.dim() != 2:
+        if t.dtype != _torch.float64 or t.dim() != 2:
             raise TypeError("points must be a 2-D float64 tensor")
-        t = t.contiguous()
+        if not t.is_contiguous():
+            t = t.contiguous()
         n, d = t.shape
         if t.is_cuda:
             o.points_on_device = 1
-            o.device = t.device.index if device is None else device
-            o.stream = ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream) if stream is None \
-                else ctypes.c_void_p(stream)
+            dev = t.get_device()
+            o.device = dev if device is None else device
+            o.stream = ctypes.c_void_p(_current_stream(dev)) if stream is None else ctypes.c_void_p(stream)
         else:
             o.points_on_device = 0
             o.device = 0 if device is None else device
