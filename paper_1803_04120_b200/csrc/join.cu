@@ -95,6 +95,45 @@ void plan_from_buckets(const double *bucket_est, uint64_t nbk, uint64_t width, u
     cuts.clear();
     est.clear();
     const uint64_t nq = q1 - q0;
+    {
+        // fast path (the join's common case, on its critical path): no bucket needs splitting and the
+        // estimate cuts already give >= min_batches ranges -- then every bucket lies in one range and
+        // the general walk below reduces to one pass (same cuts, same estimates)
+        const double target = std::max(1.0, (double)capacity / (1.0 + margin));
+        double total = 0, mx = 0;
+        uint64_t nu = 0;
+        for (uint64_t s = 0; s < nbk && q0 + s * width < q1; ++s, ++nu) {
+            total += bucket_est[s];
+            mx = std::max(mx, bucket_est[s]);
+        }
+        if (nq > 0 && total > 0 && nu > 0 && !(mx > target)) {
+            uint64_t k = std::max<uint64_t>((uint64_t)min_batches, (uint64_t)std::ceil(total / target));
+            k = std::min<uint64_t>(k, nq);
+            const double per = total / (double)k;
+            cuts.push_back(q0);
+            double acc = 0;
+            for (uint64_t u = 0; u + 1 < nu; ++u) {
+                acc += bucket_est[u];
+                const uint64_t b = std::min(q1, q0 + (u + 1) * width);
+                if (acc >= per * (double)cuts.size() && b > cuts.back()) cuts.push_back(b);
+            }
+            if (q1 > cuts.back() || cuts.size() == 1) cuts.push_back(q1);
+            if (cuts.size() - 1 >= (size_t)min_batches) {
+                std::vector<double> e(cuts.size() - 1, 0.0);
+                size_t r = 0;
+                for (uint64_t u = 0; u < nu; ++u) {
+                    const uint64_t a = q0 + u * width;
+                    while (r + 2 < cuts.size() && cuts[r + 1] <= a) ++r;
+                    e[r] += bucket_est[u];
+                }
+                est.resize(e.size());
+                for (size_t i = 0; i < e.size(); ++i) est[i] = (uint64_t)std::ceil(e[i]);
+                *estimated_total = (uint64_t)std::llround(total);
+                return;
+            }
+            cuts.clear();
+        }
+    }
     struct Unit { uint64_t a, b; double e; };
     std::vector<Unit> units;
     units.reserve(nbk);
@@ -416,10 +455,34 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             res->batches.resize(nb);
             std::vector<uint64_t> counts(nb, 0);
             const bool own_slots = nb <= (size_t)64 * S;
+            // the batches' buffers first (host bookkeeping), so the launches then go out back to back
+            if (own_slots) {
+                for (size_t b = 0; b < nb; ++b) {
+                    const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(
+                        o.batch_capacity_pairs, est[b] + est[b] / 4 + 65536));
+                    sj_batch &bt = res->batches[b];
+                    bt.pairs = static_cast<uint64_t *>(
+                        result_buffer_get(idx->device, cap * sizeof(uint64_t), cx.streams[b % S]));
+                    bt.cap = cap;
+                    bt.on_device = 1;
+                }
+            }
             for (size_t b = 0; b < nb; ++b) {
                 const int si = (int)(b % S);
                 cudaStream_t s = cx.streams[si];
                 const size_t slot = own_slots ? b / S : 0;
+                if (own_slots) {
+                    sj_batch &bt = res->batches[b];
+                    run_batch(cuts[b], cuts[b + 1], bt.pairs, bt.cap, dslot(si, slot), si, false);
+                    if (b + S >= nb) {                // the stream's last batch: its block back to the host,
+                        SJ_CUDA(cudaMemcpyAsync(hbase + kBlock * si, dbase + kBlock * si, kBlock,
+                                                cudaMemcpyDeviceToHost, s));
+                        SJ_CUDA(cudaEventRecord(cx.events[2 + si], s));
+                        // then zeroed for the next join on this context (off the critical path)
+                        SJ_CUDA(cudaMemsetAsync(dbase + kBlock * si, 0, kBlock, s));
+                    }
+                    continue;
+                }
                 if (!own_slots && b >= (size_t)S) {   // stream si's previous batch must have published its cursor
                     SJ_CUDA(cudaStreamSynchronize(s));
                     counts[b - S] = hslot(si, 0)->cursor;   // (+ the batch's self pairs below)
@@ -440,7 +503,11 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 }
             }
             tr.mark("batches launched");
-            for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
+            // wait for the read-back copies (not for the zeroing behind them)
+            for (int i = 0; i < S && i < (int)nb; ++i) {
+                if (own_slots) SJ_CUDA(cudaEventSynchronize(cx.events[2 + i]));
+                else SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
+            }
             tr.mark("batches done (synced)");
             add_work();                           // (the device blocks are being zeroed behind the copies)
             work_read = true;
