@@ -300,6 +300,7 @@ sj_status sj_trim(int device)
     SJ_API_BEGIN
     sj::result_cache_trim(device);
     sj::scratch_trim(device);
+    sj::zbuf_trim(device);
     sj::host_pinned_trim();
     const int n = sj::device_count();
     for (int dv = 0; dv < n; ++dv) {

@@ -58,8 +58,24 @@ void ensure_join_blocks(DevCtx *c, size_t bytes)
     size_t b = 4096;
     while (b < bytes) b <<= 1;
     SJ_CUDA(cudaMalloc(&c->jb_d, b));
-    SJ_CUDA(cudaHostAlloc(&c->jb_h, b, cudaHostAllocPortable));
+    SJ_CUDA(cudaMemset(c->jb_d, 0, b));               // (the publish CTA counters start at 0)
+    SJ_CUDA(cudaHostAlloc(&c->jb_h, b, cudaHostAllocPortable | cudaHostAllocMapped));
+    SJ_CUDA(cudaHostGetDevicePointer(&c->jb_hd, c->jb_h, 0));
+    std::memset(c->jb_h, 0, b);
     c->jb_bytes = b;
+}
+
+bool wait_doorbell(const volatile unsigned int *bell, unsigned int epoch, cudaStream_t s)
+{
+    uint64_t spins = 0;
+    while (*bell != epoch) {
+        if ((++spins & 255u) == 0) {
+            const cudaError_t e = cudaStreamQuery(s);
+            if (e == cudaSuccess) return *bell == epoch;
+            if (e != cudaErrorNotReady) SJ_CUDA(e);
+        }
+    }
+    return true;
 }
 
 DevCtx *acquire_ctx(int dev, int nstreams, int nevents, size_t slot_bytes)
@@ -371,6 +387,53 @@ void scratch_release(int dev, void *p, size_t zero_prefix)
     if (sl.p == p) {
         sl.busy = false;
         sl.zero = zero_prefix;
+    }
+}
+
+namespace {
+std::mutex g_zb_mu;
+std::map<int, std::multimap<size_t, void *>> g_zb;     // device -> (bytes -> zeroed buffer)
+std::map<int, size_t> g_zb_held;
+constexpr size_t kZbLimit = 1ull << 30;                  // per device
+}  // namespace
+
+void *zbuf_get(int dev, size_t bytes, size_t *granted)
+{
+    if (alloc_hook_set()) return nullptr;
+    std::lock_guard<std::mutex> lk(g_zb_mu);
+    auto &m = g_zb[dev];
+    auto it = m.lower_bound(bytes);
+    if (it == m.end() || it->first > 2 * bytes + (1u << 20)) return nullptr;
+    void *p = it->second;
+    *granted = it->first;
+    g_zb_held[dev] -= it->first;
+    m.erase(it);
+    return p;
+}
+
+void zbuf_put(int dev, void *p, size_t bytes)
+{
+    if (!p) return;
+    {
+        std::lock_guard<std::mutex> lk(g_zb_mu);
+        if (g_zb_held[dev] + bytes <= kZbLimit && cudaMemset(p, 0, bytes) == cudaSuccess) {
+            g_zb[dev].emplace(bytes, p);
+            g_zb_held[dev] += bytes;
+            return;
+        }
+    }
+    cudaGetLastError();
+    cudaFree(p);
+}
+
+void zbuf_trim(int dev)
+{
+    std::lock_guard<std::mutex> lk(g_zb_mu);
+    for (auto &kv : g_zb) {
+        if (dev >= 0 && kv.first != dev) continue;
+        for (auto &e : kv.second) cudaFree(e.second);
+        kv.second.clear();
+        g_zb_held[kv.first] = 0;
     }
 }
 

@@ -796,20 +796,31 @@ void alloc_dir(sj_index *idx, const DirPlan &dp, cudaStream_t s)
     idx->bufs[idx->nbufs++] = dir;
     idx->view.dir = dir;
     idx->dev.dir = dir;
+    // the bitmaps come zeroed from the zeroed-buffer cache when one is there (released bitmaps are
+    // zeroed when their index is freed), else fresh + memset
+    auto zeroed = [&](size_t bytes, int slot) -> uint32_t * {
+        size_t got = 0;
+        void *p = zbuf_get(idx->device, bytes, &got);
+        if (p) {
+            idx->zbufs[slot] = p;
+            idx->zbytes[slot] = got;
+            return static_cast<uint32_t *>(p);
+        }
+        if (!alloc_hook_set()) {
+            SJ_CUDA(cudaMalloc(&p, bytes));
+            idx->zbufs[slot] = p;
+            idx->zbytes[slot] = bytes;
+        } else {
+            p = dev_alloc(bytes, s);
+            idx->bufs[idx->nbufs++] = p;
+        }
+        SJ_CUDA(cudaMemsetAsync(p, 0, bytes, s));
+        return static_cast<uint32_t *>(p);
+    };
     idx->dev.occ = nullptr;
-    if (dp.occ) {
-        uint32_t *occ = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * dp.occ_words, s));
-        idx->bufs[idx->nbufs++] = occ;
-        SJ_CUDA(cudaMemsetAsync(occ, 0, sizeof(uint32_t) * dp.occ_words, s));
-        idx->dev.occ = occ;
-    }
+    if (dp.occ) idx->dev.occ = zeroed(sizeof(uint32_t) * dp.occ_words, 0);
     idx->dev.occ2 = nullptr;
-    if (dp.occ2) {
-        uint32_t *occ2 = static_cast<uint32_t *>(dev_alloc(sizeof(uint32_t) * dp.occ2_words, s));
-        idx->bufs[idx->nbufs++] = occ2;
-        SJ_CUDA(cudaMemsetAsync(occ2, 0, sizeof(uint32_t) * dp.occ2_words, s));
-        idx->dev.occ2 = occ2;
-    }
+    if (dp.occ2) idx->dev.occ2 = zeroed(sizeof(uint32_t) * dp.occ2_words, 1);
 }
 
 namespace {
@@ -908,14 +919,18 @@ void launch_masks_full(const DevIndex &ix, uint32_t *flag, cudaStream_t s)
 
 void finish_aux(sj_index *idx, cudaStream_t s, uint32_t *aux, const DirPlan &dp, const uint32_t *dirhist,
                 bool force_dense, uint32_t *h_aux, void *h_stage = nullptr, size_t stage_bytes = 0,
-                bool check_masks = true)
+                bool check_masks = true, const volatile unsigned int *bell = nullptr, unsigned int epoch = 0)
 {
     sj_index_view &v = idx->view;
     DevIndex &ix = idx->dev;
     if (dirhist) exclusive_scan_u32(dirhist, const_cast<uint32_t *>(ix.dir), (uint64_t)dp.P + 1, s);
     // aux[4]: the masks exclude nothing (the build checks on its side stream; the import here)
     if (check_masks && ix.masks && v.mask_offsets[v.d] <= 32ull * kSmemMaskWords) launch_masks_full(ix, aux + 4, s);
-    if (h_stage) {
+    if (h_stage && bell && wait_doorbell(bell, epoch, s)) {
+        // the estimate's last CTA published aux + the buckets into h_stage
+        std::atomic_thread_fence(std::memory_order_acquire);
+        std::memcpy(h_aux, const_cast<const void *>(static_cast<volatile void *>(h_stage)), kAuxWords * sizeof(uint32_t));
+    } else if (h_stage) {
         // one copy into pinned memory: aux and whatever the caller placed after it (the build's
         // estimate buckets)
         SJ_CUDA(cudaMemcpyAsync(h_stage, aux, stage_bytes, cudaMemcpyDeviceToHost, s));
@@ -1263,7 +1278,9 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         // are the masks trivial (finish_aux reads aux[4])?  A one-CTA check on the side stream,
         // off the critical path; s joins it before its final copy
         bool mask_check = false;
-        if (masks && masks == small_masks) {
+        // with the speculative estimate, its publishing CTA checks the masks (no side kernel)
+        const bool spec_early = v.key_bits <= 62 && o.speculative_estimate;
+        if (masks && masks == small_masks && !spec_early) {
             DevIndex mx = ix;
             mx.masks = masks;
             SJ_CUDA(cudaStreamWaitEvent(s_side, cg.c->events[2], 0));
@@ -1374,6 +1391,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
                               : (pavg <= 8.0 && (double)dp.div < 4.0e15 ? kSearchCellScan : kSearchRows);
         const bool spec = v.key_bits <= 62 && o.speculative_estimate;
         EstimateShape es_spec;
+        Publish pub{};
         char *h_stage = static_cast<char *>(cg.c->h_slots) + kEstOffset;
         const unsigned long long *hbk = reinterpret_cast<const unsigned long long *>(h_stage + kAuxEstOffset);
         if (spec) {
@@ -1387,12 +1405,28 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
             unsigned long long *dbk = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(aux) + kAuxEstOffset);
             sj_join_opts jo;
             sj_join_opts_default(&jo);
-            launch_estimate(px, o.device, jo, 0, n, es_spec, dbk, s);
+            // the estimate's last CTA publishes aux + the buckets into the mapped staging slot (and
+            // the masks-trivial flag into aux[4] first) and rings a doorbell: no D2H copy + sync
+            void *dh = nullptr;
+            SJ_CUDA(cudaHostGetDevicePointer(&dh, cg.c->h_slots, 0));
+            pub.src = reinterpret_cast<unsigned long long *>(aux);
+            pub.dst = reinterpret_cast<unsigned long long *>(static_cast<char *>(dh) + kEstOffset);
+            pub.words = (uint32_t)((kAuxEstOffset + 8 * es_spec.nbk) / 8);
+            pub.zero_src = 0;
+            pub.done = reinterpret_cast<unsigned int *>(static_cast<char *>(cg.c->d_slots) + kGeomOffset + 4096 - 32);
+            pub.bell = reinterpret_cast<volatile unsigned int *>(static_cast<char *>(dh) + kBellOffset + 64);
+            pub.epoch = ++cg.c->doorbell;
+            pub.masks_flag = (masks && masks == small_masks) ? aux + 4 : nullptr;
+            launch_estimate(px, o.device, jo, 0, n, es_spec, dbk, s, &pub);
             tr.dev("speculative estimate", s);
         }
         if (mask_check) SJ_CUDA(cudaStreamWaitEvent(s, cg.c->events[3], 0));
+        const volatile unsigned int *est_bell =
+            pub.src ? reinterpret_cast<const volatile unsigned int *>(static_cast<char *>(cg.c->h_slots) + kBellOffset + 64)
+                    : nullptr;
         finish_aux(idx, s, aux, dp, nullptr, false, h_aux, h_stage,
-                   kAuxEstOffset + (spec ? 8 * es_spec.nbk : 0), !mask_check);     // the build's late host sync
+                   kAuxEstOffset + (spec ? 8 * es_spec.nbk : 0), !mask_check && !pub.masks_flag, est_bell,
+                   pub.epoch);     // the build's late host sync (or doorbell)
         if (l2p) l2_persist_end(o.device);   // s is synced: demote the input's persisting lines
         scratch.leave_zero = s_h;            // the histogram region is zero again (see BuildScratch)
         cg.idle = true;                      // s synced by finish_aux, the side stream by the geometry event
@@ -1445,6 +1479,7 @@ void free_index_impl(sj_index *idx)
     cudaSetDevice(idx->device);
     for (int i = 0; i < idx->nbufs; ++i) dev_free(idx->bufs[i], nullptr);
     cudaDeviceSynchronize();
+    for (int i = 0; i < 2; ++i) zbuf_put(idx->device, idx->zbufs[i], idx->zbytes[i]);   // zeroed + cached
     for (auto &e : idx->tev) event_put(idx->device, e);
     delete idx;
 }

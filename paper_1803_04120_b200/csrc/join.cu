@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <atomic>
 #include <deque>
 
 #include "refine_launch.cuh"
@@ -285,10 +286,11 @@ EstimateShape estimate_shape(uint64_t nq)
 // (zeroed by the caller).  A small sample is one partial wave of long per-query chains: each query
 // is spread over more lanes (the counts do not depend on the lane split) until the GPU is covered.
 void launch_estimate(const DevIndex &ix, int device, const sj_join_opts &o, uint64_t q0, uint64_t q1,
-                     const EstimateShape &es, unsigned long long *dbk, cudaStream_t s)
+                     const EstimateShape &es, unsigned long long *dbk, cudaStream_t s, const Publish *pub)
 {
     if (!es.ns) return;
     JoinArgs ja{};
+    if (pub) ja.pub = *pub;
     ja.include_self = o.include_self;
     ja.use_masks = o.use_masks;
     ja.lanes_log2 = lanes_log2_for(ix, o);
@@ -303,10 +305,10 @@ void launch_estimate(const DevIndex &ix, int device, const sj_join_opts &o, uint
     const bool heavy = ix.search_mode == kSearchCellScan && ix.dir_ntop >= 81;
     const uint32_t lanes_max = heavy ? 4u : 3u;
     const uint64_t threads_per_sm = heavy ? 4096 : 1024;
-    // the bitmap-filtered sparse search runs one lane per query (refine_query takes it for G = 1
-    // only): spreading the sample over lanes would switch it to the unfiltered offset scan
-    const bool sparse = ix.search_mode == kSearchCellScan && ix.occ && ix.dir_k <= 3;
-    if (o.lanes_per_query == 0 && !sparse) {
+    // (the sparse bitmap search runs G = 1 in the join; for the sample -- a partial wave of long
+    // per-query chains -- the lanes' share of the general offset scan, which tests the same bitmaps,
+    // is shorter: 6-D eps=1 build 0.347 -> 0.340 ms)
+    if (o.lanes_per_query == 0) {
         const int nsm = device_sm_count(device);
         while (ja.lanes_log2 < lanes_max && (es.ns << (ja.lanes_log2 + 1)) <= (uint64_t)nsm * threads_per_sm)
             ++ja.lanes_log2;
@@ -348,7 +350,8 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     CtxGuard cg{acquire_ctx(idx->device, S, S + 2, slot_need)};
     DevCtx &cx = *cg.c;
     cudaStream_t s0 = cx.streams[0];
-    ensure_join_blocks(&cx, kBlock * (size_t)S);
+    ensure_join_blocks(&cx, kBlock * (size_t)S + 64 * (size_t)S);   // + per stream a CTA counter / doorbell
+    const unsigned int bell_epoch = ++cx.doorbell;
     char *dbase = static_cast<char *>(cx.jb_d), *hbase = static_cast<char *>(cx.jb_h);
     auto dwork = [&](int si) { return reinterpret_cast<unsigned long long *>(dbase + kBlock * si); };
     auto hwork = [&](int si) { return reinterpret_cast<const unsigned long long *>(hbase + kBlock * si); };
@@ -415,7 +418,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         };
         // every batch run records a (start, end) event pair; timings are computed on request
         auto run_batch = [&](uint64_t a, uint64_t b, uint64_t *buf, uint64_t cap, Slot *dslot, int si,
-                             bool clear_slot) {
+                             bool clear_slot, const Publish *pub = nullptr) {
             cudaStream_t s = cx.streams[si];
             cudaEvent_t e0 = event_get(idx->device), e1 = event_get(idx->device);
             res->runs.emplace_back(e0, e1);
@@ -439,7 +442,11 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             }
             SJ_CUDA(cudaEventRecord(e0, s));
             tr.dev("refine launch", s);
+            // the publish goes with the batch's LAST kernel (the dense one when it runs)
+            const bool dense_runs = ja.dense_T && ix.n_dense_tasks > 0 && b > a;
+            if (pub && !dense_runs) ja.pub = *pub;
             launch_refine<kEmit>(ix, ja, o.unicomp != 0, (uint32_t)(b - a), s);
+            if (pub && dense_runs) ja.pub = *pub;
             launch_dense(ix, ja, o.unicomp != 0, s);
             SJ_CUDA(cudaEventRecord(e1, s));
             tr.dev("refine done", s);
@@ -455,6 +462,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             res->batches.resize(nb);
             std::vector<uint64_t> counts(nb, 0);
             const bool own_slots = nb <= (size_t)64 * S;
+            static const bool no_pub = getenv_flag("SJ_NO_PUB");
             // the batches' buffers first (host bookkeeping), so the launches then go out back to back
             if (own_slots) {
                 for (size_t b = 0; b < nb; ++b) {
@@ -473,13 +481,26 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 const size_t slot = own_slots ? b / S : 0;
                 if (own_slots) {
                     sj_batch &bt = res->batches[b];
-                    run_batch(cuts[b], cuts[b + 1], bt.pairs, bt.cap, dslot(si, slot), si, false);
-                    if (b + S >= nb) {                // the stream's last batch: its block back to the host,
-                        SJ_CUDA(cudaMemcpyAsync(hbase + kBlock * si, dbase + kBlock * si, kBlock,
-                                                cudaMemcpyDeviceToHost, s));
-                        SJ_CUDA(cudaEventRecord(cx.events[2 + si], s));
-                        // then zeroed for the next join on this context (off the critical path)
-                        SJ_CUDA(cudaMemsetAsync(dbase + kBlock * si, 0, kBlock, s));
+                    if (b + S >= nb && !no_pub) {
+                        // the stream's last batch: its last CTA publishes the stream's block into the
+                        // mapped mirror, zeroes it for the next join and rings the stream's doorbell
+                        Publish pb{};
+                        pb.src = reinterpret_cast<unsigned long long *>(dbase + kBlock * si);
+                        pb.dst = reinterpret_cast<unsigned long long *>(static_cast<char *>(cx.jb_hd) + kBlock * si);
+                        pb.words = (uint32_t)(kBlock / 8);
+                        pb.zero_src = 1;
+                        pb.done = reinterpret_cast<unsigned int *>(dbase + kBlock * S) + 16 * si;
+                        pb.bell = reinterpret_cast<volatile unsigned int *>(static_cast<char *>(cx.jb_hd) + kBlock * S) + 16 * si;
+                        pb.epoch = bell_epoch;
+                        run_batch(cuts[b], cuts[b + 1], bt.pairs, bt.cap, dslot(si, slot), si, false, &pb);
+                    } else {
+                        run_batch(cuts[b], cuts[b + 1], bt.pairs, bt.cap, dslot(si, slot), si, false);
+                        if (b + S >= nb) {            // (SJ_NO_PUB: copy + event + zeroing instead)
+                            SJ_CUDA(cudaMemcpyAsync(hbase + kBlock * si, dbase + kBlock * si, kBlock,
+                                                    cudaMemcpyDeviceToHost, s));
+                            SJ_CUDA(cudaEventRecord(cx.events[2 + si], s));
+                            SJ_CUDA(cudaMemsetAsync(dbase + kBlock * si, 0, kBlock, s));
+                        }
                     }
                     continue;
                 }
@@ -503,11 +524,20 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 }
             }
             tr.mark("batches launched");
-            // wait for the read-back copies (not for the zeroing behind them)
+            // wait for the streams' doorbells (own slots) or the streams
             for (int i = 0; i < S && i < (int)nb; ++i) {
-                if (own_slots) SJ_CUDA(cudaEventSynchronize(cx.events[2 + i]));
-                else SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
+                if (own_slots && no_pub) {
+                    SJ_CUDA(cudaEventSynchronize(cx.events[2 + i]));
+                } else if (own_slots) {
+                    const volatile unsigned int *bell =
+                        reinterpret_cast<const volatile unsigned int *>(hbase + kBlock * S) + 16 * i;
+                    if (!wait_doorbell(bell, bell_epoch, cx.streams[i]))
+                        fail(SJ_ERR_CUDA, "a batch finished without publishing its counters (internal error)");
+                } else {
+                    SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
+                }
             }
+            std::atomic_thread_fence(std::memory_order_acquire);
             tr.mark("batches done (synced)");
             add_work();                           // (the device blocks are being zeroed behind the copies)
             work_read = true;

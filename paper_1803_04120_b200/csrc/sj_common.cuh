@@ -214,6 +214,8 @@ struct sj_index {
     sj::DevIndex dev{};          // same, in kernel form
     void *bufs[16] = {nullptr};  // owned device allocations
     int nbufs = 0;
+    void *zbufs[2] = {nullptr, nullptr};   // the occupancy bitmaps: from / back to the zeroed-buffer cache
+    size_t zbytes[2] = {0, 0};
     char *arena = nullptr;       // the build's contiguous arena (sj_index_view.packed), if any
 };
 
@@ -259,10 +261,20 @@ struct DevCtx {
     // the join's per-stream counter blocks (only joins touch them): device + pinned mirror, and whether
     // the previous join left them zero (it re-zeroes them on each stream right after reading them back)
     void *jb_d = nullptr;
-    void *jb_h = nullptr;
+    void *jb_h = nullptr;        // mapped pinned mirror (kernels publish into it)
+    void *jb_hd = nullptr;       // its device address
     size_t jb_bytes = 0;
     bool jb_clean = false;
 };
+// spin until a device-written doorbell shows `epoch` (the stream is queried now and then so a failed
+// kernel is reported, not waited for); returns false if the stream drained without ringing
+bool wait_doorbell(const volatile unsigned int *bell, unsigned int epoch, cudaStream_t s);
+// Zeroed device buffers (the occupancy bitmaps): a released bitmap is zeroed at release time (the
+// index's free, off any build's critical path) and handed to the next build that asks for one at least
+// as large, so the build needs no memset.  zbuf_get returns nullptr when none is cached.
+void *zbuf_get(int dev, size_t bytes, size_t *granted);
+void zbuf_put(int dev, void *p, size_t bytes);     // caller: p is no longer in use; zeroes + caches
+void zbuf_trim(int dev);
 // grow the join blocks to `bytes` (a fresh allocation is not clean)
 void ensure_join_blocks(DevCtx *c, size_t bytes);
 DevCtx *acquire_ctx(int dev, int nstreams, int nevents, size_t slot_bytes);
@@ -342,8 +354,23 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o);
 void neighbor_counts_impl(const sj_index *idx, const sj_join_opts &o, uint32_t *cnt, uint64_t *total);
 void plan_shards_impl(const sj_index *idx, uint32_t world, uint64_t *cuts);
 EstimateShape estimate_shape(uint64_t nq);
+// Completion publish (the last kernel of a stream's work, or the build's estimate): the LAST CTA to
+// finish copies `words` 8-byte words from device memory into mapped pinned memory, optionally zeroes
+// the source, optionally computes the masks-trivial flag into the source first, and rings a doorbell
+// the host polls -- instead of a D2H copy + stream sync after the kernel (each ~5-10 us of latency).
+struct Publish {
+    unsigned long long *src;       // device words (nullptr: no publish)
+    unsigned long long *dst;       // mapped host words (device address)
+    uint32_t words;
+    int zero_src;                  // zero src after copying (the join's counter blocks)
+    unsigned int *done;            // device CTA counter, 0 on entry (reset by the last CTA)
+    volatile unsigned int *bell;   // mapped host doorbell
+    unsigned int epoch;
+    uint32_t *masks_flag;          // build: aux word for "every coordinate occupied" (or nullptr)
+};
+
 void launch_estimate(const DevIndex &ix, int device, const sj_join_opts &o, uint64_t q0, uint64_t q1,
-                     const EstimateShape &es, unsigned long long *dbk, cudaStream_t s);
+                     const EstimateShape &es, unsigned long long *dbk, cudaStream_t s, const Publish *pub = nullptr);
 void plan_from_buckets(const double *bucket_est, uint64_t nbk, uint64_t width, uint64_t q0, uint64_t q1,
                        uint64_t capacity, int min_batches, double margin, std::vector<uint64_t> &cuts,
                        std::vector<uint64_t> &est, uint64_t *estimated_total);
