@@ -337,6 +337,20 @@ __device__ __noinline__ void geometry_products(const uint64_t *cpd, int d, uint3
     G.masks_on = want_masks && mt <= 32ull * kSmemMaskWords;
 }
 
+// floor(fl(t / w)) for t >= 0 (reading R7's rounded quotient) without a division in the common case:
+// y = fl(t * fl(1/w)) is within 1.5 * 2^-52 * t/w of t/w and the correctly rounded fl(t/w) within
+// 2^-53 * t/w, so both lie in [y - d, y + d] with d = 2^-49 y (the computed ends, rounded, still
+// bracket that); when floor() is the same at both ends it is the floor of fl(t/w).  Otherwise (y within
+// ~2^-49 relative of an integer) the exact division decides.  Pinned by the bit-exact index tests.
+__device__ __forceinline__ double cell_floor(double t, double w, double inv_w)
+{
+    const double y = __dmul_rn(t, inv_w);
+    const double d = __dmul_rn(y, 0x1p-49);
+    const double lo = floor(__dsub_rn(y, d));
+    if (lo == floor(__dadd_rn(y, d))) return lo;
+    return floor(__ddiv_rn(t, w));
+}
+
 // Cell coordinate c_j = 1 + floor(fl(fl(x_j - min_j) / w))  (reading R7), linear id with
 // dimension 1 fastest (R8): key = sum_j c_j * stride_j (exact: < prod |g_j| < 2^64).
 // Masks M_j as one bitmap over all dimensions (bit mask_off[j] + c): each CTA ORs
@@ -381,6 +395,7 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
     const bool use_masks = g->masks_on != 0;
     const bool use_hist = g->use_bucket != 0;
     const int dir_k = g->k;
+    const double inv_w = 1.0 / g->w;
     const double w = g->w;
     const uint32_t mask_words = (uint32_t)((g->mask_off[D] + 31) / 32);
     if (threadIdx.x < D) {
@@ -402,7 +417,7 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
         for (int jj = 0; jj < D; ++jj) {
             const int j = D - 1 - jj;
             const double x = xr[j];
-            const double t = floor(__ddiv_rn(__dsub_rn(x, s_min[j]), w));
+            const double t = cell_floor(__dsub_rn(x, s_min[j]), w, inv_w);
             const uint64_t c = 1ull + (uint64_t)t;
             key += c * s_str[j];
             prefix += c * s_pstr[j];

@@ -585,3 +585,31 @@ def test_torch_allocator_hook(sj):
     # and the library's own pool again
     idx = sj.build_index(P, 4.0)
     assert np.array_equal(sj.self_join(idx).to_numpy(), want)
+
+
+def test_cell_coordinates_at_cell_boundaries(sj):
+    """The key pass's division-free c_j (cell_floor: fl(t * fl(1/w)) with an exact-division fallback
+    near integers) against the oracle's floor(fl(t / w)) on coordinates AT the cell boundaries:
+    k * w and its neighbours within +-3 ulps for every k, so t / w sits within ulps of integers."""
+    rng = np.random.default_rng(1234)
+    for d, eps in ((3, 0.7), (6, 3.3), (2, 0.013)):
+        base = np.array([[0.0] * d, [100.0] * d])
+        w = ir.build_index(base, eps).geom.w
+        vals = []
+        for k in range(0, int(100.0 / w) + 1):
+            x = k * w
+            for s in range(-3, 4):
+                y = x
+                for _ in range(abs(s)):
+                    y = np.nextafter(y, np.inf if s > 0 else -np.inf)
+                if 0.0 <= y <= 100.0:
+                    vals.append(y)
+        vals = np.array(vals)
+        pts = np.vstack([base, vals[rng.integers(0, len(vals), (4000, d))]])
+        ref = ir.build_index(pts, eps)
+        assert ref.geom.w == w
+        idx = sj.build_index(torch.from_numpy(pts).cuda(), eps)
+        arr = idx.arrays()
+        assert arr["B"].cpu().numpy().tolist() == ref.B
+        assert np.array_equal(arr["A"].cpu().numpy().astype(np.int64), ref.A)
+        assert np.array_equal(sj.self_join(idx).to_numpy(), oracle.grid_join(pts, eps))
