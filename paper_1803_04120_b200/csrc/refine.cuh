@@ -71,7 +71,10 @@ struct JoinArgs {
 // the round trip of that atomic -- contended by every warp of the launch -- is off the warp's
 // critical path (ncu: 23% of the dense kernel's stall samples sat on the flush's shuffle of the
 // returned base).  Every reservation covers exactly the pairs it is for, so the batch stays dense.
-constexpr int kWarpBufPairs = 1024;
+#ifndef SJ_RING
+#define SJ_RING 1024
+#endif
+constexpr int kWarpBufPairs = SJ_RING;   // power of two >= 512
 struct WarpBuf {
     uint64_t *buf;        // [kWarpBufPairs] ring in shared memory
     double *tx;           // [D][32] candidate tile (SoA)
@@ -232,18 +235,23 @@ __device__ __forceinline__ void emit_tile(const JoinArgs &ja, WarpBuf &wb, uint3
     constexpr uint32_t R = (uint32_t)kWarpBufPairs;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t sbuf = (uint32_t)__cvta_generic_to_shared(wb.buf);
-#pragma unroll 1
-    for (int part = 0; part < 2; ++part) {
-        uint32_t m = hm;
-        uint32_t n = __popc(m) * per;
-        uint32_t total = __reduce_add_sync(0xffffffffu, n);
-        if (total == 0u) return;
-        if (total > R) {                                 // split: the low half now, the high half next
-            m = hm & 0xFFFFu;
-            n = __popc(m) * per;
-            total = __reduce_add_sync(0xffffffffu, n);
+    // chunks of cw candidates, each fitting the ring: 32, else 16 if both halves fit, else 8 (a chunk
+    // of 8 yields <= 32 * 8 * per <= 512 pairs)
+    uint32_t cw = 32;
+    {
+        const uint32_t t = __reduce_add_sync(0xffffffffu, __popc(hm) * per);
+        if (t == 0u) return;
+        if (t > R) {
+            const uint32_t tlo = __reduce_add_sync(0xffffffffu, __popc(hm & 0xFFFFu) * per);
+            cw = (tlo <= R && t - tlo <= R) ? 16u : 8u;
         }
-        hm &= ~m;
+    }
+#pragma unroll 1
+    for (uint32_t c = 0; c < 32u; c += cw) {
+        uint32_t m = cw == 32u ? hm : hm & (((1u << cw) - 1u) << c);
+        const uint32_t n = __popc(m) * per;
+        const uint32_t total = __reduce_add_sync(0xffffffffu, n);
+        if (total == 0u) continue;
         uint32_t inc = n;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -900,7 +908,10 @@ __device__ __forceinline__ void publish_epilogue(const DevIndex &ix, const Publi
 // shared-memory buffer (one cursor atomic per flush instead of one per candidate step).
 constexpr int kDenseWarps = 8;
 template <int D, bool UNICOMP>
-__global__ void __launch_bounds__(32 * kDenseWarps, D <= 3 ? 3 : 2)   // 3 CTAs/SM: smem fits up to d = 4, registers (80) up to d = 3
+#ifndef SJ_DENSE_MINB
+#define SJ_DENSE_MINB 3
+#endif
+__global__ void __launch_bounds__(32 * kDenseWarps, D <= 3 ? SJ_DENSE_MINB : 2)   // 3 CTAs/SM: smem fits up to d = 4, registers (80) up to d = 3
 k_refine_dense(const DevIndex ix, const JoinArgs ja)
 {
     // dynamic shared memory: [rings | tiles | ids] (dense_smem_per_warp each warp) and, in the

@@ -6,7 +6,7 @@ SRCS=$(python -c "import os; from paper_1803_04120_b200 import build as b; print
 mkdir -p build/variants
 while [ $# -gt 1 ]; do
   name=$1; defs=$2; shift 2
-  /usr/local/cuda/bin/nvcc $FLAGS $defs $SRCS -o build/variants/libsj_$name.so &
+  /usr/local/cuda/bin/nvcc $FLAGS $defs $SRCS -shared -cudart static -o build/variants/libsj_$name.so &
 done
 wait
 ls -la build/variants
