@@ -65,6 +65,36 @@ void ensure_join_blocks(DevCtx *c, size_t bytes)
     c->jb_bytes = b;
 }
 
+namespace {
+__global__ void __launch_bounds__(256) k_publish(const Publish p)
+{
+    if (p.masks_flag) {                           // masks M_j trivial? (the build's estimate only)
+        __shared__ int s_bad;
+        if (threadIdx.x == 0) s_bad = 0;
+        __syncthreads();
+        for (int j = 0; j < p.d; ++j)
+            for (uint64_t b = p.mask_lo[j] + threadIdx.x; b <= p.mask_hi[j]; b += blockDim.x)
+                if (!((__ldcg(p.masks + (b >> 5)) >> (b & 31)) & 1u)) s_bad = 1;
+        __syncthreads();
+        if (threadIdx.x == 0) *p.masks_flag = s_bad ? 0u : 1u;
+        __syncthreads();
+    }
+    for (uint32_t i = threadIdx.x; i < p.words; i += blockDim.x) {
+        p.dst[i] = __ldcg(p.src + i);
+        if (p.zero_src) p.src[i] = 0ull;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) *p.bell = p.epoch;
+}
+}  // namespace
+
+void launch_publish(const Publish &p, cudaStream_t s)
+{
+    k_publish<<<1, 256, 0, s>>>(p);
+    SJ_LAUNCHED();
+}
+
 bool wait_doorbell(const volatile unsigned int *bell, unsigned int epoch, cudaStream_t s)
 {
     uint64_t spins = 0;

@@ -1428,10 +1428,15 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
             pub.dst = reinterpret_cast<unsigned long long *>(static_cast<char *>(dh) + kEstOffset);
             pub.words = (uint32_t)((kAuxEstOffset + 8 * es_spec.nbk) / 8);
             pub.zero_src = 0;
-            pub.done = reinterpret_cast<unsigned int *>(static_cast<char *>(cg.c->d_slots) + kGeomOffset + 4096 - 32);
             pub.bell = reinterpret_cast<volatile unsigned int *>(static_cast<char *>(dh) + kBellOffset + 64);
             pub.epoch = ++cg.c->doorbell;
             pub.masks_flag = (masks && masks == small_masks) ? aux + 4 : nullptr;
+            pub.masks = masks;
+            pub.d = d;
+            for (int j = 0; j < d; ++j) {
+                pub.mask_lo[j] = v.mask_offsets[j] + 1;
+                pub.mask_hi[j] = v.mask_offsets[j] + v.cpd[j] - 2;
+            }
             launch_estimate(px, o.device, jo, 0, n, es_spec, dbk, s, &pub);
             tr.dev("speculative estimate", s);
         }

@@ -290,7 +290,6 @@ void launch_estimate(const DevIndex &ix, int device, const sj_join_opts &o, uint
 {
     if (!es.ns) return;
     JoinArgs ja{};
-    if (pub) ja.pub = *pub;
     ja.include_self = o.include_self;
     ja.use_masks = o.use_masks;
     ja.lanes_log2 = lanes_log2_for(ix, o);
@@ -314,6 +313,7 @@ void launch_estimate(const DevIndex &ix, int device, const sj_join_opts &o, uint
             ++ja.lanes_log2;
     }
     launch_refine<kCountQuery>(ix, ja, o.unicomp != 0, (uint32_t)es.ns, s);
+    if (pub) launch_publish(*pub, s);
 }
 
 // The build's speculative estimate is valid for a join with the default predicate options over
@@ -442,12 +442,9 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             }
             SJ_CUDA(cudaEventRecord(e0, s));
             tr.dev("refine launch", s);
-            // the publish goes with the batch's LAST kernel (the dense one when it runs)
-            const bool dense_runs = ja.dense_T && ix.n_dense_tasks > 0 && b > a;
-            if (pub && !dense_runs) ja.pub = *pub;
             launch_refine<kEmit>(ix, ja, o.unicomp != 0, (uint32_t)(b - a), s);
-            if (pub && dense_runs) ja.pub = *pub;
             launch_dense(ix, ja, o.unicomp != 0, s);
+            if (pub) launch_publish(*pub, s);      // the stream's counters to the host behind the batch
             SJ_CUDA(cudaEventRecord(e1, s));
             tr.dev("refine done", s);
             ++launches;
@@ -489,7 +486,6 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                         pb.dst = reinterpret_cast<unsigned long long *>(static_cast<char *>(cx.jb_hd) + kBlock * si);
                         pb.words = (uint32_t)(kBlock / 8);
                         pb.zero_src = 1;
-                        pb.done = reinterpret_cast<unsigned int *>(dbase + kBlock * S) + 16 * si;
                         pb.bell = reinterpret_cast<volatile unsigned int *>(static_cast<char *>(cx.jb_hd) + kBlock * S) + 16 * si;
                         pb.epoch = bell_epoch;
                         run_batch(cuts[b], cuts[b + 1], bt.pairs, bt.cap, dslot(si, slot), si, false, &pb);

@@ -38,7 +38,6 @@ namespace sj {
 enum RefineMode { kEmit = 0, kCountQuery = 1, kCountPoint = 2 };
 
 struct JoinArgs {
-    Publish pub;                   // see Publish (zero: none)
     uint64_t *out;                 // kEmit: batch pair buffer
     unsigned long long *cursor;    // kEmit: pairs emitted (exact even on overflow)
     uint64_t cap;                  // kEmit: capacity of out
@@ -864,44 +863,6 @@ __device__ __forceinline__ void flush_work(const JoinArgs &ja, unsigned long lon
     }
 }
 
-// Called by every thread of every CTA at the very end of a refine kernel.
-__device__ __forceinline__ void publish_epilogue(const DevIndex &ix, const Publish &p)
-{
-    if (!p.src) return;
-    __shared__ int s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();                          // this CTA's counter / bucket atomics before its ticket
-        s_last = atomicAdd(p.done, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (p.masks_flag) {                           // masks M_j trivial? (the build's estimate only)
-        __shared__ int s_bad;
-        if (threadIdx.x == 0) s_bad = 0;
-        __syncthreads();
-        for (int j = 0; j < ix.d; ++j) {
-            const uint64_t lo = ix.mask_off[j] + 1, hi = ix.mask_off[j] + ix.cpd[j] - 2;
-            for (uint64_t b = lo + threadIdx.x; b <= hi; b += blockDim.x)
-                if (!((__ldcg(ix.masks + (b >> 5)) >> (b & 31)) & 1u)) s_bad = 1;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) *p.masks_flag = s_bad ? 0u : 1u;
-        __syncthreads();
-    }
-    for (uint32_t i = threadIdx.x; i < p.words; i += blockDim.x) {
-        p.dst[i] = __ldcg(p.src + i);
-        if (p.zero_src) p.src[i] = 0ull;
-    }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        *p.done = 0u;
-        *p.bell = p.epoch;
-    }
-}
-
 // Dense kernel (kEmit): one warp per task = up to 32 consecutive queries of one populous cell
 // (>= dense_T points).  All lanes share the home cell, so the whole neighbour enumeration and every
 // candidate loop are warp-uniform: candidates are broadcast loads, hits go through the per-warp
@@ -965,7 +926,6 @@ k_refine_dense(const DevIndex ix, const JoinArgs ja)
     }
     ring_drain(ja, wb);                                // the ring lives across the warp's tasks
     flush_work(ja, q.probes, q.tests, q.emitted);
-    publish_epilogue(ix, ja.pub);
 }
 
 // MINB: CTAs per SM the register budget is sized for -- kRefineMinBlocks (5) in general; 6 for the
@@ -1014,7 +974,6 @@ k_refine(const DevIndex ix, const JoinArgs ja)
         if (active && q.sub == 0) atomicAdd(ja.qbucket + qi / ja.group, (unsigned long long)e);
     }
     flush_work(ja, q.probes, q.tests, q.emitted);
-    publish_epilogue(ix, ja.pub);
 }
 
 // ---------------------------------------------------------------- queued cell scan (many offsets)
@@ -1306,7 +1265,6 @@ k_refine_q(const DevIndex ix, const JoinArgs ja)
         if (active && q.sub == 0) atomicAdd(ja.qbucket + qi / ja.group, (unsigned long long)e);
     }
     flush_work(ja, q.probes, q.tests, q.emitted);
-    publish_epilogue(ix, ja.pub);
 }
 
 }  // namespace sj

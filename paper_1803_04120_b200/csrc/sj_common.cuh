@@ -354,20 +354,25 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o);
 void neighbor_counts_impl(const sj_index *idx, const sj_join_opts &o, uint32_t *cnt, uint64_t *total);
 void plan_shards_impl(const sj_index *idx, uint32_t world, uint64_t *cuts);
 EstimateShape estimate_shape(uint64_t nq);
-// Completion publish (the last kernel of a stream's work, or the build's estimate): the LAST CTA to
-// finish copies `words` 8-byte words from device memory into mapped pinned memory, optionally zeroes
-// the source, optionally computes the masks-trivial flag into the source first, and rings a doorbell
-// the host polls -- instead of a D2H copy + stream sync after the kernel (each ~5-10 us of latency).
+// Completion publish: a one-CTA kernel (k_publish) launched right behind the work it reports, on the
+// same stream (a stream's last batch, or the build's estimate), copies `words` 8-byte words from
+// device memory into mapped pinned memory, optionally zeroes the source, optionally computes the
+// masks-trivial flag into the source first, and rings a doorbell the host polls -- instead of a D2H
+// copy + stream sync (each ~5-10 us of latency).  (An epilogue inside the refine kernels raised their
+// register spills: 6-D eps=8 join 4.1 -> 6.0 ms.)
 struct Publish {
     unsigned long long *src;       // device words (nullptr: no publish)
     unsigned long long *dst;       // mapped host words (device address)
     uint32_t words;
     int zero_src;                  // zero src after copying (the join's counter blocks)
-    unsigned int *done;            // device CTA counter, 0 on entry (reset by the last CTA)
     volatile unsigned int *bell;   // mapped host doorbell
     unsigned int epoch;
     uint32_t *masks_flag;          // build: aux word for "every coordinate occupied" (or nullptr)
+    const uint32_t *masks;         //   the masks and, per dimension, the bit range [lo, hi] of the
+    int d;                         //   coordinates 1 .. |g_j|-2 that must all be set
+    uint64_t mask_lo[SJ_MAX_DIM], mask_hi[SJ_MAX_DIM];
 };
+void launch_publish(const Publish &p, cudaStream_t s);
 
 void launch_estimate(const DevIndex &ix, int device, const sj_join_opts &o, uint64_t q0, uint64_t q1,
                      const EstimateShape &es, unsigned long long *dbk, cudaStream_t s, const Publish *pub = nullptr);
