@@ -48,3 +48,26 @@ def test_no_fma_in_predicate_kernels(sass):
     # refine: 5 dims x (emit/count-query/count-point) x unicomp on/off (+ 6-CTA variants);
     # dense refine: 5 x 2; brute force: 5
     assert checked >= 30, checked
+
+
+def test_refine_kernels_do_not_spill_heavily():
+    """Guard against code that silently raises the refine kernels' register spills (an epilogue added
+    to them once took the 6-D eps=8 join from 4.1 to 6.0 ms): every k_refine* kernel keeps a small
+    stack frame (their budget is <= 51 / 80 / 128 registers by launch bounds)."""
+    from paper_1803_04120_b200 import build as b
+    lib = b.build()
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([tool, "--dump-resource-usage", lib], capture_output=True, text=True).stdout
+    fn = None
+    worst = {}
+    for line in out.splitlines():
+        m = re.search(r"Function (\S+):", line)
+        if m:
+            fn = m.group(1)
+            continue
+        m = re.search(r"STACK:(\d+)", line)
+        if m and fn and "k_refine" in fn:
+            worst[fn] = int(m.group(1))
+    assert worst, "no refine kernels found"
+    bad = {k: v for k, v in worst.items() if v > 256}
+    assert not bad, bad
