@@ -79,9 +79,32 @@ __global__ void __launch_bounds__(256) k_publish(const Publish p)
         if (threadIdx.x == 0) *p.masks_flag = s_bad ? 0u : 1u;
         __syncthreads();
     }
-    for (uint32_t i = threadIdx.x; i < p.words; i += blockDim.x) {
-        p.dst[i] = __ldcg(p.src + i);
-        if (p.zero_src) p.src[i] = 0ull;
+    if (p.reduce_slots) {
+        // work counters: 4 sums over reduce_slots slots of 4 words, then the cursor slots
+        __shared__ unsigned long long s_sum[4][8];
+        unsigned long long a[4] = {0, 0, 0, 0};
+        for (uint32_t sl = threadIdx.x; sl < p.reduce_slots; sl += blockDim.x)
+            for (int c = 0; c < 4; ++c) a[c] += __ldcg(p.src + 4 * sl + c);
+        for (int c = 0; c < 4; ++c) {
+            for (int o = 16; o; o >>= 1) a[c] += __shfl_xor_sync(0xffffffffu, a[c], o);
+            if ((threadIdx.x & 31) == 0) s_sum[c][threadIdx.x >> 5] = a[c];
+        }
+        __syncthreads();
+        if (threadIdx.x < 4) {
+            unsigned long long t = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_sum[threadIdx.x][w];
+            p.dst[threadIdx.x] = t;
+        }
+        const unsigned long long *slots = p.src + 4 * p.reduce_slots;
+        for (uint32_t i = threadIdx.x; i < 2 * p.nslots; i += blockDim.x) p.dst[4 + i] = __ldcg(slots + i);
+        __syncthreads();
+        if (p.zero_src)
+            for (uint32_t i = threadIdx.x; i < p.words; i += blockDim.x) p.src[i] = 0ull;
+    } else {
+        for (uint32_t i = threadIdx.x; i < p.words; i += blockDim.x) {
+            p.dst[i] = __ldcg(p.src + i);
+            if (p.zero_src) p.src[i] = 0ull;
+        }
     }
     __threadfence_system();
     __syncthreads();

@@ -486,6 +486,8 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                         pb.dst = reinterpret_cast<unsigned long long *>(static_cast<char *>(cx.jb_hd) + kBlock * si);
                         pb.words = (uint32_t)(kBlock / 8);
                         pb.zero_src = 1;
+                        pb.reduce_slots = kWorkSlots;
+                        pb.nslots = (uint32_t)((nb - 1 - si) / S + 1);     // this stream's batches
                         pb.bell = reinterpret_cast<volatile unsigned int *>(static_cast<char *>(cx.jb_hd) + kBlock * S) + 16 * si;
                         pb.epoch = bell_epoch;
                         run_batch(cuts[b], cuts[b + 1], bt.pairs, bt.cap, dslot(si, slot), si, false, &pb);
@@ -535,10 +537,22 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             }
             std::atomic_thread_fence(std::memory_order_acquire);
             tr.mark("batches done (synced)");
-            add_work();                           // (the device blocks are being zeroed behind the copies)
+            const bool published = own_slots && !no_pub;
+            if (published) {
+                // each stream's published [work sums | cursor slots]
+                for (int i = 0; i < S && i < (int)nb; ++i) {
+                    const unsigned long long *pw = reinterpret_cast<const unsigned long long *>(hbase + kBlock * i);
+                    for (int c = 0; c < 3; ++c) wsum[c] += pw[c];
+                }
+            } else {
+                add_work();                       // (the device blocks are being zeroed behind the copies)
+            }
             work_read = true;
             cudaStream_t st_sort = s0;
-            if (own_slots) {
+            if (published) {
+                for (size_t b = 0; b < nb; ++b)
+                    counts[b] = reinterpret_cast<const unsigned long long *>(hbase + kBlock * (b % S))[4 + 2 * (b / S)];
+            } else if (own_slots) {
                 for (size_t b = 0; b < nb; ++b) counts[b] = hslot((int)(b % S), b / S)->cursor;
             } else {
                 for (size_t b = (nb > (size_t)S ? nb - S : 0); b < nb; ++b) counts[b] = hslot((int)(b % S), 0)->cursor;

@@ -367,6 +367,10 @@ struct Publish {
     int zero_src;                  // zero src after copying (the join's counter blocks)
     volatile unsigned int *bell;   // mapped host doorbell
     unsigned int epoch;
+    // join counter blocks: instead of the raw block, publish [sum of the work slots (4 words) | the
+    // first nslots cursor slots (2 words each)] -- 8 KB less over PCIe
+    uint32_t reduce_slots;         // work slots to sum (0: plain copy of `words`)
+    uint32_t nslots;
     uint32_t *masks_flag;          // build: aux word for "every coordinate occupied" (or nullptr)
     const uint32_t *masks;         //   the masks and, per dimension, the bit range [lo, hi] of the
     int d;                         //   coordinates 1 .. |g_j|-2 that must all be set
