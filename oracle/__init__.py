@@ -13,6 +13,10 @@ Contents, each citing the passage it follows (PAPER.md line numbers, SPEC.md as 
 * ``index_ref`` -- the grid index of §4.2-4.4 (geometry, cell coordinates, linearisation, B, G,
   A, M) and the Alg. 1 / Alg. 2 cell enumerations, in plain numpy / Python, following the
   paper's notation with the DESIGN.md readings R6-R13.
+* ``join_sets`` / ``knn`` -- the SURVEY.md §8(f) rank-4 variants on the same predicate
+  (``sj_variants_oracle.c``): the two-set similarity join J(Q,P) (reading R19) by
+  brute force or a sorted-tuple grid, and the kNN self-join (reading R20) by brute
+  force with ties broken by the smaller id.
 * ``expected_pairs_uniform`` -- the exact expectation of |S| for iid uniform points (SURVEY.md
   §8(c) P4), used as a statistical pin.
 
@@ -36,6 +40,7 @@ from . import index_ref  # noqa: F401  (re-export)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sj_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "sj_variants_oracle.c")]
 _LIB = os.path.join(_HERE, "libsj_oracle.so")
 _lib = None
 
@@ -45,9 +50,9 @@ CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fno-unsafe-math-optimi
 
 def build(force: bool = False) -> str:
     """Compile the C oracle (building the checker is not using it)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(f) for f in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, *_SRCS, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -68,6 +73,12 @@ def _load():
         lib.orc_grid_join.restype = i64
         lib.orc_grid_digest.argtypes = [p, i64, i32, dbl, i32, i64, i64, i32, p, p]
         lib.orc_grid_digest.restype = i64
+        lib.orc_join_sets_brute.argtypes = [p, i64, p, i64, i32, dbl, p, i64]
+        lib.orc_join_sets_brute.restype = i64
+        lib.orc_join_sets_grid.argtypes = [p, i64, p, i64, i32, dbl, i32, p, p, i64]
+        lib.orc_join_sets_grid.restype = i64
+        lib.orc_knn.argtypes = [p, i64, p, p, i64, i32, i32, i32, p, p]
+        lib.orc_knn.restype = i32
         lib.orc_mix.argtypes = [i32, ctypes.c_uint64]
         lib.orc_mix.restype = ctypes.c_uint64
         _lib = lib
@@ -216,3 +227,63 @@ def expected_pairs_uniform(n: int, d: int, eps: float, L: float = 100.0) -> floa
         F += ((-1) ** k) * math.comb(d, k) * math.pi ** ((d - k) / 2) / math.gamma(1 + (d + k) / 2) \
             * r ** (d + k)
     return n + n * (n - 1) * F
+
+
+def join_sets(queries, points, eps: float, method: str = "grid", nthreads: int | None = None,
+              count_only: bool = False):
+    """J(Q,P) = {(i,k) : s(q_i,p_k) <= fl(eps^2)} packed (i<<32|k), sorted (sj_variants_oracle.c;
+    PAPER.md:52 "the related similarity join", reading R19).  method: "brute" (the definition
+    written out) or "grid" (sorted-tuple filter, full 3^d scan).  count_only: per-query counts."""
+    Q = _pts(queries)
+    P = _pts(points)
+    if Q.shape[1] != P.shape[1]:
+        raise ValueError("dimension mismatch")
+    nq, d = Q.shape
+    n = P.shape[0]
+    lib = _load()
+    if method == "brute":
+        if count_only:
+            raise ValueError("count_only needs method='grid'")
+        total = lib.orc_join_sets_brute(_ptr(Q), nq, _ptr(P), n, d, float(eps), None, 0)
+        if total < 0:
+            raise ValueError("bad arguments")
+        out = np.empty(total, dtype=np.uint64)
+        lib.orc_join_sets_brute(_ptr(Q), nq, _ptr(P), n, d, float(eps), _ptr(out), total)
+        return out
+    nthreads = nthreads or default_threads()
+    counts = np.zeros(nq, dtype=np.int64)
+    total = lib.orc_join_sets_grid(_ptr(Q), nq, _ptr(P), n, d, float(eps), nthreads, _ptr(counts), None, 0)
+    if total < 0:
+        raise ValueError("bad arguments")
+    if count_only:
+        return counts
+    out = np.empty(total, dtype=np.uint64)
+    got = lib.orc_join_sets_grid(_ptr(Q), nq, _ptr(P), n, d, float(eps), nthreads, None, _ptr(out), total)
+    assert got == total
+    return out
+
+
+def knn(points, k: int, qids: Iterable[int] | None = None, queries=None, nthreads: int | None = None):
+    """k nearest neighbours by brute force (sj_variants_oracle.c orc_knn, reading R20):
+    for each query, the k points of `points` with the smallest (s, id), s the predicate's distance.
+
+    Self kNN (queries=None): query i is points[i] for i in qids (default all) and excludes itself.
+    Two-set (queries given): rows of `queries`, nothing excluded.
+    Returns (ids int64 [nq, k] (-1 = fewer than k points), s float64 [nq, k] (+inf there))."""
+    P = _pts(points)
+    n, d = P.shape
+    if queries is None:
+        q = np.arange(n, dtype=np.int64) if qids is None else np.ascontiguousarray(np.asarray(list(qids) if not isinstance(qids, np.ndarray) else qids, dtype=np.int64))
+        Q = np.ascontiguousarray(P[q])
+        qself = q
+    else:
+        Q = _pts(queries)
+        qself = None
+    nq = Q.shape[0]
+    ids = np.empty((nq, k), dtype=np.int64)
+    s = np.empty((nq, k), dtype=np.float64)
+    rc = _load().orc_knn(_ptr(Q), nq, _ptr(qself) if qself is not None else None, _ptr(P), n, d, int(k),
+                         nthreads or default_threads(), _ptr(ids), _ptr(s))
+    if rc != 0:
+        raise ValueError("bad arguments")
+    return ids, s
