@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SJ_ABI_VERSION 4   /* 4: sj_join_opts.drain_csr, CSR batches, sj_dbscan, sj_result_counters */
+#define SJ_ABI_VERSION 5   /* 5: sj_join_sets, sj_knn_self; 4: drain_csr, CSR batches, sj_dbscan, sj_result_counters */
 #define SJ_MAX_DIM 6
 
 typedef enum {
@@ -273,6 +273,50 @@ sj_status sj_neighbor_counts(const sj_index *idx, const sj_join_opts *opts, uint
  * the paper's brute-force comparison, not for large N. */
 sj_status sj_brute_force_join(const double *points, uint64_t n, int d, double eps, const sj_build_opts *bopts,
                               const sj_join_opts *jopts, sj_result **out);
+
+/* ---- SURVEY §8(f) rank 4 variants on the same index and predicate --------------------------- */
+
+/* Two-set similarity join J(Q,P) ("the related similarity join"; R19): every
+ * ordered pair (i,k), i a row of `queries`, k an original id of the index's points P, with
+ * s(q_i,p_k) <= fl(eps^2) (the self-join's predicate and eps -- the index's), packed (i << 32) | k.
+ * Each query probes the 3^d cells around its own cell in P's grid (R7 against P's geometry; no
+ * unicomp, no self rule).  Two passes over the queries: exact per-query counts, then contiguous query
+ * ranges of <= batch_capacity_pairs pairs (and >= min_batches batches when there is output) filled
+ * with warp-aggregated emission -- exact sizes, no overflow re-runs.
+ *   queries : row-major nq x d float64, device memory on the index's device (queries_on_device = 1;
+ *             read after the work queued on the legacy default stream) or host memory (copied).
+ *   opts    : NULL = defaults; batch_capacity_pairs, min_batches, result_on_host and sort_pairs are
+ *             used; drain_csr must be 0; the query range / unicomp / include_self / masks / lanes /
+ *             dense options do not apply and are ignored.
+ *   *out    : a result like sj_self_join's (sj_result_* accessors, copy, CSR, fingerprints); its
+ *             n_points is max(nq, N).  sj_dbscan rejects it.  Blocks until complete.
+ * Errors: SJ_ERR_STATE (NULL index), SJ_ERR_ARG (nq >= 2^32, NULL queries with nq > 0, drain_csr,
+ *         capacity 0), SJ_ERR_NONFINITE (a query coordinate NaN / inf), SJ_ERR_NOMEM, SJ_ERR_CUDA. */
+sj_status sj_join_sets(const sj_index *idx, const double *queries, uint64_t nq, int queries_on_device,
+                       const sj_join_opts *opts, sj_result **out);
+
+typedef struct {
+    uint32_t rounds;             /* radius doublings + 1 (index builds)                             */
+    double eps_final;            /* radius of the last round                                        */
+    uint64_t cells_probed;       /* cell lookups over all rounds                                    */
+    uint64_t candidates_tested;  /* distance evaluations over all rounds                            */
+} sj_knn_stats;
+
+/* kNN self-join ("other spatial searches, such as kNN"; R20): for every point
+ * i the k points j != i with the smallest (s(p_i,p_j), j) -- s the self-join's rounded distance, ties
+ * to the smaller id -- written as row i of ids[n*k] (original ids) and dist2[n*k] (s), ascending.
+ * The ε-grid does it: an index with radius eps0; each point's k best among the points of its 3^d
+ * neighbour cells within eps are final when there are k of them (every other point fails the
+ * predicate); the rest are re-run on an index with 2*eps, until none is left.
+ *   points : row-major n x d float64, host or device per bopts->points_on_device.
+ *   k      : 1..32, k + 1 <= n < 2^32.       eps0: the first radius, finite, > 0 (about the k-th
+ *            neighbour distance is cheapest; too small costs rounds, too large costs candidates).
+ *   ids, dist2 : DEVICE memory on bopts->device, n*k uint32 / float64, caller-owned.
+ *   stats  : NULL or receives the rounds / final radius / work counters.
+ * Blocks until written.  Errors: SJ_ERR_ARG, SJ_ERR_DIM, SJ_ERR_NONFINITE (from the index build),
+ *         SJ_ERR_KEY_OVERFLOW (eps0 too small for the range), SJ_ERR_NOMEM, SJ_ERR_CUDA. */
+sj_status sj_knn_self(const double *points, uint64_t n, int d, uint32_t k, double eps0, const sj_build_opts *bopts,
+                      uint32_t *ids, double *dist2, sj_knn_stats *stats);
 
 /* Multi-GPU shard plan: cut the A-order queries [0, N) into `world` contiguous
  * ranges cuts[r] .. cuts[r+1] (cuts: world + 1 host uint64) of about equal estimated work, using

@@ -15,7 +15,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libsj.so")
 SOURCES = ["api.cu", "context.cu", "index_build.cu", "radix_sort.cu", "join.cu", "extras.cu", "diag.cu",
-           "refine_d2.cu", "refine_d3.cu", "refine_d4.cu", "refine_d5.cu", "refine_d6.cu", "dbscan.cu"]
+           "refine_d2.cu", "refine_d3.cu", "refine_d4.cu", "refine_d5.cu", "refine_d6.cu", "dbscan.cu", "variants.cu"]
 HEADERS = ["sj_common.cuh", "refine.cuh", "refine_launch.cuh", "scan.cuh"]
 
 OBJDIR = os.path.join(ROOT, "build", "obj")

@@ -473,6 +473,33 @@ sj_status sj_brute_force_join(const double *points, uint64_t n, int d, double ep
     SJ_API_END
 }
 
+sj_status sj_join_sets(const sj_index *idx, const double *queries, uint64_t nq, int queries_on_device,
+                       const sj_join_opts *opts, sj_result **out)
+{
+    SJ_API_BEGIN
+    if (!out) sj::fail(SJ_ERR_ARG, "out is NULL");
+    sj_join_opts jo;
+    if (opts) jo = *opts;
+    else sj_join_opts_default(&jo);
+    *out = sj::join_sets_impl(idx, queries, nq, queries_on_device, jo);
+    return SJ_OK;
+    SJ_API_END
+}
+
+sj_status sj_knn_self(const double *points, uint64_t n, int d, uint32_t k, double eps0, const sj_build_opts *bopts,
+                      uint32_t *ids, double *dist2, sj_knn_stats *stats)
+{
+    SJ_API_BEGIN
+    sj_build_opts bo;
+    if (bopts) bo = *bopts;
+    else sj_build_opts_default(&bo);
+    sj_knn_stats st{};
+    sj::knn_self_impl(points, n, d, k, eps0, bo, ids, dist2, &st);
+    if (stats) *stats = st;
+    return SJ_OK;
+    SJ_API_END
+}
+
 sj_status sj_index_timings(const sj_index *idx, sj_index_view *view)
 {
     SJ_API_BEGIN

@@ -145,6 +145,7 @@ void dbscan_impl(const sj_result *r, uint32_t min_pts, int32_t *labels, uint64_t
     if (!r) fail(SJ_ERR_STATE, "result is NULL");
     if (!labels) fail(SJ_ERR_ARG, "labels is NULL");
     if (min_pts < 1) fail(SJ_ERR_ARG, "min_pts must be >= 1");
+    if (r->two_set) fail(SJ_ERR_ARG, "DBSCAN needs a self-join result, not a two-set join");
     if (r->q0 != 0 || r->q1 != r->n_points)
         fail(SJ_ERR_ARG, "DBSCAN needs the whole self-join (the result covers only a query range)");
     for (const auto &b : r->batches)

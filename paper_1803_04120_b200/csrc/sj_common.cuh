@@ -246,6 +246,7 @@ struct sj_result {
     // predicate options of the join that produced them
     uint64_t q0 = 0, q1 = 0;
     int include_self = 1, unicomp = 1;
+    int two_set = 0;             // a two-set join J(Q,P) (variants.cu): keys are query rows, not a self-join
 };
 
 namespace sj {
@@ -348,6 +349,12 @@ void batch_to_csr_device(const uint64_t *pairs, uint64_t n, uint64_t rows, bool 
 void result_fingerprint_impl(const sj_result *r, uint64_t *fp, uint32_t *counts);
 sj_result *brute_force_impl(const double *points, uint64_t n, int d, double eps, const sj_build_opts &bo,
                             const sj_join_opts &jo);
+
+// variants.cu
+sj_result *join_sets_impl(const sj_index *idx, const double *queries, uint64_t nq, int queries_on_device,
+                          const sj_join_opts &o);
+void knn_self_impl(const double *points, uint64_t n, int d, uint32_t k, double eps0, const sj_build_opts &bo,
+                   uint32_t *ids, double *dist2, sj_knn_stats *st);
 
 // join.cu
 sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o);

@@ -1,0 +1,504 @@
+// variants.cu -- SURVEY.md §8(f) rank 4: queries from outside the index's own A-order over the same
+// grid index and predicate.
+//
+//   * two-set similarity join J(Q,P) ("the related similarity join"; R19): every
+//     query of Q probes the 3^d cells around its own cell in P's grid, full search (no unicomp: Q != P).
+//   * kNN self-join ("other spatial searches, such as kNN"; R20): every point's k
+//     best (s, id) among the points of its 3^d neighbour cells that satisfy the join predicate; certified
+//     when there are k of them, otherwise re-run on an index with 2*eps.
+//
+// One kernel, k_probe<D, MODE>, ONE WARP PER QUERY:
+//   1. the query's coordinates are warp-uniform; per dimension the <= 3 neighbour coordinates that lie in
+//      [1, |g_j|-2] and are occupied (M_j, Alg. 1 l.6) form a 3-bit set, so boundary and masked queries
+//      enumerate only the product of what can exist;
+//   2. the lanes look up 32 of those cells at a time: linear id (R8), prefix p = sum c_j * pstride_j, the
+//      directory range [dir[p], dir[p+1]) of B, one bounded binary search (PAPER.md:173 B, G);
+//   3. the cells' point ranges are concatenated by a warp prefix sum and swept 32 candidates per step,
+//      each lane finding its candidate's cell by a 5-step shuffle search -- the warp stays converged and
+//      every lane tests a candidate even when the cells hold one point each (sparse 6-D);
+//   4. the predicate is the self-join's (R1: __dsub_rn/__dmul_rn/__dadd_rn left to right, <= fl(eps^2));
+//   5. count: hits per query; fill: warp-aggregated emission (one atomic per 32 candidates);
+//      kNN: a warp-wide sorted top-k list (lane i holds the i-th best (s, id)), each surviving candidate
+//      inserted by one ballot + one shuffle-up.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "sj_common.cuh"
+
+namespace sj {
+namespace {
+
+constexpr int kProbeThreads = 256;
+constexpr int kMaxK = 32;
+enum ProbeMode { kPCount = 0, kPFill = 1, kPKnn = 2 };
+
+struct ProbeArgs {
+    const double *q;              // AoS query coordinates [rows][D] (unused with q_index)
+    const uint32_t *qlist;        // optional: query rows to process (kNN re-runs: original ids)
+    uint32_t q_begin, nq;         // queries q_begin .. q_begin+nq-1 (rows, or qlist entries)
+    int q_index;                  // 1: the queries are the index's own points in A-order (X, A)
+    int self;                     // kNN: skip the candidate whose id is the query's
+    uint32_t *counts;             // count: per query (index t - q_begin)
+    unsigned long long *buckets;  // count: per 1024 queries
+    uint32_t *nonfinite;          // count: set when a query coordinate is NaN / inf
+    uint64_t *out;                // fill: pair buffer, cursor, capacity, overflow flag
+    unsigned long long *cursor;
+    uint64_t cap;
+    uint32_t *overflow;
+    uint32_t k;                   // kNN: neighbours per query (1..32)
+    uint32_t *ids;                // kNN: [N][k] rows by original id
+    double *dist2;
+    uint32_t *unres;              // kNN: ids of uncertified queries, count in *n_unres
+    uint32_t *n_unres;
+    unsigned long long *work;     // [0] cells probed, [1] candidates tested, [2] pairs / hits
+};
+
+__device__ __forceinline__ bool kv_less(uint64_t as, uint32_t ai, uint64_t bs, uint32_t bi)
+{
+    return as < bs || (as == bs && ai < bi);
+}
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(kProbeThreads) k_probe(const DevIndex ix, const ProbeArgs pa)
+{
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t n = ix.n;
+    unsigned long long probes = 0, tests = 0, hits_all = 0;
+    for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < pa.nq; t += warps) {
+        const uint32_t row = pa.q_begin + t;
+        uint32_t qid;
+        double x[D];
+        if (pa.q_index) {
+            qid = __ldg(ix.A + row);
+#pragma unroll
+            for (int j = 0; j < D; ++j) x[j] = __ldg(ix.X + (uint64_t)j * n + row);
+        } else {
+            qid = pa.qlist ? __ldg(pa.qlist + row) : row;
+#pragma unroll
+            for (int j = 0; j < D; ++j) x[j] = __ldg(pa.q + (uint64_t)qid * D + j);
+        }
+        // ---- 1. per dimension: c_j - 1 (R7 against the index's geometry) and the valid neighbour set
+        uint64_t c0[D];
+        uint32_t sel[D];
+        uint32_t ncell = 1;
+        bool finite = true;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            finite = finite && isfinite(x[j]);
+            const double tq = floor(__ddiv_rn(__dsub_rn(x[j], ix.mins[j]), ix.w));   // = c_j - 1
+            uint32_t m = 0;
+            c0[j] = 0;
+            if (tq >= -1.0 && tq <= (double)ix.cpd[j]) {       // some of tq .. tq+2 may be in [1, |g_j|-2]
+                const int64_t b = (int64_t)tq;
+#pragma unroll
+                for (int e = 0; e < 3; ++e) {
+                    const int64_t cc = b + e;
+                    bool ok = cc >= 1 && cc <= (int64_t)ix.cpd[j] - 2;
+                    if (ok && ix.masks) {
+                        const uint64_t bit = ix.mask_off[j] + (uint64_t)cc;
+                        ok = (__ldg(ix.masks + (bit >> 5)) >> (bit & 31u)) & 1u;
+                    }
+                    if (ok) m |= 1u << e;
+                }
+                c0[j] = (uint64_t)(b + 1);                      // as unsigned: b >= -1
+            }
+            sel[j] = m;
+            ncell *= (uint32_t)__popc(m);
+        }
+        if (MODE == kPCount && !finite && lane == 0) atomicOr(pa.nonfinite, 1u);
+        // kNN state: lane i < k holds the i-th best (s bits, id); sentinels sort last
+        uint64_t bs = ~0ull;
+        uint32_t bi = 0xffffffffu;
+        uint64_t kth_s = ~0ull;
+        uint32_t kth_i = 0xffffffffu;
+        uint32_t found = 0;
+        // ---- 2-3. 32 cells per round, looked up by the lanes, candidates swept by the whole warp
+        for (uint32_t base = 0; base < ncell; base += 32u) {
+            uint32_t lo = 0, hi = 0;
+            const uint32_t o = base + lane;
+            if (o < ncell) {
+                uint32_t r = o;
+                uint64_t key = 0, p = 0;
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    const uint32_t nj = (uint32_t)__popc(sel[j]);
+                    const uint32_t rj = r % nj;
+                    r /= nj;
+                    uint32_t m = sel[j];
+                    if (rj >= 1u) m &= m - 1u;
+                    if (rj >= 2u) m &= m - 1u;
+                    const uint64_t cj = c0[j] - 1u + (uint64_t)(__ffs(m) - 1);   // (c_j - 1) + e
+                    key += cj * ix.strides[j];
+                    p += cj * ix.pstride[j];
+                }
+                ++probes;
+                uint32_t h = __ldg(ix.dir + p);
+                uint32_t h1 = __ldg(ix.dir + p + 1);
+                while (h < h1) {
+                    const uint32_t mid = (h + h1) >> 1;
+                    if (__ldg(ix.B + mid) < key) h = mid + 1;
+                    else h1 = mid;
+                }
+                if (h < ix.nG && __ldg(ix.B + h) == key) {
+                    lo = __ldg(ix.G + h);
+                    hi = __ldg(ix.G + h + 1);
+                }
+            }
+            const uint32_t len = hi - lo;
+            uint32_t inc = len;
+#pragma unroll
+            for (int s = 1; s < 32; s <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, inc, s);
+                if (lane >= (uint32_t)s) inc += v;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+            const uint32_t exc = inc - len;
+            for (uint32_t f0 = 0; f0 < total; f0 += 32u) {
+                const uint32_t f = f0 + lane;
+                uint32_t pos = 0;                               // lanes whose range ends at or before f
+#pragma unroll
+                for (uint32_t s = 16; s; s >>= 1) {
+                    const uint32_t v = __shfl_sync(0xffffffffu, inc, pos + s - 1u);
+                    if (v <= f) pos += s;
+                }
+                const uint32_t olo = __shfl_sync(0xffffffffu, lo, pos & 31u);
+                const uint32_t oexc = __shfl_sync(0xffffffffu, exc, pos & 31u);
+                const bool act = f < total;
+                const uint32_t m = olo + (f - oexc);
+                bool hit = false;
+                double s = 0.0;
+                uint32_t pid = 0;
+                if (act) {
+                    {
+                        const double d0 = __dsub_rn(x[0], __ldg(ix.X + m));
+                        s = __dmul_rn(d0, d0);
+                    }
+#pragma unroll
+                    for (int j = 1; j < D; ++j) {
+                        const double dj = __dsub_rn(x[j], __ldg(ix.X + (uint64_t)j * n + m));
+                        s = __dadd_rn(s, __dmul_rn(dj, dj));
+                    }
+                    ++tests;
+                    hit = s <= ix.eps2;
+                    if (hit) {
+                        pid = __ldg(ix.A + m);
+                        if (MODE == kPKnn && pa.self && pid == qid) hit = false;
+                    }
+                }
+                const unsigned hb = __ballot_sync(0xffffffffu, hit);
+                found += (uint32_t)__popc(hb);
+                if constexpr (MODE == kPFill) {
+                    if (hb) {
+                        unsigned long long b0 = 0;
+                        if (lane == 0) b0 = atomicAdd(pa.cursor, (unsigned long long)__popc(hb));
+                        b0 = __shfl_sync(0xffffffffu, b0, 0);
+                        if (hit) {
+                            const unsigned long long at = b0 + (unsigned long long)__popc(hb & ((1u << lane) - 1u));
+                            if (at < pa.cap) pa.out[at] = ((uint64_t)qid << 32) | pid;
+                            else atomicOr(pa.overflow, 1u);
+                        }
+                    }
+                } else if constexpr (MODE == kPKnn) {
+                    const uint64_t sb = (uint64_t)__double_as_longlong(s);
+                    unsigned surv = __ballot_sync(0xffffffffu, hit && kv_less(sb, pid, kth_s, kth_i));
+                    while (surv) {
+                        const int src = __ffs(surv) - 1;
+                        surv &= surv - 1u;
+                        const uint64_t cs = __shfl_sync(0xffffffffu, sb, src);
+                        const uint32_t ci = __shfl_sync(0xffffffffu, pid, src);
+                        if (!kv_less(cs, ci, kth_s, kth_i)) continue;          // warp-uniform
+                        const bool gt = lane < pa.k && kv_less(cs, ci, bs, bi);
+                        const uint32_t ins = pa.k - (uint32_t)__popc(__ballot_sync(0xffffffffu, gt));
+                        const uint64_t us = __shfl_up_sync(0xffffffffu, bs, 1);
+                        const uint32_t ui = __shfl_up_sync(0xffffffffu, bi, 1);
+                        if (lane == ins) { bs = cs; bi = ci; }
+                        else if (lane > ins && lane < pa.k) { bs = us; bi = ui; }
+                        kth_s = __shfl_sync(0xffffffffu, bs, pa.k - 1u);
+                        kth_i = __shfl_sync(0xffffffffu, bi, pa.k - 1u);
+                    }
+                }
+            }
+        }
+        hits_all += found;
+        if constexpr (MODE == kPCount) {
+            if (lane == 0) {
+                pa.counts[t] = found;
+                atomicAdd(pa.buckets + (t >> 10), (unsigned long long)found);
+            }
+        } else if constexpr (MODE == kPKnn) {
+            if (found >= pa.k) {
+                if (lane < pa.k) {
+                    pa.ids[(uint64_t)qid * pa.k + lane] = bi;
+                    pa.dist2[(uint64_t)qid * pa.k + lane] = __longlong_as_double((long long)bs);
+                }
+            } else if (lane == 0) {
+                pa.unres[atomicAdd(pa.n_unres, 1u)] = qid;
+            }
+        }
+    }
+    // per-lane counters: probes differ by lane, tests too; one atomic per warp and counter
+#pragma unroll
+    for (int s = 16; s; s >>= 1) {
+        probes += __shfl_xor_sync(0xffffffffu, probes, s);
+        tests += __shfl_xor_sync(0xffffffffu, tests, s);
+    }
+    if (lane == 0 && pa.work) {
+        atomicAdd(pa.work + 0, probes);
+        atomicAdd(pa.work + 1, tests);
+        atomicAdd(pa.work + 2, hits_all);
+    }
+}
+
+template <int D>
+void launch_probe_d(int mode, const DevIndex &ix, const ProbeArgs &pa, dim3 grid, cudaStream_t s)
+{
+    switch (mode) {
+    case kPCount: k_probe<D, kPCount><<<grid, kProbeThreads, 0, s>>>(ix, pa); break;
+    case kPFill: k_probe<D, kPFill><<<grid, kProbeThreads, 0, s>>>(ix, pa); break;
+    default: k_probe<D, kPKnn><<<grid, kProbeThreads, 0, s>>>(ix, pa); break;
+    }
+}
+
+void launch_probe(int mode, const DevIndex &ix, const ProbeArgs &pa, int dev, cudaStream_t s)
+{
+    if (pa.nq == 0) return;
+    // one warp per query, grid-strided; 8 CTAs of 256 per SM fill it
+    const uint64_t want = ((uint64_t)pa.nq + (kProbeThreads / 32) - 1) / (kProbeThreads / 32);
+    const dim3 grid((uint32_t)std::min<uint64_t>(want, (uint64_t)device_sm_count(dev) * 8));
+    switch (ix.d) {
+    case 2: launch_probe_d<2>(mode, ix, pa, grid, s); break;
+    case 3: launch_probe_d<3>(mode, ix, pa, grid, s); break;
+    case 4: launch_probe_d<4>(mode, ix, pa, grid, s); break;
+    case 5: launch_probe_d<5>(mode, ix, pa, grid, s); break;
+    case 6: launch_probe_d<6>(mode, ix, pa, grid, s); break;
+    default: fail(SJ_ERR_DIM, "bad d");
+    }
+    SJ_LAUNCHED();
+}
+
+void free_batches(sj_result *res)
+{
+    for (auto &b : res->batches) {
+        if (b.on_device) dev_free(b.pairs, nullptr);
+        else host_pinned_free(b.pairs);
+    }
+    res->batches.clear();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ two-set join
+sj_result *join_sets_impl(const sj_index *idx, const double *queries, uint64_t nq, int queries_on_device,
+                          const sj_join_opts &o)
+{
+    if (!idx) fail(SJ_ERR_STATE, "index is NULL");
+    if (nq >= (1ull << 32)) fail(SJ_ERR_ARG, "the number of queries must be < 2^32");
+    if (nq && !queries) fail(SJ_ERR_ARG, "queries is NULL");
+    if (o.batch_capacity_pairs == 0) fail(SJ_ERR_ARG, "batch_capacity_pairs must be > 0");
+    if (o.drain_csr) fail(SJ_ERR_ARG, "drain_csr is not supported by the two-set join");
+    const DevIndex &ix = idx->dev;
+    const int dev = idx->device;
+    SJ_CUDA(cudaSetDevice(dev));
+    CtxGuard cg{acquire_ctx(dev, 1, 2, 64)};
+    cudaStream_t s = cg.c->streams[0];
+    // ordered after the caller's work on the legacy default stream (e.g. torch producing Q)
+    SJ_CUDA(cudaEventRecord(cg.c->events[1], cudaStreamLegacy));
+    SJ_CUDA(cudaStreamWaitEvent(s, cg.c->events[1], 0));
+    const uint32_t NQ = (uint32_t)nq;
+    const int D = ix.d;
+    const double *qd = queries;
+    Scratch<double> qcopy;
+    if (nq && !queries_on_device) {
+        qcopy.p = dalloc<double>(nq * D, s);
+        qcopy.s = s;
+        SJ_CUDA(cudaMemcpyAsync(qcopy.p, queries, sizeof(double) * nq * D, cudaMemcpyHostToDevice, s));
+        qd = qcopy.p;
+    }
+    const uint64_t nbk = (nq + 1023) / 1024;
+    // device words: [0..3) work, [3] nonfinite flag, [4] cursor, [5] overflow; then the bucket sums
+    Scratch<unsigned long long> words(8 + nbk, s);
+    Scratch<uint32_t> counts(nq, s);
+    SJ_CUDA(cudaMemsetAsync(words.p, 0, sizeof(unsigned long long) * (8 + nbk), s));
+    ProbeArgs pa{};
+    pa.q = qd;
+    pa.q_begin = 0;
+    pa.nq = NQ;
+    pa.counts = counts.p;
+    pa.buckets = words.p + 8;
+    pa.nonfinite = reinterpret_cast<uint32_t *>(words.p + 3);
+    pa.work = words.p;
+    launch_probe(kPCount, ix, pa, dev, s);
+    std::vector<unsigned long long> hw(8 + nbk);
+    SJ_CUDA(cudaMemcpyAsync(hw.data(), words.p, sizeof(unsigned long long) * hw.size(), cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaStreamSynchronize(s));
+    if (hw[3]) fail(SJ_ERR_NONFINITE, "a query coordinate is NaN or inf");
+    uint64_t total = 0;
+    for (uint64_t b = 0; b < nbk; ++b) total += hw[8 + b];
+
+    // ---- batch plan: contiguous query ranges of <= target pairs (exact counts: no overflow re-runs);
+    //      at least min_batches when there is output (the paper's pipeline shape)
+    uint64_t target = o.batch_capacity_pairs;
+    if (o.min_batches > 1 && total) target = std::min<uint64_t>(target, (total + o.min_batches - 1) / o.min_batches);
+    target = std::max<uint64_t>(target, 1);
+    std::vector<uint64_t> cuts{0};
+    std::vector<uint64_t> sizes;
+    {
+        std::vector<uint32_t> qc;     // per-query counts of a bucket larger than the target (fetched lazily)
+        uint64_t acc = 0;
+        for (uint64_t b = 0; b < nbk; ++b) {
+            const uint64_t bq0 = b * 1024, bq1 = std::min<uint64_t>(nq, bq0 + 1024);
+            if (hw[8 + b] <= target) {
+                if (acc && acc + hw[8 + b] > target) { cuts.push_back(bq0); sizes.push_back(acc); acc = 0; }
+                acc += hw[8 + b];
+                continue;
+            }
+            qc.resize(bq1 - bq0);
+            SJ_CUDA(cudaMemcpy(qc.data(), counts.p + bq0, sizeof(uint32_t) * qc.size(), cudaMemcpyDeviceToHost));
+            for (uint64_t q = bq0; q < bq1; ++q) {
+                const uint64_t c = qc[q - bq0];
+                if (acc && acc + c > target) { cuts.push_back(q); sizes.push_back(acc); acc = 0; }
+                acc += c;
+            }
+        }
+        cuts.push_back(nq);
+        sizes.push_back(acc);
+    }
+
+    sj_result *res = new sj_result();
+    res->device = dev;
+    res->n_points = std::max<uint64_t>(nq, ix.n);
+    res->q0 = 0;
+    res->q1 = nq;
+    res->include_self = 1;
+    res->unicomp = 0;
+    res->two_set = 1;
+    try {
+        const uint64_t w0 = hw[0], w1 = hw[1];
+        SJ_CUDA(cudaMemsetAsync(words.p, 0, sizeof(unsigned long long) * 8, s));
+        for (size_t b = 0; b + 1 < cuts.size(); ++b) {
+            if (total && sizes[b] == 0) continue;     // an empty range between two non-empty ones
+            sj_batch bt;
+            bt.cap = std::max<uint64_t>(sizes[b], 1);
+            bt.pairs = dalloc<uint64_t>(bt.cap, s);
+            bt.on_device = 1;
+            bt.n = sizes[b];
+            SJ_CUDA(cudaMemsetAsync(words.p + 4, 0, 16, s));
+            ProbeArgs pf{};
+            pf.q = qd;
+            pf.q_begin = (uint32_t)cuts[b];
+            pf.nq = (uint32_t)(cuts[b + 1] - cuts[b]);
+            pf.out = bt.pairs;
+            pf.cursor = words.p + 4;
+            pf.cap = bt.cap;
+            pf.overflow = reinterpret_cast<uint32_t *>(words.p + 5);
+            pf.work = nullptr;
+            if (sizes[b]) launch_probe(kPFill, ix, pf, dev, s);
+            if (o.sort_pairs) sort_pairs_device(bt.pairs, bt.n, res->n_points, s);
+            if (o.result_on_host) {
+                uint64_t *h = static_cast<uint64_t *>(host_pinned_alloc(bt.cap * 8, nullptr));
+                if (bt.n) SJ_CUDA(cudaMemcpyAsync(h, bt.pairs, bt.n * 8, cudaMemcpyDeviceToHost, s));
+                SJ_CUDA(cudaStreamSynchronize(s));
+                dev_free(bt.pairs, s);
+                bt.pairs = h;
+                bt.on_device = 0;
+            }
+            res->batches.push_back(bt);
+        }
+        unsigned long long tail[2];
+        SJ_CUDA(cudaMemcpyAsync(tail, words.p + 4, 16, cudaMemcpyDeviceToHost, s));
+        SJ_CUDA(cudaStreamSynchronize(s));
+        if (tail[1]) fail(SJ_ERR_STATE, "two-set join: fill pass exceeded its exact count (internal error)");
+        res->total = total;
+        res->stats.pairs = total;
+        res->stats.estimated_pairs = total;
+        res->stats.cells_probed = 2 * w0;
+        res->stats.candidates_tested = 2 * w1;
+        res->stats.batches = (uint32_t)res->batches.size();
+        res->stats.refine_launches = (uint32_t)res->batches.size() + 1;
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        free_batches(res);
+        delete res;
+        throw;
+    }
+    return res;
+}
+
+// ------------------------------------------------------------------ kNN self-join
+void knn_self_impl(const double *points, uint64_t n, int d, uint32_t k, double eps0, const sj_build_opts &bo,
+                   uint32_t *ids, double *dist2, sj_knn_stats *st)
+{
+    if (d < 2 || d > SJ_MAX_DIM) fail(SJ_ERR_DIM, "d must be in [2,6]");
+    if (!points || !ids || !dist2) fail(SJ_ERR_ARG, "points / ids / dist2 is NULL");
+    if (k < 1 || k > (uint32_t)kMaxK) fail(SJ_ERR_ARG, "k must be in [1, 32]");
+    if (n < (uint64_t)k + 1 || n >= (1ull << 32)) fail(SJ_ERR_ARG, "N must satisfy k + 1 <= N < 2^32");
+    if (!std::isfinite(eps0) || !(eps0 > 0.0)) fail(SJ_ERR_ARG, "eps0 must be finite and > 0");
+    if (bo.device < 0 || bo.device >= device_count()) fail(SJ_ERR_ARG, "bad device ordinal");
+    SJ_CUDA(cudaSetDevice(bo.device));
+    CtxGuard cg{acquire_ctx(bo.device, 1, 2, 64)};
+    cudaStream_t s = cg.c->streams[0];
+    SJ_CUDA(cudaEventRecord(cg.c->events[1], cudaStreamLegacy));
+    SJ_CUDA(cudaStreamWaitEvent(s, cg.c->events[1], 0));
+    const double *pd = points;
+    Scratch<double> pcopy;
+    if (!bo.points_on_device) {
+        pcopy.p = dalloc<double>(n * d, s);
+        pcopy.s = s;
+        SJ_CUDA(cudaMemcpyAsync(pcopy.p, points, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
+        pd = pcopy.p;
+    }
+    Scratch<uint32_t> unres[2] = {Scratch<uint32_t>(n, s), Scratch<uint32_t>(n, s)};
+    Scratch<unsigned long long> words(8, s);
+    sj_build_opts b2 = bo;
+    b2.points_on_device = 1;
+    b2.stream = s;
+    b2.speculative_estimate = 0;
+    double eps = eps0;
+    uint64_t pending = n, probes = 0, tests = 0;
+    uint32_t rounds = 0;
+    int cur = 0;
+    while (pending) {
+        if (++rounds > 64) fail(SJ_ERR_STATE, "kNN: not certified after 64 radius doublings");
+        sj_index *idx = build_index_impl(pd, n, d, eps, b2);
+        try {
+            SJ_CUDA(cudaMemsetAsync(words.p, 0, sizeof(unsigned long long) * 8, s));
+            ProbeArgs pa{};
+            pa.q = pd;
+            pa.q_index = rounds == 1;                 // first round: every point, in the index's A-order
+            pa.qlist = rounds == 1 ? nullptr : unres[cur].p;
+            pa.q_begin = 0;
+            pa.nq = (uint32_t)pending;
+            pa.self = 1;
+            pa.k = k;
+            pa.ids = ids;
+            pa.dist2 = dist2;
+            pa.unres = unres[cur ^ 1].p;
+            pa.n_unres = reinterpret_cast<uint32_t *>(words.p + 4);
+            pa.work = words.p;
+            launch_probe(kPKnn, idx->dev, pa, bo.device, s);
+            unsigned long long hw[5];
+            SJ_CUDA(cudaMemcpyAsync(hw, words.p, sizeof hw, cudaMemcpyDeviceToHost, s));
+            SJ_CUDA(cudaStreamSynchronize(s));
+            probes += hw[0];
+            tests += hw[1];
+            pending = (uint32_t)hw[4];
+        } catch (...) {
+            free_index_impl(idx);
+            throw;
+        }
+        free_index_impl(idx);
+        cur ^= 1;
+        if (pending) eps *= 2.0;
+    }
+    if (st) {
+        st->rounds = rounds;
+        st->eps_final = eps;
+        st->cells_probed = probes;
+        st->candidates_tested = tests;
+    }
+}
+
+}  // namespace sj

@@ -49,6 +49,11 @@ class Stats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class KnnStats(ctypes.Structure):
+    _fields_ = [("rounds", ctypes.c_uint32), ("eps_final", ctypes.c_double), ("cells_probed", ctypes.c_uint64),
+                ("candidates_tested", ctypes.c_uint64)]
+
+
 class IndexView(ctypes.Structure):
     _fields_ = [("d", i32), ("device", i32), ("n", u64), ("n_cells", u64),
                 ("eps", dbl), ("eps2", dbl), ("w", dbl),
@@ -129,6 +134,10 @@ def load_library(path: str = LIB_PATH):
     L.sj_neighbor_counts.restype = i32
     L.sj_brute_force_join.argtypes = [vp, u64, i32, dbl, P(BuildOpts), P(JoinOpts), P(vp)]
     L.sj_brute_force_join.restype = i32
+    L.sj_join_sets.argtypes = [vp, vp, u64, i32, P(JoinOpts), P(vp)]
+    L.sj_join_sets.restype = i32
+    L.sj_knn_self.argtypes = [vp, u64, i32, u32, dbl, P(BuildOpts), vp, vp, P(KnnStats)]
+    L.sj_knn_self.restype = i32
     L.sj_index_export.argtypes = [vp, P(IndexView)]
     L.sj_index_export.restype = i32
     L.sj_index_timings.argtypes = [vp, P(IndexView)]
@@ -610,6 +619,63 @@ def brute_force_join(points, eps: float, include_self: bool = True, result_on_ho
     r = Result(h.value)
     r.device = bo.device
     return r
+
+
+def join_sets(index: Index, queries, batch_capacity_pairs: Optional[int] = None, min_batches: Optional[int] = None,
+              result_on_host: bool = False, sort_pairs: bool = False) -> Result:
+    """sj_join_sets ("the related similarity join"; R19): pairs (i<<32|k) of query
+    row i and index point k within the index's eps.  queries: nq x d float64 torch tensor (cuda on the
+    index's device, or cpu) or numpy array."""
+    import torch
+    L = load_library()
+    if isinstance(queries, torch.Tensor):
+        t = queries.contiguous()
+        if t.dtype != torch.float64 or t.dim() != 2:
+            raise TypeError("queries must be a 2-D float64 tensor")
+        keep, ptr, on_dev = t, t.data_ptr(), int(t.is_cuda)
+        nq, d = t.shape
+    else:
+        a = np.ascontiguousarray(queries, dtype=np.float64)
+        if a.ndim != 2:
+            raise TypeError("queries must be nq x d")
+        keep, ptr, on_dev = a, a.ctypes.data, 0
+        nq, d = a.shape
+    if d != index.d:
+        raise ValueError(f"queries have d={d}, the index d={index.d}")
+    kw = dict(result_on_host=result_on_host, sort_pairs=sort_pairs)
+    if batch_capacity_pairs is not None:
+        kw["batch_capacity_pairs"] = batch_capacity_pairs
+    if min_batches is not None:
+        kw["min_batches"] = min_batches
+    o = join_opts(**kw)
+    h = ctypes.c_void_p()
+    _check(L.sj_join_sets(index.handle, ctypes.c_void_p(ptr if nq else None), nq, on_dev, ctypes.byref(o),
+                          ctypes.byref(h)))
+    del keep
+    r = Result(h.value)
+    r.device = index.device
+    return r
+
+
+def knn_self(points, k: int, eps0: float, device: Optional[int] = None, with_stats: bool = False):
+    """sj_knn_self (PAPER.md:609 kNN; R20): for every point its k nearest other points,
+    ascending in (s, id) -> (ids int32 [n, k], dist2 float64 [n, k]) cuda tensors (+ stats dict)."""
+    import torch
+    L = load_library()
+    bo, ptr, n, d, keep = _points_arg(points, device, None)
+    bo.stream = None
+    bo.speculative_estimate = 0
+    dev = bo.device
+    ids = torch.empty((n, k), dtype=torch.int32, device=f"cuda:{dev}")
+    dist2 = torch.empty((n, k), dtype=torch.float64, device=f"cuda:{dev}")
+    st = KnnStats()
+    _check(L.sj_knn_self(ctypes.c_void_p(ptr), n, d, int(k), float(eps0), ctypes.byref(bo),
+                         ctypes.c_void_p(ids.data_ptr()), ctypes.c_void_p(dist2.data_ptr()), ctypes.byref(st)))
+    del keep
+    if with_stats:
+        return ids, dist2, dict(rounds=st.rounds, eps_final=st.eps_final, cells_probed=st.cells_probed,
+                                candidates_tested=st.candidates_tested)
+    return ids, dist2
 
 
 def plan_shards(index: Index, world: int) -> np.ndarray:

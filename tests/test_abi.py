@@ -38,7 +38,7 @@ def test_abi_struct_sizes_match_header(sj):
     would need a GPU-free C program; here: field count and 8-byte alignment sanity)."""
     assert ctypes.sizeof(sj.sj.JoinOpts) % 8 == 0
     assert ctypes.sizeof(sj.sj.Stats) == 8 * 4 + 4 * 2 + 4 * 4 + 4 + 4
-    assert sj.load_library().sj_abi_version() == 4
+    assert sj.load_library().sj_abi_version() == 5
 
 
 def test_defaults(sj):
