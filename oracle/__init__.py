@@ -16,7 +16,8 @@ Contents, each citing the passage it follows (PAPER.md line numbers, SPEC.md as 
 * ``join_sets`` / ``knn`` -- the SURVEY.md §8(f) rank-4 variants on the same predicate
   (``sj_variants_oracle.c``): the two-set similarity join J(Q,P) (reading R19) by
   brute force or a sorted-tuple grid, and the kNN self-join (reading R20) by brute
-  force with ties broken by the smaller id.
+  force with ties broken by the smaller id; ``brute_force_f32`` -- the self-join in binary32
+  (reading R21).
 * ``expected_pairs_uniform`` -- the exact expectation of |S| for iid uniform points (SURVEY.md
   §8(c) P4), used as a statistical pin.
 
@@ -77,6 +78,8 @@ def _load():
         lib.orc_join_sets_brute.restype = i64
         lib.orc_join_sets_grid.argtypes = [p, i64, p, i64, i32, dbl, i32, p, p, i64]
         lib.orc_join_sets_grid.restype = i64
+        lib.orc_brute_force_f32.argtypes = [p, i64, i32, ctypes.c_float, i32, p, i64]
+        lib.orc_brute_force_f32.restype = i64
         lib.orc_knn.argtypes = [p, i64, p, p, i64, i32, i32, i32, p, p]
         lib.orc_knn.restype = i32
         lib.orc_mix.argtypes = [i32, ctypes.c_uint64]
@@ -287,3 +290,20 @@ def knn(points, k: int, qids: Iterable[int] | None = None, queries=None, nthread
     if rc != 0:
         raise ValueError("bad arguments")
     return ids, s
+
+
+def brute_force_f32(points, eps: float, include_self: bool = True) -> np.ndarray:
+    """The self-join in binary32 (sj_variants_oracle.c orc_brute_force_f32; PAPER.md:393 SuperEGO's
+    32-bit floats, R21): points and eps as float32, s32 <= fl32(eps*eps), pairs sorted."""
+    P = np.ascontiguousarray(points, dtype=np.float32)
+    if P.ndim != 2:
+        raise ValueError("points must be N x d")
+    n, d = P.shape
+    e = float(np.float32(eps))
+    lib = _load()
+    total = lib.orc_brute_force_f32(_ptr(P), n, d, e, int(include_self), None, 0)
+    if total < 0:
+        raise ValueError("bad arguments")
+    out = np.empty(total, dtype=np.uint64)
+    lib.orc_brute_force_f32(_ptr(P), n, d, e, int(include_self), _ptr(out), total)
+    return out

@@ -263,3 +263,37 @@ int orc_knn(const double *Q, int64_t nq, const int64_t *qself, const double *P, 
     free(th); free(jobs);
     return 0;
 }
+
+/* ---- FP32 self-join, brute force (SURVEY.md §8(f) rank 4 "FP32 coordinates (SuperEGO's precision)";
+ *      PAPER.md:393 "We execute the algorithm using 32-bit floats"; reading R21) ------------
+ * The self-join's definition with every coordinate, difference, square and sum a binary32 value:
+ *     s32(a,b) = (((a_0-b_0)^2 + (a_1-b_1)^2) + ...) in float, left to right, no FMA,
+ *     (i,k) in S32  <=>  s32(p_i,p_k) <= fl32(eps*eps),   eps itself a float.
+ * Writes up to cap pairs (may be NULL), sorted (loop order); returns |S32| or -1. */
+static float vo_dist_f32(const float *a, const float *b, int d)
+{
+    float s = 0.0f;
+    for (int j = 0; j < d; ++j) {
+        float t = a[j] - b[j];
+        float t2 = t * t;
+        s = s + t2;
+    }
+    return s;
+}
+
+int64_t orc_brute_force_f32(const float *pts, int64_t n, int d, float eps, int include_self,
+                            uint64_t *out, int64_t cap)
+{
+    if (n < 0 || d < 1 || !(eps > 0.0f)) return -1;
+    float E = eps * eps;
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = 0; k < n; ++k) {
+            if (i == k && !include_self) continue;
+            if (vo_dist_f32(pts + i * d, pts + k * d, d) <= E) {
+                if (out && cnt < cap) out[cnt] = ((uint64_t)i << 32) | (uint64_t)k;
+                ++cnt;
+            }
+        }
+    return cnt;
+}

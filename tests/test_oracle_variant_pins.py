@@ -149,3 +149,42 @@ def test_knn_two_set_form_and_sample_rows():
     i3, s3 = oracle.knn(P, 7, queries=P[q])
     assert i3[:, 0].tolist() == q and (s3[:, 0] == 0).all()
     assert np.array_equal(i3[:, 1:], ids[q])
+
+
+# ---------------------------------------------------------------- FP32 self-join (R21)
+@pytest.mark.parametrize("d,L", [(2, 8), (3, 6), (4, 4), (6, 3)])
+def test_f32_lattice_closed_form(d, L):
+    """Integer lattice, eps = 1: every coordinate, difference and square is an exact small integer in
+    binary32, so S32 = S = L^d + 2d(L-1)L^(d-1) pairs (the same closed form as the FP64 join)."""
+    P = datagen.lattice(L, d).astype(np.float32)
+    got = oracle.brute_force_f32(P, 1.0)
+    assert len(got) == L ** d + 2 * d * (L - 1) * L ** (d - 1)
+    assert np.array_equal(got, oracle.brute_force(P.astype(np.float64), 1.0))
+
+
+def test_f32_rounding_accepts_what_fp64_rejects():
+    """Worked by hand: a = (0,0), b = (1, 2^-13), eps = 1.  Exactly s = 1 + 2^-26 > 1, which binary64
+    keeps (rejects the pair); in binary32 1 + 2^-26 is below half an ulp of 1 (2^-24) and rounds to 1,
+    so the FP32 predicate accepts it.  (3,4) at eps 5 is the exact tie both include (S.235)."""
+    P = np.array([[0.0, 0.0], [1.0, 2.0 ** -13]])
+    assert oracle.brute_force_f32(P, 1.0).tolist() == [0, 1, 1 << 32, (1 << 32) | 1]
+    assert oracle.brute_force(P, 1.0).tolist() == [0, (1 << 32) | 1]
+    T = np.array([[0.0, 0.0], [3.0, 4.0]])
+    assert len(oracle.brute_force_f32(T, 5.0)) == 4 and len(oracle.brute_force_f32(T, 4.99)) == 2
+
+
+@pytest.mark.parametrize("d", [2, 4, 6])
+def test_f32_bracketed_by_fp64(d):
+    """Random float32 points: the FP32 set lies between the (pinned) FP64 joins at eps(1 -+ 1e-5)
+    (binary32 rounding moves a distance by < 1e-6 relative), and is exactly the FP64 set whenever no
+    pair sits inside that bracket."""
+    P = datagen.uniform(1500, d, seed=60 + d, hi=10.0).astype(np.float32)
+    eps = float(np.float32([0.4, 2.5, 4.0][d // 2 - 1]))
+    got = set(oracle.brute_force_f32(P, eps).tolist())
+    P64 = P.astype(np.float64)
+    lo = set(oracle.brute_force(P64, eps * (1 - 1e-5)).tolist())
+    hi = set(oracle.brute_force(P64, eps * (1 + 1e-5)).tolist())
+    assert lo <= got <= hi
+    assert len(got) > 2 * len(P)
+    if lo == hi:
+        assert got == lo
