@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SJ_ABI_VERSION 5   /* 5: sj_join_sets, sj_knn_self; 4: drain_csr, CSR batches, sj_dbscan, sj_result_counters */
+#define SJ_ABI_VERSION 5   /* 5: sj_join_sets, sj_knn_self, sj_self_join_f32; 4: drain_csr, CSR batches, sj_dbscan, sj_result_counters */
 #define SJ_MAX_DIM 6
 
 typedef enum {
@@ -294,6 +294,21 @@ sj_status sj_brute_force_join(const double *points, uint64_t n, int d, double ep
  *         capacity 0), SJ_ERR_NONFINITE (a query coordinate NaN / inf), SJ_ERR_NOMEM, SJ_ERR_CUDA. */
 sj_status sj_join_sets(const sj_index *idx, const double *queries, uint64_t nq, int queries_on_device,
                        const sj_join_opts *opts, sj_result **out);
+
+/* FP32 self-join (SURVEY §8(f) rank 4 "FP32 coordinates (SuperEGO's precision)"; PAPER.md:393 runs
+ * SuperEGO "using 32-bit floats"; R21): the self-join of float points with every coordinate
+ * difference, square and sum a binary32 round-to-nearest operation, left to right, no FMA:
+ *     (i,k) in S32  <=>  (((p_i0-p_k0)^2 + (p_i1-p_k1)^2) + ...) <= fl32(eps*eps)   (all in float).
+ * Pairs / ids / result as sj_self_join (both orientations; (p,p) unless include_self == 0).  The grid
+ * index is built from the points widened exactly to binary64 for radius eps * (1 + 2^-16), so every
+ * pair the float predicate accepts lies in adjacent cells; each point then probes its full 3^d
+ * neighbourhood (no unicomp), count pass then fill pass (exact batch sizes, no overflow re-runs).
+ *   points : row-major n x d float32, host or device per bopts->points_on_device.   eps: float > 0,
+ *            fl32(eps*eps) normal.   jopts: include_self, batch_capacity_pairs, min_batches,
+ *            result_on_host, sort_pairs are used; drain_csr must be 0.
+ * Errors: as sj_build_index / sj_self_join. */
+sj_status sj_self_join_f32(const float *points, uint64_t n, int d, float eps, const sj_build_opts *bopts,
+                           const sj_join_opts *jopts, sj_result **out);
 
 typedef struct {
     uint32_t rounds;             /* radius doublings + 1 (index builds)                             */

@@ -486,6 +486,22 @@ sj_status sj_join_sets(const sj_index *idx, const double *queries, uint64_t nq, 
     SJ_API_END
 }
 
+sj_status sj_self_join_f32(const float *points, uint64_t n, int d, float eps, const sj_build_opts *bopts,
+                           const sj_join_opts *jopts, sj_result **out)
+{
+    SJ_API_BEGIN
+    if (!out) sj::fail(SJ_ERR_ARG, "out is NULL");
+    sj_build_opts bo;
+    if (bopts) bo = *bopts;
+    else sj_build_opts_default(&bo);
+    sj_join_opts jo;
+    if (jopts) jo = *jopts;
+    else sj_join_opts_default(&jo);
+    *out = sj::self_join_f32_impl(points, n, d, eps, bo, jo);
+    return SJ_OK;
+    SJ_API_END
+}
+
 sj_status sj_knn_self(const double *points, uint64_t n, int d, uint32_t k, double eps0, const sj_build_opts *bopts,
                       uint32_t *ids, double *dist2, sj_knn_stats *stats)
 {

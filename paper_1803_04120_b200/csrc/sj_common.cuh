@@ -353,6 +353,8 @@ sj_result *brute_force_impl(const double *points, uint64_t n, int d, double eps,
 // variants.cu
 sj_result *join_sets_impl(const sj_index *idx, const double *queries, uint64_t nq, int queries_on_device,
                           const sj_join_opts &o);
+sj_result *self_join_f32_impl(const float *points, uint64_t n, int d, float eps, const sj_build_opts &bo,
+                              const sj_join_opts &o);
 void knn_self_impl(const double *points, uint64_t n, int d, uint32_t k, double eps0, const sj_build_opts &bo,
                    uint32_t *ids, double *dist2, sj_knn_stats *st);
 

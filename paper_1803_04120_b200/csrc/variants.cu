@@ -39,7 +39,9 @@ struct ProbeArgs {
     const uint32_t *qlist;        // optional: query rows to process (kNN re-runs: original ids)
     uint32_t q_begin, nq;         // queries q_begin .. q_begin+nq-1 (rows, or qlist entries)
     int q_index;                  // 1: the queries are the index's own points in A-order (X, A)
-    int self;                     // kNN: skip the candidate whose id is the query's
+    int self;                     // skip the candidate whose id is the query's (kNN; include_self = 0)
+    int f32;                      // predicate in binary32 (FP32 self-join, R21): s32 <= eps2f
+    float eps2f;
     uint32_t *counts;             // count: per query (index t - q_begin)
     unsigned long long *buckets;  // count: per 1024 queries
     uint32_t *nonfinite;          // count: set when a query coordinate is NaN / inf
@@ -171,7 +173,26 @@ __global__ void __launch_bounds__(kProbeThreads) k_probe(const DevIndex ix, cons
                 bool hit = false;
                 double s = 0.0;
                 uint32_t pid = 0;
-                if (act) {
+                if (act && pa.f32) {
+                    // R21: coordinates are floats widened exactly; the distance in binary32, left to right
+                    float s32;
+                    {
+                        const float d0 = __fsub_rn((float)x[0], (float)__ldg(ix.X + m));
+                        s32 = __fmul_rn(d0, d0);
+                    }
+#pragma unroll
+                    for (int j = 1; j < D; ++j) {
+                        const float dj = __fsub_rn((float)x[j], (float)__ldg(ix.X + (uint64_t)j * n + m));
+                        s32 = __fadd_rn(s32, __fmul_rn(dj, dj));
+                    }
+                    ++tests;
+                    s = (double)s32;
+                    hit = s32 <= pa.eps2f;
+                    if (hit) {
+                        pid = __ldg(ix.A + m);
+                        if (pa.self && pid == qid) hit = false;
+                    }
+                } else if (act) {
                     {
                         const double d0 = __dsub_rn(x[0], __ldg(ix.X + m));
                         s = __dmul_rn(d0, d0);
@@ -185,7 +206,7 @@ __global__ void __launch_bounds__(kProbeThreads) k_probe(const DevIndex ix, cons
                     hit = s <= ix.eps2;
                     if (hit) {
                         pid = __ldg(ix.A + m);
-                        if (MODE == kPKnn && pa.self && pid == qid) hit = false;
+                        if (pa.self && pid == qid) hit = false;
                     }
                 }
                 const unsigned hb = __ballot_sync(0xffffffffu, hit);
@@ -290,42 +311,22 @@ void free_batches(sj_result *res)
 
 }  // namespace
 
-// ------------------------------------------------------------------ two-set join
-sj_result *join_sets_impl(const sj_index *idx, const double *queries, uint64_t nq, int queries_on_device,
-                          const sj_join_opts &o)
+// ------------------------------------------------------------------ count -> plan -> fill
+namespace {
+// Runs the exact two-pass join of the queries described by `q` (q.q / q.qlist / q.q_index / q.self /
+// q.f32 set by the caller) over ix into res: per-query counts, a batch plan of contiguous query ranges
+// of <= target pairs, one fill launch per batch.  Throws SJ_ERR_NONFINITE for a non-finite query.
+void probe_join(const DevIndex &ix, int dev, const ProbeArgs &q, uint64_t nq, const sj_join_opts &o,
+                cudaStream_t s, sj_result *res)
 {
-    if (!idx) fail(SJ_ERR_STATE, "index is NULL");
-    if (nq >= (1ull << 32)) fail(SJ_ERR_ARG, "the number of queries must be < 2^32");
-    if (nq && !queries) fail(SJ_ERR_ARG, "queries is NULL");
-    if (o.batch_capacity_pairs == 0) fail(SJ_ERR_ARG, "batch_capacity_pairs must be > 0");
-    if (o.drain_csr) fail(SJ_ERR_ARG, "drain_csr is not supported by the two-set join");
-    const DevIndex &ix = idx->dev;
-    const int dev = idx->device;
-    SJ_CUDA(cudaSetDevice(dev));
-    CtxGuard cg{acquire_ctx(dev, 1, 2, 64)};
-    cudaStream_t s = cg.c->streams[0];
-    // ordered after the caller's work on the legacy default stream (e.g. torch producing Q)
-    SJ_CUDA(cudaEventRecord(cg.c->events[1], cudaStreamLegacy));
-    SJ_CUDA(cudaStreamWaitEvent(s, cg.c->events[1], 0));
-    const uint32_t NQ = (uint32_t)nq;
-    const int D = ix.d;
-    const double *qd = queries;
-    Scratch<double> qcopy;
-    if (nq && !queries_on_device) {
-        qcopy.p = dalloc<double>(nq * D, s);
-        qcopy.s = s;
-        SJ_CUDA(cudaMemcpyAsync(qcopy.p, queries, sizeof(double) * nq * D, cudaMemcpyHostToDevice, s));
-        qd = qcopy.p;
-    }
     const uint64_t nbk = (nq + 1023) / 1024;
     // device words: [0..3) work, [3] nonfinite flag, [4] cursor, [5] overflow; then the bucket sums
     Scratch<unsigned long long> words(8 + nbk, s);
     Scratch<uint32_t> counts(nq, s);
     SJ_CUDA(cudaMemsetAsync(words.p, 0, sizeof(unsigned long long) * (8 + nbk), s));
-    ProbeArgs pa{};
-    pa.q = qd;
+    ProbeArgs pa = q;
     pa.q_begin = 0;
-    pa.nq = NQ;
+    pa.nq = (uint32_t)nq;
     pa.counts = counts.p;
     pa.buckets = words.p + 8;
     pa.nonfinite = reinterpret_cast<uint32_t *>(words.p + 3);
@@ -357,9 +358,9 @@ sj_result *join_sets_impl(const sj_index *idx, const double *queries, uint64_t n
             }
             qc.resize(bq1 - bq0);
             SJ_CUDA(cudaMemcpy(qc.data(), counts.p + bq0, sizeof(uint32_t) * qc.size(), cudaMemcpyDeviceToHost));
-            for (uint64_t q = bq0; q < bq1; ++q) {
-                const uint64_t c = qc[q - bq0];
-                if (acc && acc + c > target) { cuts.push_back(q); sizes.push_back(acc); acc = 0; }
+            for (uint64_t i = bq0; i < bq1; ++i) {
+                const uint64_t c = qc[i - bq0];
+                if (acc && acc + c > target) { cuts.push_back(i); sizes.push_back(acc); acc = 0; }
                 acc += c;
             }
         }
@@ -367,6 +368,76 @@ sj_result *join_sets_impl(const sj_index *idx, const double *queries, uint64_t n
         sizes.push_back(acc);
     }
 
+    const uint64_t w0 = hw[0], w1 = hw[1];
+    SJ_CUDA(cudaMemsetAsync(words.p, 0, sizeof(unsigned long long) * 8, s));
+    for (size_t b = 0; b + 1 < cuts.size(); ++b) {
+        if (total && sizes[b] == 0) continue;     // an empty range between two non-empty ones
+        sj_batch bt;
+        bt.cap = std::max<uint64_t>(sizes[b], 1);
+        bt.pairs = dalloc<uint64_t>(bt.cap, s);
+        bt.on_device = 1;
+        bt.n = sizes[b];
+        res->batches.push_back(bt);               // owned by res from here (freed on failure)
+        SJ_CUDA(cudaMemsetAsync(words.p + 4, 0, 16, s));
+        ProbeArgs pf = q;
+        pf.q_begin = (uint32_t)cuts[b];
+        pf.nq = (uint32_t)(cuts[b + 1] - cuts[b]);
+        pf.out = bt.pairs;
+        pf.cursor = words.p + 4;
+        pf.cap = bt.cap;
+        pf.overflow = reinterpret_cast<uint32_t *>(words.p + 5);
+        pf.work = nullptr;
+        if (sizes[b]) launch_probe(kPFill, ix, pf, dev, s);
+        if (o.sort_pairs) sort_pairs_device(bt.pairs, bt.n, res->n_points, s);
+        if (o.result_on_host) {
+            uint64_t *h = static_cast<uint64_t *>(host_pinned_alloc(bt.cap * 8, nullptr));
+            if (bt.n) SJ_CUDA(cudaMemcpyAsync(h, bt.pairs, bt.n * 8, cudaMemcpyDeviceToHost, s));
+            SJ_CUDA(cudaStreamSynchronize(s));
+            dev_free(bt.pairs, s);
+            res->batches.back().pairs = h;
+            res->batches.back().on_device = 0;
+        }
+    }
+    unsigned long long tail[2];
+    SJ_CUDA(cudaMemcpyAsync(tail, words.p + 4, 16, cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaStreamSynchronize(s));
+    if (tail[1]) fail(SJ_ERR_STATE, "probe join: fill pass exceeded its exact count (internal error)");
+    res->total = total;
+    res->stats.pairs = total;
+    res->stats.estimated_pairs = total;
+    res->stats.cells_probed = 2 * w0;
+    res->stats.candidates_tested = 2 * w1;
+    res->stats.batches = (uint32_t)res->batches.size();
+    res->stats.refine_launches = (uint32_t)res->batches.size() + 1;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ two-set join
+sj_result *join_sets_impl(const sj_index *idx, const double *queries, uint64_t nq, int queries_on_device,
+                          const sj_join_opts &o)
+{
+    if (!idx) fail(SJ_ERR_STATE, "index is NULL");
+    if (nq >= (1ull << 32)) fail(SJ_ERR_ARG, "the number of queries must be < 2^32");
+    if (nq && !queries) fail(SJ_ERR_ARG, "queries is NULL");
+    if (o.batch_capacity_pairs == 0) fail(SJ_ERR_ARG, "batch_capacity_pairs must be > 0");
+    if (o.drain_csr) fail(SJ_ERR_ARG, "drain_csr is not supported by the two-set join");
+    const DevIndex &ix = idx->dev;
+    const int dev = idx->device;
+    SJ_CUDA(cudaSetDevice(dev));
+    CtxGuard cg{acquire_ctx(dev, 1, 2, 64)};
+    cudaStream_t s = cg.c->streams[0];
+    // ordered after the caller's work on the legacy default stream (e.g. torch producing Q)
+    SJ_CUDA(cudaEventRecord(cg.c->events[1], cudaStreamLegacy));
+    SJ_CUDA(cudaStreamWaitEvent(s, cg.c->events[1], 0));
+    const int D = ix.d;
+    const double *qd = queries;
+    Scratch<double> qcopy;
+    if (nq && !queries_on_device) {
+        qcopy.p = dalloc<double>(nq * D, s);
+        qcopy.s = s;
+        SJ_CUDA(cudaMemcpyAsync(qcopy.p, queries, sizeof(double) * nq * D, cudaMemcpyHostToDevice, s));
+        qd = qcopy.p;
+    }
     sj_result *res = new sj_result();
     res->device = dev;
     res->n_points = std::max<uint64_t>(nq, ix.n);
@@ -376,54 +447,88 @@ sj_result *join_sets_impl(const sj_index *idx, const double *queries, uint64_t n
     res->unicomp = 0;
     res->two_set = 1;
     try {
-        const uint64_t w0 = hw[0], w1 = hw[1];
-        SJ_CUDA(cudaMemsetAsync(words.p, 0, sizeof(unsigned long long) * 8, s));
-        for (size_t b = 0; b + 1 < cuts.size(); ++b) {
-            if (total && sizes[b] == 0) continue;     // an empty range between two non-empty ones
-            sj_batch bt;
-            bt.cap = std::max<uint64_t>(sizes[b], 1);
-            bt.pairs = dalloc<uint64_t>(bt.cap, s);
-            bt.on_device = 1;
-            bt.n = sizes[b];
-            SJ_CUDA(cudaMemsetAsync(words.p + 4, 0, 16, s));
-            ProbeArgs pf{};
-            pf.q = qd;
-            pf.q_begin = (uint32_t)cuts[b];
-            pf.nq = (uint32_t)(cuts[b + 1] - cuts[b]);
-            pf.out = bt.pairs;
-            pf.cursor = words.p + 4;
-            pf.cap = bt.cap;
-            pf.overflow = reinterpret_cast<uint32_t *>(words.p + 5);
-            pf.work = nullptr;
-            if (sizes[b]) launch_probe(kPFill, ix, pf, dev, s);
-            if (o.sort_pairs) sort_pairs_device(bt.pairs, bt.n, res->n_points, s);
-            if (o.result_on_host) {
-                uint64_t *h = static_cast<uint64_t *>(host_pinned_alloc(bt.cap * 8, nullptr));
-                if (bt.n) SJ_CUDA(cudaMemcpyAsync(h, bt.pairs, bt.n * 8, cudaMemcpyDeviceToHost, s));
-                SJ_CUDA(cudaStreamSynchronize(s));
-                dev_free(bt.pairs, s);
-                bt.pairs = h;
-                bt.on_device = 0;
-            }
-            res->batches.push_back(bt);
-        }
-        unsigned long long tail[2];
-        SJ_CUDA(cudaMemcpyAsync(tail, words.p + 4, 16, cudaMemcpyDeviceToHost, s));
-        SJ_CUDA(cudaStreamSynchronize(s));
-        if (tail[1]) fail(SJ_ERR_STATE, "two-set join: fill pass exceeded its exact count (internal error)");
-        res->total = total;
-        res->stats.pairs = total;
-        res->stats.estimated_pairs = total;
-        res->stats.cells_probed = 2 * w0;
-        res->stats.candidates_tested = 2 * w1;
-        res->stats.batches = (uint32_t)res->batches.size();
-        res->stats.refine_launches = (uint32_t)res->batches.size() + 1;
+        ProbeArgs q{};
+        q.q = qd;
+        probe_join(ix, dev, q, nq, o, s, res);
     } catch (...) {
         cudaStreamSynchronize(s);
         free_batches(res);
         delete res;
         throw;
     }
+    return res;
+}
+
+// ------------------------------------------------------------------ FP32 self-join
+namespace {
+__global__ void k_f32_to_f64(const float *__restrict__ in, double *__restrict__ out, uint64_t m)
+{
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = (double)in[i];
+}
+}  // namespace
+
+sj_result *self_join_f32_impl(const float *points, uint64_t n, int d, float eps, const sj_build_opts &bo,
+                              const sj_join_opts &o)
+{
+    if (d < 2 || d > SJ_MAX_DIM) fail(SJ_ERR_DIM, "d must be in [2,6]");
+    if (!points) fail(SJ_ERR_ARG, "points is NULL");
+    if (n == 0 || n >= (1ull << 32)) fail(SJ_ERR_ARG, "N must satisfy 1 <= N < 2^32");
+    if (!std::isfinite(eps) || !(eps > 0.0f)) fail(SJ_ERR_ARG, "eps must be finite and > 0");
+    volatile float e2v = eps * eps;              // fl32(eps*eps)
+    const float eps2f = e2v;
+    if (!std::isnormal(eps2f)) fail(SJ_ERR_ARG, "fl32(eps*eps) must be a normal float");
+    if (o.batch_capacity_pairs == 0) fail(SJ_ERR_ARG, "batch_capacity_pairs must be > 0");
+    if (o.drain_csr) fail(SJ_ERR_ARG, "drain_csr is not supported by the FP32 join");
+    if (bo.device < 0 || bo.device >= device_count()) fail(SJ_ERR_ARG, "bad device ordinal");
+    SJ_CUDA(cudaSetDevice(bo.device));
+    CtxGuard cg{acquire_ctx(bo.device, 1, 2, 64)};
+    cudaStream_t s = cg.c->streams[0];
+    SJ_CUDA(cudaEventRecord(cg.c->events[1], cudaStreamLegacy));
+    SJ_CUDA(cudaStreamWaitEvent(s, cg.c->events[1], 0));
+    // the points widened to binary64 (exact) for the grid index
+    const uint64_t m = n * (uint64_t)d;
+    Scratch<float> fcopy;
+    const float *fp = points;
+    if (!bo.points_on_device) {
+        fcopy.p = dalloc<float>(m, s);
+        fcopy.s = s;
+        SJ_CUDA(cudaMemcpyAsync(fcopy.p, points, sizeof(float) * m, cudaMemcpyHostToDevice, s));
+        fp = fcopy.p;
+    }
+    Scratch<double> wide(m, s);
+    k_f32_to_f64<<<(unsigned)std::min<uint64_t>((m + 255) / 256, (uint64_t)device_sm_count(bo.device) * 8), 256, 0, s>>>(
+        fp, wide.p, m);
+    SJ_LAUNCHED();
+    // R21: the float predicate can accept a pair whose exact distance exceeds eps by a relative
+    // (d + 3) * 2^-24 at most; a grid for eps * (1 + 2^-16) keeps every such pair in adjacent cells
+    sj_build_opts b2 = bo;
+    b2.points_on_device = 1;
+    b2.stream = s;
+    b2.speculative_estimate = 0;
+    sj_index *idx = build_index_impl(wide.p, n, d, (double)eps * (1.0 + std::ldexp(1.0, -16)), b2);
+    sj_result *res = new sj_result();
+    res->device = bo.device;
+    res->n_points = n;
+    res->q0 = 0;
+    res->q1 = n;
+    res->include_self = o.include_self;
+    res->unicomp = 0;
+    try {
+        ProbeArgs q{};
+        q.q_index = 1;
+        q.self = !o.include_self;
+        q.f32 = 1;
+        q.eps2f = eps2f;
+        probe_join(idx->dev, bo.device, q, n, o, s, res);
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        free_batches(res);
+        delete res;
+        free_index_impl(idx);
+        throw;
+    }
+    free_index_impl(idx);
     return res;
 }
 

@@ -136,6 +136,8 @@ def load_library(path: str = LIB_PATH):
     L.sj_brute_force_join.restype = i32
     L.sj_join_sets.argtypes = [vp, vp, u64, i32, P(JoinOpts), P(vp)]
     L.sj_join_sets.restype = i32
+    L.sj_self_join_f32.argtypes = [vp, u64, i32, ctypes.c_float, P(BuildOpts), P(JoinOpts), P(vp)]
+    L.sj_self_join_f32.restype = i32
     L.sj_knn_self.argtypes = [vp, u64, i32, u32, dbl, P(BuildOpts), vp, vp, P(KnnStats)]
     L.sj_knn_self.restype = i32
     L.sj_index_export.argtypes = [vp, P(IndexView)]
@@ -654,6 +656,46 @@ def join_sets(index: Index, queries, batch_capacity_pairs: Optional[int] = None,
     del keep
     r = Result(h.value)
     r.device = index.device
+    return r
+
+
+def self_join_f32(points, eps: float, include_self: bool = True, result_on_host: bool = False,
+                  sort_pairs: bool = False, batch_capacity_pairs: Optional[int] = None,
+                  min_batches: Optional[int] = None, device: Optional[int] = None) -> Result:
+    """sj_self_join_f32 (PAPER.md:393 32-bit floats; R21): the self-join of float32 points with
+    the predicate evaluated in binary32.  points: n x d float32 torch tensor (cuda or cpu) or numpy."""
+    import torch
+    L = load_library()
+    bo = BuildOpts()
+    L.sj_build_opts_default(ctypes.byref(bo))
+    if isinstance(points, torch.Tensor):
+        t = points.contiguous()
+        if t.dtype != torch.float32 or t.dim() != 2:
+            raise TypeError("points must be a 2-D float32 tensor")
+        keep, ptr = t, t.data_ptr()
+        bo.points_on_device = int(t.is_cuda)
+        bo.device = (t.device.index if t.is_cuda else 0) if device is None else device
+        n, d = t.shape
+    else:
+        a = np.ascontiguousarray(points, dtype=np.float32)
+        if a.ndim != 2:
+            raise TypeError("points must be n x d")
+        keep, ptr = a, a.ctypes.data
+        bo.points_on_device = 0
+        bo.device = 0 if device is None else device
+        n, d = a.shape
+    kw = dict(include_self=include_self, result_on_host=result_on_host, sort_pairs=sort_pairs)
+    if batch_capacity_pairs is not None:
+        kw["batch_capacity_pairs"] = batch_capacity_pairs
+    if min_batches is not None:
+        kw["min_batches"] = min_batches
+    o = join_opts(**kw)
+    h = ctypes.c_void_p()
+    _check(L.sj_self_join_f32(ctypes.c_void_p(ptr), n, d, float(np.float32(eps)), ctypes.byref(bo), ctypes.byref(o),
+                              ctypes.byref(h)))
+    del keep
+    r = Result(h.value)
+    r.device = bo.device
     return r
 
 

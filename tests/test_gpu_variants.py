@@ -4,7 +4,8 @@
 * two-set join J(Q,P) (sj_join_sets; DESIGN.md R19): pair sets bit-exact after canonical sort;
 * kNN self-join (sj_knn_self; R20): ids AND the float64 bits of s bit-exact (the same operation order on
   both sides, ties broken by id), at sizes spanning many warps and radius rounds, and on sampled rows
-  at full size.
+  at full size;
+* FP32 self-join (sj_self_join_f32; R21): pair sets bit-exact against the binary32 oracle.
 """
 import math
 
@@ -200,3 +201,58 @@ def test_knn_full_size_sampled_rows(sj, cfg, d, k, eps0):
     wi, ws = oracle.knn(P, k, qids=q)
     assert np.array_equal(ids[q], wi)
     assert np.array_equal(s[q].view(np.uint64), ws.view(np.uint64))
+
+
+# ------------------------------------------------------------------ FP32 self-join (R21)
+F32 = [(d, m) for d in (2, 3, 4, 5, 6) for m in (2, 50)]
+
+
+@pytest.mark.parametrize("d,m", F32)
+def test_f32_self_join_exact(sj, d, m):
+    """float32 uniform points, ~m neighbours: the GPU's binary32 join == the oracle's, pair for pair,
+    with and without self pairs, device and host input."""
+    P = datagen.uniform(4000, d, seed=500 + d, hi=50.0).astype(np.float32)
+    eps = float(np.float32(_eps_for(4000, d, m, L=50.0)))
+    want = oracle.brute_force_f32(P, eps)
+    res = sj.self_join_f32(torch.from_numpy(P).cuda(), eps)
+    assert np.array_equal(res.to_numpy(sort=True), want)
+    assert res.n_batches >= 3
+    ns = sj.self_join_f32(P, eps, include_self=False, batch_capacity_pairs=999).to_numpy(sort=True)
+    assert np.array_equal(ns, oracle.brute_force_f32(P, eps, include_self=False))
+
+
+@pytest.mark.parametrize("d", [2, 3, 6])
+def test_f32_knife_edge_and_rounding(sj, d):
+    """Knife-edge float lattices (pairs at eps and +-1-2 float ulps), the hand-worked (1, 2^-13) case
+    (binary32 accepts, binary64 rejects) and the lattice closed form."""
+    eps = 0.75
+    P = datagen.knife_edge(3000, d, eps, seed=21 + d).astype(np.float32)
+    assert np.array_equal(sj.self_join_f32(P, eps).to_numpy(sort=True), oracle.brute_force_f32(P, eps))
+    A = np.zeros((2, d), np.float32)
+    A[1, 0] = 1.0
+    A[1, 1] = 2.0 ** -13
+    assert sj.self_join_f32(A, 1.0).to_numpy(sort=True).tolist() == [0, 1, 1 << 32, (1 << 32) | 1]
+    L = {2: 30, 3: 10, 6: 3}[d]
+    Lp = datagen.lattice(L, d).astype(np.float32)
+    assert sj.self_join_f32(Lp, 1.0).n_pairs == L ** d + 2 * d * (L - 1) * L ** (d - 1)
+
+
+def test_f32_full_size(sj):
+    """Syn-6D 2 M (C2) rounded to float32 at eps = 8 (the C3 density): the GPU set lies between the
+    (pinned) FP64 oracle joins at eps(1 -+ 1e-5), and every pair inside that bracket is decided as the
+    FP32 oracle decides it on the pair alone."""
+    P32 = datagen.uniform_config("C2", 6).astype(np.float32)
+    res = sj.self_join_f32(torch.from_numpy(P32).cuda(), 8.0)
+    got = res.to_numpy(sort=True)
+    P64 = P32.astype(np.float64)
+    lo = oracle.grid_join(P64, 8.0 * (1 - 1e-5))
+    hi = oracle.grid_join(P64, 8.0 * (1 + 1e-5))
+    assert np.isin(lo, got).all() and np.isin(got, hi).all()
+    diff = np.setdiff1d(hi, lo)
+    assert len(diff) < 5000
+    ing = np.isin(diff, got)
+    for x, g in zip(diff.tolist(), ing.tolist()):
+        i, k = x >> 32, x & 0xFFFFFFFF
+        want = len(oracle.brute_force_f32(P32[[i, k]], 8.0, include_self=False)) == 2
+        assert g == want, (i, k)
+    res.free()
