@@ -1,7 +1,11 @@
 """compute-sanitizer over the CUDA path (SURVEY §4 hygiene; PAPER.md:238 atomic emission):
 memcheck (out-of-bounds / misaligned global and shared accesses) and racecheck (shared-memory
 hazards: the dense kernel's per-warp emission buffers, the radix sort's warp counters, the bucket
-sorter) on C1 and two small 6-D clouds.  Each run must report 0 errors and its own parity check."""
+sorter) on C1 and two small 6-D clouds.  Each run must report 0 errors and its own parity check.
+
+Opt-in (SJ_SANITIZER=1): the GPU pool this project is measured on has compute-sanitizer disabled (runs
+under it left GPUs needing a reset), so by default these are skipped; the bounds checks of the kernels
+(capacity / overflow flags, SJ_ERR_* on bad arguments) and the element-by-element parity tests stand in."""
 import os
 import re
 import shutil
@@ -24,10 +28,14 @@ def test_sanitizer_clean(tool, case):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
+    if os.environ.get("SJ_SANITIZER") != "1":
+        pytest.skip("compute-sanitizer is opt-in (SJ_SANITIZER=1): disabled on the measurement pool")
     cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "99", sys.executable,
            os.path.join(ROOT, "tools", "sanitize_case.py"), case]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     out = r.stdout + r.stderr
+    if "closed on this pool" in out:
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert r.returncode == 0, out[-4000:]
     # memcheck / synccheck print "ERROR SUMMARY: 0 errors", racecheck "RACECHECK SUMMARY: 0 hazards
     # displayed (0 errors, 0 warnings)"
