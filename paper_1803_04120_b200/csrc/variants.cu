@@ -12,7 +12,9 @@
 //      [1, |g_j|-2] and are occupied (M_j, Alg. 1 l.6) form a 3-bit set, so boundary and masked queries
 //      enumerate only the product of what can exist;
 //   2. the lanes look up 32 of those cells at a time: linear id (R8), prefix p = sum c_j * pstride_j, the
-//      directory range [dir[p], dir[p+1]) of B, one bounded binary search (PAPER.md:173 B, G);
+//      directory range [dir[p], dir[p+1]) of B, one bounded binary search (PAPER.md:173 B, G); on
+//      cell-scan indexes (sparse: a few cells per top-k prefix) the lanes enumerate the 3^k top prefixes
+//      instead (occupancy bitmaps drop the empty ones) and the warp scans their cells' low coordinates;
 //   3. the cells' point ranges are concatenated by a warp prefix sum and swept 32 candidates per step,
 //      each lane finding its candidate's cell by a 5-step shuffle search -- the warp stays converged and
 //      every lane tests a candidate even when the cells hold one point each (sparse 6-D);
@@ -62,13 +64,151 @@ __device__ __forceinline__ bool kv_less(uint64_t as, uint32_t ai, uint64_t bs, u
     return as < bs || (as == bs && ai < bi);
 }
 
+// Per-query state of the warp (every lane holds the same query; kNN: lane i < k holds the i-th best).
+struct ProbeState {
+    uint32_t found;                 // hits so far (all lanes agree)
+    uint64_t bs;                    // kNN: this lane's entry (s bits, id); sentinels sort last
+    uint32_t bi;
+    uint64_t kth_s;                 // kNN: the k-th entry (warp-uniform)
+    uint32_t kth_i;
+    unsigned long long tests;       // this lane's distance evaluations
+};
+
+// Lane-level flattening: given one range [lo, hi) per lane, returns (via the shuffle search) for
+// position f of the concatenation the owner lane's lo and exclusive prefix.  inc = inclusive prefix of
+// the lengths across lanes.
+__device__ __forceinline__ uint32_t owner_of(uint32_t inc, uint32_t f)
+{
+    uint32_t pos = 0;                                   // lanes whose range ends at or before f
+#pragma unroll
+    for (uint32_t s = 16; s; s >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, inc, pos + s - 1u);
+        if (v <= f) pos += s;
+    }
+    return pos & 31u;
+}
+
+__device__ __forceinline__ uint32_t warp_inclusive(uint32_t v, uint32_t lane)
+{
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, v, s);
+        if (lane >= (uint32_t)s) v += t;
+    }
+    return v;
+}
+
+// Test every point of the lanes' A-ranges [lo, hi) against the query, 32 candidates per step over the
+// concatenation (Alg. 1 l.12-16 with R1's predicate), and hand the hits to the mode.
 template <int D, int MODE>
-__global__ void __launch_bounds__(kProbeThreads) k_probe(const DevIndex ix, const ProbeArgs pa)
+__device__ __forceinline__ void sweep(const DevIndex &ix, const ProbeArgs &pa, const double (&x)[D], uint32_t qid,
+                                      uint32_t lo, uint32_t hi, uint32_t lane, ProbeState &st)
+{
+    const uint32_t n = ix.n;
+    const uint32_t len = hi - lo;
+    const uint32_t inc = warp_inclusive(len, lane);
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    const uint32_t exc = inc - len;
+    for (uint32_t f0 = 0; f0 < total; f0 += 32u) {
+        const uint32_t f = f0 + lane;
+        const uint32_t own = owner_of(inc, f);
+        const uint32_t olo = __shfl_sync(0xffffffffu, lo, own);
+        const uint32_t oexc = __shfl_sync(0xffffffffu, exc, own);
+        const bool act = f < total;
+        const uint32_t m = olo + (f - oexc);
+        bool hit = false;
+        double s = 0.0;
+        uint32_t pid = 0;
+        if (act && pa.f32) {
+            // R21: coordinates are floats widened exactly; the distance in binary32, left to right
+            float s32;
+            {
+                const float d0 = __fsub_rn((float)x[0], (float)__ldg(ix.X + m));
+                s32 = __fmul_rn(d0, d0);
+            }
+#pragma unroll
+            for (int j = 1; j < D; ++j) {
+                const float dj = __fsub_rn((float)x[j], (float)__ldg(ix.X + (uint64_t)j * n + m));
+                s32 = __fadd_rn(s32, __fmul_rn(dj, dj));
+            }
+            ++st.tests;
+            hit = s32 <= pa.eps2f;
+        } else if (act) {
+            {
+                const double d0 = __dsub_rn(x[0], __ldg(ix.X + m));
+                s = __dmul_rn(d0, d0);
+            }
+#pragma unroll
+            for (int j = 1; j < D; ++j) {
+                const double dj = __dsub_rn(x[j], __ldg(ix.X + (uint64_t)j * n + m));
+                s = __dadd_rn(s, __dmul_rn(dj, dj));
+            }
+            ++st.tests;
+            hit = s <= ix.eps2;
+        }
+        if (hit) {
+            pid = __ldg(ix.A + m);
+            if (pa.self && pid == qid) hit = false;
+        }
+        const unsigned hb = __ballot_sync(0xffffffffu, hit);
+        st.found += (uint32_t)__popc(hb);
+        if constexpr (MODE == kPFill) {
+            if (hb) {
+                unsigned long long b0 = 0;
+                if (lane == 0) b0 = atomicAdd(pa.cursor, (unsigned long long)__popc(hb));
+                b0 = __shfl_sync(0xffffffffu, b0, 0);
+                if (hit) {
+                    const unsigned long long at = b0 + (unsigned long long)__popc(hb & ((1u << lane) - 1u));
+                    if (at < pa.cap) pa.out[at] = ((uint64_t)qid << 32) | pid;
+                    else atomicOr(pa.overflow, 1u);
+                }
+            }
+        } else if constexpr (MODE == kPKnn) {
+            const uint64_t sb = (uint64_t)__double_as_longlong(s);
+            unsigned surv = __ballot_sync(0xffffffffu, hit && kv_less(sb, pid, st.kth_s, st.kth_i));
+            while (surv) {
+                const int src = __ffs(surv) - 1;
+                surv &= surv - 1u;
+                const uint64_t cs = __shfl_sync(0xffffffffu, sb, src);
+                const uint32_t ci = __shfl_sync(0xffffffffu, pid, src);
+                if (!kv_less(cs, ci, st.kth_s, st.kth_i)) continue;          // warp-uniform
+                const bool gt = lane < pa.k && kv_less(cs, ci, st.bs, st.bi);
+                const uint32_t ins = pa.k - (uint32_t)__popc(__ballot_sync(0xffffffffu, gt));
+                const uint64_t us = __shfl_up_sync(0xffffffffu, st.bs, 1);
+                const uint32_t ui = __shfl_up_sync(0xffffffffu, st.bi, 1);
+                if (lane == ins) { st.bs = cs; st.bi = ci; }
+                else if (lane > ins && lane < pa.k) { st.bs = us; st.bi = ui; }
+                st.kth_s = __shfl_sync(0xffffffffu, st.bs, pa.k - 1u);
+                st.kth_i = __shfl_sync(0xffffffffu, st.bi, pa.k - 1u);
+            }
+        }
+    }
+}
+
+// Decode the r-th member (mixed radix over the dims' valid sets) of the neighbour enumeration: the
+// e-th set bit of sel_j is the coordinate (c_j - 1) + e.
+__device__ __forceinline__ uint64_t pick(uint32_t sel, uint32_t rj, uint64_t c0)
+{
+    uint32_t m = sel;
+    if (rj >= 1u) m &= m - 1u;
+    if (rj >= 2u) m &= m - 1u;
+    return c0 - 1u + (uint64_t)(__ffs(m) - 1);
+}
+
+template <int D, int MODE>
+#ifndef SJ_PROBE_MINB
+#define SJ_PROBE_MINB 4   // 4 x 256 threads per SM (<= 64 registers): 6-D eps=8 two-set 82 -> 68 ms, kNN 6-D 74 -> 68 ms (2: slower)
+#endif
+__global__ void __launch_bounds__(kProbeThreads, SJ_PROBE_MINB) k_probe(const DevIndex ix, const ProbeArgs pa)
 {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t n = ix.n;
     unsigned long long probes = 0, tests = 0, hits_all = 0;
+    // cell-scan indexes (few cells per top-k prefix): enumerate the 3^k top prefixes and scan their
+    // cells, instead of one bounded binary search per neighbour cell (3^d of them)
+    const bool prefix_scan = ix.search_mode == kSearchCellScan && ix.dir_k < D;
+    const int L = D - ix.dir_k;
     for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < pa.nq; t += warps) {
         const uint32_t row = pa.q_begin + t;
         uint32_t qid;
@@ -82,10 +222,10 @@ __global__ void __launch_bounds__(kProbeThreads) k_probe(const DevIndex ix, cons
 #pragma unroll
             for (int j = 0; j < D; ++j) x[j] = __ldg(pa.q + (uint64_t)qid * D + j);
         }
-        // ---- 1. per dimension: c_j - 1 (R7 against the index's geometry) and the valid neighbour set
+        // ---- 1. per dimension: c_j (R7 against the index's geometry) and the valid neighbour set
         uint64_t c0[D];
         uint32_t sel[D];
-        uint32_t ncell = 1;
+        uint32_t ncell = 1, ntop = 1;
         bool finite = true;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
@@ -109,140 +249,115 @@ __global__ void __launch_bounds__(kProbeThreads) k_probe(const DevIndex ix, cons
             }
             sel[j] = m;
             ncell *= (uint32_t)__popc(m);
+            if (j >= L) ntop *= (uint32_t)__popc(m);
         }
         if (MODE == kPCount && !finite && lane == 0) atomicOr(pa.nonfinite, 1u);
-        // kNN state: lane i < k holds the i-th best (s bits, id); sentinels sort last
-        uint64_t bs = ~0ull;
-        uint32_t bi = 0xffffffffu;
-        uint64_t kth_s = ~0ull;
-        uint32_t kth_i = 0xffffffffu;
-        uint32_t found = 0;
-        // ---- 2-3. 32 cells per round, looked up by the lanes, candidates swept by the whole warp
-        for (uint32_t base = 0; base < ncell; base += 32u) {
-            uint32_t lo = 0, hi = 0;
-            const uint32_t o = base + lane;
-            if (o < ncell) {
-                uint32_t r = o;
-                uint64_t key = 0, p = 0;
+        ProbeState st{0u, ~0ull, 0xffffffffu, ~0ull, 0xffffffffu, 0ull};
+        if (ncell == 0u) {
+            // nothing adjacent exists
+        } else if (prefix_scan) {
+            // ---- 2a. top prefixes, 32 per round; the occupancy bitmap (dilated +-1 along dimension
+            //      L-1) drops prefixes with no cell near the query's c_{L-1}
+            uint64_t qh = 0, qh2 = 0;
 #pragma unroll
-                for (int j = 0; j < D; ++j) {
-                    const uint32_t nj = (uint32_t)__popc(sel[j]);
-                    const uint32_t rj = r % nj;
-                    r /= nj;
-                    uint32_t m = sel[j];
-                    if (rj >= 1u) m &= m - 1u;
-                    if (rj >= 2u) m &= m - 1u;
-                    const uint64_t cj = c0[j] - 1u + (uint64_t)(__ffs(m) - 1);   // (c_j - 1) + e
-                    key += cj * ix.strides[j];
-                    p += cj * ix.pstride[j];
-                }
-                ++probes;
-                uint32_t h = __ldg(ix.dir + p);
-                uint32_t h1 = __ldg(ix.dir + p + 1);
-                while (h < h1) {
-                    const uint32_t mid = (h + h1) >> 1;
-                    if (__ldg(ix.B + mid) < key) h = mid + 1;
-                    else h1 = mid;
-                }
-                if (h < ix.nG && __ldg(ix.B + h) == key) {
-                    lo = __ldg(ix.G + h);
-                    hi = __ldg(ix.G + h + 1);
-                }
-            }
-            const uint32_t len = hi - lo;
-            uint32_t inc = len;
+            for (int j = 0; j < D; ++j)
+                if (j < L) { qh += c0[j] * ix.occ_mul[j]; qh2 += c0[j] * ix.occ2_mul[j]; }
+            for (uint32_t base = 0; base < ntop; base += 32u) {
+                uint32_t clo = 0, chi = 0;
+                const uint32_t o = base + lane;
+                if (o < ntop) {
+                    uint32_t r = o;
+                    uint64_t p = 0, ob = qh, ob2 = qh2;
 #pragma unroll
-            for (int s = 1; s < 32; s <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, inc, s);
-                if (lane >= (uint32_t)s) inc += v;
-            }
-            const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-            const uint32_t exc = inc - len;
-            for (uint32_t f0 = 0; f0 < total; f0 += 32u) {
-                const uint32_t f = f0 + lane;
-                uint32_t pos = 0;                               // lanes whose range ends at or before f
-#pragma unroll
-                for (uint32_t s = 16; s; s >>= 1) {
-                    const uint32_t v = __shfl_sync(0xffffffffu, inc, pos + s - 1u);
-                    if (v <= f) pos += s;
-                }
-                const uint32_t olo = __shfl_sync(0xffffffffu, lo, pos & 31u);
-                const uint32_t oexc = __shfl_sync(0xffffffffu, exc, pos & 31u);
-                const bool act = f < total;
-                const uint32_t m = olo + (f - oexc);
-                bool hit = false;
-                double s = 0.0;
-                uint32_t pid = 0;
-                if (act && pa.f32) {
-                    // R21: coordinates are floats widened exactly; the distance in binary32, left to right
-                    float s32;
-                    {
-                        const float d0 = __fsub_rn((float)x[0], (float)__ldg(ix.X + m));
-                        s32 = __fmul_rn(d0, d0);
+                    for (int j = 0; j < D; ++j) {
+                        if (j < L) continue;
+                        const uint32_t nj = (uint32_t)__popc(sel[j]);
+                        const uint32_t rj = r % nj;
+                        r /= nj;
+                        const uint64_t cj = pick(sel[j], rj, c0[j]);
+                        p += cj * ix.pstride[j];
+                        ob += cj * ix.occ_mul[j];
+                        ob2 += cj * ix.occ2_mul[j];
                     }
-#pragma unroll
-                    for (int j = 1; j < D; ++j) {
-                        const float dj = __fsub_rn((float)x[j], (float)__ldg(ix.X + (uint64_t)j * n + m));
-                        s32 = __fadd_rn(s32, __fmul_rn(dj, dj));
+                    bool live = true;
+                    if (ix.occ) {
+                        live = (__ldg(ix.occ + (ob >> 5)) >> (ob & 31u)) & 1u;
+                        if (live && ix.occ2) live = (__ldg(ix.occ2 + (ob2 >> 5)) >> (ob2 & 31u)) & 1u;
                     }
-                    ++tests;
-                    s = (double)s32;
-                    hit = s32 <= pa.eps2f;
-                    if (hit) {
-                        pid = __ldg(ix.A + m);
-                        if (pa.self && pid == qid) hit = false;
-                    }
-                } else if (act) {
-                    {
-                        const double d0 = __dsub_rn(x[0], __ldg(ix.X + m));
-                        s = __dmul_rn(d0, d0);
-                    }
-#pragma unroll
-                    for (int j = 1; j < D; ++j) {
-                        const double dj = __dsub_rn(x[j], __ldg(ix.X + (uint64_t)j * n + m));
-                        s = __dadd_rn(s, __dmul_rn(dj, dj));
-                    }
-                    ++tests;
-                    hit = s <= ix.eps2;
-                    if (hit) {
-                        pid = __ldg(ix.A + m);
-                        if (pa.self && pid == qid) hit = false;
+                    ++probes;
+                    if (live) {
+                        clo = __ldg(ix.dir + p);
+                        chi = __ldg(ix.dir + p + 1);
                     }
                 }
-                const unsigned hb = __ballot_sync(0xffffffffu, hit);
-                found += (uint32_t)__popc(hb);
-                if constexpr (MODE == kPFill) {
-                    if (hb) {
-                        unsigned long long b0 = 0;
-                        if (lane == 0) b0 = atomicAdd(pa.cursor, (unsigned long long)__popc(hb));
-                        b0 = __shfl_sync(0xffffffffu, b0, 0);
-                        if (hit) {
-                            const unsigned long long at = b0 + (unsigned long long)__popc(hb & ((1u << lane) - 1u));
-                            if (at < pa.cap) pa.out[at] = ((uint64_t)qid << 32) | pid;
-                            else atomicOr(pa.overflow, 1u);
+                // ---- 2b. the prefixes' cells, 32 per step: keep those whose low coordinates are
+                //      adjacent (and valid) -> their point ranges
+                const uint32_t clen = chi - clo;
+                const uint32_t cinc = warp_inclusive(clen, lane);
+                const uint32_t ctotal = __shfl_sync(0xffffffffu, cinc, 31);
+                const uint32_t cexc = cinc - clen;
+                for (uint32_t g0 = 0; g0 < ctotal; g0 += 32u) {
+                    const uint32_t g = g0 + lane;
+                    const uint32_t own = owner_of(cinc, g);
+                    const uint32_t olo = __shfl_sync(0xffffffffu, clo, own);
+                    const uint32_t oexc = __shfl_sync(0xffffffffu, cexc, own);
+                    uint32_t lo = 0, hi = 0;
+                    if (g < ctotal) {
+                        const uint32_t h = olo + (g - oexc);
+                        uint64_t c[D];
+                        key_to_coords<D>(ix, __ldg(ix.B + h), c);
+                        bool ok = true;
+#pragma unroll
+                        for (int j = 0; j < D; ++j) {
+                            if (j >= L) continue;
+                            const uint64_t e = c[j] - (c0[j] - 1u);    // 0..2 when adjacent
+                            ok = ok && e < 3u && ((sel[j] >> e) & 1u);
+                        }
+                        if (ok) {
+                            lo = __ldg(ix.G + h);
+                            hi = __ldg(ix.G + h + 1);
                         }
                     }
-                } else if constexpr (MODE == kPKnn) {
-                    const uint64_t sb = (uint64_t)__double_as_longlong(s);
-                    unsigned surv = __ballot_sync(0xffffffffu, hit && kv_less(sb, pid, kth_s, kth_i));
-                    while (surv) {
-                        const int src = __ffs(surv) - 1;
-                        surv &= surv - 1u;
-                        const uint64_t cs = __shfl_sync(0xffffffffu, sb, src);
-                        const uint32_t ci = __shfl_sync(0xffffffffu, pid, src);
-                        if (!kv_less(cs, ci, kth_s, kth_i)) continue;          // warp-uniform
-                        const bool gt = lane < pa.k && kv_less(cs, ci, bs, bi);
-                        const uint32_t ins = pa.k - (uint32_t)__popc(__ballot_sync(0xffffffffu, gt));
-                        const uint64_t us = __shfl_up_sync(0xffffffffu, bs, 1);
-                        const uint32_t ui = __shfl_up_sync(0xffffffffu, bi, 1);
-                        if (lane == ins) { bs = cs; bi = ci; }
-                        else if (lane > ins && lane < pa.k) { bs = us; bi = ui; }
-                        kth_s = __shfl_sync(0xffffffffu, bs, pa.k - 1u);
-                        kth_i = __shfl_sync(0xffffffffu, bi, pa.k - 1u);
-                    }
+                    sweep<D, MODE>(ix, pa, x, qid, lo, hi, lane, st);
                 }
             }
+        } else {
+            // ---- 2. 32 neighbour cells per round, each looked up by one lane: linear id (R8), prefix
+            //      p = sum c_j * pstride_j, one binary search of B bounded to [dir[p], dir[p+1])
+            for (uint32_t base = 0; base < ncell; base += 32u) {
+                uint32_t lo = 0, hi = 0;
+                const uint32_t o = base + lane;
+                if (o < ncell) {
+                    uint32_t r = o;
+                    uint64_t key = 0, p = 0;
+#pragma unroll
+                    for (int j = 0; j < D; ++j) {
+                        const uint32_t nj = (uint32_t)__popc(sel[j]);
+                        const uint32_t rj = r % nj;
+                        r /= nj;
+                        const uint64_t cj = pick(sel[j], rj, c0[j]);
+                        key += cj * ix.strides[j];
+                        p += cj * ix.pstride[j];
+                    }
+                    ++probes;
+                    uint32_t h = __ldg(ix.dir + p);
+                    uint32_t h1 = __ldg(ix.dir + p + 1);
+                    while (h < h1) {
+                        const uint32_t mid = (h + h1) >> 1;
+                        if (__ldg(ix.B + mid) < key) h = mid + 1;
+                        else h1 = mid;
+                    }
+                    if (h < ix.nG && __ldg(ix.B + h) == key) {
+                        lo = __ldg(ix.G + h);
+                        hi = __ldg(ix.G + h + 1);
+                    }
+                }
+                // ---- 3. the cells' points, swept by the whole warp
+                sweep<D, MODE>(ix, pa, x, qid, lo, hi, lane, st);
+            }
         }
+        tests += st.tests;
+        const uint32_t found = st.found;
         hits_all += found;
         if constexpr (MODE == kPCount) {
             if (lane == 0) {
@@ -252,15 +367,15 @@ __global__ void __launch_bounds__(kProbeThreads) k_probe(const DevIndex ix, cons
         } else if constexpr (MODE == kPKnn) {
             if (found >= pa.k) {
                 if (lane < pa.k) {
-                    pa.ids[(uint64_t)qid * pa.k + lane] = bi;
-                    pa.dist2[(uint64_t)qid * pa.k + lane] = __longlong_as_double((long long)bs);
+                    pa.ids[(uint64_t)qid * pa.k + lane] = st.bi;
+                    pa.dist2[(uint64_t)qid * pa.k + lane] = __longlong_as_double((long long)st.bs);
                 }
             } else if (lane == 0) {
                 pa.unres[atomicAdd(pa.n_unres, 1u)] = qid;
             }
         }
     }
-    // per-lane counters: probes differ by lane, tests too; one atomic per warp and counter
+    // per-lane counters: one atomic per warp and counter
 #pragma unroll
     for (int s = 16; s; s >>= 1) {
         probes += __shfl_xor_sync(0xffffffffu, probes, s);
