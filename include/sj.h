@@ -299,13 +299,12 @@ sj_status sj_join_sets(const sj_index *idx, const double *queries, uint64_t nq, 
  * SuperEGO "using 32-bit floats"; R21): the self-join of float points with every coordinate
  * difference, square and sum a binary32 round-to-nearest operation, left to right, no FMA:
  *     (i,k) in S32  <=>  (((p_i0-p_k0)^2 + (p_i1-p_k1)^2) + ...) <= fl32(eps*eps)   (all in float).
- * Pairs / ids / result as sj_self_join (both orientations; (p,p) unless include_self == 0).  The grid
- * index is built from the points widened exactly to binary64 for radius eps * (1 + 2^-16), so every
- * pair the float predicate accepts lies in adjacent cells; each point then probes its full 3^d
- * neighbourhood (no unicomp), count pass then fill pass (exact batch sizes, no overflow re-runs).
+ * Pairs / ids / result and every join option as sj_self_join (unicomp holds: the float distance is
+ * symmetric).  The grid index is built from the points widened exactly to binary64 for radius
+ * eps * (1 + 2^-16), so every pair the float predicate accepts lies in adjacent cells; the self-join's
+ * path then runs with the predicate in binary32 (estimate, batches, sparse / dense refine, drains).
  *   points : row-major n x d float32, host or device per bopts->points_on_device.   eps: float > 0,
- *            fl32(eps*eps) normal.   jopts: include_self, batch_capacity_pairs, min_batches,
- *            result_on_host, sort_pairs are used; drain_csr must be 0.
+ *            fl32(eps*eps) normal.   jopts: NULL = defaults.
  * Errors: as sj_build_index / sj_self_join. */
 sj_status sj_self_join_f32(const float *points, uint64_t n, int d, float eps, const sj_build_opts *bopts,
                            const sj_join_opts *jopts, sj_result **out);

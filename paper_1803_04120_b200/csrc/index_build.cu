@@ -59,7 +59,15 @@ __device__ __forceinline__ double ord_to_double(unsigned long long k)
     return __longlong_as_double((long long)u);
 }
 
+// SJ_DEBUG_SYNC=1: synchronise and check after the build's phases (fault localisation)
+static bool debug_sync()
+{
+    static const bool on = [] { const char *e = std::getenv("SJ_DEBUG_SYNC"); return e && *e && *e != '0'; }();
+    return on;
+}
+
 // directory size cap: P_k <= max(mult * N, 2^16) entries (SJ_DIR_CAP overrides mult)
+
 static uint32_t dir_cap_mult()
 {
     static const uint32_t m = [] {
@@ -208,7 +216,9 @@ k_minmax_geom(const double *__restrict__ pts, uint32_t n, unsigned long long *__
               DevGeom *__restrict__ g, uint32_t *__restrict__ zero_words, uint32_t nzero, DevGeom *hgeom,
               volatile uint32_t *hbell, uint32_t epoch)
 {
+#ifndef SJ_PDL_TRIGGER_END
     pdl_trigger();                   // the key pass may launch now (it loads its rows, then waits)
+#endif
     const uint64_t total = (uint64_t)n * D;
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
@@ -278,6 +288,9 @@ k_minmax_geom(const double *__restrict__ pts, uint32_t n, unsigned long long *__
         out[D + j] = ord_key(b);
     }
     if (threadIdx.x == 0) out[2 * D] = any_bad ? 1ull : 0ull;
+#ifdef SJ_PDL_TRIGGER_END
+    pdl_trigger();
+#endif
     // last CTA: geometry from all partials
     __shared__ bool s_last;
     __threadfence();
@@ -360,7 +373,7 @@ __device__ __forceinline__ double cell_floor(double t, double w, double inv_w)
 // the sort needs no histogram pass of its own.  Geometry from the device (k_geometry).
 template <int D>
 __global__ void __launch_bounds__(kThreads)
-k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g, uint64_t *__restrict__ keys,
+k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *g, uint64_t *__restrict__ keys,
        uint32_t *__restrict__ ids, uint32_t *__restrict__ masks, uint32_t *__restrict__ bhist)
 {
     __shared__ uint32_t s_mask[kSmemMaskWords];
@@ -390,20 +403,38 @@ k_keys(const double *__restrict__ pts, uint32_t n, const DevGeom *__restrict__ g
             for (int j = 0; j < D; ++j) xr[j] = pts[i * D + j];
         }
     }
+    // The geometry is written by the primary grid (k_minmax_geom's last CTA): read it only after the
+    // wait, through L2 (__ldcg).  (With g declared const __restrict__ the compiler hoisted the status
+    // load above griddepcontrol.wait as a read-only .CONSTANT load: a small build whose key pass
+    // launched early read the previous build's status -- e.g. a failed build's -- and skipped its keys.)
     pdl_wait();
-    if (g->status) return;
-    const bool use_masks = g->masks_on != 0;
-    const bool use_hist = g->use_bucket != 0;
-    const int dir_k = g->k;
-    const double inv_w = 1.0 / g->w;
-    const double w = g->w;
-    const uint32_t mask_words = (uint32_t)((g->mask_off[D] + 31) / 32);
-    if (threadIdx.x < D) {
-        s_min[threadIdx.x] = g->mins[threadIdx.x];
-        s_str[threadIdx.x] = g->strides[threadIdx.x];
-        s_pstr[threadIdx.x] = g->pstride[threadIdx.x];
-        s_moff[threadIdx.x] = g->mask_off[threadIdx.x];
+    // one coherent read per CTA (into shared memory): the same few words read through L2 by every
+    // thread of every CTA cost the key pass ~40 us of L2 hot-spot serialisation
+    __shared__ int s_status, s_masks_on, s_use_bucket, s_k;
+    __shared__ double s_w;
+    __shared__ uint64_t s_moffD;
+    if (threadIdx.x == 0) {
+        s_status = __ldcg(&g->status);
+        s_masks_on = __ldcg(&g->masks_on);
+        s_use_bucket = __ldcg(&g->use_bucket);
+        s_k = __ldcg(&g->k);
+        s_w = __ldcg(&g->w);
+        s_moffD = __ldcg(&g->mask_off[D]);
     }
+    if (threadIdx.x < D) {
+        s_min[threadIdx.x] = __ldcg(&g->mins[threadIdx.x]);
+        s_str[threadIdx.x] = __ldcg(&g->strides[threadIdx.x]);
+        s_pstr[threadIdx.x] = __ldcg(&g->pstride[threadIdx.x]);
+        s_moff[threadIdx.x] = __ldcg(&g->mask_off[threadIdx.x]);
+    }
+    __syncthreads();
+    if (s_status) return;
+    const bool use_masks = s_masks_on != 0;
+    const bool use_hist = s_use_bucket != 0;
+    const int dir_k = s_k;
+    const double w = s_w;
+    const double inv_w = 1.0 / w;
+    const uint32_t mask_words = (uint32_t)((s_moffD + 31) / 32);
     if (use_masks)
         for (uint32_t w2 = threadIdx.x; w2 < mask_words; w2 += blockDim.x) s_mask[w2] = 0;
     __syncthreads();
@@ -1189,6 +1220,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ev.rec(3, s);
         SJ_CUDA(cudaEventRecord(cg.c->events[2], s));          // keys (and the small masks) done
         tr.dev("keys", s);
+        if (debug_sync()) { SJ_CUDA(cudaStreamSynchronize(s)); std::fprintf(stderr, "[sj-debug] keys ok\n"); }
         tr.mark("minmax/geometry/keys enqueued");
         {
             // poll the doorbell (the stream is queried now and then, so a failed launch is reported
@@ -1348,12 +1380,15 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
             if (in_tmp) SJ_CUDA(cudaMemcpyAsync(A, ids_tmp, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
             ev.rec(4, s);
             tr.mark("sort enqueued");
+            if (debug_sync()) { SJ_CUDA(cudaStreamSynchronize(s)); std::fprintf(stderr, "[sj-debug] sort ok\n"); }
             // ---- a4: cell numbering (heads + scan), compaction, SoA gather, directory histogram,
             // occupancy bits.  B and G are sized for the upper bound N cells so no host round trip is
             // needed here; |G| is read back by the single sync of finish_aux.
             k_heads<<<grid, kThreads, 0, s>>>(skeys, N, flags);
             SJ_LAUNCHED();
+            if (debug_sync()) { SJ_CUDA(cudaStreamSynchronize(s)); std::fprintf(stderr, "[sj-debug] heads ok\n"); }
             inclusive_scan_u32(flags, pcell, n, s);
+            if (debug_sync()) { SJ_CUDA(cudaStreamSynchronize(s)); std::fprintf(stderr, "[sj-debug] scan ok\n"); }
             SJ_CUDA(cudaMemcpyAsync(aux, pcell + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
             dirhist.p = dalloc<uint32_t>((size_t)dp.P + 1, s);
             dirhist.s = s;
@@ -1379,6 +1414,7 @@ sj_index *build_index_impl2(const double *points, uint64_t n, int d, double eps,
         ix.cmask = cmask;
         ev.rec(5, s);
         tr.mark("compaction enqueued");
+        if (debug_sync()) { SJ_CUDA(cudaStreamSynchronize(s)); std::fprintf(stderr, "[sj-debug] compaction ok\n"); }
 
         v.n_cells = n;            // provisional upper bound until finish_aux() reads |G|
         v.B = B;

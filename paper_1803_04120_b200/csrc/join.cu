@@ -31,11 +31,11 @@ void launch_dense(const DevIndex &ix, const JoinArgs &ja, bool unicomp, cudaStre
         std::min<uint64_t>(ix.n_dense_tasks, (uint64_t)(ja.q1 - ja.q0 + ix.dense_T - 1) / ix.dense_T + 4);
     const dim3 grid((uint32_t)((max_tasks + kDenseWarps - 1) / kDenseWarps));
     switch (ix.d) {
-    case 2: launch_dense_d<2>(ix, ja, unicomp, grid, s); break;
-    case 3: launch_dense_d<3>(ix, ja, unicomp, grid, s); break;
-    case 4: launch_dense_d<4>(ix, ja, unicomp, grid, s); break;
-    case 5: launch_dense_d<5>(ix, ja, unicomp, grid, s); break;
-    case 6: launch_dense_d<6>(ix, ja, unicomp, grid, s); break;
+    case 2: launch_dense_d<2>(ix, ja, unicomp, ix.f32 != 0, grid, s); break;
+    case 3: launch_dense_d<3>(ix, ja, unicomp, ix.f32 != 0, grid, s); break;
+    case 4: launch_dense_d<4>(ix, ja, unicomp, ix.f32 != 0, grid, s); break;
+    case 5: launch_dense_d<5>(ix, ja, unicomp, ix.f32 != 0, grid, s); break;
+    case 6: launch_dense_d<6>(ix, ja, unicomp, ix.f32 != 0, grid, s); break;
     default: fail(SJ_ERR_DIM, "bad d");
     }
     SJ_LAUNCHED();
@@ -53,12 +53,13 @@ void launch_refine(const DevIndex &ix, const JoinArgs &ja, bool unicomp, uint32_
     const uint32_t nthreads = (uint32_t)nthreads64;
     const dim3 grid((nthreads + kRefineThreads - 1) / kRefineThreads);
     const bool occ6 = MODE == kEmit && ix.search_mode == kSearchCellScan && !ix.occ && ix.dir_ntop >= 81;
+    const int mode = MODE | (ix.f32 ? kF32 : 0);      // the FP32 join's index: binary32 predicate (R21)
     switch (ix.d) {
-    case 2: launch_refine_d<2>(MODE, ix, ja, unicomp, occ6, queued, grid, s); break;
-    case 3: launch_refine_d<3>(MODE, ix, ja, unicomp, occ6, queued, grid, s); break;
-    case 4: launch_refine_d<4>(MODE, ix, ja, unicomp, occ6, queued, grid, s); break;
-    case 5: launch_refine_d<5>(MODE, ix, ja, unicomp, occ6, queued, grid, s); break;
-    case 6: launch_refine_d<6>(MODE, ix, ja, unicomp, occ6, queued, grid, s); break;
+    case 2: launch_refine_d<2>(mode, ix, ja, unicomp, occ6, queued, grid, s); break;
+    case 3: launch_refine_d<3>(mode, ix, ja, unicomp, occ6, queued, grid, s); break;
+    case 4: launch_refine_d<4>(mode, ix, ja, unicomp, occ6, queued, grid, s); break;
+    case 5: launch_refine_d<5>(mode, ix, ja, unicomp, occ6, queued, grid, s); break;
+    case 6: launch_refine_d<6>(mode, ix, ja, unicomp, occ6, queued, grid, s); break;
     default: fail(SJ_ERR_DIM, "bad d");
     }
     SJ_LAUNCHED();

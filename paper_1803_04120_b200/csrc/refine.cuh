@@ -36,6 +36,10 @@
 namespace sj {
 
 enum RefineMode { kEmit = 0, kCountQuery = 1, kCountPoint = 2 };
+// mode flag: the predicate in binary32 (FP32 self-join, R21: coordinates are floats widened
+// exactly, s32 = (((x0-y0)^2 + (x1-y1)^2) + ...) in float with __fsub_rn/__fmul_rn/__fadd_rn, <= eps2f)
+constexpr int kModeMask = 3;
+constexpr int kF32 = 8;
 
 struct JoinArgs {
     uint64_t *out;                 // kEmit: batch pair buffer
@@ -120,10 +124,10 @@ struct QueryState {
 template <int MODE, bool BOTH>
 __device__ __forceinline__ void emit(const JoinArgs &ja, bool hit, uint32_t pid, uint32_t qid, uint32_t &emitted)
 {
-    if constexpr (MODE == kCountQuery) {
+    if constexpr ((MODE & kModeMask) == kCountQuery) {
         if (hit) emitted += BOTH ? 2u : 1u;
         return;
-    } else if constexpr (MODE == kCountPoint) {
+    } else if constexpr ((MODE & kModeMask) == kCountPoint) {
         if (hit) {
             emitted += BOTH ? 2u : 1u;
             atomicAdd(ja.pcount + pid, 1u);
@@ -158,7 +162,7 @@ __device__ __forceinline__ void emit(const JoinArgs &ja, bool hit, uint32_t pid,
 template <int MODE>
 __device__ __forceinline__ void emit_self(const JoinArgs &ja, uint32_t k, uint32_t pid, uint32_t &emitted)
 {
-    if constexpr (MODE == kEmit) {
+    if constexpr ((MODE & kModeMask) == kEmit) {
         const uint64_t pos = (uint64_t)(k - ja.q0);
         if (pos < ja.cap) ja.out[pos] = ((uint64_t)pid << 32) | pid;
         else atomicOr(ja.overflow, 1u);
@@ -348,6 +352,27 @@ __device__ __forceinline__ void scan_range(const DevIndex &ix, const JoinArgs &j
             const uint32_t npair = (lim + 1u) >> 1;         // warp-uniform
             // fully unrolled (constant bit positions: the hit bit is one predicated OR); the
             // ragged last tile of a range leaves early by a uniform branch
+            if constexpr ((MODE & kF32) != 0) {
+#pragma unroll
+                for (uint32_t e2 = 0; e2 < 16u; ++e2) {
+                    if (e2 >= npair) break;
+                    double2 c = t2[e2];
+                    float ta = __fsub_rn((float)q.x[0], (float)c.x), tb = __fsub_rn((float)q.x[0], (float)c.y);
+                    float sa = __fmul_rn(ta, ta), sb = __fmul_rn(tb, tb);
+#pragma unroll
+                    for (int j = 1; j < D; ++j) {
+                        c = t2[j * 16 + e2];
+                        ta = __fsub_rn((float)q.x[j], (float)c.x);
+                        tb = __fsub_rn((float)q.x[j], (float)c.y);
+                        sa = __fadd_rn(sa, __fmul_rn(ta, ta));
+                        sb = __fadd_rn(sb, __fmul_rn(tb, tb));
+                    }
+                    if (sa <= ix.eps2f) hm |= 1u << (2u * e2);
+                    if (sb <= ix.eps2f) hm |= 2u << (2u * e2);
+                }
+                emit_tile<BOTH>(ja, *wb, hm & vm, q.pid, q.emitted);
+                continue;
+            }
 #pragma unroll
             for (uint32_t e2 = 0; e2 < 16u; ++e2) {
                 if (e2 >= npair) break;
@@ -370,20 +395,35 @@ __device__ __forceinline__ void scan_range(const DevIndex &ix, const JoinArgs &j
         return;
     }
     for (uint32_t m = m0; m < m1; m += stride) {
-        double s;
-        {
-            const double t = __dsub_rn(q.x[0], __ldg(ix.X + m));
-            s = __dmul_rn(t, t);
-        }
+        bool hit;
+        if constexpr ((MODE & kF32) != 0) {
+            float s;
+            {
+                const float t = __fsub_rn((float)q.x[0], (float)__ldg(ix.X + m));
+                s = __fmul_rn(t, t);
+            }
 #pragma unroll
-        for (int j = 1; j < D; ++j) {
-            const double t = __dsub_rn(q.x[j], __ldg(ix.X + (uint64_t)j * n + m));
-            s = __dadd_rn(s, __dmul_rn(t, t));
+            for (int j = 1; j < D; ++j) {
+                const float t = __fsub_rn((float)q.x[j], (float)__ldg(ix.X + (uint64_t)j * n + m));
+                s = __fadd_rn(s, __fmul_rn(t, t));
+            }
+            hit = s <= ix.eps2f;
+        } else {
+            double s;
+            {
+                const double t = __dsub_rn(q.x[0], __ldg(ix.X + m));
+                s = __dmul_rn(t, t);
+            }
+#pragma unroll
+            for (int j = 1; j < D; ++j) {
+                const double t = __dsub_rn(q.x[j], __ldg(ix.X + (uint64_t)j * n + m));
+                s = __dadd_rn(s, __dmul_rn(t, t));
+            }
+            hit = s <= ix.eps2;
         }
         ++q.tests;
-        const bool hit = s <= ix.eps2;
         uint32_t qid = 0;
-        if (MODE != kCountQuery && hit) qid = __ldg(ix.A + m);
+        if ((MODE & kModeMask) != kCountQuery && hit) qid = __ldg(ix.A + m);
         emit<MODE, BOTH>(ja, hit, q.pid, qid, q.emitted);
     }
 }
@@ -868,7 +908,7 @@ __device__ __forceinline__ void flush_work(const JoinArgs &ja, unsigned long lon
 // candidate loop are warp-uniform: candidates are broadcast loads, hits go through the per-warp
 // shared-memory buffer (one cursor atomic per flush instead of one per candidate step).
 constexpr int kDenseWarps = 8;
-template <int D, bool UNICOMP>
+template <int D, bool UNICOMP, bool F32 = false>
 #ifndef SJ_DENSE_MINB
 #define SJ_DENSE_MINB 3
 #endif
@@ -930,7 +970,7 @@ k_refine_dense(const DevIndex ix, const JoinArgs ja)
             // that load and broadcast candidates but never emit (they take the first query's point)
             const uint32_t k = a + lane;
             q.valid = k < b;
-            refine_query<D, kEmit, UNICOMP, true>(ix, ja, q.valid ? k : a, h, __ldg(ix.G + h), __ldg(ix.G + h + 1),
+            refine_query<D, F32 ? (kEmit | kF32) : kEmit, UNICOMP, true>(ix, ja, q.valid ? k : a, h, __ldg(ix.G + h), __ldg(ix.G + h + 1),
                                                   0xffffffffu, q, tt, &wb);
         }
     }
@@ -959,7 +999,7 @@ k_refine(const DevIndex ix, const JoinArgs ja)
     q.emitted = q.probes = q.tests = 0;
     uint32_t k;
     bool active;
-    if constexpr (MODE == kCountQuery) {
+    if constexpr ((MODE & kModeMask) == kCountQuery) {
         // sample qi: lane qi%32 of run qi/32; run r = the first 32 queries of block [r*32*step, ...)
         k = ja.q0 + (qi >> 5) * (32u * ja.step) + (qi & 31u);
         active = qi < ja.nsamples && k < ja.q1;
@@ -973,11 +1013,11 @@ k_refine(const DevIndex ix, const JoinArgs ja)
         cs = __ldg(ix.G + h);
         ce = __ldg(ix.G + h + 1);
         // queries of populous cells are handled by the warp-per-task dense kernel
-        if (MODE == kEmit && ja.dense_T && ce - cs >= ja.dense_T) active = false;
+        if ((MODE & kModeMask) == kEmit && ja.dense_T && ce - cs >= ja.dense_T) active = false;
     }
     const unsigned wmask = __ballot_sync(0xffffffffu, active);   // before any divergence
     if (active) refine_query<D, MODE, UNICOMP>(ix, ja, k, h, cs, ce, wmask, q, tt);
-    if constexpr (MODE == kCountQuery) {
+    if constexpr ((MODE & kModeMask) == kCountQuery) {
         // sum the group's partial counts (all lanes of a group share `active`)
         uint32_t e = q.emitted;
         for (uint32_t o = 1; o < q.G; o <<= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
@@ -1080,22 +1120,36 @@ __device__ __forceinline__ void q_drain(const DevIndex &ix, const JoinArgs &ja, 
             if (valid) {
                 const uint32_t m = st + (t - ex);
                 const double *qx = w.qx + ql * D;
-                double s;
-                {
-                    const double d0 = __dsub_rn(qx[0], __ldg(ix.X + m));
-                    s = __dmul_rn(d0, d0);
-                }
+                if constexpr ((MODE & kF32) != 0) {
+                    float s;
+                    {
+                        const float d0 = __fsub_rn((float)qx[0], (float)__ldg(ix.X + m));
+                        s = __fmul_rn(d0, d0);
+                    }
 #pragma unroll
-                for (int j = 1; j < D; ++j) {
-                    const double dj = __dsub_rn(qx[j], __ldg(ix.X + (uint64_t)j * n + m));
-                    s = __dadd_rn(s, __dmul_rn(dj, dj));
+                    for (int j = 1; j < D; ++j) {
+                        const float dj = __fsub_rn((float)qx[j], (float)__ldg(ix.X + (uint64_t)j * n + m));
+                        s = __fadd_rn(s, __fmul_rn(dj, dj));
+                    }
+                    hit = s <= ix.eps2f;
+                } else {
+                    double s;
+                    {
+                        const double d0 = __dsub_rn(qx[0], __ldg(ix.X + m));
+                        s = __dmul_rn(d0, d0);
+                    }
+#pragma unroll
+                    for (int j = 1; j < D; ++j) {
+                        const double dj = __dsub_rn(qx[j], __ldg(ix.X + (uint64_t)j * n + m));
+                        s = __dadd_rn(s, __dmul_rn(dj, dj));
+                    }
+                    hit = s <= ix.eps2;
                 }
                 ++tests;
-                hit = s <= ix.eps2;
-                if (MODE != kCountQuery && hit) cid = __ldg(ix.A + m);
+                if ((MODE & kModeMask) != kCountQuery && hit) cid = __ldg(ix.A + m);
             }
             const uint32_t pid = w.qid[ql];
-            if constexpr (MODE == kCountQuery) {
+            if constexpr ((MODE & kModeMask) == kCountQuery) {
                 if (hit) atomicAdd(w.qem + ql, BOTH ? 2u : 1u);
             } else {
                 uint32_t dummy = 0;
@@ -1219,7 +1273,7 @@ k_refine_q(const DevIndex ix, const JoinArgs ja)
     q.emitted = q.probes = q.tests = 0;
     uint32_t k;
     bool active;
-    if constexpr (MODE == kCountQuery) {
+    if constexpr ((MODE & kModeMask) == kCountQuery) {
         k = ja.q0 + (qi >> 5) * (32u * ja.step) + (qi & 31u);
         active = qi < ja.nsamples && k < ja.q1;
     } else {
@@ -1231,7 +1285,7 @@ k_refine_q(const DevIndex ix, const JoinArgs ja)
         h = __ldg(ix.pcell + k);
         cs = __ldg(ix.G + h);
         ce = __ldg(ix.G + h + 1);
-        if (MODE == kEmit && ja.dense_T && ce - cs >= ja.dense_T) active = false;
+        if ((MODE & kModeMask) == kEmit && ja.dense_T && ce - cs >= ja.dense_T) active = false;
     }
     uint64_t key = 0;
     uint32_t bad = 0xFFFFFFFFu;
@@ -1267,7 +1321,7 @@ k_refine_q(const DevIndex ix, const JoinArgs ja)
     }
     if (active) bad = bad_moves<D, UNICOMP>(ix, ja, q, h);
     search_cell_scan_q<D, MODE, UNICOMP>(ix, ja, q, active, h, key, bad, tt, w);
-    if constexpr (MODE == kCountQuery) {
+    if constexpr ((MODE & kModeMask) == kCountQuery) {
         __syncwarp();
         q.emitted += w.qem[lane];                    // hits of the ranges this lane queued
         uint32_t e = q.emitted;

@@ -7,45 +7,14 @@ template <>
 void launch_refine_d<5>(int mode, const DevIndex &ix, const JoinArgs &ja, bool unicomp, bool occ6, bool queued,
                         dim3 grid, cudaStream_t s)
 {
-    const dim3 block(kRefineThreads);
-#define SJ_MODE_CASE(M)                                                                          \
-    case M:                                                                                      \
-        if (queued) {                                                                            \
-            if (unicomp) k_refine_q<5, M, true><<<grid, block, 0, s>>>(ix, ja);                  \
-            else k_refine_q<5, M, false><<<grid, block, 0, s>>>(ix, ja);                         \
-            break;                                                                               \
-        }                                                                                        \
-        if constexpr (M == kEmit) {                                                              \
-            if (occ6) {                                                                          \
-                if (unicomp) k_refine<5, M, true, 6><<<grid, block, 0, s>>>(ix, ja);             \
-                else k_refine<5, M, false, 6><<<grid, block, 0, s>>>(ix, ja);                    \
-                break;                                                                           \
-            }                                                                                    \
-        }                                                                                        \
-        if (unicomp) k_refine<5, M, true><<<grid, block, 0, s>>>(ix, ja);                        \
-        else k_refine<5, M, false><<<grid, block, 0, s>>>(ix, ja);                               \
-        break;
-    switch (mode) {
-        SJ_MODE_CASE(kEmit)
-        SJ_MODE_CASE(kCountQuery)
-        SJ_MODE_CASE(kCountPoint)
-    default: fail(SJ_ERR_ARG, "bad refine mode");
-    }
-#undef SJ_MODE_CASE
+    launch_refine_body<5>(mode, ix, ja, unicomp, occ6, queued, grid, s);
 }
 
 template <>
-void launch_dense_d<5>(const DevIndex &ix, const JoinArgs &ja, bool unicomp, dim3 grid, cudaStream_t s)
+void launch_dense_d<5>(const DevIndex &ix, const JoinArgs &ja, bool unicomp, bool f32, dim3 grid, cudaStream_t s)
 {
-    const dim3 block(32 * kDenseWarps);
-    const size_t smem = kDenseWarps * dense_smem_per_warp<5>() + (ix.search_mode == kSearchCellScan ? sizeof(TopTable) : 0);
-    if (unicomp) {
-        set_max_dyn_smem(reinterpret_cast<const void *>(k_refine_dense<5, true>), (int)smem);
-        k_refine_dense<5, true><<<grid, block, smem, s>>>(ix, ja);
-    } else {
-        set_max_dyn_smem(reinterpret_cast<const void *>(k_refine_dense<5, false>), (int)smem);
-        k_refine_dense<5, false><<<grid, block, smem, s>>>(ix, ja);
-    }
+    if (f32) launch_dense_body<5, true>(ix, ja, unicomp, grid, s);
+    else launch_dense_body<5, false>(ix, ja, unicomp, grid, s);
 }
 
 }  // namespace sj

@@ -161,6 +161,10 @@ struct DevIndex {
     const uint32_t *dense_tasks;
     uint32_t n_dense_tasks;
     uint32_t dense_T;
+    // FP32 self-join (R21; sj_self_join_f32 sets these on its private index): the refine
+    // evaluates the predicate in binary32, s32 <= eps2f, instead of R1's binary64 s <= eps2
+    int f32;
+    float eps2f;
 };
 
 enum SearchMode { kSearchDenseRows = 0, kSearchCellScan = 1, kSearchRows = 2 };

@@ -19,6 +19,7 @@
 //      each lane finding its candidate's cell by a 5-step shuffle search -- the warp stays converged and
 //      every lane tests a candidate even when the cells hold one point each (sparse 6-D);
 //   4. the predicate is the self-join's (R1: __dsub_rn/__dmul_rn/__dadd_rn left to right, <= fl(eps^2));
+//      (the FP32 self-join, R21, is the self-join's own path with a binary32 predicate: refine.cuh kF32)
 //   5. count: hits per query; fill: warp-aggregated emission (one atomic per 32 candidates);
 //      kNN: a warp-wide sorted top-k list (lane i holds the i-th best (s, id)), each surviving candidate
 //      inserted by one ballot + one shuffle-up.
@@ -41,9 +42,7 @@ struct ProbeArgs {
     const uint32_t *qlist;        // optional: query rows to process (kNN re-runs: original ids)
     uint32_t q_begin, nq;         // queries q_begin .. q_begin+nq-1 (rows, or qlist entries)
     int q_index;                  // 1: the queries are the index's own points in A-order (X, A)
-    int self;                     // skip the candidate whose id is the query's (kNN; include_self = 0)
-    int f32;                      // predicate in binary32 (FP32 self-join, R21): s32 <= eps2f
-    float eps2f;
+    int self;                     // skip the candidate whose id is the query's (kNN)
     uint32_t *counts;             // count: per query (index t - q_begin)
     unsigned long long *buckets;  // count: per 1024 queries
     uint32_t *nonfinite;          // count: set when a query coordinate is NaN / inf
@@ -119,21 +118,7 @@ __device__ __forceinline__ void sweep(const DevIndex &ix, const ProbeArgs &pa, c
         bool hit = false;
         double s = 0.0;
         uint32_t pid = 0;
-        if (act && pa.f32) {
-            // R21: coordinates are floats widened exactly; the distance in binary32, left to right
-            float s32;
-            {
-                const float d0 = __fsub_rn((float)x[0], (float)__ldg(ix.X + m));
-                s32 = __fmul_rn(d0, d0);
-            }
-#pragma unroll
-            for (int j = 1; j < D; ++j) {
-                const float dj = __fsub_rn((float)x[j], (float)__ldg(ix.X + (uint64_t)j * n + m));
-                s32 = __fadd_rn(s32, __fmul_rn(dj, dj));
-            }
-            ++st.tests;
-            hit = s32 <= pa.eps2f;
-        } else if (act) {
+        if (act) {
             {
                 const double d0 = __dsub_rn(x[0], __ldg(ix.X + m));
                 s = __dmul_rn(d0, d0);
@@ -593,8 +578,6 @@ sj_result *self_join_f32_impl(const float *points, uint64_t n, int d, float eps,
     volatile float e2v = eps * eps;              // fl32(eps*eps)
     const float eps2f = e2v;
     if (!std::isnormal(eps2f)) fail(SJ_ERR_ARG, "fl32(eps*eps) must be a normal float");
-    if (o.batch_capacity_pairs == 0) fail(SJ_ERR_ARG, "batch_capacity_pairs must be > 0");
-    if (o.drain_csr) fail(SJ_ERR_ARG, "drain_csr is not supported by the FP32 join");
     if (bo.device < 0 || bo.device >= device_count()) fail(SJ_ERR_ARG, "bad device ordinal");
     SJ_CUDA(cudaSetDevice(bo.device));
     CtxGuard cg{acquire_ctx(bo.device, 1, 2, 64)};
@@ -622,24 +605,15 @@ sj_result *self_join_f32_impl(const float *points, uint64_t n, int d, float eps,
     b2.stream = s;
     b2.speculative_estimate = 0;
     sj_index *idx = build_index_impl(wide.p, n, d, (double)eps * (1.0 + std::ldexp(1.0, -16)), b2);
-    sj_result *res = new sj_result();
-    res->device = bo.device;
-    res->n_points = n;
-    res->q0 = 0;
-    res->q1 = n;
-    res->include_self = o.include_self;
-    res->unicomp = 0;
+    // the self-join's whole path (estimate, plan, batches, unicomp -- the binary32 distance is symmetric
+    // too --, sparse / dense / queued refine kernels, host drain, CSR) with the predicate in binary32
+    idx->dev.f32 = 1;
+    idx->dev.eps2f = eps2f;
+    sj_result *res = nullptr;
     try {
-        ProbeArgs q{};
-        q.q_index = 1;
-        q.self = !o.include_self;
-        q.f32 = 1;
-        q.eps2f = eps2f;
-        probe_join(idx->dev, bo.device, q, n, o, s, res);
+        SJ_CUDA(cudaStreamSynchronize(s));      // the widened copy is read by the build only
+        res = self_join_impl(idx, o);
     } catch (...) {
-        cudaStreamSynchronize(s);
-        free_batches(res);
-        delete res;
         free_index_impl(idx);
         throw;
     }

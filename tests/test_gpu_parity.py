@@ -613,3 +613,23 @@ def test_cell_coordinates_at_cell_boundaries(sj):
         assert arr["B"].cpu().numpy().tolist() == ref.B
         assert np.array_equal(arr["A"].cpu().numpy().astype(np.int64), ref.A)
         assert np.array_equal(sj.self_join(idx).to_numpy(), oracle.grid_join(pts, eps))
+
+
+def test_build_after_failed_build(sj):
+    """Regression: the key pass launches programmatically behind the min/max pass and must read the
+    geometry only after griddepcontrol.wait.  A small 2-D build, a failed build (NaN -> SJ_ERR_NONFINITE,
+    overflow -> SJ_ERR_KEY_OVERFLOW) and then C1 once faulted in the compaction: the key pass had read
+    the failed build's status (a load the compiler hoisted above the wait) and skipped its keys."""
+    P = datagen.uniform(5000, 2, seed=3)
+    sj.build_index(torch.from_numpy(P).cuda(), 4.0).free()
+    bad = datagen.uniform(100, 3, seed=1)
+    bad[17, 2] = np.nan
+    with pytest.raises(sj.SJError):
+        sj.build_index(torch.from_numpy(bad).cuda(), 1.0)
+    pts = datagen.uniform_config("C1", 2)
+    got, _, _ = gpu_pairs(sj, pts, 2.5)
+    assert np.array_equal(got, oracle.grid_join(pts, 2.5))
+    with pytest.raises(sj.SJError):
+        sj.build_index(torch.from_numpy(datagen.uniform(100, 6, seed=2, hi=1e6)).cuda(), 1e-3)
+    got, _, _ = gpu_pairs(sj, pts, 2.5)
+    assert np.array_equal(got, oracle.grid_join(pts, 2.5))

@@ -13,6 +13,9 @@ import subprocess
 import pytest
 
 PREDICATE_KERNELS = re.compile(r"k_refine|k_refine_dense|k_brute_force")
+# FP32 self-join instantiations: k_refine*<D, kEmit|kF32 (8) or kCountQuery|kF32 (9), ...> and
+# k_refine_dense<D, UNICOMP, F32 = true>
+F32_INSTANCE = re.compile(r"k_refine(_q)?ILi\dELi(8|9)E|k_refine_denseILi\dELb[01]ELb1E")
 
 
 @pytest.fixture(scope="module")
@@ -43,7 +46,12 @@ def test_no_fma_in_predicate_kernels(sass):
             continue
         body = "\n".join(lines)
         assert not re.search(r"\bDFMA\b", body), f"DFMA in {name}"
-        assert re.search(r"\bDADD\b", body) and re.search(r"\bDMUL\b", body), name
+        if F32_INSTANCE.search(name):
+            # the FP32 join's instantiations (reading R21): binary32 FADD/FMUL, no fused FFMA
+            assert not re.search(r"\bFFMA\b", body), f"FFMA in {name}"
+            assert re.search(r"\bFADD\b", body) and re.search(r"\bFMUL\b", body), name
+        else:
+            assert re.search(r"\bDADD\b", body) and re.search(r"\bDMUL\b", body), name
         checked += 1
     # refine: 5 dims x (emit/count-query/count-point) x unicomp on/off (+ 6-CTA variants);
     # dense refine: 5 x 2; brute force: 5
