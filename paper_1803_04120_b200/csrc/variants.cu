@@ -43,6 +43,7 @@ struct ProbeArgs {
     uint32_t q_begin, nq;         // queries q_begin .. q_begin+nq-1 (rows, or qlist entries)
     int q_index;                  // 1: the queries are the index's own points in A-order (X, A)
     int self;                     // skip the candidate whose id is the query's (kNN)
+    int tiled;                    // count / fill through k_probe_tiled (qlist sorted by cell)
     uint32_t *counts;             // count: per query (index t - q_begin)
     unsigned long long *buckets;  // count: per 1024 queries
     uint32_t *nonfinite;          // count: set when a query coordinate is NaN / inf
@@ -180,20 +181,181 @@ __device__ __forceinline__ uint64_t pick(uint32_t sel, uint32_t rj, uint64_t c0)
     return c0 - 1u + (uint64_t)(__ffs(m) - 1);
 }
 
+// One query (warp-uniform qid and point): its neighbour cells, their candidates, the mode's epilogue.
+// t = the query's position in this launch (count: index of counts[]).
 template <int D, int MODE>
+__device__ __forceinline__ void probe_query(const DevIndex &ix, const ProbeArgs &pa, uint32_t t, uint32_t qid,
+                                            const double (&x)[D], uint32_t lane, unsigned long long &probes,
+                                            unsigned long long &tests, unsigned long long &hits_all)
+{
+    // cell-scan indexes (few cells per top-k prefix): enumerate the 3^k top prefixes and scan their
+    // cells, instead of one bounded binary search per neighbour cell (3^d of them)
+    const bool prefix_scan = ix.search_mode == kSearchCellScan && ix.dir_k < D;
+    const int L = D - ix.dir_k;
+    // ---- 1. per dimension: c_j (R7 against the index's geometry) and the valid neighbour set
+    uint64_t c0[D];
+    uint32_t sel[D];
+    uint32_t ncell = 1, ntop = 1;
+    bool finite = true;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        finite = finite && isfinite(x[j]);
+        const double tq = floor(__ddiv_rn(__dsub_rn(x[j], ix.mins[j]), ix.w));   // = c_j - 1
+        uint32_t m = 0;
+        c0[j] = 0;
+        if (tq >= -1.0 && tq <= (double)ix.cpd[j]) {       // some of tq .. tq+2 may be in [1, |g_j|-2]
+            const int64_t b = (int64_t)tq;
+#pragma unroll
+            for (int e = 0; e < 3; ++e) {
+                const int64_t cc = b + e;
+                bool ok = cc >= 1 && cc <= (int64_t)ix.cpd[j] - 2;
+                if (ok && ix.masks) {
+                    const uint64_t bit = ix.mask_off[j] + (uint64_t)cc;
+                    ok = (__ldg(ix.masks + (bit >> 5)) >> (bit & 31u)) & 1u;
+                }
+                if (ok) m |= 1u << e;
+            }
+            c0[j] = (uint64_t)(b + 1);                      // as unsigned: b >= -1
+        }
+        sel[j] = m;
+        ncell *= (uint32_t)__popc(m);
+        if (j >= L) ntop *= (uint32_t)__popc(m);
+    }
+    if (MODE == kPCount && !finite && lane == 0) atomicOr(pa.nonfinite, 1u);
+    ProbeState st{0u, ~0ull, 0xffffffffu, ~0ull, 0xffffffffu, 0ull};
+    if (ncell == 0u) {
+        // nothing adjacent exists
+    } else if (prefix_scan) {
+        // ---- 2a. top prefixes, 32 per round; the occupancy bitmap (dilated +-1 along dimension
+        //      L-1) drops prefixes with no cell near the query's c_{L-1}
+        uint64_t qh = 0, qh2 = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            if (j < L) { qh += c0[j] * ix.occ_mul[j]; qh2 += c0[j] * ix.occ2_mul[j]; }
+        for (uint32_t base = 0; base < ntop; base += 32u) {
+            uint32_t clo = 0, chi = 0;
+            const uint32_t o = base + lane;
+            if (o < ntop) {
+                uint32_t r = o;
+                uint64_t p = 0, ob = qh, ob2 = qh2;
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    if (j < L) continue;
+                    const uint32_t nj = (uint32_t)__popc(sel[j]);
+                    const uint32_t rj = r % nj;
+                    r /= nj;
+                    const uint64_t cj = pick(sel[j], rj, c0[j]);
+                    p += cj * ix.pstride[j];
+                    ob += cj * ix.occ_mul[j];
+                    ob2 += cj * ix.occ2_mul[j];
+                }
+                bool live = true;
+                if (ix.occ) {
+                    live = (__ldg(ix.occ + (ob >> 5)) >> (ob & 31u)) & 1u;
+                    if (live && ix.occ2) live = (__ldg(ix.occ2 + (ob2 >> 5)) >> (ob2 & 31u)) & 1u;
+                }
+                ++probes;
+                if (live) {
+                    clo = __ldg(ix.dir + p);
+                    chi = __ldg(ix.dir + p + 1);
+                }
+            }
+            // ---- 2b. the prefixes' cells, 32 per step: keep those whose low coordinates are
+            //      adjacent (and valid) -> their point ranges
+            const uint32_t clen = chi - clo;
+            const uint32_t cinc = warp_inclusive(clen, lane);
+            const uint32_t ctotal = __shfl_sync(0xffffffffu, cinc, 31);
+            const uint32_t cexc = cinc - clen;
+            for (uint32_t g0 = 0; g0 < ctotal; g0 += 32u) {
+                const uint32_t g = g0 + lane;
+                const uint32_t own = owner_of(cinc, g);
+                const uint32_t olo = __shfl_sync(0xffffffffu, clo, own);
+                const uint32_t oexc = __shfl_sync(0xffffffffu, cexc, own);
+                uint32_t lo = 0, hi = 0;
+                if (g < ctotal) {
+                    const uint32_t h = olo + (g - oexc);
+                    uint64_t c[D];
+                    key_to_coords<D>(ix, __ldg(ix.B + h), c);
+                    bool ok = true;
+#pragma unroll
+                    for (int j = 0; j < D; ++j) {
+                        if (j >= L) continue;
+                        const uint64_t e = c[j] - (c0[j] - 1u);    // 0..2 when adjacent
+                        ok = ok && e < 3u && ((sel[j] >> e) & 1u);
+                    }
+                    if (ok) {
+                        lo = __ldg(ix.G + h);
+                        hi = __ldg(ix.G + h + 1);
+                    }
+                }
+                sweep<D, MODE>(ix, pa, x, qid, lo, hi, lane, st);
+            }
+        }
+    } else {
+        // ---- 2. 32 neighbour cells per round, each looked up by one lane: linear id (R8), prefix
+        //      p = sum c_j * pstride_j, one binary search of B bounded to [dir[p], dir[p+1])
+        for (uint32_t base = 0; base < ncell; base += 32u) {
+            uint32_t lo = 0, hi = 0;
+            const uint32_t o = base + lane;
+            if (o < ncell) {
+                uint32_t r = o;
+                uint64_t key = 0, p = 0;
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    const uint32_t nj = (uint32_t)__popc(sel[j]);
+                    const uint32_t rj = r % nj;
+                    r /= nj;
+                    const uint64_t cj = pick(sel[j], rj, c0[j]);
+                    key += cj * ix.strides[j];
+                    p += cj * ix.pstride[j];
+                }
+                ++probes;
+                uint32_t h = __ldg(ix.dir + p);
+                uint32_t h1 = __ldg(ix.dir + p + 1);
+                while (h < h1) {
+                    const uint32_t mid = (h + h1) >> 1;
+                    if (__ldg(ix.B + mid) < key) h = mid + 1;
+                    else h1 = mid;
+                }
+                if (h < ix.nG && __ldg(ix.B + h) == key) {
+                    lo = __ldg(ix.G + h);
+                    hi = __ldg(ix.G + h + 1);
+                }
+            }
+            // ---- 3. the cells' points, swept by the whole warp
+            sweep<D, MODE>(ix, pa, x, qid, lo, hi, lane, st);
+        }
+    }
+    tests += st.tests;
+    const uint32_t found = st.found;
+    hits_all += found;
+    if constexpr (MODE == kPCount) {
+        if (lane == 0) {
+            pa.counts[t] = found;
+            atomicAdd(pa.buckets + (t >> 10), (unsigned long long)found);
+        }
+    } else if constexpr (MODE == kPKnn) {
+        if (found >= pa.k) {
+            if (lane < pa.k) {
+                pa.ids[(uint64_t)qid * pa.k + lane] = st.bi;
+                pa.dist2[(uint64_t)qid * pa.k + lane] = __longlong_as_double((long long)st.bs);
+            }
+        } else if (lane == 0) {
+            pa.unres[atomicAdd(pa.n_unres, 1u)] = qid;
+        }
+    }
+}
+
 #ifndef SJ_PROBE_MINB
 #define SJ_PROBE_MINB 4   // 4 x 256 threads per SM (<= 64 registers): 6-D eps=8 two-set 82 -> 68 ms, kNN 6-D 74 -> 68 ms (2: slower)
 #endif
+template <int D, int MODE>
 __global__ void __launch_bounds__(kProbeThreads, SJ_PROBE_MINB) k_probe(const DevIndex ix, const ProbeArgs pa)
 {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t n = ix.n;
     unsigned long long probes = 0, tests = 0, hits_all = 0;
-    // cell-scan indexes (few cells per top-k prefix): enumerate the 3^k top prefixes and scan their
-    // cells, instead of one bounded binary search per neighbour cell (3^d of them)
-    const bool prefix_scan = ix.search_mode == kSearchCellScan && ix.dir_k < D;
-    const int L = D - ix.dir_k;
     for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < pa.nq; t += warps) {
         const uint32_t row = pa.q_begin + t;
         uint32_t qid;
@@ -207,158 +369,7 @@ __global__ void __launch_bounds__(kProbeThreads, SJ_PROBE_MINB) k_probe(const De
 #pragma unroll
             for (int j = 0; j < D; ++j) x[j] = __ldg(pa.q + (uint64_t)qid * D + j);
         }
-        // ---- 1. per dimension: c_j (R7 against the index's geometry) and the valid neighbour set
-        uint64_t c0[D];
-        uint32_t sel[D];
-        uint32_t ncell = 1, ntop = 1;
-        bool finite = true;
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            finite = finite && isfinite(x[j]);
-            const double tq = floor(__ddiv_rn(__dsub_rn(x[j], ix.mins[j]), ix.w));   // = c_j - 1
-            uint32_t m = 0;
-            c0[j] = 0;
-            if (tq >= -1.0 && tq <= (double)ix.cpd[j]) {       // some of tq .. tq+2 may be in [1, |g_j|-2]
-                const int64_t b = (int64_t)tq;
-#pragma unroll
-                for (int e = 0; e < 3; ++e) {
-                    const int64_t cc = b + e;
-                    bool ok = cc >= 1 && cc <= (int64_t)ix.cpd[j] - 2;
-                    if (ok && ix.masks) {
-                        const uint64_t bit = ix.mask_off[j] + (uint64_t)cc;
-                        ok = (__ldg(ix.masks + (bit >> 5)) >> (bit & 31u)) & 1u;
-                    }
-                    if (ok) m |= 1u << e;
-                }
-                c0[j] = (uint64_t)(b + 1);                      // as unsigned: b >= -1
-            }
-            sel[j] = m;
-            ncell *= (uint32_t)__popc(m);
-            if (j >= L) ntop *= (uint32_t)__popc(m);
-        }
-        if (MODE == kPCount && !finite && lane == 0) atomicOr(pa.nonfinite, 1u);
-        ProbeState st{0u, ~0ull, 0xffffffffu, ~0ull, 0xffffffffu, 0ull};
-        if (ncell == 0u) {
-            // nothing adjacent exists
-        } else if (prefix_scan) {
-            // ---- 2a. top prefixes, 32 per round; the occupancy bitmap (dilated +-1 along dimension
-            //      L-1) drops prefixes with no cell near the query's c_{L-1}
-            uint64_t qh = 0, qh2 = 0;
-#pragma unroll
-            for (int j = 0; j < D; ++j)
-                if (j < L) { qh += c0[j] * ix.occ_mul[j]; qh2 += c0[j] * ix.occ2_mul[j]; }
-            for (uint32_t base = 0; base < ntop; base += 32u) {
-                uint32_t clo = 0, chi = 0;
-                const uint32_t o = base + lane;
-                if (o < ntop) {
-                    uint32_t r = o;
-                    uint64_t p = 0, ob = qh, ob2 = qh2;
-#pragma unroll
-                    for (int j = 0; j < D; ++j) {
-                        if (j < L) continue;
-                        const uint32_t nj = (uint32_t)__popc(sel[j]);
-                        const uint32_t rj = r % nj;
-                        r /= nj;
-                        const uint64_t cj = pick(sel[j], rj, c0[j]);
-                        p += cj * ix.pstride[j];
-                        ob += cj * ix.occ_mul[j];
-                        ob2 += cj * ix.occ2_mul[j];
-                    }
-                    bool live = true;
-                    if (ix.occ) {
-                        live = (__ldg(ix.occ + (ob >> 5)) >> (ob & 31u)) & 1u;
-                        if (live && ix.occ2) live = (__ldg(ix.occ2 + (ob2 >> 5)) >> (ob2 & 31u)) & 1u;
-                    }
-                    ++probes;
-                    if (live) {
-                        clo = __ldg(ix.dir + p);
-                        chi = __ldg(ix.dir + p + 1);
-                    }
-                }
-                // ---- 2b. the prefixes' cells, 32 per step: keep those whose low coordinates are
-                //      adjacent (and valid) -> their point ranges
-                const uint32_t clen = chi - clo;
-                const uint32_t cinc = warp_inclusive(clen, lane);
-                const uint32_t ctotal = __shfl_sync(0xffffffffu, cinc, 31);
-                const uint32_t cexc = cinc - clen;
-                for (uint32_t g0 = 0; g0 < ctotal; g0 += 32u) {
-                    const uint32_t g = g0 + lane;
-                    const uint32_t own = owner_of(cinc, g);
-                    const uint32_t olo = __shfl_sync(0xffffffffu, clo, own);
-                    const uint32_t oexc = __shfl_sync(0xffffffffu, cexc, own);
-                    uint32_t lo = 0, hi = 0;
-                    if (g < ctotal) {
-                        const uint32_t h = olo + (g - oexc);
-                        uint64_t c[D];
-                        key_to_coords<D>(ix, __ldg(ix.B + h), c);
-                        bool ok = true;
-#pragma unroll
-                        for (int j = 0; j < D; ++j) {
-                            if (j >= L) continue;
-                            const uint64_t e = c[j] - (c0[j] - 1u);    // 0..2 when adjacent
-                            ok = ok && e < 3u && ((sel[j] >> e) & 1u);
-                        }
-                        if (ok) {
-                            lo = __ldg(ix.G + h);
-                            hi = __ldg(ix.G + h + 1);
-                        }
-                    }
-                    sweep<D, MODE>(ix, pa, x, qid, lo, hi, lane, st);
-                }
-            }
-        } else {
-            // ---- 2. 32 neighbour cells per round, each looked up by one lane: linear id (R8), prefix
-            //      p = sum c_j * pstride_j, one binary search of B bounded to [dir[p], dir[p+1])
-            for (uint32_t base = 0; base < ncell; base += 32u) {
-                uint32_t lo = 0, hi = 0;
-                const uint32_t o = base + lane;
-                if (o < ncell) {
-                    uint32_t r = o;
-                    uint64_t key = 0, p = 0;
-#pragma unroll
-                    for (int j = 0; j < D; ++j) {
-                        const uint32_t nj = (uint32_t)__popc(sel[j]);
-                        const uint32_t rj = r % nj;
-                        r /= nj;
-                        const uint64_t cj = pick(sel[j], rj, c0[j]);
-                        key += cj * ix.strides[j];
-                        p += cj * ix.pstride[j];
-                    }
-                    ++probes;
-                    uint32_t h = __ldg(ix.dir + p);
-                    uint32_t h1 = __ldg(ix.dir + p + 1);
-                    while (h < h1) {
-                        const uint32_t mid = (h + h1) >> 1;
-                        if (__ldg(ix.B + mid) < key) h = mid + 1;
-                        else h1 = mid;
-                    }
-                    if (h < ix.nG && __ldg(ix.B + h) == key) {
-                        lo = __ldg(ix.G + h);
-                        hi = __ldg(ix.G + h + 1);
-                    }
-                }
-                // ---- 3. the cells' points, swept by the whole warp
-                sweep<D, MODE>(ix, pa, x, qid, lo, hi, lane, st);
-            }
-        }
-        tests += st.tests;
-        const uint32_t found = st.found;
-        hits_all += found;
-        if constexpr (MODE == kPCount) {
-            if (lane == 0) {
-                pa.counts[t] = found;
-                atomicAdd(pa.buckets + (t >> 10), (unsigned long long)found);
-            }
-        } else if constexpr (MODE == kPKnn) {
-            if (found >= pa.k) {
-                if (lane < pa.k) {
-                    pa.ids[(uint64_t)qid * pa.k + lane] = st.bi;
-                    pa.dist2[(uint64_t)qid * pa.k + lane] = __longlong_as_double((long long)st.bs);
-                }
-            } else if (lane == 0) {
-                pa.unres[atomicAdd(pa.n_unres, 1u)] = qid;
-            }
-        }
+        probe_query<D, MODE>(ix, pa, t, qid, x, lane, probes, tests, hits_all);
     }
     // per-lane counters: one atomic per warp and counter
 #pragma unroll
@@ -373,9 +384,233 @@ __global__ void __launch_bounds__(kProbeThreads, SJ_PROBE_MINB) k_probe(const De
     }
 }
 
+// ---- two-set join, dense regimes: queries sorted by their cell in P's grid, 32 per warp.  A warp
+// whose 32 queries share one cell (populous cells) shares the candidates too: each 32-candidate tile
+// of the neighbour cells is staged once in shared memory (SoA) and every lane tests it against its own
+// query (32 x 32 tests per tile instead of 32 per tile); other warps take their queries one by one
+// (probe_query).  Count / fill only.
+constexpr int kTileWarps = kProbeThreads / 32;
+
+// cell key of every query in P's grid (R7, R8), or 2^key_bits when no neighbour cell can exist
+// (a coordinate outside the pad cells 0 .. |g_j|-1, or non-finite): the sort key of the tiled join
+template <int D>
+__global__ void __launch_bounds__(256) k_qkeys(const DevIndex ix, const double *__restrict__ q, uint32_t nq,
+                                               uint64_t sentinel, uint64_t *__restrict__ keys,
+                                               uint32_t *__restrict__ vals)
+{
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nq; t += gridDim.x * blockDim.x) {
+        uint64_t key = 0;
+        bool ok = true;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const double tq = floor(__ddiv_rn(__dsub_rn(__ldg(q + (uint64_t)t * D + j), ix.mins[j]), ix.w));
+            ok = ok && tq >= -1.0 && tq <= (double)ix.cpd[j] - 2.0;    // c_j = tq + 1 in [0, |g_j| - 1]
+            if (ok) key += (uint64_t)(tq + 1.0) * ix.strides[j];
+        }
+        keys[t] = ok ? key : sentinel;
+        vals[t] = t;
+    }
+}
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(kProbeThreads, SJ_PROBE_MINB) k_probe_tiled(const DevIndex ix, const ProbeArgs pa)
+{
+    __shared__ __align__(16) double s_tx[kTileWarps][D * 32];
+    __shared__ uint32_t s_tid[kTileWarps][32];
+    const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+    const uint32_t groups = (pa.nq + 31u) >> 5;
+    const uint32_t n = ix.n;
+    double *tx = s_tx[wib];
+    uint32_t *tid = s_tid[wib];
+    unsigned long long probes = 0, tests = 0, hits_all = 0;
+    for (uint32_t grp = blockIdx.x * kTileWarps + wib; grp < groups; grp += gridDim.x * kTileWarps) {
+        const uint32_t t = grp * 32u + lane;             // this lane's query position in the launch
+        const bool have = t < pa.nq;
+        uint32_t qid = 0;
+        double x[D];
+        double tq[D];
+        bool ok = have;
+        if (have) {
+            qid = __ldg(pa.qlist + pa.q_begin + t);
+#pragma unroll
+            for (int j = 0; j < D; ++j) x[j] = __ldg(pa.q + (uint64_t)qid * D + j);
+        } else {
+#pragma unroll
+            for (int j = 0; j < D; ++j) x[j] = 0.0;
+        }
+        uint64_t mykey = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            tq[j] = floor(__ddiv_rn(__dsub_rn(x[j], ix.mins[j]), ix.w));   // c_j - 1
+            ok = ok && tq[j] >= -1.0 && tq[j] <= (double)ix.cpd[j] - 2.0;  // some neighbour can exist
+            if (ok) mykey += (uint64_t)(tq[j] + 1.0) * ix.strides[j];
+        }
+        // the group's runs of queries sharing a cell (sorted: runs are contiguous lanes); lanes whose
+        // query has no possible neighbour take a key of their own and no run
+        const unsigned peers = __match_any_sync(0xffffffffu, ok ? mykey : (0x8000000000000000ull | lane));
+        const unsigned leaders = __ballot_sync(0xffffffffu, ok && (uint32_t)(__ffs(peers) - 1) == lane);
+        uint32_t found = 0;
+        if (__popc(leaders) > 4) {
+            // many cells (sparse regime): the queries one by one, each over a flattened sweep
+            for (uint32_t i = 0; i < 32u; ++i) {
+                const uint32_t ti = grp * 32u + i;
+                if (ti >= pa.nq) break;                  // warp-uniform
+                const uint32_t qi = __shfl_sync(0xffffffffu, qid, i);
+                double xi[D];
+#pragma unroll
+                for (int j = 0; j < D; ++j) xi[j] = __shfl_sync(0xffffffffu, x[j], i);
+                probe_query<D, MODE>(ix, pa, ti, qi, xi, lane, probes, tests, hits_all);
+            }
+            continue;
+        }
+        for (unsigned lead = leaders; lead; lead &= lead - 1u) {
+        const int ld = __ffs(lead) - 1;
+        const bool mine = (__shfl_sync(0xffffffffu, peers, ld) >> lane) & 1u;   // this lane's query is in the run
+        // ---- the run's cell: its neighbour coordinates (valid, occupied), as in probe_query
+        uint64_t c0[D];
+        uint32_t sel[D];
+        uint32_t ncell = 1;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const int64_t b = (int64_t)__shfl_sync(0xffffffffu, tq[j], ld);
+            uint32_t m = 0;
+#pragma unroll
+            for (int e = 0; e < 3; ++e) {
+                const int64_t cc = b + e;
+                bool v = cc >= 1 && cc <= (int64_t)ix.cpd[j] - 2;
+                if (v && ix.masks) {
+                    const uint64_t bit = ix.mask_off[j] + (uint64_t)cc;
+                    v = (__ldg(ix.masks + (bit >> 5)) >> (bit & 31u)) & 1u;
+                }
+                if (v) m |= 1u << e;
+            }
+            c0[j] = (uint64_t)(b + 1);
+            sel[j] = m;
+            ncell *= (uint32_t)__popc(m);
+        }
+        for (uint32_t base = 0; base < ncell; base += 32u) {
+            uint32_t lo = 0, hi = 0;
+            const uint32_t o = base + lane;
+            if (o < ncell) {
+                uint32_t r = o;
+                uint64_t key = 0, p = 0;
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    const uint32_t nj = (uint32_t)__popc(sel[j]);
+                    const uint32_t rj = r % nj;
+                    r /= nj;
+                    const uint64_t cj = pick(sel[j], rj, c0[j]);
+                    key += cj * ix.strides[j];
+                    p += cj * ix.pstride[j];
+                }
+                ++probes;
+                uint32_t h = __ldg(ix.dir + p);
+                uint32_t h1 = __ldg(ix.dir + p + 1);
+                while (h < h1) {
+                    const uint32_t mid = (h + h1) >> 1;
+                    if (__ldg(ix.B + mid) < key) h = mid + 1;
+                    else h1 = mid;
+                }
+                if (h < ix.nG && __ldg(ix.B + h) == key) {
+                    lo = __ldg(ix.G + h);
+                    hi = __ldg(ix.G + h + 1);
+                }
+            }
+            unsigned pend = __ballot_sync(0xffffffffu, lo < hi);
+            while (pend) {
+                const int src = __ffs(pend) - 1;
+                pend &= pend - 1u;
+                const uint32_t rlo = __shfl_sync(0xffffffffu, lo, src), rhi = __shfl_sync(0xffffffffu, hi, src);
+                for (uint32_t m0 = rlo; m0 < rhi; m0 += 32u) {
+                    const uint32_t lim = min(32u, rhi - m0);
+                    __syncwarp();
+                    if (lane < lim) {
+#pragma unroll
+                        for (int j = 0; j < D; ++j) tx[j * 32 + lane] = __ldg(ix.X + (uint64_t)j * n + m0 + lane);
+                        tid[lane] = __ldg(ix.A + m0 + lane);
+                    }
+                    __syncwarp();
+                    // two candidates per 16-byte broadcast load per dimension; fully unrolled (constant bit
+                    // positions), the ragged last tile leaves by a uniform branch
+                    uint32_t hm = 0;
+                    const double2 *t2 = reinterpret_cast<const double2 *>(tx);
+                    const uint32_t npair = (lim + 1u) >> 1;
+#pragma unroll
+                    for (uint32_t e2 = 0; e2 < 16u; ++e2) {
+                        if (e2 >= npair) break;
+                        double2 c = t2[e2];
+                        double ta = __dsub_rn(x[0], c.x), tb = __dsub_rn(x[0], c.y);
+                        double sa = __dmul_rn(ta, ta), sb = __dmul_rn(tb, tb);
+#pragma unroll
+                        for (int j = 1; j < D; ++j) {
+                            c = t2[j * 16 + e2];
+                            ta = __dsub_rn(x[j], c.x);
+                            tb = __dsub_rn(x[j], c.y);
+                            sa = __dadd_rn(sa, __dmul_rn(ta, ta));
+                            sb = __dadd_rn(sb, __dmul_rn(tb, tb));
+                        }
+                        if (sa <= ix.eps2) hm |= 1u << (2u * e2);
+                        if (sb <= ix.eps2) hm |= 2u << (2u * e2);
+                    }
+                    hm &= lim == 32u ? 0xffffffffu : ((1u << lim) - 1u);   // (the odd tail's partner is stale)
+                    if (!mine) hm = 0u;
+                    tests += lim;
+                    const uint32_t cnt = (uint32_t)__popc(hm);
+                    found += cnt;
+                    if constexpr (MODE == kPFill) {
+                        const uint32_t inc = warp_inclusive(cnt, lane);
+                        const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+                        if (tot) {
+                            unsigned long long b0 = 0;
+                            if (lane == 31) b0 = atomicAdd(pa.cursor, (unsigned long long)tot);
+                            b0 = __shfl_sync(0xffffffffu, b0, 31);
+                            unsigned long long at = b0 + (inc - cnt);
+                            uint32_t mm = hm;
+                            while (mm) {
+                                const int e = __ffs(mm) - 1;
+                                mm &= mm - 1u;
+                                if (at < pa.cap) pa.out[at] = ((uint64_t)qid << 32) | tid[e];
+                                else atomicOr(pa.overflow, 1u);
+                                ++at;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        }   // runs
+        hits_all += found;
+        if constexpr (MODE == kPCount) {
+            pa.counts[t] = found;
+            unsigned long long sum = found;
+#pragma unroll
+            for (int o2 = 16; o2; o2 >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o2);
+            if (lane == 0) atomicAdd(pa.buckets + (t >> 10), sum);      // a group never straddles a bucket
+        }
+    }
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) {
+        probes += __shfl_xor_sync(0xffffffffu, probes, o2);
+        tests += __shfl_xor_sync(0xffffffffu, tests, o2);
+        hits_all += __shfl_xor_sync(0xffffffffu, hits_all, o2);
+    }
+    if (lane == 0 && pa.work) {
+        atomicAdd(pa.work + 0, probes);
+        atomicAdd(pa.work + 1, tests);
+        atomicAdd(pa.work + 2, hits_all);
+    }
+}
+
 template <int D>
 void launch_probe_d(int mode, const DevIndex &ix, const ProbeArgs &pa, dim3 grid, cudaStream_t s)
 {
+    if (pa.tiled && mode != kPKnn) {
+        const uint64_t groups = ((uint64_t)pa.nq + 31) / 32;
+        const dim3 g2((uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((groups + kTileWarps - 1) / kTileWarps, grid.x)));
+        if (mode == kPCount) k_probe_tiled<D, kPCount><<<g2, kProbeThreads, 0, s>>>(ix, pa);
+        else k_probe_tiled<D, kPFill><<<g2, kProbeThreads, 0, s>>>(ix, pa);
+        return;
+    }
     switch (mode) {
     case kPCount: k_probe<D, kPCount><<<grid, kProbeThreads, 0, s>>>(ix, pa); break;
     case kPFill: k_probe<D, kPFill><<<grid, kProbeThreads, 0, s>>>(ix, pa); break;
@@ -549,6 +784,28 @@ sj_result *join_sets_impl(const sj_index *idx, const double *queries, uint64_t n
     try {
         ProbeArgs q{};
         q.q = qd;
+        // queries sorted by their cell in P's grid (LSD radix sort of (key, row)): neighbouring queries
+        // share neighbour cells (L2 reuse) and a warp of one populous cell shares candidate tiles
+        Scratch<uint64_t> qk(nq, s), qk2(nq, s);
+        Scratch<uint32_t> qv(nq, s), qv2(nq, s);
+        if (nq) {
+            // keys < prod |g_j| <= 2^key_bits; the sentinel 2^key_bits (all ones at 64 bits) sorts last
+            const int kb = std::min(64, idx->view.key_bits + 1);
+            const uint64_t sentinel = idx->view.key_bits >= 64 ? ~0ull : (1ull << idx->view.key_bits);
+            const unsigned g = (unsigned)std::min<uint64_t>((nq + 255) / 256, (uint64_t)device_sm_count(dev) * 8);
+            switch (D) {
+            case 2: k_qkeys<2><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p); break;
+            case 3: k_qkeys<3><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p); break;
+            case 4: k_qkeys<4><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p); break;
+            case 5: k_qkeys<5><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p); break;
+            default: k_qkeys<6><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p); break;
+            }
+            SJ_LAUNCHED();
+            bool in_tmp = false;
+            radix_sort_pairs(qk.p, qv.p, qk2.p, qv2.p, (uint32_t)nq, kb, s, &in_tmp);
+            q.qlist = in_tmp ? qv2.p : qv.p;
+            q.tiled = 1;
+        }
         probe_join(ix, dev, q, nq, o, s, res);
     } catch (...) {
         cudaStreamSynchronize(s);
