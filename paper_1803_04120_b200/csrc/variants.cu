@@ -390,6 +390,10 @@ __global__ void __launch_bounds__(kProbeThreads, SJ_PROBE_MINB) k_probe(const De
 // query (32 x 32 tests per tile instead of 32 per tile); other warps take their queries one by one
 // (probe_query).  Count / fill only.
 constexpr int kTileWarps = kProbeThreads / 32;
+#ifndef SJ_TILE_RUNS
+#define SJ_TILE_RUNS 4    // a warp with more cell runs than this takes its queries one by one (8: 3-D
+                          // about equal, 16 / 32: 3-D 5.2 -> 8.7 / 9.4 ms)
+#endif
 
 // cell key of every query in P's grid (R7, R8), or 2^key_bits when no neighbour cell can exist
 // (a coordinate outside the pad cells 0 .. |g_j|-1, or non-finite): the sort key of the tiled join
@@ -450,7 +454,13 @@ __global__ void __launch_bounds__(kProbeThreads, SJ_PROBE_MINB) k_probe_tiled(co
         const unsigned peers = __match_any_sync(0xffffffffu, ok ? mykey : (0x8000000000000000ull | lane));
         const unsigned leaders = __ballot_sync(0xffffffffu, ok && (uint32_t)(__ffs(peers) - 1) == lane);
         uint32_t found = 0;
-        if (__popc(leaders) > 4) {
+        if constexpr (MODE == kPCount) {
+            bool finite = true;
+#pragma unroll
+            for (int j = 0; j < D; ++j) finite = finite && isfinite(x[j]);
+            if (have && !finite) atomicOr(pa.nonfinite, 1u);
+        }
+        if (__popc(leaders) > SJ_TILE_RUNS) {
             // many cells (sparse regime): the queries one by one, each over a flattened sweep
             for (uint32_t i = 0; i < 32u; ++i) {
                 const uint32_t ti = grp * 32u + i;

@@ -256,3 +256,21 @@ def test_f32_full_size(sj):
         want = len(oracle.brute_force_f32(P32[[i, k]], 8.0, include_self=False)) == 2
         assert g == want, (i, k)
     res.free()
+
+
+def test_join_sets_nonfinite_in_a_tiled_warp(sj):
+    """A NaN query among queries of one populous cell (the tiled path takes the whole warp) is still
+    reported (SJ_ERR_NONFINITE), and so is one among a few queries."""
+    P = np.concatenate([datagen.uniform(3000, 2, seed=1), np.full((200, 2), 50.0)])
+    idx = sj.build_index(torch.from_numpy(P).cuda(), 2.0)
+    Q = np.full((64, 2), 50.25)
+    Q[37, 0] = np.nan
+    with pytest.raises(sj.SJError) as e:
+        sj.join_sets(idx, Q)
+    assert e.value.status == 2
+    Q2 = np.full((3, 2), 50.25)
+    Q2[1, 1] = np.inf
+    with pytest.raises(sj.SJError):
+        sj.join_sets(idx, Q2)
+    ok = np.full((64, 2), 50.25)
+    assert np.array_equal(sj.join_sets(idx, ok).to_numpy(sort=True), oracle.join_sets(ok, P, 2.0))
