@@ -52,6 +52,8 @@ def parse_args(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle sample duration")
     ap.add_argument("--phases", action="store_true", help="also print per-phase timings (stderr)")
     ap.add_argument("--also-eps", type=float, default=8.0, help="secondary eps of the same metric (0: off)")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the f4 variant lines (FP32 self-join, two-set join, kNN; rank 0, N=1 only)")
     ap.add_argument("--dry-run", action="store_true", help="CPU-only multi-rank plumbing test (gloo)")
     ap.add_argument("--backend", default=None, choices=[None, "nccl", "gloo"],
                     help="process-group backend for N>1 (default nccl; gloo when ranks share a GPU)")
@@ -369,6 +371,61 @@ def profile_child(args):
         idx.free()
 
 
+def bench_variants(sj, pts_dev, pts, args, flush, stream, dev):
+    """FP32 self-join (R21), two-set join (R19) and kNN (R20) on the headline's point set: median device
+    ms of K calls after W warm-up calls."""
+    import math
+
+    import torch
+
+    def timed_call(fn, k, w):
+        for _ in range(w):
+            r = fn()
+            if hasattr(r, "free"):
+                r.free()
+        ms, last = [], None
+        for i in range(k):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            last = fn()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms.append(e0.elapsed_time(e1))
+            if hasattr(last, "free") and i < k - 1:
+                last.free()
+        ms.sort()
+        return ms[len(ms) // 2], last
+
+    out = {}
+    k, w = max(3, min(args.steps, 5)), max(1, min(args.warmup, 3))
+    try:
+        p32 = pts_dev.float()
+        ms, r = timed_call(lambda: sj.self_join_f32(p32, args.eps), k, w)
+        out["fp32_self_join"] = {"ms": ms, "pairs": r.n_pairs, "pairs_per_s": r.n_pairs / (ms / 1e3),
+                                 "config": f"the headline points rounded to float32, eps={args.eps}"}
+        r.free()
+        del p32
+        import datagen
+        q = torch.from_numpy(datagen.uniform(args.n, args.d, seed=777 + args.d)).to(dev)
+        idx = sj.build_index(pts_dev, args.eps)
+        ms, r = timed_call(lambda: sj.join_sets(idx, q), k, w)
+        out["two_set_join"] = {"ms": ms, "pairs": r.n_pairs, "queries_per_s": args.n / (ms / 1e3),
+                               "config": f"P = the headline points, Q = {args.n} independent uniform points, eps={args.eps}"}
+        r.free()
+        del idx, q
+        kk = 8
+        vol = kk / args.n * 100.0 ** args.d
+        eps0 = 1.3 * (vol * math.gamma(1 + args.d / 2) / math.pi ** (args.d / 2)) ** (1.0 / args.d)
+        ms, r = timed_call(lambda: sj.knn_self(pts_dev, kk, eps0)[0], k, w)
+        out["knn_self_join"] = {"ms": ms, "queries_per_s": args.n / (ms / 1e3),
+                                "config": f"the headline points, k={kk}, eps0={eps0:.4g} (radius doubling)"}
+    except Exception as e:  # noqa: BLE001 -- reported, the headline line stands
+        out["error"] = f"{type(e).__name__}: {e}"
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -546,6 +603,13 @@ def run_ours(args):
                 "pairs_per_step": pairs2, "refine_span_ms": span2, "candidates_tested": c2,
                 "fp64_frac": ((3 * args.d * c2 / world) / (span2 / 1e3) / fp64_peak) if (span2 and fp64_peak) else None}
 
+    # ---- SURVEY §8(f) rank-4 variants on the same point set (rank 0, N=1): device time per call with
+    # CUDA events around the library call (it returns when its result is complete), L2 flushed before
+    # each, best-effort (an error is reported in the line instead of failing the bench)
+    variants = None
+    if rank == 0 and world == 1 and not args.no_variants:
+        variants = bench_variants(sj, pts_dev, pts, args, flush, stream, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(pts, args.eps, args.cpu_seconds)
@@ -563,7 +627,7 @@ def run_ours(args):
                            "l2": "flushed (512 MB write) before every timed step",
                            "results": "device-resident batches (value); pinned-host drained batches (e2e)"},
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
-                "cpu_baseline": cpu, "phases": phases, "also": also}
+                "cpu_baseline": cpu, "phases": phases, "also": also, "variants": variants}
         print(json.dumps(line), flush=True)
         if args.phases:
             print(json.dumps(phases, indent=1), file=sys.stderr)
