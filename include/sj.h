@@ -310,7 +310,7 @@ sj_status sj_self_join_f32(const float *points, uint64_t n, int d, float eps, co
                            const sj_join_opts *jopts, sj_result **out);
 
 typedef struct {
-    uint32_t rounds;             /* radius doublings + 1 (index builds)                             */
+    uint32_t rounds;             /* radius steps + 1 (index builds)                                  */
     double eps_final;            /* radius of the last round                                        */
     uint64_t cells_probed;       /* cell lookups over all rounds                                    */
     uint64_t candidates_tested;  /* distance evaluations over all rounds                            */
@@ -321,7 +321,8 @@ typedef struct {
  * to the smaller id -- written as row i of ids[n*k] (original ids) and dist2[n*k] (s), ascending.
  * The ε-grid does it: an index with radius eps0; each point's k best among the points of its 3^d
  * neighbour cells within eps are final when there are k of them (every other point fails the
- * predicate); the rest are re-run on an index with 2*eps, until none is left.
+ * predicate); the rest are re-run on an index for eps * 4^(1/d) (the neighbourhood volume x 4), until
+ * none is left.
  *   points : row-major n x d float64, host or device per bopts->points_on_device.
  *   k      : 1..32, k + 1 <= n < 2^32.       eps0: the first radius, finite, > 0 (about the k-th
  *            neighbour distance is cheapest; too small costs rounds, too large costs candidates).

@@ -5,7 +5,7 @@
 //     query of Q probes the 3^d cells around its own cell in P's grid, full search (no unicomp: Q != P).
 //   * kNN self-join ("other spatial searches, such as kNN"; R20): every point's k
 //     best (s, id) among the points of its 3^d neighbour cells that satisfy the join predicate; certified
-//     when there are k of them, otherwise re-run on an index with 2*eps.
+//     when there are k of them, otherwise re-run on an index with a larger eps (x 4^(1/d)).
 //
 // One kernel, k_probe<D, MODE>, ONE WARP PER QUERY:
 //   1. the query's coordinates are warp-uniform; per dimension the <= 3 neighbour coordinates that lie in
@@ -918,11 +918,18 @@ void knn_self_impl(const double *points, uint64_t n, int d, uint32_t k, double e
     b2.stream = s;
     b2.speculative_estimate = 0;
     double eps = eps0;
+    // radius growth per round: the 3^d neighbourhood's volume x SJ_KNN_GROW_VOL (a doubling of eps
+    // multiplies a 6-D neighbourhood's candidates by 64 for the few uncertified -- mostly boundary --
+    // queries); the certificate does not depend on the schedule
+#ifndef SJ_KNN_GROW_VOL
+#define SJ_KNN_GROW_VOL 4.0
+#endif
+    const double grow = std::max(1.1, std::pow(SJ_KNN_GROW_VOL, 1.0 / d));
     uint64_t pending = n, probes = 0, tests = 0;
     uint32_t rounds = 0;
     int cur = 0;
     while (pending) {
-        if (++rounds > 64) fail(SJ_ERR_STATE, "kNN: not certified after 64 radius doublings");
+        if (++rounds > 400) fail(SJ_ERR_STATE, "kNN: not certified after 400 radius steps");
         sj_index *idx = build_index_impl(pd, n, d, eps, b2);
         try {
             SJ_CUDA(cudaMemsetAsync(words.p, 0, sizeof(unsigned long long) * 8, s));
@@ -952,7 +959,7 @@ void knn_self_impl(const double *points, uint64_t n, int d, uint32_t k, double e
         }
         free_index_impl(idx);
         cur ^= 1;
-        if (pending) eps *= 2.0;
+        if (pending) eps *= grow;
     }
     if (st) {
         st->rounds = rounds;
