@@ -885,15 +885,22 @@ __device__ __forceinline__ void refine_query(const DevIndex &ix, const JoinArgs 
 // as the whole sparse 6-D refine; a CTA-wide reduction instead made every warp wait at a barrier
 // for the CTA's slowest warp (19% of the stall samples).
 constexpr int kWorkSlots = 256;
+// Sum of a 64-bit per-lane counter over the full warp with two REDUX.SUM (32-bit warp reductions):
+// the low 27 bits of 32 lanes sum below 2^32, the high parts below 2^32 for any counter < 2^59.  (Five
+// rounds of 64-bit shuffles were 7 % of the sparse refine's instructions, for statistics only.)
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
+{
+    const unsigned lo = __reduce_add_sync(0xffffffffu, (unsigned)(v & 0x7FFFFFFull));
+    const unsigned hi = __reduce_add_sync(0xffffffffu, (unsigned)(v >> 27));
+    return (unsigned long long)lo + ((unsigned long long)hi << 27);
+}
+
 __device__ __forceinline__ void flush_work(const JoinArgs &ja, unsigned long long p, unsigned long long c,
                                            unsigned long long em)
 {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        p += __shfl_xor_sync(0xffffffffu, p, o);
-        c += __shfl_xor_sync(0xffffffffu, c, o);
-        em += __shfl_xor_sync(0xffffffffu, em, o);
-    }
+    p = warp_sum_u64(p);
+    c = warp_sum_u64(c);
+    em = warp_sum_u64(em);
     if ((threadIdx.x & 31) == 0 && ja.work) {
         const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
         unsigned long long *w = ja.work + 4 * (gw % kWorkSlots);
