@@ -80,6 +80,8 @@ def _load():
         lib.orc_join_sets_grid.restype = i64
         lib.orc_brute_force_f32.argtypes = [p, i64, i32, ctypes.c_float, i32, p, i64]
         lib.orc_brute_force_f32.restype = i64
+        lib.orc_join_sets_digest.argtypes = [p, i64, p, i64, i32, dbl, i32, p, p]
+        lib.orc_join_sets_digest.restype = i64
         lib.orc_knn.argtypes = [p, i64, p, p, i64, i32, i32, i32, p, p]
         lib.orc_knn.restype = i32
         lib.orc_mix.argtypes = [i32, ctypes.c_uint64]
@@ -306,4 +308,22 @@ def brute_force_f32(points, eps: float, include_self: bool = True) -> np.ndarray
         raise ValueError("bad arguments")
     out = np.empty(total, dtype=np.uint64)
     lib.orc_brute_force_f32(_ptr(P), n, d, e, int(include_self), _ptr(out), total)
+    return out
+
+
+def join_sets_digest(queries, points, eps: float, nthreads: int | None = None, with_counts: bool = False):
+    """|J(Q,P)| and the order-independent fingerprints F_a, F_b of the pair multiset (the grid join of
+    join_sets, accumulated instead of stored; the mixers of sj_oracle.c): dict(pairs, fa, fb[, counts])."""
+    Q = _pts(queries)
+    P = _pts(points)
+    nq, d = Q.shape
+    counts = np.zeros(nq, dtype=np.int64) if with_counts else None
+    fp = np.zeros(2, dtype=np.uint64)
+    total = _load().orc_join_sets_digest(_ptr(Q), nq, _ptr(P), P.shape[0], d, float(eps), nthreads or default_threads(),
+                                         _ptr(counts) if counts is not None else None, _ptr(fp))
+    if total < 0:
+        raise ValueError("bad arguments")
+    out = dict(pairs=int(total), fa=int(fp[0]), fb=int(fp[1]))
+    if with_counts:
+        out["counts"] = counts
     return out

@@ -297,3 +297,88 @@ int64_t orc_brute_force_f32(const float *pts, int64_t n, int d, float eps, int i
         }
     return cnt;
 }
+
+/* ---- J(Q,P) fingerprints (full-size parity of two-set results too large to hold) ------------------
+ * The grid join above, accumulating instead of storing: |J|, F_a = sum of mix_a(pair), F_b = sum of
+ * mix_b(pair) (mod 2^64; the mixers of sj_oracle.c, orc_mix), per-query counts optional. */
+uint64_t orc_mix(int which, uint64_t x);
+
+typedef struct {
+    const vo_grid *g; const double *Q; double E;
+    int64_t q0, q1;
+    int64_t *counts;
+    int64_t total; uint64_t fa, fb;
+} vo_dig_job;
+
+static void *vo_digest_worker(void *arg)
+{
+    vo_dig_job *J = (vo_dig_job *)arg;
+    const vo_grid *g = J->g;
+    int d = g->d;
+    int64_t noff = 1;
+    for (int j = 0; j < d; ++j) noff *= 3;
+    int64_t ci[VO_MAXD], nb[VO_MAXD];
+    for (int64_t i = J->q0; i < J->q1; ++i) {
+        const double *q = J->Q + i * d;
+        int64_t cnt = 0;
+        if (vo_tuple(q, d, g->w, ci)) {
+            for (int64_t o = 0; o < noff; ++o) {
+                int64_t r = o;
+                for (int j = 0; j < d; ++j) { nb[j] = ci[j] + (r % 3) - 1; r /= 3; }
+                for (int64_t m = vo_lower(g, nb); m < g->n; ++m) {
+                    int64_t k = g->order[m];
+                    if (vo_cmp_tuple(g->tup + k * d, nb, d) != 0) break;
+                    if (vo_dist(q, g->P + k * d, d) <= J->E) {
+                        uint64_t x = ((uint64_t)i << 32) | (uint64_t)k;
+                        J->fa += orc_mix(0, x);
+                        J->fb += orc_mix(1, x);
+                        ++cnt;
+                    }
+                }
+            }
+        }
+        if (J->counts) J->counts[i] = cnt;
+        J->total += cnt;
+    }
+    return NULL;
+}
+
+int64_t orc_join_sets_digest(const double *Q, int64_t nq, const double *P, int64_t n, int d, double eps,
+                             int nthreads, int64_t *counts, uint64_t *fp)
+{
+    if (nq < 0 || n < 0 || d < 1 || d > VO_MAXD || !(eps > 0.0) || !fp) return -1;
+    if (nthreads < 1) nthreads = 1;
+    double maxabs = 0.0;
+    for (int64_t i = 0; i < n * d; ++i) if (fabs(P[i]) > maxabs) maxabs = fabs(P[i]);
+    for (int64_t i = 0; i < nq * d; ++i) if (fabs(Q[i]) > maxabs) maxabs = fabs(Q[i]);
+    vo_grid g;
+    g.d = d; g.n = n; g.P = P;
+    g.w = eps * (1.0 + ldexp(1.0, -30)) + ldexp(maxabs, -40);
+    g.tup = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n * d > 0 ? n * d : 1));
+    g.order = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    for (int64_t k = 0; k < n; ++k) {
+        g.order[k] = k;
+        if (!vo_tuple(P + k * d, d, g.w, g.tup + k * d)) { free(g.tup); free(g.order); return -2; }
+    }
+    VO_CTX = &g;
+    qsort(g.order, (size_t)n, sizeof(int64_t), vo_cmp_point);
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    vo_dig_job *jobs = (vo_dig_job *)calloc((size_t)nthreads, sizeof(vo_dig_job));
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t].g = &g; jobs[t].Q = Q; jobs[t].E = eps * eps;
+        jobs[t].q0 = nq * t / nthreads;
+        jobs[t].q1 = nq * (t + 1) / nthreads;
+        jobs[t].counts = counts;
+        pthread_create(&th[t], NULL, vo_digest_worker, &jobs[t]);
+    }
+    int64_t total = 0;
+    fp[0] = fp[1] = 0;
+    for (int t = 0; t < nthreads; ++t) {
+        pthread_join(th[t], NULL);
+        total += jobs[t].total;
+        fp[0] += jobs[t].fa; fp[1] += jobs[t].fb;
+    }
+    free(th); free(jobs);
+    free(g.tup); free(g.order);
+    return total;
+}

@@ -188,3 +188,15 @@ def test_f32_bracketed_by_fp64(d):
     assert len(got) > 2 * len(P)
     if lo == hi:
         assert got == lo
+
+
+def test_join_sets_digest_matches_explicit_pairs():
+    """The two-set digest (|J|, F_a, F_b, per-query counts) equals the fingerprints of the explicit grid
+    join (itself pinned above), on clustered data with duplicates."""
+    P = datagen.clustered_small(2500, 3, seed=12)
+    Q = P[::2] + 0.01                             # near P's clusters (and its quantised duplicates)
+    want = oracle.join_sets(Q, P, 0.6, method="brute")
+    dg = oracle.join_sets_digest(Q, P, 0.6, with_counts=True)
+    assert dg["pairs"] == len(want) > 1000
+    assert (dg["fa"], dg["fb"]) == oracle.fingerprint_pairs(want)
+    assert np.array_equal(dg["counts"], np.bincount((want >> np.uint64(32)).astype(np.int64), minlength=len(Q)))
