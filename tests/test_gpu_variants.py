@@ -274,3 +274,25 @@ def test_join_sets_nonfinite_in_a_tiled_warp(sj):
         sj.join_sets(idx, Q2)
     ok = np.full((64, 2), 50.25)
     assert np.array_equal(sj.join_sets(idx, ok).to_numpy(sort=True), oracle.join_sets(ok, P, 2.0))
+
+
+@pytest.mark.parametrize("cfg,d,eps", [("C2", 2, 1.0), ("C3", 6, 16.0), ("C4", 2, 0.005)])
+def test_join_sets_full_size_fingerprints(sj, cfg, d, eps):
+    """Full-size two-set results too large to hold twice (1.2e9 pairs at C2 2-D): |J|, the multiset
+    fingerprints F_a / F_b (device, over all batches) and the per-query counts against the oracle's
+    grid digest.  C4: P = the 15.2 M skewed cloud, Q = 2 M points of another skewed draw (the tiled
+    path's populous cells and the per-query path's sparse ones in one join)."""
+    if cfg == "C4":
+        P = datagen.skewed(15_228_633, d)
+        Q = datagen.skewed(2_000_000, d, seed=5)
+    else:
+        P = datagen.uniform_config(cfg, d)
+        Q = datagen.uniform(len(P), d, seed=779 + d)
+    idx = sj.build_index(torch.from_numpy(P).cuda(), eps)
+    res = sj.join_sets(idx, torch.from_numpy(Q).cuda())
+    want = oracle.join_sets_digest(Q, P, eps, with_counts=True)
+    assert res.n_pairs == want["pairs"]
+    fa, fb, cnt = res.fingerprint(counts=True, n_points=max(len(P), len(Q)))
+    assert (fa, fb) == (want["fa"], want["fb"])
+    assert np.array_equal(cnt.cpu().numpy()[:len(Q)].astype(np.int64), want["counts"])
+    res.free()
