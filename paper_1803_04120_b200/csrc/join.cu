@@ -90,6 +90,12 @@ void validate(const sj_index *idx, const sj_join_opts &o, uint64_t *qb, uint64_t
 // bucket_est[i].  Cut points are placed at bucket boundaries where the running estimate crosses
 // multiples of total/k, k = max(min_batches, ceil(total / (capacity/(1+margin)))); a bucket whose
 // estimate alone exceeds the target is split evenly (it is not sampled any finer).
+#ifndef SJ_PLAN_MARGIN
+#define SJ_PLAN_MARGIN 0.75   // batches target C / 1.75: the sampled per-batch estimates of skewed data miss by up
+                              // to ~50 % (C4 2-D eps=0.02: margin 0.25 -> 3 overflow re-runs in 14 batches,
+                              // 31.2 ms; 0.5 -> 2 in 17, 27.0 ms; 0.75 -> none in 20, 24.7 ms; C3 eps=24
+                              // 198 -> 188 ms; C2 2-D unchanged)
+#endif
 void plan_from_buckets(const double *bucket_est, uint64_t nbk, uint64_t width, uint64_t q0, uint64_t q1,
                        uint64_t capacity, int min_batches, double margin, std::vector<uint64_t> &cuts,
                        std::vector<uint64_t> &est, uint64_t *estimated_total)
@@ -402,7 +408,7 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
         {
             std::vector<double> be(nbk);
             for (uint64_t i = 0; i < nbk; ++i) be[i] = (double)bk[i] * (double)es.step;
-            plan_from_buckets(be.data(), nbk, es.step * es.group, q0, q1, o.batch_capacity_pairs, o.min_batches, 0.25,
+            plan_from_buckets(be.data(), nbk, es.step * es.group, q0, q1, o.batch_capacity_pairs, o.min_batches, SJ_PLAN_MARGIN,
                               cuts, est, &est_total);
         }
         stats.estimated_pairs = est_total;

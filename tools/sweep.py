@@ -61,7 +61,8 @@ for name, d, eps, gen in work:
     mode = {0: "dense", 1: "cellscan", 2: "rows"}
     print(f"{name} d={d} eps={eps:<6} N={len(P):>9} pairs={pairs:>11} total={dt*1e3:8.2f}ms "
           f"build={bt['total_ms']:6.2f} (sort {bt['sort_ms']:5.2f}) join={st['total_ms']:8.2f} "
-          f"(est {st['estimate_ms']:.2f}, refine_sum {st['refine_ms']:.2f}, batches {st['batches']}) "
+          f"(est {st['estimate_ms']:.2f}, refine_sum {st['refine_ms']:.2f}, batches {st['batches']}, "
+          f"retries {st['retries']}, est/pairs {st['estimated_pairs'] / max(pairs, 1):.3f}) "
           f"nG={g['n_cells']} k={g['dir_k']} cand={st['candidates_tested']:.3e} Gpairs/s={pairs/dt/1e9:.3f} "
           f"first_call={first*1e3:.2f}ms",
           flush=True)
