@@ -400,14 +400,16 @@ constexpr int kTileWarps = kProbeThreads / 32;
 template <int D>
 __global__ void __launch_bounds__(256) k_qkeys(const DevIndex ix, const double *__restrict__ q, uint32_t nq,
                                                uint64_t sentinel, uint64_t *__restrict__ keys,
-                                               uint32_t *__restrict__ vals)
+                                               uint32_t *__restrict__ vals, uint32_t *__restrict__ nonfinite)
 {
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nq; t += gridDim.x * blockDim.x) {
         uint64_t key = 0;
         bool ok = true;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            const double tq = floor(__ddiv_rn(__dsub_rn(__ldg(q + (uint64_t)t * D + j), ix.mins[j]), ix.w));
+            const double xj = __ldg(q + (uint64_t)t * D + j);
+            if (!isfinite(xj)) atomicOr(nonfinite, 1u);
+            const double tq = floor(__ddiv_rn(__dsub_rn(xj, ix.mins[j]), ix.w));
             ok = ok && tq >= -1.0 && tq <= (double)ix.cpd[j] - 2.0;    // c_j = tq + 1 in [0, |g_j| - 1]
             if (ok) key += (uint64_t)(tq + 1.0) * ix.strides[j];
         }
@@ -574,14 +576,21 @@ __global__ void __launch_bounds__(kProbeThreads, SJ_PROBE_MINB) k_probe_tiled(co
                             unsigned long long b0 = 0;
                             if (lane == 31) b0 = atomicAdd(pa.cursor, (unsigned long long)tot);
                             b0 = __shfl_sync(0xffffffffu, b0, 31);
-                            unsigned long long at = b0 + (inc - cnt);
-                            uint32_t mm = hm;
-                            while (mm) {
-                                const int e = __ffs(mm) - 1;
-                                mm &= mm - 1u;
-                                if (at < pa.cap) pa.out[at] = ((uint64_t)qid << 32) | tid[e];
-                                else atomicOr(pa.overflow, 1u);
-                                ++at;
+                            // the tile's pairs written cooperatively: output slot k (lane k mod 32) is hit
+                            // k - excl(L) of the owner lane L -- consecutive slots, coalesced stores
+                            // (per-lane loops over their own hits stored 32 scattered runs per instruction)
+                            for (uint32_t k0 = 0; k0 < tot; k0 += 32u) {
+                                const uint32_t k = k0 + lane;
+                                const uint32_t own = owner_of(inc, k);
+                                const uint32_t ohm = __shfl_sync(0xffffffffu, hm, own);
+                                const uint32_t oex = __shfl_sync(0xffffffffu, inc - cnt, own);
+                                const uint32_t oqid = __shfl_sync(0xffffffffu, qid, own);
+                                if (k < tot) {
+                                    const uint32_t e = __fns(ohm, 0u, (int)(k - oex) + 1);
+                                    const unsigned long long at = b0 + k;
+                                    if (at < pa.cap) pa.out[at] = ((uint64_t)oqid << 32) | tid[e];
+                                    else atomicOr(pa.overflow, 1u);
+                                }
                             }
                         }
                     }
@@ -755,6 +764,141 @@ void probe_join(const DevIndex &ix, int dev, const ProbeArgs &q, uint64_t nq, co
     res->stats.batches = (uint32_t)res->batches.size();
     res->stats.refine_launches = (uint32_t)res->batches.size() + 1;
 }
+
+// the sampled two-set plan (the paper's estimate-then-batch scheme, PAPER.md:262 / reading R15, for
+// J(Q,P)): runs of 32 consecutive sorted queries every R positions (~1.5 %, >= 4096 queries) are
+// counted; each run stands for its R positions; batches of <= capacity / 1.75 estimated pairs are filled
+// into buffers of 1.75x their estimate, and a batch whose cursor overflowed is counted exactly and
+// filled again.  One pass over the queries instead of the exact plan's count + fill.
+__global__ void k_sample_list(const uint32_t *__restrict__ qlist, uint32_t nq, uint32_t R, uint32_t nruns,
+                              uint32_t *__restrict__ out)
+{
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nruns * 32u; i += gridDim.x * blockDim.x) {
+        const uint64_t pos = (uint64_t)(i >> 5) * R + (i & 31u);
+        out[i] = qlist[pos < nq ? pos : nq - 1];
+    }
+}
+
+void probe_join_sampled(const DevIndex &ix, int dev, const ProbeArgs &q, uint64_t nq, const sj_join_opts &o,
+                        cudaStream_t s, sj_result *res, const uint32_t *d_nonfinite)
+{
+    constexpr double kMargin = 0.75;
+    const uint64_t want = std::max<uint64_t>(4096, nq / 64);
+    const uint64_t runs = (want + 31) / 32;
+    const uint64_t R = std::max<uint64_t>(32, (nq / runs) & ~31ull);
+    const uint64_t nruns = (nq + R - 1) / R;
+    const uint32_t ns = (uint32_t)(nruns * 32);
+    Scratch<uint32_t> slist(ns, s), scnt(ns, s);
+    const uint64_t nbk = (ns + 1023) / 1024;
+    Scratch<unsigned long long> words(8 + nbk, s);
+    SJ_CUDA(cudaMemsetAsync(words.p, 0, sizeof(unsigned long long) * (8 + nbk), s));
+    k_sample_list<<<(unsigned)std::min<uint64_t>((ns + 255) / 256, 1024), 256, 0, s>>>(q.qlist, (uint32_t)nq, (uint32_t)R,
+                                                                                       (uint32_t)nruns, slist.p);
+    SJ_LAUNCHED();
+    ProbeArgs pa = q;
+    pa.qlist = slist.p;
+    pa.q_begin = 0;
+    pa.nq = ns;
+    pa.counts = scnt.p;
+    pa.buckets = words.p + 8;
+    pa.nonfinite = reinterpret_cast<uint32_t *>(words.p + 3);
+    pa.work = words.p;
+    launch_probe(kPCount, ix, pa, dev, s);
+    std::vector<uint32_t> hc(ns);
+    unsigned long long hw[8];
+    uint32_t hbad = 0;
+    SJ_CUDA(cudaMemcpyAsync(hc.data(), scnt.p, sizeof(uint32_t) * ns, cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaMemcpyAsync(hw, words.p, sizeof hw, cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaMemcpyAsync(&hbad, d_nonfinite, sizeof hbad, cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaStreamSynchronize(s));
+    if (hbad) fail(SJ_ERR_NONFINITE, "a query coordinate is NaN or inf");
+    std::vector<double> be(nruns, 0.0);
+    for (uint64_t r = 0; r < nruns; ++r) {
+        double c = 0;
+        uint32_t v = 0;
+        for (uint32_t l = 0; l < 32; ++l)
+            if (r * R + l < nq) { c += hc[r * 32 + l]; ++v; }
+        const uint64_t span = std::min<uint64_t>(R, nq - r * R);
+        be[r] = v ? c * (double)span / (double)v : 0.0;
+    }
+    std::vector<uint64_t> cuts, est;
+    uint64_t est_total = 0;
+    plan_from_buckets(be.data(), nruns, R, 0, nq, o.batch_capacity_pairs, std::max(1, o.min_batches), kMargin, cuts,
+                      est, &est_total);
+    const size_t nb = cuts.size() - 1;
+    // fill every batch (per-batch cursor slots), read the cursors back once, re-fill the overflowed
+    Scratch<unsigned long long> cur(2 * nb + 8, s);
+    SJ_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(unsigned long long) * (2 * nb + 8), s));
+    unsigned long long *work = cur.p + 2 * nb;
+    auto fill = [&](size_t b, uint64_t cap) {
+        sj_batch &bt = res->batches[b];
+        bt.cap = cap;
+        bt.pairs = dalloc<uint64_t>(cap, s);
+        bt.on_device = 1;
+        ProbeArgs pf = q;
+        pf.q_begin = (uint32_t)cuts[b];
+        pf.nq = (uint32_t)(cuts[b + 1] - cuts[b]);
+        pf.out = bt.pairs;
+        pf.cursor = cur.p + 2 * b;
+        pf.cap = cap;
+        pf.overflow = reinterpret_cast<uint32_t *>(cur.p + 2 * b + 1);
+        pf.work = work;
+        launch_probe(kPFill, ix, pf, dev, s);
+    };
+    res->batches.resize(nb);
+    for (size_t b = 0; b < nb; ++b) {
+        const uint64_t cap = std::min<uint64_t>(o.batch_capacity_pairs, (uint64_t)((double)est[b] * (1.0 + kMargin))) + 4096;
+        fill(b, cap);
+    }
+    std::vector<unsigned long long> hcur(2 * nb);
+    SJ_CUDA(cudaMemcpyAsync(hcur.data(), cur.p, sizeof(unsigned long long) * 2 * nb, cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaStreamSynchronize(s));
+    uint32_t retries = 0;
+    for (size_t b = 0; b < nb; ++b) {
+        if (hcur[2 * b] > res->batches[b].cap) {          // overflowed: the cursor kept the exact count
+            const uint64_t exact = hcur[2 * b];
+            dev_free(res->batches[b].pairs, s);
+            res->batches[b].pairs = nullptr;
+            SJ_CUDA(cudaMemsetAsync(cur.p + 2 * b, 0, 16, s));
+            fill(b, exact);
+            ++retries;
+        }
+        res->batches[b].n = hcur[2 * b];
+    }
+    if (retries) {
+        std::vector<unsigned long long> h2(2 * nb);
+        SJ_CUDA(cudaMemcpyAsync(h2.data(), cur.p, sizeof(unsigned long long) * 2 * nb, cudaMemcpyDeviceToHost, s));
+        SJ_CUDA(cudaStreamSynchronize(s));
+        for (size_t b = 0; b < nb; ++b)
+            if (h2[2 * b] > res->batches[b].cap) fail(SJ_ERR_STATE, "two-set join: exact re-fill overflowed (internal error)");
+    }
+    uint64_t total = 0;
+    for (size_t b = 0; b < nb; ++b) {
+        sj_batch &bt = res->batches[b];
+        total += bt.n;
+        if (o.sort_pairs) sort_pairs_device(bt.pairs, bt.n, res->n_points, s);
+        if (o.result_on_host) {
+            uint64_t *h = static_cast<uint64_t *>(host_pinned_alloc(std::max<uint64_t>(bt.n, 1) * 8, nullptr));
+            if (bt.n) SJ_CUDA(cudaMemcpyAsync(h, bt.pairs, bt.n * 8, cudaMemcpyDeviceToHost, s));
+            SJ_CUDA(cudaStreamSynchronize(s));
+            dev_free(bt.pairs, s);
+            bt.pairs = h;
+            bt.on_device = 0;
+            bt.cap = std::max<uint64_t>(bt.n, 1);
+        }
+    }
+    unsigned long long hwk[3];
+    SJ_CUDA(cudaMemcpyAsync(hwk, work, sizeof hwk, cudaMemcpyDeviceToHost, s));
+    SJ_CUDA(cudaStreamSynchronize(s));
+    res->total = total;
+    res->stats.pairs = total;
+    res->stats.estimated_pairs = est_total;
+    res->stats.cells_probed = hw[0] + hwk[0];
+    res->stats.candidates_tested = hw[1] + hwk[1];
+    res->stats.batches = (uint32_t)nb;
+    res->stats.retries = retries;
+    res->stats.refine_launches = (uint32_t)(nb + retries + 1);
+}
 }  // namespace
 
 // ------------------------------------------------------------------ two-set join
@@ -797,18 +941,19 @@ sj_result *join_sets_impl(const sj_index *idx, const double *queries, uint64_t n
         // queries sorted by their cell in P's grid (LSD radix sort of (key, row)): neighbouring queries
         // share neighbour cells (L2 reuse) and a warp of one populous cell shares candidate tiles
         Scratch<uint64_t> qk(nq, s), qk2(nq, s);
-        Scratch<uint32_t> qv(nq, s), qv2(nq, s);
+        Scratch<uint32_t> qv(nq, s), qv2(nq, s), bad(1, s);
+        SJ_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(uint32_t), s));
         if (nq) {
             // keys < prod |g_j| <= 2^key_bits; the sentinel 2^key_bits (all ones at 64 bits) sorts last
             const int kb = std::min(64, idx->view.key_bits + 1);
             const uint64_t sentinel = idx->view.key_bits >= 64 ? ~0ull : (1ull << idx->view.key_bits);
             const unsigned g = (unsigned)std::min<uint64_t>((nq + 255) / 256, (uint64_t)device_sm_count(dev) * 8);
             switch (D) {
-            case 2: k_qkeys<2><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p); break;
-            case 3: k_qkeys<3><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p); break;
-            case 4: k_qkeys<4><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p); break;
-            case 5: k_qkeys<5><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p); break;
-            default: k_qkeys<6><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p); break;
+            case 2: k_qkeys<2><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p, bad.p); break;
+            case 3: k_qkeys<3><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p, bad.p); break;
+            case 4: k_qkeys<4><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p, bad.p); break;
+            case 5: k_qkeys<5><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p, bad.p); break;
+            default: k_qkeys<6><<<g, 256, 0, s>>>(ix, qd, (uint32_t)nq, sentinel, qk.p, qv.p, bad.p); break;
             }
             SJ_LAUNCHED();
             bool in_tmp = false;
@@ -816,7 +961,12 @@ sj_result *join_sets_impl(const sj_index *idx, const double *queries, uint64_t n
             q.qlist = in_tmp ? qv2.p : qv.p;
             q.tiled = 1;
         }
-        probe_join(ix, dev, q, nq, o, s, res);
+        // large query sets: the sampled plan (one pass); small ones: exact counts (cheap, no re-runs)
+#ifndef SJ_SETS_SAMPLE_MIN
+#define SJ_SETS_SAMPLE_MIN 65536
+#endif
+        if (nq >= SJ_SETS_SAMPLE_MIN) probe_join_sampled(ix, dev, q, nq, o, s, res, bad.p);
+        else probe_join(ix, dev, q, nq, o, s, res);
     } catch (...) {
         cudaStreamSynchronize(s);
         free_batches(res);

@@ -296,3 +296,27 @@ def test_join_sets_full_size_fingerprints(sj, cfg, d, eps):
     assert (fa, fb) == (want["fa"], want["fb"])
     assert np.array_equal(cnt.cpu().numpy()[:len(Q)].astype(np.int64), want["counts"])
     res.free()
+
+
+@pytest.mark.parametrize("cap", [None, 20_000, 3_000])
+def test_join_sets_sampled_plan(sj, cap):
+    """>= 65536 queries take the sampled one-pass plan (the estimate-then-batch scheme, reading R15):
+    skewed queries (clusters + background) and small capacities force many batches and overflowed
+    batches re-filled from their exact cursor; the set is unchanged, and a NaN query is still caught."""
+    P = datagen.clustered_small(20_000, 2, seed=21, n_clusters=5, sigma=0.8)
+    rng = np.random.default_rng(3)
+    Q = np.concatenate([datagen.clustered_small(60_000, 2, seed=22, n_clusters=5, sigma=0.8),
+                        rng.uniform(-2, 22, (12_000, 2))])
+    rng.shuffle(Q)
+    eps = 0.15
+    want = oracle.join_sets(Q, P, eps)
+    kw = {} if cap is None else dict(batch_capacity_pairs=cap)
+    got, res = gpu_sets(sj, P, Q, eps, **kw)
+    assert np.array_equal(got, want)
+    assert res.stats["estimated_pairs"] > 0
+    if cap is not None:
+        assert res.n_batches >= len(want) // cap
+    bad = Q.copy()
+    bad[40_000, 1] = np.inf
+    with pytest.raises(sj.SJError):
+        gpu_sets(sj, P, bad, eps, **kw)
