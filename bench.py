@@ -420,7 +420,7 @@ def bench_variants(sj, pts_dev, pts, args, flush, stream, dev):
         eps0 = 1.3 * (vol * math.gamma(1 + args.d / 2) / math.pi ** (args.d / 2)) ** (1.0 / args.d)
         ms, r = timed_call(lambda: sj.knn_self(pts_dev, kk, eps0)[0], k, w)
         out["knn_self_join"] = {"ms": ms, "queries_per_s": args.n / (ms / 1e3),
-                                "config": f"the headline points, k={kk}, eps0={eps0:.4g} (radius doubling)"}
+                                "config": f"the headline points, k={kk}, eps0={eps0:.4g} (growing radius)"}
     except Exception as e:  # noqa: BLE001 -- reported, the headline line stands
         out["error"] = f"{type(e).__name__}: {e}"
     return out
