@@ -280,9 +280,11 @@ sj_status sj_brute_force_join(const double *points, uint64_t n, int d, double ep
  * ordered pair (i,k), i a row of `queries`, k an original id of the index's points P, with
  * s(q_i,p_k) <= fl(eps^2) (the self-join's predicate and eps -- the index's), packed (i << 32) | k.
  * Each query probes the 3^d cells around its own cell in P's grid (R7 against P's geometry; no
- * unicomp, no self rule).  Two passes over the queries: exact per-query counts, then contiguous query
- * ranges of <= batch_capacity_pairs pairs (and >= min_batches batches when there is output) filled
- * with warp-aggregated emission -- exact sizes, no overflow re-runs.
+ * unicomp, no self rule); the queries are processed sorted by that cell (a warp of one populous cell
+ * shares candidate tiles).  Batches are contiguous ranges of the sorted queries (>= min_batches when
+ * there is output): with >= 65536 queries planned from a sampled count (the self-join's estimate-
+ * then-batch scheme; buffers of 1.75x the estimate, an overflowed batch re-filled at its exact size),
+ * else from exact per-query counts (a count pass, then exact sizes).
  *   queries : row-major nq x d float64, device memory on the index's device (queries_on_device = 1;
  *             read after the work queued on the legacy default stream) or host memory (copied).
  *   opts    : NULL = defaults; batch_capacity_pairs, min_batches, result_on_host and sort_pairs are
