@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SJ_ABI_VERSION 5   /* 5: sj_join_sets, sj_knn_self, sj_self_join_f32; 4: drain_csr, CSR batches, sj_dbscan, sj_result_counters */
+#define SJ_ABI_VERSION 5   /* 5: sj_join_sets, sj_knn_self, sj_knn_join, sj_self_join_f32; 4: drain_csr, CSR batches, sj_dbscan, sj_result_counters */
 #define SJ_MAX_DIM 6
 
 typedef enum {
@@ -334,6 +334,16 @@ typedef struct {
  *         SJ_ERR_KEY_OVERFLOW (eps0 too small for the range), SJ_ERR_NOMEM, SJ_ERR_CUDA. */
 sj_status sj_knn_self(const double *points, uint64_t n, int d, uint32_t k, double eps0, const sj_build_opts *bopts,
                       uint32_t *ids, double *dist2, sj_knn_stats *stats);
+
+/* kNN join of query rows against points (the two-set form of sj_knn_self; DESIGN.md
+ * R20): row i of ids[nq*k] / dist2[nq*k] = the k points j of `points` with the smallest
+ * (s(q_i,p_j), j), ascending; nothing is excluded (a query equal to a point gets it at s = 0).  Same
+ * growing-radius grid certificate (R19's cells for queries outside the points' box).
+ *   points (n x d) and queries (nq x d): row-major float64, both host or both device per
+ *   bopts->points_on_device.  k: 1..32, k <= n < 2^32, nq < 2^32.  ids / dist2: DEVICE memory.
+ * Errors: as sj_knn_self, and SJ_ERR_NONFINITE for a NaN / inf query. */
+sj_status sj_knn_join(const double *points, uint64_t n, const double *queries, uint64_t nq, int d, uint32_t k,
+                      double eps0, const sj_build_opts *bopts, uint32_t *ids, double *dist2, sj_knn_stats *stats);
 
 /* Multi-GPU shard plan: cut the A-order queries [0, N) into `world` contiguous
  * ranges cuts[r] .. cuts[r+1] (cuts: world + 1 host uint64) of about equal estimated work, using

@@ -502,6 +502,22 @@ sj_status sj_self_join_f32(const float *points, uint64_t n, int d, float eps, co
     SJ_API_END
 }
 
+sj_status sj_knn_join(const double *points, uint64_t n, const double *queries, uint64_t nq, int d, uint32_t k,
+                      double eps0, const sj_build_opts *bopts, uint32_t *ids, double *dist2, sj_knn_stats *stats)
+{
+    SJ_API_BEGIN
+    if (nq && !queries) sj::fail(SJ_ERR_ARG, "queries is NULL");
+    sj_build_opts bo;
+    if (bopts) bo = *bopts;
+    else sj_build_opts_default(&bo);
+    sj_knn_stats st{};
+    static const double kNoQueries = 0.0;       // nq == 0: a non-NULL marker for the two-set form
+    sj::knn_impl(points, n, nq ? queries : &kNoQueries, nq, d, k, eps0, bo, ids, dist2, &st);
+    if (stats) *stats = st;
+    return SJ_OK;
+    SJ_API_END
+}
+
 sj_status sj_knn_self(const double *points, uint64_t n, int d, uint32_t k, double eps0, const sj_build_opts *bopts,
                       uint32_t *ids, double *dist2, sj_knn_stats *stats)
 {

@@ -359,6 +359,8 @@ sj_result *join_sets_impl(const sj_index *idx, const double *queries, uint64_t n
                           const sj_join_opts &o);
 sj_result *self_join_f32_impl(const float *points, uint64_t n, int d, float eps, const sj_build_opts &bo,
                               const sj_join_opts &o);
+void knn_impl(const double *points, uint64_t n, const double *queries, uint64_t nq, int d, uint32_t k, double eps0,
+              const sj_build_opts &bo, uint32_t *ids, double *dist2, sj_knn_stats *st);
 void knn_self_impl(const double *points, uint64_t n, int d, uint32_t k, double eps0, const sj_build_opts &bo,
                    uint32_t *ids, double *dist2, sj_knn_stats *st);
 

@@ -1039,13 +1039,27 @@ sj_result *self_join_f32_impl(const float *points, uint64_t n, int d, float eps,
 }
 
 // ------------------------------------------------------------------ kNN self-join
-void knn_self_impl(const double *points, uint64_t n, int d, uint32_t k, double eps0, const sj_build_opts &bo,
-                   uint32_t *ids, double *dist2, sj_knn_stats *st)
+namespace {
+__global__ void k_nonfinite(const double *__restrict__ a, uint64_t m, uint32_t *__restrict__ flag)
 {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+        if (!isfinite(a[i])) atomicOr(flag, 1u);
+}
+}  // namespace
+
+// kNN over the growing-radius grid (R20): queries == nullptr is the self join (queries = the points,
+// each excluding itself); otherwise nq query rows against the n points, nothing excluded.
+void knn_impl(const double *points, uint64_t n, const double *queries, uint64_t nq, int d, uint32_t k, double eps0,
+              const sj_build_opts &bo, uint32_t *ids, double *dist2, sj_knn_stats *st)
+{
+    const bool self = queries == nullptr;
+    if (self) nq = n;
     if (d < 2 || d > SJ_MAX_DIM) fail(SJ_ERR_DIM, "d must be in [2,6]");
-    if (!points || !ids || !dist2) fail(SJ_ERR_ARG, "points / ids / dist2 is NULL");
+    if (!points || (nq && (!ids || !dist2))) fail(SJ_ERR_ARG, "points / ids / dist2 is NULL");
     if (k < 1 || k > (uint32_t)kMaxK) fail(SJ_ERR_ARG, "k must be in [1, 32]");
-    if (n < (uint64_t)k + 1 || n >= (1ull << 32)) fail(SJ_ERR_ARG, "N must satisfy k + 1 <= N < 2^32");
+    if (n < (uint64_t)k + (self ? 1 : 0) || n >= (1ull << 32))
+        fail(SJ_ERR_ARG, self ? "N must satisfy k + 1 <= N < 2^32" : "N must satisfy k <= N < 2^32");
+    if (nq >= (1ull << 32)) fail(SJ_ERR_ARG, "the number of queries must be < 2^32");
     if (!std::isfinite(eps0) || !(eps0 > 0.0)) fail(SJ_ERR_ARG, "eps0 must be finite and > 0");
     if (bo.device < 0 || bo.device >= device_count()) fail(SJ_ERR_ARG, "bad device ordinal");
     SJ_CUDA(cudaSetDevice(bo.device));
@@ -1061,8 +1075,30 @@ void knn_self_impl(const double *points, uint64_t n, int d, uint32_t k, double e
         SJ_CUDA(cudaMemcpyAsync(pcopy.p, points, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
         pd = pcopy.p;
     }
-    Scratch<uint32_t> unres[2] = {Scratch<uint32_t>(n, s), Scratch<uint32_t>(n, s)};
+    const double *qd = pd;
+    Scratch<double> qcopy;
     Scratch<unsigned long long> words(8, s);
+    if (!self) {
+        qd = queries;
+        if (nq && !bo.points_on_device) {
+            qcopy.p = dalloc<double>(nq * d, s);
+            qcopy.s = s;
+            SJ_CUDA(cudaMemcpyAsync(qcopy.p, queries, sizeof(double) * nq * d, cudaMemcpyHostToDevice, s));
+            qd = qcopy.p;
+        }
+        // a non-finite query would never be certified: rejected up front
+        SJ_CUDA(cudaMemsetAsync(words.p, 0, 8, s));
+        if (nq) {
+            k_nonfinite<<<(unsigned)std::min<uint64_t>((nq * d + 255) / 256, 4096), 256, 0, s>>>(
+                qd, nq * d, reinterpret_cast<uint32_t *>(words.p));
+            SJ_LAUNCHED();
+        }
+        uint32_t bad = 0;
+        SJ_CUDA(cudaMemcpyAsync(&bad, words.p, sizeof bad, cudaMemcpyDeviceToHost, s));
+        SJ_CUDA(cudaStreamSynchronize(s));
+        if (bad) fail(SJ_ERR_NONFINITE, "a query coordinate is NaN or inf");
+    }
+    Scratch<uint32_t> unres[2] = {Scratch<uint32_t>(nq, s), Scratch<uint32_t>(nq, s)};
     sj_build_opts b2 = bo;
     b2.points_on_device = 1;
     b2.stream = s;
@@ -1075,7 +1111,7 @@ void knn_self_impl(const double *points, uint64_t n, int d, uint32_t k, double e
 #define SJ_KNN_GROW_VOL 4.0
 #endif
     const double grow = std::max(1.1, std::pow(SJ_KNN_GROW_VOL, 1.0 / d));
-    uint64_t pending = n, probes = 0, tests = 0;
+    uint64_t pending = nq, probes = 0, tests = 0;
     uint32_t rounds = 0;
     int cur = 0;
     while (pending) {
@@ -1084,12 +1120,13 @@ void knn_self_impl(const double *points, uint64_t n, int d, uint32_t k, double e
         try {
             SJ_CUDA(cudaMemsetAsync(words.p, 0, sizeof(unsigned long long) * 8, s));
             ProbeArgs pa{};
-            pa.q = pd;
-            pa.q_index = rounds == 1;                 // first round: every point, in the index's A-order
+            pa.q = qd;
+            // first self round: every point, in the index's A-order (coalesced, cell-sorted)
+            pa.q_index = self && rounds == 1;
             pa.qlist = rounds == 1 ? nullptr : unres[cur].p;
             pa.q_begin = 0;
             pa.nq = (uint32_t)pending;
-            pa.self = 1;
+            pa.self = self ? 1 : 0;
             pa.k = k;
             pa.ids = ids;
             pa.dist2 = dist2;
@@ -1117,6 +1154,12 @@ void knn_self_impl(const double *points, uint64_t n, int d, uint32_t k, double e
         st->cells_probed = probes;
         st->candidates_tested = tests;
     }
+}
+
+void knn_self_impl(const double *points, uint64_t n, int d, uint32_t k, double eps0, const sj_build_opts &bo,
+                   uint32_t *ids, double *dist2, sj_knn_stats *st)
+{
+    knn_impl(points, n, nullptr, 0, d, k, eps0, bo, ids, dist2, st);
 }
 
 }  // namespace sj

@@ -138,6 +138,8 @@ def load_library(path: str = LIB_PATH):
     L.sj_join_sets.restype = i32
     L.sj_self_join_f32.argtypes = [vp, u64, i32, ctypes.c_float, P(BuildOpts), P(JoinOpts), P(vp)]
     L.sj_self_join_f32.restype = i32
+    L.sj_knn_join.argtypes = [vp, u64, vp, u64, i32, u32, dbl, P(BuildOpts), vp, vp, P(KnnStats)]
+    L.sj_knn_join.restype = i32
     L.sj_knn_self.argtypes = [vp, u64, i32, u32, dbl, P(BuildOpts), vp, vp, P(KnnStats)]
     L.sj_knn_self.restype = i32
     L.sj_index_export.argtypes = [vp, P(IndexView)]
@@ -714,6 +716,45 @@ def knn_self(points, k: int, eps0: float, device: Optional[int] = None, with_sta
     _check(L.sj_knn_self(ctypes.c_void_p(ptr), n, d, int(k), float(eps0), ctypes.byref(bo),
                          ctypes.c_void_p(ids.data_ptr()), ctypes.c_void_p(dist2.data_ptr()), ctypes.byref(st)))
     del keep
+    if with_stats:
+        return ids, dist2, dict(rounds=st.rounds, eps_final=st.eps_final, cells_probed=st.cells_probed,
+                                candidates_tested=st.candidates_tested)
+    return ids, dist2
+
+
+def knn_join(points, queries, k: int, eps0: float, device: Optional[int] = None, with_stats: bool = False):
+    """sj_knn_join: for every query row its k nearest points (ascending (s, id)), nothing excluded ->
+    (ids int32 [nq, k], dist2 float64 [nq, k]) cuda tensors (+ stats).  points / queries: both torch cuda
+    tensors on one device, or both host (numpy / cpu tensors)."""
+    import torch
+    L = load_library()
+    bo, ptr, n, d, keep = _points_arg(points, device, None)
+    bo.stream = None
+    bo.speculative_estimate = 0
+    if isinstance(queries, torch.Tensor):
+        qt = queries.contiguous()
+        if qt.dtype != torch.float64 or qt.dim() != 2:
+            raise TypeError("queries must be a 2-D float64 tensor")
+        if bool(qt.is_cuda) != bool(bo.points_on_device):
+            raise ValueError("points and queries must both be on the device or both on the host")
+        qkeep, qptr = qt, qt.data_ptr()
+        nq, dq = qt.shape
+    else:
+        if bo.points_on_device:
+            raise ValueError("points and queries must both be on the device or both on the host")
+        qa = np.ascontiguousarray(queries, dtype=np.float64)
+        qkeep, qptr = qa, qa.ctypes.data
+        nq, dq = qa.shape
+    if dq != d:
+        raise ValueError("dimension mismatch")
+    dev = bo.device
+    ids = torch.empty((nq, k), dtype=torch.int32, device=f"cuda:{dev}")
+    dist2 = torch.empty((nq, k), dtype=torch.float64, device=f"cuda:{dev}")
+    st = KnnStats()
+    _check(L.sj_knn_join(ctypes.c_void_p(ptr), n, ctypes.c_void_p(qptr if nq else None), nq, d, int(k), float(eps0),
+                         ctypes.byref(bo), ctypes.c_void_p(ids.data_ptr()), ctypes.c_void_p(dist2.data_ptr()),
+                         ctypes.byref(st)))
+    del keep, qkeep
     if with_stats:
         return ids, dist2, dict(rounds=st.rounds, eps_final=st.eps_final, cells_probed=st.cells_probed,
                                 candidates_tested=st.candidates_tested)

@@ -320,3 +320,39 @@ def test_join_sets_sampled_plan(sj, cap):
     bad[40_000, 1] = np.inf
     with pytest.raises(sj.SJError):
         gpu_sets(sj, P, bad, eps, **kw)
+
+
+@pytest.mark.parametrize("d,k", [(2, 1), (2, 16), (3, 8), (4, 32), (6, 8)])
+def test_knn_join_exact(sj, d, k):
+    """kNN join of query rows against points (sj_knn_join): ids and the bits of s equal the oracle's
+    brute force (queries form: nothing excluded); queries include copies of points (s = 0, tie by id
+    with duplicates) and points far outside the points' box (many radius steps)."""
+    P = datagen.uniform(4000, d, seed=600 + d)
+    rng = np.random.default_rng(d)
+    Q = np.concatenate([datagen.uniform(1500, d, seed=700 + d), P[:50], rng.uniform(-80, 180, (30, d))])
+    eps0 = 0.8 * _eps_for(4000, d, k)
+    ids, s, st = sj.knn_join(torch.from_numpy(P).cuda(), torch.from_numpy(Q).cuda(), k, eps0, with_stats=True)
+    wi, ws = oracle.knn(P, k, queries=Q)
+    assert np.array_equal(ids.cpu().numpy().astype(np.int64), wi)
+    assert np.array_equal(s.cpu().numpy().view(np.uint64), ws.view(np.uint64))
+    assert st["rounds"] >= 2
+
+
+def test_knn_join_edges(sj):
+    """Host inputs; k = n (every point); no queries; a NaN query is rejected; mixed residency rejected."""
+    P = datagen.uniform(20, 3, seed=1)
+    Q = datagen.uniform(7, 3, seed=2)
+    ids, s = sj.knn_join(P, Q, 20, 5.0)
+    wi, ws = oracle.knn(P, 20, queries=Q)
+    assert np.array_equal(ids.cpu().numpy(), wi) and np.array_equal(s.cpu().numpy(), ws)
+    ids0, _ = sj.knn_join(P, np.empty((0, 3)), 4, 5.0)
+    assert ids0.shape == (0, 4)
+    bad = Q.copy()
+    bad[3, 0] = np.nan
+    with pytest.raises(sj.SJError) as e:
+        sj.knn_join(P, bad, 4, 5.0)
+    assert e.value.status == 2
+    with pytest.raises(sj.SJError):
+        sj.knn_join(P, Q, 21, 5.0)
+    with pytest.raises(ValueError):
+        sj.knn_join(torch.from_numpy(P).cuda(), Q, 4, 5.0)
