@@ -1,6 +1,6 @@
 """Device timing of the SURVEY §8(f) rank-4 variants (variants.cu) on the BASELINE configs' point sets.
 
-    python tools/variants_bench.py [--steps K] [--warmup W] [--only sets,knn,f32] [--json]
+    python tools/variants_bench.py [--steps K] [--warmup W] [--only sets,knn,knnjoin,f32] [--json]
 
 Each case: W untimed calls, then K calls timed with CUDA events on torch's stream around the whole
 library call (it blocks until its result is complete), the L2 flushed (512 MB write) before each.  Work
@@ -93,7 +93,7 @@ def main():
                              candidates_tested=st["candidates_tested"],
                              fp64_frac=3 * d * st["candidates_tested"] / (med / 1e3) / fp64,
                              pair_write_hbm_frac=8 * pairs / (med / 1e3) / 1e9 / hbm,
-                             note="count pass + fill pass (work counters cover both)"))
+                             note="queries sorted by cell; >= 65536 queries: sampled plan, one fill pass (counters: sample + fill)"))
             res.free()
             del idx, P, Q
             torch.cuda.empty_cache()
@@ -118,6 +118,25 @@ def main():
             del P
             torch.cuda.empty_cache()
 
+    if "knnjoin" in only or "knn" in only:
+        for cfg, d, k in (("C2", 6, 8), ("C2", 2, 16)):
+            P = torch.from_numpy(datagen.uniform_config(cfg, d)).cuda()
+            Q = torch.from_numpy(datagen.uniform(P.shape[0], d, seed=777 + d)).cuda()
+            eps0 = 1.3 * knn_radius(P.shape[0], d, k)
+            info = {}
+
+            def runj():
+                ids, s2, st = sj.knn_join(P, Q, k, eps0, with_stats=True)
+                info.update(st)
+                return ids
+            med, mn, _ = timeit(runj, a.steps, a.warmup, flush)
+            rows.append(dict(variant="kNN join", config=f"{cfg} {d}-D P 2M x Q 2M uniform, k={k}, eps0={eps0:.4g}",
+                             ms=med, ms_min=mn, queries_per_s=Q.shape[0] / (med / 1e3), rounds=info["rounds"],
+                             cells_probed=info["cells_probed"], candidates_tested=info["candidates_tested"],
+                             fp64_frac=3 * d * info["candidates_tested"] / (med / 1e3) / fp64))
+            del P, Q
+            torch.cuda.empty_cache()
+
     if "f32" in only:
         for cfg, d, eps in (("C2", 6, 8.0), ("C2", 3, 1.0), ("C2", 2, 1.0)):
             P = torch.from_numpy(datagen.uniform_config(cfg, d).astype(np.float32)).cuda()
@@ -128,7 +147,7 @@ def main():
                              ms=med, ms_min=mn, pairs=pairs, pairs_per_s=pairs / (med / 1e3),
                              cells_probed=st["cells_probed"], candidates_tested=st["candidates_tested"],
                              pair_write_hbm_frac=8 * pairs / (med / 1e3) / 1e9 / hbm,
-                             note="index build + count pass + fill pass, full 3^d search"))
+                             note="the self-join path (build, estimate, unicomp batches) with the binary32 predicate"))
             res.free()
             del P
             torch.cuda.empty_cache()
