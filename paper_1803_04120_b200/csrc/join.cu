@@ -354,7 +354,9 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
     // stream waits for another (no event hops on the GPU between the batches and the read-back)
     const size_t kBlock = kWorkBytes + kSlotsBytes;
     const size_t slot_need = 8 * (size_t)(nbk + 1);
-    CtxGuard cg{acquire_ctx(idx->device, S, S + 2, slot_need)};
+    // host drain: S more streams, one copy stream per compute stream (the drain of a batch overlaps the
+    // next batch's refine on the same compute stream: double-buffered staging)
+    CtxGuard cg{acquire_ctx(idx->device, o.result_on_host ? 2 * S : S, S + 2, slot_need)};
     DevCtx &cx = *cg.c;
     cudaStream_t s0 = cx.streams[0];
     ensure_join_blocks(&cx, kBlock * (size_t)S + 64 * (size_t)S);   // + per stream a CTA counter / doorbell
@@ -606,31 +608,38 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(o.batch_capacity_pairs,
                                                                     maxest + maxest / 4 + 65536));
             if (o.drain_csr) cap = std::min<uint64_t>(cap, 0xffffffffull);   // uint32 row offsets
-            std::vector<uint64_t *> staging(S, nullptr);
-            std::vector<uint64_t> scap(S, cap);           // per-stream staging capacity
+            // two staging buffers per compute stream i (parity p): batch k+1 on stream i refines into
+            // buffer p^1 while the copy stream S+i converts / drains buffer p; stream i waits for the
+            // copy stream's event on a buffer before it overwrites it
+            const int S2 = 2 * S;
+            std::vector<uint64_t *> staging(S2, nullptr);
+            std::vector<uint64_t> scap(S2, cap);          // per-buffer staging capacity
+            std::vector<int> parity(S, 0);
+            std::vector<cudaEvent_t> copied(S2, nullptr), computed(S, nullptr);
             struct StagingGuard {
-                std::vector<uint64_t *> &v; DevCtx &cx;
-                ~StagingGuard() { for (size_t i = 0; i < v.size(); ++i) if (v[i]) dev_free(v[i], cx.streams[i]); }
-            } sg{staging, cx};
-            for (int i = 0; i < S; ++i) staging[i] = dalloc<uint64_t>(cap, cx.streams[i]);
-            // drain_csr: per stream the CSR of the finished batch is built in device memory
-            // ([offsets | neighbours] contiguous, one D2H copy) with two N+1 scratch arrays
+                std::vector<uint64_t *> &v; std::vector<cudaEvent_t> &e1, &e2; DevCtx &cx; int dev;
+                ~StagingGuard() {
+                    for (size_t i = 0; i < v.size(); ++i) if (v[i]) dev_free(v[i], cx.streams[i / 2]);   // buffer 2s+p: stream s
+                    for (auto e : e1) event_put(dev, e);
+                    for (auto e : e2) event_put(dev, e);
+                }
+            } sg{staging, copied, computed, cx, idx->device};
+            for (int i = 0; i < S2; ++i) staging[i] = dalloc<uint64_t>(cap, cx.streams[i / 2]);
+            for (int i = 0; i < S; ++i) computed[i] = event_get(idx->device);
+            // drain_csr: per buffer the CSR of the finished batch is built in device memory
+            // ([offsets | neighbours] contiguous, one D2H copy) with two N+1 scratch arrays per copy stream
             const uint64_t rows = ix.n;
-            std::vector<uint32_t *> csr_blk(S, nullptr), csr_tmp(S, nullptr);
+            std::vector<uint32_t *> csr_blk(S2, nullptr), csr_tmp(S, nullptr);
             struct CsrGuard {
                 std::vector<uint32_t *> &a, &b; DevCtx &cx;
                 ~CsrGuard() {
-                    for (size_t i = 0; i < a.size(); ++i) {
-                        if (a[i]) dev_free(a[i], cx.streams[i]);
-                        if (b[i]) dev_free(b[i], cx.streams[i]);
-                    }
+                    for (size_t i = 0; i < a.size(); ++i) if (a[i]) dev_free(a[i], cx.streams[i / 2]);
+                    for (size_t i = 0; i < b.size(); ++i) if (b[i]) dev_free(b[i], cx.streams[i]);
                 }
             } cgd{csr_blk, csr_tmp, cx};
             if (o.drain_csr) {
-                for (int i = 0; i < S; ++i) {
-                    csr_blk[i] = dalloc<uint32_t>(rows + 1 + cap, cx.streams[i]);
-                    csr_tmp[i] = dalloc<uint32_t>(2 * (rows + 1), cx.streams[i]);
-                }
+                for (int i = 0; i < S2; ++i) csr_blk[i] = dalloc<uint32_t>(rows + 1 + cap, cx.streams[i / 2]);
+                for (int i = 0; i < S; ++i) csr_tmp[i] = dalloc<uint32_t>(2 * (rows + 1), cx.streams[i]);
             }
             const int nsm = device_sm_count(idx->device);
             std::deque<std::pair<uint64_t, uint64_t>> pending;
@@ -641,7 +650,9 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                 auto r = pending.front();
                 pending.pop_front();
                 inflight[i] = r;
-                run_batch(r.first, r.second, staging[i], scap[i], dslot(i, 0), i, true);
+                const int bi = 2 * i + parity[i];
+                if (copied[bi]) SJ_CUDA(cudaStreamWaitEvent(cx.streams[i], copied[bi], 0));   // its last drain
+                run_batch(r.first, r.second, staging[bi], scap[bi], dslot(i, 0), i, true);
                 SJ_CUDA(cudaMemcpyAsync(hslot(i, 0), dslot(i, 0), sizeof(Slot), cudaMemcpyDeviceToHost,
                                         cx.streams[i]));
                 order.push_back(i);
@@ -650,23 +661,26 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
             while (!order.empty()) {
                 const int i = order.front();
                 order.pop_front();
-                // the cursor copy follows the kernel on stream i; the previous D2H on this stream
-                // precedes the kernel, so a stream sync here waits for exactly that batch.
+                // the cursor copy follows the kernel on stream i: a stream sync waits for exactly that
+                // batch (its drain, on the copy stream, is not on stream i)
                 SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
                 const auto r = inflight[i];
+                const int bi = 2 * i + parity[i];
+                cudaStream_t cs = cx.streams[S + i];
                 const uint64_t n = hslot(i, 0)->cursor + nself_of(r.first, r.second);
-                if (n > scap[i]) {
+                if (n > scap[bi]) {
                     ++stats.retries;
                     if (r.second - r.first < 2) {
                         // one query emits more than the staging buffer holds: grow it to fit
                         if (o.drain_csr && n > 0xffffffffull)
                             fail(SJ_ERR_ARG, "drain_csr: one query emits >= 2^32 pairs");
-                        dev_free(staging[i], cx.streams[i]);
-                        staging[i] = dalloc<uint64_t>(n, cx.streams[i]);
-                        scap[i] = n;
+                        if (copied[bi]) SJ_CUDA(cudaStreamWaitEvent(cx.streams[i], copied[bi], 0));
+                        dev_free(staging[bi], cx.streams[i]);
+                        staging[bi] = dalloc<uint64_t>(n, cx.streams[i]);
+                        scap[bi] = n;
                         if (o.drain_csr) {
-                            dev_free(csr_blk[i], cx.streams[i]);
-                            csr_blk[i] = dalloc<uint32_t>(rows + 1 + n, cx.streams[i]);
+                            dev_free(csr_blk[bi], cx.streams[i]);
+                            csr_blk[bi] = dalloc<uint32_t>(rows + 1 + n, cx.streams[i]);
                         }
                         pending.emplace_front(r);
                     } else {
@@ -680,28 +694,33 @@ sj_result *self_join_impl(const sj_index *idx, const sj_join_opts &o)
                     bt.on_device = 0;
                     bt.n = n;
                     bt.cap = n;
+                    // the drain on the copy stream, behind the batch's kernels
+                    SJ_CUDA(cudaEventRecord(computed[i], cx.streams[i]));
+                    SJ_CUDA(cudaStreamWaitEvent(cs, computed[i], 0));
                     if (o.drain_csr) {
                         // 4 B per pair + 4 B per row cross PCIe instead of 8 B per pair
-                        if (n && o.sort_pairs) sort_pairs_device(staging[i], n, ix.n, cx.streams[i]);
-                        batch_to_csr_device(staging[i], n, rows, o.sort_pairs != 0, csr_tmp[i], csr_tmp[i] + rows + 1,
-                                            csr_blk[i], csr_blk[i] + rows + 1, cx.streams[i], nsm);
+                        if (n && o.sort_pairs) sort_pairs_device(staging[bi], n, ix.n, cs);
+                        batch_to_csr_device(staging[bi], n, rows, o.sort_pairs != 0, csr_tmp[i], csr_tmp[i] + rows + 1,
+                                            csr_blk[bi], csr_blk[bi] + rows + 1, cs, nsm);
                         const size_t bytes = sizeof(uint32_t) * (rows + 1 + n);
                         bt.pairs = static_cast<uint64_t *>(host_pinned_alloc(bytes, nullptr));
                         bt.csr = 1;
                         bt.rows = rows;
-                        SJ_CUDA(cudaMemcpyAsync(bt.pairs, csr_blk[i], bytes, cudaMemcpyDeviceToHost, cx.streams[i]));
+                        SJ_CUDA(cudaMemcpyAsync(bt.pairs, csr_blk[bi], bytes, cudaMemcpyDeviceToHost, cs));
                     } else if (n) {
-                        if (o.sort_pairs) sort_pairs_device(staging[i], n, ix.n, cx.streams[i]);
+                        if (o.sort_pairs) sort_pairs_device(staging[bi], n, ix.n, cs);
                         bt.pairs = static_cast<uint64_t *>(host_pinned_alloc(n * sizeof(uint64_t), nullptr));
-                        SJ_CUDA(cudaMemcpyAsync(bt.pairs, staging[i], n * sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                                                cx.streams[i]));
+                        SJ_CUDA(cudaMemcpyAsync(bt.pairs, staging[bi], n * sizeof(uint64_t), cudaMemcpyDeviceToHost, cs));
                     }
+                    if (!copied[bi]) copied[bi] = event_get(idx->device);
+                    SJ_CUDA(cudaEventRecord(copied[bi], cs));
+                    parity[i] ^= 1;
                     res->batches.push_back(bt);
                     res->total += n;
                 }
                 if (!pending.empty()) launch_on(i);
             }
-            for (int i = 0; i < S; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
+            for (int i = 0; i < S2; ++i) SJ_CUDA(cudaStreamSynchronize(cx.streams[i]));
         }
 
         // ---- work counters: the device path read them with its first round; re-runs (which counted
