@@ -200,3 +200,16 @@ def test_join_sets_digest_matches_explicit_pairs():
     assert dg["pairs"] == len(want) > 1000
     assert (dg["fa"], dg["fb"]) == oracle.fingerprint_pairs(want)
     assert np.array_equal(dg["counts"], np.bincount((want >> np.uint64(32)).astype(np.int64), minlength=len(Q)))
+
+
+@pytest.mark.parametrize("d", [2, 4, 6])
+def test_knn_join_form_equals_kdtree(d):
+    """kNN join (queries form, nothing excluded) on continuous random data == scipy cKDTree.query(k) of
+    the queries against the points: ids exactly, distances to the library's rounding."""
+    rng = np.random.default_rng(400 + d)
+    P = rng.uniform(0.0, 10.0, (800, d))
+    Q = rng.uniform(-3.0, 13.0, (300, d))
+    ids, s = oracle.knn(P, 9, queries=Q)
+    dist, nbr = scipy_spatial.cKDTree(P).query(Q, 9)
+    assert np.array_equal(ids, nbr)
+    np.testing.assert_allclose(np.sqrt(s), dist, rtol=1e-12)
